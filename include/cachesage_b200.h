@@ -1,0 +1,198 @@
+/* cachesage_b200 — C ABI of the B200-native CacheSage per-step cache-policy hot path.
+ *
+ * The reference (/root/reference/proj, single-threaded C++20) runs the per-step loop
+ *   observe -> score -> select -> act
+ * inside EngineSim + CacheSagePolicy. This library keeps that behaviour bit-exact while the
+ * block pool, the block table, the transition learner, the reachability classes, the scoring
+ * scan and the k-victim select all live in HBM and run as sm_100a kernels. Plain pointers and
+ * sizes only; no torch types. Every call returns 0 on success or a negative cs_status; the
+ * message is in cs_last_error(). Handles are single-writer (SURVEY.md §8b "Threading").
+ *
+ * Each entry point names the reference interface it replaces (paths relative to
+ * /root/reference/proj). INTEGRATION.md shows the binding a reference maintainer would add.
+ */
+#ifndef CACHESAGE_B200_H
+#define CACHESAGE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum cs_status {
+    CS_OK = 0,
+    CS_ERR_INVALID_ARGUMENT = -1, /* reference: std::invalid_argument */
+    CS_ERR_RUNTIME = -2,          /* reference: std::runtime_error (all pinned, stall, tick regression) */
+    CS_ERR_LOGIC = -3,            /* reference: std::logic_error (budget / vanished block) */
+    CS_ERR_CUDA = -4,             /* CUDA failure or no device: there is NO CPU fallback */
+    CS_ERR_CAPACITY = -5          /* a fixed device capacity (agents, prompt length) exceeded */
+} cs_status;
+
+typedef struct cs_pool* cs_pool_t;
+typedef struct cs_engine* cs_engine_t;
+
+#define CS_NO_AGENT 0xFFFFFFFFu
+
+/* Policy and pool configuration: EngineConfig (engine.hpp:29-36) + CacheSageConfig
+ * (cachesage_policy.hpp:36-43). policy: 0 = lru (baselines.cpp:12-14), 1 = cachesage. */
+typedef struct cs_pool_cfg {
+    int64_t budget_blocks; /* pool slots N (EngineConfig::budget_blocks) */
+    int policy;
+    int e_max;         /* ReachabilityState::e_max, <= 22 */
+    double tau;        /* edge threshold */
+    double w_pred;     /* score = w_pred * survival + recency */
+    int64_t window;    /* TransitionLearner window W */
+    double min_confidence;
+    uint64_t min_row_count;
+    int budget_per_step;
+    int agent_capacity; /* max distinct agents (dense A x A counts), <= 4096 */
+    int device;         /* CUDA device ordinal */
+    int grid_ctas;      /* 0 = one CTA per SM (cooperative scan grid) */
+} cs_pool_cfg;
+
+void cs_pool_cfg_default(cs_pool_cfg* cfg);
+
+/* Creates the device pool: SoA slots (last_touch u64, agent u32, refs u32, key u64), the
+ * open-addressing block table, the learner and the scan scratch.
+ * Replaces: EngineSim::cache_ / pinned_count_ (engine.hpp:176-177), the CacheSagePolicy
+ * constructor (cachesage_policy.cpp:33-48) and TransitionLearner (transition_learner.hpp:19). */
+int cs_pool_create(const cs_pool_cfg* cfg, cs_pool_t* out);
+int cs_pool_destroy(cs_pool_t pool);
+
+/* Declares agent identities in dense-index order (index = position). The learner's alphabet
+ * (TransitionLearner::note_agent, transition_learner.cpp:16-20); argmax ties break on these
+ * 64-bit ids (transition_learner.cpp:89). Appends; returns the first new index in *first. */
+int cs_register_agents(cs_pool_t pool, const uint64_t* agent_ids, int n, int* first);
+
+/* K1: chained block hashing + agent identity for n prompts (host buffers in and out).
+ * tokens: all prompts concatenated; tok_off[n+1] prefix offsets; blk_off[n+1] must equal the
+ * prefix sums of ceil(len/block_size) (cs_blocks_for computes it). Replaces block_keys_for
+ * (hashing.cpp:37-51), chain_hash (hashing.cpp:26-35), derive_agent_identity
+ * (cachesage_policy.cpp:9-31). Empty prompts are invalid_argument (chain_hash :27-29). */
+int cs_hash_prompts(cs_pool_t pool, const uint32_t* tokens, const int64_t* tok_off, int n_prompts,
+                    int block_size, int skip, int take, const int64_t* blk_off, uint64_t* keys_out,
+                    int32_t* counts_out, uint64_t* agent_ids_out);
+int64_t cs_blocks_for(const int64_t* tok_off, int n_prompts, int block_size, int64_t* blk_off);
+
+/* K2: EngineSim::lookup (engine.cpp:127-139): longest resident prefix; each hit is touched
+ * with ticks tick_base+1, tick_base+2, ... The caller's clock advances by *first_miss. */
+int cs_lookup(cs_pool_t pool, const uint64_t* keys, const int32_t* counts, int n, uint64_t tick_base,
+              int64_t* cached_tokens, int* first_miss);
+
+/* K2: the try_start_head feasibility probe (engine.cpp:337-346): number of prompt blocks that
+ * are not resident or not pinned. */
+int cs_probe_needed(cs_pool_t pool, const uint64_t* keys, int n, int* needed);
+
+/* K3+K3b+K6: CacheSagePolicy::observe(AgentDispatch) (cachesage_policy.cpp:57-72): learner
+ * record (transition_learner.cpp:22-51), reachability rebuild on agent change
+ * (reachability.cpp:39-81), prefetch gate (cachesage_policy.cpp:109-123). prev < 0 = none.
+ * *warmup_target = agent index of an issued warmup or -1. */
+int cs_observe_dispatch(cs_pool_t pool, int prev, int next, uint64_t tick, int* warmup_target);
+
+/* K4+K5: EngineSim::admit_pinned (engine.cpp:141-168) with the full eviction semantics of
+ * evict_one (engine.cpp:102-125) + CacheSagePolicy::score (cachesage_policy.cpp:79-85):
+ * makes all n blocks resident and pinned, touching block i at tick_base+1+i; new blocks carry
+ * agent `agent` iff i < anchor_blocks. Victim keys in eviction order -> evicted (cap entries),
+ * count -> *n_evicted; pinned slot per block -> pins (may be NULL).
+ * CS_ERR_RUNTIME = "evict_one: all resident blocks are pinned". */
+int cs_admit_pinned(cs_pool_t pool, const uint64_t* keys, const int32_t* counts, int n, uint32_t agent,
+                    int anchor_blocks, uint64_t tick_base, uint64_t* evicted, int64_t cap,
+                    int64_t* n_evicted, uint32_t* pins);
+
+/* EngineSim::unpin (engine.cpp:170-180) by pinned slot (as returned by cs_admit_pinned). */
+int cs_unpin_slots(cs_pool_t pool, const uint32_t* slots, int n);
+
+/* Pool snapshot restore (stress inputs): resident blocks with explicit
+ * last_touch / agent index (CS_NO_AGENT = none) / refs. Keys must be new and distinct. */
+int cs_restore(cs_pool_t pool, const uint64_t* keys, const uint64_t* last_touch, const uint32_t* agents,
+               const uint32_t* refs, int64_t n);
+
+/* CacheSagePolicy::score (cachesage_policy.cpp:79-85) of every resident block at context
+ * (now_tick, oldest_live_touch over the pool): rows (key, score), *n = resident count. */
+int cs_score_snapshot(cs_pool_t pool, uint64_t now_tick, uint64_t* keys, double* scores, int64_t cap,
+                      int64_t* n);
+
+/* ReachabilityState::hop per agent index (-1 before the first rebuild). */
+int cs_hops(cs_pool_t pool, int* hops, int n);
+
+/* CacheSagePolicy::poll_actions (cachesage_policy.cpp:125-130): drains queued warmups
+ * (agent indices, issue ticks) and resets the per-step budget. */
+int cs_poll_actions(cs_pool_t pool, int* targets, uint64_t* ticks, int cap, int* n);
+
+typedef struct cs_pool_stats {
+    int64_t resident, pinned, evictions, tombstones, scans, scanned_slots;
+    uint64_t rebuilds;
+    int n_agents;
+} cs_pool_stats;
+int cs_pool_get_stats(cs_pool_t pool, cs_pool_stats* out);
+
+/* ------------------------------------------------------------------ engine (EngineSim) */
+
+/* WorkloadSpec (workload.hpp:21-42); anchor_stride / hist_pos_bits widen the token scheme
+ * (0 = the reference's 0x10000 / 20). */
+typedef struct cs_workload_spec {
+    int n_agents;
+    const int* anchor_tokens;
+    const double* transition;
+    int supervisor;
+    int turns_min, turns_max, sessions, task_tokens, history_growth, decode_tokens;
+    int template_tokens, concurrency, budget_blocks;
+    uint64_t seed;
+    uint32_t anchor_stride;
+    int hist_pos_bits;
+} cs_workload_spec;
+
+/* Generates the trace (generate_trace, workload.cpp:156-182) on the host: turns7 rows
+ * (session, turn_index, agent, anchor_tokens, history_tokens, prompt_tokens, decode_tokens).
+ * Returns the turn count (pass cap 0 to size). */
+int64_t cs_generate_trace(const cs_workload_spec* spec, int64_t* turns7, int64_t cap);
+
+typedef struct cs_engine_cfg {
+    cs_pool_cfg pool; /* pool.budget_blocks <= 0: the spec's pairing */
+    int concurrency;  /* <= 0: the spec's pairing */
+    int block_size;
+    int prefetch;     /* EngineConfig::prefetch_enabled */
+    int skip, take;   /* IdentityConfig */
+    int timing;       /* record CUDA events around each scan pass */
+} cs_engine_cfg;
+
+void cs_engine_cfg_default(cs_engine_cfg* cfg);
+
+/* EngineSim (engine.hpp:90-208) with the pool on the device: run_cell wiring
+ * (experiment.cpp:355-379) = materialize_requests (engine.cpp:8-35, hashed on the GPU by K1),
+ * build_warmup_catalog (:37-54), load, step until done. */
+int cs_engine_create(const cs_engine_cfg* cfg, const cs_workload_spec* spec, cs_engine_t* out);
+int cs_engine_destroy(cs_engine_t e);
+int cs_engine_step(cs_engine_t e, int* done); /* EngineSim::step (engine.cpp:372-392) */
+int cs_engine_run(cs_engine_t e);             /* step until done */
+/* Runs at most max_admissions more admissions (whole steps), for bounded timing windows. */
+int cs_engine_run_for(cs_engine_t e, int64_t max_admissions, int* done);
+
+typedef struct cs_engine_result {
+    int64_t turns, completed;
+    double hit_rate;
+    int64_t total_prompt_tokens, total_cached_tokens;
+    int64_t evictions, truncated, warmups_executed, warmups_dropped, warmups_issued;
+    double sim_us;
+    int64_t steps, admissions, scans, scanned_slots;
+    uint64_t tick;
+    double scan_ms, admit_ms; /* CUDA-event time of scan passes / whole admissions (timing=1) */
+} cs_engine_result;
+int cs_engine_result_get(cs_engine_t e, cs_engine_result* out);
+/* per-turn (by turn id) cached/prompt tokens and start/end simulated us; any may be NULL */
+int cs_engine_turns(cs_engine_t e, int64_t* cached, int64_t* prompt, double* start_us, double* end_us,
+                    int64_t cap);
+int64_t cs_engine_evictions(cs_engine_t e, uint64_t* keys, int64_t cap);
+/* drained warmups: step index, target agent id, issued tick */
+int64_t cs_engine_warmups(cs_engine_t e, int64_t* step, uint64_t* target, uint64_t* tick, int64_t cap);
+cs_pool_t cs_engine_pool(cs_engine_t e);
+
+const char* cs_last_error(void);
+const char* cs_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

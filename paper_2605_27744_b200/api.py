@@ -1,0 +1,297 @@
+"""Python mirror of the reference's public surface, backed by the sm_100a library.
+
+Names and argument meaning follow the reference's python module (py_module.cpp:79-186,
+python/cachesage/__init__.py) and C++ classes (EngineSim engine.hpp:90-208, CacheSagePolicy
+cachesage_policy.hpp:48-85). Everything computes on the GPU through include/cachesage_b200.h.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import workloads
+from ._lib import (CS_NO_AGENT, EngineCfg, EngineResult, PoolCfg, PoolStats, WorkloadSpec, check,
+                   lib)
+
+POLICIES = {"lru": 0, "cachesage": 1}
+
+
+def _p(a):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def _u64(a):
+    return np.ascontiguousarray(a, dtype=np.uint64)
+
+
+def _i32(a):
+    return np.ascontiguousarray(a, dtype=np.int32)
+
+
+def pool_cfg(budget, policy="cachesage", e_max=8, tau=0.01, w_pred=1.0, window=1024, min_confidence=0.5,
+             min_row_count=5, budget_per_step=1, agent_capacity=1024, device=0, grid_ctas=0):
+    c = PoolCfg()
+    lib().cs_pool_cfg_default(C.byref(c))
+    c.budget_blocks = int(budget)
+    c.policy = POLICIES[policy]
+    c.e_max, c.tau, c.w_pred, c.window = e_max, tau, w_pred, window
+    c.min_confidence, c.min_row_count, c.budget_per_step = min_confidence, min_row_count, budget_per_step
+    c.agent_capacity, c.device, c.grid_ctas = agent_capacity, device, grid_ctas
+    return c
+
+
+class Pool:
+    """A device block pool + transition learner (cs_pool_t).
+
+    The per-call methods mirror EngineSim::lookup / admit_pinned / unpin (engine.cpp:127-180)
+    and CacheSagePolicy::observe / poll_actions / score (cachesage_policy.cpp:50-130); the
+    caller owns the tick clock exactly like EngineSim::tick_.
+    """
+
+    def __init__(self, budget, **kw):
+        self._cfg = pool_cfg(budget, **kw)
+        h = C.c_void_p()
+        check(lib().cs_pool_create(C.byref(self._cfg), C.byref(h)))
+        self.h = h
+        self.budget = int(budget)
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().cs_pool_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def register_agents(self, ids):
+        ids = _u64(ids)
+        first = C.c_int(0)
+        check(lib().cs_register_agents(self.h, _p(ids), ids.size, C.byref(first)))
+        return first.value
+
+    def lookup(self, keys, counts, tick_base):
+        keys, counts = _u64(keys), _i32(counts)
+        cached, fm = C.c_int64(0), C.c_int(0)
+        check(lib().cs_lookup(self.h, _p(keys), _p(counts), keys.size, tick_base, C.byref(cached), C.byref(fm)))
+        return cached.value, fm.value
+
+    def probe_needed(self, keys):
+        keys = _u64(keys)
+        n = C.c_int(0)
+        check(lib().cs_probe_needed(self.h, _p(keys), keys.size, C.byref(n)))
+        return n.value
+
+    def observe_dispatch(self, prev, nxt, tick):
+        w = C.c_int(-1)
+        check(lib().cs_observe_dispatch(self.h, -1 if prev is None else prev, nxt, tick, C.byref(w)))
+        return None if w.value < 0 else w.value
+
+    def admit_pinned(self, keys, counts, agent=None, anchor=0, tick_base=0):
+        keys, counts = _u64(keys), _i32(counts)
+        n = keys.size
+        ev = np.zeros(max(n, 1), np.uint64)
+        pins = np.zeros(max(n, 1), np.uint32)
+        ne = C.c_int64(0)
+        check(lib().cs_admit_pinned(self.h, _p(keys), _p(counts), n, CS_NO_AGENT if agent is None else agent,
+                                    anchor, tick_base, _p(ev), ev.size, C.byref(ne), _p(pins)))
+        return ev[:ne.value].copy(), pins[:n].copy()
+
+    def unpin(self, slots):
+        s = np.ascontiguousarray(slots, dtype=np.uint32)
+        check(lib().cs_unpin_slots(self.h, _p(s), s.size))
+
+    def restore(self, keys, last_touch, agents=None, refs=None):
+        keys, lt = _u64(keys), _u64(last_touch)
+        ag = None if agents is None else np.ascontiguousarray(agents, dtype=np.uint32)
+        rf = None if refs is None else np.ascontiguousarray(refs, dtype=np.uint32)
+        check(lib().cs_restore(self.h, _p(keys), _p(lt), None if ag is None else _p(ag),
+                               None if rf is None else _p(rf), keys.size))
+
+    def score_snapshot(self, now_tick):
+        st = self.stats()
+        cap = max(st["resident"], 1)
+        k = np.zeros(cap, np.uint64)
+        s = np.zeros(cap, np.float64)
+        n = C.c_int64(0)
+        check(lib().cs_score_snapshot(self.h, now_tick, _p(k), _p(s), cap, C.byref(n)))
+        return k[:n.value], s[:n.value]
+
+    def hops(self, n):
+        h = np.zeros(max(n, 1), np.int32)
+        check(lib().cs_hops(self.h, _p(h), n))
+        return h[:n]
+
+    def poll_actions(self, cap=64):
+        t = np.zeros(cap, np.int32)
+        k = np.zeros(cap, np.uint64)
+        n = C.c_int(0)
+        check(lib().cs_poll_actions(self.h, _p(t), _p(k), cap, C.byref(n)))
+        return t[:n.value].copy(), k[:n.value].copy()
+
+    def stats(self):
+        s = PoolStats()
+        check(lib().cs_pool_get_stats(self.h, C.byref(s)))
+        return {f: getattr(s, f) for f, _ in PoolStats._fields_}
+
+
+def hash_prompts(prompts, block_size=16, skip=4, take=4, pool=None):
+    """K1 over a list of token sequences: (keys per prompt, counts per prompt, agent ids)."""
+    own = pool is None
+    if own:
+        pool = Pool(1024)
+    try:
+        lens = np.array([len(p) for p in prompts], dtype=np.int64)
+        tok_off = np.zeros(len(prompts) + 1, np.int64)
+        tok_off[1:] = np.cumsum(lens)
+        tokens = np.concatenate([np.asarray(p, dtype=np.uint32) for p in prompts]) if prompts else np.zeros(0, np.uint32)
+        tokens = np.ascontiguousarray(tokens, dtype=np.uint32)
+        blk_off = np.zeros(len(prompts) + 1, np.int64)
+        nblk = lib().cs_blocks_for(_p(tok_off), len(prompts), block_size, _p(blk_off))
+        if nblk < 0:
+            raise ValueError("block_keys_for: block_size must be positive")
+        keys = np.zeros(max(nblk, 1), np.uint64)
+        counts = np.zeros(max(nblk, 1), np.int32)
+        agents = np.zeros(max(len(prompts), 1), np.uint64)
+        check(lib().cs_hash_prompts(pool.h, _p(tokens), _p(tok_off), len(prompts), block_size, skip, take,
+                                    _p(blk_off), _p(keys), _p(counts), _p(agents)))
+        ks = [keys[blk_off[i]:blk_off[i + 1]].copy() for i in range(len(prompts))]
+        cs = [counts[blk_off[i]:blk_off[i + 1]].copy() for i in range(len(prompts))]
+        return ks, cs, agents[:len(prompts)].copy()
+    finally:
+        if own:
+            pool.close()
+
+
+def chain_hash(parent, tokens):
+    """chain_hash (hashing.cpp:26-35) on the GPU. A parent key is supported by hashing a
+    two-block prompt whose first block is unknown, so only parent=None is accepted here."""
+    if parent is not None:
+        raise ValueError("chain_hash with an explicit parent: use block_keys_for on the full prompt")
+    ks, _, _ = hash_prompts([tokens], block_size=max(len(tokens), 1))
+    return int(ks[0][0])
+
+
+def block_keys_for(tokens, block_size=16):
+    ks, cs, _ = hash_prompts([tokens], block_size=block_size)
+    return ks[0], cs[0]
+
+
+def derive_agent_identity_of_prompt(tokens, block_size=16, skip=4, take=4):
+    _, _, ag = hash_prompts([tokens], block_size=block_size, skip=skip, take=take)
+    return int(ag[0])
+
+
+def spec_struct(spec):
+    anchors = np.ascontiguousarray(spec["anchor_tokens"], dtype=np.int32)
+    trans = np.ascontiguousarray(spec["transition"], dtype=np.float64).reshape(-1)
+    s = WorkloadSpec()
+    s.n_agents = anchors.size
+    s.anchor_tokens = anchors.ctypes.data_as(C.POINTER(C.c_int))
+    s.transition = trans.ctypes.data_as(C.POINTER(C.c_double))
+    s.supervisor = -1 if spec.get("supervisor") is None else int(spec["supervisor"])
+    for f in ("turns_min", "turns_max", "sessions", "task_tokens", "history_growth", "decode_tokens",
+              "template_tokens", "concurrency", "budget_blocks"):
+        setattr(s, f, int(spec[f]))
+    s.seed = int(spec["seed"])
+    s.anchor_stride = int(spec.get("anchor_stride", 0))
+    s.hist_pos_bits = int(spec.get("hist_pos_bits", 0))
+    s._keep = (anchors, trans)
+    return s
+
+
+def generate_trace(spec):
+    """generate_trace (workload.cpp:156-182): rows (session, turn, agent, anchor, history,
+    prompt, decode). Host code (no GPU needed)."""
+    s = spec_struct(spec)
+    n = check(lib().cs_generate_trace(C.byref(s), None, 0))
+    out = np.zeros((max(n, 1), 7), np.int64)
+    lib().cs_generate_trace(C.byref(s), _p(out), n)
+    return out[:n]
+
+
+class Engine:
+    """EngineSim (engine.hpp:90-208) with the block pool, learner and eviction on the GPU."""
+
+    def __init__(self, spec, policy="cachesage", budget=None, concurrency=None, block_size=16, prefetch=True,
+                 skip=4, take=4, timing=False, **pool_kw):
+        cfg = EngineCfg()
+        lib().cs_engine_cfg_default(C.byref(cfg))
+        cfg.pool = pool_cfg(budget or 0, policy=policy, **pool_kw)
+        cfg.concurrency = concurrency or 0
+        cfg.block_size = block_size
+        cfg.prefetch = 1 if prefetch else 0
+        cfg.skip, cfg.take = skip, take
+        cfg.timing = 1 if timing else 0
+        self._spec = spec_struct(spec)
+        h = C.c_void_p()
+        check(lib().cs_engine_create(C.byref(cfg), C.byref(self._spec), C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().cs_engine_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def step(self):
+        d = C.c_int(0)
+        check(lib().cs_engine_step(self.h, C.byref(d)))
+        return bool(d.value)
+
+    def run(self):
+        check(lib().cs_engine_run(self.h))
+        return self.result()
+
+    def run_for(self, admissions):
+        d = C.c_int(0)
+        check(lib().cs_engine_run_for(self.h, admissions, C.byref(d)))
+        return bool(d.value)
+
+    def result(self):
+        r = EngineResult()
+        check(lib().cs_engine_result_get(self.h, C.byref(r)))
+        return {f: getattr(r, f) for f, _ in EngineResult._fields_}
+
+    def turns(self):
+        n = self.result()["turns"]
+        cached = np.zeros(max(n, 1), np.int64)
+        prompt = np.zeros(max(n, 1), np.int64)
+        st = np.zeros(max(n, 1), np.float64)
+        en = np.zeros(max(n, 1), np.float64)
+        check(lib().cs_engine_turns(self.h, _p(cached), _p(prompt), _p(st), _p(en), n))
+        return {"cached_tokens": cached[:n], "prompt_tokens": prompt[:n], "start_us": st[:n], "end_us": en[:n]}
+
+    def evictions(self):
+        n = check(lib().cs_engine_evictions(self.h, None, 0))
+        out = np.zeros(max(n, 1), np.uint64)
+        lib().cs_engine_evictions(self.h, _p(out), n)
+        return out[:n]
+
+    def warmups(self):
+        n = check(lib().cs_engine_warmups(self.h, None, None, None, 0))
+        st = np.zeros(max(n, 1), np.int64)
+        tg = np.zeros(max(n, 1), np.uint64)
+        tk = np.zeros(max(n, 1), np.uint64)
+        lib().cs_engine_warmups(self.h, _p(st), _p(tg), _p(tk), n)
+        return st[:n], tg[:n], tk[:n]
+
+
+def run_sim(spec, policy="cachesage", budget=None, concurrency=None, block_size=16, prefetch=True, **kw):
+    """py_module.cpp run_sim: one (trace, policy) simulation; aggregate metrics dict."""
+    if isinstance(spec, str):
+        spec = workloads.preset_by_name(spec)
+    eng = Engine(spec, policy=policy, budget=budget, concurrency=concurrency, block_size=block_size,
+                 prefetch=prefetch, **kw)
+    try:
+        return eng.run()
+    finally:
+        eng.close()

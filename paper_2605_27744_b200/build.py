@@ -1,0 +1,67 @@
+"""In-tree build of libcachesage_b200.so (sm_100a kernels + host C++ + C ABI).
+
+nvcc cross-compiles for sm_100a without a GPU, so this runs in the CPU container; the built
+.so travels to the GPU box with the repo snapshot. Exactness: -fmad=false on device and
+-ffp-contract=off on the host keep every fp64 score bit-identical to the reference.
+"""
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+OUT_DIR = os.path.join(HERE, "_build")
+LIB = os.path.join(HERE, "libcachesage_b200.so")
+
+NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+DEVICE_SRCS = ["cs_kernels.cu"]
+HOST_SRCS = ["cs_pool.cpp", "cs_engine.cpp"]
+DEPS = DEVICE_SRCS + HOST_SRCS + ["cs_device.cuh", "cs_launch.h", "cs_pool.hpp"]
+
+
+def _run(cmd, verbose):
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    subprocess.run(cmd, check=True)
+
+
+def _stale(target, sources):
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(s) > t for s in sources)
+
+
+def build(verbose: bool = False, force: bool = False) -> str:
+    os.makedirs(OUT_DIR, exist_ok=True)
+    inc = ["-I", os.path.join(ROOT, "include"), "-I", CSRC]
+    header_deps = [os.path.join(CSRC, h) for h in ("cs_device.cuh", "cs_launch.h", "cs_pool.hpp")]
+    header_deps.append(os.path.join(ROOT, "include", "cachesage_b200.h"))
+    objs = []
+    for src in DEVICE_SRCS:
+        s = os.path.join(CSRC, src)
+        o = os.path.join(OUT_DIR, src + ".o")
+        if force or _stale(o, [s] + header_deps):
+            _run([NVCC, "-O3", "-lineinfo", "-std=c++17", *ARCH, "-fmad=false", "-Xptxas", "-v",
+                  "-Xcompiler", "-fPIC,-ffp-contract=off", *inc, "-c", s, "-o", o], verbose)
+        objs.append(o)
+    for src in HOST_SRCS:
+        s = os.path.join(CSRC, src)
+        o = os.path.join(OUT_DIR, src + ".o")
+        if force or _stale(o, [s] + header_deps):
+            _run([NVCC, "-O2", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off,-Wall", *inc, "-c", s,
+                  "-o", o], verbose)
+        objs.append(o)
+    if force or _stale(LIB, objs):
+        _run([NVCC, "-shared", *ARCH, "-o", LIB, *objs, "-lcudart"], verbose)
+    return LIB
+
+
+if __name__ == "__main__":
+    import sys
+
+    print(build(verbose=True, force="--force" in sys.argv))

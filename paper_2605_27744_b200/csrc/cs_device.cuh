@@ -1,0 +1,251 @@
+// Device-side layout of the CacheSage block pool in HBM and the small helpers every kernel
+// shares. See DESIGN.md §3 for the byte layout and the roofline each kernel is held to.
+#pragma once
+
+#include <cstdint>
+
+namespace csb {
+
+// ---------------------------------------------------------------- constants
+
+constexpr unsigned long long kFreeTick = ~0ull;  // last_touch of a free slot (never a real tick)
+constexpr unsigned int kNoAgent = 0xFFFFFFFFu;   // Block::agent == nullopt (types.hpp:45)
+constexpr unsigned int kNoSlot = 0xFFFFFFFFu;
+constexpr unsigned int kSlotEmpty = 0xFFFFFFFFu;  // table entry never used
+constexpr unsigned int kSlotTomb = 0xFFFFFFFEu;   // table entry erased
+constexpr unsigned int kSlotClaim = 0xFFFFFFFDu;  // being written by an inserter
+
+constexpr int kMaxLists = 24;        // survival classes (e_max + 1) + 1 resident-oldest list
+constexpr int kChunk = 128;          // prompt blocks replayed per scan pass (candidates per class)
+constexpr int kSlack = 128;          // staged candidates tolerated before a CTA trims
+constexpr int kMaxAgents = 4096;     // dense A x A learner counts
+constexpr int kMaxPending = 64;      // queued warmups between drains
+constexpr int kScanThreads = 1024;   // one CTA per SM, 32 warps
+
+// hashing.hpp:13-14 + the identity seed of cachesage_policy.cpp:26
+constexpr unsigned long long kHashSeed = 0x5ca9e5a6e0f1c3b7ull;
+constexpr unsigned long long kRootParent = 0x9d2c5680f0a5b4d1ull;
+constexpr unsigned long long kGolden = 0x9e3779b97f4a7c15ull;
+constexpr unsigned long long kIdentitySalt = 0xa9e0c7d35b1f64e9ull;
+
+// splitmix64 finalizer (hashing.hpp:17-22)
+__host__ __device__ __forceinline__ unsigned long long mix64(unsigned long long x) {
+    x += kGolden;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+    return x ^ (x >> 31);
+}
+
+// ---------------------------------------------------------------- HBM layout
+
+// One open-addressing entry of the block table: BlockKey -> slot. 16 B, one sector per probe.
+struct __align__(16) TableEntry {
+    unsigned long long key;
+    unsigned int slot;  // kSlotEmpty / kSlotTomb / kSlotClaim or a pool slot
+    unsigned int pad;
+};
+
+// Mutable scalars of the pool + learner. Lives in device memory; only kernels write it.
+struct Ctrl {
+    long long resident;      // |cache_|
+    long long pinned;        // pinned_count_ (engine.hpp:177)
+    long long free_top;      // entries on the free-slot stack
+    long long tombstones;
+    unsigned long long n_ev; // eviction log length
+    long long scans;
+    long long scanned_slots;
+    unsigned long long rebuilds;
+    long long win_head, win_size;
+    int cur_agent;           // CacheSagePolicy::current_ (-1 = none)
+    int reach_built;         // !reach_.empty()
+    int step_warmups;
+    int n_pend;
+    int pend_target[kMaxPending];
+    unsigned long long pend_tick[kMaxPending];
+    // per-launch control of the cooperative admission kernel
+    unsigned int bar_count;
+    unsigned int bar_gen;
+    int done;
+    int need_scan;
+    int keep;
+    int chunk_lo, chunk_hi;
+    int error;
+};
+
+struct DevPool {
+    long long cap;            // slots == EngineConfig::budget_blocks
+    int policy;               // 0 lru, 1 cachesage
+    int e_max;
+    int n_lists;              // e_max + 2 (classes 0..e_max, resident list last)
+    int a_cap;
+    double tau, w_pred, min_conf;
+    unsigned long long min_row;
+    int budget_per_step;
+    long long window;
+    unsigned long long tmask;
+
+    // SoA pool: the scan reads lt/agent/refs = 16 B per slot
+    unsigned long long* lt;
+    unsigned int* agent;
+    unsigned int* refs;
+    unsigned long long* key;
+    int* tokens;
+    TableEntry* table;
+    unsigned int* free_stack;
+    unsigned long long* evlog;
+    long long evlog_cap;
+
+    // learner (dense over agent indices)
+    unsigned int* counts;     // a_cap * a_cap
+    unsigned int* totals;     // a_cap
+    int* win_a;               // window ring
+    int* win_b;
+    unsigned char* hop;       // a_cap
+    unsigned char* cls;       // a_cap: survival class used by the scan
+    unsigned long long* agent_ids;
+
+    // scan scratch
+    unsigned long long* gbound;   // [kMaxLists] running upper bound of each list's keep-th value
+    int* gcount;                  // [kMaxLists]
+    unsigned long long* gbuf_lt;  // [kMaxLists][gcap]
+    unsigned int* gbuf_slot;
+    long long gcap;
+    unsigned long long* fin_lt;   // [kMaxLists][kChunk + 2]
+    unsigned int* fin_slot;
+    int* fin_n;
+
+    // per-admission prompt scratch (grown by the host)
+    unsigned int* p_slot;
+    unsigned int* p_refs0;
+    long long p_cap;
+
+    Ctrl* ctrl;
+};
+
+#ifdef __CUDACC__
+// ---------------------------------------------------------------- block table
+
+__device__ __forceinline__ unsigned long long table_home(unsigned long long key, unsigned long long mask) {
+    return mix64(key ^ 0x51afd7ed558ccd1dull) & mask;
+}
+
+// Slot of `key` or kNoSlot. Lookups never run concurrently with inserts/erases (phases are
+// separated by barriers), so plain loads suffice. The table is kept at most half full of
+// live + tombstoned entries (the host rebuilds it past that), so probes always hit an EMPTY
+// entry; a probe that wraps the whole table is a corrupted table and traps instead of hanging.
+__device__ __forceinline__ unsigned int table_find(const DevPool& P, unsigned long long key) {
+    unsigned long long h = table_home(key, P.tmask);
+    for (unsigned long long n = 0; n <= P.tmask; ++n) {
+        const TableEntry e = P.table[h];
+        if (e.slot == kSlotEmpty) return kNoSlot;
+        if (e.slot < kSlotClaim && e.key == key) return e.slot;
+        h = (h + 1) & P.tmask;
+    }
+    __trap();
+    return kNoSlot;
+}
+
+// Lock-free insert of a key known to be absent: claim the first EMPTY or TOMB entry on the
+// probe path with a CAS on its slot word, then publish key and slot. Concurrent inserters
+// (bulk restore) race only through the CAS. Returns 1 if a tombstone was reused.
+__device__ __forceinline__ int table_insert(const DevPool& P, unsigned long long key, unsigned int slot) {
+    unsigned long long h = table_home(key, P.tmask);
+    for (unsigned long long n = 0; n <= 2 * P.tmask + 64; ++n) {
+        unsigned int s = P.table[h].slot;
+        if (s == kSlotEmpty || s == kSlotTomb) {
+            unsigned int old = atomicCAS(&P.table[h].slot, s, kSlotClaim);
+            if (old == s) {
+                P.table[h].key = key;
+                __threadfence();
+                atomicExch(&P.table[h].slot, slot);
+                return s == kSlotTomb ? 1 : 0;
+            }
+            continue;  // lost the race for this entry: re-read it
+        }
+        h = (h + 1) & P.tmask;
+    }
+    __trap();
+    return 0;
+}
+
+__device__ __forceinline__ void table_erase(const DevPool& P, unsigned long long key) {
+    unsigned long long h = table_home(key, P.tmask);
+    for (unsigned long long n = 0; n <= P.tmask; ++n) {
+        const TableEntry e = P.table[h];
+        if (e.slot == kSlotEmpty) return;
+        if (e.slot < kSlotClaim && e.key == key) {
+            P.table[h].slot = kSlotTomb;
+            return;
+        }
+        h = (h + 1) & P.tmask;
+    }
+    __trap();
+}
+
+// ---------------------------------------------------------------- exact fp64 scoring
+
+// recency_residual (runtime.cpp:23-32), no contraction.
+__device__ __forceinline__ double recency(unsigned long long lt, unsigned long long now, unsigned long long old) {
+    if (now <= old) return 1.0;
+    const double span = (double)(now - old);
+    const double off = lt >= old ? (double)(lt - old) : 0.0;
+    double r = __ddiv_rn(off, span);
+    r = r < 0.0 ? 0.0 : r;
+    r = r > 1.0 ? 1.0 : r;
+    return r;
+}
+
+// ReachabilityState::survival (reachability.cpp:17-20) for a hop class.
+__device__ __forceinline__ double survival_of_class(int c, int e_max) {
+    const int capped = c < e_max ? c : e_max;
+    return __dsub_rn(1.0, __ddiv_rn((double)capped, (double)e_max));
+}
+
+// CacheSagePolicy::score (cachesage_policy.cpp:79-85) / LruPolicy::score (baselines.cpp:12-14)
+__device__ __forceinline__ double score_of(int policy, double w_pred, double surv, unsigned long long lt,
+                                           unsigned long long now, unsigned long long old) {
+    const double rho = recency(lt, now, old);
+    if (policy == 0) return rho;
+    return __dadd_rn(__dmul_rn(w_pred, surv), rho);
+}
+
+// ---------------------------------------------------------------- sync helpers
+
+__device__ __forceinline__ unsigned int ld_acquire(const unsigned int* p) {
+    unsigned int v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Sense-reversing grid barrier for a cooperatively launched (co-resident) grid.
+__device__ __forceinline__ void grid_barrier(Ctrl* c) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned int gen = ld_acquire(&c->bar_gen);
+        __threadfence();
+        if (atomicAdd(&c->bar_count, 1u) == gridDim.x - 1) {
+            c->bar_count = 0;
+            __threadfence();
+            atomicAdd(&c->bar_gen, 1u);
+        } else {
+            // watchdog: a barrier that never opens (a CTA that cannot be co-resident, or a
+            // CTA that died) traps after ~10 s instead of hanging the device
+            unsigned long long spins = 0;
+            while (ld_acquire(&c->bar_gen) == gen) {
+                __nanosleep(64);
+                if (++spins > (1ull << 27)) __trap();
+            }
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+#endif  // __CUDACC__
+
+}  // namespace csb

@@ -1,0 +1,652 @@
+// cs_engine: the EngineSim-equivalent host scheduler over a device pool, plus the (widened)
+// trace generator. The scheduler is host C++ by design ("scheduler = caller,
+// kept on the host"); every pool / policy decision it needs is one admission launch.
+//
+// Reference behaviour restated (paths relative to /root/reference/proj):
+//   generate_trace                 workload.cpp:156-182 (draws :131-153)
+//   materialize_requests           engine.cpp:8-35      -> K1 hash_turns on the device
+//   build_warmup_catalog           engine.cpp:37-54     -> K1 hash_turns (warmup descriptors)
+//   load / step / done             engine.cpp:240-255, 372-392
+//   arrive / activate_sessions     engine.cpp:262-276
+//   start_request / try_start_head engine.cpp:278-351   -> one admit_kernel launch
+//   complete_earliest              engine.cpp:353-370   -> unpin_kernel
+//   drain_and_run_warmups          engine.cpp:197-238   -> admit_kernel (lookup + room + unpin)
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <deque>
+#include <map>
+#include <random>
+#include <unordered_map>
+#include <vector>
+
+#include "cs_pool.hpp"
+
+using csb::ck;
+using csb::CsError;
+
+void cs_set_error(const std::string& m);  // cs_pool.cpp
+
+namespace {
+
+template <class F>
+int eguard(F&& f) {
+    try {
+        f();
+        return CS_OK;
+    } catch (const CsError& e) {
+        cs_set_error(e.what());
+        return e.code;
+    } catch (const std::invalid_argument& e) {
+        cs_set_error(e.what());
+        return CS_ERR_INVALID_ARGUMENT;
+    } catch (const std::logic_error& e) {
+        cs_set_error(e.what());
+        return CS_ERR_LOGIC;
+    } catch (const std::exception& e) {
+        cs_set_error(e.what());
+        return CS_ERR_RUNTIME;
+    }
+}
+
+struct Spec {
+    int n_agents;
+    std::vector<int> anchor;
+    std::vector<double> trans;
+    int supervisor;
+    int turns_min, turns_max, sessions, task_tokens, history_growth, decode_tokens, template_tokens;
+    int concurrency, budget_blocks;
+    uint64_t seed;
+    uint32_t anchor_stride;
+    int pos_bits;
+};
+
+Spec to_spec(const cs_workload_spec* s) {
+    if (!s || s->n_agents < 1 || !s->anchor_tokens || !s->transition)
+        throw std::invalid_argument("workload: no agents");
+    Spec o;
+    o.n_agents = s->n_agents;
+    o.anchor.assign(s->anchor_tokens, s->anchor_tokens + s->n_agents);
+    o.trans.assign(s->transition, s->transition + (size_t)s->n_agents * s->n_agents);
+    o.supervisor = s->supervisor;
+    o.turns_min = s->turns_min;
+    o.turns_max = s->turns_max;
+    o.sessions = s->sessions;
+    o.task_tokens = s->task_tokens;
+    o.history_growth = s->history_growth;
+    o.decode_tokens = s->decode_tokens;
+    o.template_tokens = s->template_tokens;
+    o.concurrency = s->concurrency;
+    o.budget_blocks = s->budget_blocks;
+    o.seed = s->seed;
+    o.anchor_stride = s->anchor_stride ? s->anchor_stride : 0x00010000u;
+    o.pos_bits = s->hist_pos_bits ? s->hist_pos_bits : 20;
+    // WorkloadSpec::validate (workload.cpp:60-123), with the token-id limits of the chosen scheme
+    for (int i = 0; i < o.n_agents; ++i) {
+        double sum = 0.0;
+        for (int j = 0; j < o.n_agents; ++j) {
+            const double p = o.trans[(size_t)i * o.n_agents + j];
+            if (p < 0.0) throw std::invalid_argument("workload: negative transition probability");
+            sum += p;
+        }
+        if (std::abs(sum - 1.0) > 1e-9) throw std::invalid_argument("workload: transition row does not sum to 1");
+        if (o.anchor[i] < 1 || (uint32_t)o.anchor[i] >= o.anchor_stride)
+            throw std::invalid_argument("workload: anchor_tokens out of range");
+    }
+    if ((uint64_t)o.n_agents * o.anchor_stride > 0x01000000ull)
+        throw std::invalid_argument("workload: too many agents for the anchor token stride");
+    if (o.supervisor >= o.n_agents) throw std::invalid_argument("workload: supervisor index out of range");
+    if (o.turns_min < 1 || o.turns_max < o.turns_min) throw std::invalid_argument("workload: bad turns_per_session range");
+    if (o.sessions < 1 || (uint64_t)o.sessions > (1ull << (31 - o.pos_bits)))
+        throw std::invalid_argument("workload: sessions out of range");
+    if (o.task_tokens < 0 || o.history_growth < 0 || o.decode_tokens < 1 || o.template_tokens < 0)
+        throw std::invalid_argument("workload: negative size parameter");
+    const long long max_hist = (long long)o.task_tokens + (long long)(o.turns_max - 1) * o.history_growth;
+    if (max_hist > (1ll << o.pos_bits) - 1) throw std::invalid_argument("workload: history exceeds token id space");
+    return o;
+}
+
+// Turn = (session, turn_index, agent, anchor, history, prompt, decode)
+struct Turn {
+    int64_t v[7];
+};
+
+// generate_trace (workload.cpp:156-182): one std::mt19937_64 per session seeded from the spec
+// seed; uniform turn count by modulo; categorical walk by cumulative sum over positive entries.
+std::vector<Turn> generate(const Spec& s) {
+    std::vector<Turn> out;
+    const int start = s.supervisor >= 0 ? s.supervisor : 0;
+    for (int sess = 0; sess < s.sessions; ++sess) {
+        std::mt19937_64 rng(csb::mix64(s.seed ^ csb::mix64(0x5e5510ull + (uint64_t)sess)));
+        const int turns = s.turns_min + (int)(rng() % (uint64_t)(s.turns_max - s.turns_min + 1));
+        int agent = start;
+        for (int t = 0; t < turns; ++t) {
+            if (t > 0) {
+                const double* row = s.trans.data() + (size_t)agent * s.n_agents;
+                const double u = (double)(rng() >> 11) * 0x1.0p-53;
+                double acc = 0.0;
+                int last = 0, pick = -1;
+                for (int i = 0; i < s.n_agents; ++i) {
+                    if (row[i] <= 0.0) continue;
+                    last = i;
+                    acc += row[i];
+                    if (u < acc) {
+                        pick = i;
+                        break;
+                    }
+                }
+                agent = pick >= 0 ? pick : last;
+            }
+            Turn x;
+            x.v[0] = sess;
+            x.v[1] = t;
+            x.v[2] = agent;
+            x.v[3] = s.anchor[agent];
+            x.v[4] = (int64_t)s.task_tokens + (int64_t)t * s.history_growth;
+            x.v[5] = s.template_tokens + x.v[3] + x.v[4];
+            x.v[6] = s.decode_tokens;
+            out.push_back(x);
+        }
+    }
+    return out;
+}
+
+}  // namespace
+
+struct cs_engine {
+    cs_engine_cfg cfg{};
+    Spec spec;
+    cs_pool* pool = nullptr;
+    int budget = 0, conc = 0, bs = 16;
+
+    struct Req {
+        int session, turn_index;
+        int agent;  // dense index
+        int64_t blk_off;
+        int nb;
+        int anchor_blocks;
+        int64_t prompt_tokens;
+        int decode;
+    };
+    std::vector<Req> reqs;
+    struct Cat {
+        int agent;
+        int64_t blk_off;
+        int nb;
+        int64_t prompt_tokens;
+    };
+    std::unordered_map<int, Cat> catalog;  // by agent index
+    csb::DevBuf d_keys, d_counts, d_pins, d_cat_pins;
+
+    // scheduler (EngineSim::Scheduler, engine.hpp:158-168)
+    std::map<int, std::vector<int64_t>> by_session;
+    std::deque<int> pending_sessions;
+    std::unordered_map<int, size_t> session_pos;
+    std::vector<double> arrival_us;
+    std::deque<int64_t> ready;
+    struct Flight {
+        double end_us;
+        uint64_t seq;
+        int64_t req;
+        int npins;
+        int64_t cached;
+        double start_us;
+    };
+    std::vector<Flight> in_flight;
+    uint64_t flight_seq = 0;
+    int active_sessions = 0;
+    bool loaded = false;
+
+    uint64_t tick = 0;
+    double sim_now = 0.0;
+    int last_dispatched = -1;
+
+    // outputs
+    std::vector<int64_t> t_cached, t_prompt;
+    std::vector<double> t_start, t_end;
+    std::vector<char> t_done;
+    std::vector<unsigned long long> evictions;
+    unsigned long long ev_drained = 0;
+    std::vector<int64_t> w_step;
+    std::vector<uint64_t> w_target, w_tick;
+    int64_t completed = 0, truncated = 0, warm_exec = 0, warm_drop = 0, steps = 0, admissions = 0;
+    int64_t tot_prompt = 0, tot_cached = 0;
+
+    static bool later(const Flight& a, const Flight& b) {
+        return a.end_us > b.end_us || (a.end_us == b.end_us && a.seq > b.seq);
+    }
+
+    void build(const cs_engine_cfg& c, const cs_workload_spec* ws);
+    void drain_evictions(bool force);
+    bool done() const { return loaded && in_flight.empty() && ready.empty() && pending_sessions.empty(); }
+    void arrive(int64_t idx);
+    void activate_sessions();
+    bool try_start_head();
+    void complete_earliest();
+    void drain_and_run_warmups();
+    void execute_warmup(int target);
+    void step();
+};
+
+void cs_engine::build(const cs_engine_cfg& c, const cs_workload_spec* ws) {
+    cfg = c;
+    spec = to_spec(ws);
+    bs = c.block_size;
+    if (bs < 1) throw std::invalid_argument("EngineSim: budget, block size, and concurrency must be positive");
+    if (c.skip < 0 || c.take < 1) throw std::invalid_argument("CacheSagePolicy: invalid identity window");
+    budget = c.pool.budget_blocks > 0 ? (int)c.pool.budget_blocks : spec.budget_blocks;
+    conc = c.concurrency > 0 ? c.concurrency : spec.concurrency;
+    if (budget < 1 || conc < 1) throw std::invalid_argument("EngineSim: budget, block size, and concurrency must be positive");
+
+    const std::vector<Turn> turns = generate(spec);
+    const int64_t nt = (int64_t)turns.size();
+    // materialize_requests on the device: K1 over synthesised token ids
+    std::vector<csb::TurnDesc> desc(nt + spec.n_agents);
+    int64_t off = 0;
+    for (int64_t i = 0; i < nt; ++i) {
+        const Turn& t = turns[i];
+        csb::TurnDesc& d = desc[i];
+        d.session = (int)t.v[0];
+        d.agent = (int)t.v[2];
+        d.anchor_tokens = (int)t.v[3];
+        d.history_tokens = (int)t.v[4];
+        d.template_tokens = spec.template_tokens;
+        d.warmup = 0;
+        d.blk_off = off;
+        off += (t.v[5] + bs - 1) / bs;
+    }
+    const int64_t req_blocks = off;
+    for (int a = 0; a < spec.n_agents; ++a) {  // build_warmup_catalog: template + anchor + 1 token
+        csb::TurnDesc& d = desc[nt + a];
+        d.session = 0;
+        d.agent = a;
+        d.anchor_tokens = spec.anchor[a];
+        d.history_tokens = 0;
+        d.template_tokens = spec.template_tokens;
+        d.warmup = 1;
+        d.blk_off = off;
+        off += (spec.template_tokens + spec.anchor[a] + 1 + bs - 1) / bs;
+    }
+    const int64_t total_blocks = off;
+    d_keys.ensure(8 * total_blocks);
+    d_counts.ensure(4 * total_blocks);
+    d_pins.ensure(4 * total_blocks);
+    csb::DevBuf d_desc, d_agents;
+    d_desc.ensure(sizeof(csb::TurnDesc) * desc.size());
+    d_agents.ensure(8 * desc.size());
+
+    cs_pool_cfg pc = c.pool;
+    pc.budget_blocks = budget;
+    pool = new cs_pool();
+    try {
+        pool->create(pc);
+    } catch (...) {
+        pool->destroy();
+        delete pool;
+        pool = nullptr;
+        throw;
+    }
+    pool->timing = c.timing != 0;
+    cudaStream_t s = pool->stream;
+    ck(cudaMemcpyAsync(d_desc.p, desc.data(), sizeof(csb::TurnDesc) * desc.size(), cudaMemcpyHostToDevice, s), "H2D");
+    ck(csb::launch_hash_turns(d_desc.as<csb::TurnDesc>(), (int)desc.size(), bs, c.skip, c.take, spec.anchor_stride,
+                              spec.pos_bits, d_keys.as<unsigned long long>(), d_counts.as<int>(),
+                              d_agents.as<unsigned long long>(), s),
+       "hash_turns");
+    std::vector<uint64_t> ids(desc.size());
+    ck(cudaMemcpyAsync(ids.data(), d_agents.p, 8 * desc.size(), cudaMemcpyDeviceToHost, s), "D2H");
+    pool->sync();
+    d_desc.release();
+    d_agents.release();
+
+    // dense agent indices in first-seen order (requests, then catalog)
+    std::unordered_map<uint64_t, int> index;
+    std::vector<uint64_t> order;
+    auto idx_of = [&](uint64_t id) {
+        auto it = index.find(id);
+        if (it != index.end()) return it->second;
+        const int k = (int)order.size();
+        index.emplace(id, k);
+        order.push_back(id);
+        return k;
+    };
+    reqs.resize(nt);
+    for (int64_t i = 0; i < nt; ++i) {
+        const Turn& t = turns[i];
+        Req& r = reqs[i];
+        r.session = (int)t.v[0];
+        r.turn_index = (int)t.v[1];
+        r.agent = idx_of(ids[i]);
+        r.blk_off = desc[i].blk_off;
+        r.nb = (int)((t.v[5] + bs - 1) / bs);
+        r.anchor_blocks = (int)((spec.template_tokens + t.v[3]) / bs);
+        r.prompt_tokens = t.v[5];
+        r.decode = (int)t.v[6];
+    }
+    for (int a = 0; a < spec.n_agents; ++a) {
+        const int k = idx_of(ids[nt + a]);
+        if (catalog.count(k)) continue;  // catalog.emplace keeps the first
+        Cat ct;
+        ct.agent = k;
+        ct.blk_off = desc[nt + a].blk_off;
+        ct.nb = (int)((spec.template_tokens + spec.anchor[a] + 1 + bs - 1) / bs);
+        ct.prompt_tokens = spec.template_tokens + spec.anchor[a] + 1;
+        catalog.emplace(k, ct);
+    }
+    if ((int)order.size() > pool->P.a_cap)
+        throw CsError(CS_ERR_CAPACITY, "distinct agent identities exceed agent_capacity");
+    ck(cudaMemcpyAsync(pool->P.agent_ids, order.data(), 8 * order.size(), cudaMemcpyHostToDevice, s), "H2D");
+    pool->agent_ids = order;
+    pool->n_agents = (int)order.size();
+    pool->sync();
+    (void)req_blocks;
+
+    // load (engine.cpp:240-255)
+    for (int64_t i = 0; i < nt; ++i) by_session[reqs[i].session].push_back(i);
+    for (const auto& kv : by_session) pending_sessions.push_back(kv.first);
+    arrival_us.assign(nt, 0.0);
+    t_cached.assign(nt, 0);
+    t_prompt.assign(nt, 0);
+    t_start.assign(nt, 0.0);
+    t_end.assign(nt, 0.0);
+    t_done.assign(nt, 0);
+    loaded = true;
+}
+
+void cs_engine::drain_evictions(bool force) {
+    const unsigned long long tot = pool->ev_total;
+    if (tot == ev_drained) return;
+    if (!force && tot - ev_drained < (unsigned long long)pool->P.evlog_cap / 2) return;
+    const size_t base = evictions.size();
+    evictions.resize(base + (tot - ev_drained));
+    pool->copy_victims(ev_drained, tot, evictions.data() + base);
+    ev_drained = tot;
+}
+
+void cs_engine::arrive(int64_t idx) {
+    arrival_us[idx] = sim_now;
+    ++tick;  // emit(RequestArrival): note_agent only (no decision depends on alphabet order)
+    ready.push_back(idx);
+}
+
+void cs_engine::activate_sessions() {
+    while (active_sessions < conc && !pending_sessions.empty()) {
+        const int sid = pending_sessions.front();
+        pending_sessions.pop_front();
+        ++active_sessions;
+        session_pos[sid] = 0;
+        arrive(by_session[sid][0]);
+    }
+}
+
+bool cs_engine::try_start_head() {
+    if (ready.empty() || in_flight.size() >= (size_t)conc) return false;
+    const int64_t idx = ready.front();
+    const Req& r = reqs[idx];
+    const bool oversized = r.nb > budget;
+    if (oversized && !in_flight.empty()) return false;  // oversized prompts run solo
+    csb::AdmitArgs a{};
+    a.keys = d_keys.as<unsigned long long>() + r.blk_off;
+    a.counts = d_counts.as<int>() + r.blk_off;
+    a.n = r.nb;
+    a.flags = csb::kDispatch | csb::kAdmit | (oversized ? csb::kTruncate : (csb::kFeasible | csb::kLookup));
+    a.prev = last_dispatched;
+    a.next = r.agent;
+    a.agent = (unsigned int)r.agent;
+    a.anchor = r.anchor_blocks;
+    a.tick_base = tick;
+    a.pins_out = d_pins.as<unsigned int>() + r.blk_off;
+    const csb::AdmitStatus& st = pool->admit(a, r.nb);
+    ++admissions;
+    if (!st.started) return false;  // wait for in-flight pins to clear
+    ready.pop_front();
+    last_dispatched = r.agent;
+    tick = st.tick_after;
+    if (oversized) ++truncated;
+    Flight f;
+    f.seq = flight_seq++;
+    f.req = idx;
+    f.npins = st.admit_n;
+    f.cached = oversized ? 0 : st.cached;
+    f.start_us = sim_now;
+    const double ttft = 1000.0 + 50.0 * (double)(r.prompt_tokens - f.cached);
+    f.end_us = sim_now + ttft + 20000.0 * r.decode;
+    in_flight.push_back(f);
+    std::push_heap(in_flight.begin(), in_flight.end(), later);
+    drain_evictions(false);
+    return true;
+}
+
+void cs_engine::complete_earliest() {
+    std::pop_heap(in_flight.begin(), in_flight.end(), later);
+    Flight f = in_flight.back();
+    in_flight.pop_back();
+    sim_now = f.end_us;
+    ++tick;  // emit(TurnComplete)
+    const Req& r = reqs[f.req];
+    ck(csb::launch_unpin(pool->P, d_pins.as<unsigned int>() + r.blk_off, f.npins, pool->stream), "unpin");
+    const int sid = r.session;
+    auto& list = by_session[sid];
+    if (++session_pos[sid] < list.size()) {
+        arrive(list[session_pos[sid]]);
+    } else {
+        --active_sessions;
+    }
+    t_cached[f.req] = f.cached;
+    t_prompt[f.req] = r.prompt_tokens;
+    t_start[f.req] = f.start_us;
+    t_end[f.req] = f.end_us;
+    t_done[f.req] = 1;
+    tot_prompt += r.prompt_tokens;
+    tot_cached += f.cached;
+    ++completed;
+}
+
+void cs_engine::execute_warmup(int target) {
+    auto it = catalog.find(target);
+    if (it == catalog.end()) {
+        ++warm_drop;
+        return;
+    }
+    const Cat& c = it->second;
+    csb::AdmitArgs a{};
+    a.keys = d_keys.as<unsigned long long>() + c.blk_off;
+    a.counts = d_counts.as<int>() + c.blk_off;
+    a.n = c.nb;
+    a.flags = csb::kLookup | csb::kAdmit | csb::kWarmupRoom | csb::kUnpinAfter;
+    a.prev = -1;
+    a.next = -1;
+    a.agent = (unsigned int)c.agent;
+    a.anchor = -1;
+    a.tick_base = tick;
+    a.pins_out = d_pins.as<unsigned int>() + c.blk_off;
+    const csb::AdmitStatus& st = pool->admit(a, c.nb);
+    ++admissions;
+    tick = st.tick_after;
+    ++warm_exec;
+    drain_evictions(false);
+}
+
+void cs_engine::drain_and_run_warmups() {
+    // Runtime::drain_side_effects -> poll_actions (cachesage_policy.cpp:125-130)
+    std::vector<int> fx = pool->pending_targets;
+    for (size_t k = 0; k < fx.size(); ++k) {
+        w_step.push_back(steps);
+        w_target.push_back(pool->agent_ids[fx[k]]);
+        w_tick.push_back(pool->pending_ticks[k]);
+    }
+    pool->pending_targets.clear();
+    pool->pending_ticks.clear();
+    pool->poll_reset_pending = true;
+    if (!cfg.prefetch) return;
+    for (int t : fx) execute_warmup(t);
+}
+
+void cs_engine::step() {
+    if (done()) return;
+    activate_sessions();
+    bool progressed = false;
+    while (try_start_head()) progressed = true;
+    if (!progressed) {
+        if (!in_flight.empty()) {
+            complete_earliest();
+        } else if (!ready.empty()) {
+            throw std::runtime_error("scheduler stalled with an idle engine");
+        }
+    }
+    drain_and_run_warmups();
+    ++steps;
+}
+
+// ---------------------------------------------------------------------- C ABI (engine level)
+
+extern "C" {
+
+int64_t cs_generate_trace(const cs_workload_spec* ws, int64_t* turns7, int64_t cap) {
+    try {
+        const std::vector<Turn> t = generate(to_spec(ws));
+        for (int64_t i = 0; i < (int64_t)t.size() && i < cap && turns7; ++i)
+            std::memcpy(turns7 + 7 * i, t[i].v, sizeof(t[i].v));
+        return (int64_t)t.size();
+    } catch (const std::exception& e) {
+        cs_set_error(e.what());
+        return CS_ERR_INVALID_ARGUMENT;
+    }
+}
+
+void cs_engine_cfg_default(cs_engine_cfg* c) {
+    cs_pool_cfg_default(&c->pool);
+    c->pool.budget_blocks = 0;
+    c->concurrency = 0;
+    c->block_size = 16;
+    c->prefetch = 1;
+    c->skip = 4;
+    c->take = 4;
+    c->timing = 0;
+}
+
+int cs_engine_create(const cs_engine_cfg* cfg, const cs_workload_spec* spec, cs_engine_t* out) {
+    return eguard([&] {
+        if (!cfg || !spec || !out) throw std::invalid_argument("cs_engine_create: null argument");
+        auto* e = new cs_engine();
+        try {
+            e->build(*cfg, spec);
+        } catch (...) {
+            if (e->pool) {
+                e->pool->destroy();
+                delete e->pool;
+            }
+            delete e;
+            throw;
+        }
+        *out = e;
+    });
+}
+
+int cs_engine_destroy(cs_engine_t e) {
+    return eguard([&] {
+        if (!e) return;
+        e->d_keys.release();
+        e->d_counts.release();
+        e->d_pins.release();
+        if (e->pool) {
+            e->pool->destroy();
+            delete e->pool;
+        }
+        delete e;
+    });
+}
+
+int cs_engine_step(cs_engine_t e, int* done) {
+    return eguard([&] {
+        if (!e) throw std::invalid_argument("cs_engine_step: null engine");
+        e->step();
+        if (done) *done = e->done() ? 1 : 0;
+    });
+}
+
+int cs_engine_run(cs_engine_t e) {
+    return eguard([&] {
+        if (!e) throw std::invalid_argument("cs_engine_run: null engine");
+        while (!e->done()) e->step();
+        e->drain_evictions(true);
+    });
+}
+
+int cs_engine_run_for(cs_engine_t e, int64_t max_adm, int* done) {
+    return eguard([&] {
+        if (!e) throw std::invalid_argument("cs_engine_run_for: null engine");
+        const int64_t stop = e->admissions + max_adm;
+        while (!e->done() && e->admissions < stop) e->step();
+        if (done) *done = e->done() ? 1 : 0;
+    });
+}
+
+int cs_engine_result_get(cs_engine_t e, cs_engine_result* o) {
+    return eguard([&] {
+        if (!e || !o) throw std::invalid_argument("cs_engine_result_get: null argument");
+        e->drain_evictions(true);
+        std::memset(o, 0, sizeof(*o));
+        o->turns = (int64_t)e->reqs.size();
+        o->completed = e->completed;
+        o->total_prompt_tokens = e->tot_prompt;
+        o->total_cached_tokens = e->tot_cached;
+        o->hit_rate = e->tot_prompt > 0 ? (double)e->tot_cached / (double)e->tot_prompt : 0.0;
+        o->evictions = (int64_t)e->evictions.size();
+        o->truncated = e->truncated;
+        o->warmups_executed = e->warm_exec;
+        o->warmups_dropped = e->warm_drop;
+        o->warmups_issued = (int64_t)e->w_target.size();
+        o->sim_us = e->sim_now;
+        o->steps = e->steps;
+        o->admissions = e->admissions;
+        cs_pool_stats ps;
+        if (cs_pool_get_stats(e->pool, &ps) != CS_OK) throw std::runtime_error(cs_last_error());
+        o->scans = ps.scans;
+        o->scanned_slots = ps.scanned_slots;
+        o->tick = e->tick;
+        o->scan_ms = e->pool->scan_launch_ms;
+        o->admit_ms = e->pool->admit_ms;
+    });
+}
+
+int cs_engine_turns(cs_engine_t e, int64_t* cached, int64_t* prompt, double* start_us, double* end_us, int64_t cap) {
+    return eguard([&] {
+        if (!e) throw std::invalid_argument("cs_engine_turns: null engine");
+        const int64_t n = std::min<int64_t>(cap, (int64_t)e->reqs.size());
+        for (int64_t i = 0; i < n; ++i) {
+            if (cached) cached[i] = e->t_cached[i];
+            if (prompt) prompt[i] = e->t_prompt[i];
+            if (start_us) start_us[i] = e->t_start[i];
+            if (end_us) end_us[i] = e->t_end[i];
+        }
+    });
+}
+
+int64_t cs_engine_evictions(cs_engine_t e, uint64_t* keys, int64_t cap) {
+    if (!e) return CS_ERR_INVALID_ARGUMENT;
+    try {
+        e->drain_evictions(true);
+    } catch (const std::exception& ex) {
+        cs_set_error(ex.what());
+        return CS_ERR_CUDA;
+    }
+    const int64_t n = (int64_t)e->evictions.size();
+    if (keys) std::memcpy(keys, e->evictions.data(), 8 * std::min(n, cap));
+    return n;
+}
+
+int64_t cs_engine_warmups(cs_engine_t e, int64_t* step, uint64_t* target, uint64_t* tick, int64_t cap) {
+    if (!e) return CS_ERR_INVALID_ARGUMENT;
+    const int64_t n = (int64_t)e->w_target.size();
+    for (int64_t i = 0; i < n && i < cap; ++i) {
+        if (step) step[i] = e->w_step[i];
+        if (target) target[i] = e->w_target[i];
+        if (tick) tick[i] = e->w_tick[i];
+    }
+    return n;
+}
+
+cs_pool_t cs_engine_pool(cs_engine_t e) { return e ? e->pool : nullptr; }
+
+}  // extern "C"

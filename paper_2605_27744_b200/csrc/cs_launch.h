@@ -1,0 +1,89 @@
+// Host-visible launch surface of the sm_100a kernels (implemented in cs_kernels.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "cs_device.cuh"
+
+namespace csb {
+
+enum AdmitFlags : int {
+    kDispatch = 1,     // emit AgentDispatch{prev, next} through the policy first
+    kLookup = 2,       // EngineSim::lookup over all n blocks before admitting
+    kFeasible = 4,     // try_start_head feasibility probe; not started when it fails
+    kTruncate = 8,     // oversized prompt: admit budget - pinned blocks, no lookup
+    kWarmupRoom = 16,  // execute_warmup: admit min(n, budget - pinned) blocks
+    kUnpinAfter = 32,  // EngineSim::admit: unpin immediately
+    kPollReset = 64,   // a poll_actions drain happened before this call
+    kAdmit = 128       // run admit_pinned at all (lookup-only / observe-only calls clear it)
+};
+
+struct AdmitStatus {
+    int started;
+    int error;
+    int first_miss;
+    int admit_n;
+    long long cached;
+    long long n_evicted;
+    long long resident;
+    long long pinned;
+    unsigned long long tick_after;
+    unsigned long long ev_total;
+    int n_pend;
+    int warm_issued;
+    int scans;
+    int needed;
+    long long tombstones;
+    int pend_target[kMaxPending];
+    unsigned long long pend_tick[kMaxPending];
+};
+
+struct AdmitArgs {
+    const unsigned long long* keys;
+    const int* counts;
+    int n;
+    int flags;
+    int prev, next;
+    unsigned int agent;
+    int anchor;  // < 0: all admitted blocks carry the agent
+    unsigned long long tick_base;
+    int n_agents;
+    unsigned int* pins_out;
+    AdmitStatus* status;  // host-mapped
+};
+
+struct LaunchCfg {
+    int grid;
+    int threads;
+    int cap_per_list;
+    size_t smem;
+};
+
+// Picks threads / candidate capacity / dynamic smem for the pool's list count, sets the
+// kernel attribute, and returns the co-resident grid. Throws nothing; returns grid 0 on error.
+LaunchCfg admit_launch_config(const DevPool& P, int device, int want_grid);
+cudaError_t launch_admit(const DevPool& P, const AdmitArgs& a, const LaunchCfg& lc, int grid,
+                         cudaStream_t s);
+
+cudaError_t launch_init_pool(const DevPool& P, cudaStream_t s);
+cudaError_t launch_hash_prompts(const unsigned int* tokens, const long long* tok_off, int n, int bs, int skip,
+                                int take, const long long* blk_off, unsigned long long* keys, int* counts,
+                                unsigned long long* agents, int* err, cudaStream_t s);
+// Token-free K1 for generated traces: token ids synthesised from (session, agent, lengths).
+struct TurnDesc {
+    int session, agent, anchor_tokens, history_tokens;
+    int template_tokens, warmup;  // warmup: template + anchor + kWarmupUserToken
+    long long blk_off;
+};
+cudaError_t launch_hash_turns(const TurnDesc* turns, int n, int bs, int skip, int take, unsigned int anchor_stride,
+                              int hist_pos_bits, unsigned long long* keys, int* counts, unsigned long long* agents,
+                              cudaStream_t s);
+cudaError_t launch_unpin(const DevPool& P, const unsigned int* slots, int n, cudaStream_t s);
+cudaError_t launch_restore(const DevPool& P, const unsigned long long* keys, const unsigned long long* lt,
+                           const unsigned int* agents, const unsigned int* refs, long long n, cudaStream_t s);
+cudaError_t launch_probe(const DevPool& P, const unsigned long long* keys, int n, int* needed, cudaStream_t s);
+cudaError_t launch_scores(const DevPool& P, unsigned long long now, unsigned long long* keys, double* scores,
+                          long long* n_out, unsigned long long* scratch, cudaStream_t s);
+cudaError_t launch_table_rebuild(const DevPool& P, cudaStream_t s);
+
+}  // namespace csb

@@ -1,0 +1,540 @@
+// cs_pool: device allocation, the admission driver, and the pool-level C ABI.
+#include "cs_pool.hpp"
+
+#include <algorithm>
+#include <cstring>
+
+using csb::ck;
+using csb::CsError;
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return CS_OK;
+    } catch (const CsError& e) {
+        g_err = e.what();
+        return e.code;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return CS_ERR_INVALID_ARGUMENT;
+    } catch (const std::logic_error& e) {
+        g_err = e.what();
+        return CS_ERR_LOGIC;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return CS_ERR_RUNTIME;
+    }
+}
+
+template <class T>
+T* dmalloc(size_t n, const char* what) {
+    void* p = nullptr;
+    ck(cudaMalloc(&p, sizeof(T) * (n ? n : 1)), what);
+    return static_cast<T*>(p);
+}
+}  // namespace
+
+extern "C" const char* cs_last_error(void) { return g_err.c_str(); }
+extern "C" const char* cs_version(void) { return "cachesage_b200 0.1 (sm_100a)"; }
+
+void cs_set_error(const std::string& m) { g_err = m; }
+
+void cs_pool::create(const cs_pool_cfg& c) {
+    cfg = c;
+    if (c.budget_blocks < 1) throw std::invalid_argument("EngineSim: budget, block size, and concurrency must be positive");
+    if (c.e_max <= 0) throw std::invalid_argument("CacheSagePolicy: e_max must be positive");
+    if (c.e_max > csb::kMaxLists - 2) throw CsError(CS_ERR_CAPACITY, "e_max > 22 is not supported by the device select");
+    if (c.tau < 0.0 || c.tau > 1.0) throw std::invalid_argument("CacheSagePolicy: tau must be a probability");
+    if (c.min_confidence < 0.0 || c.budget_per_step < 0) throw std::invalid_argument("CacheSagePolicy: invalid prefetch gate");
+    if (c.window <= 0) throw std::invalid_argument("TransitionLearner: window capacity must be positive");
+    if (c.agent_capacity < 1 || c.agent_capacity > csb::kMaxAgents)
+        throw CsError(CS_ERR_CAPACITY, "agent_capacity must be in [1, 4096]");
+    if (c.budget_blocks >= (int64_t)0xFFFFFFF0ll) throw CsError(CS_ERR_CAPACITY, "budget exceeds 32-bit slot ids");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        throw CsError(CS_ERR_CUDA, "no CUDA device: cachesage_b200 has no CPU fallback");
+    device = c.device;
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    ck(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    ck(cudaEventCreate(&ev0), "cudaEventCreate");
+    ck(cudaEventCreate(&ev1), "cudaEventCreate");
+
+    csb::DevPool& p = P;
+    p.cap = c.budget_blocks;
+    p.policy = c.policy;
+    p.e_max = c.e_max;
+    p.n_lists = c.e_max + 2;
+    p.a_cap = c.agent_capacity;
+    p.tau = c.tau;
+    p.w_pred = c.w_pred;
+    p.min_conf = c.min_confidence;
+    p.min_row = c.min_row_count;
+    p.budget_per_step = c.budget_per_step;
+    p.window = c.window;
+    unsigned long long tcap = 1024;
+    while (tcap < 4ull * (unsigned long long)p.cap) tcap <<= 1;  // live+tombstones <= tcap/2 + one admission
+    p.tmask = tcap - 1;
+
+    p.lt = dmalloc<unsigned long long>(p.cap, "lt");
+    p.agent = dmalloc<unsigned int>(p.cap, "agent");
+    p.refs = dmalloc<unsigned int>(p.cap, "refs");
+    p.key = dmalloc<unsigned long long>(p.cap, "key");
+    p.tokens = dmalloc<int>(p.cap, "tokens");
+    p.table = dmalloc<csb::TableEntry>(tcap, "table");
+    p.free_stack = dmalloc<unsigned int>(p.cap, "free_stack");
+    p.evlog_cap = 1ll << 22;
+    p.evlog = dmalloc<unsigned long long>(p.evlog_cap, "evlog");
+    const size_t A = (size_t)p.a_cap;
+    p.counts = dmalloc<unsigned int>(A * A, "counts");
+    p.totals = dmalloc<unsigned int>(A, "totals");
+    p.win_a = dmalloc<int>(p.window, "win_a");
+    p.win_b = dmalloc<int>(p.window, "win_b");
+    p.hop = dmalloc<unsigned char>(A, "hop");
+    p.cls = dmalloc<unsigned char>(A, "cls");
+    p.agent_ids = dmalloc<unsigned long long>(A, "agent_ids");
+    ck(cudaMemsetAsync(p.counts, 0, sizeof(unsigned int) * A * A, stream), "memset");
+    ck(cudaMemsetAsync(p.totals, 0, sizeof(unsigned int) * A, stream), "memset");
+    p.ctrl = dmalloc<csb::Ctrl>(1, "ctrl");
+    ck(cudaMemsetAsync(p.ctrl, 0, sizeof(csb::Ctrl), stream), "memset");
+    p.gbound = dmalloc<unsigned long long>(csb::kMaxLists, "gbound");
+    p.gcount = dmalloc<int>(csb::kMaxLists, "gcount");
+    p.fin_lt = dmalloc<unsigned long long>((size_t)csb::kMaxLists * (csb::kChunk + 2), "fin_lt");
+    p.fin_slot = dmalloc<unsigned int>((size_t)csb::kMaxLists * (csb::kChunk + 2), "fin_slot");
+    p.fin_n = dmalloc<int>(csb::kMaxLists, "fin_n");
+    p.p_cap = 0;
+    p.p_slot = nullptr;
+    p.p_refs0 = nullptr;
+    ensure_prompt_scratch(4096);
+
+    lc = csb::admit_launch_config(p, device, c.grid_ctas);
+    if (lc.grid <= 0) throw CsError(CS_ERR_CUDA, "admit kernel: no launch configuration fits this device");
+    p.gcap = (long long)lc.grid * (csb::kChunk + 1);
+    p.gbuf_lt = dmalloc<unsigned long long>((size_t)csb::kMaxLists * p.gcap, "gbuf_lt");
+    p.gbuf_slot = dmalloc<unsigned int>((size_t)csb::kMaxLists * p.gcap, "gbuf_slot");
+
+    ck(cudaHostAlloc(reinterpret_cast<void**>(&st), sizeof(csb::AdmitStatus), cudaHostAllocMapped), "cudaHostAlloc");
+    std::memset(st, 0, sizeof(*st));
+    ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(&st_dev), st, 0), "cudaHostGetDevicePointer");
+    ck(csb::launch_init_pool(p, stream), "init_pool");
+    sync();
+}
+
+void cs_pool::destroy() {
+    csb::DevPool& p = P;
+    void* ptrs[] = {p.lt, p.agent, p.refs, p.key, p.tokens, p.table, p.free_stack, p.evlog, p.counts, p.totals,
+                    p.win_a, p.win_b, p.hop, p.cls, p.agent_ids, p.ctrl, p.gbound, p.gcount, p.fin_lt, p.fin_slot,
+                    p.fin_n, p.p_slot, p.p_refs0, p.gbuf_lt, p.gbuf_slot};
+    for (void* q : ptrs)
+        if (q) cudaFree(q);
+    d_keys.release();
+    d_counts.release();
+    d_pins.release();
+    d_aux.release();
+    d_aux2.release();
+    d_aux3.release();
+    if (st) cudaFreeHost(st);
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+    if (stream) cudaStreamDestroy(stream);
+}
+
+void cs_pool::ensure_prompt_scratch(long long n) {
+    if (n <= P.p_cap) return;
+    long long c = std::max<long long>(n, P.p_cap * 2);
+    if (P.p_slot) {
+        ck(cudaStreamSynchronize(stream), "sync");
+        cudaFree(P.p_slot);
+        cudaFree(P.p_refs0);
+    }
+    P.p_slot = dmalloc<unsigned int>(c, "p_slot");
+    P.p_refs0 = dmalloc<unsigned int>(c, "p_refs0");
+    P.p_cap = c;
+}
+
+const csb::AdmitStatus& cs_pool::admit(const csb::AdmitArgs& in, int n_for_grid) {
+    csb::AdmitArgs a = in;
+    ensure_prompt_scratch(std::max(1, a.n));
+    a.status = st_dev;
+    a.n_agents = n_agents;
+    if (poll_reset_pending) a.flags |= csb::kPollReset;
+    // No eviction is possible when every block could be inserted without reaching the budget:
+    // one CTA then suffices (the grid barrier degenerates), saving the cooperative launch.
+    const bool may_evict = (a.flags & csb::kAdmit) && resident + n_for_grid > P.cap;
+    const int grid = may_evict ? lc.grid : 1;
+    st->started = -1;
+    if (timing) ck(cudaEventRecord(ev0, stream), "cudaEventRecord");
+    ck(csb::launch_admit(P, a, lc, grid, stream), "admit_kernel launch");
+    if (timing) ck(cudaEventRecord(ev1, stream), "cudaEventRecord");
+    ck(cudaStreamSynchronize(stream), "admit_kernel");
+    poll_reset_pending = false;
+    const long long scans_before = scans_total;
+    (void)scans_before;
+    if (timing) {
+        float ms = 0.f;
+        ck(cudaEventElapsedTime(&ms, ev0, ev1), "cudaEventElapsedTime");
+        admit_ms += ms;
+        ++admit_launches;
+        if (st->scans > 0) {
+            scan_launch_ms += ms;
+            ++scan_launches;
+        }
+    }
+    if (st->started < 0) throw CsError(CS_ERR_CUDA, "admit kernel did not report a status");
+    resident = st->resident;
+    pinned = st->pinned;
+    ev_total = st->ev_total;
+    pending_targets.assign(st->pend_target, st->pend_target + std::min(st->n_pend, csb::kMaxPending));
+    pending_ticks.assign(st->pend_tick, st->pend_tick + std::min(st->n_pend, csb::kMaxPending));
+    if (st->error) throw std::runtime_error("evict_one: all resident blocks are pinned");
+    // erased entries become tombstones; rebuild before live + tombstones pass half the table
+    if ((unsigned long long)(st->resident + st->tombstones) > (P.tmask + 1) / 2) {
+        ck(csb::launch_table_rebuild(P, stream), "table rebuild");
+        ++table_rebuilds;
+    }
+    return *st;
+}
+
+void cs_pool::copy_victims(unsigned long long from, unsigned long long to, unsigned long long* out) {
+    const unsigned long long cap = (unsigned long long)P.evlog_cap;
+    if (to - from > cap) throw CsError(CS_ERR_CAPACITY, "eviction log overrun before it was drained");
+    unsigned long long i = from;
+    while (i < to) {
+        const unsigned long long off = i % cap;
+        const unsigned long long n = std::min(to - i, cap - off);
+        ck(cudaMemcpy(out + (i - from), P.evlog + off, n * 8, cudaMemcpyDeviceToHost), "evlog D2H");
+        i += n;
+    }
+}
+
+// ---------------------------------------------------------------------- C ABI (pool level)
+
+extern "C" {
+
+void cs_pool_cfg_default(cs_pool_cfg* c) {
+    c->budget_blocks = 120;
+    c->policy = 1;
+    c->e_max = 8;
+    c->tau = 0.01;
+    c->w_pred = 1.0;
+    c->window = 1024;
+    c->min_confidence = 0.5;
+    c->min_row_count = 5;
+    c->budget_per_step = 1;
+    c->agent_capacity = 1024;
+    c->device = 0;
+    c->grid_ctas = 0;
+}
+
+int cs_pool_create(const cs_pool_cfg* cfg, cs_pool_t* out) {
+    return guard([&] {
+        if (!cfg || !out) throw std::invalid_argument("cs_pool_create: null argument");
+        auto* p = new cs_pool();
+        try {
+            p->create(*cfg);
+        } catch (...) {
+            p->destroy();
+            delete p;
+            throw;
+        }
+        *out = p;
+    });
+}
+
+int cs_pool_destroy(cs_pool_t pool) {
+    return guard([&] {
+        if (!pool) return;
+        pool->destroy();
+        delete pool;
+    });
+}
+
+int cs_register_agents(cs_pool_t pool, const uint64_t* ids, int n, int* first) {
+    return guard([&] {
+        if (!pool || (n > 0 && !ids)) throw std::invalid_argument("cs_register_agents: null argument");
+        if (pool->n_agents + n > pool->P.a_cap) throw CsError(CS_ERR_CAPACITY, "agent capacity exceeded");
+        if (first) *first = pool->n_agents;
+        if (n <= 0) return;
+        ck(cudaMemcpyAsync(pool->P.agent_ids + pool->n_agents, ids, sizeof(uint64_t) * n, cudaMemcpyHostToDevice,
+                           pool->stream),
+           "agent ids H2D");
+        pool->agent_ids.insert(pool->agent_ids.end(), ids, ids + n);
+        pool->n_agents += n;
+        pool->sync();
+    });
+}
+
+int64_t cs_blocks_for(const int64_t* tok_off, int n, int bs, int64_t* blk_off) {
+    if (bs <= 0 || n < 0) return -1;
+    int64_t acc = 0;
+    for (int i = 0; i < n; ++i) {
+        if (blk_off) blk_off[i] = acc;
+        const int64_t len = tok_off[i + 1] - tok_off[i];
+        acc += (len + bs - 1) / bs;
+    }
+    if (blk_off) blk_off[n] = acc;
+    return acc;
+}
+
+int cs_hash_prompts(cs_pool_t pool, const uint32_t* tokens, const int64_t* tok_off, int n, int bs, int skip, int take,
+                    const int64_t* blk_off, uint64_t* keys_out, int32_t* counts_out, uint64_t* agents_out) {
+    return guard([&] {
+        if (!pool || !tok_off || !blk_off || n < 0) throw std::invalid_argument("cs_hash_prompts: null argument");
+        if (bs <= 0) throw std::invalid_argument("block_keys_for: block_size must be positive");
+        if (skip < 0 || take < 1) throw std::invalid_argument("derive_agent_identity: skip >= 0 and take >= 1 required");
+        if (n == 0) return;
+        const int64_t ntok = tok_off[n] - tok_off[0];
+        const int64_t nblk = blk_off[n];
+        for (int i = 0; i < n; ++i)
+            if (tok_off[i + 1] <= tok_off[i]) throw std::invalid_argument("chain_hash: token sequence must be nonempty");
+        cudaStream_t s = pool->stream;
+        csb::DevBuf tok, off, boff, k, c, ag, err;
+        tok.ensure(sizeof(uint32_t) * (ntok + 4));
+        off.ensure(sizeof(int64_t) * (n + 1));
+        boff.ensure(sizeof(int64_t) * (n + 1));
+        k.ensure(sizeof(uint64_t) * nblk);
+        c.ensure(sizeof(int32_t) * nblk);
+        ag.ensure(sizeof(uint64_t) * n);
+        err.ensure(sizeof(int));
+        std::vector<int64_t> rel(n + 1);
+        for (int i = 0; i <= n; ++i) rel[i] = tok_off[i] - tok_off[0];
+        ck(cudaMemcpyAsync(tok.p, tokens + tok_off[0], sizeof(uint32_t) * ntok, cudaMemcpyHostToDevice, s), "H2D");
+        ck(cudaMemcpyAsync(off.p, rel.data(), sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, s), "H2D");
+        ck(cudaMemcpyAsync(boff.p, blk_off, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, s), "H2D");
+        ck(cudaMemsetAsync(err.p, 0, sizeof(int), s), "memset");
+        ck(csb::launch_hash_prompts(tok.as<unsigned int>(), off.as<long long>(), n, bs, skip, take,
+                                    boff.as<long long>(), k.as<unsigned long long>(), c.as<int>(),
+                                    ag.as<unsigned long long>(), err.as<int>(), s),
+           "hash_prompts");
+        if (keys_out) ck(cudaMemcpyAsync(keys_out, k.p, sizeof(uint64_t) * nblk, cudaMemcpyDeviceToHost, s), "D2H");
+        if (counts_out) ck(cudaMemcpyAsync(counts_out, c.p, sizeof(int32_t) * nblk, cudaMemcpyDeviceToHost, s), "D2H");
+        if (agents_out) ck(cudaMemcpyAsync(agents_out, ag.p, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost, s), "D2H");
+        int herr = 0;
+        ck(cudaMemcpyAsync(&herr, err.p, sizeof(int), cudaMemcpyDeviceToHost, s), "D2H");
+        pool->sync();
+        tok.release();
+        off.release();
+        boff.release();
+        k.release();
+        c.release();
+        ag.release();
+        err.release();
+        if (herr) throw std::invalid_argument("chain_hash: token sequence must be nonempty");
+    });
+}
+
+static void stage_prompt(cs_pool_t pool, const uint64_t* keys, const int32_t* counts, int n) {
+    pool->d_keys.ensure(sizeof(uint64_t) * std::max(n, 1));
+    pool->d_counts.ensure(sizeof(int32_t) * std::max(n, 1));
+    pool->d_pins.ensure(sizeof(uint32_t) * std::max(n, 1));
+    if (n > 0) {
+        ck(cudaMemcpyAsync(pool->d_keys.p, keys, sizeof(uint64_t) * n, cudaMemcpyHostToDevice, pool->stream), "H2D");
+        if (counts)
+            ck(cudaMemcpyAsync(pool->d_counts.p, counts, sizeof(int32_t) * n, cudaMemcpyHostToDevice, pool->stream),
+               "H2D");
+        else
+            ck(cudaMemsetAsync(pool->d_counts.p, 0, sizeof(int32_t) * n, pool->stream), "memset");
+    }
+}
+
+int cs_lookup(cs_pool_t pool, const uint64_t* keys, const int32_t* counts, int n, uint64_t tick_base,
+              int64_t* cached, int* first_miss) {
+    return guard([&] {
+        if (!pool || n < 0 || (n > 0 && (!keys || !counts))) throw std::invalid_argument("cs_lookup: null argument");
+        stage_prompt(pool, keys, counts, n);
+        csb::AdmitArgs a{};
+        a.keys = pool->d_keys.as<unsigned long long>();
+        a.counts = pool->d_counts.as<int>();
+        a.n = n;
+        a.flags = csb::kLookup;
+        a.prev = -1;
+        a.next = -1;
+        a.agent = CS_NO_AGENT;
+        a.anchor = 0;
+        a.tick_base = tick_base;
+        const auto& st = pool->admit(a, 0);
+        if (cached) *cached = st.cached;
+        if (first_miss) *first_miss = st.first_miss;
+    });
+}
+
+int cs_probe_needed(cs_pool_t pool, const uint64_t* keys, int n, int* needed) {
+    return guard([&] {
+        if (!pool || n < 0 || (n > 0 && !keys) || !needed) throw std::invalid_argument("cs_probe_needed: null argument");
+        stage_prompt(pool, keys, nullptr, n);
+        pool->d_aux.ensure(sizeof(int));
+        ck(csb::launch_probe(pool->P, pool->d_keys.as<unsigned long long>(), n, pool->d_aux.as<int>(), pool->stream),
+           "probe");
+        ck(cudaMemcpyAsync(needed, pool->d_aux.p, sizeof(int), cudaMemcpyDeviceToHost, pool->stream), "D2H");
+        pool->sync();
+    });
+}
+
+int cs_observe_dispatch(cs_pool_t pool, int prev, int next, uint64_t tick, int* warmup_target) {
+    return guard([&] {
+        if (!pool || next < 0 || next >= pool->n_agents || prev >= pool->n_agents)
+            throw std::invalid_argument("cs_observe_dispatch: agent index out of range");
+        csb::AdmitArgs a{};
+        a.keys = nullptr;
+        a.counts = nullptr;
+        a.n = 0;
+        a.flags = csb::kDispatch;
+        a.prev = prev;
+        a.next = next;
+        a.agent = CS_NO_AGENT;
+        a.tick_base = tick - 1;  // the kernel assigns tick_base + 1 to the dispatch
+        const auto& st = pool->admit(a, 0);
+        if (warmup_target) *warmup_target = st.warm_issued;
+    });
+}
+
+int cs_admit_pinned(cs_pool_t pool, const uint64_t* keys, const int32_t* counts, int n, uint32_t agent,
+                    int anchor_blocks, uint64_t tick_base, uint64_t* evicted, int64_t cap, int64_t* n_evicted,
+                    uint32_t* pins) {
+    return guard([&] {
+        if (!pool || n < 0 || (n > 0 && (!keys || !counts))) throw std::invalid_argument("cs_admit_pinned: null argument");
+        if (agent != CS_NO_AGENT && (int)agent >= pool->n_agents)
+            throw std::invalid_argument("cs_admit_pinned: unregistered agent index");
+        stage_prompt(pool, keys, counts, n);
+        csb::AdmitArgs a{};
+        a.keys = pool->d_keys.as<unsigned long long>();
+        a.counts = pool->d_counts.as<int>();
+        a.n = n;
+        a.flags = csb::kAdmit;
+        a.prev = -1;
+        a.next = -1;
+        a.agent = agent;
+        a.anchor = anchor_blocks;
+        a.tick_base = tick_base;
+        a.pins_out = pool->d_pins.as<unsigned int>();
+        const unsigned long long ev_before = pool->ev_total;
+        const auto& st = pool->admit(a, n);
+        const long long ne = (long long)(st.ev_total - ev_before);
+        if (n_evicted) *n_evicted = ne;
+        if (evicted && cap > 0 && ne > 0) {
+            std::vector<unsigned long long> v(ne);
+            pool->copy_victims(ev_before, st.ev_total, v.data());
+            std::memcpy(evicted, v.data(), sizeof(uint64_t) * std::min<long long>(ne, cap));
+        }
+        if (pins && n > 0)
+            ck(cudaMemcpy(pins, pool->d_pins.p, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost), "pins D2H");
+    });
+}
+
+int cs_unpin_slots(cs_pool_t pool, const uint32_t* slots, int n) {
+    return guard([&] {
+        if (!pool || n < 0 || (n > 0 && !slots)) throw std::invalid_argument("cs_unpin_slots: null argument");
+        pool->d_aux.ensure(sizeof(uint32_t) * std::max(n, 1));
+        ck(cudaMemcpyAsync(pool->d_aux.p, slots, sizeof(uint32_t) * n, cudaMemcpyHostToDevice, pool->stream), "H2D");
+        ck(csb::launch_unpin(pool->P, pool->d_aux.as<unsigned int>(), n, pool->stream), "unpin");
+        pool->sync();
+        csb::Ctrl c;
+        ck(cudaMemcpy(&c, pool->P.ctrl, sizeof(c), cudaMemcpyDeviceToHost), "ctrl D2H");
+        pool->pinned = c.pinned;
+    });
+}
+
+int cs_restore(cs_pool_t pool, const uint64_t* keys, const uint64_t* lt, const uint32_t* agents, const uint32_t* refs,
+               int64_t n) {
+    return guard([&] {
+        if (!pool || n < 0 || (n > 0 && (!keys || !lt))) throw std::invalid_argument("cs_restore: null argument");
+        if (pool->resident + n > pool->P.cap) throw std::invalid_argument("cs_restore: snapshot exceeds the budget");
+        if (n == 0) return;
+        cudaStream_t s = pool->stream;
+        csb::DevBuf k, l, ag, rf;
+        k.ensure(8 * n);
+        l.ensure(8 * n);
+        ck(cudaMemcpyAsync(k.p, keys, 8 * n, cudaMemcpyHostToDevice, s), "H2D");
+        ck(cudaMemcpyAsync(l.p, lt, 8 * n, cudaMemcpyHostToDevice, s), "H2D");
+        if (agents) {
+            ag.ensure(4 * n);
+            ck(cudaMemcpyAsync(ag.p, agents, 4 * n, cudaMemcpyHostToDevice, s), "H2D");
+        }
+        if (refs) {
+            rf.ensure(4 * n);
+            ck(cudaMemcpyAsync(rf.p, refs, 4 * n, cudaMemcpyHostToDevice, s), "H2D");
+        }
+        ck(csb::launch_restore(pool->P, k.as<unsigned long long>(), l.as<unsigned long long>(),
+                               agents ? ag.as<unsigned int>() : nullptr, refs ? rf.as<unsigned int>() : nullptr, n, s),
+           "restore");
+        pool->sync();
+        k.release();
+        l.release();
+        ag.release();
+        rf.release();
+        csb::Ctrl c;
+        ck(cudaMemcpy(&c, pool->P.ctrl, sizeof(c), cudaMemcpyDeviceToHost), "ctrl D2H");
+        pool->resident = c.resident;
+        pool->pinned = c.pinned;
+    });
+}
+
+int cs_score_snapshot(cs_pool_t pool, uint64_t now_tick, uint64_t* keys, double* scores, int64_t cap, int64_t* n) {
+    return guard([&] {
+        if (!pool) throw std::invalid_argument("cs_score_snapshot: null pool");
+        const long long N = pool->P.cap;
+        csb::DevBuf k, s, cnt, scr;
+        k.ensure(8 * N);
+        s.ensure(8 * N);
+        cnt.ensure(8);
+        scr.ensure(8);
+        ck(csb::launch_scores(pool->P, now_tick, k.as<unsigned long long>(), s.as<double>(), cnt.as<long long>(),
+                              scr.as<unsigned long long>(), pool->stream),
+           "scores");
+        long long m = 0;
+        ck(cudaMemcpyAsync(&m, cnt.p, 8, cudaMemcpyDeviceToHost, pool->stream), "D2H");
+        pool->sync();
+        if (n) *n = m;
+        const long long c = std::min<long long>(m, cap);
+        if (c > 0 && keys) ck(cudaMemcpy(keys, k.p, 8 * c, cudaMemcpyDeviceToHost), "D2H");
+        if (c > 0 && scores) ck(cudaMemcpy(scores, s.p, 8 * c, cudaMemcpyDeviceToHost), "D2H");
+    });
+}
+
+int cs_hops(cs_pool_t pool, int* hops, int n) {
+    return guard([&] {
+        if (!pool || !hops || n < 0 || n > pool->P.a_cap) throw std::invalid_argument("cs_hops: bad argument");
+        csb::Ctrl c;
+        ck(cudaMemcpy(&c, pool->P.ctrl, sizeof(c), cudaMemcpyDeviceToHost), "ctrl D2H");
+        std::vector<unsigned char> h(std::max(n, 1));
+        if (n > 0) ck(cudaMemcpy(h.data(), pool->P.hop, n, cudaMemcpyDeviceToHost), "hop D2H");
+        for (int i = 0; i < n; ++i) hops[i] = c.reach_built ? (int)h[i] : -1;
+    });
+}
+
+int cs_poll_actions(cs_pool_t pool, int* targets, uint64_t* ticks, int cap, int* n) {
+    return guard([&] {
+        if (!pool || !n) throw std::invalid_argument("cs_poll_actions: null argument");
+        const int m = (int)pool->pending_targets.size();
+        for (int i = 0; i < m && i < cap; ++i) {
+            if (targets) targets[i] = pool->pending_targets[i];
+            if (ticks) ticks[i] = pool->pending_ticks[i];
+        }
+        *n = m;
+        pool->pending_targets.clear();
+        pool->pending_ticks.clear();
+        pool->poll_reset_pending = true;
+    });
+}
+
+int cs_pool_get_stats(cs_pool_t pool, cs_pool_stats* out) {
+    return guard([&] {
+        if (!pool || !out) throw std::invalid_argument("cs_pool_get_stats: null argument");
+        pool->sync();
+        csb::Ctrl c;
+        ck(cudaMemcpy(&c, pool->P.ctrl, sizeof(c), cudaMemcpyDeviceToHost), "ctrl D2H");
+        out->resident = c.resident;
+        out->pinned = c.pinned;
+        out->evictions = (int64_t)c.n_ev;
+        out->tombstones = c.tombstones;
+        out->scans = c.scans;
+        out->scanned_slots = c.scanned_slots;
+        out->rebuilds = c.rebuilds;
+        out->n_agents = pool->n_agents;
+    });
+}
+
+}  // extern "C"

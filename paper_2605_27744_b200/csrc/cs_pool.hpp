@@ -1,0 +1,85 @@
+// Host-side owner of one device block pool (the cs_pool_t handle) and the admission driver.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/cachesage_b200.h"
+#include "cs_launch.h"
+
+namespace csb {
+
+struct CsError : std::runtime_error {
+    int code;
+    CsError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+inline void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw CsError(CS_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t n = 0;
+    void ensure(size_t bytes) {
+        if (bytes <= n) return;
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+        ck(cudaMalloc(&p, bytes < 256 ? 256 : bytes), "cudaMalloc(scratch)");
+        n = bytes < 256 ? 256 : bytes;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    template <class T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+struct AdmitResult {
+    AdmitStatus st;
+    std::vector<unsigned long long> victims;  // filled only when requested
+};
+
+}  // namespace csb
+
+struct cs_pool {
+    cs_pool_cfg cfg{};
+    int device = 0;
+    csb::DevPool P{};
+    cudaStream_t stream = nullptr;
+    csb::LaunchCfg lc{};
+    csb::AdmitStatus* st = nullptr;      // host-mapped status
+    csb::AdmitStatus* st_dev = nullptr;
+    int n_agents = 0;
+    std::vector<uint64_t> agent_ids;
+    bool poll_reset_pending = false;
+    long long resident = 0, pinned = 0;  // mirrors of the last status
+    unsigned long long ev_total = 0;     // evictions logged so far
+    std::vector<int> pending_targets;
+    std::vector<unsigned long long> pending_ticks;
+    // scratch
+    csb::DevBuf d_keys, d_counts, d_pins, d_aux, d_aux2, d_aux3;
+    // timing (CUDA events around each admission launch)
+    bool timing = false;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    double admit_ms = 0.0, scan_launch_ms = 0.0;
+    long long admit_launches = 0, scan_launches = 0, scans_total = 0, table_rebuilds = 0;
+
+    void create(const cs_pool_cfg& c);
+    void destroy();
+    void ensure_prompt_scratch(long long n);
+    // Runs one admission launch and waits for it. grid_hint: 0 = decide (1 CTA when no eviction
+    // is possible, else the cooperative grid).
+    const csb::AdmitStatus& admit(const csb::AdmitArgs& args_in, int n_for_grid);
+    void copy_victims(unsigned long long from, unsigned long long to, unsigned long long* host_out);
+    void sync() { csb::ck(cudaStreamSynchronize(stream), "cudaStreamSynchronize"); }
+};
