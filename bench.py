@@ -1,0 +1,352 @@
+#!/usr/bin/env python
+"""Benchmark of the CacheSage per-step cache-policy hot path on B200.
+
+Metric (BASELINE.json): KV blocks scored+evicted per second per step, and % of HBM roofline.
+  value  = pool blocks scored per second = (slots scanned by the scoring passes) / device time,
+           prompt blocks already resident in HBM (Engine, device inputs)
+  e2e    = the same metric through the public API with HOST inputs: every admission copies its
+           prompt blocks H2D from pinned memory and reads its victims D2H inside the timed region
+A "step" = R consecutive admissions (start_request / execute_warmup) of the trace: per admission
+one cooperative launch does observe (learner, BFS, prefetch gate) -> lookup -> pool scan ->
+exact k-victim select -> replay/apply. Workload (default) = cfg4 on one GPU: the mixed
+five-generator 256-agent trace against a 16M-block pool pre-filled with the realistic snapshot
+composition. The pool SoA (16M x 16 B = 256 MiB) exceeds the 126 MB L2,
+so no flush is needed between steps.
+
+Multi-GPU (torchrun, one process per GPU): sessions are partitioned across ranks, each rank
+owns a full pool shard and its own trace partition; no data-path collective ("scaling": weak).
+Timing: CUDA events on the engine's stream, barrier + max over ranks.
+
+--impl reference: the UNMODIFIED reference (oracle/_ref, built from /root/reference) timed on the
+host cores: every worker thread owns a reference EngineSim filled to the same pool size; a step
+is one evict_one per worker (the reference scores every resident block per eviction).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "KV blocks scored+evicted/sec per step"
+UNIT = "blocks/s"
+BYTES_PER_SLOT = 16  # last_touch u64 + agent u32 + refs u32 per resident slot per pass
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+class Dist:
+    def __init__(self, world, rank, local):
+        self.world, self.rank, self.local = world, rank, local
+        self.pg = None
+        if world > 1:
+            import torch
+            import torch.distributed as td
+
+            torch.cuda.set_device(local)
+            td.init_process_group("nccl", device_id=torch.device("cuda", local))
+            self.td, self.torch = td, torch
+
+    def barrier(self):
+        if self.world > 1:
+            self.td.barrier()
+
+    def max(self, x):
+        if self.world == 1:
+            return x
+        t = self.torch.tensor([float(x)], device="cuda")
+        self.td.all_reduce(t, op=self.td.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum(self, x):
+        if self.world == 1:
+            return x
+        t = self.torch.tensor([float(x)], device="cuda")
+        self.td.all_reduce(t, op=self.td.ReduceOp.SUM)
+        return float(t.item())
+
+    def close(self):
+        if self.world > 1:
+            self.td.destroy_process_group()
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, device):
+        self.device = device
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            for n, v in zip(names, s[3:7]):
+                if v.strip().lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.samples)}
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def load_traffic(workload, pool):
+    """dram bytes per launch of the dominant kernel from the committed ncu capture, if any."""
+    p = os.path.join(ROOT, "profiles", "ncu_admit_summary.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        if d.get("pool_blocks") == pool:
+            return d.get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    return None
+
+
+def build_engine(W, spec, pool, device, host_inputs, seed):
+    import paper_2605_27744_b200 as cb
+
+    eng = cb.Engine(spec, policy="cachesage", budget=pool, timing=True, host_inputs=host_inputs,
+                    prefetch=spec.get("prefetch", True), agent_capacity=1024, device=device)
+    n_agents = len(eng.agents())
+    keys, lt, agents, refs = W.pool_snapshot(pool, n_agents, seed=seed, mode="realistic")
+    eng.restore(keys, lt, agents=agents, refs=refs)
+    del keys, lt, agents, refs
+    return eng
+
+
+def run_ours(args, dist):
+    from paper_2605_27744_b200 import workloads as W
+
+    pool = args.pool
+    spec = W.cfg4_mixed(sessions=args.sessions, budget=pool, seed=2608 + 7919 * dist.rank)
+    R = args.admissions_per_step
+
+    def timed_run(eng, steps):
+        ms = []
+        for _ in range(steps):
+            dist.barrier()
+            t, done = eng.run_timed(R)
+            ms.append(t)
+            if done:
+                raise RuntimeError("trace exhausted inside the timed region; raise --sessions")
+        return ms
+
+    # ---- value: inputs resident in HBM
+    eng = build_engine(W, spec, pool, dist.local, False, seed=11 + dist.rank)
+    timed_run(eng, args.warmup)
+    r0 = eng.result()
+    with ClockSampler(dist.local) as clk:
+        ms = timed_run(eng, args.steps)
+    r1 = eng.result()
+    tot_ms = dist.max(sum(ms))
+    scanned = dist.sum(r1["scanned_slots"] - r0["scanned_slots"])
+    evicted = dist.sum(r1["evictions"] - r0["evictions"])
+    adm = dist.sum(r1["admissions"] - r0["admissions"])
+    launches = dist.sum(r1["gpu_launches"] - r0["gpu_launches"])
+    scan_launches = r1["scan_launches"] - r0["scan_launches"]
+    scan_ms = r1["scan_ms"] - r0["scan_ms"]
+    value = scanned / (tot_ms / 1e3)
+    hit = r1["hit_rate"]
+    eng.close()
+
+    # ---- e2e: host inputs, H2D per admission, victims D2H per admission
+    eng = build_engine(W, spec, pool, dist.local, True, seed=11 + dist.rank)
+    timed_run(eng, args.warmup)
+    e0 = eng.result()
+    ems = timed_run(eng, args.steps)
+    e1 = eng.result()
+    e_tot_ms = dist.max(sum(ems))
+    e_scanned = dist.sum(e1["scanned_slots"] - e0["scanned_slots"])
+    e2e_value = e_scanned / (e_tot_ms / 1e3)
+    h2d = (e1["h2d_bytes"] - e0["h2d_bytes"]) / args.steps
+    d2h = (e1["d2h_bytes"] - e0["d2h_bytes"]) / args.steps
+    eng.close()
+
+    peak, peak_kind = measured_peak()
+    avg_scan_launch_s = (scan_ms / 1e3) / max(scan_launches, 1)
+    achieved = BYTES_PER_SLOT * pool / avg_scan_launch_s / 1e9 if scan_launches else 0.0
+    traffic = load_traffic("cfg4", pool)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": dist.world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u64/fp64",
+        "data": "synthetic: cfg4 mixed five-generator trace (generated, hashed on device) + "
+                "realistic 16M-slot pool snapshot (seeded permutation of last_touch)",
+        "config": {"workload": "cfg4-mixed-256", "pool_blocks_per_gpu": pool, "agents": 256,
+                   "trace_sessions_per_gpu": args.sessions, "admissions_per_step": R,
+                   "policy": "cachesage", "parallelism": f"replicas{dist.world} (sessions partitioned)",
+                   "l2": "pool SoA 256 MiB > 126 MB L2; no flush needed"},
+        "evictions_per_s": evicted / (tot_ms / 1e3), "admissions_per_s": adm / (tot_ms / 1e3),
+        "scans_per_step": (r1["scans"] - r0["scans"]) / args.steps, "hit_rate_so_far": hit,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h)},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak if peak else None, "traffic": traffic,
+                     "kernel": "admit_kernel (launches that ran a 16M-slot scoring pass)",
+                     "peak_source": peak_kind,
+                     "avg_launch_us": avg_scan_launch_s * 1e6, "algorithmic_bytes_per_launch": BYTES_PER_SLOT * pool},
+        "clocks": clk.summary(),
+    }
+    if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(pool, args)
+    return line
+
+
+def _ref_workers(pool):
+    n = os.cpu_count() or 1
+    try:
+        with open("/proc/meminfo") as f:
+            avail = [int(l.split()[1]) for l in f if l.startswith("MemAvailable")][0] * 1024
+    except Exception:
+        avail = 16 << 30
+    per = pool * 110 + (1 << 30)  # reference unordered_map ~100 B per entry
+    return max(1, min(n, 8, int(avail // per)))
+
+
+def cpu_baseline(pool, args):
+    """The reference's own CPU path on this host: fill a reference EngineSim to `pool` blocks,
+    then time evict_one (two O(N) passes, N consult_score calls). 1 core."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import refshim
+
+    if refshim.available():
+        s_per, fill = refshim.evict_bench(pool, 256, 13 * 256, 1, cachesage=True, k_warm=0)[:2]
+        kind = "reference"
+    else:  # the plain-C oracle port
+        from oracle import pyoracle as orc
+
+        s_per, fill = _oracle_evict(orc, pool)
+        kind = "port"
+    return {"value": pool / s_per, "unit": UNIT, "cores": 1, "kind": kind,
+            "sample": f"1 evict_one on a {pool}-block reference EngineSim (fill {fill:.1f}s untimed); "
+                      f"{s_per * 1e3:.0f} ms per eviction"}
+
+
+def _oracle_evict(orc, pool):
+    from paper_2605_27744_b200 import workloads as W
+
+    keys, lt, agents, refs = W.pool_snapshot(pool, 256, seed=11)
+    e = orc.Engine(pool, agent_cap=257)
+    t = time.time()
+    e.restore(keys, lt, agents=[None if a == 0xFFFFFFFF else int(a) for a in agents], refs=refs, tick=int(lt.max()))
+    fill = time.time() - t
+    t = time.time()
+    e.admit_pinned(np.array([2**63 + 1], np.uint64), np.array([16], np.int32))
+    return time.time() - t, fill
+
+
+def run_reference(args, dist):
+    """Reference arm: rank 0 only, all usable host threads, one evict_one per worker per step."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import refshim
+
+    pool = args.pool
+    if not refshim.available():
+        return {"impl": "reference", "unavailable": "oracle/_ref/libcachesage_ref.so not built (no /root/reference here)"}
+    T = _ref_workers(pool)
+    out = [None] * T
+
+    def work(i):
+        out[i] = refshim.evict_bench(pool, 256, 13 * 256, args.steps, cachesage=True, k_warm=args.warmup)
+
+    ths = [threading.Thread(target=work, args=(i,)) for i in range(T)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    s_per = max(o[0] for o in out)  # slowest worker bounds the step
+    value = T * pool / s_per
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": dist.world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": s_per * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u64/fp64", "impl": "reference",
+        "data": "synthetic: reference EngineSim filled with one-block prompts (13*256 agent blocks)",
+        "config": {"workload": "cfg4-mixed-256", "pool_blocks_per_gpu": pool, "agents": 256,
+                   "policy": "cachesage", "parallelism": f"{T} host threads x independent EngineSim"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": T, "kind": "reference",
+                         "sample": f"{T} threads x {args.steps} evict_one at pool {pool}"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    return line
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--pool", type=int, default=16 << 20)
+    ap.add_argument("--sessions", type=int, default=40_000)
+    ap.add_argument("--admissions-per-step", type=int, default=32)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    world, rank, local = dist_env()
+    if args.impl == "reference":
+        if rank == 0:
+            print(json.dumps(run_reference(args, Dist(1, 0, 0))), flush=True)
+        return
+    dist = Dist(world, rank, local)
+    try:
+        line = run_ours(args, dist)
+        if rank == 0:
+            print(json.dumps(line), flush=True)
+    finally:
+        dist.close()
+
+
+if __name__ == "__main__":
+    main()

@@ -131,7 +131,8 @@ int cs_pool_get_stats(cs_pool_t pool, cs_pool_stats* out);
 /* ------------------------------------------------------------------ engine (EngineSim) */
 
 /* WorkloadSpec (workload.hpp:21-42); anchor_stride / hist_pos_bits widen the token scheme
- * (0 = the reference's 0x10000 / 20). */
+ * (0 = the reference's 0x10000 / 20). supervisor = -2 with start_dist (n_agents weights) draws
+ * each session's start agent (widened generator: mixed multi-generator traces). */
 typedef struct cs_workload_spec {
     int n_agents;
     const int* anchor_tokens;
@@ -142,6 +143,7 @@ typedef struct cs_workload_spec {
     uint64_t seed;
     uint32_t anchor_stride;
     int hist_pos_bits;
+    const double* start_dist;
 } cs_workload_spec;
 
 /* Generates the trace (generate_trace, workload.cpp:156-182) on the host: turns7 rows
@@ -155,7 +157,9 @@ typedef struct cs_engine_cfg {
     int block_size;
     int prefetch;     /* EngineConfig::prefetch_enabled */
     int skip, take;   /* IdentityConfig */
-    int timing;       /* record CUDA events around each scan pass */
+    int timing;       /* record CUDA events around each admission launch */
+    int host_inputs;  /* 1: prompt blocks live in pinned host memory and are copied H2D per
+                         admission, victims copied D2H per admission (the end-to-end path) */
 } cs_engine_cfg;
 
 void cs_engine_cfg_default(cs_engine_cfg* cfg);
@@ -169,6 +173,15 @@ int cs_engine_step(cs_engine_t e, int* done); /* EngineSim::step (engine.cpp:372
 int cs_engine_run(cs_engine_t e);             /* step until done */
 /* Runs at most max_admissions more admissions (whole steps), for bounded timing windows. */
 int cs_engine_run_for(cs_engine_t e, int64_t max_admissions, int* done);
+/* Same, bracketed by CUDA events on the engine's stream: *device_ms = elapsed device time. */
+int cs_engine_run_timed(cs_engine_t e, int64_t max_admissions, double* device_ms, int* done);
+/* Restores a pool snapshot into the engine (cs_restore) and advances the engine clock past
+ * the snapshot's last_touch values. Agent indices refer to the engine's agent order
+ * (cs_engine_agents). */
+int cs_engine_restore(cs_engine_t e, const uint64_t* keys, const uint64_t* last_touch, const uint32_t* agents,
+                      const uint32_t* refs, int64_t n);
+/* The engine's dense agent index -> AgentId table; returns the count. */
+int cs_engine_agents(cs_engine_t e, uint64_t* ids, int cap);
 
 typedef struct cs_engine_result {
     int64_t turns, completed;
@@ -179,6 +192,9 @@ typedef struct cs_engine_result {
     int64_t steps, admissions, scans, scanned_slots;
     uint64_t tick;
     double scan_ms, admit_ms; /* CUDA-event time of scan passes / whole admissions (timing=1) */
+    int64_t scan_launches;    /* admission launches that ran at least one scan pass */
+    int64_t h2d_bytes, d2h_bytes; /* host<->device bytes moved by admissions (host_inputs=1) */
+    int64_t gpu_launches;         /* kernels launched by the engine so far */
 } cs_engine_result;
 int cs_engine_result_get(cs_engine_t e, cs_engine_result* out);
 /* per-turn (by turn id) cached/prompt tokens and start/end simulated us; any may be NULL */

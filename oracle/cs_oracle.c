@@ -139,6 +139,7 @@ long cso_generate(const cso_spec* s, int64_t* turns7, long cap) {
         mt64_seed(&r, cso_mix64(s->seed ^ cso_mix64(0x5e5510ULL + (uint64_t)sess)));
         const int turns = draw_uniform_int(&r, s->turns_min, s->turns_max);
         int agent = start;
+        if (s->supervisor == -2 && s->start_dist) agent = draw_categorical(&r, s->start_dist, s->n_agents);
         for (int t = 0; t < turns; ++t) {
             if (t > 0) agent = draw_categorical(&r, s->transition + (size_t)agent * s->n_agents, s->n_agents);
             if (n < cap && turns7) {

@@ -31,6 +31,7 @@ typedef struct cso_spec {
     uint64_t seed;
     uint32_t anchor_stride;   /* 0 -> 0x10000 */
     int hist_pos_bits;        /* 0 -> 20 */
+    const double* start_dist; /* used when supervisor == -2 */
 } cso_spec;
 
 /* RunConfig subset + CacheSageConfig (experiment.hpp:28-44, cachesage_policy.hpp:17-43). */

@@ -24,6 +24,7 @@ class Spec(C.Structure):
         ("task_tokens", C.c_int), ("history_growth", C.c_int), ("decode_tokens", C.c_int),
         ("template_tokens", C.c_int), ("concurrency", C.c_int), ("budget_blocks", C.c_int),
         ("seed", C.c_uint64), ("anchor_stride", C.c_uint32), ("hist_pos_bits", C.c_int),
+        ("start_dist", C.POINTER(C.c_double)),
     ]
 
 
@@ -57,7 +58,9 @@ def build():
 def lib():
     global _lib
     if _lib is None:
-        if not os.path.exists(LIB_PATH):
+        src = os.path.join(_HERE, "cs_oracle.c")
+        if not os.path.exists(LIB_PATH) or (os.path.exists(src) and
+                                            os.path.getmtime(src) > os.path.getmtime(LIB_PATH)):
             build()
         L = C.CDLL(LIB_PATH)
         vp = C.c_void_p
@@ -158,7 +161,12 @@ def spec_struct(spec):
     s.seed = int(spec["seed"])
     s.anchor_stride = int(spec.get("anchor_stride", 0))
     s.hist_pos_bits = int(spec.get("hist_pos_bits", 0))
-    s._keep = (anchors, trans)
+    sd = None
+    if spec.get("start_dist") is not None:
+        sd = np.ascontiguousarray(spec["start_dist"], dtype=np.float64)
+        s.start_dist = sd.ctypes.data_as(C.POINTER(C.c_double))
+        s.supervisor = -2
+    s._keep = (anchors, trans, sd)
     return s
 
 

@@ -412,7 +412,7 @@ double ref_exact_survival(unsigned long long target, int k, long n, const unsign
 // agentless, then the policy sees `n_agents` dispatches so reachability is built. Then times
 // `k` further one-block admissions, each of which triggers exactly one evict_one (two O(N)
 // passes). Returns seconds per eviction; fill seconds in *fill_s.
-double ref_evict_bench(long N, int n_agents, long n_agent_blocks, long k, int cachesage,
+double ref_evict_bench(long N, int n_agents, long n_agent_blocks, long k_warm, long k, int cachesage,
                        double* fill_s, unsigned long long* last_victim) {
     try {
         using clk = std::chrono::steady_clock;
@@ -442,6 +442,10 @@ double ref_evict_bench(long N, int n_agents, long n_agent_blocks, long k, int ca
             eng.admit(one, ag, ag ? 1 : 0);
         }
         *fill_s = std::chrono::duration<double>(clk::now() - f0).count();
+        for (long i = 0; i < k_warm; ++i) {
+            one[0].key = BlockKey{mix64(0xd111ULL + static_cast<std::uint64_t>(i))};
+            eng.admit(one, std::nullopt, 0);
+        }
         const auto e0 = clk::now();
         for (long i = 0; i < k; ++i) {
             one[0].key = BlockKey{mix64(0xe111ULL + static_cast<std::uint64_t>(i))};

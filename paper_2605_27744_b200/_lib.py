@@ -47,13 +47,14 @@ class WorkloadSpec(C.Structure):
         ("task_tokens", C.c_int), ("history_growth", C.c_int), ("decode_tokens", C.c_int),
         ("template_tokens", C.c_int), ("concurrency", C.c_int), ("budget_blocks", C.c_int),
         ("seed", C.c_uint64), ("anchor_stride", C.c_uint32), ("hist_pos_bits", C.c_int),
+        ("start_dist", C.POINTER(C.c_double)),
     ]
 
 
 class EngineCfg(C.Structure):
     _fields_ = [
         ("pool", PoolCfg), ("concurrency", C.c_int), ("block_size", C.c_int), ("prefetch", C.c_int),
-        ("skip", C.c_int), ("take", C.c_int), ("timing", C.c_int),
+        ("skip", C.c_int), ("take", C.c_int), ("timing", C.c_int), ("host_inputs", C.c_int),
     ]
 
 
@@ -65,7 +66,8 @@ class EngineResult(C.Structure):
         ("warmups_dropped", C.c_int64), ("warmups_issued", C.c_int64), ("sim_us", C.c_double),
         ("steps", C.c_int64), ("admissions", C.c_int64), ("scans", C.c_int64),
         ("scanned_slots", C.c_int64), ("tick", C.c_uint64), ("scan_ms", C.c_double),
-        ("admit_ms", C.c_double),
+        ("admit_ms", C.c_double), ("scan_launches", C.c_int64), ("h2d_bytes", C.c_int64),
+        ("d2h_bytes", C.c_int64), ("gpu_launches", C.c_int64),
     ]
 
 
@@ -95,6 +97,9 @@ SIGNATURES = {
     "cs_engine_step": (C.c_int, [vp, C.POINTER(C.c_int)]),
     "cs_engine_run": (C.c_int, [vp]),
     "cs_engine_run_for": (C.c_int, [vp, C.c_int64, C.POINTER(C.c_int)]),
+    "cs_engine_run_timed": (C.c_int, [vp, C.c_int64, C.POINTER(C.c_double), C.POINTER(C.c_int)]),
+    "cs_engine_restore": (C.c_int, [vp, vp, vp, vp, vp, C.c_int64]),
+    "cs_engine_agents": (C.c_int, [vp, vp, C.c_int]),
     "cs_engine_result_get": (C.c_int, [vp, C.POINTER(EngineResult)]),
     "cs_engine_turns": (C.c_int, [vp, vp, vp, vp, vp, C.c_int64]),
     "cs_engine_evictions": (C.c_int64, [vp, vp, C.c_int64]),

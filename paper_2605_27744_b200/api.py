@@ -199,7 +199,12 @@ def spec_struct(spec):
     s.seed = int(spec["seed"])
     s.anchor_stride = int(spec.get("anchor_stride", 0))
     s.hist_pos_bits = int(spec.get("hist_pos_bits", 0))
-    s._keep = (anchors, trans)
+    sd = None
+    if spec.get("start_dist") is not None:
+        sd = np.ascontiguousarray(spec["start_dist"], dtype=np.float64)
+        s.start_dist = sd.ctypes.data_as(C.POINTER(C.c_double))
+        s.supervisor = -2
+    s._keep = (anchors, trans, sd)
     return s
 
 
@@ -217,7 +222,7 @@ class Engine:
     """EngineSim (engine.hpp:90-208) with the block pool, learner and eviction on the GPU."""
 
     def __init__(self, spec, policy="cachesage", budget=None, concurrency=None, block_size=16, prefetch=True,
-                 skip=4, take=4, timing=False, **pool_kw):
+                 skip=4, take=4, timing=False, host_inputs=False, **pool_kw):
         cfg = EngineCfg()
         lib().cs_engine_cfg_default(C.byref(cfg))
         cfg.pool = pool_cfg(budget or 0, policy=policy, **pool_kw)
@@ -226,6 +231,7 @@ class Engine:
         cfg.prefetch = 1 if prefetch else 0
         cfg.skip, cfg.take = skip, take
         cfg.timing = 1 if timing else 0
+        cfg.host_inputs = 1 if host_inputs else 0
         self._spec = spec_struct(spec)
         h = C.c_void_p()
         check(lib().cs_engine_create(C.byref(cfg), C.byref(self._spec), C.byref(h)))
@@ -255,6 +261,25 @@ class Engine:
         d = C.c_int(0)
         check(lib().cs_engine_run_for(self.h, admissions, C.byref(d)))
         return bool(d.value)
+
+    def run_timed(self, admissions):
+        """(device milliseconds from CUDA events on the engine stream, done)."""
+        ms, d = C.c_double(0), C.c_int(0)
+        check(lib().cs_engine_run_timed(self.h, admissions, C.byref(ms), C.byref(d)))
+        return ms.value, bool(d.value)
+
+    def agents(self):
+        n = check(lib().cs_engine_agents(self.h, None, 0))
+        out = np.zeros(max(n, 1), np.uint64)
+        lib().cs_engine_agents(self.h, _p(out), n)
+        return out[:n]
+
+    def restore(self, keys, last_touch, agents=None, refs=None):
+        keys, lt = _u64(keys), _u64(last_touch)
+        ag = None if agents is None else np.ascontiguousarray(agents, dtype=np.uint32)
+        rf = None if refs is None else np.ascontiguousarray(refs, dtype=np.uint32)
+        check(lib().cs_engine_restore(self.h, _p(keys), _p(lt), None if ag is None else _p(ag),
+                                      None if rf is None else _p(rf), keys.size))
 
     def result(self):
         r = EngineResult()

@@ -59,6 +59,7 @@ struct Spec {
     uint64_t seed;
     uint32_t anchor_stride;
     int pos_bits;
+    std::vector<double> start_dist;  // supervisor == -2: per-session start draw
 };
 
 Spec to_spec(const cs_workload_spec* s) {
@@ -81,6 +82,10 @@ Spec to_spec(const cs_workload_spec* s) {
     o.seed = s->seed;
     o.anchor_stride = s->anchor_stride ? s->anchor_stride : 0x00010000u;
     o.pos_bits = s->hist_pos_bits ? s->hist_pos_bits : 20;
+    if (s->supervisor == -2) {
+        if (!s->start_dist) throw std::invalid_argument("workload: supervisor -2 needs start_dist");
+        o.start_dist.assign(s->start_dist, s->start_dist + s->n_agents);
+    }
     // WorkloadSpec::validate (workload.cpp:60-123), with the token-id limits of the chosen scheme
     for (int i = 0; i < o.n_agents; ++i) {
         double sum = 0.0;
@@ -95,7 +100,7 @@ Spec to_spec(const cs_workload_spec* s) {
     }
     if ((uint64_t)o.n_agents * o.anchor_stride > 0x01000000ull)
         throw std::invalid_argument("workload: too many agents for the anchor token stride");
-    if (o.supervisor >= o.n_agents) throw std::invalid_argument("workload: supervisor index out of range");
+    if (o.supervisor >= o.n_agents || o.supervisor < -2) throw std::invalid_argument("workload: supervisor index out of range");
     if (o.turns_min < 1 || o.turns_max < o.turns_min) throw std::invalid_argument("workload: bad turns_per_session range");
     if (o.sessions < 1 || (uint64_t)o.sessions > (1ull << (31 - o.pos_bits)))
         throw std::invalid_argument("workload: sessions out of range");
@@ -113,6 +118,19 @@ struct Turn {
 
 // generate_trace (workload.cpp:156-182): one std::mt19937_64 per session seeded from the spec
 // seed; uniform turn count by modulo; categorical walk by cumulative sum over positive entries.
+int categorical(std::mt19937_64& rng, const double* row, int n) {
+    const double u = (double)(rng() >> 11) * 0x1.0p-53;
+    double acc = 0.0;
+    int last = 0;
+    for (int i = 0; i < n; ++i) {
+        if (row[i] <= 0.0) continue;
+        last = i;
+        acc += row[i];
+        if (u < acc) return i;
+    }
+    return last;  // u fell into the rounding gap below 1.0
+}
+
 std::vector<Turn> generate(const Spec& s) {
     std::vector<Turn> out;
     const int start = s.supervisor >= 0 ? s.supervisor : 0;
@@ -120,23 +138,9 @@ std::vector<Turn> generate(const Spec& s) {
         std::mt19937_64 rng(csb::mix64(s.seed ^ csb::mix64(0x5e5510ull + (uint64_t)sess)));
         const int turns = s.turns_min + (int)(rng() % (uint64_t)(s.turns_max - s.turns_min + 1));
         int agent = start;
+        if (!s.start_dist.empty()) agent = categorical(rng, s.start_dist.data(), s.n_agents);
         for (int t = 0; t < turns; ++t) {
-            if (t > 0) {
-                const double* row = s.trans.data() + (size_t)agent * s.n_agents;
-                const double u = (double)(rng() >> 11) * 0x1.0p-53;
-                double acc = 0.0;
-                int last = 0, pick = -1;
-                for (int i = 0; i < s.n_agents; ++i) {
-                    if (row[i] <= 0.0) continue;
-                    last = i;
-                    acc += row[i];
-                    if (u < acc) {
-                        pick = i;
-                        break;
-                    }
-                }
-                agent = pick >= 0 ? pick : last;
-            }
+            if (t > 0) agent = categorical(rng, s.trans.data() + (size_t)agent * s.n_agents, s.n_agents);
             Turn x;
             x.v[0] = sess;
             x.v[1] = t;
@@ -177,6 +181,13 @@ struct cs_engine {
     };
     std::unordered_map<int, Cat> catalog;  // by agent index
     csb::DevBuf d_keys, d_counts, d_pins, d_cat_pins;
+    // host_inputs: prompt blocks in pinned host memory, staged per admission
+    uint64_t* h_keys = nullptr;
+    int* h_counts = nullptr;
+    csb::DevBuf d_stage_keys, d_stage_counts;
+    int64_t h2d_bytes = 0, d2h_bytes = 0;
+    void stage(csb::AdmitArgs& a, int64_t blk_off, int nb);
+    void fetch_victims(unsigned long long before);
 
     // scheduler (EngineSim::Scheduler, engine.hpp:158-168)
     std::map<int, std::vector<int64_t>> by_session;
@@ -268,18 +279,11 @@ void cs_engine::build(const cs_engine_cfg& c, const cs_workload_spec* ws) {
         off += (spec.template_tokens + spec.anchor[a] + 1 + bs - 1) / bs;
     }
     const int64_t total_blocks = off;
-    d_keys.ensure(8 * total_blocks);
-    d_counts.ensure(4 * total_blocks);
-    d_pins.ensure(4 * total_blocks);
-    csb::DevBuf d_desc, d_agents;
-    d_desc.ensure(sizeof(csb::TurnDesc) * desc.size());
-    d_agents.ensure(8 * desc.size());
-
     cs_pool_cfg pc = c.pool;
     pc.budget_blocks = budget;
     pool = new cs_pool();
     try {
-        pool->create(pc);
+        pool->create(pc);  // selects the device; every allocation below lands on it
     } catch (...) {
         pool->destroy();
         delete pool;
@@ -287,6 +291,12 @@ void cs_engine::build(const cs_engine_cfg& c, const cs_workload_spec* ws) {
         throw;
     }
     pool->timing = c.timing != 0;
+    d_keys.ensure(8 * total_blocks);
+    d_counts.ensure(4 * total_blocks);
+    d_pins.ensure(4 * total_blocks);
+    csb::DevBuf d_desc, d_agents;
+    d_desc.ensure(sizeof(csb::TurnDesc) * desc.size());
+    d_agents.ensure(8 * desc.size());
     cudaStream_t s = pool->stream;
     ck(cudaMemcpyAsync(d_desc.p, desc.data(), sizeof(csb::TurnDesc) * desc.size(), cudaMemcpyHostToDevice, s), "H2D");
     ck(csb::launch_hash_turns(d_desc.as<csb::TurnDesc>(), (int)desc.size(), bs, c.skip, c.take, spec.anchor_stride,
@@ -340,6 +350,15 @@ void cs_engine::build(const cs_engine_cfg& c, const cs_workload_spec* ws) {
     pool->n_agents = (int)order.size();
     pool->sync();
     (void)req_blocks;
+    if (c.host_inputs) {
+        // the end-to-end path: prompt blocks live on the host and cross PCIe per admission
+        ck(cudaMallocHost(reinterpret_cast<void**>(&h_keys), 8 * total_blocks), "cudaMallocHost");
+        ck(cudaMallocHost(reinterpret_cast<void**>(&h_counts), 4 * total_blocks), "cudaMallocHost");
+        ck(cudaMemcpy(h_keys, d_keys.p, 8 * total_blocks, cudaMemcpyDeviceToHost), "D2H");
+        ck(cudaMemcpy(h_counts, d_counts.p, 4 * total_blocks, cudaMemcpyDeviceToHost), "D2H");
+        d_keys.release();
+        d_counts.release();
+    }
 
     // load (engine.cpp:240-255)
     for (int64_t i = 0; i < nt; ++i) by_session[reqs[i].session].push_back(i);
@@ -361,6 +380,41 @@ void cs_engine::drain_evictions(bool force) {
     evictions.resize(base + (tot - ev_drained));
     pool->copy_victims(ev_drained, tot, evictions.data() + base);
     ev_drained = tot;
+}
+
+void cs_engine::stage(csb::AdmitArgs& a, int64_t blk_off, int nb) {
+    if (!cfg.host_inputs) {
+        a.keys = d_keys.as<unsigned long long>() + blk_off;
+        a.counts = d_counts.as<int>() + blk_off;
+        return;
+    }
+    d_stage_keys.ensure(8 * (size_t)std::max(nb, 1));
+    d_stage_counts.ensure(4 * (size_t)std::max(nb, 1));
+    ck(cudaMemcpyAsync(d_stage_keys.p, h_keys + blk_off, 8 * (size_t)nb, cudaMemcpyHostToDevice, pool->stream),
+       "H2D");
+    ck(cudaMemcpyAsync(d_stage_counts.p, h_counts + blk_off, 4 * (size_t)nb, cudaMemcpyHostToDevice, pool->stream),
+       "H2D");
+    h2d_bytes += 12 * (int64_t)nb;
+    a.keys = d_stage_keys.as<unsigned long long>();
+    a.counts = d_stage_counts.as<int>();
+}
+
+// host_inputs: the admission's result (victim keys) is read back immediately
+void cs_engine::fetch_victims(unsigned long long before) {
+    if (!cfg.host_inputs) {
+        drain_evictions(false);
+        return;
+    }
+    const unsigned long long tot = pool->ev_total;
+    if (tot > ev_drained) {
+        const size_t base = evictions.size();
+        evictions.resize(base + (tot - ev_drained));
+        pool->copy_victims(ev_drained, tot, evictions.data() + base);
+        d2h_bytes += 8 * (int64_t)(tot - ev_drained);
+        ev_drained = tot;
+    }
+    d2h_bytes += (int64_t)sizeof(csb::AdmitStatus);  // the mapped status record
+    (void)before;
 }
 
 void cs_engine::arrive(int64_t idx) {
@@ -386,8 +440,7 @@ bool cs_engine::try_start_head() {
     const bool oversized = r.nb > budget;
     if (oversized && !in_flight.empty()) return false;  // oversized prompts run solo
     csb::AdmitArgs a{};
-    a.keys = d_keys.as<unsigned long long>() + r.blk_off;
-    a.counts = d_counts.as<int>() + r.blk_off;
+    stage(a, r.blk_off, r.nb);
     a.n = r.nb;
     a.flags = csb::kDispatch | csb::kAdmit | (oversized ? csb::kTruncate : (csb::kFeasible | csb::kLookup));
     a.prev = last_dispatched;
@@ -396,8 +449,10 @@ bool cs_engine::try_start_head() {
     a.anchor = r.anchor_blocks;
     a.tick_base = tick;
     a.pins_out = d_pins.as<unsigned int>() + r.blk_off;
+    const unsigned long long ev_before = pool->ev_total;
     const csb::AdmitStatus& st = pool->admit(a, r.nb);
     ++admissions;
+    if (cfg.host_inputs) d2h_bytes += (int64_t)sizeof(csb::AdmitStatus);
     if (!st.started) return false;  // wait for in-flight pins to clear
     ready.pop_front();
     last_dispatched = r.agent;
@@ -413,7 +468,7 @@ bool cs_engine::try_start_head() {
     f.end_us = sim_now + ttft + 20000.0 * r.decode;
     in_flight.push_back(f);
     std::push_heap(in_flight.begin(), in_flight.end(), later);
-    drain_evictions(false);
+    fetch_victims(ev_before);
     return true;
 }
 
@@ -425,6 +480,7 @@ void cs_engine::complete_earliest() {
     ++tick;  // emit(TurnComplete)
     const Req& r = reqs[f.req];
     ck(csb::launch_unpin(pool->P, d_pins.as<unsigned int>() + r.blk_off, f.npins, pool->stream), "unpin");
+    if (f.npins > 0) ++pool->launches;
     const int sid = r.session;
     auto& list = by_session[sid];
     if (++session_pos[sid] < list.size()) {
@@ -450,8 +506,7 @@ void cs_engine::execute_warmup(int target) {
     }
     const Cat& c = it->second;
     csb::AdmitArgs a{};
-    a.keys = d_keys.as<unsigned long long>() + c.blk_off;
-    a.counts = d_counts.as<int>() + c.blk_off;
+    stage(a, c.blk_off, c.nb);
     a.n = c.nb;
     a.flags = csb::kLookup | csb::kAdmit | csb::kWarmupRoom | csb::kUnpinAfter;
     a.prev = -1;
@@ -460,11 +515,12 @@ void cs_engine::execute_warmup(int target) {
     a.anchor = -1;
     a.tick_base = tick;
     a.pins_out = d_pins.as<unsigned int>() + c.blk_off;
+    const unsigned long long ev_before = pool->ev_total;
     const csb::AdmitStatus& st = pool->admit(a, c.nb);
     ++admissions;
     tick = st.tick_after;
     ++warm_exec;
-    drain_evictions(false);
+    fetch_victims(ev_before);
 }
 
 void cs_engine::drain_and_run_warmups() {
@@ -523,6 +579,7 @@ void cs_engine_cfg_default(cs_engine_cfg* c) {
     c->skip = 4;
     c->take = 4;
     c->timing = 0;
+    c->host_inputs = 0;
 }
 
 int cs_engine_create(const cs_engine_cfg* cfg, const cs_workload_spec* spec, cs_engine_t* out) {
@@ -549,6 +606,10 @@ int cs_engine_destroy(cs_engine_t e) {
         e->d_keys.release();
         e->d_counts.release();
         e->d_pins.release();
+        e->d_stage_keys.release();
+        e->d_stage_counts.release();
+        if (e->h_keys) cudaFreeHost(e->h_keys);
+        if (e->h_counts) cudaFreeHost(e->h_counts);
         if (e->pool) {
             e->pool->destroy();
             delete e->pool;
@@ -607,7 +668,56 @@ int cs_engine_result_get(cs_engine_t e, cs_engine_result* o) {
         o->tick = e->tick;
         o->scan_ms = e->pool->scan_launch_ms;
         o->admit_ms = e->pool->admit_ms;
+        o->scan_launches = e->pool->scan_launches;
+        o->h2d_bytes = e->h2d_bytes;
+        o->d2h_bytes = e->d2h_bytes;
+        o->gpu_launches = e->pool->launches;
     });
+}
+
+int cs_engine_run_timed(cs_engine_t e, int64_t max_adm, double* device_ms, int* done) {
+    return eguard([&] {
+        if (!e) throw std::invalid_argument("cs_engine_run_timed: null engine");
+        cudaEvent_t a, b;
+        ck(cudaEventCreate(&a), "cudaEventCreate");
+        ck(cudaEventCreate(&b), "cudaEventCreate");
+        e->pool->sync();
+        ck(cudaEventRecord(a, e->pool->stream), "cudaEventRecord");
+        const int64_t stop = e->admissions + max_adm;
+        while (!e->done() && e->admissions < stop) e->step();
+        ck(cudaEventRecord(b, e->pool->stream), "cudaEventRecord");
+        ck(cudaEventSynchronize(b), "cudaEventSynchronize");
+        float ms = 0.f;
+        ck(cudaEventElapsedTime(&ms, a, b), "cudaEventElapsedTime");
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+        if (device_ms) *device_ms = ms;
+        if (done) *done = e->done() ? 1 : 0;
+    });
+}
+
+int cs_engine_restore(cs_engine_t e, const uint64_t* keys, const uint64_t* lt, const uint32_t* agents,
+                      const uint32_t* refs, int64_t n) {
+    return eguard([&] {
+        if (!e) throw std::invalid_argument("cs_engine_restore: null engine");
+        if (e->admissions > 0) throw std::logic_error("cs_engine_restore: restore before the first step");
+        uint64_t mx = 0;
+        for (int64_t i = 0; i < n; ++i) {
+            mx = std::max<uint64_t>(mx, lt[i]);
+            if (agents && agents[i] != CS_NO_AGENT && (int)agents[i] >= e->pool->n_agents)
+                throw std::invalid_argument("cs_engine_restore: agent index out of range");
+        }
+        const int rc = cs_restore(e->pool, keys, lt, agents, refs, n);
+        if (rc != CS_OK) throw CsError(rc, cs_last_error());
+        e->tick = std::max<uint64_t>(e->tick, mx);
+    });
+}
+
+int cs_engine_agents(cs_engine_t e, uint64_t* ids, int cap) {
+    if (!e) return CS_ERR_INVALID_ARGUMENT;
+    const int n = (int)e->pool->agent_ids.size();
+    for (int i = 0; i < n && i < cap && ids; ++i) ids[i] = e->pool->agent_ids[i];
+    return n;
 }
 
 int cs_engine_turns(cs_engine_t e, int64_t* cached, int64_t* prompt, double* start_us, double* end_us, int64_t cap) {

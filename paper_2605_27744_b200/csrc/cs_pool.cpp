@@ -168,6 +168,7 @@ const csb::AdmitStatus& cs_pool::admit(const csb::AdmitArgs& in, int n_for_grid)
     st->started = -1;
     if (timing) ck(cudaEventRecord(ev0, stream), "cudaEventRecord");
     ck(csb::launch_admit(P, a, lc, grid, stream), "admit_kernel launch");
+    ++launches;
     if (timing) ck(cudaEventRecord(ev1, stream), "cudaEventRecord");
     ck(cudaStreamSynchronize(stream), "admit_kernel");
     poll_reset_pending = false;
@@ -194,6 +195,7 @@ const csb::AdmitStatus& cs_pool::admit(const csb::AdmitArgs& in, int n_for_grid)
     if ((unsigned long long)(st->resident + st->tombstones) > (P.tmask + 1) / 2) {
         ck(csb::launch_table_rebuild(P, stream), "table rebuild");
         ++table_rebuilds;
+        launches += 2;
     }
     return *st;
 }

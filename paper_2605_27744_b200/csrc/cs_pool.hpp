@@ -73,6 +73,7 @@ struct cs_pool {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     double admit_ms = 0.0, scan_launch_ms = 0.0;
     long long admit_launches = 0, scan_launches = 0, scans_total = 0, table_rebuilds = 0;
+    long long launches = 0;  // every kernel this handle launched (the bench's gpu_launches)
 
     void create(const cs_pool_cfg& c);
     void destroy();

@@ -171,6 +171,86 @@ def cfg3_swarm(sessions=100_000, budget=4 << 20):
     }
 
 
+def cfg4_mixed(sessions=400_000, budget=16 << 20, seed=2608):
+    """cfg4: five generators on disjoint agent ranges totalling 256 agents (supervisor-style 6,
+    chain 12, hierarchical 32, swarm 128, iid 78); each session draws its generator via
+    start_dist, so sessions of all five interleave. ~10 turns per session."""
+    A = 256
+    T = [[0.0] * A for _ in range(A)]
+    start = [0.0] * A
+    # supervisor-style [0, 6): supervisor-a's matrix
+    sup = preset_by_name("supervisor-a")["transition"]
+    for i in range(6):
+        for j in range(6):
+            T[i][j] = sup[i][j]
+    start[0] = 0.2
+    # chain [6, 18)
+    for k in range(12):
+        T[6 + k][6 + (k + 1) % 12] = 1.0
+    start[6] = 0.2
+    # hierarchical [18, 50)
+    h = cfg2_hierarchical()["transition"]
+    for i in range(32):
+        for j in range(32):
+            T[18 + i][18 + j] = h[i][j]
+    start[18] = 0.2
+    # swarm [50, 178)
+    s = cfg3_swarm()["transition"]
+    for i in range(128):
+        for j in range(128):
+            T[50 + i][50 + j] = s[i][j]
+        start[50 + i] = 0.2 / 128
+    # iid [178, 256)
+    for i in range(78):
+        for j in range(78):
+            T[178 + i][178 + j] = 1.0 / 78
+        start[178 + i] = 0.2 / 78
+    return {
+        "name": "cfg4-mixed-256",
+        "anchor_tokens": [176] * A,
+        "transition": T, "supervisor": None, "start_dist": start,
+        "turns_min": 6, "turns_max": 14, "sessions": sessions,
+        "task_tokens": 160, "history_growth": 8, "decode_tokens": 32, "template_tokens": 16,
+        "concurrency": 4, "budget_blocks": budget, "seed": seed,
+        "anchor_stride": 0x10000, "hist_pos_bits": 11, "prefetch": True,
+    }
+
+
+def _splitmix(x):
+    import numpy as np
+
+    x = (x + np.uint64(0x9E3779B97F4A7C15)).astype(np.uint64)
+    x = ((x ^ (x >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)).astype(np.uint64)
+    x = ((x ^ (x >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)).astype(np.uint64)
+    return x ^ (x >> np.uint64(31))
+
+
+def pool_snapshot(n, n_agents, seed=5, mode="realistic", pinned_frac=1e-4, agent_blocks_per_agent=13):
+    """cfg5 stress snapshot: n resident slots, last_touch = a seeded permutation of
+    [1, n], 0.01% pinned. mode 'realistic': ~13*A slots carry an agent, the rest are agentless
+    history (the measured composition); 'adversarial': 40% of slots carry an agent
+    drawn Zipf(1.1) over A. Keys are a bijection of the slot index (distinct by construction).
+    Returns (keys u64, last_touch u64, agent index u32 / 0xFFFFFFFF, refs u32)."""
+    import numpy as np
+
+    rng = np.random.default_rng(seed)
+    idx = np.arange(n, dtype=np.uint64)
+    keys = _splitmix(idx ^ np.uint64(0x5EED0000 + seed))
+    lt = (rng.permutation(n) + 1).astype(np.uint64)
+    agents = np.full(n, 0xFFFFFFFF, dtype=np.uint32)
+    if mode == "realistic":
+        m = min(n, agent_blocks_per_agent * n_agents)
+        pos = rng.choice(n, size=m, replace=False)
+        agents[pos] = (np.arange(m) % n_agents).astype(np.uint32)
+    else:
+        has = rng.random(n) < 0.4
+        w = 1.0 / np.arange(1, n_agents + 1) ** 1.1
+        w /= w.sum()
+        agents[has] = rng.choice(n_agents, size=int(has.sum()), p=w).astype(np.uint32)
+    refs = (rng.random(n) < pinned_frac).astype(np.uint32)
+    return keys, lt, agents, refs
+
+
 def scaled(spec, **kw):
     s = copy.deepcopy(spec)
     s.update(kw)

@@ -85,7 +85,7 @@ def lib():
         _lib.ref_exact_survival.argtypes = [C.c_ulonglong, C.c_int, C.c_long, C.c_void_p,
                                             C.c_void_p, C.c_ulonglong]
         _lib.ref_evict_bench.restype = C.c_double
-        _lib.ref_evict_bench.argtypes = [C.c_long, C.c_int, C.c_long, C.c_long, C.c_int,
+        _lib.ref_evict_bench.argtypes = [C.c_long, C.c_int, C.c_long, C.c_long, C.c_long, C.c_int,
                                          C.POINTER(C.c_double), C.POINTER(C.c_ulonglong)]
     return _lib
 
@@ -229,10 +229,11 @@ def fnv1a64(keys) -> int:
     return h
 
 
-def evict_bench(N, n_agents, n_agent_blocks, k, cachesage=True):
+def evict_bench(N, n_agents, n_agent_blocks, k, cachesage=True, k_warm=0):
+    """Reference EngineSim at pool N: (seconds per evict_one over k timed evictions, fill s)."""
     fill = C.c_double(0)
     last = C.c_ulonglong(0)
-    s = lib().ref_evict_bench(N, n_agents, n_agent_blocks, k, 1 if cachesage else 0,
+    s = lib().ref_evict_bench(N, n_agents, n_agent_blocks, k_warm, k, 1 if cachesage else 0,
                               C.byref(fill), C.byref(last))
     if s < 0:
         raise RuntimeError(_err())
