@@ -125,6 +125,9 @@ typedef struct cs_pool_stats {
     int64_t resident, pinned, evictions, tombstones, scans, scanned_slots;
     uint64_t rebuilds;
     int n_agents;
+    /* device time per admission-kernel phase summed over launches (globaltimer ns, CTA 0):
+     * probe/observe/lookup, prep+barrier, scan+barrier, select+barrier, replay+apply, epilogue */
+    uint64_t phase_ns[16];
 } cs_pool_stats;
 int cs_pool_get_stats(cs_pool_t pool, cs_pool_stats* out);
 

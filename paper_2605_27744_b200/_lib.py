@@ -35,7 +35,7 @@ class PoolStats(C.Structure):
     _fields_ = [
         ("resident", C.c_int64), ("pinned", C.c_int64), ("evictions", C.c_int64),
         ("tombstones", C.c_int64), ("scans", C.c_int64), ("scanned_slots", C.c_int64),
-        ("rebuilds", C.c_uint64), ("n_agents", C.c_int),
+        ("rebuilds", C.c_uint64), ("n_agents", C.c_int), ("phase_ns", C.c_uint64 * 16),
     ]
 
 

@@ -135,7 +135,9 @@ class Pool:
     def stats(self):
         s = PoolStats()
         check(lib().cs_pool_get_stats(self.h, C.byref(s)))
-        return {f: getattr(s, f) for f, _ in PoolStats._fields_}
+        d = {f: getattr(s, f) for f, _ in PoolStats._fields_}
+        d["phase_ns"] = list(s.phase_ns)
+        return d
 
 
 def hash_prompts(prompts, block_size=16, skip=4, take=4, pool=None):

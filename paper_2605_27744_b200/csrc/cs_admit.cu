@@ -1,0 +1,1255 @@
+// The admission kernel: ONE cooperative launch per EngineSim admission
+// (start_request / execute_warmup / admit, engine.cpp:141-323), paths relative to
+// /root/reference/proj.
+//
+//   phase 0  (CTA 0)  poll reset, K2 probe of the prompt, try_start_head feasibility,
+//                     K3/K3b/K6 observe(AgentDispatch), K2 lookup touches
+//   per chunk of <= 128 prompt blocks:
+//     prep   (CTA 0)  can this chunk evict? reset the per-list bounds
+//     K4 scan (all)   one streaming pass over the SoA pool (16 B per slot): per survival
+//                     class the `keep` oldest unpinned slots + the keep+1 oldest resident
+//     K5a     (CTA l) exact select of list l over all CTAs' survivors, sorted by last_touch
+//     K5b     (CTA 0) exact replay of admit_pinned with evict_one (engine.cpp:102-125) over
+//                     the class heads, then block-table / SoA updates
+//
+// Why per-class heads are exact: inside one survival class the score w_pred*S + rho is a
+// non-decreasing function of last_touch and ties break on last_touch (engine.cpp:111-114), so
+// the class's oldest unpinned block is its best candidate; classes only lose members during an
+// admission (new and reached blocks are pinned at once), at most one per prompt block, so the
+// `keep` oldest per class at the start of a chunk contain every head the chunk needs. The
+// resident-oldest list gives oldest_live_touch (engine.cpp:90-100) the same way. DESIGN.md §4.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "cs_block.cuh"
+#include "cs_launch.h"
+
+namespace csb {
+
+constexpr int kThreads = 512;            // one CTA per SM (cooperative grid)
+constexpr int kV = 4;                    // slots per thread per tile (2 x LDG.128 + 2 x LDG.128)
+constexpr int kTile = kThreads * kV;     // 2048 slots = 32 KiB of SoA per tile
+constexpr int kDepth = 3;                // tiles of loads in flight per thread
+constexpr int kStage = 8192;             // staged candidates per CTA (all lists share it)
+constexpr int kFlushAt = kStage - 2 * kTile;  // a tile appends at most 2 entries per slot
+constexpr int kSide = kMaxLists * (kChunk + 1);
+
+// ------------------------------------------------------------------ shared state
+
+struct ScanSmem {
+    unsigned long long thr[kMaxLists];  // inclusive acceptance bound per list
+    unsigned long long gbw[kMaxLists];
+    int count;                          // staged entries
+    int side_n;
+    int lcnt[kMaxLists];
+    int wcnt[kMaxLists], wbase[kMaxLists], wpos[kMaxLists];
+    unsigned long long flush_ns, flushes;  // instrumentation (reported by CTA 0)
+    unsigned long long hint[kMaxLists];
+    unsigned int rej;
+};
+
+struct AdmSmem {
+    unsigned long long tick;         // engine clock (EngineSim::tick_)
+    unsigned long long first_touch;  // earliest tick admit_pinned touched in this admission
+    long long cached, n_ev_adm, resident, pinned, free_top;
+    int first_miss, admit_n, anchor, chunk, started, error, needed, warm_issued, scans;
+    unsigned long long ph[kPhases], tl;  // phase timestamps (CTA 0, thread 0)
+};
+
+// Dynamic shared memory, phase by phase (the regions alias across phases):
+//   scan    : staging (lt, slot, list) x kStage | side (lt, slot, list) x kSide | cls table
+//   select  : staging holds list l's candidates, side the sorted output
+//   replay  : ReplaySmem
+//   phase 0 : BFS window (pairs + edge flags) and hop table
+struct ScanBufs {
+    unsigned long long* st_lt;
+    unsigned int* st_slot;
+    unsigned char* st_list;
+    unsigned long long* sd_lt;
+    unsigned int* sd_slot;
+    unsigned char* sd_list;
+    unsigned char* cls;
+};
+
+constexpr size_t kOffStSlot = 8ull * kStage;
+constexpr size_t kOffStList = kOffStSlot + 4ull * kStage;
+constexpr size_t kOffSdLt = (kOffStList + kStage + 15) & ~size_t(15);
+constexpr size_t kOffSdSlot = kOffSdLt + 8ull * kSide;
+constexpr size_t kOffSdList = kOffSdSlot + 4ull * kSide;
+constexpr size_t kOffCls = (kOffSdList + kSide + 15) & ~size_t(15);
+
+__device__ __forceinline__ ScanBufs scan_bufs(unsigned char* d) {
+    ScanBufs b;
+    b.st_lt = reinterpret_cast<unsigned long long*>(d);
+    b.st_slot = reinterpret_cast<unsigned int*>(d + kOffStSlot);
+    b.st_list = d + kOffStList;
+    b.sd_lt = reinterpret_cast<unsigned long long*>(d + kOffSdLt);
+    b.sd_slot = reinterpret_cast<unsigned int*>(d + kOffSdSlot);
+    b.sd_list = d + kOffSdList;
+    b.cls = d + kOffCls;
+    return b;
+}
+
+struct ReplaySmem {
+    unsigned long long L_lt[kMaxLists][kChunk + 2];
+    unsigned int L_slot[kMaxLists][kChunk + 2];
+    short L_pidx[kMaxLists][kChunk + 2];  // chunk-relative prompt index of the slot, or -1
+    short L_rpos[kMaxLists][kChunk + 2];  // position in the resident list, or -1
+    int L_n[kMaxLists];
+    unsigned char touched[kChunk];       // prompt block touched+pinned by this chunk
+    unsigned char pevict[kChunk];        // prompt block evicted before it was reached
+    unsigned char rremoved[kChunk + 2];  // resident-list entry evicted
+    unsigned int c_slot[kChunk];
+    unsigned int c_refs0[kChunk];
+    unsigned int out_slot[kChunk];
+    unsigned long long out_lt[kChunk];
+    unsigned char out_new[kChunk];
+    unsigned int victims[kChunk];
+    unsigned int freeslots[kChunk];
+    unsigned int ph_key[512];  // slot -> chunk index hash of the chunk's resident prompt blocks
+    short ph_val[512];
+    unsigned int vh_key[512];  // victim-slot set for fixing up later chunks
+    int n_vict, n_new_global, n_reused;
+    int pdom;  // length of the class-E prefix whose heads beat every other class outright
+    int bulk;  // this chunk was replayed in bulk (no serial loop)
+};
+static_assert(sizeof(ReplaySmem) <= kOffCls, "replay view must fit the scan region");
+
+struct BfsSmem {
+    unsigned short wa[8192];
+    unsigned short wb[8192];
+    unsigned char edge[8192];
+    unsigned char hop[kMaxAgents];
+};
+static_assert(sizeof(BfsSmem) <= kOffCls, "BFS view must fit the scan region");
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+__device__ __forceinline__ void stamp(AdmSmem& A, int k) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        const unsigned long long t = gtimer();
+        A.ph[k] += t - A.tl;
+        A.tl = t;
+    }
+}
+
+// ------------------------------------------------------------------ K3 / K3b / K6
+
+// CacheSagePolicy::observe(AgentDispatch) (cachesage_policy.cpp:57-72). CTA 0, all threads.
+__device__ void observe_dispatch(const DevPool& P, int prev, int next, unsigned long long tick, int n_agents,
+                                 unsigned char* dsm, RedSmem& Red, AdmSmem& A) {
+    Ctrl* C = P.ctrl;
+    const int tid = threadIdx.x, T = blockDim.x;
+    const long long W = P.window;
+    const int Acap = P.a_cap;
+    if (P.policy == 0) return;  // LruPolicy::observe is a no-op (baselines.cpp:10)
+    // K3: TransitionLearner::record (transition_learner.cpp:22-51): one pair per dispatch
+    if (prev >= 0 && tid == 0) {
+        const long long head = C->win_head, size = C->win_size;
+        P.counts[(long long)prev * Acap + next] += 1u;
+        P.totals[prev] += 1u;
+        if (size == W) {
+            const int oa = P.win_a[head], ob = P.win_b[head];
+            P.win_a[head] = prev;
+            P.win_b[head] = next;
+            P.counts[(long long)oa * Acap + ob] -= 1u;
+            P.totals[oa] -= 1u;
+            C->win_head = (head + 1) % W;
+        } else {
+            const long long pos = (head + size) % W;
+            P.win_a[pos] = prev;
+            P.win_b[pos] = next;
+            C->win_size = size + 1;
+        }
+    }
+    __syncthreads();
+    const bool changed = C->cur_agent != next;
+    __syncthreads();
+    if (tid == 0) C->cur_agent = next;
+    if (changed) {
+        // K3b: rebuild_reachability (reachability.cpp:39-81), level-synchronous over the
+        // window's pairs (every positive count cell is a window pair). Edge iff
+        // !(count/total < tau) in fp64; depth d expands only while d + 1 < e_max.
+        const int e = P.e_max;
+        const long long head = C->win_head, size = C->win_size;
+        BfsSmem& B = *reinterpret_cast<BfsSmem*>(dsm);
+        const bool in_smem = size <= 8192;
+        for (int x = tid; x < n_agents; x += T) B.hop[x] = (unsigned char)e;
+        for (long long j = tid; in_smem && j < size; j += T) {
+            const long long q = (head + j) % W;
+            const int a = P.win_a[q], b = P.win_b[q];
+            const double c = (double)P.counts[(long long)a * Acap + b];
+            const double t = (double)P.totals[a];
+            B.wa[j] = (unsigned short)a;
+            B.wb[j] = (unsigned short)b;
+            B.edge[j] = __ddiv_rn(c, t) < P.tau ? 0 : 1;
+        }
+        __syncthreads();
+        if (tid == 0) B.hop[next] = 0;
+        __syncthreads();
+        for (int d = 0; d + 1 < e; ++d) {
+            int any = 0;
+            for (long long j = tid; j < size; j += T) {
+                int a, b, ok;
+                if (in_smem) {
+                    a = B.wa[j];
+                    b = B.wb[j];
+                    ok = B.edge[j];
+                } else {
+                    const long long q = (head + j) % W;
+                    a = P.win_a[q];
+                    b = P.win_b[q];
+                    ok = !(__ddiv_rn((double)P.counts[(long long)a * Acap + b], (double)P.totals[a]) < P.tau);
+                }
+                if (!ok || B.hop[a] != d) continue;
+                if (B.hop[b] > d + 1) {
+                    B.hop[b] = (unsigned char)(d + 1);
+                    any = 1;
+                }
+            }
+            if (!__syncthreads_or(any)) break;
+        }
+        for (int x = tid; x < n_agents; x += T) {
+            P.hop[x] = B.hop[x];
+            P.cls[x] = B.hop[x];
+        }
+        if (tid == 0) {
+            C->rebuilds += 1ull;
+            C->reach_built = 1;
+        }
+        __syncthreads();
+    }
+    // K6: maybe_prefetch (cachesage_policy.cpp:109-123) with argmax_row
+    // (transition_learner.cpp:79-96): max count, ties -> smaller 64-bit AgentId
+    const int budget_ok = C->step_warmups < P.budget_per_step;
+    const unsigned int total = P.totals[next];
+    if (budget_ok && (unsigned long long)total >= P.min_row && total > 0u) {
+        unsigned long long best_c = 0ull, best_id = ~0ull;
+        int best_b = -1;
+        for (int b = tid; b < n_agents; b += T) {
+            const unsigned int c = P.counts[(long long)next * Acap + b];
+            if (c == 0u) continue;
+            const unsigned long long id = P.agent_ids[b];
+            if (best_b < 0 || c > best_c || (c == best_c && id < best_id)) {
+                best_c = c;
+                best_id = id;
+                best_b = b;
+            }
+        }
+        for (int o = 16; o; o >>= 1) {
+            const unsigned long long oc = __shfl_xor_sync(0xffffffffu, best_c, o);
+            const unsigned long long oi = __shfl_xor_sync(0xffffffffu, best_id, o);
+            const int ob = __shfl_xor_sync(0xffffffffu, best_b, o);
+            if (ob >= 0 && (best_b < 0 || oc > best_c || (oc == best_c && oi < best_id))) {
+                best_c = oc;
+                best_id = oi;
+                best_b = ob;
+            }
+        }
+        __syncthreads();
+        if (lane_id() == 0) {
+            Red.u[warp_id()] = best_c;
+            Red.v[warp_id()] = (long long)best_b;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            const int nw = (T + 31) >> 5;
+            best_c = 0;
+            best_b = -1;
+            best_id = ~0ull;
+            for (int w = 0; w < nw; ++w) {
+                const int b = (int)Red.v[w];
+                if (b < 0) continue;
+                const unsigned long long c = Red.u[w], id = P.agent_ids[b];
+                if (best_b < 0 || c > best_c || (c == best_c && id < best_id)) {
+                    best_c = c;
+                    best_id = id;
+                    best_b = b;
+                }
+            }
+            if (best_b >= 0) {
+                const double p = __ddiv_rn((double)best_c, (double)total);
+                if (!(p < P.min_conf)) {
+                    C->step_warmups += 1;
+                    if (C->n_pend < kMaxPending) {
+                        C->pend_target[C->n_pend] = best_b;
+                        C->pend_tick[C->n_pend] = tick;
+                        C->n_pend += 1;
+                    }
+                    A.warm_issued = best_b;
+                }
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// ------------------------------------------------------------------ K4: the pool scan
+
+__device__ __forceinline__ int keep_of(int l, int NL, int keep) { return l == NL - 1 ? keep + 1 : keep; }
+
+// Per list: keep the keep_l smallest staged entries (exact select), tighten the list's bound,
+// publish it grid-wide, and compact the staging pool.
+__device__ void stage_flush(const DevPool& P, int NL, int keep, const ScanBufs& B, ScanSmem& S, SelectSmem& Sel,
+                            bool final_flush) {
+    const int tid = threadIdx.x, T = blockDim.x;
+    const int m = S.count;
+    const unsigned long long t_in = tid == 0 ? gtimer() : 0ull;
+    if (tid < NL) S.lcnt[tid] = 0;
+    __syncthreads();
+    for (int j0 = 0; j0 < m; j0 += T) {  // per-list counts, aggregated per warp (match_any)
+        const int j = j0 + tid;
+        const unsigned int act = __ballot_sync(0xffffffffu, j < m);
+        if (j < m) {
+            const unsigned int tg = B.st_list[j];
+            const unsigned int peers = __match_any_sync(act, tg);
+            if (lane_id() == __ffs(peers) - 1) atomicAdd(&S.lcnt[tg], __popc(peers));
+        }
+    }
+    __syncthreads();
+    for (int l = 0; l < NL; ++l) {
+        const int kl = keep_of(l, NL, keep);
+        if (S.lcnt[l] >= kl && (S.lcnt[l] > kl || final_flush)) {
+            const unsigned long long v = block_kth(B.st_lt, B.st_list, (unsigned char)l, m, kl, Sel);
+            if (tid == 0) {
+                if (v < S.thr[l]) S.thr[l] = v;
+                atomicMin(P.gbound + l, v);
+                if (final_flush) atomicMax(P.gmaxk + l, v);  // next scan's hint
+            }
+        }
+    }
+    if (tid == 0) S.side_n = 0;
+    __syncthreads();
+    for (int j0 = 0; j0 < m; j0 += T) {  // compaction of the survivors, one atomic per warp
+        const int j = j0 + tid;
+        bool keep_it = false;
+        unsigned char l = 0;
+        unsigned long long x = 0;
+        if (j < m) {
+            l = B.st_list[j];
+            x = B.st_lt[j];
+            keep_it = x <= S.thr[l];
+        }
+        const unsigned int ball = __ballot_sync(0xffffffffu, keep_it);
+        int base = 0;
+        if (lane_id() == 0 && ball) base = atomicAdd(&S.side_n, __popc(ball));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (keep_it) {
+            const int p = base + __popc(ball & ((1u << lane_id()) - 1u));
+            B.sd_lt[p] = x;
+            B.sd_slot[p] = B.st_slot[j];
+            B.sd_list[p] = l;
+        }
+    }
+    __syncthreads();
+    const int n2 = S.side_n;
+    for (int j = tid; j < n2; j += T) {
+        B.st_lt[j] = B.sd_lt[j];
+        B.st_slot[j] = B.sd_slot[j];
+        B.st_list[j] = B.sd_list[j];
+    }
+    __syncthreads();
+    if (tid == 0) {
+        S.count = n2;
+        S.flush_ns += gtimer() - t_in;
+        S.flushes += 1;
+    }
+    __syncthreads();
+}
+
+struct Quad {
+    unsigned long long l[kV];
+    unsigned int a[kV], r[kV];
+};
+
+__device__ __forceinline__ void load_quad(const DevPool& P, long long i, long long hi, Quad& q) {
+    if (i + kV <= hi) {
+        const ulonglong2 l01 = __ldcs(reinterpret_cast<const ulonglong2*>(P.lt + i));
+        const ulonglong2 l23 = __ldcs(reinterpret_cast<const ulonglong2*>(P.lt + i + 2));
+        const uint4 aa = __ldcs(reinterpret_cast<const uint4*>(P.agent + i));
+        const uint4 rr = __ldcs(reinterpret_cast<const uint4*>(P.refs + i));
+        q.l[0] = l01.x;
+        q.l[1] = l01.y;
+        q.l[2] = l23.x;
+        q.l[3] = l23.y;
+        q.a[0] = aa.x;
+        q.a[1] = aa.y;
+        q.a[2] = aa.z;
+        q.a[3] = aa.w;
+        q.r[0] = rr.x;
+        q.r[1] = rr.y;
+        q.r[2] = rr.z;
+        q.r[3] = rr.w;
+    } else {
+#pragma unroll
+        for (int k = 0; k < kV; ++k) {
+            if (i + k < hi) {
+                q.l[k] = __ldcs(P.lt + i + k);
+                q.a[k] = __ldcs(P.agent + i + k);
+                q.r[k] = __ldcs(P.refs + i + k);
+            } else {
+                q.l[k] = kFreeTick;
+                q.a[k] = kNoAgent;
+                q.r[k] = 1u;
+            }
+        }
+    }
+}
+
+// One streaming pass over this CTA's contiguous slot range: 16 B per slot read exactly once,
+// kDepth tiles (96 KiB per SM) of 128-bit loads in flight; survivors go to a staging pool that
+// is flushed (exact per-list select) only when it could overflow on the next tile.
+__device__ void scan_pass(const DevPool& P, int NL, int keep, const ScanBufs& B, ScanSmem& S, SelectSmem& Sel) {
+    const int tid = threadIdx.x, T = blockDim.x;
+    const long long TV = (long long)T * kV;
+    long long per = (P.cap + gridDim.x - 1) / gridDim.x;
+    per = (per + kV - 1) / kV * kV;
+    const long long lo = min(P.cap, (long long)blockIdx.x * per);
+    const long long hi = min(P.cap, lo + per);
+    const int R = NL - 1;
+    const int E = P.e_max;  // class of agentless / unreachable blocks (survival 0)
+    const unsigned char* cls = B.cls;
+    if (tid < NL) {
+        // start from the previous scan's hint: no accept-everything warm-up tiles
+        const unsigned long long h = P.ghint[tid];
+        S.hint[tid] = h;
+        S.thr[tid] = min(ld_relaxed_u64(P.gbound + tid), h);
+    }
+    if (tid == 0) {
+        S.count = 0;
+        S.flush_ns = 0;
+        S.flushes = 0;
+        S.rej = 0u;
+    }
+    __syncthreads();
+    volatile unsigned long long* thr = S.thr;
+    const unsigned long long hintR = S.hint[R], hintE = S.hint[E];
+    unsigned int rej = 0u;  // lists with an element above the hint (verified after the select)
+
+    Quad q[kDepth];
+#pragma unroll
+    for (int d = 0; d < kDepth; ++d) load_quad(P, lo + d * TV + (long long)tid * kV, hi, q[d]);
+
+    for (long long base = lo; base < hi; base += kDepth * TV) {
+#pragma unroll
+        for (int d = 0; d < kDepth; ++d) {
+            const long long tb = base + d * TV;
+            if (tb >= hi) break;
+            unsigned long long gbn = ~0ull;
+            if (tid < NL) gbn = ld_relaxed_u64(P.gbound + tid);
+            const unsigned long long thrR = thr[R];
+            const unsigned long long thrE = thr[E];
+            const long long i0 = tb + (long long)tid * kV;
+            // classify the 4 slots: bit k -> resident list, bit 4+k -> class list cl[k]
+            unsigned int acc = 0u;
+            int cl[kV];
+#pragma unroll
+            for (int k = 0; k < kV; ++k) {
+                const unsigned long long x = q[d].l[k];
+                cl[k] = E;
+                if (x == kFreeTick) continue;
+                if (x <= thrR) acc |= 1u << k;
+                if (x > hintR) rej |= 1u << R;
+                if (q[d].r[k] == 0u) {
+                    const unsigned int a = q[d].a[k];
+                    unsigned long long tc = thrE, hc = hintE;
+                    if (a != kNoAgent) {
+                        cl[k] = cls[a];
+                        tc = thr[cl[k]];
+                        hc = S.hint[cl[k]];
+                    }
+                    if (x <= tc) acc |= 1u << (kV + k);
+                    if (x > hc) rej |= 1u << cl[k];
+                }
+            }
+            // warp-aggregated reservation: one shared atomic per warp per tile
+            const int mine = __popc(acc);
+            int incl = mine;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane_id() >= o) incl += t;
+            }
+            const int wtot = __shfl_sync(0xffffffffu, incl, 31);
+            int base = 0;
+            if (lane_id() == 31 && wtot) base = atomicAdd(&S.count, wtot);
+            base = __shfl_sync(0xffffffffu, base, 31);
+            int p = base + incl - mine;
+            const int maxpos = wtot ? base + wtot - 1 : -1;
+            if (acc) {
+#pragma unroll
+                for (int k = 0; k < kV; ++k) {
+                    if (acc & (1u << k)) {
+                        B.st_lt[p] = q[d].l[k];
+                        B.st_slot[p] = (unsigned int)(i0 + k);
+                        B.st_list[p] = (unsigned char)R;
+                        ++p;
+                    }
+                    if (acc & (1u << (kV + k))) {
+                        B.st_lt[p] = q[d].l[k];
+                        B.st_slot[p] = (unsigned int)(i0 + k);
+                        B.st_list[p] = (unsigned char)cl[k];
+                        ++p;
+                    }
+                }
+            }
+            load_quad(P, tb + kDepth * TV + (long long)tid * kV, hi, q[d]);
+            if (tid < NL && gbn < thr[tid]) thr[tid] = gbn;
+            if (__syncthreads_or(maxpos >= kFlushAt)) stage_flush(P, NL, keep, B, S, Sel, false);
+        }
+    }
+    rej = __reduce_or_sync(0xffffffffu, rej);
+    if (lane_id() == 0 && rej) atomicOr(&S.rej, rej);
+    __syncthreads();
+    if (S.count > 0) stage_flush(P, NL, keep, B, S, Sel, true);
+    if (tid == 0 && S.rej) atomicOr(P.grej, S.rej);
+    // publish this CTA's survivors that can still be among the global keep smallest
+    if (tid < NL) {
+        S.gbw[tid] = ld_relaxed_u64(P.gbound + tid);
+        S.wcnt[tid] = 0;
+        S.wpos[tid] = 0;
+    }
+    __syncthreads();
+    const int m = S.count;
+    for (int j = tid; j < m; j += T)
+        if (B.st_lt[j] <= S.gbw[B.st_list[j]]) atomicAdd(&S.wcnt[B.st_list[j]], 1);
+    __syncthreads();
+    if (tid < NL) S.wbase[tid] = S.wcnt[tid] ? atomicAdd(P.gcount + tid, S.wcnt[tid]) : 0;
+    __syncthreads();
+    for (int j = tid; j < m; j += T) {
+        const unsigned char l = B.st_list[j];
+        const unsigned long long x = B.st_lt[j];
+        if (x <= S.gbw[l]) {
+            const long long o = (long long)l * P.gcap + S.wbase[l] + atomicAdd(&S.wpos[l], 1);
+            P.gbuf_lt[o] = x;
+            P.gbuf_slot[o] = B.st_slot[j];
+        }
+    }
+    __syncthreads();
+}
+
+// ------------------------------------------------------------------ K5a: exact per-list select
+
+__device__ void finalize_list(const DevPool& P, int l, int NL, int keep, const ScanBufs& B, SelectSmem& Sel) {
+    const int tid = threadIdx.x, T = blockDim.x;
+    const int kl = keep_of(l, NL, keep);
+    const int m = *(volatile int*)(P.gcount + l);
+    const unsigned long long* g = P.gbuf_lt + (long long)l * P.gcap;
+    const unsigned int* gs = P.gbuf_slot + (long long)l * P.gcap;
+    // stage the candidates on chip when they fit (the common case), else select from L2
+    const bool local = m <= kStage;
+    if (local) {
+        for (int j = tid; j < m; j += T) {
+            B.st_lt[j] = g[j];
+            B.st_slot[j] = gs[j];
+        }
+        __syncthreads();
+    }
+    const unsigned long long* src = local ? B.st_lt : g;
+    const unsigned int* srs = local ? B.st_slot : gs;
+    unsigned long long v = ~0ull;
+    if (m > kl) v = block_kth(src, nullptr, 0, m, kl, Sel);
+    unsigned long long* t_lt = B.sd_lt;
+    unsigned int* t_slot = B.sd_slot;
+    if (tid == 0) Sel.tmp = 0;
+    __syncthreads();
+    for (int j = tid; j < m; j += T) {
+        const unsigned long long x = src[j];
+        if (x <= v) {
+            const int p = atomicAdd(&Sel.tmp, 1);
+            t_lt[p] = x;
+            t_slot[p] = srs[j];
+        }
+    }
+    __syncthreads();
+    const int n = Sel.tmp;
+    for (int j = tid; j < 256; j += T)
+        if (j >= n) {
+            t_lt[j] = ~0ull;
+            t_slot[j] = kNoSlot;
+        }
+    __syncthreads();
+    for (int k = 2; k <= 256; k <<= 1) {
+        for (int jj = k >> 1; jj > 0; jj >>= 1) {
+            for (int i = tid; i < 256; i += T) {
+                const int ixj = i ^ jj;
+                if (ixj > i) {
+                    const bool asc = (i & k) == 0;
+                    const unsigned long long a = t_lt[i], b = t_lt[ixj];
+                    if ((a > b) == asc) {
+                        t_lt[i] = b;
+                        t_lt[ixj] = a;
+                        const unsigned int sa = t_slot[i];
+                        t_slot[i] = t_slot[ixj];
+                        t_slot[ixj] = sa;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (int j = tid; j < n; j += T) {
+        P.fin_lt[(long long)l * (kChunk + 2) + j] = t_lt[j];
+        P.fin_slot[(long long)l * (kChunk + 2) + j] = t_slot[j];
+    }
+    if (tid == 0) {
+        P.fin_n[l] = n;
+        // Hint verification: a list that came up short while some member was rejected only by
+        // its hint may be missing candidates -> the whole pass is redone without hints.
+        const bool hinted = P.ghint[l] != ~0ull;
+        const unsigned int rej = *(volatile unsigned int*)P.grej;
+        if (n < kl && hinted && ((rej >> l) & 1u)) atomicExch(&P.ctrl->rescan, 1);
+        const unsigned long long mk = *(volatile unsigned long long*)(P.gmaxk + l);
+        P.ghint[l] = mk ? mk : ~0ull;
+    }
+    __syncthreads();
+}
+
+// ------------------------------------------------------------------ K5b: replay + apply
+
+__device__ __forceinline__ unsigned int hslot(unsigned int s) { return (s * 2654435761u) >> 23; }  // 9 bits
+
+// Exact replay of admit_pinned over prompt blocks [lo, hi) (engine.cpp:141-168). Each
+// eviction is evict_one (engine.cpp:102-125): the argmin of (score, last_touch) over the class
+// heads; oldest_live_touch (engine.cpp:90-100) = min(tick, resident-list head, earliest touch
+// of this admission). One warp; lane l owns list l.
+__device__ void replay_apply(const DevPool& P, const AdmitArgs& a, ReplaySmem& R, AdmSmem& A, int NL, bool scanned,
+                             RedSmem& Red) {
+    Ctrl* C = P.ctrl;
+    const int tid = threadIdx.x, T = blockDim.x;
+    const int lo = A.chunk * kChunk;
+    const int hi = min(A.admit_n, lo + kChunk);
+    const int len = hi - lo;
+    const int Rl = NL - 1;
+
+    // ---- setup (all threads)
+    for (int j = tid; j < 512; j += T) {
+        R.ph_key[j] = kNoSlot;
+        R.vh_key[j] = kNoSlot;
+    }
+    for (int i = tid; i < len; i += T) {
+        R.c_slot[i] = P.p_slot[lo + i];
+        R.c_refs0[i] = P.p_refs0[lo + i];
+        R.touched[i] = 0;
+        R.pevict[i] = 0;
+    }
+    for (int j = tid; j < kChunk + 2; j += T) R.rremoved[j] = 0;
+    const long long ftop = C->free_top;
+    for (int j = tid; j < len && j < ftop; j += T) R.freeslots[j] = P.free_stack[ftop - 1 - j];
+    if (tid == 0) {
+        R.n_vict = 0;
+        R.n_new_global = 0;
+        R.n_reused = 0;
+    }
+    for (int l = 0; l < NL; ++l) {
+        const int n = scanned ? P.fin_n[l] : 0;
+        for (int j = tid; j < n; j += T) {
+            R.L_lt[l][j] = P.fin_lt[(long long)l * (kChunk + 2) + j];
+            R.L_slot[l][j] = P.fin_slot[(long long)l * (kChunk + 2) + j];
+        }
+        if (tid == 0) R.L_n[l] = n;
+    }
+    __syncthreads();
+    // slot -> prompt index of this chunk's resident blocks
+    for (int i = tid; i < len; i += T) {
+        const unsigned int s = R.c_slot[i];
+        if (s == kNoSlot) continue;
+        unsigned int h = hslot(s);
+        for (int n = 0; n < 512; ++n) {
+            const unsigned int old = atomicCAS(&R.ph_key[h], kNoSlot, s);
+            if (old == kNoSlot || old == s) {
+                R.ph_val[h] = (short)i;
+                break;
+            }
+            h = (h + 1) & 511u;
+        }
+    }
+    __syncthreads();
+    // per list entry: prompt index (touch removes it) and resident-list position (eviction
+    // from a class list also removes it from the resident list)
+    const int nres = R.L_n[Rl];
+    for (int l = 0; l < NL; ++l) {
+        const int n = R.L_n[l];
+        for (int j = tid; j < n; j += T) {
+            const unsigned int s = R.L_slot[l][j];
+            short pi = -1;
+            unsigned int h = hslot(s);
+            for (int c = 0; c < 512; ++c) {
+                const unsigned int k = R.ph_key[h];
+                if (k == kNoSlot) break;
+                if (k == s) {
+                    pi = R.ph_val[h];
+                    break;
+                }
+                h = (h + 1) & 511u;
+            }
+            R.L_pidx[l][j] = pi;
+            short rp = -1;
+            if (l == Rl) {
+                rp = (short)j;
+            } else {
+                const unsigned long long x = R.L_lt[l][j];
+                int lo2 = 0, hi2 = nres;  // binary search by the unique last_touch
+                while (lo2 < hi2) {
+                    const int mid = (lo2 + hi2) >> 1;
+                    if (R.L_lt[Rl][mid] < x) lo2 = mid + 1;
+                    else hi2 = mid;
+                }
+                if (lo2 < nres && R.L_lt[Rl][lo2] == x) rp = (short)lo2;
+            }
+            R.L_rpos[l][j] = rp;
+        }
+    }
+    __syncthreads();
+    // Dominance prefix. Within an admission `now` only grows and oldest_live_touch never
+    // decreases, so rho(lt) of a fixed block only shrinks (exact ratio shrinks, rounding is
+    // monotone). A class-E (survival 0, score = rho) entry whose rho at the replay-start context
+    // is < min over the other non-empty classes of w_pred*S_c therefore beats every other class
+    // head at every later eviction of this chunk: score_c >= fl(w_pred*S_c) > rho_E. Since rho
+    // grows with lt along the sorted list, those entries form a prefix.
+    {
+        const int E = P.e_max;
+        double bound = __longlong_as_double(0x7ff0000000000000ll);  // +inf: no other class
+        bool ok = true;
+        if (P.policy == 1) {
+            if (!(P.w_pred > 0.0)) ok = false;
+            for (int c = 0; c < E; ++c)
+                if (R.L_n[c] > 0) bound = fmin(bound, __dmul_rn(P.w_pred, survival_of_class(c, E)));
+        }
+        const unsigned long long tick0 = A.tick;
+        unsigned long long old0 = tick0;
+        if (R.L_n[Rl] > 0 && R.L_lt[Rl][0] < old0) old0 = R.L_lt[Rl][0];
+        if (A.first_touch < old0) old0 = A.first_touch;
+        const int nE = R.L_n[E];
+        long long first_fail = ok ? nE : 0;
+        for (int j = tid; ok && j < nE; j += T) {
+            const double rho = recency(R.L_lt[E][j], tick0, old0);
+            if (!(rho < bound)) first_fail = min(first_fail, (long long)j);
+        }
+        first_fail = block_min(first_fail, Red);
+        if (tid == 0) R.pdom = (int)first_fail;
+    }
+    __syncthreads();
+    // Bulk replay (the common case, no serial loop): when the victims are the first n_ev
+    // class-E candidates, all inside the dominance prefix and none of them a prompt block of
+    // this chunk, the sequential replay reduces to: absent block of rank r takes a free slot
+    // while the pool is below budget, else the next class-E candidate; every block is touched
+    // once in prompt order (tick0 + 1 + i).
+    {
+        const int E = P.e_max;
+        const long long res0 = C->resident;
+        int absent = 0, pre_unpinned = 0;
+        for (int i = tid; i < len; i += T) {
+            if (R.c_slot[i] == kNoSlot) ++absent;
+            else if (R.c_refs0[i] == 0u) ++pre_unpinned;
+        }
+        absent = (int)block_sum(absent, Red);
+        pre_unpinned = (int)block_sum(pre_unpinned, Red);
+        const long long room = P.cap - res0;
+        const int n_free = (int)min((long long)absent, room > 0 ? room : 0ll);
+        const int n_ev = absent - n_free;
+        int clash = 0;  // a needed victim is one of this chunk's prompt blocks
+        for (int j = tid; j < n_ev && j < R.L_n[E]; j += T) clash |= R.L_pidx[E][j] >= 0;
+        clash = __syncthreads_or(clash);
+        const bool bulk = n_ev <= R.pdom && !clash;
+        if (bulk) {
+            // exclusive rank of each absent block (len <= kChunk = 128: 4 warps)
+            __shared__ int wsum[kChunk / 32];
+            int rank = 0;
+            if (tid < kChunk) {
+                const bool ab = tid < len && R.c_slot[tid] == kNoSlot;
+                const unsigned int ball = __ballot_sync(0xffffffffu, ab);
+                if (lane_id() == 0) wsum[warp_id()] = __popc(ball);
+                rank = __popc(ball & ((1u << lane_id()) - 1u));
+            }
+            __syncthreads();
+            if (tid < len) {
+                for (int w = 0; w < warp_id(); ++w) rank += wsum[w];
+                const unsigned long long t = A.tick + 1 + (unsigned long long)tid;
+                const unsigned int s = R.c_slot[tid];
+                R.out_lt[tid] = t;
+                if (s != kNoSlot) {
+                    R.out_slot[tid] = s;
+                    R.out_new[tid] = 0;
+                } else {
+                    R.out_slot[tid] = rank < n_free ? R.freeslots[rank] : R.L_slot[E][rank - n_free];
+                    R.out_new[tid] = 1;
+                }
+            }
+            for (int k = tid; k < n_ev; k += T) R.victims[k] = R.L_slot[E][k];
+            __syncthreads();
+            if (tid == 0) {
+                if (len > 0 && A.first_touch == ~0ull) A.first_touch = A.tick + 1;
+                A.tick += (unsigned long long)len;
+                A.resident = res0 + absent - n_ev;
+                A.pinned = C->pinned + pre_unpinned + absent;
+                R.n_vict = n_ev;
+                R.n_reused = n_ev;
+                R.n_new_global = n_free;
+                A.ph[11] += (unsigned long long)n_ev;
+                A.ph[12] += (unsigned long long)n_ev;
+                A.ph[14] += 1;  // bulk chunks
+            }
+        }
+        if (tid == 0) R.bulk = bulk ? 1 : 0;
+        __syncthreads();
+    }
+    stamp(A, 6);
+
+    // ---- the sequential replay (warp 0)
+    if (warp_id() == 0 && !R.bulk) {
+        const int lane = lane_id();
+        int cursor = 0;
+        const int my_n = lane < NL ? R.L_n[lane] : 0;
+        const double my_surv = survival_of_class(lane, P.e_max);
+        unsigned long long tick = A.tick;
+        unsigned long long first_touch = A.first_touch;
+        long long resident = C->resident;
+        long long pinned = C->pinned;
+        int nv = 0, nre = 0, nglob = 0;
+        int error = 0;
+        const int E = P.e_max;      // agentless / unreachable class (survival 0)
+        const int pdom = R.pdom;    // class-E heads below this index win outright
+        long long fast = 0;
+        for (int i = 0; i < len; ++i) {
+            const unsigned int s = R.c_slot[i];
+            if (s != kNoSlot && !R.pevict[i]) {  // resident: touch + pin
+                ++tick;
+                if (lane == 0) {
+                    R.out_slot[i] = s;
+                    R.out_lt[i] = tick;
+                    R.out_new[i] = 0;
+                    R.touched[i] = 1;
+                }
+                if (R.c_refs0[i] == 0u) ++pinned;
+                if (first_touch == ~0ull) first_touch = tick;
+                __syncwarp();
+                continue;
+            }
+            while (resident >= P.cap) {
+                // fast path: the class-E head is inside the dominated prefix (see pdom)
+                if (lane == E) {
+                    while (cursor < my_n) {
+                        const short pi = R.L_pidx[E][cursor];
+                        if (!(pi >= 0 && R.touched[pi])) break;
+                        ++cursor;
+                    }
+                }
+                const int ecur = __shfl_sync(0xffffffffu, cursor, E);
+                if (ecur < pdom) {
+                    if (lane == E) {
+                        const short pi = R.L_pidx[E][cursor];
+                        const short rp = R.L_rpos[E][cursor];
+                        if (pi >= 0) R.pevict[pi] = 1;
+                        if (rp >= 0) R.rremoved[rp] = 1;
+                        R.victims[nv] = R.L_slot[E][cursor];
+                        ++cursor;
+                    }
+                    ++nv;
+                    --resident;
+                    ++fast;
+                    __syncwarp();
+                    continue;
+                }
+                if (lane < NL) {  // skip entries touched (pinned) or evicted via another list
+                    while (cursor < my_n) {
+                        const short pi = R.L_pidx[lane][cursor];
+                        const bool gone = (pi >= 0 && R.touched[pi]) || (lane == Rl && R.rremoved[cursor]);
+                        if (!gone) break;
+                        ++cursor;
+                    }
+                }
+                const unsigned long long rhead =
+                    __shfl_sync(0xffffffffu, (lane == Rl && cursor < my_n) ? R.L_lt[Rl][cursor] : ~0ull, Rl);
+                unsigned long long old = tick;
+                if (rhead < old) old = rhead;
+                if (first_touch < old) old = first_touch;
+                // (score, last_touch) as two 64-bit keys; non-negative doubles order like their bits
+                unsigned long long sk = ~0ull, lk = ~0ull;
+                if (lane < Rl && cursor < my_n) {
+                    lk = R.L_lt[lane][cursor];
+                    sk = (unsigned long long)__double_as_longlong(score_of(P.policy, P.w_pred, my_surv, lk, tick, old));
+                }
+                const unsigned int m1 = __reduce_min_sync(0xffffffffu, (unsigned int)(sk >> 32));
+                if (m1 == 0xffffffffu) {
+                    error = 1;  // evict_one: all resident blocks are pinned
+                    break;
+                }
+                bool c = (unsigned int)(sk >> 32) == m1;
+                const unsigned int m2 = __reduce_min_sync(0xffffffffu, c ? (unsigned int)sk : 0xffffffffu);
+                c = c && (unsigned int)sk == m2;
+                unsigned int ball = __ballot_sync(0xffffffffu, c);
+                if (__popc(ball) > 1) {  // equal scores: the older block wins (engine.cpp:111-114)
+                    const unsigned int m3 = __reduce_min_sync(0xffffffffu, c ? (unsigned int)(lk >> 32) : 0xffffffffu);
+                    c = c && (unsigned int)(lk >> 32) == m3;
+                    const unsigned int m4 = __reduce_min_sync(0xffffffffu, c ? (unsigned int)lk : 0xffffffffu);
+                    c = c && (unsigned int)lk == m4;
+                    ball = __ballot_sync(0xffffffffu, c);
+                }
+                const int w = __ffs(ball) - 1;
+                if (lane == w) {
+                    const unsigned int v = R.L_slot[lane][cursor];
+                    const short pi = R.L_pidx[lane][cursor];
+                    const short rp = R.L_rpos[lane][cursor];
+                    if (pi >= 0) R.pevict[pi] = 1;  // reached later in this chunk: absent then
+                    if (rp >= 0) R.rremoved[rp] = 1;
+                    R.victims[nv] = v;
+                    ++cursor;
+                }
+                ++nv;
+                --resident;
+                __syncwarp();
+            }
+            if (error) break;
+            // allocate: this chunk's victims first, then the free stack
+            unsigned int ns;
+            if (nre < nv) {
+                ns = R.victims[nre++];
+            } else {
+                ns = R.freeslots[nglob++];
+            }
+            ++tick;
+            if (lane == 0) {
+                R.out_slot[i] = ns;
+                R.out_lt[i] = tick;
+                R.out_new[i] = 1;
+            }
+            ++resident;
+            ++pinned;
+            if (first_touch == ~0ull) first_touch = tick;
+            __syncwarp();
+        }
+        if (lane == 0) {
+            A.tick = tick;
+            A.first_touch = first_touch;
+            A.resident = resident;
+            A.pinned = pinned;
+            R.n_vict = nv;
+            R.n_reused = nre;
+            R.n_new_global = nglob;
+            if (error) A.error = 1;
+            A.ph[11] += (unsigned long long)fast;  // instrumentation: evictions on the fast path
+            A.ph[12] += (unsigned long long)nv;
+        }
+    }
+    __syncthreads();
+    stamp(A, 7);
+    const bool err = A.error != 0;
+    const int nv = R.n_vict;
+    // ---- apply: victims first (erase key, free slot), then inserts and touches
+    const unsigned long long ev0 = C->n_ev;
+    for (int k = tid; k < nv; k += T) {
+        const unsigned int v = R.victims[k];
+        const unsigned long long kk = P.key[v];
+        table_erase(P, kk);
+        P.evlog[(ev0 + k) % (unsigned long long)P.evlog_cap] = kk;  // ring; the host drains it
+        P.lt[v] = kFreeTick;
+        P.refs[v] = 0u;
+        P.agent[v] = kNoAgent;
+        unsigned int h = hslot(v);
+        for (int c = 0; c < 512; ++c) {
+            if (atomicCAS(&R.vh_key[h], kNoSlot, v) == kNoSlot) break;
+            h = (h + 1) & 511u;
+        }
+    }
+    __syncthreads();
+    long long reused_tomb = 0;
+    const int done_len = err ? 0 : len;  // an erroring chunk is not applied
+    for (int i = tid; i < done_len; i += T) {
+        const unsigned int s = R.out_slot[i];
+        if (R.out_new[i]) {
+            const int gi = lo + i;
+            P.key[s] = a.keys[gi];
+            P.tokens[s] = a.counts[gi];
+            P.agent[s] = (a.agent != kNoAgent && gi < A.anchor) ? a.agent : kNoAgent;
+            P.lt[s] = R.out_lt[i];
+            P.refs[s] = 1u;
+            reused_tomb += table_insert(P, a.keys[gi], s);
+        } else {
+            P.lt[s] = R.out_lt[i];
+            atomicAdd(&P.refs[s], 1u);
+        }
+        P.p_slot[lo + i] = s;
+    }
+    // blocks of later chunks evicted here are absent when reached
+    if (nv > 0) {
+        for (int j = hi + tid; j < A.admit_n; j += T) {
+            const unsigned int s = P.p_slot[j];
+            if (s == kNoSlot) continue;
+            unsigned int h = hslot(s);
+            for (int c = 0; c < 512; ++c) {
+                const unsigned int k = R.vh_key[h];
+                if (k == kNoSlot) break;
+                if (k == s) {
+                    P.p_slot[j] = kNoSlot;
+                    break;
+                }
+                h = (h + 1) & 511u;
+            }
+        }
+    }
+    reused_tomb = block_sum(reused_tomb, Red);
+    if (tid == 0) {
+        long long top = ftop - R.n_new_global;
+        for (int k = R.n_reused; k < nv; ++k) P.free_stack[top++] = R.victims[k];
+        C->resident = A.resident;
+        C->pinned = A.pinned;
+        C->free_top = top;
+        C->n_ev = ev0 + nv;
+        C->tombstones += (long long)nv - reused_tomb;
+        A.n_ev_adm += nv;
+    }
+    __syncthreads();
+    stamp(A, 8);
+}
+
+// ------------------------------------------------------------------ the admission kernel
+
+__device__ void write_status(const DevPool& P, const AdmitArgs& a, const AdmSmem& A) {
+    Ctrl* C = P.ctrl;
+    AdmitStatus* st = a.status;
+    st->started = A.started;
+    st->error = A.error;
+    st->first_miss = A.first_miss;
+    st->admit_n = A.admit_n;
+    st->cached = A.cached;
+    st->n_evicted = A.n_ev_adm;
+    st->resident = C->resident;
+    st->pinned = C->pinned;
+    st->tick_after = A.tick;
+    st->ev_total = C->n_ev;
+    st->warm_issued = A.warm_issued;
+    st->needed = A.needed;
+    st->scans = A.scans;
+    st->tombstones = C->tombstones;
+    for (int k = 0; k < kPhases; ++k) st->phase_ns[k] = A.ph[k];
+    st->n_pend = C->n_pend;
+    for (int k = 0; k < C->n_pend && k < kMaxPending; ++k) {
+        st->pend_target[k] = C->pend_target[k];
+        st->pend_tick[k] = C->pend_tick[k];
+    }
+    __threadfence_system();
+}
+
+__global__ void __launch_bounds__(kThreads, 1) admit_kernel(DevPool P, AdmitArgs a) {
+    extern __shared__ __align__(16) unsigned char dsm[];
+    __shared__ ScanSmem S;
+    __shared__ SelectSmem Sel;
+    __shared__ RedSmem Red;
+    __shared__ AdmSmem A;
+    Ctrl* C = P.ctrl;
+    const int tid = threadIdx.x, T = blockDim.x;
+    const int NL = P.n_lists;
+    const ScanBufs B = scan_bufs(dsm);
+    ReplaySmem& Rp = *reinterpret_cast<ReplaySmem*>(dsm);
+
+    // ---- phase 0 (CTA 0): poll reset, probe, feasibility, dispatch, lookup
+    if (blockIdx.x == 0) {
+        if (tid == 0) {
+            A.started = 1;
+            A.error = 0;
+            A.cached = 0;
+            A.n_ev_adm = 0;
+            A.first_miss = 0;
+            A.admit_n = 0;
+            A.chunk = 0;
+            A.needed = 0;
+            A.warm_issued = -1;
+            A.scans = 0;
+            A.first_touch = ~0ull;
+            A.tick = a.tick_base;
+            for (int k = 0; k < kPhases; ++k) A.ph[k] = 0;
+            A.tl = gtimer();
+            C->done = 0;
+            C->error = 0;
+            if (a.flags & kPollReset) {
+                C->step_warmups = 0;
+                C->n_pend = 0;
+            }
+        }
+        __syncthreads();
+        const int n = a.n;
+        long long miss_min = n, need = 0;
+        for (int i = tid; i < n; i += T) {
+            const unsigned int s = table_find(P, a.keys[i]);
+            const unsigned int r0 = s == kNoSlot ? 0u : P.refs[s];
+            P.p_slot[i] = s;
+            P.p_refs0[i] = r0;
+            if (s == kNoSlot && i < miss_min) miss_min = i;
+            if (s == kNoSlot || r0 == 0u) ++need;
+        }
+        need = block_sum(need, Red);
+        miss_min = block_min(miss_min, Red);
+        if (tid == 0) A.needed = (int)need;
+        if ((a.flags & kFeasible) && C->pinned + need > P.cap) {
+            if (tid == 0) A.started = 0;  // try_start_head: wait for in-flight pins to clear
+        }
+        __syncthreads();
+        if (A.started) {
+            if (a.flags & kDispatch) {
+                if (tid == 0) A.tick = A.tick + 1;
+                __syncthreads();
+                observe_dispatch(P, a.prev, a.next, A.tick, a.n_agents, dsm, Red, A);
+            }
+            if (a.flags & kLookup) {
+                const int f = (int)miss_min;
+                long long cached = 0;
+                for (int i = tid; i < f; i += T) {
+                    cached += a.counts[i];
+                    P.lt[P.p_slot[i]] = A.tick + 1 + (unsigned long long)i;  // EngineSim::touch
+                }
+                cached = block_sum(cached, Red);
+                if (tid == 0) {
+                    A.first_miss = f;
+                    A.cached = cached;
+                    A.tick += (unsigned long long)f;
+                }
+            }
+            if (tid == 0) {
+                int an = (a.flags & kAdmit) ? n : 0;
+                const long long room = P.cap - C->pinned;
+                if (a.flags & kTruncate) an = (int)room;
+                if (a.flags & kWarmupRoom) an = (int)min((long long)n, room);
+                A.admit_n = an;
+                A.anchor = a.anchor < 0 ? an : a.anchor;
+            }
+        }
+        __syncthreads();
+        stamp(A, 0);
+    }
+
+    // ---- chunk loop: prep (CTA 0) | scan (all) | select (one CTA per list) | replay (CTA 0)
+    for (;;) {
+        if (blockIdx.x == 0) {
+            const bool stop = !A.started || A.error || A.chunk * kChunk >= A.admit_n;
+            if (stop) {
+                if (tid == 0) C->done = 1;
+            } else {
+                const int lo = A.chunk * kChunk, hi = min(A.admit_n, lo + kChunk);
+                long long absent = 0;
+                for (int j = lo + tid; j < hi; j += T) absent += P.p_slot[j] == kNoSlot ? 1 : 0;
+                absent = block_sum(absent, Red);
+                const int need_scan = C->resident + absent > P.cap ? 1 : 0;
+                if (tid < NL && need_scan) {
+                    P.gbound[tid] = ~0ull;
+                    P.gcount[tid] = 0;
+                    P.gmaxk[tid] = 0ull;
+                }
+                if (tid == 0) {
+                    *P.grej = 0u;
+                    C->rescan = 0;
+                    C->need_scan = need_scan;
+                    C->keep = hi - lo;
+                    if (need_scan) {
+                        A.scans += 1;
+                        C->scans += 1;
+                        C->scanned_slots += P.cap;
+                    }
+                }
+            }
+            __threadfence();
+        }
+        grid_barrier(C);
+        stamp(A, 1);
+        if (*(volatile int*)&C->done) break;
+        const int need_scan = *(volatile int*)&C->need_scan;
+        const int keep = *(volatile int*)&C->keep;
+        if (need_scan) {
+            for (int x = tid; x < a.n_agents; x += T) B.cls[x] = P.cls[x];
+            __syncthreads();
+            for (int pass = 0; pass < 2; ++pass) {
+                scan_pass(P, NL, keep, B, S, Sel);
+                if (blockIdx.x == 0 && tid == 0) {
+                    A.ph[9] += S.flush_ns;
+                    A.ph[10] += S.flushes;
+                }
+                grid_barrier(C);
+                stamp(A, 2);
+                for (int l = blockIdx.x; l < NL; l += gridDim.x) finalize_list(P, l, NL, keep, B, Sel);
+                grid_barrier(C);
+                stamp(A, 3);
+                // C->rescan is only cleared by the next chunk's prep, after every CTA read it
+                if (pass == 1 || !*(volatile int*)&C->rescan) break;
+                // a hint was too tight for some list: redo the pass with no hints (exact)
+                if (blockIdx.x == 0) {
+                    if (tid < NL) {
+                        P.ghint[tid] = ~0ull;
+                        P.gbound[tid] = ~0ull;
+                        P.gcount[tid] = 0;
+                        P.gmaxk[tid] = 0ull;
+                    }
+                    if (tid == 0) {
+                        *P.grej = 0u;
+                        C->rescans += 1;
+                        A.ph[13] += 1;
+                    }
+                    __threadfence();
+                }
+                grid_barrier(C);
+            }
+        }
+        if (blockIdx.x == 0) {
+            replay_apply(P, a, Rp, A, NL, need_scan != 0, Red);
+            if (tid == 0) A.chunk += 1;
+            __syncthreads();
+            stamp(A, 4);
+        }
+    }
+
+    // ---- epilogue (CTA 0): EngineSim::admit unpins at once; pins out; status
+    if (blockIdx.x == 0) {
+        if (A.started && !A.error) {
+            long long dec = 0;
+            for (int i = tid; i < A.admit_n; i += T) {
+                const unsigned int s = P.p_slot[i];
+                if (a.pins_out) a.pins_out[i] = s;
+                if (a.flags & kUnpinAfter) {
+                    if (atomicSub(&P.refs[s], 1u) == 1u) ++dec;
+                }
+            }
+            dec = block_sum(dec, Red);
+            if (tid == 0) C->pinned -= dec;
+        }
+        __syncthreads();
+        stamp(A, 5);
+        if (tid == 0) write_status(P, a, A);
+    }
+}
+
+// ------------------------------------------------------------------ host side
+
+LaunchCfg admit_launch_config(const DevPool& P, int device, int want_grid) {
+    LaunchCfg lc{0, 0, 0, 0};
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return lc;
+    const size_t smem = kOffCls + (size_t)((P.a_cap + 15) & ~15);
+    if (smem + sizeof(ScanSmem) + sizeof(SelectSmem) + sizeof(RedSmem) + sizeof(AdmSmem) > prop.sharedMemPerBlockOptin)
+        return lc;
+    if (cudaFuncSetAttribute(admit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return lc;
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, admit_kernel, kThreads, smem) != cudaSuccess || occ < 1)
+        return lc;
+    int grid = prop.multiProcessorCount * occ;
+    if (want_grid > 0 && want_grid < grid) grid = want_grid;
+    lc.grid = grid;
+    lc.threads = kThreads;
+    lc.cap_per_list = 0;
+    lc.smem = smem;
+    return lc;
+}
+
+cudaError_t launch_admit(const DevPool& P, const AdmitArgs& a, const LaunchCfg& lc, int grid, cudaStream_t s) {
+    DevPool p = P;
+    AdmitArgs aa = a;
+    void* args[] = {&p, &aa};
+    if (grid <= 1) return cudaLaunchKernel((const void*)admit_kernel, dim3(1), dim3(lc.threads), args, lc.smem, s);
+    return cudaLaunchCooperativeKernel((const void*)admit_kernel, dim3(grid), dim3(lc.threads), args, lc.smem, s);
+}
+
+}  // namespace csb

@@ -20,7 +20,7 @@ constexpr int kChunk = 128;          // prompt blocks replayed per scan pass (ca
 constexpr int kSlack = 128;          // staged candidates tolerated before a CTA trims
 constexpr int kMaxAgents = 4096;     // dense A x A learner counts
 constexpr int kMaxPending = 64;      // queued warmups between drains
-constexpr int kScanThreads = 1024;   // one CTA per SM, 32 warps
+constexpr int kPhases = 16;          // per-phase device timers reported with each admission
 
 // hashing.hpp:13-14 + the identity seed of cachesage_policy.cpp:26
 constexpr unsigned long long kHashSeed = 0x5ca9e5a6e0f1c3b7ull;
@@ -70,6 +70,8 @@ struct Ctrl {
     int keep;
     int chunk_lo, chunk_hi;
     int error;
+    int rescan;        // a hinted list came up short: scan again without hints
+    long long rescans; // instrumentation
 };
 
 struct DevPool {
@@ -107,6 +109,9 @@ struct DevPool {
     // scan scratch
     unsigned long long* gbound;   // [kMaxLists] running upper bound of each list's keep-th value
     int* gcount;                  // [kMaxLists]
+    unsigned long long* ghint;    // [kMaxLists] acceptance hint carried to the next scan (~0 = none)
+    unsigned long long* gmaxk;    // [kMaxLists] max over CTAs of their local keep-th value
+    unsigned int* grej;           // bit l: some element of list l was rejected only by its hint
     unsigned long long* gbuf_lt;  // [kMaxLists][gcap]
     unsigned int* gbuf_slot;
     long long gcap;
@@ -187,6 +192,7 @@ __device__ __forceinline__ void table_erase(const DevPool& P, unsigned long long
 // recency_residual (runtime.cpp:23-32), no contraction.
 __device__ __forceinline__ double recency(unsigned long long lt, unsigned long long now, unsigned long long old) {
     if (now <= old) return 1.0;
+    if (lt <= old) return 0.0;  // offset 0 -> 0/span = +0.0 exactly (skips the fp64 divide)
     const double span = (double)(now - old);
     const double off = lt >= old ? (double)(lt - old) : 0.0;
     double r = __ddiv_rn(off, span);
@@ -238,8 +244,8 @@ __device__ __forceinline__ void grid_barrier(Ctrl* c) {
             // CTA that died) traps after ~10 s instead of hanging the device
             unsigned long long spins = 0;
             while (ld_acquire(&c->bar_gen) == gen) {
-                __nanosleep(64);
-                if (++spins > (1ull << 27)) __trap();
+                if (++spins > 4096) __nanosleep(64);  // hot spin first: barriers are short
+                if (spins > (1ull << 27)) __trap();
             }
         }
         __threadfence();

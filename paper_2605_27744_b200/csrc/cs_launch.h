@@ -34,6 +34,11 @@ struct AdmitStatus {
     int scans;
     int needed;
     long long tombstones;
+    // CTA-0 view of the phase boundaries (%globaltimer ns), summed over chunks:
+    // [0] phase 0 (probe/dispatch/lookup)  [1] prep + barrier  [2] scan + barrier
+    // [3] finalize + barrier  [4] replay + apply  [5] epilogue
+    // [6] replay setup [7] replay loop [8] apply [9] scan flushes (CTA 0) [10] flush count
+    unsigned long long phase_ns[kPhases];
     int pend_target[kMaxPending];
     unsigned long long pend_tick[kMaxPending];
 };

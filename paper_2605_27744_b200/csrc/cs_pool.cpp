@@ -102,6 +102,10 @@ void cs_pool::create(const cs_pool_cfg& c) {
     ck(cudaMemsetAsync(p.ctrl, 0, sizeof(csb::Ctrl), stream), "memset");
     p.gbound = dmalloc<unsigned long long>(csb::kMaxLists, "gbound");
     p.gcount = dmalloc<int>(csb::kMaxLists, "gcount");
+    p.ghint = dmalloc<unsigned long long>(csb::kMaxLists, "ghint");
+    p.gmaxk = dmalloc<unsigned long long>(csb::kMaxLists, "gmaxk");
+    p.grej = dmalloc<unsigned int>(1, "grej");
+    ck(cudaMemsetAsync(p.ghint, 0xff, sizeof(unsigned long long) * csb::kMaxLists, stream), "memset");
     p.fin_lt = dmalloc<unsigned long long>((size_t)csb::kMaxLists * (csb::kChunk + 2), "fin_lt");
     p.fin_slot = dmalloc<unsigned int>((size_t)csb::kMaxLists * (csb::kChunk + 2), "fin_slot");
     p.fin_n = dmalloc<int>(csb::kMaxLists, "fin_n");
@@ -127,7 +131,7 @@ void cs_pool::destroy() {
     csb::DevPool& p = P;
     void* ptrs[] = {p.lt, p.agent, p.refs, p.key, p.tokens, p.table, p.free_stack, p.evlog, p.counts, p.totals,
                     p.win_a, p.win_b, p.hop, p.cls, p.agent_ids, p.ctrl, p.gbound, p.gcount, p.fin_lt, p.fin_slot,
-                    p.fin_n, p.p_slot, p.p_refs0, p.gbuf_lt, p.gbuf_slot};
+                    p.fin_n, p.p_slot, p.p_refs0, p.gbuf_lt, p.gbuf_slot, p.ghint, p.gmaxk, p.grej};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     d_keys.release();
@@ -188,6 +192,7 @@ const csb::AdmitStatus& cs_pool::admit(const csb::AdmitArgs& in, int n_for_grid)
     resident = st->resident;
     pinned = st->pinned;
     ev_total = st->ev_total;
+    for (int k = 0; k < csb::kPhases; ++k) phase_ns[k] += st->phase_ns[k];
     pending_targets.assign(st->pend_target, st->pend_target + std::min(st->n_pend, csb::kMaxPending));
     pending_ticks.assign(st->pend_tick, st->pend_tick + std::min(st->n_pend, csb::kMaxPending));
     if (st->error) throw std::runtime_error("evict_one: all resident blocks are pinned");
@@ -536,6 +541,7 @@ int cs_pool_get_stats(cs_pool_t pool, cs_pool_stats* out) {
         out->scanned_slots = c.scanned_slots;
         out->rebuilds = c.rebuilds;
         out->n_agents = pool->n_agents;
+        for (int k = 0; k < csb::kPhases; ++k) out->phase_ns[k] = pool->phase_ns[k];
     });
 }
 

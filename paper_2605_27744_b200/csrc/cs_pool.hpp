@@ -74,6 +74,7 @@ struct cs_pool {
     double admit_ms = 0.0, scan_launch_ms = 0.0;
     long long admit_launches = 0, scan_launches = 0, scans_total = 0, table_rebuilds = 0;
     long long launches = 0;  // every kernel this handle launched (the bench's gpu_launches)
+    unsigned long long phase_ns[csb::kPhases] = {};
 
     void create(const cs_pool_cfg& c);
     void destroy();

@@ -1,0 +1,55 @@
+"""cfg5-style stress driver: a pre-filled pool snapshot, then admissions of k fresh blocks
+(each evicts k victims) through the C ABI. Prints the per-phase device time of the admission
+kernel; used under ncu to capture the scan. Not part of the product path."""
+import argparse
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, ".")
+import paper_2605_27744_b200 as cb  # noqa: E402
+from paper_2605_27744_b200 import workloads as W  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--pool", type=int, default=16 << 20)
+ap.add_argument("--agents", type=int, default=256)
+ap.add_argument("--k", type=int, default=64)
+ap.add_argument("--iters", type=int, default=20)
+ap.add_argument("--mode", default="realistic")
+ap.add_argument("--policy", default="cachesage")
+args = ap.parse_args()
+
+g = cb.Pool(args.pool, policy=args.policy)
+ids = [int(x) for x in W._splitmix(np.arange(args.agents, dtype=np.uint64) + np.uint64(77))]
+g.register_agents(ids)
+t = time.time()
+keys, lt, agents, refs = W.pool_snapshot(args.pool, args.agents, seed=3, mode=args.mode)
+g.restore(keys, lt, agents=agents, refs=refs)
+print(f"restore {args.pool} slots: {time.time() - t:.2f}s", flush=True)
+tick = int(lt.max())
+rng = np.random.default_rng(1)
+prev = None
+times = []
+st0 = g.stats()
+for it in range(args.iters):
+    a = int(rng.integers(0, args.agents))
+    g.observe_dispatch(prev, a, tick + 1)
+    tick += 1
+    prev = a
+    prompt = (rng.choice(2**62, size=args.k).astype(np.uint64) + np.uint64(2**62))
+    t0 = time.perf_counter()
+    ev, pins = g.admit_pinned(prompt, np.full(args.k, 16, np.int32), agent=a, anchor=8, tick_base=tick)
+    times.append(time.perf_counter() - t0)
+    tick += args.k
+    g.unpin(pins)
+st1 = g.stats()
+ph = np.array(st1["phase_ns"], dtype=np.float64) - np.array(st0["phase_ns"], dtype=np.float64)
+n = args.iters
+names = ["probe/observe/lookup", "prep+barrier", "scan+barrier", "select+barrier", "replay(rest)", "epilogue",
+         "replay-setup", "replay-loop", "apply", "cta0-flush", "cta0-flushes(x1e3)",
+         "fast-evictions", "evictions", "rescans", "bulk-chunks", "-"]
+print("per admission (us, CTA-0 globaltimer): " + ", ".join(
+    f"{nm}={(v / n if k >= 10 else v / n / 1e3):.1f}" for k, (nm, v) in enumerate(zip(names, ph))))
+print(f"host wall per admit call: median {np.median(times) * 1e6:.0f} us; scans={st1['scans'] - st0['scans']}")
+print(f"scan roofline at 16 B/slot: {16 * args.pool / (ph[2] / n * 1e-9) / 1e9:.0f} GB/s over the scan phase")
