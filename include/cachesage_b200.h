@@ -130,6 +130,8 @@ typedef struct cs_pool_stats {
     uint64_t phase_ns[16];
 } cs_pool_stats;
 int cs_pool_get_stats(cs_pool_t pool, cs_pool_stats* out);
+/* Instrumentation: per-CTA scan timestamps of the last admission (grid x 8 u64). */
+int cs_pool_debug(cs_pool_t pool, uint64_t* out, int cap, int* grid);
 
 /* ------------------------------------------------------------------ engine (EngineSim) */
 

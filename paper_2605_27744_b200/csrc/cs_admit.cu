@@ -30,8 +30,8 @@ namespace csb {
 constexpr int kThreads = 512;            // one CTA per SM (cooperative grid)
 constexpr int kV = 4;                    // slots per thread per tile (2 x LDG.128 + 2 x LDG.128)
 constexpr int kTile = kThreads * kV;     // 2048 slots = 32 KiB of SoA per tile
-constexpr int kDepth = 3;                // tiles of loads in flight per thread
-constexpr int kStage = 8192;             // staged candidates per CTA (all lists share it)
+constexpr int kRing = 3;                 // TMA stages (32 KiB of SoA each) per CTA
+constexpr int kStage = 6144;             // staged candidates per CTA (all lists share it)
 constexpr int kFlushAt = kStage - 2 * kTile;  // a tile appends at most 2 entries per slot
 constexpr int kSide = kMaxLists * (kChunk + 1);
 
@@ -46,7 +46,9 @@ struct ScanSmem {
     int wcnt[kMaxLists], wbase[kMaxLists], wpos[kMaxLists];
     unsigned long long flush_ns, flushes;  // instrumentation (reported by CTA 0)
     unsigned long long hint[kMaxLists];
-    unsigned int rej;
+    int overflow;
+    __align__(8) unsigned long long mbar[kRing];        // TMA ring: stage filled
+    __align__(8) unsigned long long mbar_empty[kRing];  // TMA ring: stage released by all consumers
 };
 
 struct AdmSmem {
@@ -78,6 +80,10 @@ constexpr size_t kOffSdLt = (kOffStList + kStage + 15) & ~size_t(15);
 constexpr size_t kOffSdSlot = kOffSdLt + 8ull * kSide;
 constexpr size_t kOffSdList = kOffSdSlot + 4ull * kSide;
 constexpr size_t kOffCls = (kOffSdList + kSide + 15) & ~size_t(15);
+constexpr size_t kOffRing = (kOffCls + kMaxAgents + 127) & ~size_t(127);  // TMA ring (128-B aligned)
+constexpr size_t kRingLt = 8ull * kTile, kRingAg = 4ull * kTile, kRingRf = 4ull * kTile;
+constexpr size_t kRingStage = kRingLt + kRingAg + kRingRf;  // 32 KiB
+constexpr size_t kDynSmem = kOffRing + kRing * kRingStage;
 
 __device__ __forceinline__ ScanBufs scan_bufs(unsigned char* d) {
     ScanBufs b;
@@ -362,58 +368,161 @@ __device__ void stage_flush(const DevPool& P, int NL, int keep, const ScanBufs& 
     __syncthreads();
 }
 
-struct Quad {
-    unsigned long long l[kV];
-    unsigned int a[kV], r[kV];
-};
+// ---- TMA (cp.async.bulk) + mbarrier helpers for the SoA stream
+__device__ __forceinline__ unsigned int smem_u32(const void* p) { return (unsigned int)__cvta_generic_to_shared(p); }
 
-__device__ __forceinline__ void load_quad(const DevPool& P, long long i, long long hi, Quad& q) {
-    if (i + kV <= hi) {
-        const ulonglong2 l01 = __ldcs(reinterpret_cast<const ulonglong2*>(P.lt + i));
-        const ulonglong2 l23 = __ldcs(reinterpret_cast<const ulonglong2*>(P.lt + i + 2));
-        const uint4 aa = __ldcs(reinterpret_cast<const uint4*>(P.agent + i));
-        const uint4 rr = __ldcs(reinterpret_cast<const uint4*>(P.refs + i));
-        q.l[0] = l01.x;
-        q.l[1] = l01.y;
-        q.l[2] = l23.x;
-        q.l[3] = l23.y;
-        q.a[0] = aa.x;
-        q.a[1] = aa.y;
-        q.a[2] = aa.z;
-        q.a[3] = aa.w;
-        q.r[0] = rr.x;
-        q.r[1] = rr.y;
-        q.r[2] = rr.z;
-        q.r[3] = rr.w;
+__device__ __forceinline__ void mbar_init(unsigned long long* m, unsigned int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(m)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* m, unsigned int bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(m)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned long long* m, unsigned int parity) {
+    asm volatile(
+        "{\n.reg .pred p;\nWAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(m)),
+        "r"(parity)
+        : "memory");
+}
+
+// 1-D bulk copy global -> this CTA's shared memory, completion counted on mbarrier m
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned int bytes, unsigned long long* m) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(m))
+                 : "memory");
+}
+
+// One streaming pass over this CTA's contiguous slot range: 16 B per slot read exactly once.
+// The SoA arrives through a kRing-stage TMA ring (cp.async.bulk into shared memory, one
+// elected thread issues, mbarrier transaction counts complete), so kRing-1 tiles of 32 KiB
+// are in flight independently of the threads' progress and no registers hold in-flight data.
+// Survivors go to a staging pool flushed (exact per-list select) only when it could overflow.
+__device__ __forceinline__ void mbar_arrive(unsigned long long* m) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(m)) : "memory");
+}
+
+// Classifies this thread's 4 slots of the current tile. Bit k: resident-oldest list R; bit
+// 4+k: survival-class list cl[k] (unpinned only). Thresholds are < kFreeTick, so free slots
+// never pass a compare. Branch-free except for agent-carrying slots (rare in real pools).
+__device__ __forceinline__ unsigned int classify4(const unsigned long long (&x4)[kV], const unsigned int (&a4)[kV],
+                                                  const unsigned int (&r4)[kV], unsigned long long thrR,
+                                                  unsigned long long thrE, volatile unsigned long long* thr,
+                                                  const unsigned char* cls, int E, int (&cl)[kV]) {
+    unsigned int acc = 0u;
+#pragma unroll
+    for (int k = 0; k < kV; ++k) {
+        const unsigned long long x = x4[k];
+        acc |= (unsigned int)(x <= thrR) << k;
+        cl[k] = E;
+        if (a4[k] == kNoAgent) {
+            acc |= (unsigned int)(r4[k] == 0u && x <= thrE) << (kV + k);
+        } else if (r4[k] == 0u) {
+            const int c = cls[a4[k]];
+            cl[k] = c;
+            acc |= (unsigned int)(x <= thr[c]) << (kV + k);
+        }
+    }
+    return acc;
+}
+
+// Warp-aggregated append of the accepted entries (one shared atomic per warp). Returns the last
+// reserved position (-1: none). With `bounded`, a reservation past the staging capacity sets
+// S.overflow and writes nothing (the fast pass is then redone in safe mode).
+__device__ __forceinline__ int append4(unsigned int acc, const unsigned long long (&x4)[kV], const int (&cl)[kV],
+                                       long long i0, int R, const ScanBufs& B, ScanSmem& S, bool bounded) {
+    if (!__any_sync(0xffffffffu, acc != 0u)) return -1;
+    const int mine = __popc(acc);
+    int incl = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane_id() >= o) incl += v;
+    }
+    const int wtot = __shfl_sync(0xffffffffu, incl, 31);
+    int base = 0;
+    if (lane_id() == 31) base = atomicAdd(&S.count, wtot);
+    base = __shfl_sync(0xffffffffu, base, 31);
+    if (bounded && base + wtot > kStage) {
+        S.overflow = 1;
+        return kStage;
+    }
+    int p = base + incl - mine;
+#pragma unroll
+    for (int k = 0; k < kV; ++k) {
+        if (acc & (1u << k)) {
+            B.st_lt[p] = x4[k];
+            B.st_slot[p] = (unsigned int)(i0 + k);
+            B.st_list[p] = (unsigned char)R;
+            ++p;
+        }
+        if (acc & (1u << (kV + k))) {
+            B.st_lt[p] = x4[k];
+            B.st_slot[p] = (unsigned int)(i0 + k);
+            B.st_list[p] = (unsigned char)cl[k];
+            ++p;
+        }
+    }
+    return base + wtot - 1;
+}
+
+// Reads this thread's 4 slots of ring stage `st` (kFreeTick / no agent / pinned when the
+// thread has no slots in the tile).
+__device__ __forceinline__ void read4(const unsigned char* st, int tid, bool valid, unsigned long long (&x4)[kV],
+                                      unsigned int (&a4)[kV], unsigned int (&r4)[kV]) {
+    if (valid) {
+        const ulonglong2 l01 = *reinterpret_cast<const ulonglong2*>(st + (size_t)tid * 32);
+        const ulonglong2 l23 = *reinterpret_cast<const ulonglong2*>(st + (size_t)tid * 32 + 16);
+        const uint4 aa = *reinterpret_cast<const uint4*>(st + kRingLt + (size_t)tid * 16);
+        const uint4 rr = *reinterpret_cast<const uint4*>(st + kRingLt + kRingAg + (size_t)tid * 16);
+        x4[0] = l01.x;
+        x4[1] = l01.y;
+        x4[2] = l23.x;
+        x4[3] = l23.y;
+        a4[0] = aa.x;
+        a4[1] = aa.y;
+        a4[2] = aa.z;
+        a4[3] = aa.w;
+        r4[0] = rr.x;
+        r4[1] = rr.y;
+        r4[2] = rr.z;
+        r4[3] = rr.w;
     } else {
 #pragma unroll
         for (int k = 0; k < kV; ++k) {
-            if (i + k < hi) {
-                q.l[k] = __ldcs(P.lt + i + k);
-                q.a[k] = __ldcs(P.agent + i + k);
-                q.r[k] = __ldcs(P.refs + i + k);
-            } else {
-                q.l[k] = kFreeTick;
-                q.a[k] = kNoAgent;
-                q.r[k] = 1u;
-            }
+            x4[k] = kFreeTick;
+            a4[k] = kNoAgent;
+            r4[k] = 1u;
         }
     }
 }
 
-// One streaming pass over this CTA's contiguous slot range: 16 B per slot read exactly once,
-// kDepth tiles (96 KiB per SM) of 128-bit loads in flight; survivors go to a staging pool that
-// is flushed (exact per-list select) only when it could overflow on the next tile.
-__device__ void scan_pass(const DevPool& P, int NL, int keep, const ScanBufs& B, ScanSmem& S, SelectSmem& Sel) {
-    const int tid = threadIdx.x, T = blockDim.x;
-    const long long TV = (long long)T * kV;
-    long long per = (P.cap + gridDim.x - 1) / gridDim.x;
+// One streaming pass over this CTA's contiguous slot range: 16 B per slot read exactly once.
+// The SoA arrives through a kRing-stage TMA ring (cp.async.bulk into shared memory, mbarrier
+// transaction counts), so the loads are independent of the threads' progress.
+//   fast: warp-specialized. A producer warp refills a stage as soon as the 16 consumer warps
+//         release it (per-stage "empty" mbarriers); no CTA-wide barrier per tile. Used when
+//         every list has a hint (or is known small), so survivors fit the staging pool; an
+//         overflow aborts the pass and the caller redoes it in safe mode.
+//   safe: one CTA barrier per tile decides whether the staging pool must be flushed (exact
+//         per-list select) before it could overflow; any threshold state works.
+// Returns with S.overflow set when a fast pass overflowed.
+__device__ void scan_pass(const DevPool& P, int NL, int keep, const ScanBufs& B, ScanSmem& S, SelectSmem& Sel,
+                          unsigned char* dsm, bool fast) {
+    const int tid = threadIdx.x;
+    const long long TV = kTile;  // consumer threads (kThreads) x kV slots
+    long long per = (P.cap_scan + gridDim.x - 1) / gridDim.x;
     per = (per + kV - 1) / kV * kV;
-    const long long lo = min(P.cap, (long long)blockIdx.x * per);
-    const long long hi = min(P.cap, lo + per);
+    const long long lo = min(P.cap_scan, (long long)blockIdx.x * per);
+    const long long hi = min(P.cap_scan, lo + per);  // multiple of 4 slots: 16-B granules
+    const int ntiles = (int)((hi - lo + TV - 1) / TV);
     const int R = NL - 1;
     const int E = P.e_max;  // class of agentless / unreachable blocks (survival 0)
     const unsigned char* cls = B.cls;
+    unsigned char* ring = dsm + kOffRing;
     if (tid < NL) {
         // start from the previous scan's hint: no accept-everything warm-up tiles
         const unsigned long long h = P.ghint[tid];
@@ -422,92 +531,103 @@ __device__ void scan_pass(const DevPool& P, int NL, int keep, const ScanBufs& B,
     }
     if (tid == 0) {
         S.count = 0;
+        S.overflow = 0;
         S.flush_ns = 0;
         S.flushes = 0;
-        S.rej = 0u;
-    }
-    __syncthreads();
-    volatile unsigned long long* thr = S.thr;
-    const unsigned long long hintR = S.hint[R], hintE = S.hint[E];
-    unsigned int rej = 0u;  // lists with an element above the hint (verified after the select)
-
-    Quad q[kDepth];
-#pragma unroll
-    for (int d = 0; d < kDepth; ++d) load_quad(P, lo + d * TV + (long long)tid * kV, hi, q[d]);
-
-    for (long long base = lo; base < hi; base += kDepth * TV) {
-#pragma unroll
-        for (int d = 0; d < kDepth; ++d) {
-            const long long tb = base + d * TV;
-            if (tb >= hi) break;
-            unsigned long long gbn = ~0ull;
-            if (tid < NL) gbn = ld_relaxed_u64(P.gbound + tid);
-            const unsigned long long thrR = thr[R];
-            const unsigned long long thrE = thr[E];
-            const long long i0 = tb + (long long)tid * kV;
-            // classify the 4 slots: bit k -> resident list, bit 4+k -> class list cl[k]
-            unsigned int acc = 0u;
-            int cl[kV];
-#pragma unroll
-            for (int k = 0; k < kV; ++k) {
-                const unsigned long long x = q[d].l[k];
-                cl[k] = E;
-                if (x == kFreeTick) continue;
-                if (x <= thrR) acc |= 1u << k;
-                if (x > hintR) rej |= 1u << R;
-                if (q[d].r[k] == 0u) {
-                    const unsigned int a = q[d].a[k];
-                    unsigned long long tc = thrE, hc = hintE;
-                    if (a != kNoAgent) {
-                        cl[k] = cls[a];
-                        tc = thr[cl[k]];
-                        hc = S.hint[cl[k]];
-                    }
-                    if (x <= tc) acc |= 1u << (kV + k);
-                    if (x > hc) rej |= 1u << cl[k];
-                }
-            }
-            // warp-aggregated reservation: one shared atomic per warp per tile
-            const int mine = __popc(acc);
-            int incl = mine;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int t = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane_id() >= o) incl += t;
-            }
-            const int wtot = __shfl_sync(0xffffffffu, incl, 31);
-            int base = 0;
-            if (lane_id() == 31 && wtot) base = atomicAdd(&S.count, wtot);
-            base = __shfl_sync(0xffffffffu, base, 31);
-            int p = base + incl - mine;
-            const int maxpos = wtot ? base + wtot - 1 : -1;
-            if (acc) {
-#pragma unroll
-                for (int k = 0; k < kV; ++k) {
-                    if (acc & (1u << k)) {
-                        B.st_lt[p] = q[d].l[k];
-                        B.st_slot[p] = (unsigned int)(i0 + k);
-                        B.st_list[p] = (unsigned char)R;
-                        ++p;
-                    }
-                    if (acc & (1u << (kV + k))) {
-                        B.st_lt[p] = q[d].l[k];
-                        B.st_slot[p] = (unsigned int)(i0 + k);
-                        B.st_list[p] = (unsigned char)cl[k];
-                        ++p;
-                    }
-                }
-            }
-            load_quad(P, tb + kDepth * TV + (long long)tid * kV, hi, q[d]);
-            if (tid < NL && gbn < thr[tid]) thr[tid] = gbn;
-            if (__syncthreads_or(maxpos >= kFlushAt)) stage_flush(P, NL, keep, B, S, Sel, false);
+        for (int s = 0; s < kRing; ++s) {
+            mbar_init(&S.mbar[s], 1u);
+            mbar_init(&S.mbar_empty[s], (unsigned int)(kThreads / 32));
         }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    rej = __reduce_or_sync(0xffffffffu, rej);
-    if (lane_id() == 0 && rej) atomicOr(&S.rej, rej);
     __syncthreads();
+    auto issue = [&](int t) {  // one elected thread
+        const int s = t % kRing;
+        const long long b0 = lo + (long long)t * TV;
+        const unsigned int nsl = (unsigned int)min(TV, hi - b0);
+        unsigned char* st = ring + (size_t)s * kRingStage;
+        mbar_expect_tx(&S.mbar[s], nsl * 16u);
+        bulk_g2s(st, P.lt + b0, nsl * 8u, &S.mbar[s]);
+        bulk_g2s(st + kRingLt, P.agent + b0, nsl * 4u, &S.mbar[s]);
+        bulk_g2s(st + kRingLt + kRingAg, P.refs + b0, nsl * 4u, &S.mbar[s]);
+    };
+    if (tid == 0) {
+        P.dbg[blockIdx.x * 16 + 0] = gtimer();
+        P.dbg[blockIdx.x * 16 + 7] = clock64();
+    }
+    volatile unsigned long long* thr = S.thr;
+    const bool consumer = tid < kThreads;
+
+    if (fast) {
+        if (!consumer) {  // producer warp
+            if (lane_id() == 0) {
+                for (int t = 0; t < ntiles; ++t) {
+                    const int s = t % kRing;
+                    if (t >= kRing) mbar_wait(&S.mbar_empty[s], (unsigned int)(((t / kRing) - 1) & 1));
+                    issue(t);
+                }
+            }
+            __syncwarp();
+        } else {
+            unsigned long long gbn = ~0ull;
+            for (int t = 0; t < ntiles; ++t) {
+                const int s = t % kRing;
+                if (tid < NL && s == 0) {  // grid-wide bounds: refreshed every kRing tiles, applied a round later
+                    if (gbn < thr[tid]) thr[tid] = gbn;
+                    gbn = ld_relaxed_u64(P.gbound + tid);
+                }
+                const long long i0 = lo + (long long)t * TV + (long long)tid * kV;
+                const unsigned char* st = ring + (size_t)s * kRingStage;
+                mbar_wait(&S.mbar[s], (unsigned int)((t / kRing) & 1));
+                unsigned long long x4[kV];
+                unsigned int a4[kV], r4[kV];
+                read4(st, tid, i0 + kV <= hi, x4, a4, r4);
+                __syncwarp();
+                if (lane_id() == 0) mbar_arrive(&S.mbar_empty[s]);  // stage s consumed by this warp
+                int cl[kV];
+                const unsigned int acc = classify4(x4, a4, r4, thr[R], thr[E], thr, cls, E, cl);
+                append4(acc, x4, cl, i0, R, B, S, true);
+            }
+        }
+        __syncthreads();
+        if (S.overflow) {
+            if (tid == 0) atomicExch(&P.ctrl->rescan, 1);
+            return;  // the caller redoes this pass in safe mode
+        }
+    } else {
+        if (tid == 0)
+            for (int t = 0; t < kRing && t < ntiles; ++t) issue(t);
+        unsigned long long gbn = ~0ull;
+        for (int t = 0; t < ntiles; ++t) {
+            const int s = t % kRing;
+            if (tid < NL && s == 0) {
+                if (gbn < thr[tid]) thr[tid] = gbn;
+                gbn = ld_relaxed_u64(P.gbound + tid);
+            }
+            const long long i0 = lo + (long long)t * TV + (long long)tid * kV;
+            const unsigned char* st = ring + (size_t)s * kRingStage;
+            mbar_wait(&S.mbar[s], (unsigned int)((t / kRing) & 1));
+            unsigned long long x4[kV];
+            unsigned int a4[kV], r4[kV];
+            read4(st, tid, consumer && i0 + kV <= hi, x4, a4, r4);
+            int cl[kV];
+            const unsigned int acc = classify4(x4, a4, r4, thr[R], thr[E], thr, cls, E, cl);
+            const int maxpos = append4(acc, x4, cl, i0, R, B, S, false);
+            // every thread is done with stage s: refill it with tile t + kRing
+            const int need_flush = __syncthreads_or(maxpos >= kFlushAt);
+            if (tid == 0 && t + kRing < ntiles) issue(t + kRing);
+            if (need_flush) stage_flush(P, NL, keep, B, S, Sel, false);
+        }
+        __syncthreads();
+    }
+    if (tid == 0) {
+        P.dbg[blockIdx.x * 16 + 1] = gtimer();
+        P.dbg[blockIdx.x * 16 + 5] = S.count;
+        P.dbg[blockIdx.x * 16 + 6] = clock64() - P.dbg[blockIdx.x * 16 + 7];  // SM cycles of the stream
+        P.dbg[blockIdx.x * 16 + 8] = fast ? 1 : 0;
+    }
     if (S.count > 0) stage_flush(P, NL, keep, B, S, Sel, true);
-    if (tid == 0 && S.rej) atomicOr(P.grej, S.rej);
+    if (tid == 0) P.dbg[blockIdx.x * 16 + 2] = gtimer();
     // publish this CTA's survivors that can still be among the global keep smallest
     if (tid < NL) {
         S.gbw[tid] = ld_relaxed_u64(P.gbound + tid);
@@ -516,6 +636,7 @@ __device__ void scan_pass(const DevPool& P, int NL, int keep, const ScanBufs& B,
     }
     __syncthreads();
     const int m = S.count;
+    const int T = blockDim.x;
     for (int j = tid; j < m; j += T)
         if (B.st_lt[j] <= S.gbw[B.st_list[j]]) atomicAdd(&S.wcnt[B.st_list[j]], 1);
     __syncthreads();
@@ -531,6 +652,7 @@ __device__ void scan_pass(const DevPool& P, int NL, int keep, const ScanBufs& B,
         }
     }
     __syncthreads();
+    if (tid == 0) P.dbg[blockIdx.x * 16 + 3] = gtimer();
 }
 
 // ------------------------------------------------------------------ K5a: exact per-list select
@@ -601,11 +723,13 @@ __device__ void finalize_list(const DevPool& P, int l, int NL, int keep, const S
         P.fin_n[l] = n;
         // Hint verification: a list that came up short while some member was rejected only by
         // its hint may be missing candidates -> the whole pass is redone without hints.
-        const bool hinted = P.ghint[l] != ~0ull;
-        const unsigned int rej = *(volatile unsigned int*)P.grej;
-        if (n < kl && hinted && ((rej >> l) & 1u)) atomicExch(&P.ctrl->rescan, 1);
+        // Hints are only carried for lists that were full (n == keep) in the previous scan; a
+        // hinted list that now comes up short may be missing members above its hint.
+        const bool hinted = P.ghint[l] < kNoBound;
+        if (n < kl && hinted) atomicExch(&P.ctrl->rescan, 1);
         const unsigned long long mk = *(volatile unsigned long long*)(P.gmaxk + l);
-        P.ghint[l] = mk ? mk : ~0ull;
+        P.ghint[l] = (n == kl && mk) ? mk : kNoBound;
+        P.gsmall[l] = n < kl ? 1 : 0;
     }
     __syncthreads();
 }
@@ -1036,7 +1160,7 @@ __device__ void write_status(const DevPool& P, const AdmitArgs& a, const AdmSmem
     __threadfence_system();
 }
 
-__global__ void __launch_bounds__(kThreads, 1) admit_kernel(DevPool P, AdmitArgs a) {
+__global__ void __launch_bounds__(kThreads + 32, 1) admit_kernel(DevPool P, AdmitArgs a) {
     extern __shared__ __align__(16) unsigned char dsm[];
     __shared__ ScanSmem S;
     __shared__ SelectSmem Sel;
@@ -1136,13 +1260,18 @@ __global__ void __launch_bounds__(kThreads, 1) admit_kernel(DevPool P, AdmitArgs
                 absent = block_sum(absent, Red);
                 const int need_scan = C->resident + absent > P.cap ? 1 : 0;
                 if (tid < NL && need_scan) {
-                    P.gbound[tid] = ~0ull;
+                    P.gbound[tid] = kNoBound;
                     P.gcount[tid] = 0;
                     P.gmaxk[tid] = 0ull;
                 }
                 if (tid == 0) {
                     *P.grej = 0u;
                     C->rescan = 0;
+                    // warp-specialized pass only when every list has a hint or is known small
+                    int fast = 1;
+                    for (int l = 0; l < NL; ++l)
+                        if (!(P.ghint[l] < kNoBound) && !P.gsmall[l]) fast = 0;
+                    C->fast = fast;
                     C->need_scan = need_scan;
                     C->keep = hi - lo;
                     if (need_scan) {
@@ -1163,12 +1292,13 @@ __global__ void __launch_bounds__(kThreads, 1) admit_kernel(DevPool P, AdmitArgs
             for (int x = tid; x < a.n_agents; x += T) B.cls[x] = P.cls[x];
             __syncthreads();
             for (int pass = 0; pass < 2; ++pass) {
-                scan_pass(P, NL, keep, B, S, Sel);
+                scan_pass(P, NL, keep, B, S, Sel, dsm, pass == 0 && *(volatile int*)&C->fast);
                 if (blockIdx.x == 0 && tid == 0) {
                     A.ph[9] += S.flush_ns;
                     A.ph[10] += S.flushes;
                 }
                 grid_barrier(C);
+                if (tid == 0) P.dbg[blockIdx.x * 16 + 4] = gtimer();
                 stamp(A, 2);
                 for (int l = blockIdx.x; l < NL; l += gridDim.x) finalize_list(P, l, NL, keep, B, Sel);
                 grid_barrier(C);
@@ -1178,8 +1308,8 @@ __global__ void __launch_bounds__(kThreads, 1) admit_kernel(DevPool P, AdmitArgs
                 // a hint was too tight for some list: redo the pass with no hints (exact)
                 if (blockIdx.x == 0) {
                     if (tid < NL) {
-                        P.ghint[tid] = ~0ull;
-                        P.gbound[tid] = ~0ull;
+                        P.ghint[tid] = kNoBound;
+                        P.gbound[tid] = kNoBound;
                         P.gcount[tid] = 0;
                         P.gmaxk[tid] = 0ull;
                     }
@@ -1227,18 +1357,19 @@ LaunchCfg admit_launch_config(const DevPool& P, int device, int want_grid) {
     LaunchCfg lc{0, 0, 0, 0};
     cudaDeviceProp prop;
     if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return lc;
-    const size_t smem = kOffCls + (size_t)((P.a_cap + 15) & ~15);
+    const size_t smem = kDynSmem;
     if (smem + sizeof(ScanSmem) + sizeof(SelectSmem) + sizeof(RedSmem) + sizeof(AdmSmem) > prop.sharedMemPerBlockOptin)
         return lc;
     if (cudaFuncSetAttribute(admit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return lc;
     int occ = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, admit_kernel, kThreads, smem) != cudaSuccess || occ < 1)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, admit_kernel, kThreads + 32, smem) != cudaSuccess ||
+        occ < 1)
         return lc;
     int grid = prop.multiProcessorCount * occ;
     if (want_grid > 0 && want_grid < grid) grid = want_grid;
     lc.grid = grid;
-    lc.threads = kThreads;
+    lc.threads = kThreads + 32;  // 16 consumer warps + 1 TMA producer warp
     lc.cap_per_list = 0;
     lc.smem = smem;
     return lc;

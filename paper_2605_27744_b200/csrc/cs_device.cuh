@@ -9,6 +9,7 @@ namespace csb {
 // ---------------------------------------------------------------- constants
 
 constexpr unsigned long long kFreeTick = ~0ull;  // last_touch of a free slot (never a real tick)
+constexpr unsigned long long kNoBound = ~0ull - 1;  // "no threshold": every real tick passes, free slots do not
 constexpr unsigned int kNoAgent = 0xFFFFFFFFu;   // Block::agent == nullopt (types.hpp:45)
 constexpr unsigned int kNoSlot = 0xFFFFFFFFu;
 constexpr unsigned int kSlotEmpty = 0xFFFFFFFFu;  // table entry never used
@@ -71,11 +72,13 @@ struct Ctrl {
     int chunk_lo, chunk_hi;
     int error;
     int rescan;        // a hinted list came up short: scan again without hints
+    int fast;          // this chunk's first scan pass runs warp-specialized (no per-tile barrier)
     long long rescans; // instrumentation
 };
 
 struct DevPool {
     long long cap;            // slots == EngineConfig::budget_blocks
+    long long cap_scan;       // cap rounded up to 64: the SoA tail is padded with free slots
     int policy;               // 0 lru, 1 cachesage
     int e_max;
     int n_lists;              // e_max + 2 (classes 0..e_max, resident list last)
@@ -111,13 +114,16 @@ struct DevPool {
     int* gcount;                  // [kMaxLists]
     unsigned long long* ghint;    // [kMaxLists] acceptance hint carried to the next scan (~0 = none)
     unsigned long long* gmaxk;    // [kMaxLists] max over CTAs of their local keep-th value
-    unsigned int* grej;           // bit l: some element of list l was rejected only by its hint
+    unsigned int* grej;           // unused (kept for layout stability)
+    unsigned char* gsmall;        // [kMaxLists] list had fewer than keep members in its last scan
     unsigned long long* gbuf_lt;  // [kMaxLists][gcap]
     unsigned int* gbuf_slot;
     long long gcap;
     unsigned long long* fin_lt;   // [kMaxLists][kChunk + 2]
     unsigned int* fin_slot;
     int* fin_n;
+
+    unsigned long long* dbg;      // [grid * 8] per-CTA instrumentation timestamps
 
     // per-admission prompt scratch (grown by the host)
     unsigned int* p_slot;

@@ -19,12 +19,14 @@ __global__ void init_pool_kernel(DevPool P) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long stride = (long long)gridDim.x * blockDim.x;
     for (long long s = i; s < P.cap; s += stride) {
-        P.lt[s] = kFreeTick;
-        P.agent[s] = kNoAgent;
-        P.refs[s] = 0u;
         P.key[s] = 0ull;
         P.tokens[s] = 0;
         P.free_stack[s] = (unsigned int)(P.cap - 1 - s);  // pops hand out slot 0 first
+    }
+    for (long long s = i; s < P.cap_scan; s += stride) {  // pad slots stay free forever
+        P.lt[s] = kFreeTick;
+        P.agent[s] = kNoAgent;
+        P.refs[s] = 0u;
     }
     for (long long e = i; e <= (long long)P.tmask; e += stride) {
         P.table[e].key = 0ull;

@@ -79,9 +79,10 @@ void cs_pool::create(const cs_pool_cfg& c) {
     while (tcap < 4ull * (unsigned long long)p.cap) tcap <<= 1;  // live+tombstones <= tcap/2 + one admission
     p.tmask = tcap - 1;
 
-    p.lt = dmalloc<unsigned long long>(p.cap, "lt");
-    p.agent = dmalloc<unsigned int>(p.cap, "agent");
-    p.refs = dmalloc<unsigned int>(p.cap, "refs");
+    p.cap_scan = (p.cap + 63) & ~63ll;  // bulk copies move whole 16-B granules
+    p.lt = dmalloc<unsigned long long>(p.cap_scan, "lt");
+    p.agent = dmalloc<unsigned int>(p.cap_scan, "agent");
+    p.refs = dmalloc<unsigned int>(p.cap_scan, "refs");
     p.key = dmalloc<unsigned long long>(p.cap, "key");
     p.tokens = dmalloc<int>(p.cap, "tokens");
     p.table = dmalloc<csb::TableEntry>(tcap, "table");
@@ -105,6 +106,8 @@ void cs_pool::create(const cs_pool_cfg& c) {
     p.ghint = dmalloc<unsigned long long>(csb::kMaxLists, "ghint");
     p.gmaxk = dmalloc<unsigned long long>(csb::kMaxLists, "gmaxk");
     p.grej = dmalloc<unsigned int>(1, "grej");
+    p.gsmall = dmalloc<unsigned char>(csb::kMaxLists, "gsmall");
+    ck(cudaMemsetAsync(p.gsmall, 0, csb::kMaxLists, stream), "memset");
     ck(cudaMemsetAsync(p.ghint, 0xff, sizeof(unsigned long long) * csb::kMaxLists, stream), "memset");
     p.fin_lt = dmalloc<unsigned long long>((size_t)csb::kMaxLists * (csb::kChunk + 2), "fin_lt");
     p.fin_slot = dmalloc<unsigned int>((size_t)csb::kMaxLists * (csb::kChunk + 2), "fin_slot");
@@ -119,6 +122,8 @@ void cs_pool::create(const cs_pool_cfg& c) {
     p.gcap = (long long)lc.grid * (csb::kChunk + 1);
     p.gbuf_lt = dmalloc<unsigned long long>((size_t)csb::kMaxLists * p.gcap, "gbuf_lt");
     p.gbuf_slot = dmalloc<unsigned int>((size_t)csb::kMaxLists * p.gcap, "gbuf_slot");
+    p.dbg = dmalloc<unsigned long long>((size_t)lc.grid * 16, "dbg");
+    ck(cudaMemsetAsync(p.dbg, 0, sizeof(unsigned long long) * lc.grid * 16, stream), "memset");
 
     ck(cudaHostAlloc(reinterpret_cast<void**>(&st), sizeof(csb::AdmitStatus), cudaHostAllocMapped), "cudaHostAlloc");
     std::memset(st, 0, sizeof(*st));
@@ -131,7 +136,7 @@ void cs_pool::destroy() {
     csb::DevPool& p = P;
     void* ptrs[] = {p.lt, p.agent, p.refs, p.key, p.tokens, p.table, p.free_stack, p.evlog, p.counts, p.totals,
                     p.win_a, p.win_b, p.hop, p.cls, p.agent_ids, p.ctrl, p.gbound, p.gcount, p.fin_lt, p.fin_slot,
-                    p.fin_n, p.p_slot, p.p_refs0, p.gbuf_lt, p.gbuf_slot, p.ghint, p.gmaxk, p.grej};
+                    p.fin_n, p.p_slot, p.p_refs0, p.gbuf_lt, p.gbuf_slot, p.ghint, p.gmaxk, p.grej, p.dbg, p.gsmall};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     d_keys.release();
@@ -524,6 +529,17 @@ int cs_poll_actions(cs_pool_t pool, int* targets, uint64_t* ticks, int cap, int*
         pool->pending_targets.clear();
         pool->pending_ticks.clear();
         pool->poll_reset_pending = true;
+    });
+}
+
+/* Instrumentation: per-CTA timestamps of the last scan (grid x 8 u64, globaltimer ns). */
+int cs_pool_debug(cs_pool_t pool, uint64_t* out, int cap, int* grid) {
+    return guard([&] {
+        if (!pool || !out) throw std::invalid_argument("cs_pool_debug: null argument");
+        pool->sync();
+        const int n = std::min(cap, pool->lc.grid * 16);
+        ck(cudaMemcpy(out, pool->P.dbg, 8 * (size_t)n, cudaMemcpyDeviceToHost), "dbg D2H");
+        if (grid) *grid = pool->lc.grid;
     });
 }
 

@@ -5,6 +5,7 @@
 //   tma-loop  : same classification, SoA tiles staged by cp.async.bulk + mbarrier ring
 // Build: nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o scan_bench scan_bench.cu
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("%s: %s\n", #x, cudaGetErrorString(e)); return 1; } } while (0)
@@ -123,10 +124,18 @@ __global__ void __launch_bounds__(512, 1) tma_loop(const unsigned long long* lt,
 }
 
 int main() {
-    const long long N = 16ll << 20;
+    const long long N = 64ll << 20;  // 1 GiB of SoA: far beyond the 126 MB L2
     unsigned long long* lt; unsigned int *ag, *rf; unsigned long long* out;
     CK(cudaMalloc(&lt, N * 8)); CK(cudaMalloc(&ag, N * 4)); CK(cudaMalloc(&rf, N * 4)); CK(cudaMalloc(&out, 8));
-    CK(cudaMemset(lt, 0x11, N * 8)); CK(cudaMemset(ag, 0x22, N * 4)); CK(cudaMemset(rf, 0x33, N * 4));
+    {   // random contents (no compressible / constant pages)
+        unsigned long long* h = (unsigned long long*)malloc(N * 8);
+        unsigned long long x = 88172645463325252ull;
+        for (long long i = 0; i < N; ++i) { x ^= x << 13; x ^= x >> 7; x ^= x << 17; h[i] = x; }
+        CK(cudaMemcpy(lt, h, N * 8, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(ag, h, N * 4, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(rf, (char*)h + N * 4, N * 4, cudaMemcpyHostToDevice));
+        free(h);
+    }
     cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
     int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     auto timeit = [&](const char* name, auto fn) {

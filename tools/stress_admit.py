@@ -53,3 +53,22 @@ print("per admission (us, CTA-0 globaltimer): " + ", ".join(
     f"{nm}={(v / n if k >= 10 else v / n / 1e3):.1f}" for k, (nm, v) in enumerate(zip(names, ph))))
 print(f"host wall per admit call: median {np.median(times) * 1e6:.0f} us; scans={st1['scans'] - st0['scans']}")
 print(f"scan roofline at 16 B/slot: {16 * args.pool / (ph[2] / n * 1e-9) / 1e9:.0f} GB/s over the scan phase")
+
+# per-CTA timeline of the last scan (instrumentation buffer)
+import ctypes as C
+from paper_2605_27744_b200._lib import lib
+buf = (C.c_uint64 * (16 * 1024))()
+grid = C.c_int(0)
+lib().cs_pool_debug(g.h, buf, 16 * 1024, C.byref(grid))
+d = np.array(buf[:16 * grid.value], dtype=np.int64).reshape(grid.value, 16)
+t0 = d[:, 0].min()
+rel = (d[:, :5] - t0) / 1e3
+print(f"CTAs={grid.value}: scan start spread {rel[:,0].max():.1f} us; stream end min/med/max "
+      f"{rel[:,1].min():.1f}/{np.median(rel[:,1]):.1f}/{rel[:,1].max():.1f}; final flush end max {rel[:,2].max():.1f}; "
+      f"writeout end max {rel[:,3].max():.1f}; barrier exit {rel[:,4].max():.1f} us")
+print(f"staged at stream end: med {np.median(d[:,5]):.0f} max {d[:,5].max()}")
+mhz = d[:, 6] / ((d[:, 1] - d[:, 0]) / 1e3)
+print(f"SM clock during the stream (clock64 / globaltimer): med {np.median(mhz):.0f} MHz (min {mhz.min():.0f})")
+print("stream time per CTA (us): min/med/max", np.round(np.percentile(rel[:,1]-rel[:,0],[0,50,100]),1))
+nt = 0
+print("last scan ran fast (warp-specialized):", bool(d[0, 8]))
