@@ -46,6 +46,7 @@ struct ScanSmem {
     int wcnt[kMaxLists], wbase[kMaxLists], wpos[kMaxLists];
     unsigned long long flush_ns, flushes;  // instrumentation (reported by CTA 0)
     unsigned long long hint[kMaxLists];
+    unsigned long long lmin[kMaxLists];
     int overflow;
     __align__(8) unsigned long long mbar[kRing];        // TMA ring: stage filled
     __align__(8) unsigned long long mbar_empty[kRing];  // TMA ring: stage released by all consumers
@@ -112,6 +113,7 @@ struct ReplaySmem {
     unsigned long long out_lt[kChunk];
     unsigned char out_new[kChunk];
     unsigned int victims[kChunk];
+    unsigned long long vkey[kChunk];
     unsigned int freeslots[kChunk];
     unsigned int ph_key[512];  // slot -> chunk index hash of the chunk's resident prompt blocks
     short ph_val[512];
@@ -157,15 +159,15 @@ __device__ void observe_dispatch(const DevPool& P, int prev, int next, unsigned 
     // K3: TransitionLearner::record (transition_learner.cpp:22-51): one pair per dispatch
     if (prev >= 0 && tid == 0) {
         const long long head = C->win_head, size = C->win_size;
-        P.counts[(long long)prev * Acap + next] += 1u;
-        P.totals[prev] += 1u;
+        atomicAdd(&P.counts[(long long)prev * Acap + next], 1u);  // fire-and-forget (RED)
+        atomicAdd(&P.totals[prev], 1u);
         if (size == W) {
             const int oa = P.win_a[head], ob = P.win_b[head];
             P.win_a[head] = prev;
             P.win_b[head] = next;
-            P.counts[(long long)oa * Acap + ob] -= 1u;
-            P.totals[oa] -= 1u;
-            C->win_head = (head + 1) % W;
+            atomicSub(&P.counts[(long long)oa * Acap + ob], 1u);
+            atomicSub(&P.totals[oa], 1u);
+            C->win_head = head + 1 == W ? 0 : head + 1;
         } else {
             const long long pos = (head + size) % W;
             P.win_a[pos] = prev;
@@ -261,6 +263,7 @@ __device__ void observe_dispatch(const DevPool& P, int prev, int next, unsigned 
         if (lane_id() == 0) {
             Red.u[warp_id()] = best_c;
             Red.v[warp_id()] = (long long)best_b;
+            Red.w[warp_id()] = best_id;
         }
         __syncthreads();
         if (tid == 0) {
@@ -271,7 +274,7 @@ __device__ void observe_dispatch(const DevPool& P, int prev, int next, unsigned 
             for (int w = 0; w < nw; ++w) {
                 const int b = (int)Red.v[w];
                 if (b < 0) continue;
-                const unsigned long long c = Red.u[w], id = P.agent_ids[b];
+                const unsigned long long c = Red.u[w], id = Red.w[w];
                 if (best_b < 0 || c > best_c || (c == best_c && id < best_id)) {
                     best_c = c;
                     best_id = id;
@@ -301,11 +304,71 @@ __device__ __forceinline__ int keep_of(int l, int NL, int keep) { return l == NL
 
 // Per list: keep the keep_l smallest staged entries (exact select), tighten the list's bound,
 // publish it grid-wide, and compact the staging pool.
+// Small staging pools: rank of each entry among the same list's entries (ticks are distinct),
+// O(m^2 / threads) compares and no multi-pass barriers. The entry of rank keep_l - 1 is the
+// list's new bound; entries of rank < keep_l survive.
+constexpr int kRankSelectMax = 768;
+
+__device__ void stage_flush_rank(const DevPool& P, int NL, int keep, const ScanBufs& B, ScanSmem& S,
+                                 bool final_flush) {
+    const int tid = threadIdx.x, T = blockDim.x;
+    const int m = S.count;
+    if (tid == 0) S.side_n = 0;
+    __syncthreads();
+    for (int j0 = 0; j0 < m; j0 += T) {
+        const int j = j0 + tid;
+        bool keep_it = false;
+        unsigned char l = 0;
+        unsigned long long x = 0;
+        if (j < m) {
+            l = B.st_list[j];
+            x = B.st_lt[j];
+            int r = 0;
+            for (int k = 0; k < m; ++k) r += (B.st_list[k] == l) & (B.st_lt[k] < x);
+            const int kl = keep_of(l, NL, keep);
+            keep_it = r < kl;
+            if (r == kl - 1) {  // exactly kl entries of list l are <= x: a valid bound
+                if (x < S.thr[l]) S.thr[l] = x;
+                atomicMin(P.gbound + l, x);
+                if (final_flush) atomicMax(P.gmaxk + l, x);  // next scan's hint
+            }
+        }
+        const unsigned int ball = __ballot_sync(0xffffffffu, keep_it);
+        int base = 0;
+        if (lane_id() == 0 && ball) base = atomicAdd(&S.side_n, __popc(ball));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (keep_it) {
+            const int p = base + __popc(ball & ((1u << lane_id()) - 1u));
+            B.sd_lt[p] = x;
+            B.sd_slot[p] = B.st_slot[j];
+            B.sd_list[p] = l;
+        }
+    }
+    __syncthreads();
+    const int n2 = S.side_n;
+    for (int j = tid; j < n2; j += T) {
+        B.st_lt[j] = B.sd_lt[j];
+        B.st_slot[j] = B.sd_slot[j];
+        B.st_list[j] = B.sd_list[j];
+    }
+    __syncthreads();
+    if (tid == 0) S.count = n2;
+    __syncthreads();
+}
+
 __device__ void stage_flush(const DevPool& P, int NL, int keep, const ScanBufs& B, ScanSmem& S, SelectSmem& Sel,
                             bool final_flush) {
     const int tid = threadIdx.x, T = blockDim.x;
     const int m = S.count;
     const unsigned long long t_in = tid == 0 ? gtimer() : 0ull;
+    if (m <= kRankSelectMax) {
+        stage_flush_rank(P, NL, keep, B, S, final_flush);
+        if (tid == 0) {
+            S.flush_ns += gtimer() - t_in;
+            S.flushes += 1;
+        }
+        return;
+    }
     if (tid < NL) S.lcnt[tid] = 0;
     __syncthreads();
     for (int j0 = 0; j0 < m; j0 += T) {  // per-list counts, aggregated per warp (match_any)
@@ -633,14 +696,22 @@ __device__ void scan_pass(const DevPool& P, int NL, int keep, const ScanBufs& B,
         S.gbw[tid] = ld_relaxed_u64(P.gbound + tid);
         S.wcnt[tid] = 0;
         S.wpos[tid] = 0;
+        S.lmin[tid] = kNoBound;
     }
     __syncthreads();
     const int m = S.count;
     const int T = blockDim.x;
-    for (int j = tid; j < m; j += T)
-        if (B.st_lt[j] <= S.gbw[B.st_list[j]]) atomicAdd(&S.wcnt[B.st_list[j]], 1);
+    for (int j = tid; j < m; j += T) {
+        const unsigned char l = B.st_list[j];
+        atomicMin(&S.lmin[l], B.st_lt[j]);
+        if (B.st_lt[j] <= S.gbw[l]) atomicAdd(&S.wcnt[l], 1);
+    }
     __syncthreads();
-    if (tid < NL) S.wbase[tid] = S.wcnt[tid] ? atomicAdd(P.gcount + tid, S.wcnt[tid]) : 0;
+    if (tid < NL) {
+        S.wbase[tid] = S.wcnt[tid] ? atomicAdd(P.gcount + tid, S.wcnt[tid]) : 0;
+        // this CTA's smallest candidate: the select bound is the keep-th smallest CTA minimum
+        P.gmin[(long long)tid * gridDim.x + blockIdx.x] = S.lmin[tid];
+    }
     __syncthreads();
     for (int j = tid; j < m; j += T) {
         const unsigned char l = B.st_list[j];
@@ -663,24 +734,52 @@ __device__ void finalize_list(const DevPool& P, int l, int NL, int keep, const S
     const int m = *(volatile int*)(P.gcount + l);
     const unsigned long long* g = P.gbuf_lt + (long long)l * P.gcap;
     const unsigned int* gs = P.gbuf_slot + (long long)l * P.gcap;
-    // stage the candidates on chip when they fit (the common case), else select from L2
-    const bool local = m <= kStage;
-    if (local) {
-        for (int j = tid; j < m; j += T) {
-            B.st_lt[j] = g[j];
-            B.st_slot[j] = gs[j];
-        }
-        __syncthreads();
+    // Pre-filter bound: the kl-th smallest of the CTAs' minima. At most kl CTAs can have a
+    // minimum below the global kl-th smallest value v* (each such minimum is a distinct element
+    // <= v*), so this bound is >= v* and keeps the whole answer, and at least kl written
+    // candidates are <= it. It cuts the ~grid*kl written candidates to ~kl.
+    const int G = gridDim.x;
+    unsigned long long* mins = B.sd_lt;  // G <= kSide minima staged on chip
+    if (tid == 0) {
+        Sel.tmp = 0;
+        Sel.prefix = kNoBound;
     }
+    for (int i = tid; i < G; i += T) mins[i] = P.gmin[(long long)l * G + i];
+    __syncthreads();
+    for (int i = tid; i < G; i += T) {
+        const unsigned long long x = mins[i];
+        if (x >= kNoBound) continue;  // that CTA had no candidate of this list
+        int r = 0;
+        for (int k = 0; k < G; ++k) r += mins[k] < x;  // CTA minima are distinct ticks
+        if (r == kl - 1) Sel.prefix = x;
+    }
+    __syncthreads();
+    const unsigned long long fb = Sel.prefix;
+    // stage the filtered candidates on chip when they fit (the common case), else select from L2
+    for (int j = tid; j < m; j += T) {
+        const unsigned long long x = g[j];
+        if (x <= fb) {
+            const int p = atomicAdd(&Sel.tmp, 1);
+            if (p < kStage) {
+                B.st_lt[p] = x;
+                B.st_slot[p] = gs[j];
+            }
+        }
+    }
+    __syncthreads();
+    const int mf = Sel.tmp;
+    const bool local = mf <= kStage;
     const unsigned long long* src = local ? B.st_lt : g;
     const unsigned int* srs = local ? B.st_slot : gs;
+    const int ms = local ? mf : m;
+    __syncthreads();
     unsigned long long v = ~0ull;
-    if (m > kl) v = block_kth(src, nullptr, 0, m, kl, Sel);
+    if (ms > kl) v = block_kth(src, nullptr, 0, ms, kl, Sel);
     unsigned long long* t_lt = B.sd_lt;
     unsigned int* t_slot = B.sd_slot;
     if (tid == 0) Sel.tmp = 0;
     __syncthreads();
-    for (int j = tid; j < m; j += T) {
+    for (int j = tid; j < ms; j += T) {
         const unsigned long long x = src[j];
         if (x <= v) {
             const int p = atomicAdd(&Sel.tmp, 1);
@@ -690,40 +789,17 @@ __device__ void finalize_list(const DevPool& P, int l, int NL, int keep, const S
     }
     __syncthreads();
     const int n = Sel.tmp;
-    for (int j = tid; j < 256; j += T)
-        if (j >= n) {
-            t_lt[j] = ~0ull;
-            t_slot[j] = kNoSlot;
-        }
-    __syncthreads();
-    for (int k = 2; k <= 256; k <<= 1) {
-        for (int jj = k >> 1; jj > 0; jj >>= 1) {
-            for (int i = tid; i < 256; i += T) {
-                const int ixj = i ^ jj;
-                if (ixj > i) {
-                    const bool asc = (i & k) == 0;
-                    const unsigned long long a = t_lt[i], b = t_lt[ixj];
-                    if ((a > b) == asc) {
-                        t_lt[i] = b;
-                        t_lt[ixj] = a;
-                        const unsigned int sa = t_slot[i];
-                        t_slot[i] = t_slot[ixj];
-                        t_slot[ixj] = sa;
-                    }
-                }
-            }
-            __syncthreads();
-        }
-    }
+    // rank sort of the (at most keep + 1) survivors: distinct ticks, one barrier
     for (int j = tid; j < n; j += T) {
-        P.fin_lt[(long long)l * (kChunk + 2) + j] = t_lt[j];
-        P.fin_slot[(long long)l * (kChunk + 2) + j] = t_slot[j];
+        const unsigned long long x = t_lt[j];
+        int r = 0;
+        for (int k = 0; k < n; ++k) r += t_lt[k] < x;
+        P.fin_lt[(long long)l * (kChunk + 2) + r] = x;
+        P.fin_slot[(long long)l * (kChunk + 2) + r] = t_slot[j];
     }
     if (tid == 0) {
         P.fin_n[l] = n;
-        // Hint verification: a list that came up short while some member was rejected only by
-        // its hint may be missing candidates -> the whole pass is redone without hints.
-        // Hints are only carried for lists that were full (n == keep) in the previous scan; a
+        // Hint verification. Hints are only carried for lists that were full (n == keep) in the previous scan; a
         // hinted list that now comes up short may be missing members above its hint.
         const bool hinted = P.ghint[l] < kNoBound;
         if (n < kl && hinted) atomicExch(&P.ctrl->rescan, 1);
@@ -794,78 +870,41 @@ __device__ void replay_apply(const DevPool& P, const AdmitArgs& a, ReplaySmem& R
         }
     }
     __syncthreads();
-    // per list entry: prompt index (touch removes it) and resident-list position (eviction
-    // from a class list also removes it from the resident list)
-    const int nres = R.L_n[Rl];
-    for (int l = 0; l < NL; ++l) {
-        const int n = R.L_n[l];
-        for (int j = tid; j < n; j += T) {
-            const unsigned int s = R.L_slot[l][j];
-            short pi = -1;
-            unsigned int h = hslot(s);
-            for (int c = 0; c < 512; ++c) {
-                const unsigned int k = R.ph_key[h];
-                if (k == kNoSlot) break;
-                if (k == s) {
-                    pi = R.ph_val[h];
-                    break;
-                }
-                h = (h + 1) & 511u;
-            }
-            R.L_pidx[l][j] = pi;
-            short rp = -1;
-            if (l == Rl) {
-                rp = (short)j;
-            } else {
-                const unsigned long long x = R.L_lt[l][j];
-                int lo2 = 0, hi2 = nres;  // binary search by the unique last_touch
-                while (lo2 < hi2) {
-                    const int mid = (lo2 + hi2) >> 1;
-                    if (R.L_lt[Rl][mid] < x) lo2 = mid + 1;
-                    else hi2 = mid;
-                }
-                if (lo2 < nres && R.L_lt[Rl][lo2] == x) rp = (short)lo2;
-            }
-            R.L_rpos[l][j] = rp;
-        }
-    }
-    __syncthreads();
-    // Dominance prefix. Within an admission `now` only grows and oldest_live_touch never
-    // decreases, so rho(lt) of a fixed block only shrinks (exact ratio shrinks, rounding is
-    // monotone). A class-E (survival 0, score = rho) entry whose rho at the replay-start context
-    // is < min over the other non-empty classes of w_pred*S_c therefore beats every other class
-    // head at every later eviction of this chunk: score_c >= fl(w_pred*S_c) > rho_E. Since rho
-    // grows with lt along the sorted list, those entries form a prefix.
-    {
-        const int E = P.e_max;
-        double bound = __longlong_as_double(0x7ff0000000000000ll);  // +inf: no other class
-        bool ok = true;
-        if (P.policy == 1) {
-            if (!(P.w_pred > 0.0)) ok = false;
-            for (int c = 0; c < E; ++c)
-                if (R.L_n[c] > 0) bound = fmin(bound, __dmul_rn(P.w_pred, survival_of_class(c, E)));
-        }
-        const unsigned long long tick0 = A.tick;
-        unsigned long long old0 = tick0;
-        if (R.L_n[Rl] > 0 && R.L_lt[Rl][0] < old0) old0 = R.L_lt[Rl][0];
-        if (A.first_touch < old0) old0 = A.first_touch;
-        const int nE = R.L_n[E];
-        long long first_fail = ok ? nE : 0;
-        for (int j = tid; ok && j < nE; j += T) {
-            const double rho = recency(R.L_lt[E][j], tick0, old0);
-            if (!(rho < bound)) first_fail = min(first_fail, (long long)j);
-        }
-        first_fail = block_min(first_fail, Red);
-        if (tid == 0) R.pdom = (int)first_fail;
-    }
-    __syncthreads();
     // Bulk replay (the common case, no serial loop): when the victims are the first n_ev
-    // class-E candidates, all inside the dominance prefix and none of them a prompt block of
-    // this chunk, the sequential replay reduces to: absent block of rank r takes a free slot
-    // while the pool is below budget, else the next class-E candidate; every block is touched
-    // once in prompt order (tick0 + 1 + i).
+    // class-E candidates, all inside the dominance prefix (below) and none of them a prompt
+    // block of this chunk, the sequential replay reduces to: the absent block of rank r takes a
+    // free slot while the pool is below budget, else the next class-E candidate; every block is
+    // touched once in prompt order (tick0 + 1 + i).
+    //
+    // Dominance: within an admission `now` only grows and oldest_live_touch never decreases,
+    // so rho(lt) of a fixed block only shrinks (the exact ratio shrinks, rounding is monotone).
+    // A class-E (survival 0, score = rho) entry whose rho at the replay-start context is below
+    // min over the other non-empty classes of fl(w_pred*S_c) therefore beats every other class
+    // head at every later eviction of this chunk (score_c >= fl(w_pred*S_c) > rho_E); rho grows
+    // with lt along the sorted list, so those entries form a prefix [0, pdom).
+    const int E = P.e_max;
+    double dom_bound = __longlong_as_double(0x7ff0000000000000ll);  // +inf: no other class
+    bool dom_ok = true;
+    if (P.policy == 1) {
+        if (!(P.w_pred > 0.0)) dom_ok = false;
+        for (int c = 0; c < E; ++c)
+            if (R.L_n[c] > 0) dom_bound = fmin(dom_bound, __dmul_rn(P.w_pred, survival_of_class(c, E)));
+    }
+    const unsigned long long tick0 = A.tick;
+    unsigned long long old0 = tick0;
+    if (R.L_n[Rl] > 0 && R.L_lt[Rl][0] < old0) old0 = R.L_lt[Rl][0];
+    if (A.first_touch < old0) old0 = A.first_touch;
+    auto prompt_index = [&](unsigned int s) -> short {
+        unsigned int h = hslot(s);
+        for (int c = 0; c < 512; ++c) {
+            const unsigned int k = R.ph_key[h];
+            if (k == kNoSlot) return -1;
+            if (k == s) return R.ph_val[h];
+            h = (h + 1) & 511u;
+        }
+        return -1;
+    };
     {
-        const int E = P.e_max;
         const long long res0 = C->resident;
         int absent = 0, pre_unpinned = 0;
         for (int i = tid; i < len; i += T) {
@@ -877,10 +916,11 @@ __device__ void replay_apply(const DevPool& P, const AdmitArgs& a, ReplaySmem& R
         const long long room = P.cap - res0;
         const int n_free = (int)min((long long)absent, room > 0 ? room : 0ll);
         const int n_ev = absent - n_free;
-        int clash = 0;  // a needed victim is one of this chunk's prompt blocks
-        for (int j = tid; j < n_ev && j < R.L_n[E]; j += T) clash |= R.L_pidx[E][j] >= 0;
-        clash = __syncthreads_or(clash);
-        const bool bulk = n_ev <= R.pdom && !clash;
+        int bad = n_ev > R.L_n[E] || (n_ev > 0 && !dom_ok);
+        // a needed victim that is one of this chunk's prompt blocks, or outside the prefix
+        for (int j = tid; !bad && j < n_ev; j += T) bad |= prompt_index(R.L_slot[E][j]) >= 0;
+        if (!bad && tid == 0 && n_ev > 0) bad = !(recency(R.L_lt[E][n_ev - 1], tick0, old0) < dom_bound);
+        const bool bulk = !__syncthreads_or(bad);
         if (bulk) {
             // exclusive rank of each absent block (len <= kChunk = 128: 4 warps)
             __shared__ int wsum[kChunk / 32];
@@ -921,6 +961,41 @@ __device__ void replay_apply(const DevPool& P, const AdmitArgs& a, ReplaySmem& R
             }
         }
         if (tid == 0) R.bulk = bulk ? 1 : 0;
+        __syncthreads();
+    }
+    if (!R.bulk) {
+        // serial path: per list entry, the prompt index (a touch removes it) and the position in
+        // the resident list (an eviction from a class list removes it there too); pdom in full
+        const int nres = R.L_n[Rl];
+        for (int l = 0; l < NL; ++l) {
+            const int n = R.L_n[l];
+            for (int j = tid; j < n; j += T) {
+                const unsigned int s = R.L_slot[l][j];
+                R.L_pidx[l][j] = prompt_index(s);
+                short rp = -1;
+                if (l == Rl) {
+                    rp = (short)j;
+                } else {
+                    const unsigned long long x = R.L_lt[l][j];
+                    int lo2 = 0, hi2 = nres;  // binary search by the unique last_touch
+                    while (lo2 < hi2) {
+                        const int mid = (lo2 + hi2) >> 1;
+                        if (R.L_lt[Rl][mid] < x) lo2 = mid + 1;
+                        else hi2 = mid;
+                    }
+                    if (lo2 < nres && R.L_lt[Rl][lo2] == x) rp = (short)lo2;
+                }
+                R.L_rpos[l][j] = rp;
+            }
+        }
+        const int nE = R.L_n[E];
+        long long first_fail = dom_ok ? nE : 0;
+        for (int j = tid; dom_ok && j < nE; j += T) {
+            const double rho = recency(R.L_lt[E][j], tick0, old0);
+            if (!(rho < dom_bound)) first_fail = min(first_fail, (long long)j);
+        }
+        first_fail = block_min(first_fail, Red);
+        if (tid == 0) R.pdom = (int)first_fail;
         __syncthreads();
     }
     stamp(A, 6);
@@ -1067,14 +1142,10 @@ __device__ void replay_apply(const DevPool& P, const AdmitArgs& a, ReplaySmem& R
     const int nv = R.n_vict;
     // ---- apply: victims first (erase key, free slot), then inserts and touches
     const unsigned long long ev0 = C->n_ev;
+    // victim keys first (a reused victim slot is rewritten below)
     for (int k = tid; k < nv; k += T) {
         const unsigned int v = R.victims[k];
-        const unsigned long long kk = P.key[v];
-        table_erase(P, kk);
-        P.evlog[(ev0 + k) % (unsigned long long)P.evlog_cap] = kk;  // ring; the host drains it
-        P.lt[v] = kFreeTick;
-        P.refs[v] = 0u;
-        P.agent[v] = kNoAgent;
+        R.vkey[k] = P.key[v];
         unsigned int h = hslot(v);
         for (int c = 0; c < 512; ++c) {
             if (atomicCAS(&R.vh_key[h], kNoSlot, v) == kNoSlot) break;
@@ -1082,6 +1153,21 @@ __device__ void replay_apply(const DevPool& P, const AdmitArgs& a, ReplaySmem& R
         }
     }
     __syncthreads();
+    for (int k = tid; k < nv; k += T) {
+        const unsigned long long kk = R.vkey[k];
+        table_erase(P, kk);
+        P.evlog[(ev0 + k) % (unsigned long long)P.evlog_cap] = kk;  // ring; the host drains it
+        if (k >= R.n_reused) {  // victims[0, n_reused) are overwritten by new blocks below
+            const unsigned int v = R.victims[k];
+            P.lt[v] = kFreeTick;
+            P.refs[v] = 0u;
+            P.agent[v] = kNoAgent;
+        }
+    }
+    // Bulk chunks never re-insert a key they evicted (their victims are not prompt blocks of
+    // the chunk), so erases and inserts touch distinct keys and run in one round; the serial
+    // path may evict a later prompt block and re-insert it, so it orders the two rounds.
+    if (!R.bulk) __syncthreads();
     long long reused_tomb = 0;
     const int done_len = err ? 0 : len;  // an erroring chunk is not applied
     for (int i = tid; i < done_len; i += T) {
@@ -1157,7 +1243,7 @@ __device__ void write_status(const DevPool& P, const AdmitArgs& a, const AdmSmem
         st->pend_target[k] = C->pend_target[k];
         st->pend_tick[k] = C->pend_tick[k];
     }
-    __threadfence_system();
+    // no system fence: the host reads the mapped record only after the launch completes
 }
 
 __global__ void __launch_bounds__(kThreads + 32, 1) admit_kernel(DevPool P, AdmitArgs a) {
@@ -1247,12 +1333,32 @@ __global__ void __launch_bounds__(kThreads + 32, 1) admit_kernel(DevPool P, Admi
         stamp(A, 0);
     }
 
-    // ---- chunk loop: prep (CTA 0) | scan (all) | select (one CTA per list) | replay (CTA 0)
+    // ---- command loop. CTA 0 decides the next step (scan pass of a chunk, or done); every CTA
+    // scans; CTAs 0..NL-1 select one list each; only CTA 0 consumes the lists, so it waits on
+    // a counter instead of a grid barrier; CTA 0 replays. Per chunk: 2 grid barriers.
+    bool pending_rescan = false;  // CTA 0: the last pass must be redone (safe, no hints)
     for (;;) {
         if (blockIdx.x == 0) {
             const bool stop = !A.started || A.error || A.chunk * kChunk >= A.admit_n;
             if (stop) {
                 if (tid == 0) C->done = 1;
+            } else if (pending_rescan) {
+                // a hint was too tight (or the fast pass overflowed): same chunk, safe pass
+                if (tid < NL) {
+                    P.ghint[tid] = kNoBound;
+                    P.gbound[tid] = kNoBound;
+                    P.gcount[tid] = 0;
+                    P.gmaxk[tid] = 0ull;
+                }
+                if (tid == 0) {
+                    C->rescan = 0;
+                    C->fin_done = 0u;
+                    C->pass = 1;
+                    C->fast = 0;
+                    C->need_scan = 1;
+                    C->rescans += 1;
+                    A.ph[13] += 1;
+                }
             } else {
                 const int lo = A.chunk * kChunk, hi = min(A.admit_n, lo + kChunk);
                 long long absent = 0;
@@ -1264,14 +1370,13 @@ __global__ void __launch_bounds__(kThreads + 32, 1) admit_kernel(DevPool P, Admi
                     P.gcount[tid] = 0;
                     P.gmaxk[tid] = 0ull;
                 }
+                // warp-specialized pass only when every list has a hint or is known small
+                const int slow = __syncthreads_or(tid < NL && !(P.ghint[tid] < kNoBound) && !P.gsmall[tid]);
                 if (tid == 0) {
-                    *P.grej = 0u;
                     C->rescan = 0;
-                    // warp-specialized pass only when every list has a hint or is known small
-                    int fast = 1;
-                    for (int l = 0; l < NL; ++l)
-                        if (!(P.ghint[l] < kNoBound) && !P.gsmall[l]) fast = 0;
-                    C->fast = fast;
+                    C->fin_done = 0u;
+                    C->pass = 0;
+                    C->fast = slow ? 0 : 1;
                     C->need_scan = need_scan;
                     C->keep = hi - lo;
                     if (need_scan) {
@@ -1281,7 +1386,6 @@ __global__ void __launch_bounds__(kThreads + 32, 1) admit_kernel(DevPool P, Admi
                     }
                 }
             }
-            __threadfence();
         }
         grid_barrier(C);
         stamp(A, 1);
@@ -1289,41 +1393,43 @@ __global__ void __launch_bounds__(kThreads + 32, 1) admit_kernel(DevPool P, Admi
         const int need_scan = *(volatile int*)&C->need_scan;
         const int keep = *(volatile int*)&C->keep;
         if (need_scan) {
+            const int pass = *(volatile int*)&C->pass;
             for (int x = tid; x < a.n_agents; x += T) B.cls[x] = P.cls[x];
             __syncthreads();
-            for (int pass = 0; pass < 2; ++pass) {
-                scan_pass(P, NL, keep, B, S, Sel, dsm, pass == 0 && *(volatile int*)&C->fast);
-                if (blockIdx.x == 0 && tid == 0) {
-                    A.ph[9] += S.flush_ns;
-                    A.ph[10] += S.flushes;
+            scan_pass(P, NL, keep, B, S, Sel, dsm, pass == 0 && *(volatile int*)&C->fast);
+            if (blockIdx.x == 0 && tid == 0) {
+                A.ph[9] += S.flush_ns;
+                A.ph[10] += S.flushes;
+            }
+            grid_barrier(C);
+            if (tid == 0) P.dbg[blockIdx.x * 16 + 4] = gtimer();
+            stamp(A, 2);
+            int mine = 0;
+            for (int l = blockIdx.x; l < NL; l += gridDim.x) {
+                finalize_list(P, l, NL, keep, B, Sel);
+                ++mine;
+            }
+            if (blockIdx.x != 0) {
+                if (tid == 0 && mine) {
+                    __threadfence();
+                    atomicAdd(&C->fin_done, (unsigned int)mine);
                 }
-                grid_barrier(C);
-                if (tid == 0) P.dbg[blockIdx.x * 16 + 4] = gtimer();
-                stamp(A, 2);
-                for (int l = blockIdx.x; l < NL; l += gridDim.x) finalize_list(P, l, NL, keep, B, Sel);
-                grid_barrier(C);
-                stamp(A, 3);
-                // C->rescan is only cleared by the next chunk's prep, after every CTA read it
-                if (pass == 1 || !*(volatile int*)&C->rescan) break;
-                // a hint was too tight for some list: redo the pass with no hints (exact)
-                if (blockIdx.x == 0) {
-                    if (tid < NL) {
-                        P.ghint[tid] = kNoBound;
-                        P.gbound[tid] = kNoBound;
-                        P.gcount[tid] = 0;
-                        P.gmaxk[tid] = 0ull;
-                    }
-                    if (tid == 0) {
-                        *P.grej = 0u;
-                        C->rescans += 1;
-                        A.ph[13] += 1;
+            } else {
+                if (tid == 0) {  // CTA 0 waits for the other lists' selects
+                    const unsigned int want = (unsigned int)(NL - mine);
+                    unsigned long long spins = 0;
+                    while (ld_acquire(&C->fin_done) < want) {
+                        if (++spins > 4096) __nanosleep(64);
+                        if (spins > (1ull << 27)) __trap();
                     }
                     __threadfence();
                 }
-                grid_barrier(C);
+                __syncthreads();
+                stamp(A, 3);
+                pending_rescan = pass == 0 && *(volatile int*)&C->rescan;
             }
         }
-        if (blockIdx.x == 0) {
+        if (blockIdx.x == 0 && !pending_rescan) {
             replay_apply(P, a, Rp, A, NL, need_scan != 0, Red);
             if (tid == 0) A.chunk += 1;
             __syncthreads();

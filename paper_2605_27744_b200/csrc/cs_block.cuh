@@ -13,6 +13,7 @@ __device__ __forceinline__ int warp_id() { return threadIdx.x >> 5; }
 struct RedSmem {
     long long v[32];
     unsigned long long u[32];
+    unsigned long long w[32];
 };
 
 __device__ __forceinline__ long long block_sum(long long x, RedSmem& R) {

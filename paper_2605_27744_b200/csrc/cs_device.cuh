@@ -73,6 +73,8 @@ struct Ctrl {
     int error;
     int rescan;        // a hinted list came up short: scan again without hints
     int fast;          // this chunk's first scan pass runs warp-specialized (no per-tile barrier)
+    unsigned int fin_done;  // lists finalized in this pass (CTA 0 waits for all, no grid barrier)
+    int pass;          // scan pass of the current chunk (1 = safe, no hints)
     long long rescans; // instrumentation
 };
 
@@ -116,6 +118,7 @@ struct DevPool {
     unsigned long long* gmaxk;    // [kMaxLists] max over CTAs of their local keep-th value
     unsigned int* grej;           // unused (kept for layout stability)
     unsigned char* gsmall;        // [kMaxLists] list had fewer than keep members in its last scan
+    unsigned long long* gmin;     // [kMaxLists][grid] each CTA's smallest candidate per list (kNoBound: none)
     unsigned long long* gbuf_lt;  // [kMaxLists][gcap]
     unsigned int* gbuf_slot;
     long long gcap;
@@ -166,8 +169,10 @@ __device__ __forceinline__ int table_insert(const DevPool& P, unsigned long long
         if (s == kSlotEmpty || s == kSlotTomb) {
             unsigned int old = atomicCAS(&P.table[h].slot, s, kSlotClaim);
             if (old == s) {
+                // Concurrent inserters only read slot words (a CLAIM entry is skipped); lookups
+                // run in later phases, ordered by the grid barrier / kernel boundary, so no
+                // fence is needed between the key write and the slot publish.
                 P.table[h].key = key;
-                __threadfence();
                 atomicExch(&P.table[h].slot, slot);
                 return s == kSlotTomb ? 1 : 0;
             }

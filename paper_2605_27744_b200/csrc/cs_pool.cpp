@@ -122,6 +122,7 @@ void cs_pool::create(const cs_pool_cfg& c) {
     p.gcap = (long long)lc.grid * (csb::kChunk + 1);
     p.gbuf_lt = dmalloc<unsigned long long>((size_t)csb::kMaxLists * p.gcap, "gbuf_lt");
     p.gbuf_slot = dmalloc<unsigned int>((size_t)csb::kMaxLists * p.gcap, "gbuf_slot");
+    p.gmin = dmalloc<unsigned long long>((size_t)csb::kMaxLists * lc.grid, "gmin");
     p.dbg = dmalloc<unsigned long long>((size_t)lc.grid * 16, "dbg");
     ck(cudaMemsetAsync(p.dbg, 0, sizeof(unsigned long long) * lc.grid * 16, stream), "memset");
 
@@ -136,7 +137,7 @@ void cs_pool::destroy() {
     csb::DevPool& p = P;
     void* ptrs[] = {p.lt, p.agent, p.refs, p.key, p.tokens, p.table, p.free_stack, p.evlog, p.counts, p.totals,
                     p.win_a, p.win_b, p.hop, p.cls, p.agent_ids, p.ctrl, p.gbound, p.gcount, p.fin_lt, p.fin_slot,
-                    p.fin_n, p.p_slot, p.p_refs0, p.gbuf_lt, p.gbuf_slot, p.ghint, p.gmaxk, p.grej, p.dbg, p.gsmall};
+                    p.fin_n, p.p_slot, p.p_refs0, p.gbuf_lt, p.gbuf_slot, p.ghint, p.gmaxk, p.grej, p.dbg, p.gsmall, p.gmin};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     d_keys.release();
