@@ -49,15 +49,21 @@ def dist_env():
 
 
 class Dist:
-    def __init__(self, world, rank, local):
+    """One process per GPU. NCCL on the box; `gloo` (CPU tensors) for the multi-process tests.
+    There is no data-path collective: only the barrier and the max/sum of the timing counters."""
+
+    def __init__(self, world, rank, local, backend="nccl"):
         self.world, self.rank, self.local = world, rank, local
-        self.pg = None
+        self.dev = "cuda" if backend == "nccl" else "cpu"
         if world > 1:
             import torch
             import torch.distributed as td
 
-            torch.cuda.set_device(local)
-            td.init_process_group("nccl", device_id=torch.device("cuda", local))
+            if backend == "nccl":
+                torch.cuda.set_device(local)
+                td.init_process_group("nccl", device_id=torch.device("cuda", local))
+            elif not td.is_initialized():
+                td.init_process_group(backend, rank=rank, world_size=world)
             self.td, self.torch = td, torch
 
     def barrier(self):
@@ -67,14 +73,14 @@ class Dist:
     def max(self, x):
         if self.world == 1:
             return x
-        t = self.torch.tensor([float(x)], device="cuda")
+        t = self.torch.tensor([float(x)], dtype=self.torch.float64, device=self.dev)
         self.td.all_reduce(t, op=self.td.ReduceOp.MAX)
         return float(t.item())
 
     def sum(self, x):
         if self.world == 1:
             return x
-        t = self.torch.tensor([float(x)], device="cuda")
+        t = self.torch.tensor([float(x)], dtype=self.torch.float64, device=self.dev)
         self.td.all_reduce(t, op=self.td.ReduceOp.SUM)
         return float(t.item())
 
@@ -165,11 +171,25 @@ def build_engine(W, spec, pool, device, host_inputs, seed):
     return eng
 
 
+def rank_workload(sessions, pool, rank):
+    """Rank r's partition of the job: its own cfg4 trace (seed offset by rank) against its own
+    pool shard and snapshot. Per-GPU work is fixed as N grows ("scaling": weak)."""
+    from paper_2605_27744_b200 import workloads as W
+
+    return W.cfg4_mixed(sessions=sessions, budget=pool, seed=2608 + 7919 * rank), 11 + rank
+
+
+def aggregate(dist, ms, scanned):
+    """Whole-job metric: units all ranks processed / the slowest rank's device time."""
+    tot_ms = dist.max(sum(ms))
+    return dist.sum(scanned) / (tot_ms / 1e3), tot_ms
+
+
 def run_ours(args, dist):
     from paper_2605_27744_b200 import workloads as W
 
     pool = args.pool
-    spec = W.cfg4_mixed(sessions=args.sessions, budget=pool, seed=2608 + 7919 * dist.rank)
+    spec, snap_seed = rank_workload(args.sessions, pool, dist.rank)
     R = args.admissions_per_step
 
     def timed_run(eng, steps):
@@ -183,32 +203,28 @@ def run_ours(args, dist):
         return ms
 
     # ---- value: inputs resident in HBM
-    eng = build_engine(W, spec, pool, dist.local, False, seed=11 + dist.rank)
+    eng = build_engine(W, spec, pool, dist.local, False, seed=snap_seed)
     timed_run(eng, args.warmup)
     r0 = eng.result()
     with ClockSampler(dist.local) as clk:
         ms = timed_run(eng, args.steps)
     r1 = eng.result()
-    tot_ms = dist.max(sum(ms))
-    scanned = dist.sum(r1["scanned_slots"] - r0["scanned_slots"])
+    value, tot_ms = aggregate(dist, ms, r1["scanned_slots"] - r0["scanned_slots"])
     evicted = dist.sum(r1["evictions"] - r0["evictions"])
     adm = dist.sum(r1["admissions"] - r0["admissions"])
     launches = dist.sum(r1["gpu_launches"] - r0["gpu_launches"])
     scan_launches = r1["scan_launches"] - r0["scan_launches"]
     scan_ms = r1["scan_ms"] - r0["scan_ms"]
-    value = scanned / (tot_ms / 1e3)
     hit = r1["hit_rate"]
     eng.close()
 
     # ---- e2e: host inputs, H2D per admission, victims D2H per admission
-    eng = build_engine(W, spec, pool, dist.local, True, seed=11 + dist.rank)
+    eng = build_engine(W, spec, pool, dist.local, True, seed=snap_seed)
     timed_run(eng, args.warmup)
     e0 = eng.result()
     ems = timed_run(eng, args.steps)
     e1 = eng.result()
-    e_tot_ms = dist.max(sum(ems))
-    e_scanned = dist.sum(e1["scanned_slots"] - e0["scanned_slots"])
-    e2e_value = e_scanned / (e_tot_ms / 1e3)
+    e2e_value, _ = aggregate(dist, ems, e1["scanned_slots"] - e0["scanned_slots"])
     h2d = (e1["h2d_bytes"] - e0["h2d_bytes"]) / args.steps
     d2h = (e1["d2h_bytes"] - e0["d2h_bytes"]) / args.steps
     eng.close()
