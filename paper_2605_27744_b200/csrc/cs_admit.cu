@@ -37,8 +37,10 @@ constexpr int kSide = kMaxLists * (kChunk + 1);
 
 // ------------------------------------------------------------------ shared state
 
+constexpr int kPend = kMaxLists;  // staged agent-carrying slot whose class phase 0 has not fixed yet
+
 struct ScanSmem {
-    unsigned long long thr[kMaxLists];  // inclusive acceptance bound per list
+    unsigned long long thr[kMaxLists + 1];  // inclusive acceptance bound per list (+ kPend)
     unsigned long long gbw[kMaxLists];
     int count;                          // staged entries
     int side_n;
@@ -48,6 +50,10 @@ struct ScanSmem {
     unsigned long long hint[kMaxLists];
     unsigned long long lmin[kMaxLists];
     int overflow;
+    int spec;       // speculative pass: phase 0 runs concurrently on CTA 0
+    int hc, dc;     // ensure_cls compaction counters
+    int cls_ready;  // B.cls holds this launch's classes (else kPend for every agent)
+    unsigned int xset[kXset];  // slots phase 0 may change: excluded here, restaged fresh by CTA 0
     __align__(8) unsigned long long mbar[kRing];        // TMA ring: stage filled
     __align__(8) unsigned long long mbar_empty[kRing];  // TMA ring: stage released by all consumers
 };
@@ -563,6 +569,119 @@ __device__ __forceinline__ void read4(const unsigned char* st, int tid, bool val
     }
 }
 
+// ---- speculative pass support: the set of slots phase 0 may change (the prompt's resident
+// blocks, touched by lookup / pinned by admit_pinned, and the slots unpinned first) and the
+// deferred classification of agent-carrying slots (the BFS of phase 0 may move them).
+__device__ __forceinline__ unsigned int xhash(unsigned int s) { return (s * 2654435761u) >> 22; }  // 10 bits
+
+__device__ __forceinline__ bool xset_insert(ScanSmem& S, unsigned int s) {
+    unsigned int h = xhash(s);
+    for (int c = 0; c < kXset; ++c) {
+        const unsigned int old = atomicCAS(&S.xset[h], kNoSlot, s);
+        if (old == kNoSlot) return true;
+        if (old == s) return false;
+        h = (h + 1) & (kXset - 1);
+    }
+    return false;  // unreachable: at most kXsetMax entries
+}
+
+__device__ __forceinline__ bool xset_has(const ScanSmem& S, unsigned int s) {
+    unsigned int h = xhash(s);
+    for (int c = 0; c < kXset; ++c) {
+        const unsigned int k = S.xset[h];
+        if (k == s) return true;
+        if (k == kNoSlot) return false;
+        h = (h + 1) & (kXset - 1);
+    }
+    return false;
+}
+
+// All threads, after this launch's phase 0: the slots it may have changed, from the prompt
+// slots CTA 0 probed (P.p_slot) and the unpin list.
+__device__ void build_xset(const DevPool& P, const AdmitArgs& a, ScanSmem& S) {
+    const int tid = threadIdx.x, T = blockDim.x;
+    for (int j = tid; j < kXset; j += T) S.xset[j] = kNoSlot;
+    __syncthreads();
+    for (int i = tid; i < a.n; i += T) {
+        const unsigned int s = __ldcg(P.p_slot + i);
+        if (s != kNoSlot) xset_insert(S, s);
+    }
+    for (int r = 0; r < a.n_unpin_ranges; ++r)
+        for (int i = tid; i < a.unpin_n[r]; i += T) xset_insert(S, a.unpin_ptr[r][i]);
+    __syncthreads();
+}
+
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// All threads of a scanning CTA, before its first flush (no bound has used a staged entry
+// yet): waits for this launch's phase 0, loads the survival classes it fixed, drops the staged
+// entries of slots phase 0 may have changed (CTA 0 restages those with their new state) and
+// classifies the staged agent-carrying entries (phase 0 never changes a slot's agent).
+__device__ void ensure_cls(const DevPool& P, const AdmitArgs& a, const ScanBufs& B, ScanSmem& S) {
+    if (!S.spec || S.cls_ready) return;
+    const int tid = threadIdx.x, T = blockDim.x;
+    if (tid == 0) {
+        unsigned long long spins = 0;
+        while (ld_acquire_u64(&P.ctrl->p0_seq) != a.seq) {
+            if (++spins > 1024) __nanosleep(128);
+            if (spins > (1ull << 27)) __trap();
+        }
+    }
+    __syncthreads();
+    for (int x = tid; x < a.n_agents; x += T) B.cls[x] = __ldcg(P.cls + x);
+    build_xset(P, a, S);
+    // Relabel, then drop (a) entries of the change set and (b) relabelled entries above their
+    // class's bound: every staged entry then satisfies the bound its list would have applied,
+    // which the hint check of finalize_list relies on. In-place compaction: the holes below the
+    // new count are filled from the survivors above it.
+    constexpr unsigned char kDrop = 0xFF;
+    const int m = S.count;
+    if (tid == 0) {
+        S.side_n = 0;
+        S.hc = 0;
+        S.dc = 0;
+    }
+    __syncthreads();
+    int dropped = 0;
+    for (int j = tid; j < m; j += T) {
+        const unsigned int sl = B.st_slot[j];
+        unsigned char l = B.st_list[j];
+        bool keep_it = !xset_has(S, sl);
+        if (keep_it && l == kPend) l = B.cls[P.agent[sl]];
+        if (keep_it && B.st_lt[j] > S.thr[l]) keep_it = false;
+        B.st_list[j] = keep_it ? l : kDrop;
+        dropped += keep_it ? 0 : 1;
+    }
+    dropped = __reduce_add_sync(0xffffffffu, dropped);
+    if (lane_id() == 0 && dropped) atomicAdd(&S.side_n, dropped);
+    __syncthreads();
+    const int n2 = m - S.side_n;
+    unsigned int* holes = reinterpret_cast<unsigned int*>(B.sd_lt);  // <= m / 2 each
+    unsigned int* donors = holes + kSide;
+    for (int j = tid; j < m; j += T) {
+        const bool d = B.st_list[j] == kDrop;
+        if (j < n2 && d) holes[atomicAdd(&S.hc, 1)] = (unsigned int)j;
+        if (j >= n2 && !d) donors[atomicAdd(&S.dc, 1)] = (unsigned int)j;
+    }
+    __syncthreads();
+    for (int i = tid; i < S.hc; i += T) {
+        const unsigned int h = holes[i], d = donors[i];
+        B.st_lt[h] = B.st_lt[d];
+        B.st_slot[h] = B.st_slot[d];
+        B.st_list[h] = B.st_list[d];
+    }
+    __syncthreads();
+    if (tid == 0) {
+        S.count = n2;
+        S.cls_ready = 1;
+    }
+    __syncthreads();
+}
+
 // One streaming pass over this CTA's contiguous slot range: 16 B per slot read exactly once.
 // The SoA arrives through a kRing-stage TMA ring (cp.async.bulk into shared memory, mbarrier
 // transaction counts), so the loads are independent of the threads' progress.
@@ -572,15 +691,20 @@ __device__ __forceinline__ void read4(const unsigned char* st, int tid, bool val
 //         overflow aborts the pass and the caller redoes it in safe mode.
 //   safe: one CTA barrier per tile decides whether the staging pool must be flushed (exact
 //         per-list select) before it could overflow; any threshold state works.
+//   spec: (either of the above) runs while CTA 0 is still in phase 0; see ensure_cls.
 // Returns with S.overflow set when a fast pass overflowed.
 __device__ void scan_pass(const DevPool& P, int NL, int keep, const ScanBufs& B, ScanSmem& S, SelectSmem& Sel,
-                          unsigned char* dsm, bool fast) {
+                          unsigned char* dsm, bool fast, const AdmitArgs& a) {
     const int tid = threadIdx.x;
     const long long TV = kTile;  // consumer threads (kThreads) x kV slots
-    long long per = (P.cap_scan + gridDim.x - 1) / gridDim.x;
+    // speculative pass: CTA 0 runs phase 0 and restages the change set instead of a range
+    const bool spec = S.spec != 0;
+    const int nscan = spec ? (int)gridDim.x - 1 : (int)gridDim.x;
+    const int me = spec ? (int)blockIdx.x - 1 : (int)blockIdx.x;
+    long long per = (P.cap_scan + nscan - 1) / nscan;
     per = (per + kV - 1) / kV * kV;
-    const long long lo = min(P.cap_scan, (long long)blockIdx.x * per);
-    const long long hi = min(P.cap_scan, lo + per);  // multiple of 4 slots: 16-B granules
+    const long long lo = me < 0 ? 0 : min(P.cap_scan, (long long)me * per);
+    const long long hi = me < 0 ? 0 : min(P.cap_scan, lo + per);  // multiple of 4 slots: 16-B granules
     const int ntiles = (int)((hi - lo + TV - 1) / TV);
     const int R = NL - 1;
     const int E = P.e_max;  // class of agentless / unreachable blocks (survival 0)
@@ -602,6 +726,12 @@ __device__ void scan_pass(const DevPool& P, int NL, int keep, const ScanBufs& B,
             mbar_init(&S.mbar_empty[s], (unsigned int)(kThreads / 32));
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (tid == 0) {  // an unclassified agent slot may land in any survival class
+        unsigned long long m = 0ull;
+        for (int c = 0; c + 1 < NL; ++c) m = max(m, S.thr[c]);
+        S.thr[kPend] = m;
     }
     __syncthreads();
     auto issue = [&](int t) {  // one elected thread
@@ -648,7 +778,7 @@ __device__ void scan_pass(const DevPool& P, int NL, int keep, const ScanBufs& B,
                 __syncwarp();
                 if (lane_id() == 0) mbar_arrive(&S.mbar_empty[s]);  // stage s consumed by this warp
                 int cl[kV];
-                const unsigned int acc = classify4(x4, a4, r4, thr[R], thr[E], thr, cls, E, cl);
+                unsigned int acc = classify4(x4, a4, r4, thr[R], thr[E], thr, cls, E, cl);
                 append4(acc, x4, cl, i0, R, B, S, true);
             }
         }
@@ -674,12 +804,15 @@ __device__ void scan_pass(const DevPool& P, int NL, int keep, const ScanBufs& B,
             unsigned int a4[kV], r4[kV];
             read4(st, tid, consumer && i0 + kV <= hi, x4, a4, r4);
             int cl[kV];
-            const unsigned int acc = classify4(x4, a4, r4, thr[R], thr[E], thr, cls, E, cl);
+            unsigned int acc = classify4(x4, a4, r4, thr[R], thr[E], thr, cls, E, cl);
             const int maxpos = append4(acc, x4, cl, i0, R, B, S, false);
             // every thread is done with stage s: refill it with tile t + kRing
             const int need_flush = __syncthreads_or(maxpos >= kFlushAt);
             if (tid == 0 && t + kRing < ntiles) issue(t + kRing);
-            if (need_flush) stage_flush(P, NL, keep, B, S, Sel, false);
+            if (need_flush) {
+                ensure_cls(P, a, B, S);
+                stage_flush(P, NL, keep, B, S, Sel, false);
+            }
         }
         __syncthreads();
     }
@@ -689,7 +822,38 @@ __device__ void scan_pass(const DevPool& P, int NL, int keep, const ScanBufs& B,
         P.dbg[blockIdx.x * 16 + 6] = clock64() - P.dbg[blockIdx.x * 16 + 7];  // SM cycles of the stream
         P.dbg[blockIdx.x * 16 + 8] = fast ? 1 : 0;
     }
-    if (S.count > 0) stage_flush(P, NL, keep, B, S, Sel, true);
+    if (spec && blockIdx.x == 0) {
+        // CTA 0 (after its phase 0): the change set with its post-phase-0 state, unfiltered
+        for (int j = tid; j < kXset; j += blockDim.x) {
+            const unsigned int sl = S.xset[j];
+            if (sl == kNoSlot) continue;
+            const unsigned long long x = P.lt[sl];
+            if (x == kFreeTick) continue;
+            const unsigned int ag = P.agent[sl];
+            const int c = ag == kNoAgent ? E : B.cls[ag];
+            // the same bounds the scanning CTAs apply (finalize_list's hint check needs them)
+            const bool in_r = x <= S.thr[R];
+            const bool in_c = P.refs[sl] == 0u && x <= S.thr[c];
+            if (!in_r && !in_c) continue;
+            int p = atomicAdd(&S.count, (in_r ? 1 : 0) + (in_c ? 1 : 0));
+            if (in_r) {
+                B.st_lt[p] = x;
+                B.st_slot[p] = sl;
+                B.st_list[p] = (unsigned char)R;
+                ++p;
+            }
+            if (in_c) {
+                B.st_lt[p] = x;
+                B.st_slot[p] = sl;
+                B.st_list[p] = (unsigned char)c;
+            }
+        }
+        __syncthreads();
+    }
+    if (S.count > 0) {
+        ensure_cls(P, a, B, S);
+        stage_flush(P, NL, keep, B, S, Sel, true);
+    }
     if (tid == 0) P.dbg[blockIdx.x * 16 + 2] = gtimer();
     // publish this CTA's survivors that can still be among the global keep smallest
     if (tid < NL) {
@@ -1257,6 +1421,7 @@ __global__ void __launch_bounds__(kThreads + 32, 1) admit_kernel(DevPool P, Admi
     const int NL = P.n_lists;
     const ScanBufs B = scan_bufs(dsm);
     ReplaySmem& Rp = *reinterpret_cast<ReplaySmem*>(dsm);
+    if (tid == 0) P.dbg[blockIdx.x * 16 + 9] = gtimer();  // kernel entry (instrumentation)
 
     // ---- phase 0 (CTA 0): poll reset, probe, feasibility, dispatch, lookup
     if (blockIdx.x == 0) {
@@ -1283,6 +1448,16 @@ __global__ void __launch_bounds__(kThreads + 32, 1) admit_kernel(DevPool P, Admi
             }
         }
         __syncthreads();
+        // deferred EngineSim::unpin calls of completed requests (engine.cpp:170-180), in order
+        if (a.n_unpin_ranges > 0) {
+            long long dec = 0;
+            for (int r = 0; r < a.n_unpin_ranges; ++r)
+                for (int i = tid; i < a.unpin_n[r]; i += T)
+                    if (atomicSub(&P.refs[a.unpin_ptr[r][i]], 1u) == 1u) ++dec;
+            dec = block_sum(dec, Red);
+            if (tid == 0) C->pinned -= dec;
+            __syncthreads();
+        }
         const int n = a.n;
         long long miss_min = n, need = 0;
         for (int i = tid; i < n; i += T) {
@@ -1330,13 +1505,88 @@ __global__ void __launch_bounds__(kThreads + 32, 1) admit_kernel(DevPool P, Admi
             }
         }
         __syncthreads();
+        if (tid == 0) {  // phase 0 is complete: publish for the speculative scanners
+            __threadfence();
+            asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(&C->p0_seq), "l"(a.seq) : "memory");
+        }
         stamp(A, 0);
+    }
+    if (tid == 0) {
+        S.spec = 0;
+        S.cls_ready = 1;
+    }
+    __syncthreads();
+
+    // ---- speculative first pass: every CTA but 0 starts scanning at once, concurrently with
+    // phase 0. Slots phase 0 may change are left out and restaged by CTA 0 with their new
+    // state; agent-carrying slots are classified once phase 0 has fixed the survival classes.
+    bool pending_rescan = false;  // CTA 0: the last pass must be redone (safe, no hints)
+    if ((a.flags & kSpeculate) && gridDim.x > 1) {
+        const int keep0 = min(a.n, kChunk);
+        int need_scan0 = 0;
+        if (tid == 0) {
+            S.spec = 1;
+            S.cls_ready = blockIdx.x == 0 ? 1 : 0;
+        }
+        if (blockIdx.x == 0) build_xset(P, a, S);
+        for (int x = tid; x < a.n_agents; x += T) B.cls[x] = blockIdx.x == 0 ? __ldcg(P.cls + x) : (unsigned char)kPend;
+        if (blockIdx.x == 0) {
+            const int hi0 = min(A.admit_n, kChunk);
+            long long absent = 0;
+            for (int j = tid; j < hi0; j += T) absent += P.p_slot[j] == kNoSlot ? 1 : 0;
+            absent = block_sum(absent, Red);
+            need_scan0 = C->resident + absent > P.cap ? 1 : 0;
+            if (tid == 0) {
+                A.scans += 1;
+                C->scans += 1;
+                C->scanned_slots += P.cap;
+                C->keep = keep0;  // a rescan of this chunk keeps the same candidate count
+            }
+        }
+        const int slow = __syncthreads_or(tid < NL && !(P.ghint[tid] < kNoBound) && !P.gsmall[tid]);
+        stamp(A, 1);
+        scan_pass(P, NL, keep0, B, S, Sel, dsm, !slow, a);
+        grid_barrier(C);
+        if (tid == 0) P.dbg[blockIdx.x * 16 + 4] = gtimer();
+        stamp(A, 2);
+        int mine = 0;
+        for (int l = blockIdx.x; l < NL; l += gridDim.x) {
+            finalize_list(P, l, NL, keep0, B, Sel);
+            ++mine;
+        }
+        if (blockIdx.x != 0) {
+            if (tid == 0 && mine) {
+                __threadfence();
+                atomicAdd(&C->fin_done, (unsigned int)mine);
+            }
+        } else {
+            if (tid == 0) {
+                const unsigned int want = (unsigned int)(NL - mine);
+                unsigned long long spins = 0;
+                while (ld_acquire(&C->fin_done) < want) {
+                    if (++spins > 4096) __nanosleep(64);
+                    if (spins > (1ull << 27)) __trap();
+                }
+                __threadfence();
+            }
+            __syncthreads();
+            stamp(A, 3);
+            pending_rescan = *(volatile int*)&C->rescan != 0;
+            const bool stop = !A.started || A.error || A.admit_n <= 0;
+            if (!pending_rescan && !stop) {
+                replay_apply(P, a, Rp, A, NL, need_scan0 != 0, Red);
+                if (tid == 0) A.chunk = 1;
+                __syncthreads();
+                stamp(A, 4);
+            }
+        }
+        if (tid == 0) S.spec = 0;
+        __syncthreads();
     }
 
     // ---- command loop. CTA 0 decides the next step (scan pass of a chunk, or done); every CTA
     // scans; CTAs 0..NL-1 select one list each; only CTA 0 consumes the lists, so it waits on
     // a counter instead of a grid barrier; CTA 0 replays. Per chunk: 2 grid barriers.
-    bool pending_rescan = false;  // CTA 0: the last pass must be redone (safe, no hints)
     for (;;) {
         if (blockIdx.x == 0) {
             const bool stop = !A.started || A.error || A.chunk * kChunk >= A.admit_n;
@@ -1396,7 +1646,7 @@ __global__ void __launch_bounds__(kThreads + 32, 1) admit_kernel(DevPool P, Admi
             const int pass = *(volatile int*)&C->pass;
             for (int x = tid; x < a.n_agents; x += T) B.cls[x] = P.cls[x];
             __syncthreads();
-            scan_pass(P, NL, keep, B, S, Sel, dsm, pass == 0 && *(volatile int*)&C->fast);
+            scan_pass(P, NL, keep, B, S, Sel, dsm, pass == 0 && *(volatile int*)&C->fast, a);
             if (blockIdx.x == 0 && tid == 0) {
                 A.ph[9] += S.flush_ns;
                 A.ph[10] += S.flushes;
@@ -1454,6 +1704,16 @@ __global__ void __launch_bounds__(kThreads + 32, 1) admit_kernel(DevPool P, Admi
         __syncthreads();
         stamp(A, 5);
         if (tid == 0) write_status(P, a, A);
+        // per-list scan state for the next launch (a speculative pass starts without a prep)
+        if (tid < kMaxLists) {
+            P.gbound[tid] = kNoBound;
+            P.gcount[tid] = 0;
+            P.gmaxk[tid] = 0ull;
+        }
+        if (tid == 0) {
+            C->fin_done = 0u;
+            C->rescan = 0;
+        }
     }
 }
 

@@ -76,6 +76,7 @@ struct Ctrl {
     unsigned int fin_done;  // lists finalized in this pass (CTA 0 waits for all, no grid barrier)
     int pass;          // scan pass of the current chunk (1 = safe, no hints)
     long long rescans; // instrumentation
+    unsigned long long p0_seq;  // AdmitArgs::seq of the launch whose phase 0 finished
 };
 
 struct DevPool {

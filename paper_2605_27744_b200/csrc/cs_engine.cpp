@@ -479,8 +479,7 @@ void cs_engine::complete_earliest() {
     sim_now = f.end_us;
     ++tick;  // emit(TurnComplete)
     const Req& r = reqs[f.req];
-    ck(csb::launch_unpin(pool->P, d_pins.as<unsigned int>() + r.blk_off, f.npins, pool->stream), "unpin");
-    if (f.npins > 0) ++pool->launches;
+    pool->defer_unpin(d_pins.as<unsigned int>() + r.blk_off, f.npins);  // runs inside the next admission launch
     const int sid = r.session;
     auto& list = by_session[sid];
     if (++session_pos[sid] < list.size()) {
@@ -630,6 +629,7 @@ int cs_engine_run(cs_engine_t e) {
     return eguard([&] {
         if (!e) throw std::invalid_argument("cs_engine_run: null engine");
         while (!e->done()) e->step();
+        e->pool->flush_unpins();
         e->drain_evictions(true);
     });
 }

@@ -37,6 +37,11 @@ __global__ void init_pool_kernel(DevPool P) {
         P.cls[x] = (unsigned char)P.e_max;
         P.hop[x] = (unsigned char)P.e_max;
     }
+    if (i < kMaxLists) {  // per-list scan state; every admission launch resets it for the next
+        P.gbound[i] = kNoBound;
+        P.gcount[i] = 0;
+        P.gmaxk[i] = 0ull;
+    }
     if (i == 0) {
         Ctrl* C = P.ctrl;
         C->resident = 0;
@@ -56,6 +61,9 @@ __global__ void init_pool_kernel(DevPool P) {
         C->bar_count = 0;
         C->bar_gen = 0;
         C->done = 0;
+        C->fin_done = 0u;
+        C->rescan = 0;
+        C->p0_seq = 0ull;
     }
 }
 

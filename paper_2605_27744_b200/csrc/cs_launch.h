@@ -15,8 +15,13 @@ enum AdmitFlags : int {
     kWarmupRoom = 16,  // execute_warmup: admit min(n, budget - pinned) blocks
     kUnpinAfter = 32,  // EngineSim::admit: unpin immediately
     kPollReset = 64,   // a poll_actions drain happened before this call
-    kAdmit = 128       // run admit_pinned at all (lookup-only / observe-only calls clear it)
+    kAdmit = 128,      // run admit_pinned at all (lookup-only / observe-only calls clear it)
+    kSpeculate = 256   // scan chunk 0 concurrently with phase 0 (cooperative grid only)
 };
+
+constexpr int kMaxUnpinRanges = 8;  // deferred EngineSim::unpin calls folded into one launch
+constexpr int kXset = 1024;         // slots phase 0 may change (prompt + unpinned), hashed per CTA
+constexpr int kXsetMax = kXset / 2; // speculation only below half load
 
 struct AdmitStatus {
     int started;
@@ -55,6 +60,11 @@ struct AdmitArgs {
     int n_agents;
     unsigned int* pins_out;
     AdmitStatus* status;  // host-mapped
+    unsigned long long seq;  // launch sequence number (phase-0 completion flag)
+    // EngineSim::unpin (engine.cpp:170-180) of completed requests, applied first in phase 0
+    const unsigned int* unpin_ptr[kMaxUnpinRanges];
+    int unpin_n[kMaxUnpinRanges];
+    int n_unpin_ranges;
 };
 
 struct LaunchCfg {

@@ -2,6 +2,7 @@
 #include "cs_pool.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 using csb::ck;
@@ -117,6 +118,7 @@ void cs_pool::create(const cs_pool_cfg& c) {
     p.p_refs0 = nullptr;
     ensure_prompt_scratch(4096);
 
+    if (const char* e = std::getenv("CS_SPECULATE")) speculate = std::atoi(e) != 0;  // A/B switch (tools)
     lc = csb::admit_launch_config(p, device, c.grid_ctas);
     if (lc.grid <= 0) throw CsError(CS_ERR_CUDA, "admit kernel: no launch configuration fits this device");
     p.gcap = (long long)lc.grid * (csb::kChunk + 1);
@@ -175,6 +177,19 @@ const csb::AdmitStatus& cs_pool::admit(const csb::AdmitArgs& in, int n_for_grid)
     // one CTA then suffices (the grid barrier degenerates), saving the cooperative launch.
     const bool may_evict = (a.flags & csb::kAdmit) && resident + n_for_grid > P.cap;
     const int grid = may_evict ? lc.grid : 1;
+    // queued unpins run first inside this launch (they fit the change set of a speculative pass)
+    if ((int)unpin_q.size() > csb::kMaxUnpinRanges) flush_unpins();
+    a.n_unpin_ranges = 0;
+    for (const auto& u : unpin_q) {
+        a.unpin_ptr[a.n_unpin_ranges] = u.first;
+        a.unpin_n[a.n_unpin_ranges] = u.second;
+        ++a.n_unpin_ranges;
+    }
+    const int xn = a.n + unpin_q_slots;
+    unpin_q.clear();
+    unpin_q_slots = 0;
+    a.seq = ++seq;
+    if (speculate && grid > 1 && xn <= csb::kXsetMax) a.flags |= csb::kSpeculate;
     st->started = -1;
     if (timing) ck(cudaEventRecord(ev0, stream), "cudaEventRecord");
     ck(csb::launch_admit(P, a, lc, grid, stream), "admit_kernel launch");
@@ -209,6 +224,22 @@ const csb::AdmitStatus& cs_pool::admit(const csb::AdmitArgs& in, int n_for_grid)
         launches += 2;
     }
     return *st;
+}
+
+void cs_pool::defer_unpin(const unsigned int* dev_slots, int n) {
+    if (n <= 0) return;
+    if ((int)unpin_q.size() == csb::kMaxUnpinRanges) flush_unpins();
+    unpin_q.emplace_back(dev_slots, n);
+    unpin_q_slots += n;
+}
+
+void cs_pool::flush_unpins() {
+    for (const auto& u : unpin_q) {
+        ck(csb::launch_unpin(P, u.first, u.second, stream), "unpin");
+        ++launches;
+    }
+    unpin_q.clear();
+    unpin_q_slots = 0;
 }
 
 void cs_pool::copy_victims(unsigned long long from, unsigned long long to, unsigned long long* out) {
@@ -377,6 +408,7 @@ int cs_lookup(cs_pool_t pool, const uint64_t* keys, const int32_t* counts, int n
 int cs_probe_needed(cs_pool_t pool, const uint64_t* keys, int n, int* needed) {
     return guard([&] {
         if (!pool || n < 0 || (n > 0 && !keys) || !needed) throw std::invalid_argument("cs_probe_needed: null argument");
+        pool->flush_unpins();
         stage_prompt(pool, keys, nullptr, n);
         pool->d_aux.ensure(sizeof(int));
         ck(csb::launch_probe(pool->P, pool->d_keys.as<unsigned long long>(), n, pool->d_aux.as<int>(), pool->stream),
@@ -440,6 +472,7 @@ int cs_admit_pinned(cs_pool_t pool, const uint64_t* keys, const int32_t* counts,
 int cs_unpin_slots(cs_pool_t pool, const uint32_t* slots, int n) {
     return guard([&] {
         if (!pool || n < 0 || (n > 0 && !slots)) throw std::invalid_argument("cs_unpin_slots: null argument");
+        pool->flush_unpins();
         pool->d_aux.ensure(sizeof(uint32_t) * std::max(n, 1));
         ck(cudaMemcpyAsync(pool->d_aux.p, slots, sizeof(uint32_t) * n, cudaMemcpyHostToDevice, pool->stream), "H2D");
         ck(csb::launch_unpin(pool->P, pool->d_aux.as<unsigned int>(), n, pool->stream), "unpin");
@@ -454,6 +487,7 @@ int cs_restore(cs_pool_t pool, const uint64_t* keys, const uint64_t* lt, const u
                int64_t n) {
     return guard([&] {
         if (!pool || n < 0 || (n > 0 && (!keys || !lt))) throw std::invalid_argument("cs_restore: null argument");
+        pool->flush_unpins();
         if (pool->resident + n > pool->P.cap) throw std::invalid_argument("cs_restore: snapshot exceeds the budget");
         if (n == 0) return;
         cudaStream_t s = pool->stream;
@@ -488,6 +522,7 @@ int cs_restore(cs_pool_t pool, const uint64_t* keys, const uint64_t* lt, const u
 int cs_score_snapshot(cs_pool_t pool, uint64_t now_tick, uint64_t* keys, double* scores, int64_t cap, int64_t* n) {
     return guard([&] {
         if (!pool) throw std::invalid_argument("cs_score_snapshot: null pool");
+        pool->flush_unpins();
         const long long N = pool->P.cap;
         csb::DevBuf k, s, cnt, scr;
         k.ensure(8 * N);
@@ -547,6 +582,7 @@ int cs_pool_debug(cs_pool_t pool, uint64_t* out, int cap, int* grid) {
 int cs_pool_get_stats(cs_pool_t pool, cs_pool_stats* out) {
     return guard([&] {
         if (!pool || !out) throw std::invalid_argument("cs_pool_get_stats: null argument");
+        pool->flush_unpins();
         pool->sync();
         csb::Ctrl c;
         ck(cudaMemcpy(&c, pool->P.ctrl, sizeof(c), cudaMemcpyDeviceToHost), "ctrl D2H");

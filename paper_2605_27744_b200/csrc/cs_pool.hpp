@@ -75,6 +75,11 @@ struct cs_pool {
     long long admit_launches = 0, scan_launches = 0, scans_total = 0, table_rebuilds = 0;
     long long launches = 0;  // every kernel this handle launched (the bench's gpu_launches)
     unsigned long long phase_ns[csb::kPhases] = {};
+    unsigned long long seq = 0;  // admission launch sequence (AdmitArgs::seq)
+    bool speculate = true;       // overlap the first scan pass with phase 0 when it can evict
+    // deferred EngineSim::unpin calls (device slot lists), folded into the next admission launch
+    std::vector<std::pair<const unsigned int*, int>> unpin_q;
+    int unpin_q_slots = 0;
 
     void create(const cs_pool_cfg& c);
     void destroy();
@@ -83,5 +88,9 @@ struct cs_pool {
     // is possible, else the cooperative grid).
     const csb::AdmitStatus& admit(const csb::AdmitArgs& args_in, int n_for_grid);
     void copy_victims(unsigned long long from, unsigned long long to, unsigned long long* host_out);
+    // Queues an unpin of device-resident slots; it runs at the start of the next admission
+    // launch (or in flush_unpins, before any other pool operation reads pins).
+    void defer_unpin(const unsigned int* dev_slots, int n);
+    void flush_unpins();
     void sync() { csb::ck(cudaStreamSynchronize(stream), "cudaStreamSynchronize"); }
 };

@@ -66,6 +66,9 @@ rel = (d[:, :5] - t0) / 1e3
 print(f"CTAs={grid.value}: scan start spread {rel[:,0].max():.1f} us; stream end min/med/max "
       f"{rel[:,1].min():.1f}/{np.median(rel[:,1]):.1f}/{rel[:,1].max():.1f}; final flush end max {rel[:,2].max():.1f}; "
       f"writeout end max {rel[:,3].max():.1f}; barrier exit {rel[:,4].max():.1f} us")
+ent = (d[:, 9] - t0) / 1e3
+print(f"kernel entry rel. to first scan start: min/max {ent.min():.1f}/{ent.max():.1f} us; "
+      f"scan start after entry med {np.median(rel[:,0]-ent):.1f} us")
 print(f"staged at stream end: med {np.median(d[:,5]):.0f} max {d[:,5].max()}")
 mhz = d[:, 6] / ((d[:, 1] - d[:, 0]) / 1e3)
 print(f"SM clock during the stream (clock64 / globaltimer): med {np.median(mhz):.0f} MHz (min {mhz.min():.0f})")
