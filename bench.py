@@ -90,28 +90,52 @@ class Dist:
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled during the timed region: NVML every 2 ms (the timed
+    region is tens of ms), nvidia-smi as the fallback."""
+
+    _REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap"}
 
     def __init__(self, device):
         self.device = device
-        self.samples = []
+        self.samples = []  # (sm_mhz, max_mhz, reasons)
         self._stop = threading.Event()
         self._t = None
+        self._nvml = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self._nvml = pynvml
+        except Exception:
+            self._nvml = None
+
+    def _sample_nvml(self):
+        nv = self._nvml
+        sm = nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)
+        mx = nv.nvmlDeviceGetMaxClockInfo(self._h, nv.NVML_CLOCK_SM)
+        try:
+            bits = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+        except Exception:
+            bits = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self._h)
+        return float(sm), float(mx), {n for b, n in self._REASONS.items() if bits & b}
+
+    def _sample_smi(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}", "--format=csv,noheader,nounits"],
+                             capture_output=True, text=True, timeout=5).stdout.strip()
+        f = [x.strip() for x in out.split(",")]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        return float(f[0]), float(f[1]), {n for n, v in zip(names, f[2:6]) if v.lower() == "active"}
 
     def _run(self):
-        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-             "clocks_event_reasons.sw_power_cap")
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
+                self.samples.append(self._sample_nvml() if self._nvml else self._sample_smi())
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.002 if self._nvml else 0.2)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -125,16 +149,12 @@ class ClockSampler:
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = set()
         for s in self.samples:
-            for n, v in zip(names, s[3:7]):
-                if v.strip().lower() == "active":
-                    reasons.add(n)
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(self.samples)}
+            reasons |= s[2]
+        return {"sm_mhz": float(np.median([s[0] for s in self.samples])),
+                "sm_max_mhz": max(s[1] for s in self.samples), "reasons": sorted(reasons),
+                "samples": len(self.samples), "source": "nvml" if self._nvml else "nvidia-smi"}
 
 
 def measured_peak():
@@ -185,6 +205,16 @@ def aggregate(dist, ms, scanned):
     return dist.sum(scanned) / (tot_ms / 1e3), tot_ms
 
 
+PHASES = ["phase0", "prep", "scan", "select", "replay", "epilogue", "replay_setup", "replay_loop", "apply",
+          "", "", "", "", "", "", "select_wait"]
+
+
+def _phases(p0, p1, launches):
+    """CTA-0 view of the admission kernel's phases (device globaltimer), per scoring launch."""
+    n = max(launches, 1)
+    return {k: round((p1[i] - p0[i]) / n / 1e3, 2) for i, k in enumerate(PHASES) if k}
+
+
 def run_ours(args, dist):
     from paper_2605_27744_b200 import workloads as W
 
@@ -206,9 +236,11 @@ def run_ours(args, dist):
     eng = build_engine(W, spec, pool, dist.local, False, seed=snap_seed)
     timed_run(eng, args.warmup)
     r0 = eng.result()
+    p0 = eng.pool_stats()["phase_ns"]
     with ClockSampler(dist.local) as clk:
         ms = timed_run(eng, args.steps)
     r1 = eng.result()
+    p1 = eng.pool_stats()["phase_ns"]
     value, tot_ms = aggregate(dist, ms, r1["scanned_slots"] - r0["scanned_slots"])
     evicted = dist.sum(r1["evictions"] - r0["evictions"])
     adm = dist.sum(r1["admissions"] - r0["admissions"])
@@ -254,6 +286,7 @@ def run_ours(args, dist):
                      "peak_source": peak_kind,
                      "avg_launch_us": avg_scan_launch_s * 1e6, "algorithmic_bytes_per_launch": BYTES_PER_SLOT * pool},
         "clocks": clk.summary(),
+        "phases_us_per_scan_launch": _phases(p0, p1, scan_launches),
     }
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(pool, args)

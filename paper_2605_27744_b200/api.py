@@ -283,6 +283,15 @@ class Engine:
         check(lib().cs_engine_restore(self.h, _p(keys), _p(lt), None if ag is None else _p(ag),
                                       None if rf is None else _p(rf), keys.size))
 
+    def pool_stats(self):
+        """Pool counters of the engine's device pool (cs_pool_get_stats), incl. the per-phase
+        device time of the admission kernel (phase_ns, CTA-0 globaltimer)."""
+        s = PoolStats()
+        check(lib().cs_pool_get_stats(lib().cs_engine_pool(self.h), C.byref(s)))
+        d = {f: getattr(s, f) for f, _ in PoolStats._fields_}
+        d["phase_ns"] = list(s.phase_ns)
+        return d
+
     def result(self):
         r = EngineResult()
         check(lib().cs_engine_result_get(self.h, C.byref(r)))

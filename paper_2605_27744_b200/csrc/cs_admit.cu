@@ -52,6 +52,7 @@ struct ScanSmem {
     int overflow;
     int spec;       // speculative pass: phase 0 runs concurrently on CTA 0
     int hc, dc;     // ensure_cls compaction counters
+    int prep_done;  // the producer warp already loaded the classes and built the change set
     int cls_ready;  // B.cls holds this launch's classes (else kPend for every agent)
     unsigned int xset[kXset];  // slots phase 0 may change: excluded here, restaged fresh by CTA 0
     __align__(8) unsigned long long mbar[kRing];        // TMA ring: stage filled
@@ -127,8 +128,14 @@ struct ReplaySmem {
     int n_vict, n_new_global, n_reused;
     int pdom;  // length of the class-E prefix whose heads beat every other class outright
     int bulk;  // this chunk was replayed in bulk (no serial loop)
+    // list-independent prologue (replay_prologue), valid from phase 0 on
+    long long res0, pinned0, ftop;
+    int absent, pre_unpinned;
+    int n_ins;  // queued inserts of this chunk
 };
-static_assert(sizeof(ReplaySmem) <= kOffCls, "replay view must fit the scan region");
+// The replay view lives in the TMA ring: free after a scan, and never used by CTA 0 during a
+// speculative pass, so CTA 0 prepares the prologue while the other CTAs still stream.
+static_assert(sizeof(ReplaySmem) <= kRing * kRingStage, "replay view must fit the TMA ring");
 
 struct BfsSmem {
     unsigned short wa[8192];
@@ -624,16 +631,18 @@ __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long
 __device__ void ensure_cls(const DevPool& P, const AdmitArgs& a, const ScanBufs& B, ScanSmem& S) {
     if (!S.spec || S.cls_ready) return;
     const int tid = threadIdx.x, T = blockDim.x;
-    if (tid == 0) {
-        unsigned long long spins = 0;
-        while (ld_acquire_u64(&P.ctrl->p0_seq) != a.seq) {
-            if (++spins > 1024) __nanosleep(128);
-            if (spins > (1ull << 27)) __trap();
+    if (!S.prep_done) {
+        if (tid == 0) {
+            unsigned long long spins = 0;
+            while (ld_acquire_u64(&P.ctrl->p0_seq) != a.seq) {
+                if (++spins > 1024) __nanosleep(128);
+                if (spins > (1ull << 27)) __trap();
+            }
         }
+        __syncthreads();
+        for (int x = tid; x < a.n_agents; x += T) B.cls[x] = __ldcg(P.cls + x);
+        build_xset(P, a, S);
     }
-    __syncthreads();
-    for (int x = tid; x < a.n_agents; x += T) B.cls[x] = __ldcg(P.cls + x);
-    build_xset(P, a, S);
     // Relabel, then drop (a) entries of the change set and (b) relabelled entries above their
     // class's bound: every staged entry then satisfies the bound its list would have applied,
     // which the hint check of finalize_list relies on. In-place compaction: the holes below the
@@ -682,6 +691,33 @@ __device__ void ensure_cls(const DevPool& P, const AdmitArgs& a, const ScanBufs&
     __syncthreads();
 }
 
+// The producer warp of a fast speculative pass, once it has issued every tile: waits for phase
+// 0, publishes the new survival classes to the consumers (a consumer that reads a class from
+// now on stages the slot under it; earlier reads left kPend) and builds the change set, so the
+// tail of the pass only filters.
+__device__ void producer_prep(const DevPool& P, const AdmitArgs& a, const ScanBufs& B, ScanSmem& S) {
+    const int lane = lane_id();
+    if (lane == 0) {
+        unsigned long long spins = 0;
+        while (ld_acquire_u64(&P.ctrl->p0_seq) != a.seq) {
+            if (++spins > 1024) __nanosleep(128);
+            if (spins > (1ull << 27)) __trap();
+        }
+    }
+    __syncwarp();
+    for (int x = lane; x < a.n_agents; x += 32) B.cls[x] = __ldcg(P.cls + x);
+    for (int j = lane; j < kXset; j += 32) S.xset[j] = kNoSlot;
+    __syncwarp();
+    for (int i = lane; i < a.n; i += 32) {
+        const unsigned int sl = __ldcg(P.p_slot + i);
+        if (sl != kNoSlot) xset_insert(S, sl);
+    }
+    for (int r = 0; r < a.n_unpin_ranges; ++r)
+        for (int i = lane; i < a.unpin_n[r]; i += 32) xset_insert(S, a.unpin_ptr[r][i]);
+    __syncwarp();
+    if (lane == 0) S.prep_done = 1;
+}
+
 // One streaming pass over this CTA's contiguous slot range: 16 B per slot read exactly once.
 // The SoA arrives through a kRing-stage TMA ring (cp.async.bulk into shared memory, mbarrier
 // transaction counts), so the loads are independent of the threads' progress.
@@ -719,6 +755,7 @@ __device__ void scan_pass(const DevPool& P, int NL, int keep, const ScanBufs& B,
     if (tid == 0) {
         S.count = 0;
         S.overflow = 0;
+        S.prep_done = 0;
         S.flush_ns = 0;
         S.flushes = 0;
         for (int s = 0; s < kRing; ++s) {
@@ -761,6 +798,7 @@ __device__ void scan_pass(const DevPool& P, int NL, int keep, const ScanBufs& B,
                 }
             }
             __syncwarp();
+            if (spec && !S.cls_ready) producer_prep(P, a, B, S);
         } else {
             unsigned long long gbn = ~0ull;
             for (int t = 0; t < ntiles; ++t) {
@@ -892,6 +930,24 @@ __device__ void scan_pass(const DevPool& P, int NL, int keep, const ScanBufs& B,
 
 // ------------------------------------------------------------------ K5a: exact per-list select
 
+constexpr int kDirectRank = 384;  // finalize_list ranks up to this many candidates directly
+
+// One thread: list l holds n sorted entries; hint bookkeeping for the next scan.
+// The next scan's hint for a full list: the largest per-CTA keep-th value (mk). A list no CTA
+// had to truncate (mk == 0: every CTA held fewer than keep of its members) is "small": the next
+// fast pass stages all of its members (a staging overflow sends it to a safe rescan).
+__device__ __forceinline__ void finish_list(const DevPool& P, int l, int n, int kl, unsigned long long hmax) {
+    P.fin_n[l] = n;
+    // Hint verification. Hints are only carried for lists that were full (n == keep) in the previous scan; a
+    // hinted list that now comes up short may be missing members above its hint.
+    const bool hinted = P.ghint[l] < kNoBound;
+    if (n < kl && hinted) atomicExch(&P.ctrl->rescan, 1);
+    const unsigned long long mk = *(volatile unsigned long long*)(P.gmaxk + l);
+    P.ghint[l] = (n == kl && mk) ? mk : kNoBound;
+    P.gsmall[l] = mk == 0ull ? 1 : 0;
+    (void)hmax;
+}
+
 __device__ void finalize_list(const DevPool& P, int l, int NL, int keep, const ScanBufs& B, SelectSmem& Sel) {
     const int tid = threadIdx.x, T = blockDim.x;
     const int kl = keep_of(l, NL, keep);
@@ -907,6 +963,7 @@ __device__ void finalize_list(const DevPool& P, int l, int NL, int keep, const S
     if (tid == 0) {
         Sel.tmp = 0;
         Sel.prefix = kNoBound;
+        Sel.hmax = 0ull;
     }
     for (int i = tid; i < G; i += T) mins[i] = P.gmin[(long long)l * G + i];
     __syncthreads();
@@ -920,8 +977,10 @@ __device__ void finalize_list(const DevPool& P, int l, int NL, int keep, const S
     __syncthreads();
     const unsigned long long fb = Sel.prefix;
     // stage the filtered candidates on chip when they fit (the common case), else select from L2
+    unsigned long long hm = 0ull;
     for (int j = tid; j < m; j += T) {
         const unsigned long long x = g[j];
+        hm = max(hm, x);
         if (x <= fb) {
             const int p = atomicAdd(&Sel.tmp, 1);
             if (p < kStage) {
@@ -930,6 +989,8 @@ __device__ void finalize_list(const DevPool& P, int l, int NL, int keep, const S
             }
         }
     }
+    for (int o = 16; o; o >>= 1) hm = max(hm, __shfl_xor_sync(0xffffffffu, hm, o));
+    if (lane_id() == 0 && hm) atomicMax(&Sel.hmax, hm);
     __syncthreads();
     const int mf = Sel.tmp;
     const bool local = mf <= kStage;
@@ -937,6 +998,21 @@ __device__ void finalize_list(const DevPool& P, int l, int NL, int keep, const S
     const unsigned int* srs = local ? B.st_slot : gs;
     const int ms = local ? mf : m;
     __syncthreads();
+    if (local && mf <= kDirectRank) {
+        // few candidates (the common case): every entry's rank directly, one pass (distinct ticks)
+        for (int j = tid; j < mf; j += T) {
+            const unsigned long long x = src[j];
+            int r = 0;
+            for (int k = 0; k < mf; ++k) r += src[k] < x;
+            if (r < kl) {
+                P.fin_lt[(long long)l * (kChunk + 2) + r] = x;
+                P.fin_slot[(long long)l * (kChunk + 2) + r] = srs[j];
+            }
+        }
+        if (tid == 0) finish_list(P, l, min(mf, kl), kl, Sel.hmax);
+        __syncthreads();
+        return;
+    }
     unsigned long long v = ~0ull;
     if (ms > kl) v = block_kth(src, nullptr, 0, ms, kl, Sel);
     unsigned long long* t_lt = B.sd_lt;
@@ -961,16 +1037,7 @@ __device__ void finalize_list(const DevPool& P, int l, int NL, int keep, const S
         P.fin_lt[(long long)l * (kChunk + 2) + r] = x;
         P.fin_slot[(long long)l * (kChunk + 2) + r] = t_slot[j];
     }
-    if (tid == 0) {
-        P.fin_n[l] = n;
-        // Hint verification. Hints are only carried for lists that were full (n == keep) in the previous scan; a
-        // hinted list that now comes up short may be missing members above its hint.
-        const bool hinted = P.ghint[l] < kNoBound;
-        if (n < kl && hinted) atomicExch(&P.ctrl->rescan, 1);
-        const unsigned long long mk = *(volatile unsigned long long*)(P.gmaxk + l);
-        P.ghint[l] = (n == kl && mk) ? mk : kNoBound;
-        P.gsmall[l] = n < kl ? 1 : 0;
-    }
+    if (tid == 0) finish_list(P, l, n, kl, Sel.hmax);
     __syncthreads();
 }
 
@@ -982,43 +1049,44 @@ __device__ __forceinline__ unsigned int hslot(unsigned int s) { return (s * 2654
 // eviction is evict_one (engine.cpp:102-125): the argmin of (score, last_touch) over the class
 // heads; oldest_live_touch (engine.cpp:90-100) = min(tick, resident-list head, earliest touch
 // of this admission). One warp; lane l owns list l.
-__device__ void replay_apply(const DevPool& P, const AdmitArgs& a, ReplaySmem& R, AdmSmem& A, int NL, bool scanned,
-                             RedSmem& Red) {
+// List-independent part of the replay of chunk A.chunk (CTA 0, all threads): the chunk's
+// prompt slots and their pins, free slots, the slot -> prompt index hash, pool counters.
+// Depends only on phase 0 and earlier chunks, so a speculative pass runs it before the lists
+// exist.
+__device__ void replay_prologue(const DevPool& P, ReplaySmem& R, const AdmSmem& A, RedSmem& Red) {
     Ctrl* C = P.ctrl;
     const int tid = threadIdx.x, T = blockDim.x;
     const int lo = A.chunk * kChunk;
     const int hi = min(A.admit_n, lo + kChunk);
     const int len = hi - lo;
-    const int Rl = NL - 1;
-
-    // ---- setup (all threads)
     for (int j = tid; j < 512; j += T) {
         R.ph_key[j] = kNoSlot;
         R.vh_key[j] = kNoSlot;
     }
+    const long long ftop = C->free_top;
+    int absent = 0, pre_unpinned = 0;
     for (int i = tid; i < len; i += T) {
-        R.c_slot[i] = P.p_slot[lo + i];
-        R.c_refs0[i] = P.p_refs0[lo + i];
+        const unsigned int sl = P.p_slot[lo + i];
+        const unsigned int r0 = P.p_refs0[lo + i];
+        R.c_slot[i] = sl;
+        R.c_refs0[i] = r0;
         R.touched[i] = 0;
         R.pevict[i] = 0;
+        if (sl == kNoSlot) ++absent;
+        else if (r0 == 0u) ++pre_unpinned;
     }
     for (int j = tid; j < kChunk + 2; j += T) R.rremoved[j] = 0;
-    const long long ftop = C->free_top;
     for (int j = tid; j < len && j < ftop; j += T) R.freeslots[j] = P.free_stack[ftop - 1 - j];
     if (tid == 0) {
         R.n_vict = 0;
         R.n_new_global = 0;
         R.n_reused = 0;
+        R.n_ins = 0;
+        R.ftop = ftop;
+        R.res0 = C->resident;
+        R.pinned0 = C->pinned;
     }
-    for (int l = 0; l < NL; ++l) {
-        const int n = scanned ? P.fin_n[l] : 0;
-        for (int j = tid; j < n; j += T) {
-            R.L_lt[l][j] = P.fin_lt[(long long)l * (kChunk + 2) + j];
-            R.L_slot[l][j] = P.fin_slot[(long long)l * (kChunk + 2) + j];
-        }
-        if (tid == 0) R.L_n[l] = n;
-    }
-    __syncthreads();
+    const long long both = block_sum(((long long)absent << 32) | (long long)pre_unpinned, Red);
     // slot -> prompt index of this chunk's resident blocks
     for (int i = tid; i < len; i += T) {
         const unsigned int s = R.c_slot[i];
@@ -1031,6 +1099,37 @@ __device__ void replay_apply(const DevPool& P, const AdmitArgs& a, ReplaySmem& R
                 break;
             }
             h = (h + 1) & 511u;
+        }
+    }
+    if (tid == 0) {
+        R.absent = (int)(both >> 32);
+        R.pre_unpinned = (int)(both & 0xffffffffll);
+    }
+    __syncthreads();
+}
+
+// Exact replay of admit_pinned over prompt blocks [lo, hi) (engine.cpp:141-168) after
+// replay_prologue. Each eviction is evict_one (engine.cpp:102-125): the argmin of
+// (score, last_touch) over the class heads; oldest_live_touch (engine.cpp:90-100) = min(tick,
+// resident-list head, earliest touch of this admission). One warp; lane l owns list l.
+__device__ void replay_apply(const DevPool& P, const AdmitArgs& a, ReplaySmem& R, AdmSmem& A, int NL, bool scanned,
+                             RedSmem& Red) {
+    Ctrl* C = P.ctrl;
+    const int tid = threadIdx.x, T = blockDim.x;
+    const int lo = A.chunk * kChunk;
+    const int hi = min(A.admit_n, lo + kChunk);
+    const int len = hi - lo;
+    const int Rl = NL - 1;
+    const long long ftop = R.ftop;
+
+    // ---- the candidate lists (one round trip: counts first into shared memory, then all entries)
+    if (tid < NL) R.L_n[tid] = scanned ? P.fin_n[tid] : 0;
+    __syncthreads();
+    for (int q = tid; q < NL * (kChunk + 2); q += T) {
+        const int l = q / (kChunk + 2), j = q - l * (kChunk + 2);
+        if (j < R.L_n[l]) {
+            R.L_lt[l][j] = P.fin_lt[q];
+            R.L_slot[l][j] = P.fin_slot[q];
         }
     }
     __syncthreads();
@@ -1069,14 +1168,8 @@ __device__ void replay_apply(const DevPool& P, const AdmitArgs& a, ReplaySmem& R
         return -1;
     };
     {
-        const long long res0 = C->resident;
-        int absent = 0, pre_unpinned = 0;
-        for (int i = tid; i < len; i += T) {
-            if (R.c_slot[i] == kNoSlot) ++absent;
-            else if (R.c_refs0[i] == 0u) ++pre_unpinned;
-        }
-        absent = (int)block_sum(absent, Red);
-        pre_unpinned = (int)block_sum(pre_unpinned, Red);
+        const long long res0 = R.res0;
+        const int absent = R.absent, pre_unpinned = R.pre_unpinned;
         const long long room = P.cap - res0;
         const int n_free = (int)min((long long)absent, room > 0 ? room : 0ll);
         const int n_ev = absent - n_free;
@@ -1115,7 +1208,7 @@ __device__ void replay_apply(const DevPool& P, const AdmitArgs& a, ReplaySmem& R
                 if (len > 0 && A.first_touch == ~0ull) A.first_touch = A.tick + 1;
                 A.tick += (unsigned long long)len;
                 A.resident = res0 + absent - n_ev;
-                A.pinned = C->pinned + pre_unpinned + absent;
+                A.pinned = R.pinned0 + pre_unpinned + absent;
                 R.n_vict = n_ev;
                 R.n_reused = n_ev;
                 R.n_new_global = n_free;
@@ -1172,8 +1265,8 @@ __device__ void replay_apply(const DevPool& P, const AdmitArgs& a, ReplaySmem& R
         const double my_surv = survival_of_class(lane, P.e_max);
         unsigned long long tick = A.tick;
         unsigned long long first_touch = A.first_touch;
-        long long resident = C->resident;
-        long long pinned = C->pinned;
+        long long resident = R.res0;
+        long long pinned = R.pinned0;
         int nv = 0, nre = 0, nglob = 0;
         int error = 0;
         const int E = P.e_max;      // agentless / unreachable class (survival 0)
@@ -1317,9 +1410,10 @@ __device__ void replay_apply(const DevPool& P, const AdmitArgs& a, ReplaySmem& R
         }
     }
     __syncthreads();
+    const int q_e = C->tq_erase, q_i = C->tq_insert;  // table updates are queued for the next launch
     for (int k = tid; k < nv; k += T) {
         const unsigned long long kk = R.vkey[k];
-        table_erase(P, kk);
+        P.tq_key[q_e + k] = kk;
         P.evlog[(ev0 + k) % (unsigned long long)P.evlog_cap] = kk;  // ring; the host drains it
         if (k >= R.n_reused) {  // victims[0, n_reused) are overwritten by new blocks below
             const unsigned int v = R.victims[k];
@@ -1328,11 +1422,9 @@ __device__ void replay_apply(const DevPool& P, const AdmitArgs& a, ReplaySmem& R
             P.agent[v] = kNoAgent;
         }
     }
-    // Bulk chunks never re-insert a key they evicted (their victims are not prompt blocks of
-    // the chunk), so erases and inserts touch distinct keys and run in one round; the serial
-    // path may evict a later prompt block and re-insert it, so it orders the two rounds.
+    // A serial chunk may evict a later prompt block and re-admit it into the victim's slot:
+    // the victim's reset above must land before the new block's writes.
     if (!R.bulk) __syncthreads();
-    long long reused_tomb = 0;
     const int done_len = err ? 0 : len;  // an erroring chunk is not applied
     for (int i = tid; i < done_len; i += T) {
         const unsigned int s = R.out_slot[i];
@@ -1343,7 +1435,9 @@ __device__ void replay_apply(const DevPool& P, const AdmitArgs& a, ReplaySmem& R
             P.agent[s] = (a.agent != kNoAgent && gi < A.anchor) ? a.agent : kNoAgent;
             P.lt[s] = R.out_lt[i];
             P.refs[s] = 1u;
-            reused_tomb += table_insert(P, a.keys[gi], s);
+            const int q = q_i + atomicAdd(&R.n_ins, 1);
+            P.tq_key[P.p_cap + q] = a.keys[gi];
+            P.tq_slot[q] = s;
         } else {
             P.lt[s] = R.out_lt[i];
             atomicAdd(&P.refs[s], 1u);
@@ -1367,7 +1461,7 @@ __device__ void replay_apply(const DevPool& P, const AdmitArgs& a, ReplaySmem& R
             }
         }
     }
-    reused_tomb = block_sum(reused_tomb, Red);
+    __syncthreads();
     if (tid == 0) {
         long long top = ftop - R.n_new_global;
         for (int k = R.n_reused; k < nv; ++k) P.free_stack[top++] = R.victims[k];
@@ -1375,11 +1469,43 @@ __device__ void replay_apply(const DevPool& P, const AdmitArgs& a, ReplaySmem& R
         C->pinned = A.pinned;
         C->free_top = top;
         C->n_ev = ev0 + nv;
-        C->tombstones += (long long)nv - reused_tomb;
+        C->tq_erase = q_e + nv;
+        C->tq_insert = q_i + R.n_ins;
         A.n_ev_adm += nv;
     }
     __syncthreads();
     stamp(A, 8);
+}
+
+// Applies the block-table updates queued by the previous admission (all threads of one CTA):
+// every erase, then every insert (a key erased and re-admitted in one admission is inserted
+// after its erase; an inserted block is pinned, so no admission erases it again).
+__device__ void apply_table_queue(const DevPool& P, RedSmem& Red) {
+    Ctrl* C = P.ctrl;
+    const int tid = threadIdx.x, T = blockDim.x;
+    const int ne = C->tq_erase, ni = C->tq_insert;
+    if (ne == 0 && ni == 0) return;
+    for (int k = tid; k < ne; k += T) table_erase(P, P.tq_key[k]);
+    __syncthreads();
+    long long reused = 0;
+    for (int i = tid; i < ni; i += T) reused += table_insert(P, P.tq_key[P.p_cap + i], P.tq_slot[i]);
+    reused = block_sum(reused, Red);
+    if (tid == 0) {
+        C->tombstones += (long long)ne - reused;
+        C->tq_erase = 0;
+        C->tq_insert = 0;
+    }
+    __syncthreads();
+}
+
+__global__ void table_flush_kernel(DevPool P) {
+    __shared__ RedSmem Red;
+    apply_table_queue(P, Red);
+}
+
+cudaError_t launch_table_flush(const DevPool& P, cudaStream_t s) {
+    table_flush_kernel<<<1, 512, 0, s>>>(P);
+    return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------ the admission kernel
@@ -1420,7 +1546,7 @@ __global__ void __launch_bounds__(kThreads + 32, 1) admit_kernel(DevPool P, Admi
     const int tid = threadIdx.x, T = blockDim.x;
     const int NL = P.n_lists;
     const ScanBufs B = scan_bufs(dsm);
-    ReplaySmem& Rp = *reinterpret_cast<ReplaySmem*>(dsm);
+    ReplaySmem& Rp = *reinterpret_cast<ReplaySmem*>(dsm + kOffRing);
     if (tid == 0) P.dbg[blockIdx.x * 16 + 9] = gtimer();  // kernel entry (instrumentation)
 
     // ---- phase 0 (CTA 0): poll reset, probe, feasibility, dispatch, lookup
@@ -1448,6 +1574,7 @@ __global__ void __launch_bounds__(kThreads + 32, 1) admit_kernel(DevPool P, Admi
             }
         }
         __syncthreads();
+        apply_table_queue(P, Red);  // the previous admission's erases / inserts
         // deferred EngineSim::unpin calls of completed requests (engine.cpp:170-180), in order
         if (a.n_unpin_ranges > 0) {
             long long dec = 0;
@@ -1544,6 +1671,7 @@ __global__ void __launch_bounds__(kThreads + 32, 1) admit_kernel(DevPool P, Admi
             }
         }
         const int slow = __syncthreads_or(tid < NL && !(P.ghint[tid] < kNoBound) && !P.gsmall[tid]);
+        if (blockIdx.x == 0) replay_prologue(P, Rp, A, Red);  // the lists are not needed for it
         stamp(A, 1);
         scan_pass(P, NL, keep0, B, S, Sel, dsm, !slow, a);
         grid_barrier(C);
@@ -1562,12 +1690,14 @@ __global__ void __launch_bounds__(kThreads + 32, 1) admit_kernel(DevPool P, Admi
         } else {
             if (tid == 0) {
                 const unsigned int want = (unsigned int)(NL - mine);
+                const unsigned long long tw = gtimer();
                 unsigned long long spins = 0;
                 while (ld_acquire(&C->fin_done) < want) {
                     if (++spins > 4096) __nanosleep(64);
                     if (spins > (1ull << 27)) __trap();
                 }
                 __threadfence();
+                A.ph[15] += gtimer() - tw;  // instrumentation: CTA 0 waiting for the other lists
             }
             __syncthreads();
             stamp(A, 3);
@@ -1680,6 +1810,7 @@ __global__ void __launch_bounds__(kThreads + 32, 1) admit_kernel(DevPool P, Admi
             }
         }
         if (blockIdx.x == 0 && !pending_rescan) {
+            replay_prologue(P, Rp, A, Red);
             replay_apply(P, a, Rp, A, NL, need_scan != 0, Red);
             if (tid == 0) A.chunk += 1;
             __syncthreads();

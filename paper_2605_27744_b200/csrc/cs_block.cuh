@@ -54,6 +54,7 @@ struct SelectSmem {
     unsigned int hist[256];
     unsigned long long acc_or, acc_and;
     unsigned long long prefix;
+    unsigned long long hmax;  // finalize_list: largest candidate written for the list
     int k;
     int tmp;
 };

@@ -77,6 +77,7 @@ struct Ctrl {
     int pass;          // scan pass of the current chunk (1 = safe, no hints)
     long long rescans; // instrumentation
     unsigned long long p0_seq;  // AdmitArgs::seq of the launch whose phase 0 finished
+    int tq_erase, tq_insert;    // block-table updates queued by the last admission (applied next)
 };
 
 struct DevPool {
@@ -133,6 +134,10 @@ struct DevPool {
     unsigned int* p_slot;
     unsigned int* p_refs0;
     long long p_cap;
+    // block-table updates of the last admission, applied at the start of the next launch
+    // (erase keys at [0, p_cap), insert keys at [p_cap, 2 p_cap) with their slots)
+    unsigned long long* tq_key;
+    unsigned int* tq_slot;
 
     Ctrl* ctrl;
 };

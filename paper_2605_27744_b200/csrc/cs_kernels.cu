@@ -64,6 +64,8 @@ __global__ void init_pool_kernel(DevPool P) {
         C->fin_done = 0u;
         C->rescan = 0;
         C->p0_seq = 0ull;
+        C->tq_erase = 0;
+        C->tq_insert = 0;
     }
 }
 
@@ -257,7 +259,11 @@ __global__ void table_fill_kernel(DevPool P) {
          s += (long long)gridDim.x * blockDim.x) {
         if (P.lt[s] != kFreeTick) table_insert(P, P.key[s], (unsigned int)s);
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) P.ctrl->tombstones = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        P.ctrl->tombstones = 0;
+        P.ctrl->tq_erase = 0;  // the SoA is the truth: queued table updates are subsumed
+        P.ctrl->tq_insert = 0;
+    }
 }
 
 // ------------------------------------------------------------------ host launchers

@@ -116,6 +116,8 @@ void cs_pool::create(const cs_pool_cfg& c) {
     p.p_cap = 0;
     p.p_slot = nullptr;
     p.p_refs0 = nullptr;
+    p.tq_key = nullptr;
+    p.tq_slot = nullptr;
     ensure_prompt_scratch(4096);
 
     if (const char* e = std::getenv("CS_SPECULATE")) speculate = std::atoi(e) != 0;  // A/B switch (tools)
@@ -139,7 +141,7 @@ void cs_pool::destroy() {
     csb::DevPool& p = P;
     void* ptrs[] = {p.lt, p.agent, p.refs, p.key, p.tokens, p.table, p.free_stack, p.evlog, p.counts, p.totals,
                     p.win_a, p.win_b, p.hop, p.cls, p.agent_ids, p.ctrl, p.gbound, p.gcount, p.fin_lt, p.fin_slot,
-                    p.fin_n, p.p_slot, p.p_refs0, p.gbuf_lt, p.gbuf_slot, p.ghint, p.gmaxk, p.grej, p.dbg, p.gsmall, p.gmin};
+                    p.fin_n, p.p_slot, p.p_refs0, p.gbuf_lt, p.gbuf_slot, p.ghint, p.gmaxk, p.grej, p.dbg, p.gsmall, p.gmin, p.tq_key, p.tq_slot};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     d_keys.release();
@@ -158,13 +160,24 @@ void cs_pool::ensure_prompt_scratch(long long n) {
     if (n <= P.p_cap) return;
     long long c = std::max<long long>(n, P.p_cap * 2);
     if (P.p_slot) {
+        ck(csb::launch_table_flush(P, stream), "table flush");  // the queue lives in this scratch
+        ++launches;
         ck(cudaStreamSynchronize(stream), "sync");
         cudaFree(P.p_slot);
         cudaFree(P.p_refs0);
+        cudaFree(P.tq_key);
+        cudaFree(P.tq_slot);
     }
     P.p_slot = dmalloc<unsigned int>(c, "p_slot");
     P.p_refs0 = dmalloc<unsigned int>(c, "p_refs0");
+    P.tq_key = dmalloc<unsigned long long>(2 * c, "tq_key");
+    P.tq_slot = dmalloc<unsigned int>(c, "tq_slot");
     P.p_cap = c;
+}
+
+void cs_pool::flush_table() {
+    ck(csb::launch_table_flush(P, stream), "table flush");
+    ++launches;
 }
 
 const csb::AdmitStatus& cs_pool::admit(const csb::AdmitArgs& in, int n_for_grid) {
@@ -409,6 +422,7 @@ int cs_probe_needed(cs_pool_t pool, const uint64_t* keys, int n, int* needed) {
     return guard([&] {
         if (!pool || n < 0 || (n > 0 && !keys) || !needed) throw std::invalid_argument("cs_probe_needed: null argument");
         pool->flush_unpins();
+        pool->flush_table();
         stage_prompt(pool, keys, nullptr, n);
         pool->d_aux.ensure(sizeof(int));
         ck(csb::launch_probe(pool->P, pool->d_keys.as<unsigned long long>(), n, pool->d_aux.as<int>(), pool->stream),
@@ -488,6 +502,7 @@ int cs_restore(cs_pool_t pool, const uint64_t* keys, const uint64_t* lt, const u
     return guard([&] {
         if (!pool || n < 0 || (n > 0 && (!keys || !lt))) throw std::invalid_argument("cs_restore: null argument");
         pool->flush_unpins();
+        pool->flush_table();
         if (pool->resident + n > pool->P.cap) throw std::invalid_argument("cs_restore: snapshot exceeds the budget");
         if (n == 0) return;
         cudaStream_t s = pool->stream;

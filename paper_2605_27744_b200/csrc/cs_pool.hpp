@@ -92,5 +92,7 @@ struct cs_pool {
     // launch (or in flush_unpins, before any other pool operation reads pins).
     void defer_unpin(const unsigned int* dev_slots, int n);
     void flush_unpins();
+    // Applies queued block-table updates (admissions defer them to the next launch's phase 0).
+    void flush_table();
     void sync() { csb::ck(cudaStreamSynchronize(stream), "cudaStreamSynchronize"); }
 };
