@@ -53,6 +53,7 @@ struct ScanSmem {
     int spec;       // speculative pass: phase 0 runs concurrently on CTA 0
     int hc, dc;     // ensure_cls compaction counters
     int prep_done;  // the producer warp already loaded the classes and built the change set
+    unsigned char hinted[kMaxLists];  // CTA 0: the lists that had a hint in this launch's first pass
     int cls_ready;  // B.cls holds this launch's classes (else kPend for every agent)
     unsigned int xset[kXset];  // slots phase 0 may change: excluded here, restaged fresh by CTA 0
     __align__(8) unsigned long long mbar[kRing];        // TMA ring: stage filled
@@ -64,6 +65,8 @@ struct AdmSmem {
     unsigned long long first_touch;  // earliest tick admit_pinned touched in this admission
     long long cached, n_ev_adm, resident, pinned, free_top;
     int first_miss, admit_n, anchor, chunk, started, error, needed, warm_issued, scans;
+    int fin_want;  // lists finalized by CTAs other than 0 in the current pass
+    double wsurv[kMaxLists];  // P.wsurv staged on chip (indexed kernel-parameter loads are slow)
     unsigned long long ph[kPhases], tl;  // phase timestamps (CTA 0, thread 0)
 };
 
@@ -157,6 +160,16 @@ __device__ __forceinline__ void stamp(AdmSmem& A, int k) {
         A.ph[k] += t - A.tl;
         A.tl = t;
     }
+}
+
+// CTA-0 sub-phase timestamps of the replay (instrumentation row 0, columns 10..15)
+__device__ __forceinline__ void dstamp(const DevPool& P, int k) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) P.dbg[10 + k] = clock64();
+}
+
+// CTA-0 sub-phase SM-clock stamps of finalize_list (instrumentation row 2, columns 10..15)
+__device__ __forceinline__ void fstamp(const DevPool& P, int k) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) P.dbg[32 + 10 + k] = clock64();
 }
 
 // ------------------------------------------------------------------ K3 / K3b / K6
@@ -613,8 +626,10 @@ __device__ void build_xset(const DevPool& P, const AdmitArgs& a, ScanSmem& S) {
         const unsigned int s = __ldcg(P.p_slot + i);
         if (s != kNoSlot) xset_insert(S, s);
     }
-    for (int r = 0; r < a.n_unpin_ranges; ++r)
-        for (int i = tid; i < a.unpin_n[r]; i += T) xset_insert(S, a.unpin_ptr[r][i]);
+#pragma unroll
+    for (int r = 0; r < kMaxUnpinRanges; ++r)  // constant indices into the kernel parameters
+        if (r < a.n_unpin_ranges)
+            for (int i = tid; i < a.unpin_n[r]; i += T) xset_insert(S, a.unpin_ptr[r][i]);
     __syncthreads();
 }
 
@@ -712,8 +727,10 @@ __device__ void producer_prep(const DevPool& P, const AdmitArgs& a, const ScanBu
         const unsigned int sl = __ldcg(P.p_slot + i);
         if (sl != kNoSlot) xset_insert(S, sl);
     }
-    for (int r = 0; r < a.n_unpin_ranges; ++r)
-        for (int i = lane; i < a.unpin_n[r]; i += 32) xset_insert(S, a.unpin_ptr[r][i]);
+#pragma unroll
+    for (int r = 0; r < kMaxUnpinRanges; ++r)
+        if (r < a.n_unpin_ranges)
+            for (int i = lane; i < a.unpin_n[r]; i += 32) xset_insert(S, a.unpin_ptr[r][i]);
     __syncwarp();
     if (lane == 0) S.prep_done = 1;
 }
@@ -959,6 +976,7 @@ __device__ void finalize_list(const DevPool& P, int l, int NL, int keep, const S
     // <= v*), so this bound is >= v* and keeps the whole answer, and at least kl written
     // candidates are <= it. It cuts the ~grid*kl written candidates to ~kl.
     const int G = gridDim.x;
+    fstamp(P, 0);
     unsigned long long* mins = B.sd_lt;  // G <= kSide minima staged on chip
     if (tid == 0) {
         Sel.tmp = 0;
@@ -975,6 +993,7 @@ __device__ void finalize_list(const DevPool& P, int l, int NL, int keep, const S
         if (r == kl - 1) Sel.prefix = x;
     }
     __syncthreads();
+    fstamp(P, 1);
     const unsigned long long fb = Sel.prefix;
     // stage the filtered candidates on chip when they fit (the common case), else select from L2
     unsigned long long hm = 0ull;
@@ -992,6 +1011,7 @@ __device__ void finalize_list(const DevPool& P, int l, int NL, int keep, const S
     for (int o = 16; o; o >>= 1) hm = max(hm, __shfl_xor_sync(0xffffffffu, hm, o));
     if (lane_id() == 0 && hm) atomicMax(&Sel.hmax, hm);
     __syncthreads();
+    fstamp(P, 2);
     const int mf = Sel.tmp;
     const bool local = mf <= kStage;
     const unsigned long long* src = local ? B.st_lt : g;
@@ -1009,8 +1029,11 @@ __device__ void finalize_list(const DevPool& P, int l, int NL, int keep, const S
                 P.fin_slot[(long long)l * (kChunk + 2) + r] = srs[j];
             }
         }
+        fstamp(P, 3);
         if (tid == 0) finish_list(P, l, min(mf, kl), kl, Sel.hmax);
         __syncthreads();
+        fstamp(P, 4);
+        if (blockIdx.x == 0 && tid == 0) P.dbg[32 + 15] = (unsigned long long)mf | ((unsigned long long)m << 32);
         return;
     }
     unsigned long long v = ~0ull;
@@ -1112,8 +1135,32 @@ __device__ void replay_prologue(const DevPool& P, ReplaySmem& R, const AdmSmem& 
 // replay_prologue. Each eviction is evict_one (engine.cpp:102-125): the argmin of
 // (score, last_touch) over the class heads; oldest_live_touch (engine.cpp:90-100) = min(tick,
 // resident-list head, earliest touch of this admission). One warp; lane l owns list l.
+// Loads the final candidate lists (all, or only E and R) from the finalizers' output: counts
+// into shared memory first, then every entry in one round.
+__device__ void load_lists(const DevPool& P, ReplaySmem& R, int NL, bool scanned, bool only_er) {
+    const int tid = threadIdx.x, T = blockDim.x;
+    const int E = P.e_max, Rl = NL - 1;
+    if (tid < NL) {
+        const bool mine = !only_er || tid == E || tid == Rl;
+        // a class list that is not final yet: 1 marks "non-empty" (all the bulk test needs)
+        R.L_n[tid] = !scanned ? 0 : mine ? P.fin_n[tid] : (P.gcount[tid] > 0 ? 1 : 0);
+    }
+    __syncthreads();
+    for (int q = tid; q < NL * (kChunk + 2); q += T) {
+        const int l = q / (kChunk + 2), j = q - l * (kChunk + 2);
+        if (only_er && l != E && l != Rl) continue;
+        if (j < R.L_n[l]) {
+            R.L_lt[l][j] = P.fin_lt[q];
+            R.L_slot[l][j] = P.fin_slot[q];
+        }
+    }
+    __syncthreads();
+}
+
+// early: only lists E and R are final (CTA 0 finalized E, CTA 1 signalled R); the other
+// lists are awaited only if the bulk test fails.
 __device__ void replay_apply(const DevPool& P, const AdmitArgs& a, ReplaySmem& R, AdmSmem& A, int NL, bool scanned,
-                             RedSmem& Red) {
+                             RedSmem& Red, bool early = false) {
     Ctrl* C = P.ctrl;
     const int tid = threadIdx.x, T = blockDim.x;
     const int lo = A.chunk * kChunk;
@@ -1121,18 +1168,12 @@ __device__ void replay_apply(const DevPool& P, const AdmitArgs& a, ReplaySmem& R
     const int len = hi - lo;
     const int Rl = NL - 1;
     const long long ftop = R.ftop;
+    early = early && scanned;
+    dstamp(P, 0);
 
-    // ---- the candidate lists (one round trip: counts first into shared memory, then all entries)
-    if (tid < NL) R.L_n[tid] = scanned ? P.fin_n[tid] : 0;
-    __syncthreads();
-    for (int q = tid; q < NL * (kChunk + 2); q += T) {
-        const int l = q / (kChunk + 2), j = q - l * (kChunk + 2);
-        if (j < R.L_n[l]) {
-            R.L_lt[l][j] = P.fin_lt[q];
-            R.L_slot[l][j] = P.fin_slot[q];
-        }
-    }
-    __syncthreads();
+    // ---- the candidate lists
+    load_lists(P, R, NL, scanned, early);
+    dstamp(P, 1);
     // Bulk replay (the common case, no serial loop): when the victims are the first n_ev
     // class-E candidates, all inside the dominance prefix (below) and none of them a prompt
     // block of this chunk, the sequential replay reduces to: the absent block of rank r takes a
@@ -1151,7 +1192,7 @@ __device__ void replay_apply(const DevPool& P, const AdmitArgs& a, ReplaySmem& R
     if (P.policy == 1) {
         if (!(P.w_pred > 0.0)) dom_ok = false;
         for (int c = 0; c < E; ++c)
-            if (R.L_n[c] > 0) dom_bound = fmin(dom_bound, __dmul_rn(P.w_pred, survival_of_class(c, E)));
+            if (R.L_n[c] > 0) dom_bound = fmin(dom_bound, A.wsurv[c]);
     }
     const unsigned long long tick0 = A.tick;
     unsigned long long old0 = tick0;
@@ -1174,10 +1215,13 @@ __device__ void replay_apply(const DevPool& P, const AdmitArgs& a, ReplaySmem& R
         const int n_free = (int)min((long long)absent, room > 0 ? room : 0ll);
         const int n_ev = absent - n_free;
         int bad = n_ev > R.L_n[E] || (n_ev > 0 && !dom_ok);
+        if (blockIdx.x == 0 && tid == 0) P.dbg[48 + 10] = clock64();
         // a needed victim that is one of this chunk's prompt blocks, or outside the prefix
         for (int j = tid; !bad && j < n_ev; j += T) bad |= prompt_index(R.L_slot[E][j]) >= 0;
         if (!bad && tid == 0 && n_ev > 0) bad = !(recency(R.L_lt[E][n_ev - 1], tick0, old0) < dom_bound);
+        if (blockIdx.x == 0 && tid == 0) P.dbg[48 + 11] = clock64();
         const bool bulk = !__syncthreads_or(bad);
+        dstamp(P, 2);
         if (bulk) {
             // exclusive rank of each absent block (len <= kChunk = 128: 4 warps)
             __shared__ int wsum[kChunk / 32];
@@ -1220,6 +1264,18 @@ __device__ void replay_apply(const DevPool& P, const AdmitArgs& a, ReplaySmem& R
         if (tid == 0) R.bulk = bulk ? 1 : 0;
         __syncthreads();
     }
+    if (!R.bulk && early) {  // the serial replay needs every list: wait for the other finalizers
+        if (tid == 0) {
+            unsigned long long spins = 0;
+            while (ld_acquire(&C->fin_done) < (unsigned int)A.fin_want) {
+                if (++spins > 4096) __nanosleep(64);
+                if (spins > (1ull << 27)) __trap();
+            }
+            __threadfence();
+        }
+        __syncthreads();
+        load_lists(P, R, NL, scanned, false);
+    }
     if (!R.bulk) {
         // serial path: per list entry, the prompt index (a touch removes it) and the position in
         // the resident list (an eviction from a class list removes it there too); pdom in full
@@ -1256,13 +1312,14 @@ __device__ void replay_apply(const DevPool& P, const AdmitArgs& a, ReplaySmem& R
         __syncthreads();
     }
     stamp(A, 6);
+    dstamp(P, 3);
 
     // ---- the sequential replay (warp 0)
     if (warp_id() == 0 && !R.bulk) {
         const int lane = lane_id();
         int cursor = 0;
         const int my_n = lane < NL ? R.L_n[lane] : 0;
-        const double my_surv = survival_of_class(lane, P.e_max);
+        const double my_ws = lane < kMaxLists ? A.wsurv[lane] : 0.0;
         unsigned long long tick = A.tick;
         unsigned long long first_touch = A.first_touch;
         long long resident = R.res0;
@@ -1329,7 +1386,8 @@ __device__ void replay_apply(const DevPool& P, const AdmitArgs& a, ReplaySmem& R
                 unsigned long long sk = ~0ull, lk = ~0ull;
                 if (lane < Rl && cursor < my_n) {
                     lk = R.L_lt[lane][cursor];
-                    sk = (unsigned long long)__double_as_longlong(score_of(P.policy, P.w_pred, my_surv, lk, tick, old));
+                    const double rho = recency(lk, tick, old);
+                    sk = (unsigned long long)__double_as_longlong(P.policy == 0 ? rho : __dadd_rn(my_ws, rho));
                 }
                 const unsigned int m1 = __reduce_min_sync(0xffffffffu, (unsigned int)(sk >> 32));
                 if (m1 == 0xffffffffu) {
@@ -1410,6 +1468,7 @@ __device__ void replay_apply(const DevPool& P, const AdmitArgs& a, ReplaySmem& R
         }
     }
     __syncthreads();
+    dstamp(P, 4);
     const int q_e = C->tq_erase, q_i = C->tq_insert;  // table updates are queued for the next launch
     for (int k = tid; k < nv; k += T) {
         const unsigned long long kk = R.vkey[k];
@@ -1475,6 +1534,7 @@ __device__ void replay_apply(const DevPool& P, const AdmitArgs& a, ReplaySmem& R
     }
     __syncthreads();
     stamp(A, 8);
+    dstamp(P, 5);
 }
 
 // Applies the block-table updates queued by the previous admission (all threads of one CTA):
@@ -1565,6 +1625,8 @@ __global__ void __launch_bounds__(kThreads + 32, 1) admit_kernel(DevPool P, Admi
             A.first_touch = ~0ull;
             A.tick = a.tick_base;
             for (int k = 0; k < kPhases; ++k) A.ph[k] = 0;
+#pragma unroll
+            for (int c = 0; c < kMaxLists; ++c) A.wsurv[c] = P.wsurv[c];  // constant indices
             A.tl = gtimer();
             C->done = 0;
             C->error = 0;
@@ -1578,9 +1640,11 @@ __global__ void __launch_bounds__(kThreads + 32, 1) admit_kernel(DevPool P, Admi
         // deferred EngineSim::unpin calls of completed requests (engine.cpp:170-180), in order
         if (a.n_unpin_ranges > 0) {
             long long dec = 0;
-            for (int r = 0; r < a.n_unpin_ranges; ++r)
-                for (int i = tid; i < a.unpin_n[r]; i += T)
-                    if (atomicSub(&P.refs[a.unpin_ptr[r][i]], 1u) == 1u) ++dec;
+#pragma unroll
+            for (int r = 0; r < kMaxUnpinRanges; ++r)
+                if (r < a.n_unpin_ranges)
+                    for (int i = tid; i < a.unpin_n[r]; i += T)
+                        if (atomicSub(&P.refs[a.unpin_ptr[r][i]], 1u) == 1u) ++dec;
             dec = block_sum(dec, Red);
             if (tid == 0) C->pinned -= dec;
             __syncthreads();
@@ -1670,6 +1734,7 @@ __global__ void __launch_bounds__(kThreads + 32, 1) admit_kernel(DevPool P, Admi
                 C->keep = keep0;  // a rescan of this chunk keeps the same candidate count
             }
         }
+        if (tid < NL) S.hinted[tid] = P.ghint[tid] < kNoBound ? 1 : 0;  // before any finalizer rewrites it
         const int slow = __syncthreads_or(tid < NL && !(P.ghint[tid] < kNoBound) && !P.gsmall[tid]);
         if (blockIdx.x == 0) replay_prologue(P, Rp, A, Red);  // the lists are not needed for it
         stamp(A, 1);
@@ -1677,38 +1742,60 @@ __global__ void __launch_bounds__(kThreads + 32, 1) admit_kernel(DevPool P, Admi
         grid_barrier(C);
         if (tid == 0) P.dbg[blockIdx.x * 16 + 4] = gtimer();
         stamp(A, 2);
+        // list owners: CTA 0 selects class E (the one the bulk replay consumes), CTA 1 the
+        // resident list, CTAs 2.. the other classes; CTA 0 waits only for the resident list
+        const int Ev = P.e_max, Rv = NL - 1;
         int mine = 0;
-        for (int l = blockIdx.x; l < NL; l += gridDim.x) {
+        for (int l = 0; l < NL; ++l) {
+            const int owner = (l == Ev ? 0 : l == Rv ? 1 : 2 + l) % (int)gridDim.x;
+            if (owner != (int)blockIdx.x) continue;
             finalize_list(P, l, NL, keep0, B, Sel);
             ++mine;
+            if (l == Rv && tid == 0) {
+                __threadfence();
+                asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(&C->r_seq), "l"(a.seq) : "memory");
+            }
         }
+        if (tid == 0 && blockIdx.x < 2) P.dbg[16 + 10 + blockIdx.x] = gtimer();  // finalize ends
         if (blockIdx.x != 0) {
             if (tid == 0 && mine) {
                 __threadfence();
                 atomicAdd(&C->fin_done, (unsigned int)mine);
             }
         } else {
+            // a hinted list that came up short (finalize_list's test, from the counts alone)
+            const int short_hint = __syncthreads_or(tid < NL && S.hinted[tid] &&
+                                                    *(volatile int*)(P.gcount + tid) < keep_of(tid, NL, keep0));
             if (tid == 0) {
-                const unsigned int want = (unsigned int)(NL - mine);
                 const unsigned long long tw = gtimer();
                 unsigned long long spins = 0;
-                while (ld_acquire(&C->fin_done) < want) {
+                while (ld_acquire_u64(&C->r_seq) != a.seq) {
                     if (++spins > 4096) __nanosleep(64);
                     if (spins > (1ull << 27)) __trap();
                 }
                 __threadfence();
-                A.ph[15] += gtimer() - tw;  // instrumentation: CTA 0 waiting for the other lists
+                A.ph[15] += gtimer() - tw;  // instrumentation: CTA 0 waiting for the resident list
             }
+            if (tid == 0) A.fin_want = NL - mine;
             __syncthreads();
             stamp(A, 3);
-            pending_rescan = *(volatile int*)&C->rescan != 0;
+            pending_rescan = short_hint || *(volatile int*)&C->rescan != 0;
             const bool stop = !A.started || A.error || A.admit_n <= 0;
             if (!pending_rescan && !stop) {
-                replay_apply(P, a, Rp, A, NL, need_scan0 != 0, Red);
+                replay_apply(P, a, Rp, A, NL, need_scan0 != 0, Red, true);
                 if (tid == 0) A.chunk = 1;
                 __syncthreads();
                 stamp(A, 4);
             }
+            // every finalizer of this pass is done before the command loop resets its state
+            if (tid == 0) {
+                unsigned long long spins = 0;
+                while (ld_acquire(&C->fin_done) < (unsigned int)A.fin_want) {
+                    if (++spins > 4096) __nanosleep(64);
+                    if (spins > (1ull << 27)) __trap();
+                }
+            }
+            __syncthreads();
         }
         if (tid == 0) S.spec = 0;
         __syncthreads();

@@ -78,6 +78,7 @@ struct Ctrl {
     long long rescans; // instrumentation
     unsigned long long p0_seq;  // AdmitArgs::seq of the launch whose phase 0 finished
     int tq_erase, tq_insert;    // block-table updates queued by the last admission (applied next)
+    unsigned long long r_seq;   // AdmitArgs::seq once the resident-oldest list is final
 };
 
 struct DevPool {
@@ -88,6 +89,7 @@ struct DevPool {
     int n_lists;              // e_max + 2 (classes 0..e_max, resident list last)
     int a_cap;
     double tau, w_pred, min_conf;
+    double wsurv[kMaxLists];  // fl(w_pred * survival(c)) per class c <= e_max, host-computed (no FMA)
     unsigned long long min_row;
     int budget_per_step;
     long long window;

@@ -121,6 +121,14 @@ void cs_pool::create(const cs_pool_cfg& c) {
     ensure_prompt_scratch(4096);
 
     if (const char* e = std::getenv("CS_SPECULATE")) speculate = std::atoi(e) != 0;  // A/B switch (tools)
+    // fl(w_pred * (1 - min(c, e_max) / e_max)) per survival class, as CacheSagePolicy::score and
+    // ReachabilityState::survival compute it (reachability.cpp:17-20); host code builds with
+    // -ffp-contract=off, so the product is the same IEEE double the device would form
+    for (int cl = 0; cl < csb::kMaxLists; ++cl) {
+        const int cap = cl < p.e_max ? cl : p.e_max;
+        const double surv = 1.0 - (double)cap / (double)p.e_max;
+        p.wsurv[cl] = p.w_pred * surv;
+    }
     lc = csb::admit_launch_config(p, device, c.grid_ctas);
     if (lc.grid <= 0) throw CsError(CS_ERR_CUDA, "admit kernel: no launch configuration fits this device");
     p.gcap = (long long)lc.grid * (csb::kChunk + 1);

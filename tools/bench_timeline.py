@@ -31,3 +31,13 @@ for it in range(6):
           f"flush end max {o[:, 2].max():.1f}; writeout max {o[:, 3].max():.1f}; barrier exit {rel[:, 4].max():.1f}; "
           f"cta0 scan start {rel[0, 0]:.1f} flush end {rel[0, 2]:.1f} writeout {rel[0, 3]:.1f}; staged med {np.median(d[1:, 5]):.0f} "
           f"max {d[1:, 5].max()}; fast {bool(d[1, 8])}")
+    b = d[:, 4].max()
+    print("  after barrier (us): finalize end cta1/cta0 %.1f/%.1f" % tuple((np.array([d[1, 10], d[1, 11]]) - b) / 1e3))
+    c = d[0, 10:16].astype(np.float64)
+    f = d[2, 10:15].astype(np.float64)
+    mhz = 1965.0
+    print("  replay (us from start, SM clock): lists %.2f checks-start %.2f checks-end %.2f bulk %.2f setup-end %.2f "
+          "vkeys %.2f apply-end %.2f" % ((c[1] - c[0]) / mhz, (d[3, 10] - c[0]) / mhz, (d[3, 11] - c[0]) / mhz,
+                                         (c[2] - c[0]) / mhz, (c[3] - c[0]) / mhz, (c[4] - c[0]) / mhz, (c[5] - c[0]) / mhz))
+    print("  finalize E by CTA0 (us): minima %.2f filter %.2f rank %.2f finish %.2f; mf %d m %d" % (
+        (f[1] - f[0]) / mhz, (f[2] - f[0]) / mhz, (f[3] - f[0]) / mhz, (f[4] - f[0]) / mhz, d[2, 15] & 0xffffffff, d[2, 15] >> 32))
