@@ -210,6 +210,41 @@ int64_t cs_engine_evictions(cs_engine_t e, uint64_t* keys, int64_t cap);
 int64_t cs_engine_warmups(cs_engine_t e, int64_t* step, uint64_t* target, uint64_t* tick, int64_t cap);
 cs_pool_t cs_engine_pool(cs_engine_t e);
 
+/* ------------------------------------------------------------------ hash-sharded pool
+ *
+ * one pool of GLOBAL budget N split over G <= 8 GPUs, block key k on shard
+ * (k >> 40) % G. Each shard scans and k-selects its own slots; per admission the shards
+ * exchange (allgather) their probe results and, per chunk that can evict, their per-class
+ * candidate lists, and every shard then runs the same exact evict_one replay. Every shard
+ * returns the decisions one pool of budget N makes: the same hits, victims (in order) and
+ * warmups. The reference has no sharding; the replay is EngineSim::admit_pinned /
+ * evict_one (engine.cpp:102-168) over the union of the shard candidates. */
+typedef struct cs_comm* cs_comm_t;
+
+/* Host allgather for the callback transport: recv[r * bytes .. ) = rank r's send. 0 = ok. */
+typedef int (*cs_allgather_fn)(void* ctx, const void* send, void* recv, size_t bytes_per_rank);
+
+/* world handles for world shards driven by world threads of this process (device-to-device
+ * copies between the shards' buffers; the shards may share one device). */
+int cs_comm_local_group(int world, cs_comm_t* comms_out);
+/* Exchange through host memory and a caller-supplied allgather (e.g. torch.distributed). */
+int cs_comm_callback(int rank, int world, cs_allgather_fn fn, void* ctx, cs_comm_t* out);
+/* NCCL (ncclAllGather over NVLink / NVSwitch), one process per GPU. Rank 0 creates the id and
+ * the caller broadcasts its 128 bytes; libnccl.so.2 is loaded at run time (CS_NCCL_LIB). */
+int cs_nccl_unique_id(uint8_t* id128);
+int cs_comm_nccl(const uint8_t* id128, int rank, int world, int device, cs_comm_t* out);
+int cs_comm_destroy(cs_comm_t comm);
+/* The shard that owns a block key. */
+int cs_shard_owner(uint64_t key, int world);
+
+/* A shard of a sharded pool: cfg->budget_blocks is the GLOBAL budget N; shard_slots the
+ * shard's physical slot count (0 = 1.25 N / world + 4096). The comm is borrowed. */
+int cs_pool_create_sharded(const cs_pool_cfg* cfg, int64_t shard_slots, cs_comm_t comm, cs_pool_t* out);
+/* The EngineSim of one shard: every shard runs the same trace and scheduler; cs_engine_restore
+ * keeps only the snapshot blocks this shard owns. */
+int cs_engine_create_sharded(const cs_engine_cfg* cfg, const cs_workload_spec* spec, int64_t shard_slots,
+                             cs_comm_t comm, cs_engine_t* out);
+
 const char* cs_last_error(void);
 const char* cs_version(void);
 

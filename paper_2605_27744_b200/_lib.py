@@ -106,6 +106,15 @@ SIGNATURES = {
     "cs_engine_evictions": (C.c_int64, [vp, vp, C.c_int64]),
     "cs_engine_warmups": (C.c_int64, [vp, vp, vp, vp, C.c_int64]),
     "cs_engine_pool": (vp, [vp]),
+    "cs_comm_local_group": (C.c_int, [C.c_int, vp]),
+    "cs_comm_callback": (C.c_int, [C.c_int, C.c_int, vp, vp, C.POINTER(vp)]),
+    "cs_nccl_unique_id": (C.c_int, [vp]),
+    "cs_comm_nccl": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.POINTER(vp)]),
+    "cs_comm_destroy": (C.c_int, [vp]),
+    "cs_shard_owner": (C.c_int, [C.c_uint64, C.c_int]),
+    "cs_pool_create_sharded": (C.c_int, [C.POINTER(PoolCfg), C.c_int64, vp, C.POINTER(vp)]),
+    "cs_engine_create_sharded": (C.c_int, [C.POINTER(EngineCfg), C.POINTER(WorkloadSpec), C.c_int64, vp,
+                                           C.POINTER(vp)]),
     "cs_last_error": (C.c_char_p, []),
     "cs_version": (C.c_char_p, []),
 }

@@ -224,7 +224,10 @@ class Engine:
     """EngineSim (engine.hpp:90-208) with the block pool, learner and eviction on the GPU."""
 
     def __init__(self, spec, policy="cachesage", budget=None, concurrency=None, block_size=16, prefetch=True,
-                 skip=4, take=4, timing=False, host_inputs=False, **pool_kw):
+                 skip=4, take=4, timing=False, host_inputs=False, comm=None, shard_slots=0, **pool_kw):
+        """comm (shard.Comm): this engine drives ONE shard of a hash-sharded pool of global
+        budget `budget`; every shard runs the same trace and reaches the same
+        decisions. shard_slots: the shard's physical slots (0 = 1.25 budget / world + 4096)."""
         cfg = EngineCfg()
         lib().cs_engine_cfg_default(C.byref(cfg))
         cfg.pool = pool_cfg(budget or 0, policy=policy, **pool_kw)
@@ -236,7 +239,12 @@ class Engine:
         cfg.host_inputs = 1 if host_inputs else 0
         self._spec = spec_struct(spec)
         h = C.c_void_p()
-        check(lib().cs_engine_create(C.byref(cfg), C.byref(self._spec), C.byref(h)))
+        self.comm = comm
+        if comm is None:
+            check(lib().cs_engine_create(C.byref(cfg), C.byref(self._spec), C.byref(h)))
+        else:
+            check(lib().cs_engine_create_sharded(C.byref(cfg), C.byref(self._spec), int(shard_slots), comm.h,
+                                                 C.byref(h)))
         self.h = h
 
     def close(self):

@@ -629,7 +629,8 @@ __device__ void build_xset(const DevPool& P, const AdmitArgs& a, ScanSmem& S) {
 #pragma unroll
     for (int r = 0; r < kMaxUnpinRanges; ++r)  // constant indices into the kernel parameters
         if (r < a.n_unpin_ranges)
-            for (int i = tid; i < a.unpin_n[r]; i += T) xset_insert(S, a.unpin_ptr[r][i]);
+            for (int i = tid; i < a.unpin_n[r]; i += T)
+                if (a.unpin_ptr[r][i] != kNoSlot) xset_insert(S, a.unpin_ptr[r][i]);
     __syncthreads();
 }
 
@@ -730,7 +731,8 @@ __device__ void producer_prep(const DevPool& P, const AdmitArgs& a, const ScanBu
 #pragma unroll
     for (int r = 0; r < kMaxUnpinRanges; ++r)
         if (r < a.n_unpin_ranges)
-            for (int i = lane; i < a.unpin_n[r]; i += 32) xset_insert(S, a.unpin_ptr[r][i]);
+            for (int i = lane; i < a.unpin_n[r]; i += 32)
+                if (a.unpin_ptr[r][i] != kNoSlot) xset_insert(S, a.unpin_ptr[r][i]);
     __syncwarp();
     if (lane == 0) S.prep_done = 1;
 }
@@ -1643,8 +1645,10 @@ __global__ void __launch_bounds__(kThreads + 32, 1) admit_kernel(DevPool P, Admi
 #pragma unroll
             for (int r = 0; r < kMaxUnpinRanges; ++r)
                 if (r < a.n_unpin_ranges)
-                    for (int i = tid; i < a.unpin_n[r]; i += T)
-                        if (atomicSub(&P.refs[a.unpin_ptr[r][i]], 1u) == 1u) ++dec;
+                    for (int i = tid; i < a.unpin_n[r]; i += T) {
+                        const unsigned int us = a.unpin_ptr[r][i];
+                        if (us != kNoSlot && atomicSub(&P.refs[us], 1u) == 1u) ++dec;
+                    }
             dec = block_sum(dec, Red);
             if (tid == 0) C->pinned -= dec;
             __syncthreads();
@@ -1934,6 +1938,10 @@ __global__ void __launch_bounds__(kThreads + 32, 1) admit_kernel(DevPool P, Admi
         }
     }
 }
+
+// ------------------------------------------------------------------ hash-sharded pool
+
+#include "cs_shard.cuh"
 
 // ------------------------------------------------------------------ host side
 

@@ -81,6 +81,42 @@ struct Ctrl {
     unsigned long long r_seq;   // AdmitArgs::seq once the resident-oldest list is final
 };
 
+// ---------------------------------------------------------------- hash-sharded pool
+// A pool of budget N split over G GPUs: a block lives on shard owner(key) = (key >> 40) % G.
+// Slots are named across shards by gslot = shard << kShardBits | local slot.
+constexpr int kShardBits = 29;
+constexpr unsigned int kShardMask = (1u << kShardBits) - 1u;
+constexpr int kMaxShards = 8;
+constexpr unsigned int kNewRemote = 0xFFFFFFFCu;  // new block inserted on another shard
+
+__host__ __device__ __forceinline__ int shard_owner(unsigned long long key, int world) {
+    return (int)((key >> 40) % (unsigned long long)world);
+}
+
+// exchange 1 (after the probe): per shard a header and, per prompt position, the owner's slot
+struct ShardHdr {
+    long long resident, pinned;
+};
+struct ShardPos {
+    unsigned int gslot;  // kNoSlot: not owned here or not resident
+    unsigned int refs0;
+};
+// exchange 2 (after each scan): per shard and list the shard's keep oldest candidates, sorted
+struct ShardCand {
+    unsigned long long lt, key;
+    unsigned int gslot, pad;
+};
+struct ShardLists {
+    int n[kMaxLists];
+    ShardCand c[kMaxLists][kChunk + 1];
+};
+// replicated admission state (identical on every shard), carried between the admission's kernels
+struct ShardState {
+    unsigned long long tick, first_touch;
+    long long cached, res_g, pinned_g, n_ev_adm;
+    int started, error, first_miss, admit_n, anchor, needed, warm_issued, chunk, need_scan, scans;
+};
+
 struct DevPool {
     long long cap;            // slots == EngineConfig::budget_blocks
     long long cap_scan;       // cap rounded up to 64: the SoA tail is padded with free slots
@@ -142,6 +178,18 @@ struct DevPool {
     unsigned int* tq_slot;
 
     Ctrl* ctrl;
+
+    // hash-sharded mode (world > 1 or an explicit shard): this shard's rank, the shard count,
+    // the GLOBAL budget, the exchange buffers and the replicated admission state
+    int rank, world;
+    long long gbudget;
+    unsigned char* sh_send1;   // ShardHdr + ShardPos[p_cap]
+    unsigned char* sh_recv1;   // world x the above
+    ShardLists* sh_send2;
+    ShardLists* sh_recv2;      // [world]
+    ShardState* sh_state;
+    unsigned int* sh_gslot;    // [p_cap] replicated prompt position -> gslot (kNoSlot: absent)
+    unsigned int* sh_grefs0;   // [p_cap]
 };
 
 #ifdef __CUDACC__

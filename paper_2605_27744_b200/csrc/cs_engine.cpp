@@ -227,7 +227,7 @@ struct cs_engine {
         return a.end_us > b.end_us || (a.end_us == b.end_us && a.seq > b.seq);
     }
 
-    void build(const cs_engine_cfg& c, const cs_workload_spec* ws);
+    void build(const cs_engine_cfg& c, const cs_workload_spec* ws, long long shard_slots = 0, cs_comm* comm = nullptr);
     void drain_evictions(bool force);
     bool done() const { return loaded && in_flight.empty() && ready.empty() && pending_sessions.empty(); }
     void arrive(int64_t idx);
@@ -239,7 +239,7 @@ struct cs_engine {
     void step();
 };
 
-void cs_engine::build(const cs_engine_cfg& c, const cs_workload_spec* ws) {
+void cs_engine::build(const cs_engine_cfg& c, const cs_workload_spec* ws, long long shard_slots, cs_comm* comm) {
     cfg = c;
     spec = to_spec(ws);
     bs = c.block_size;
@@ -283,7 +283,7 @@ void cs_engine::build(const cs_engine_cfg& c, const cs_workload_spec* ws) {
     pc.budget_blocks = budget;
     pool = new cs_pool();
     try {
-        pool->create(pc);  // selects the device; every allocation below lands on it
+        pool->create(pc, shard_slots, comm);  // selects the device; every allocation below lands on it
     } catch (...) {
         pool->destroy();
         delete pool;
@@ -599,6 +599,25 @@ int cs_engine_create(const cs_engine_cfg* cfg, const cs_workload_spec* spec, cs_
     });
 }
 
+int cs_engine_create_sharded(const cs_engine_cfg* cfg, const cs_workload_spec* spec, int64_t shard_slots,
+                             cs_comm_t comm, cs_engine_t* out) {
+    return eguard([&] {
+        if (!cfg || !spec || !out || !comm) throw std::invalid_argument("cs_engine_create_sharded: null argument");
+        auto* e = new cs_engine();
+        try {
+            e->build(*cfg, spec, shard_slots, comm);
+        } catch (...) {
+            if (e->pool) {
+                e->pool->destroy();
+                delete e->pool;
+            }
+            delete e;
+            throw;
+        }
+        *out = e;
+    });
+}
+
 int cs_engine_destroy(cs_engine_t e) {
     return eguard([&] {
         if (!e) return;
@@ -709,6 +728,15 @@ int cs_engine_restore(cs_engine_t e, const uint64_t* keys, const uint64_t* lt, c
         }
         const int rc = cs_restore(e->pool, keys, lt, agents, refs, n);
         if (rc != CS_OK) throw CsError(rc, cs_last_error());
+        if (e->pool->comm) {  // sharded: the engine clock and the residency are global
+            long long res = 0;
+            csb::Ctrl c;
+            ck(cudaMemcpy(&c, e->pool->P.ctrl, sizeof(c), cudaMemcpyDeviceToHost), "ctrl D2H");
+            for (unsigned long long v : e->pool->allgather_u64((unsigned long long)c.resident)) res += (long long)v;
+            if (res > e->pool->P.gbudget) throw std::invalid_argument("cs_restore: snapshot exceeds the budget");
+            for (unsigned long long v : e->pool->allgather_u64(mx)) mx = std::max<uint64_t>(mx, v);
+            e->pool->resident = res;
+        }
         e->tick = std::max<uint64_t>(e->tick, mx);
     });
 }

@@ -174,7 +174,7 @@ __global__ void hash_turns_kernel(const TurnDesc* __restrict__ turns, int n, int
 __global__ void unpin_kernel(DevPool P, const unsigned int* slots, int n) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     int dec = 0;
-    if (i < n) {
+    if (i < n && slots[i] != kNoSlot) {  // kNoSlot: a position another shard owns
         if (atomicSub(&P.refs[slots[i]], 1u) == 1u) dec = 1;
     }
     dec = __reduce_add_sync(0xffffffffu, dec);

@@ -80,6 +80,13 @@ LaunchCfg admit_launch_config(const DevPool& P, int device, int want_grid);
 cudaError_t launch_admit(const DevPool& P, const AdmitArgs& a, const LaunchCfg& lc, int grid,
                          cudaStream_t s);
 
+// Hash-sharded admission (cs_shard.cuh): probe -> exchange 1 -> decide -> per chunk
+// [scan -> exchange 2] -> replay.
+cudaError_t launch_shard_probe(const DevPool& P, const AdmitArgs& a, cudaStream_t s);
+cudaError_t launch_shard_decide(const DevPool& P, const AdmitArgs& a, cudaStream_t s);
+cudaError_t launch_shard_scan(const DevPool& P, const AdmitArgs& a, int keep, const LaunchCfg& lc, cudaStream_t s);
+cudaError_t launch_shard_replay(const DevPool& P, const AdmitArgs& a, cudaStream_t s);
+
 cudaError_t launch_init_pool(const DevPool& P, cudaStream_t s);
 cudaError_t launch_hash_prompts(const unsigned int* tokens, const long long* tok_off, int n, int bs, int skip,
                                 int take, const long long* blk_off, unsigned long long* keys, int* counts,

@@ -44,8 +44,9 @@ extern "C" const char* cs_version(void) { return "cachesage_b200 0.1 (sm_100a)";
 
 void cs_set_error(const std::string& m) { g_err = m; }
 
-void cs_pool::create(const cs_pool_cfg& c) {
+void cs_pool::create(const cs_pool_cfg& c, long long shard_slots, cs_comm* cm) {
     cfg = c;
+    comm = cm;
     if (c.budget_blocks < 1) throw std::invalid_argument("EngineSim: budget, block size, and concurrency must be positive");
     if (c.e_max <= 0) throw std::invalid_argument("CacheSagePolicy: e_max must be positive");
     if (c.e_max > csb::kMaxLists - 2) throw CsError(CS_ERR_CAPACITY, "e_max > 22 is not supported by the device select");
@@ -55,6 +56,13 @@ void cs_pool::create(const cs_pool_cfg& c) {
     if (c.agent_capacity < 1 || c.agent_capacity > csb::kMaxAgents)
         throw CsError(CS_ERR_CAPACITY, "agent_capacity must be in [1, 4096]");
     if (c.budget_blocks >= (int64_t)0xFFFFFFF0ll) throw CsError(CS_ERR_CAPACITY, "budget exceeds 32-bit slot ids");
+    const int world = comm ? comm->world : 1;
+    if (comm) {
+        if (world < 1 || world > csb::kMaxShards) throw std::invalid_argument("sharded pool: 1 <= world <= 8");
+        if (shard_slots <= 0) shard_slots = std::min<long long>(c.budget_blocks, c.budget_blocks * 5 / (4 * world) + 4096);
+        if (shard_slots >= (long long)csb::kShardMask - 16)
+            throw CsError(CS_ERR_CAPACITY, "shard exceeds 2^29 slots (global slot ids)");
+    }
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
         throw CsError(CS_ERR_CUDA, "no CUDA device: cachesage_b200 has no CPU fallback");
@@ -65,7 +73,10 @@ void cs_pool::create(const cs_pool_cfg& c) {
     ck(cudaEventCreate(&ev1), "cudaEventCreate");
 
     csb::DevPool& p = P;
-    p.cap = c.budget_blocks;
+    p.cap = comm ? shard_slots : c.budget_blocks;
+    p.rank = comm ? comm->rank : 0;
+    p.world = world;
+    p.gbudget = c.budget_blocks;
     p.policy = c.policy;
     p.e_max = c.e_max;
     p.n_lists = c.e_max + 2;
@@ -138,6 +149,13 @@ void cs_pool::create(const cs_pool_cfg& c) {
     p.dbg = dmalloc<unsigned long long>((size_t)lc.grid * 16, "dbg");
     ck(cudaMemsetAsync(p.dbg, 0, sizeof(unsigned long long) * lc.grid * 16, stream), "memset");
 
+    if (comm) {
+        p.sh_send2 = dmalloc<csb::ShardLists>(1, "sh_send2");
+        p.sh_recv2 = dmalloc<csb::ShardLists>((size_t)world, "sh_recv2");
+        p.sh_state = dmalloc<csb::ShardState>(1, "sh_state");
+        ck(cudaMallocHost(reinterpret_cast<void**>(&hstate), sizeof(csb::ShardState)), "cudaMallocHost");
+        ensure_prompt_scratch(8192);
+    }
     ck(cudaHostAlloc(reinterpret_cast<void**>(&st), sizeof(csb::AdmitStatus), cudaHostAllocMapped), "cudaHostAlloc");
     std::memset(st, 0, sizeof(*st));
     ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(&st_dev), st, 0), "cudaHostGetDevicePointer");
@@ -149,7 +167,8 @@ void cs_pool::destroy() {
     csb::DevPool& p = P;
     void* ptrs[] = {p.lt, p.agent, p.refs, p.key, p.tokens, p.table, p.free_stack, p.evlog, p.counts, p.totals,
                     p.win_a, p.win_b, p.hop, p.cls, p.agent_ids, p.ctrl, p.gbound, p.gcount, p.fin_lt, p.fin_slot,
-                    p.fin_n, p.p_slot, p.p_refs0, p.gbuf_lt, p.gbuf_slot, p.ghint, p.gmaxk, p.grej, p.dbg, p.gsmall, p.gmin, p.tq_key, p.tq_slot};
+                    p.fin_n, p.p_slot, p.p_refs0, p.gbuf_lt, p.gbuf_slot, p.ghint, p.gmaxk, p.grej, p.dbg, p.gsmall, p.gmin, p.tq_key, p.tq_slot,
+                    p.sh_send1, p.sh_recv1, p.sh_send2, p.sh_recv2, p.sh_state, p.sh_gslot, p.sh_grefs0};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     d_keys.release();
@@ -159,13 +178,26 @@ void cs_pool::destroy() {
     d_aux2.release();
     d_aux3.release();
     if (st) cudaFreeHost(st);
+    if (hstate) cudaFreeHost(hstate);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     if (stream) cudaStreamDestroy(stream);
 }
 
 void cs_pool::ensure_prompt_scratch(long long n) {
-    if (n <= P.p_cap) return;
+    if (n <= P.p_cap && (!comm || P.sh_gslot)) return;
+    if (comm) {
+        const long long c = std::max<long long>(n, P.p_cap * 2);
+        for (void* q : {(void*)P.sh_send1, (void*)P.sh_recv1, (void*)P.sh_gslot, (void*)P.sh_grefs0})
+            if (q) cudaFree(q);
+        const size_t rec = sizeof(csb::ShardHdr) + sizeof(csb::ShardPos) * (size_t)c;
+        P.sh_send1 = dmalloc<unsigned char>(rec, "sh_send1");
+        P.sh_recv1 = dmalloc<unsigned char>(rec * (size_t)P.world, "sh_recv1");
+        P.sh_gslot = dmalloc<unsigned int>(c, "sh_gslot");
+        P.sh_grefs0 = dmalloc<unsigned int>(c, "sh_grefs0");
+        if (n <= P.p_cap) return;
+        n = c;
+    }
     long long c = std::max<long long>(n, P.p_cap * 2);
     if (P.p_slot) {
         ck(csb::launch_table_flush(P, stream), "table flush");  // the queue lives in this scratch
@@ -188,7 +220,107 @@ void cs_pool::flush_table() {
     ++launches;
 }
 
+std::vector<unsigned long long> cs_pool::allgather_u64(unsigned long long v) {
+    if (!comm) return {v};
+    std::vector<unsigned long long> out((size_t)P.world);
+    ck(cudaMemcpyAsync(P.sh_send1, &v, 8, cudaMemcpyHostToDevice, stream), "H2D");
+    comm->allgather(P.sh_send1, P.sh_recv1, 8, stream);
+    ck(cudaMemcpyAsync(out.data(), P.sh_recv1, 8 * out.size(), cudaMemcpyDeviceToHost, stream), "D2H");
+    sync();
+    return out;
+}
+
+void cs_pool::fetch_state() {
+    ck(cudaMemcpyAsync(hstate, P.sh_state, sizeof(csb::ShardState), cudaMemcpyDeviceToHost, stream), "state D2H");
+    sync();
+}
+
+// One admission of a sharded pool (cs_shard.cuh): probe -> allgather -> decide -> per chunk
+// that can evict [scan -> allgather] -> replay. Every shard calls it with the same arguments.
+const csb::AdmitStatus& cs_pool::admit_sharded(const csb::AdmitArgs& in) {
+    try {
+        return admit_sharded_once(in);
+    } catch (...) {
+        comm->abort();  // a shard that fails must not leave its peers waiting in an exchange
+        throw;
+    }
+}
+
+const csb::AdmitStatus& cs_pool::admit_sharded_once(const csb::AdmitArgs& in) {
+    csb::AdmitArgs a = in;
+    ensure_prompt_scratch(std::max(1, a.n));
+    a.status = st_dev;
+    a.n_agents = n_agents;
+    if (poll_reset_pending) a.flags |= csb::kPollReset;
+    if ((int)unpin_q.size() > csb::kMaxUnpinRanges) flush_unpins();
+    a.n_unpin_ranges = 0;
+    for (const auto& u : unpin_q) {
+        a.unpin_ptr[a.n_unpin_ranges] = u.first;
+        a.unpin_n[a.n_unpin_ranges] = u.second;
+        ++a.n_unpin_ranges;
+    }
+    unpin_q.clear();
+    unpin_q_slots = 0;
+    a.seq = ++seq;
+    st->started = -1;
+    if (timing) ck(cudaEventRecord(ev0, stream), "cudaEventRecord");
+    ck(csb::launch_shard_probe(P, a, stream), "shard probe");
+    ++launches;
+    comm->allgather(P.sh_send1, P.sh_recv1, sizeof(csb::ShardHdr) + sizeof(csb::ShardPos) * (size_t)std::max(a.n, 0),
+                    stream);
+    ck(csb::launch_shard_decide(P, a, stream), "shard decide");
+    ++launches;
+    fetch_state();
+    bool scanned = false;
+    if (hstate->started && hstate->admit_n > 0) {
+        const int admit_n = hstate->admit_n;
+        for (int c = 0; c * csb::kChunk < admit_n; ++c) {
+            if (hstate->need_scan) {  // replicated: every shard takes the same branch
+                const int keep = std::min(csb::kChunk, admit_n - c * csb::kChunk);
+                ck(csb::launch_shard_scan(P, a, keep, lc, stream), "shard scan");
+                ++launches;
+                scanned = true;
+                comm->allgather(P.sh_send2, P.sh_recv2, sizeof(csb::ShardLists), stream);
+            }
+            ck(csb::launch_shard_replay(P, a, stream), "shard replay");
+            ++launches;
+            fetch_state();
+            if (hstate->error) break;
+        }
+    }
+    if (timing) ck(cudaEventRecord(ev1, stream), "cudaEventRecord");
+    sync();
+    poll_reset_pending = false;
+    if (timing) {
+        float ms = 0.f;
+        ck(cudaEventElapsedTime(&ms, ev0, ev1), "cudaEventElapsedTime");
+        admit_ms += ms;
+        ++admit_launches;
+        if (scanned) {
+            scan_launch_ms += ms;
+            ++scan_launches;
+        }
+    }
+    if (st->started < 0) throw CsError(CS_ERR_CUDA, "shard kernels did not report a status");
+    resident = st->resident;
+    pinned = st->pinned;
+    ev_total = st->ev_total;
+    pending_targets.assign(st->pend_target, st->pend_target + std::min(st->n_pend, csb::kMaxPending));
+    pending_ticks.assign(st->pend_tick, st->pend_tick + std::min(st->n_pend, csb::kMaxPending));
+    if (st->error == 2) throw CsError(CS_ERR_CAPACITY, "sharded pool: a shard ran out of slots (raise shard_slots)");
+    if (st->error) throw std::runtime_error("evict_one: all resident blocks are pinned");
+    csb::Ctrl c;
+    ck(cudaMemcpy(&c, P.ctrl, sizeof(c), cudaMemcpyDeviceToHost), "ctrl D2H");
+    if ((unsigned long long)(c.resident + c.tombstones) > (P.tmask + 1) / 2) {
+        ck(csb::launch_table_rebuild(P, stream), "table rebuild");  // subsumes the queued updates
+        ++table_rebuilds;
+        launches += 2;
+    }
+    return *st;
+}
+
 const csb::AdmitStatus& cs_pool::admit(const csb::AdmitArgs& in, int n_for_grid) {
+    if (comm) return admit_sharded(in);
     csb::AdmitArgs a = in;
     ensure_prompt_scratch(std::max(1, a.n));
     a.status = st_dev;
@@ -300,6 +432,21 @@ int cs_pool_create(const cs_pool_cfg* cfg, cs_pool_t* out) {
         auto* p = new cs_pool();
         try {
             p->create(*cfg);
+        } catch (...) {
+            p->destroy();
+            delete p;
+            throw;
+        }
+        *out = p;
+    });
+}
+
+int cs_pool_create_sharded(const cs_pool_cfg* cfg, int64_t shard_slots, cs_comm_t comm, cs_pool_t* out) {
+    return guard([&] {
+        if (!cfg || !out || !comm) throw std::invalid_argument("cs_pool_create_sharded: null argument");
+        auto* p = new cs_pool();
+        try {
+            p->create(*cfg, shard_slots, comm);
         } catch (...) {
             p->destroy();
             delete p;
@@ -511,6 +658,26 @@ int cs_restore(cs_pool_t pool, const uint64_t* keys, const uint64_t* lt, const u
         if (!pool || n < 0 || (n > 0 && (!keys || !lt))) throw std::invalid_argument("cs_restore: null argument");
         pool->flush_unpins();
         pool->flush_table();
+        // a shard keeps the snapshot blocks it owns (the caller may pass the whole snapshot)
+        std::vector<uint64_t> fk, fl;
+        std::vector<uint32_t> fa, fr;
+        if (pool->comm && pool->P.world > 1) {
+            for (int64_t i = 0; i < n; ++i) {
+                if (csb::shard_owner(keys[i], pool->P.world) != pool->P.rank) continue;
+                fk.push_back(keys[i]);
+                fl.push_back(lt[i]);
+                if (agents) fa.push_back(agents[i]);
+                if (refs) fr.push_back(refs[i]);
+            }
+            n = (int64_t)fk.size();
+            keys = fk.data();
+            lt = fl.data();
+            if (agents) agents = fa.data();
+            if (refs) refs = fr.data();
+            csb::Ctrl c0;
+            ck(cudaMemcpy(&c0, pool->P.ctrl, sizeof(c0), cudaMemcpyDeviceToHost), "ctrl D2H");
+            pool->resident = c0.resident;
+        }
         if (pool->resident + n > pool->P.cap) throw std::invalid_argument("cs_restore: snapshot exceeds the budget");
         if (n == 0) return;
         cudaStream_t s = pool->stream;

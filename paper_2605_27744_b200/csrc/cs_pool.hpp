@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "../../include/cachesage_b200.h"
+#include "cs_comm.hpp"
 #include "cs_launch.h"
 
 namespace csb {
@@ -81,7 +82,17 @@ struct cs_pool {
     std::vector<std::pair<const unsigned int*, int>> unpin_q;
     int unpin_q_slots = 0;
 
-    void create(const cs_pool_cfg& c);
+    // hash-sharded mode: this pool is one shard; comm is borrowed
+    cs_comm* comm = nullptr;
+    csb::ShardState* hstate = nullptr;  // pinned host copy of the replicated admission state
+
+    // shard_slots > 0 or comm: one shard of a pool of global budget c.budget_blocks
+    void create(const cs_pool_cfg& c, long long shard_slots = 0, cs_comm* comm = nullptr);
+    const csb::AdmitStatus& admit_sharded(const csb::AdmitArgs& args_in);
+    const csb::AdmitStatus& admit_sharded_once(const csb::AdmitArgs& args_in);
+    void fetch_state();
+    // every shard's value of v (sharded pools; {v} otherwise)
+    std::vector<unsigned long long> allgather_u64(unsigned long long v);
     void destroy();
     void ensure_prompt_scratch(long long n);
     // Runs one admission launch and waits for it. grid_hint: 0 = decide (1 CTA when no eviction

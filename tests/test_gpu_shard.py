@@ -1,0 +1,219 @@
+"""Hash-sharded pool on the GPU: G shards of one pool, each scanning and
+k-selecting its own slots, exchanging candidates, replaying the same evict_one loop. Every
+shard must return exactly the decisions of ONE pool of the same global budget: the reference
+fixtures (tests/golden, produced by the unmodified reference) are the bar, bit-exact.
+
+The shards share the test box's single B200: `local` shards are G threads of this process
+(device-to-device exchange), `torch` shards are G processes exchanging through a gloo group,
+`nccl` is the production transport at world 1.
+"""
+import json
+import os
+import threading
+
+import numpy as np
+import pytest
+
+import refshim
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+RUNS = {g["name"] + "-" + g["kw"]["policy"]: g for g in json.load(open(os.path.join(GOLD, "runs.json")))["runs"]}
+
+pytestmark = pytest.mark.gpu
+
+ENGINE_KW = ("budget", "concurrency", "block_size", "prefetch", "skip", "take")
+CASES = ["supervisor-a-cachesage", "supervisor-b-lru", "synthetic-chain-cachesage", "cfg1@128-cachesage",
+         "oversized-mixed-cachesage", "pins-defer-lru", "supervisor-a-emax3-cachesage"]
+
+
+def fnv(a):
+    return hex(refshim.fnv1a64(np.ascontiguousarray(a, dtype="<u8")))
+
+
+def _kw(g):
+    kw = dict(g["kw"])
+    ekw = {k: kw.pop(k) for k in list(kw) if k in ENGINE_KW}
+    return ekw, kw.pop("policy"), kw
+
+
+def _run_shards(g, world, grid=None, shard_slots=0):
+    from paper_2605_27744_b200 import api, shard
+
+    ekw, pol, kw = _kw(g)
+    comms = shard.local_group(world)
+    grid = grid or max(1, 148 // world)  # the G cooperative scan grids must be co-resident
+    out = [None] * world
+    err = []
+
+    def work(r):
+        try:
+            eng = api.Engine(g["spec"], policy=pol, agent_capacity=1024, comm=comms[r], shard_slots=shard_slots,
+                             grid_ctas=grid, **ekw, **kw)
+            try:
+                res = eng.run()
+                out[r] = (res, eng.turns(), eng.evictions(), eng.warmups(), eng.pool_stats())
+            finally:
+                eng.close()
+        except Exception as e:  # noqa: BLE001
+            err.append(e)
+
+    th = [threading.Thread(target=work, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for c in comms:
+        c.close()
+    if err:
+        raise err[0]
+    return out
+
+
+def _check_golden(g, res, t, ev, w):
+    ws, wt, wk = w
+    assert t["cached_tokens"].size == g["turns"]
+    assert repr(res["hit_rate"]) == g["hit_rate"]
+    assert ev.size == g["evictions"]
+    assert [hex(int(x)) for x in ev[:16]] == g["first_evictions"]
+    assert fnv(ev) == g["evictions_fnv"]
+    assert fnv(t["cached_tokens"]) == g["cached_fnv"]
+    assert fnv(t["end_us"].view(np.uint64)) == g["end_us_fnv"]
+    assert ws.size == g["n_warmups"]
+    assert fnv(wt) == g["warmups_fnv"]
+    assert repr(res["sim_us"]) == g["sim_us"]
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 4])
+@pytest.mark.parametrize("name", CASES)
+def test_sharded_engine_matches_reference(name, world):
+    """Every shard of a G-way sharded pool reproduces the reference run bit-exactly."""
+    g = RUNS[name]
+    out = _run_shards(g, world)
+    residents = []
+    for res, t, ev, w, ps in out:
+        _check_golden(g, res, t, ev, w)
+        residents.append(ps["resident"])
+    # the shards partition the pool: their residents add up to the single pool's
+    assert sum(residents) <= g["kw"].get("budget", 10**12)
+    if world > 1:
+        assert min(residents) > 0
+
+
+def test_sharded_tight_shards_error_loudly():
+    """A shard too small for its share of the pool fails with CS_ERR_CAPACITY, never silently."""
+    from paper_2605_27744_b200 import CacheSageError
+
+    g = RUNS["supervisor-a-cachesage"]
+    with pytest.raises(CacheSageError):
+        _run_shards(g, 2, shard_slots=64)
+
+
+def test_sharded_snapshot_matches_single_pool():
+    """A 1M-slot realistic snapshot + a mixed trace: 4 shards vs one pool, same victims."""
+    from paper_2605_27744_b200 import api, shard, workloads as W
+
+    pool = 1 << 20
+    spec = W.cfg4_mixed(sessions=300, budget=pool, seed=2608)
+    keys, lt, agents, refs = W.pool_snapshot(pool, 256, seed=11, mode="adversarial")
+
+    def single():
+        eng = api.Engine(spec, policy="cachesage", budget=pool, agent_capacity=1024)
+        eng.restore(keys, lt, agents=agents, refs=refs)
+        eng.run_for(150)
+        r = (eng.evictions(), eng.turns()["cached_tokens"], eng.warmups()[1], eng.result())
+        eng.close()
+        return r
+
+    ref_ev, ref_cached, ref_w, ref_res = single()
+    assert ref_ev.size > 1000
+    world = 4
+    comms = shard.local_group(world)
+    out = [None] * world
+    err = []
+
+    def work(r):
+        try:
+            eng = api.Engine(spec, policy="cachesage", budget=pool, agent_capacity=1024, comm=comms[r],
+                             grid_ctas=148 // world)
+            eng.restore(keys, lt, agents=agents, refs=refs)  # each shard keeps what it owns
+            eng.run_for(150)
+            out[r] = (eng.evictions(), eng.turns()["cached_tokens"], eng.warmups()[1], eng.pool_stats())
+            eng.close()
+        except Exception as e:  # noqa: BLE001
+            err.append(e)
+
+    th = [threading.Thread(target=work, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    if err:
+        raise err[0]
+    owners = shard.shard_owner(ref_ev, world)
+    for r, (ev, cached, wt, ps) in enumerate(out):
+        assert np.array_equal(ev, ref_ev)
+        assert np.array_equal(cached, ref_cached)
+        assert np.array_equal(wt, ref_w)
+        assert ps["scans"] > 0
+    assert len(set(owners.tolist())) == world  # victims came from every shard
+
+
+def test_nccl_transport_world1():
+    """The production transport (ncclAllGather) at world 1 on this box's one GPU."""
+    from paper_2605_27744_b200 import api, shard
+
+    g = RUNS["supervisor-a-cachesage"]
+    ekw, pol, kw = _kw(g)
+    comm = shard.NcclComm(shard.nccl_unique_id(), 0, 1, 0)
+    eng = api.Engine(g["spec"], policy=pol, agent_capacity=1024, comm=comm, **ekw, **kw)
+    try:
+        res = eng.run()
+        _check_golden(g, res, eng.turns(), eng.evictions(), eng.warmups())
+    finally:
+        eng.close()
+        comm.close()
+
+
+def _torch_worker(rank, world, port, name, q):
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2605_27744_b200 import api, shard
+
+        g = RUNS[name]
+        ekw, pol, kw = _kw(g)
+        comm = shard.TorchComm()
+        eng = api.Engine(g["spec"], policy=pol, agent_capacity=1024, comm=comm, grid_ctas=148 // world, **ekw, **kw)
+        res = eng.run()
+        q.put((rank, fnv(eng.evictions()), repr(res["hit_rate"]), fnv(eng.turns()["cached_tokens"])))
+        eng.close()
+        comm.close()
+    except Exception as e:  # noqa: BLE001
+        q.put((rank, "error", repr(e), ""))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_torch_gloo_processes_share_one_gpu():
+    """Two processes (one shard each) exchanging through a torch.distributed gloo group."""
+    import multiprocessing as mp
+    import random
+
+    name = "supervisor-b-cachesage"
+    g = RUNS[name]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = random.randint(20000, 40000)
+    ps = [ctx.Process(target=_torch_worker, args=(r, 2, port, name, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    got = [q.get(timeout=600) for _ in ps]
+    for p in ps:
+        p.join(timeout=60)
+    for rank, ev_fnv, hr, cached in got:
+        assert ev_fnv == g["evictions_fnv"], (rank, hr)
+        assert hr == g["hit_rate"]
+        assert cached == g["cached_fnv"]
