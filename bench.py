@@ -179,16 +179,40 @@ def load_traffic(workload, pool):
     return None
 
 
-def build_engine(W, spec, pool, device, host_inputs, seed):
+def build_engine(W, spec, pool, device, host_inputs, seed, comm=None):
+    """comm None: one full pool on this GPU. comm (shard.Comm): this GPU's shard of a
+    hash-sharded pool of world x pool slots; the shard is filled to
+    pool - SHARD_SLACK blocks of a global realistic snapshot (the slack absorbs the per-shard
+    imbalance of where new blocks land) and scans its full `pool` slots."""
     import paper_2605_27744_b200 as cb
+    from paper_2605_27744_b200 import shard
 
-    eng = cb.Engine(spec, policy="cachesage", budget=pool, timing=True, host_inputs=host_inputs,
-                    prefetch=spec.get("prefetch", True), agent_capacity=1024, device=device)
-    n_agents = len(eng.agents())
-    keys, lt, agents, refs = W.pool_snapshot(pool, n_agents, seed=seed, mode="realistic")
+    if comm is None:
+        eng = cb.Engine(spec, policy="cachesage", budget=pool, timing=True, host_inputs=host_inputs,
+                        prefetch=spec.get("prefetch", True), agent_capacity=1024, device=device)
+        keys, lt, agents, refs = W.pool_snapshot(pool, len(eng.agents()), seed=seed, mode="realistic")
+    else:
+        fill = pool - SHARD_SLACK
+        eng = cb.Engine(spec, policy="cachesage", budget=fill * comm.world, timing=True, host_inputs=host_inputs,
+                        prefetch=spec.get("prefetch", True), agent_capacity=1024, device=device, comm=comm,
+                        shard_slots=pool)
+        keys, lt, agents, refs = shard.snapshot_shard(fill, comm.world, comm.rank, len(eng.agents()), seed=seed)
     eng.restore(keys, lt, agents=agents, refs=refs)
     del keys, lt, agents, refs
     return eng
+
+
+SHARD_SLACK = 8192
+
+
+def make_comm(dist):
+    """NCCL shard exchange over NVLink: rank 0 makes the id, torch.distributed broadcasts it."""
+    from paper_2605_27744_b200 import shard
+
+    uid = [shard.nccl_unique_id() if dist.rank == 0 else None]
+    if dist.world > 1:
+        dist.td.broadcast_object_list(uid, src=0)
+    return shard.NcclComm(uid[0], dist.rank, dist.world, dist.local)
 
 
 def rank_workload(sessions, pool, rank):
@@ -219,7 +243,13 @@ def run_ours(args, dist):
     from paper_2605_27744_b200 import workloads as W
 
     pool = args.pool
-    spec, snap_seed = rank_workload(args.sessions, pool, dist.rank)
+    sharded = args.parallel == "sharded" or (args.parallel == "auto" and dist.world > 1)
+    comm = make_comm(dist) if sharded else None
+    if sharded:  # one global trace and pool, hash-partitioned: every rank runs the same trace
+        spec = W.cfg4_mixed(sessions=args.sessions, budget=pool * dist.world, seed=2608)
+        snap_seed = 11
+    else:
+        spec, snap_seed = rank_workload(args.sessions, pool, dist.rank)
     R = args.admissions_per_step
 
     def timed_run(eng, steps):
@@ -233,7 +263,7 @@ def run_ours(args, dist):
         return ms
 
     # ---- value: inputs resident in HBM
-    eng = build_engine(W, spec, pool, dist.local, False, seed=snap_seed)
+    eng = build_engine(W, spec, pool, dist.local, False, seed=snap_seed, comm=comm)
     timed_run(eng, args.warmup)
     r0 = eng.result()
     p0 = eng.pool_stats()["phase_ns"]
@@ -251,7 +281,7 @@ def run_ours(args, dist):
     eng.close()
 
     # ---- e2e: host inputs, H2D per admission, victims D2H per admission
-    eng = build_engine(W, spec, pool, dist.local, True, seed=snap_seed)
+    eng = build_engine(W, spec, pool, dist.local, True, seed=snap_seed, comm=comm)
     timed_run(eng, args.warmup)
     e0 = eng.result()
     ems = timed_run(eng, args.steps)
@@ -260,6 +290,8 @@ def run_ours(args, dist):
     h2d = (e1["h2d_bytes"] - e0["h2d_bytes"]) / args.steps
     d2h = (e1["d2h_bytes"] - e0["d2h_bytes"]) / args.steps
     eng.close()
+    if comm is not None:
+        comm.close()
 
     peak, peak_kind = measured_peak()
     avg_scan_launch_s = (scan_ms / 1e3) / max(scan_launches, 1)
@@ -273,7 +305,10 @@ def run_ours(args, dist):
                 "realistic 16M-slot pool snapshot (seeded permutation of last_touch)",
         "config": {"workload": "cfg4-mixed-256", "pool_blocks_per_gpu": pool, "agents": 256,
                    "trace_sessions_per_gpu": args.sessions, "admissions_per_step": R,
-                   "policy": "cachesage", "parallelism": f"replicas{dist.world} (sessions partitioned)",
+                   "policy": "cachesage",
+                   "parallelism": (f"hash-sharded{dist.world} (pool of {dist.world} x {pool} slots, owner = "
+                                   "(key >> 40) % N, NCCL allgather of per-shard candidates)") if sharded
+                   else f"replicas{dist.world} (sessions partitioned)",
                    "l2": "pool SoA 256 MiB > 126 MB L2; no flush needed"},
         "evictions_per_s": evicted / (tot_ms / 1e3), "admissions_per_s": adm / (tot_ms / 1e3),
         "scans_per_step": (r1["scans"] - r0["scans"]) / args.steps, "hit_rate_so_far": hit,
@@ -381,6 +416,8 @@ def main():
     ap.add_argument("--sessions", type=int, default=40_000)
     ap.add_argument("--admissions-per-step", type=int, default=32)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--parallel", default="auto", choices=["auto", "sharded", "replicas"],
+                    help="N>1: hash-sharded pool (auto) or independent replicas; 'sharded' also at N=1")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world, rank, local = dist_env()
