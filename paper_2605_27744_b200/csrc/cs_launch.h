@@ -84,7 +84,7 @@ cudaError_t launch_admit(const DevPool& P, const AdmitArgs& a, const LaunchCfg& 
 // [scan -> exchange 2] -> replay.
 cudaError_t launch_shard_probe(const DevPool& P, const AdmitArgs& a, cudaStream_t s);
 cudaError_t launch_shard_decide(const DevPool& P, const AdmitArgs& a, cudaStream_t s);
-cudaError_t launch_shard_scan(const DevPool& P, const AdmitArgs& a, int keep, const LaunchCfg& lc, cudaStream_t s);
+cudaError_t launch_shard_scan(const DevPool& P, const AdmitArgs& a, int chunk, const LaunchCfg& lc, cudaStream_t s);
 cudaError_t launch_shard_replay(const DevPool& P, const AdmitArgs& a, cudaStream_t s);
 
 cudaError_t launch_init_pool(const DevPool& P, cudaStream_t s);

@@ -270,23 +270,14 @@ const csb::AdmitStatus& cs_pool::admit_sharded_once(const csb::AdmitArgs& in) {
                     stream);
     ck(csb::launch_shard_decide(P, a, stream), "shard decide");
     ++launches;
-    fetch_state();
-    bool scanned = false;
-    if (hstate->started && hstate->admit_n > 0) {
-        const int admit_n = hstate->admit_n;
-        for (int c = 0; c * csb::kChunk < admit_n; ++c) {
-            if (hstate->need_scan) {  // replicated: every shard takes the same branch
-                const int keep = std::min(csb::kChunk, admit_n - c * csb::kChunk);
-                ck(csb::launch_shard_scan(P, a, keep, lc, stream), "shard scan");
-                ++launches;
-                scanned = true;
-                comm->allgather(P.sh_send2, P.sh_recv2, sizeof(csb::ShardLists), stream);
-            }
-            ck(csb::launch_shard_replay(P, a, stream), "shard replay");
-            ++launches;
-            fetch_state();
-            if (hstate->error) break;
-        }
+    // every possible chunk is enqueued without a host round trip: the kernels read the
+    // replicated state (admit_n, need_scan) and no-op past the admission's end
+    const int n_chunks = (std::max(a.n, 1) + csb::kChunk - 1) / csb::kChunk;
+    for (int c = 0; c < n_chunks; ++c) {
+        ck(csb::launch_shard_scan(P, a, c, lc, stream), "shard scan");
+        comm->allgather(P.sh_send2, P.sh_recv2, sizeof(csb::ShardLists), stream);
+        ck(csb::launch_shard_replay(P, a, stream), "shard replay");
+        launches += 2;
     }
     if (timing) ck(cudaEventRecord(ev1, stream), "cudaEventRecord");
     sync();
@@ -296,7 +287,7 @@ const csb::AdmitStatus& cs_pool::admit_sharded_once(const csb::AdmitArgs& in) {
         ck(cudaEventElapsedTime(&ms, ev0, ev1), "cudaEventElapsedTime");
         admit_ms += ms;
         ++admit_launches;
-        if (scanned) {
+        if (st->scans > 0) {
             scan_launch_ms += ms;
             ++scan_launches;
         }
@@ -309,9 +300,8 @@ const csb::AdmitStatus& cs_pool::admit_sharded_once(const csb::AdmitArgs& in) {
     pending_ticks.assign(st->pend_tick, st->pend_tick + std::min(st->n_pend, csb::kMaxPending));
     if (st->error == 2) throw CsError(CS_ERR_CAPACITY, "sharded pool: a shard ran out of slots (raise shard_slots)");
     if (st->error) throw std::runtime_error("evict_one: all resident blocks are pinned");
-    csb::Ctrl c;
-    ck(cudaMemcpy(&c, P.ctrl, sizeof(c), cudaMemcpyDeviceToHost), "ctrl D2H");
-    if ((unsigned long long)(c.resident + c.tombstones) > (P.tmask + 1) / 2) {
+    // this shard holds at most P.cap live entries: rebuild before cap + tombstones pass half
+    if ((unsigned long long)(P.cap + st->tombstones) > (P.tmask + 1) / 2) {
         ck(csb::launch_table_rebuild(P, stream), "table rebuild");  // subsumes the queued updates
         ++table_rebuilds;
         launches += 2;

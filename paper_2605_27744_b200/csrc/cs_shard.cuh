@@ -223,7 +223,9 @@ __global__ void __launch_bounds__(512, 1) shard_decide_kernel(DevPool P, AdmitAr
 }
 
 // ---- scan: this shard's per-list keep oldest (the single-pool K4 + K5a), packed for exchange 2
-__global__ void __launch_bounds__(kThreads + 32, 1) shard_scan_kernel(DevPool P, AdmitArgs a, int keep) {
+// The host enqueues one scan + exchange + replay per possible chunk without waiting; a chunk
+// that does not exist (admission smaller, not started) or cannot evict sends empty lists.
+__global__ void __launch_bounds__(kThreads + 32, 1) shard_scan_kernel(DevPool P, AdmitArgs a, int chunk) {
     extern __shared__ __align__(16) unsigned char dsm[];
     __shared__ ScanSmem S;
     __shared__ SelectSmem Sel;
@@ -231,6 +233,14 @@ __global__ void __launch_bounds__(kThreads + 32, 1) shard_scan_kernel(DevPool P,
     const int tid = threadIdx.x, T = blockDim.x;
     const int NL = P.n_lists;
     const ScanBufs B = scan_bufs(dsm);
+    const ShardState* SS = P.sh_state;
+    const int admit_n = SS->admit_n;
+    if (SS->error || SS->chunk != chunk || chunk * kChunk >= admit_n || !SS->need_scan) {
+        if (blockIdx.x == 0)
+            for (int l = tid; l < kMaxLists; l += T) P.sh_send2->n[l] = 0;
+        return;  // uniform across the grid: SS is not written during this kernel
+    }
+    const int keep = min(kChunk, admit_n - chunk * kChunk);
     if (tid == 0) {
         S.spec = 0;
         S.cls_ready = 1;
@@ -346,6 +356,7 @@ __global__ void __launch_bounds__(512, 1) shard_replay_kernel(DevPool P, AdmitAr
         for (int c = 0; c < kMaxLists; ++c) A.wsurv[c] = P.wsurv[c];
     }
     __syncthreads();
+    if (SS->error || !SS->started || A.chunk * kChunk >= A.admit_n) return;  // no such chunk
     const int lo = A.chunk * kChunk;
     const int hi = min(A.admit_n, lo + kChunk);
     const int len = hi - lo;
@@ -728,7 +739,7 @@ cudaError_t launch_shard_decide(const DevPool& P, const AdmitArgs& a, cudaStream
     return cudaGetLastError();
 }
 
-cudaError_t launch_shard_scan(const DevPool& P, const AdmitArgs& a, int keep, const LaunchCfg& lc, cudaStream_t s) {
+cudaError_t launch_shard_scan(const DevPool& P, const AdmitArgs& a, int chunk, const LaunchCfg& lc, cudaStream_t s) {
     static bool attr = false;
     if (!attr) {
         cudaError_t e =
@@ -738,7 +749,7 @@ cudaError_t launch_shard_scan(const DevPool& P, const AdmitArgs& a, int keep, co
     }
     DevPool p = P;
     AdmitArgs aa = a;
-    int k = keep;
+    int k = chunk;
     void* args[] = {&p, &aa, &k};
     return cudaLaunchCooperativeKernel((const void*)shard_scan_kernel, dim3(lc.grid), dim3(lc.threads), args, lc.smem,
                                        s);

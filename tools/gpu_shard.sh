@@ -1,2 +1,2 @@
-timeout 900 python -m pytest tests/test_gpu_shard.py -x -q --timeout 300 -k "tight or snapshot or nccl or torch" 2>&1 | tail -15
-timeout 600 python bench.py --parallel sharded --steps 3 --warmup 3 --no-cpu-baseline 2>&1 | tail -3
+timeout 900 python -m pytest tests/test_gpu_shard.py -x -q --timeout 300 2>&1 | tail -5
+timeout 600 python bench.py --parallel sharded --steps 5 --warmup 3 --no-cpu-baseline 2>&1 | tail -1 | cut -c1-600
