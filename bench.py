@@ -266,11 +266,13 @@ def run_ours(args, dist):
     eng = build_engine(W, spec, pool, dist.local, False, seed=snap_seed, comm=comm)
     timed_run(eng, args.warmup)
     r0 = eng.result()
-    p0 = eng.pool_stats()["phase_ns"]
+    ps0 = eng.pool_stats()
+    p0 = ps0["phase_ns"]
     with ClockSampler(dist.local) as clk:
         ms = timed_run(eng, args.steps)
     r1 = eng.result()
-    p1 = eng.pool_stats()["phase_ns"]
+    ps1 = eng.pool_stats()
+    p1 = ps1["phase_ns"]
     value, tot_ms = aggregate(dist, ms, r1["scanned_slots"] - r0["scanned_slots"])
     evicted = dist.sum(r1["evictions"] - r0["evictions"])
     adm = dist.sum(r1["admissions"] - r0["admissions"])
@@ -322,6 +324,9 @@ def run_ours(args, dist):
                      "avg_launch_us": avg_scan_launch_s * 1e6, "algorithmic_bytes_per_launch": BYTES_PER_SLOT * pool},
         "clocks": clk.summary(),
         "phases_us_per_scan_launch": _phases(p0, p1, scan_launches),
+        "prescan": {"used": ps1["prescan_used"] - ps0["prescan_used"],
+                    "fallbacks": ps1["prescan_fallbacks"] - ps0["prescan_fallbacks"],
+                    "unusable": ps1["prescan_unusable"] - ps0["prescan_unusable"]},
     }
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(pool, args)

@@ -128,6 +128,9 @@ typedef struct cs_pool_stats {
     /* device time per admission-kernel phase summed over launches (globaltimer ns, CTA 0):
      * probe/observe/lookup, prep+barrier, scan+barrier, select+barrier, replay+apply, epilogue */
     uint64_t phase_ns[16];
+    /* admissions whose chunk 0 used the previous launch's prescan / fell back to a scan;
+     * prescans that overflowed (unusable) */
+    int64_t prescan_used, prescan_fallbacks, prescan_unusable;
 } cs_pool_stats;
 int cs_pool_get_stats(cs_pool_t pool, cs_pool_stats* out);
 /* Instrumentation: per-CTA scan timestamps of the last admission (grid x 8 u64). */

@@ -36,6 +36,7 @@ class PoolStats(C.Structure):
         ("resident", C.c_int64), ("pinned", C.c_int64), ("evictions", C.c_int64),
         ("tombstones", C.c_int64), ("scans", C.c_int64), ("scanned_slots", C.c_int64),
         ("rebuilds", C.c_uint64), ("n_agents", C.c_int), ("phase_ns", C.c_uint64 * 16),
+        ("prescan_used", C.c_int64), ("prescan_fallbacks", C.c_int64), ("prescan_unusable", C.c_int64),
     ]
 
 

@@ -66,6 +66,7 @@ struct AdmSmem {
     long long cached, n_ev_adm, resident, pinned, free_top;
     int first_miss, admit_n, anchor, chunk, started, error, needed, warm_issued, scans;
     int fin_want;  // lists finalized by CTAs other than 0 in the current pass
+    int need_full; // a prescan-fed chunk needs the serial replay (every class list): scan instead
     double wsurv[kMaxLists];  // P.wsurv staged on chip (indexed kernel-parameter loads are slow)
     unsigned long long ph[kPhases], tl;  // phase timestamps (CTA 0, thread 0)
 };
@@ -1066,6 +1067,413 @@ __device__ void finalize_list(const DevPool& P, int l, int NL, int keep, const S
     __syncthreads();
 }
 
+// ------------------------------------------------------------------ prescan (pipelined K4/K5a)
+//
+// CTAs 1..grid-1 of launch k run the scoring pass of admission k+1 while CTA 0 serves admission
+// k (phase 0, replay, apply), so the pool stream overlaps the serial part of the step. The pass
+// reads a pool that CTA 0 is changing, so its lists are validated by their consumer (CTA 0 of
+// launch k+1, after its phase 0):
+//   * an entry is valid iff its slot's last_touch is unchanged: every change of a slot's list
+//     membership except an unpin also changes its last_touch (a touch, pin+touch, eviction or
+//     reuse); unpinned slots (this and the previous launch's, the set U) are dropped and re-read;
+//   * acceptance is by fixed thresholds, so list l holds EVERY member of the read state below
+//     its completeness bound T_l; after validation it holds every member of the current state
+//     below T_l (new members are younger than any read tick, or are in U);
+//   * agent-carrying slots are kept whole (class unknown until the consumer's BFS), so the
+//     class lists are the consumer's and the survival classes may change freely in between.
+// A prescan that cannot stand in for a scan (overflow, a list too short, a non-bulk replay)
+// makes its consumer scan as before; decisions are never taken from an invalid list.
+
+__device__ __forceinline__ unsigned long long sat_add(unsigned long long a, unsigned long long b) {
+    return (a > kNoBound - 1 - b) ? kNoBound : a + b;
+}
+
+// The next acceptance threshold of a list from its sorted kept entries: ~3x the rank reached
+// (the front moves by at most two admissions of victims before the next prescan is consumed).
+__device__ __forceinline__ unsigned long long next_hint(unsigned long long v1, unsigned long long base) {
+    if (base >= kNoBound || base < v1) return kNoBound;
+    const unsigned long long span = base - v1;
+    return sat_add(v1, sat_add(span, span < (kNoBound >> 2) ? 2 * span : kNoBound));
+}
+
+__device__ void prescan_pass(const DevPool& P, const ScanBufs& B, ScanSmem& S, unsigned char* dsm, int par) {
+    Ctrl* C = P.ctrl;
+    const int tid = threadIdx.x, T = blockDim.x;
+    const long long TV = kTile;
+    const int nscan = (int)gridDim.x - 1, me = (int)blockIdx.x - 1;
+    long long per = (P.cap_scan + nscan - 1) / nscan;
+    per = (per + kV - 1) / kV * kV;
+    const long long lo = min(P.cap_scan, (long long)me * per);
+    const long long hi = min(P.cap_scan, lo + per);
+    const int ntiles = (int)((hi - lo + TV - 1) / TV);
+    unsigned char* ring = dsm + kOffRing;
+    // agent-carrying slots share E's threshold: the E members among them are complete to it,
+    // and the other classes' lists are only needed non-empty (see consume_prescan)
+    const unsigned long long hE = __ldcg(P.pre_hint + 0), hR = __ldcg(P.pre_hint + 1), hP = hE;
+    if (tid == 0) {
+        S.count = 0;
+        S.overflow = 0;
+        for (int s = 0; s < kRing; ++s) {
+            mbar_init(&S.mbar[s], 1u);
+            mbar_init(&S.mbar_empty[s], (unsigned int)(kThreads / 32));
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        P.dbg[blockIdx.x * 16 + 0] = gtimer();
+    }
+    __syncthreads();
+    if (tid >= kThreads) {  // producer warp: one elected thread keeps kRing tiles in flight
+        if (lane_id() == 0) {
+            for (int t = 0; t < ntiles; ++t) {
+                const int s = t % kRing;
+                if (t >= kRing) mbar_wait(&S.mbar_empty[s], (unsigned int)(((t / kRing) - 1) & 1));
+                const long long b0 = lo + (long long)t * TV;
+                const unsigned int nsl = (unsigned int)min(TV, hi - b0);
+                unsigned char* st = ring + (size_t)s * kRingStage;
+                mbar_expect_tx(&S.mbar[s], nsl * 16u);
+                bulk_g2s(st, P.lt + b0, nsl * 8u, &S.mbar[s]);
+                bulk_g2s(st + kRingLt, P.agent + b0, nsl * 4u, &S.mbar[s]);
+                bulk_g2s(st + kRingLt + kRingAg, P.refs + b0, nsl * 4u, &S.mbar[s]);
+            }
+        }
+        __syncwarp();
+    } else {
+        for (int t = 0; t < ntiles; ++t) {
+            const int s = t % kRing;
+            const long long i0 = lo + (long long)t * TV + (long long)tid * kV;
+            const unsigned char* st = ring + (size_t)s * kRingStage;
+            mbar_wait(&S.mbar[s], (unsigned int)((t / kRing) & 1));
+            unsigned long long x4[kV];
+            unsigned int a4[kV], r4[kV];
+            read4(st, tid, i0 + kV <= hi, x4, a4, r4);
+            __syncwarp();
+            if (lane_id() == 0) mbar_arrive(&S.mbar_empty[s]);
+            // list ids: 0 = E (agentless unpinned), 1 = R (resident), 2 = pending (agent, unpinned)
+            unsigned int acc = 0u;
+            int cl[kV];
+#pragma unroll
+            for (int k = 0; k < kV; ++k) {
+                const unsigned long long x = x4[k];
+                acc |= (unsigned int)(x <= hR) << k;
+                const bool agentless = a4[k] == kNoAgent;
+                cl[k] = agentless ? 0 : 2;
+                acc |= (unsigned int)(r4[k] == 0u && x <= (agentless ? hE : hP)) << (kV + k);
+            }
+            if (!S.overflow) append4(acc, x4, cl, i0, 1, B, S, true);
+        }
+    }
+    __syncthreads();
+    if (tid == 0) P.dbg[blockIdx.x * 16 + 1] = gtimer();
+    if (S.overflow) {
+        if (tid == 0) atomicExch(&C->pre_bad[par], 1);
+        return;
+    }
+    // every staged candidate to global memory: E and R raw (selected after the barrier), the
+    // agent-carrying ones straight into the output list with their agent
+    const int m = S.count;
+    for (int j0 = 0; j0 < m; j0 += T) {
+        const int j = j0 + tid;
+        const unsigned int act = __ballot_sync(0xffffffffu, j < m);
+        if (j >= m) continue;
+        const unsigned int l = B.st_list[j];
+        const unsigned int peers = __match_any_sync(act, l);
+        const int leader = __ffs(peers) - 1;
+        int base = 0;
+        if (lane_id() == leader) base = atomicAdd(&C->pre_cnt[par][l], __popc(peers));
+        base = __shfl_sync(peers, base, leader);
+        const int pos = base + __popc(peers & ((1u << lane_id()) - 1u));
+        const unsigned long long x = B.st_lt[j];
+        const unsigned int s = B.st_slot[j];
+        if (l < 2) {
+            if (pos < P.pre_gcap) {
+                P.pre_buf_lt[l * P.pre_gcap + pos] = x;
+                P.pre_buf_slot[l * P.pre_gcap + pos] = s;
+            } else {
+                atomicExch(&C->pre_bad[par], 1);
+            }
+        } else if (pos < kPendCap) {
+            const size_t o = ((size_t)par * 3 + 2) * kPendCap + pos;
+            P.pl_lt[o] = x;
+            P.pl_slot[o] = s;
+            P.pl_agent[(size_t)par * kPendCap + pos] = __ldcg(P.agent + s);
+        } else {
+            atomicExch(&C->pre_bad[par], 1);
+        }
+    }
+}
+
+// Barrier of the prescan CTAs (1..grid-1) only: CTA 0 is busy with this launch's admission.
+__device__ void prescan_barrier(Ctrl* c) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned int gen = ld_acquire(&c->pbar_gen);
+        __threadfence();
+        if (atomicAdd(&c->pbar_count, 1u) == gridDim.x - 2) {
+            c->pbar_count = 0;
+            __threadfence();
+            atomicAdd(&c->pbar_gen, 1u);
+        } else {
+            unsigned long long spins = 0;
+            while (ld_acquire(&c->pbar_gen) == gen) {
+                if (++spins > 4096) __nanosleep(64);
+                if (spins > (1ull << 27)) __trap();
+            }
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// List l (0 = E, 1 = R) of the prescan: its kPreK oldest, sorted, and the completeness bound.
+__device__ void prescan_finalize(const DevPool& P, const ScanBufs& B, SelectSmem& Sel, int par, int l,
+                                 unsigned long long h) {
+    Ctrl* C = P.ctrl;
+    const int tid = threadIdx.x, T = blockDim.x;
+    const int m = min(*(volatile int*)&C->pre_cnt[par][l], (int)P.pre_gcap);
+    const unsigned long long* g = P.pre_buf_lt + l * P.pre_gcap;
+    const unsigned int* gs = P.pre_buf_slot + l * P.pre_gcap;
+    unsigned long long v = kNoBound;
+    if (m > kPreK) v = block_kth(g, nullptr, 0, m, kPreK, Sel);
+    if (tid == 0) Sel.tmp = 0;
+    __syncthreads();
+    for (int j = tid; j < m; j += T) {
+        const unsigned long long x = __ldcg(g + j);
+        if (m <= kPreK || x <= v) {
+            const int p = atomicAdd(&Sel.tmp, 1);
+            B.sd_lt[p] = x;
+            B.sd_slot[p] = __ldcg(gs + j);
+        }
+    }
+    __syncthreads();
+    const int n = Sel.tmp;  // distinct ticks: exactly min(m, kPreK)
+    const size_t base = ((size_t)par * 3 + l) * kPendCap;
+    unsigned long long v1 = kNoBound;
+    for (int j = tid; j < n; j += T) {
+        const unsigned long long x = B.sd_lt[j];
+        int r = 0;
+        for (int k = 0; k < n; ++k) r += B.sd_lt[k] < x;
+        P.pl_lt[base + r] = x;
+        P.pl_slot[base + r] = B.sd_slot[j];
+        if (r == 0) v1 = x;
+    }
+    if (v1 != kNoBound) Sel.prefix = v1;  // the unique rank-0 entry
+    __syncthreads();
+    if (tid == 0) {
+        const unsigned long long Tl = m > kPreK ? v : h;
+        const int bad = *(volatile int*)&C->pre_bad[par];
+        P.pl_n[par * 3 + l] = n;
+        P.pl_T[par * 3 + l] = Tl;
+        // an overflowed pass staged a subset: its kPreK-th is a tighter, safe next threshold
+        P.pre_hint[l] = n == 0 ? kNoBound : bad ? (m > kPreK ? v : h) : next_hint(Sel.prefix, Tl);
+    }
+    __syncthreads();
+}
+
+// After the barrier: CTA 1 finalizes E and the pending list, CTA 2 (CTA 1 if alone) R; the last
+// finalizer publishes the lists for the next launch.
+__device__ void prescan_finish(const DevPool& P, const AdmitArgs& a, const ScanBufs& B, SelectSmem& Sel, int par,
+                               unsigned long long hE, unsigned long long hR, unsigned long long hP) {
+    Ctrl* C = P.ctrl;
+    const int nfin = gridDim.x >= 3 ? 2 : 1;
+    const int me = (int)blockIdx.x - 1;
+    if (me >= nfin) return;
+    if (me == 0) {
+        prescan_finalize(P, B, Sel, par, 0, hE);
+        if (threadIdx.x == 0) {
+            const int np = *(volatile int*)&C->pre_cnt[par][2];
+            if (np > kPendCap) atomicExch(&C->pre_bad[par], 1);
+            P.pl_n[par * 3 + 2] = min(np, kPendCap);
+            P.pl_T[par * 3 + 2] = hP;
+            if (np > kPendCap || *(volatile int*)&C->pre_bad[par]) C->pre_badcnt += 1;
+        }
+    }
+    if (me == nfin - 1) prescan_finalize(P, B, Sel, par, 1, hR);
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(&C->pre_fin[par], 1u) == (unsigned int)nfin - 1) {
+            __threadfence();
+            C->pl_ok[par] = *(volatile int*)&C->pre_bad[par] ? 0 : 1;
+            C->pre_cnt[par][0] = C->pre_cnt[par][1] = C->pre_cnt[par][2] = 0;
+            C->pre_bad[par] = 0;
+            C->pre_fin[par] = 0u;
+            __threadfence();
+            asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(&C->pl_seq[par]), "l"(a.seq) : "memory");
+        }
+    }
+}
+
+// Acceptance thresholds for the next prescan from a regular select's lists (CTA 0, thread 0):
+// the keep oldest of E and R extrapolated to ~3 kPreK ranks. Agent-carrying slots are kept whole.
+__device__ void hints_from_fin(const DevPool& P, int NL, int keep) {
+    const int E = P.e_max, Rl = NL - 1;
+    const int lists[2] = {E, Rl};
+    for (int q = 0; q < 2; ++q) {
+        const int l = lists[q];
+        const int kl = keep_of(l, NL, keep);
+        const int n = P.fin_n[l];
+        unsigned long long h = kNoBound;
+        if (n == kl && n >= 2) {
+            const unsigned long long v1 = P.fin_lt[(long long)l * (kChunk + 2)];
+            const unsigned long long vk = P.fin_lt[(long long)l * (kChunk + 2) + n - 1];
+            const unsigned long long span = vk - v1;
+            const unsigned long long mult = (unsigned long long)((3 * kPreK + n - 1) / n);
+            h = span > (kNoBound - v1) / (mult + 1) ? kNoBound : v1 + span * mult;
+        }
+        P.pre_hint[q] = h;
+    }
+    P.pre_hint[2] = kNoBound;
+}
+
+// CTA 0, after phase 0: chunk 0's E and R lists (exact, sorted) and the other classes'
+// non-empty flags from the previous launch's prescan (parity par). False: unusable.
+__device__ bool consume_prescan(const DevPool& P, const AdmitArgs& a, const ScanBufs& B, ScanSmem& S, RedSmem& Red,
+                                int par) {
+    const int tid = threadIdx.x, T = blockDim.x;
+    const int NL = P.n_lists, E = P.e_max, Rl = NL - 1;
+    // U: the slots unpinned since the prescan may have read them (see above)
+    for (int j = tid; j < kXset; j += T) S.xset[j] = kNoSlot;
+    for (int x = tid; x < a.n_agents; x += T) B.cls[x] = __ldcg(P.cls + x);
+    if (tid < kMaxLists) S.lcnt[tid] = 0;
+    if (tid == 0) S.side_n = 0;
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kMaxUnpinRanges; ++r)
+        if (r < a.n_unpin_ranges)
+            for (int i = tid; i < a.unpin_n[r]; i += T)
+                if (a.unpin_ptr[r][i] != kNoSlot) xset_insert(S, a.unpin_ptr[r][i]);
+#pragma unroll
+    for (int r = 0; r < kMaxUnpinRanges + 1; ++r)
+        if (r < a.n_prev_ranges)
+            for (int i = tid; i < a.prev_n[r]; i += T)
+                if (a.prev_ptr[r][i] != kNoSlot) xset_insert(S, a.prev_ptr[r][i]);
+    __syncthreads();
+    const unsigned long long TE = P.pl_T[par * 3 + 0], TR = P.pl_T[par * 3 + 1], TP = P.pl_T[par * 3 + 2];
+    const unsigned long long TEs = min(TE, TP);  // agentless E members complete to TE, agent-carrying to TP
+    const int nE = P.pl_n[par * 3 + 0], nR = P.pl_n[par * 3 + 1], nP = P.pl_n[par * 3 + 2];
+    const size_t bE = ((size_t)par * 3 + 0) * kPendCap, bR = ((size_t)par * 3 + 1) * kPendCap,
+                 bP = ((size_t)par * 3 + 2) * kPendCap;
+    // staging view: [0, kPreK) E entries + valid flag, [kPreK, 2 kPreK) R entries + flag,
+    // extras (E members outside the agentless list) in the side buffers
+    unsigned long long* xl = B.sd_lt;
+    unsigned int* xs = B.sd_slot;
+    for (int j = tid; j < nE; j += T) {
+        const unsigned long long x = P.pl_lt[bE + j];
+        const unsigned int s = P.pl_slot[bE + j];
+        B.st_lt[j] = x;
+        B.st_slot[j] = s;
+        B.st_list[j] = (__ldcg(P.lt + s) == x && x <= TEs && !xset_has(S, s)) ? 1 : 0;
+    }
+    for (int j = tid; j < nR; j += T) {
+        const unsigned long long x = P.pl_lt[bR + j];
+        const unsigned int s = P.pl_slot[bR + j];
+        B.st_lt[kPreK + j] = x;
+        B.st_slot[kPreK + j] = s;
+        B.st_list[kPreK + j] = __ldcg(P.lt + s) == x ? 1 : 0;
+    }
+    auto add_member = [&](unsigned long long x, unsigned int s, int c) {
+        if (c == E) {
+            if (x <= TEs) {
+                const int p = atomicAdd(&S.side_n, 1);
+                if (p < kSide) {
+                    xl[p] = x;
+                    xs[p] = s;
+                }
+            }
+        } else {
+            S.lcnt[c] = 1;
+        }
+    };
+    for (int j = tid; j < nP; j += T) {  // agent-carrying unpinned slots: class from this launch's BFS
+        const unsigned long long x = P.pl_lt[bP + j];
+        const unsigned int s = P.pl_slot[bP + j];
+        if (__ldcg(P.lt + s) != x || xset_has(S, s)) continue;
+        add_member(x, s, B.cls[P.pl_agent[(size_t)par * kPendCap + j]]);
+    }
+    for (int j = tid; j < kXset; j += T) {  // U: re-read
+        const unsigned int s = S.xset[j];
+        if (s == kNoSlot) continue;
+        const unsigned long long x = __ldcg(P.lt + s);
+        if (x == kFreeTick || __ldcg(P.refs + s) != 0u) continue;
+        const unsigned int ag = __ldcg(P.agent + s);
+        add_member(x, s, ag == kNoAgent ? E : B.cls[ag]);
+    }
+    __syncthreads();
+    if (TP < kNoBound && tid < E) S.lcnt[tid] = 1;  // some agent-carrying members unseen: assume present
+    const int nx = S.side_n;
+    // exclusive prefix of the valid flags of E and R (sorted lists keep their order)
+    int fe = 0, fr = 0;
+    {
+        const int q = tid < kPreK ? tid : 0;
+        const int ve = tid < nE ? B.st_list[q] : 0;
+        const int vr = tid < nR ? B.st_list[kPreK + q] : 0;
+        const long long both = ((long long)ve << 32) | vr;
+        // block-wide exclusive scan over 256 entries (kPreK <= blockDim)
+        long long incl = both;
+        for (int o = 1; o < 32; o <<= 1) {
+            const long long y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane_id() >= o) incl += y;
+        }
+        if (lane_id() == 31) Red.v[warp_id()] = incl;
+        __syncthreads();
+        long long off = 0;
+        for (int w = 0; w < warp_id(); ++w) off += Red.v[w];
+        const long long excl = off + incl - both;
+        fe = (int)(excl >> 32);
+        fr = (int)(excl & 0xffffffffll);
+        __syncthreads();
+        if (tid == (int)blockDim.x - 1) {
+            Red.u[0] = (unsigned long long)(off + incl);  // totals
+        }
+        __syncthreads();
+    }
+    const long long tot = (long long)Red.u[0];
+    const int totE = (int)(tot >> 32), totR = (int)(tot & 0xffffffffll);
+    const bool ok = nx <= kSide && (totR > 0 || TR >= kNoBound);
+    if (!ok) return false;
+    const int capE = kChunk + 1, capR = kChunk + 1;
+    // R: the valid entries in order
+    if (tid < nR && B.st_list[kPreK + tid] && fr < capR) {
+        P.fin_lt[(long long)Rl * (kChunk + 2) + fr] = B.st_lt[kPreK + tid];
+        P.fin_slot[(long long)Rl * (kChunk + 2) + fr] = B.st_slot[kPreK + tid];
+    }
+    // E: merge of the valid agentless entries (sorted) with the extras (unsorted, few)
+    if (tid < nE && B.st_list[tid]) {
+        const unsigned long long x = B.st_lt[tid];
+        int r = fe;
+        for (int k = 0; k < nx; ++k) r += xl[k] < x;
+        if (r < capE) {
+            P.fin_lt[(long long)E * (kChunk + 2) + r] = x;
+            P.fin_slot[(long long)E * (kChunk + 2) + r] = B.st_slot[tid];
+        }
+    }
+    for (int i = tid; i < nx; i += T) {
+        const unsigned long long x = xl[i];
+        int r = 0;
+        for (int k = 0; k < nx; ++k) r += xl[k] < x;
+        int lo2 = 0, hi2 = nE;  // valid agentless entries below x: binary search + prefix flag count
+        while (lo2 < hi2) {
+            const int mid = (lo2 + hi2) >> 1;
+            if (B.st_lt[mid] < x) lo2 = mid + 1;
+            else hi2 = mid;
+        }
+        int cnt = 0;
+        for (int k = 0; k < lo2; ++k) cnt += B.st_list[k];
+        r += cnt;
+        if (r < capE) {
+            P.fin_lt[(long long)E * (kChunk + 2) + r] = x;
+            P.fin_slot[(long long)E * (kChunk + 2) + r] = xs[i];
+        }
+    }
+    if (tid == 0) {
+        P.fin_n[E] = min(totE + nx, capE);
+        P.fin_n[Rl] = min(totR, capR);
+    }
+    for (int c = tid; c < NL; c += T)
+        if (c != E && c != Rl) P.gcount[c] = S.lcnt[c];
+    __threadfence_block();
+    __syncthreads();
+    return true;
+}
+
 // ------------------------------------------------------------------ K5b: replay + apply
 
 __device__ __forceinline__ unsigned int hslot(unsigned int s) { return (s * 2654435761u) >> 23; }  // 9 bits
@@ -1162,7 +1570,7 @@ __device__ void load_lists(const DevPool& P, ReplaySmem& R, int NL, bool scanned
 // early: only lists E and R are final (CTA 0 finalized E, CTA 1 signalled R); the other
 // lists are awaited only if the bulk test fails.
 __device__ void replay_apply(const DevPool& P, const AdmitArgs& a, ReplaySmem& R, AdmSmem& A, int NL, bool scanned,
-                             RedSmem& Red, bool early = false) {
+                             RedSmem& Red, bool early = false, bool pre = false) {
     Ctrl* C = P.ctrl;
     const int tid = threadIdx.x, T = blockDim.x;
     const int lo = A.chunk * kChunk;
@@ -1265,6 +1673,11 @@ __device__ void replay_apply(const DevPool& P, const AdmitArgs& a, ReplaySmem& R
         }
         if (tid == 0) R.bulk = bulk ? 1 : 0;
         __syncthreads();
+    }
+    if (!R.bulk && pre) {  // prescan lists feed only the bulk replay: nothing applied, scan instead
+        if (tid == 0) A.need_full = 1;
+        __syncthreads();
+        return;
     }
     if (!R.bulk && early) {  // the serial replay needs every list: wait for the other finalizers
         if (tid == 0) {
@@ -1712,11 +2125,72 @@ __global__ void __launch_bounds__(kThreads + 32, 1) admit_kernel(DevPool P, Admi
     }
     __syncthreads();
 
+    // ---- prescan: CTAs 1.. stream the pool for the NEXT admission while CTA 0 serves this one
+    // from the lists the previous launch's prescan produced (validated, see consume_prescan)
+    const int par_prev = (int)((a.seq - 1ull) & 1ull), par_next = (int)(a.seq & 1ull);
+    const bool pre_run = (a.flags & kPrescan) && gridDim.x >= 2;
+    const bool pre_avail = pre_run && (a.flags & kUsePrescan) &&
+                           *(volatile unsigned long long*)&C->pl_seq[par_prev] == a.seq - 1ull &&
+                           *(volatile int*)&C->pl_ok[par_prev] != 0;
+    bool run_loop = true;
+    bool pending_rescan = false;  // CTA 0: the last pass must be redone (safe, no hints)
+    if (pre_avail) {
+        if (blockIdx.x != 0) {
+            const unsigned long long hE = __ldcg(P.pre_hint + 0), hR = __ldcg(P.pre_hint + 1), hP = hE;
+            prescan_pass(P, B, S, dsm, par_next);
+            prescan_barrier(C);
+            prescan_finish(P, a, B, Sel, par_next, hE, hR, hP);
+            if (tid == 0) {
+                unsigned long long spins = 0;
+                while (ld_acquire_u64(&C->verdict_seq) != a.seq) {
+                    if (++spins > 4096) __nanosleep(128);
+                    if (spins > (1ull << 28)) __trap();
+                }
+            }
+            __syncthreads();
+            run_loop = *(volatile int*)&C->verdict == 2;
+            if (!run_loop) return;
+        } else {
+            if (tid == 0) {  // this launch's scoring pass is the prescan
+                A.scans += 1;
+                C->scans += 1;
+                C->scanned_slots += P.cap;
+                A.need_full = 0;
+            }
+            __syncthreads();
+            bool need_loop = false;
+            if (A.started && !A.error && A.admit_n > 0) {
+                replay_prologue(P, Rp, A, Red);
+                stamp(A, 1);
+                const bool need0 = C->resident + Rp.absent > P.cap;
+                const bool ok = need0 ? consume_prescan(P, a, B, S, Red, par_prev) : true;
+                stamp(A, 3);
+                if (ok) replay_apply(P, a, Rp, A, NL, need0, Red, true, true);
+                if (tid == 0) {
+                    if (ok && !A.need_full) {
+                        A.chunk = 1;
+                        C->pre_used += 1;
+                    } else {
+                        C->pre_fallbacks += 1;
+                    }
+                }
+                __syncthreads();
+                stamp(A, 4);
+                need_loop = A.chunk * kChunk < A.admit_n;
+            }
+            if (tid == 0) {
+                C->verdict = need_loop ? 2 : 1;
+                __threadfence();
+                asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(&C->verdict_seq), "l"(a.seq) : "memory");
+            }
+            run_loop = need_loop;
+        }
+    }
+
     // ---- speculative first pass: every CTA but 0 starts scanning at once, concurrently with
     // phase 0. Slots phase 0 may change are left out and restaged by CTA 0 with their new
     // state; agent-carrying slots are classified once phase 0 has fixed the survival classes.
-    bool pending_rescan = false;  // CTA 0: the last pass must be redone (safe, no hints)
-    if ((a.flags & kSpeculate) && gridDim.x > 1) {
+    if (!pre_avail && (a.flags & kSpeculate) && gridDim.x > 1) {
         const int keep0 = min(a.n, kChunk);
         int need_scan0 = 0;
         if (tid == 0) {
@@ -1808,11 +2282,14 @@ __global__ void __launch_bounds__(kThreads + 32, 1) admit_kernel(DevPool P, Admi
     // ---- command loop. CTA 0 decides the next step (scan pass of a chunk, or done); every CTA
     // scans; CTAs 0..NL-1 select one list each; only CTA 0 consumes the lists, so it waits on
     // a counter instead of a grid barrier; CTA 0 replays. Per chunk: 2 grid barriers.
-    for (;;) {
+    for (; run_loop;) {
         if (blockIdx.x == 0) {
             const bool stop = !A.started || A.error || A.chunk * kChunk >= A.admit_n;
             if (stop) {
-                if (tid == 0) C->done = 1;
+                if (tid == 0) {
+                    C->done = 1;
+                    if (pre_run && !pre_avail) hints_from_fin(P, NL, C->keep);  // for the prescan below
+                }
             } else if (pending_rescan) {
                 // a hint was too tight (or the fast pass overflowed): same chunk, safe pass
                 if (tid < NL) {
@@ -1907,6 +2384,20 @@ __global__ void __launch_bounds__(kThreads + 32, 1) admit_kernel(DevPool P, Admi
             __syncthreads();
             stamp(A, 4);
         }
+    }
+
+    // ---- no usable prescan came in: CTAs 1.. now prescan for the next admission
+    if (pre_run && !pre_avail && blockIdx.x != 0) {
+        const unsigned long long hE = __ldcg(P.pre_hint + 0), hR = __ldcg(P.pre_hint + 1), hP = hE;
+        prescan_pass(P, B, S, dsm, par_next);
+        prescan_barrier(C);
+        prescan_finish(P, a, B, Sel, par_next, hE, hR, hP);
+        return;
+    }
+    if (pre_run && !pre_avail && blockIdx.x == 0 && tid == 0) {
+        A.scans += 1;
+        C->scans += 1;
+        C->scanned_slots += P.cap;
     }
 
     // ---- epilogue (CTA 0): EngineSim::admit unpins at once; pins out; status

@@ -79,7 +79,23 @@ struct Ctrl {
     unsigned long long p0_seq;  // AdmitArgs::seq of the launch whose phase 0 finished
     int tq_erase, tq_insert;    // block-table updates queued by the last admission (applied next)
     unsigned long long r_seq;   // AdmitArgs::seq once the resident-oldest list is final
+    // prescan: the next admission's scoring pass, run by CTAs 1.. of this launch while CTA 0
+    // serves this admission; double-buffered by launch-sequence parity
+    unsigned int pbar_count, pbar_gen;  // barrier of the prescan CTAs
+    int pre_cnt[2][3];                  // raw candidates written per list (E, R, pending)
+    int pre_bad[2];                     // staging / buffer overflow: the prescan is unusable
+    unsigned int pre_fin[2];            // prescan lists finalized
+    unsigned long long pl_seq[2];       // AdmitArgs::seq of the launch that produced the lists
+    int pl_ok[2];
+    unsigned long long verdict_seq;     // CTA 0 -> prescan CTAs: this launch's verdict is out
+    int verdict;                        // 1: done, 2: everyone joins the command loop
+    long long pre_used, pre_fallbacks, pre_badcnt;  // instrumentation
 };
+
+// prescan list lengths: E (agentless unpinned) and R (resident) keep the kPreK oldest; the
+// agent-carrying unpinned slots (classified by the consumer, after its BFS) are kept whole
+constexpr int kPreK = 256;
+constexpr int kPendCap = 4096;
 
 // ---------------------------------------------------------------- hash-sharded pool
 // A pool of budget N split over G GPUs: a block lives on shard owner(key) = (key >> 40) % G.
@@ -178,6 +194,19 @@ struct DevPool {
     unsigned int* tq_slot;
 
     Ctrl* ctrl;
+
+    // prescan output [parity][list E, R, pending][kPendCap] (E and R use the first kPreK),
+    // its completeness thresholds [parity][3], the raw per-list candidates [3][pre_gcap] and
+    // the acceptance thresholds of the next prescan [3]
+    unsigned long long* pl_lt;
+    unsigned int* pl_slot;
+    unsigned int* pl_agent;
+    int* pl_n;
+    unsigned long long* pl_T;
+    unsigned long long* pre_buf_lt;
+    unsigned int* pre_buf_slot;
+    long long pre_gcap;
+    unsigned long long* pre_hint;
 
     // hash-sharded mode (world > 1 or an explicit shard): this shard's rank, the shard count,
     // the GLOBAL budget, the exchange buffers and the replicated admission state

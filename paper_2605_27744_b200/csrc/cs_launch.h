@@ -16,7 +16,9 @@ enum AdmitFlags : int {
     kUnpinAfter = 32,  // EngineSim::admit: unpin immediately
     kPollReset = 64,   // a poll_actions drain happened before this call
     kAdmit = 128,      // run admit_pinned at all (lookup-only / observe-only calls clear it)
-    kSpeculate = 256   // scan chunk 0 concurrently with phase 0 (cooperative grid only)
+    kSpeculate = 256,  // scan chunk 0 concurrently with phase 0 (cooperative grid only)
+    kPrescan = 512,    // CTAs 1.. run the NEXT admission's scoring pass in this launch
+    kUsePrescan = 1024 // chunk 0 may use the lists the previous launch's prescan produced
 };
 
 constexpr int kMaxUnpinRanges = 8;  // deferred EngineSim::unpin calls folded into one launch
@@ -65,6 +67,12 @@ struct AdmitArgs {
     const unsigned int* unpin_ptr[kMaxUnpinRanges];
     int unpin_n[kMaxUnpinRanges];
     int n_unpin_ranges;
+    // slots the PREVIOUS launch unpinned (its deferred unpins and, after a warmup, its own
+    // pins): with this launch's unpins, the only slots whose membership of a list can grow
+    // between the previous launch's prescan and this launch (kUsePrescan)
+    const unsigned int* prev_ptr[kMaxUnpinRanges + 1];
+    int prev_n[kMaxUnpinRanges + 1];
+    int n_prev_ranges;
 };
 
 struct LaunchCfg {

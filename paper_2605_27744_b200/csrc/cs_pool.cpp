@@ -132,6 +132,7 @@ void cs_pool::create(const cs_pool_cfg& c, long long shard_slots, cs_comm* cm) {
     ensure_prompt_scratch(4096);
 
     if (const char* e = std::getenv("CS_SPECULATE")) speculate = std::atoi(e) != 0;  // A/B switch (tools)
+    if (const char* e = std::getenv("CS_PRESCAN")) prescan = std::atoi(e) != 0;       // A/B switch (tools)
     // fl(w_pred * (1 - min(c, e_max) / e_max)) per survival class, as CacheSagePolicy::score and
     // ReachabilityState::survival compute it (reachability.cpp:17-20); host code builds with
     // -ffp-contract=off, so the product is the same IEEE double the device would form
@@ -147,6 +148,19 @@ void cs_pool::create(const cs_pool_cfg& c, long long shard_slots, cs_comm* cm) {
     p.gbuf_slot = dmalloc<unsigned int>((size_t)csb::kMaxLists * p.gcap, "gbuf_slot");
     p.gmin = dmalloc<unsigned long long>((size_t)csb::kMaxLists * lc.grid, "gmin");
     p.dbg = dmalloc<unsigned long long>((size_t)lc.grid * 16, "dbg");
+    p.pl_lt = dmalloc<unsigned long long>((size_t)2 * 3 * csb::kPendCap, "pl_lt");
+    p.pl_slot = dmalloc<unsigned int>((size_t)2 * 3 * csb::kPendCap, "pl_slot");
+    p.pl_agent = dmalloc<unsigned int>((size_t)2 * csb::kPendCap, "pl_agent");
+    p.pl_n = dmalloc<int>(6, "pl_n");
+    p.pl_T = dmalloc<unsigned long long>(6, "pl_T");
+    p.pre_gcap = (long long)lc.grid * 6144;  // every CTA's staging pool
+    p.pre_buf_lt = dmalloc<unsigned long long>((size_t)2 * p.pre_gcap, "pre_buf_lt");
+    p.pre_buf_slot = dmalloc<unsigned int>((size_t)2 * p.pre_gcap, "pre_buf_slot");
+    p.pre_hint = dmalloc<unsigned long long>(3, "pre_hint");
+    {
+        const unsigned long long h[3] = {csb::kNoBound, csb::kNoBound, csb::kNoBound};
+        ck(cudaMemcpy(p.pre_hint, h, sizeof(h), cudaMemcpyHostToDevice), "pre_hint");
+    }
     ck(cudaMemsetAsync(p.dbg, 0, sizeof(unsigned long long) * lc.grid * 16, stream), "memset");
 
     if (comm) {
@@ -168,7 +182,8 @@ void cs_pool::destroy() {
     void* ptrs[] = {p.lt, p.agent, p.refs, p.key, p.tokens, p.table, p.free_stack, p.evlog, p.counts, p.totals,
                     p.win_a, p.win_b, p.hop, p.cls, p.agent_ids, p.ctrl, p.gbound, p.gcount, p.fin_lt, p.fin_slot,
                     p.fin_n, p.p_slot, p.p_refs0, p.gbuf_lt, p.gbuf_slot, p.ghint, p.gmaxk, p.grej, p.dbg, p.gsmall, p.gmin, p.tq_key, p.tq_slot,
-                    p.sh_send1, p.sh_recv1, p.sh_send2, p.sh_recv2, p.sh_state, p.sh_gslot, p.sh_grefs0};
+                    p.sh_send1, p.sh_recv1, p.sh_send2, p.sh_recv2, p.sh_state, p.sh_gslot, p.sh_grefs0,
+                    p.pl_lt, p.pl_slot, p.pl_agent, p.pl_n, p.pl_T, p.pre_buf_lt, p.pre_buf_slot, p.pre_hint};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     d_keys.release();
@@ -329,10 +344,23 @@ const csb::AdmitStatus& cs_pool::admit(const csb::AdmitArgs& in, int n_for_grid)
         ++a.n_unpin_ranges;
     }
     const int xn = a.n + unpin_q_slots;
+    const int cur_unpins = unpin_q_slots;
     unpin_q.clear();
     unpin_q_slots = 0;
     a.seq = ++seq;
     if (speculate && grid > 1 && xn <= csb::kXsetMax) a.flags |= csb::kSpeculate;
+    if (prescan && grid > 1) a.flags |= csb::kPrescan;
+    a.n_prev_ranges = 0;
+    if ((a.flags & csb::kPrescan) && pre_ok && cur_unpins + prev_slots <= csb::kXsetMax &&
+        (int)prev_ranges.size() <= csb::kMaxUnpinRanges + 1) {
+        a.flags |= csb::kUsePrescan;
+        for (const auto& u : prev_ranges) {
+            a.prev_ptr[a.n_prev_ranges] = u.first;
+            a.prev_n[a.n_prev_ranges] = u.second;
+            ++a.n_prev_ranges;
+        }
+    }
+    pre_ok = false;
     st->started = -1;
     if (timing) ck(cudaEventRecord(ev0, stream), "cudaEventRecord");
     ck(csb::launch_admit(P, a, lc, grid, stream), "admit_kernel launch");
@@ -353,6 +381,18 @@ const csb::AdmitStatus& cs_pool::admit(const csb::AdmitArgs& in, int n_for_grid)
         }
     }
     if (st->started < 0) throw CsError(CS_ERR_CUDA, "admit kernel did not report a status");
+    // the slots this launch unpinned, for the next launch's use of this launch's prescan
+    prev_ranges.clear();
+    prev_slots = 0;
+    for (int r = 0; r < a.n_unpin_ranges; ++r) {
+        prev_ranges.emplace_back(a.unpin_ptr[r], a.unpin_n[r]);
+        prev_slots += a.unpin_n[r];
+    }
+    if ((a.flags & csb::kUnpinAfter) && a.pins_out && st->started && !st->error && st->admit_n > 0) {
+        prev_ranges.emplace_back(a.pins_out, st->admit_n);
+        prev_slots += st->admit_n;
+    }
+    pre_ok = (a.flags & csb::kPrescan) != 0 && !st->error;
     resident = st->resident;
     pinned = st->pinned;
     ev_total = st->ev_total;
@@ -377,6 +417,7 @@ void cs_pool::defer_unpin(const unsigned int* dev_slots, int n) {
 }
 
 void cs_pool::flush_unpins() {
+    if (!unpin_q.empty()) pre_ok = false;  // unpins outside an admission launch: no prescan reuse
     for (const auto& u : unpin_q) {
         ck(csb::launch_unpin(P, u.first, u.second, stream), "unpin");
         ++launches;
@@ -632,6 +673,7 @@ int cs_unpin_slots(cs_pool_t pool, const uint32_t* slots, int n) {
     return guard([&] {
         if (!pool || n < 0 || (n > 0 && !slots)) throw std::invalid_argument("cs_unpin_slots: null argument");
         pool->flush_unpins();
+        pool->pre_ok = false;
         pool->d_aux.ensure(sizeof(uint32_t) * std::max(n, 1));
         ck(cudaMemcpyAsync(pool->d_aux.p, slots, sizeof(uint32_t) * n, cudaMemcpyHostToDevice, pool->stream), "H2D");
         ck(csb::launch_unpin(pool->P, pool->d_aux.as<unsigned int>(), n, pool->stream), "unpin");
@@ -648,6 +690,7 @@ int cs_restore(cs_pool_t pool, const uint64_t* keys, const uint64_t* lt, const u
         if (!pool || n < 0 || (n > 0 && (!keys || !lt))) throw std::invalid_argument("cs_restore: null argument");
         pool->flush_unpins();
         pool->flush_table();
+        pool->pre_ok = false;
         // a shard keeps the snapshot blocks it owns (the caller may pass the whole snapshot)
         std::vector<uint64_t> fk, fl;
         std::vector<uint32_t> fa, fr;
@@ -775,6 +818,9 @@ int cs_pool_get_stats(cs_pool_t pool, cs_pool_stats* out) {
         out->rebuilds = c.rebuilds;
         out->n_agents = pool->n_agents;
         for (int k = 0; k < csb::kPhases; ++k) out->phase_ns[k] = pool->phase_ns[k];
+        out->prescan_used = c.pre_used;
+        out->prescan_fallbacks = c.pre_fallbacks;
+        out->prescan_unusable = c.pre_badcnt;
     });
 }
 

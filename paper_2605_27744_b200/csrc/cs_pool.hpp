@@ -78,6 +78,12 @@ struct cs_pool {
     unsigned long long phase_ns[csb::kPhases] = {};
     unsigned long long seq = 0;  // admission launch sequence (AdmitArgs::seq)
     bool speculate = true;       // overlap the first scan pass with phase 0 when it can evict
+    // prescan: every cooperative launch streams the pool for the NEXT admission (kPrescan); the
+    // next launch may use those lists (kUsePrescan) unless the pool changed out of band since
+    bool prescan = true;
+    bool pre_ok = false;
+    std::vector<std::pair<const unsigned int*, int>> prev_ranges;  // slots the last launch unpinned
+    int prev_slots = 0;
     // deferred EngineSim::unpin calls (device slot lists), folded into the next admission launch
     std::vector<std::pair<const unsigned int*, int>> unpin_q;
     int unpin_q_slots = 0;
