@@ -136,10 +136,38 @@ struct ReplaySmem {
     long long res0, pinned0, ftop;
     int absent, pre_unpinned;
     int n_ins;  // queued inserts of this chunk
+    int lists_ready;  // the consumer of a prescan wrote L_* (and E keys) directly
+    unsigned long long E_key[kChunk + 2];  // keys of list E (lists_ready): victims need no key load
+    unsigned char E_key_ok[kChunk + 2];
 };
 // The replay view lives in the TMA ring: free after a scan, and never used by CTA 0 during a
 // speculative pass, so CTA 0 prepares the prologue while the other CTAs still stream.
 static_assert(sizeof(ReplaySmem) <= kRing * kRingStage, "replay view must fit the TMA ring");
+
+// Early prescan validation (CTA 0, pre path): loaded during phase 0's two load rounds, so the
+// consumer of a prescan works on chip. Lives in the TMA ring above the replay view.
+constexpr int kEarlyP = 256;  // agent-carrying entries validated early (more: the late consumer)
+constexpr int kTset = 1024;   // slots touched by this launch's lookup (hash)
+struct EarlySmem {
+    unsigned long long E_lt[kPreK], E_key[kPreK];
+    unsigned int E_slot[kPreK];
+    unsigned char E_ok[kPreK];
+    unsigned long long R_lt[kPreK];
+    unsigned int R_slot[kPreK];
+    unsigned char R_ok[kPreK];
+    unsigned long long P_lt[kEarlyP];
+    unsigned int P_slot[kEarlyP], P_agent[kEarlyP];
+    unsigned char P_ok[kEarlyP];
+    unsigned long long U_lt[kXset];  // U re-read after the unpins, by xset position
+    unsigned int U_agent[kXset];
+    unsigned char U_ok[kXset];
+    unsigned int tset[kTset];
+    unsigned long long TE, TR, TP;
+    int nE, nR, nP, ok;
+};
+constexpr size_t kEarlyOff = 64 * 1024;
+static_assert(sizeof(ReplaySmem) <= kEarlyOff, "replay view must stay below the early-validation view");
+static_assert(kEarlyOff + sizeof(EarlySmem) <= kRing * kRingStage, "early-validation view must fit the TMA ring");
 
 struct BfsSmem {
     unsigned short wa[8192];
@@ -163,6 +191,11 @@ __device__ __forceinline__ void stamp(AdmSmem& A, int k) {
     }
 }
 
+// CTA-0 serial-chain timestamps (%globaltimer), after the per-CTA rows (instrumentation)
+__device__ __forceinline__ void pstamp(const DevPool& P, int k) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) P.dbg[gridDim.x * 16 + k] = gtimer();
+}
+
 // CTA-0 sub-phase timestamps of the replay (instrumentation row 0, columns 10..15)
 __device__ __forceinline__ void dstamp(const DevPool& P, int k) {
     if (blockIdx.x == 0 && threadIdx.x == 0) P.dbg[10 + k] = clock64();
@@ -177,7 +210,7 @@ __device__ __forceinline__ void fstamp(const DevPool& P, int k) {
 
 // CacheSagePolicy::observe(AgentDispatch) (cachesage_policy.cpp:57-72). CTA 0, all threads.
 __device__ void observe_dispatch(const DevPool& P, int prev, int next, unsigned long long tick, int n_agents,
-                                 unsigned char* dsm, RedSmem& Red, AdmSmem& A) {
+                                 unsigned char* dsm, RedSmem& Red, AdmSmem& A, unsigned char* cls_smem = nullptr) {
     Ctrl* C = P.ctrl;
     const int tid = threadIdx.x, T = blockDim.x;
     const long long W = P.window;
@@ -203,6 +236,7 @@ __device__ void observe_dispatch(const DevPool& P, int prev, int next, unsigned 
         }
     }
     __syncthreads();
+    pstamp(P, 13);
     const bool changed = C->cur_agent != next;
     __syncthreads();
     if (tid == 0) C->cur_agent = next;
@@ -252,6 +286,7 @@ __device__ void observe_dispatch(const DevPool& P, int prev, int next, unsigned 
         for (int x = tid; x < n_agents; x += T) {
             P.hop[x] = B.hop[x];
             P.cls[x] = B.hop[x];
+            if (cls_smem) cls_smem[x] = B.hop[x];  // the admission kernel's class table on chip
         }
         if (tid == 0) {
             C->rebuilds += 1ull;
@@ -259,6 +294,7 @@ __device__ void observe_dispatch(const DevPool& P, int prev, int next, unsigned 
         }
         __syncthreads();
     }
+    pstamp(P, 14);
     // K6: maybe_prefetch (cachesage_policy.cpp:109-123) with argmax_row
     // (transition_learner.cpp:79-96): max count, ties -> smaller 64-bit AgentId
     const int budget_ok = C->step_warmups < P.budget_per_step;
@@ -478,12 +514,21 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* m, unsigned int pa
         : "memory");
 }
 
-// 1-D bulk copy global -> this CTA's shared memory, completion counted on mbarrier m
+// 1-D bulk copy global -> this CTA's shared memory, completion counted on mbarrier m. The pool
+// stream is read once per pass: it is marked evict-first in L2, so it does not flush the small
+// hot state CTA 0's serial chain works on (block table entries, prescan lists, learner).
+__device__ __forceinline__ unsigned long long l2_evict_first() {
+    unsigned long long pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned int bytes, unsigned long long* m) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_u32(m))
-                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(m)), "l"(l2_evict_first())
+        : "memory");
 }
 
 // One streaming pass over this CTA's contiguous slot range: 16 B per slot read exactly once.
@@ -590,6 +635,37 @@ __device__ __forceinline__ void read4(const unsigned char* st, int tid, bool val
     }
 }
 
+// ---- the unpin ranges of a launch as one flat index space: every thread loads its own entry,
+// so a launch's ranges cost one round of loads instead of one per range
+__device__ __forceinline__ int unpin_total(const AdmitArgs& a, bool with_prev) {
+    int t = 0;
+#pragma unroll
+    for (int r = 0; r < kMaxUnpinRanges; ++r) t += r < a.n_unpin_ranges ? a.unpin_n[r] : 0;
+    if (with_prev) {
+#pragma unroll
+        for (int r = 0; r < kMaxUnpinRanges + 1; ++r) t += r < a.n_prev_ranges ? a.prev_n[r] : 0;
+    }
+    return t;
+}
+
+__device__ __forceinline__ unsigned int unpin_at(const AdmitArgs& a, int i) {
+#pragma unroll
+    for (int r = 0; r < kMaxUnpinRanges; ++r) {
+        if (r < a.n_unpin_ranges) {
+            if (i < a.unpin_n[r]) return a.unpin_ptr[r][i];
+            i -= a.unpin_n[r];
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < kMaxUnpinRanges + 1; ++r) {
+        if (r < a.n_prev_ranges) {
+            if (i < a.prev_n[r]) return a.prev_ptr[r][i];
+            i -= a.prev_n[r];
+        }
+    }
+    return kNoSlot;
+}
+
 // ---- speculative pass support: the set of slots phase 0 may change (the prompt's resident
 // blocks, touched by lookup / pinned by admit_pinned, and the slots unpinned first) and the
 // deferred classification of agent-carrying slots (the BFS of phase 0 may move them).
@@ -627,11 +703,11 @@ __device__ void build_xset(const DevPool& P, const AdmitArgs& a, ScanSmem& S) {
         const unsigned int s = __ldcg(P.p_slot + i);
         if (s != kNoSlot) xset_insert(S, s);
     }
-#pragma unroll
-    for (int r = 0; r < kMaxUnpinRanges; ++r)  // constant indices into the kernel parameters
-        if (r < a.n_unpin_ranges)
-            for (int i = tid; i < a.unpin_n[r]; i += T)
-                if (a.unpin_ptr[r][i] != kNoSlot) xset_insert(S, a.unpin_ptr[r][i]);
+    const int nu = unpin_total(a, false);
+    for (int i = tid; i < nu; i += T) {
+        const unsigned int us = unpin_at(a, i);
+        if (us != kNoSlot) xset_insert(S, us);
+    }
     __syncthreads();
 }
 
@@ -729,11 +805,11 @@ __device__ void producer_prep(const DevPool& P, const AdmitArgs& a, const ScanBu
         const unsigned int sl = __ldcg(P.p_slot + i);
         if (sl != kNoSlot) xset_insert(S, sl);
     }
-#pragma unroll
-    for (int r = 0; r < kMaxUnpinRanges; ++r)
-        if (r < a.n_unpin_ranges)
-            for (int i = lane; i < a.unpin_n[r]; i += 32)
-                if (a.unpin_ptr[r][i] != kNoSlot) xset_insert(S, a.unpin_ptr[r][i]);
+    const int nu = unpin_total(a, false);
+    for (int i = lane; i < nu; i += 32) {
+        const unsigned int us = unpin_at(a, i);
+        if (us != kNoSlot) xset_insert(S, us);
+    }
     __syncwarp();
     if (lane == 0) S.prep_done = 1;
 }
@@ -1335,17 +1411,15 @@ __device__ bool consume_prescan(const DevPool& P, const AdmitArgs& a, const Scan
     if (tid < kMaxLists) S.lcnt[tid] = 0;
     if (tid == 0) S.side_n = 0;
     __syncthreads();
-#pragma unroll
-    for (int r = 0; r < kMaxUnpinRanges; ++r)
-        if (r < a.n_unpin_ranges)
-            for (int i = tid; i < a.unpin_n[r]; i += T)
-                if (a.unpin_ptr[r][i] != kNoSlot) xset_insert(S, a.unpin_ptr[r][i]);
-#pragma unroll
-    for (int r = 0; r < kMaxUnpinRanges + 1; ++r)
-        if (r < a.n_prev_ranges)
-            for (int i = tid; i < a.prev_n[r]; i += T)
-                if (a.prev_ptr[r][i] != kNoSlot) xset_insert(S, a.prev_ptr[r][i]);
+    {
+        const int nu = unpin_total(a, true);
+        for (int i = tid; i < nu; i += T) {
+            const unsigned int us = unpin_at(a, i);
+            if (us != kNoSlot) xset_insert(S, us);
+        }
+    }
     __syncthreads();
+    pstamp(P, 7);
     const unsigned long long TE = P.pl_T[par * 3 + 0], TR = P.pl_T[par * 3 + 1], TP = P.pl_T[par * 3 + 2];
     const unsigned long long TEs = min(TE, TP);  // agentless E members complete to TE, agent-carrying to TP
     const int nE = P.pl_n[par * 3 + 0], nR = P.pl_n[par * 3 + 1], nP = P.pl_n[par * 3 + 2];
@@ -1355,20 +1429,6 @@ __device__ bool consume_prescan(const DevPool& P, const AdmitArgs& a, const Scan
     // extras (E members outside the agentless list) in the side buffers
     unsigned long long* xl = B.sd_lt;
     unsigned int* xs = B.sd_slot;
-    for (int j = tid; j < nE; j += T) {
-        const unsigned long long x = P.pl_lt[bE + j];
-        const unsigned int s = P.pl_slot[bE + j];
-        B.st_lt[j] = x;
-        B.st_slot[j] = s;
-        B.st_list[j] = (__ldcg(P.lt + s) == x && x <= TEs && !xset_has(S, s)) ? 1 : 0;
-    }
-    for (int j = tid; j < nR; j += T) {
-        const unsigned long long x = P.pl_lt[bR + j];
-        const unsigned int s = P.pl_slot[bR + j];
-        B.st_lt[kPreK + j] = x;
-        B.st_slot[kPreK + j] = s;
-        B.st_list[kPreK + j] = __ldcg(P.lt + s) == x ? 1 : 0;
-    }
     auto add_member = [&](unsigned long long x, unsigned int s, int c) {
         if (c == E) {
             if (x <= TEs) {
@@ -1382,21 +1442,39 @@ __device__ bool consume_prescan(const DevPool& P, const AdmitArgs& a, const Scan
             S.lcnt[c] = 1;
         }
     };
-    for (int j = tid; j < nP; j += T) {  // agent-carrying unpinned slots: class from this launch's BFS
-        const unsigned long long x = P.pl_lt[bP + j];
-        const unsigned int s = P.pl_slot[bP + j];
-        if (__ldcg(P.lt + s) != x || xset_has(S, s)) continue;
-        add_member(x, s, B.cls[P.pl_agent[(size_t)par * kPendCap + j]]);
-    }
-    for (int j = tid; j < kXset; j += T) {  // U: re-read
-        const unsigned int s = S.xset[j];
-        if (s == kNoSlot) continue;
-        const unsigned long long x = __ldcg(P.lt + s);
-        if (x == kFreeTick || __ldcg(P.refs + s) != 0u) continue;
-        const unsigned int ag = __ldcg(P.agent + s);
-        add_member(x, s, ag == kNoAgent ? E : B.cls[ag]);
+    // one flat pass (independent loads): E entries, R entries, pending entries, U re-reads
+    const int nall = nE + nR + nP + kXset;
+    for (int q = tid; q < nall; q += T) {
+        if (q < nE) {
+            const unsigned long long x = P.pl_lt[bE + q];
+            const unsigned int s = P.pl_slot[bE + q];
+            B.st_lt[q] = x;
+            B.st_slot[q] = s;
+            B.st_list[q] = (__ldcg(P.lt + s) == x && x <= TEs && !xset_has(S, s)) ? 1 : 0;
+        } else if (q < nE + nR) {
+            const int j = q - nE;
+            const unsigned long long x = P.pl_lt[bR + j];
+            const unsigned int s = P.pl_slot[bR + j];
+            B.st_lt[kPreK + j] = x;
+            B.st_slot[kPreK + j] = s;
+            B.st_list[kPreK + j] = __ldcg(P.lt + s) == x ? 1 : 0;
+        } else if (q < nE + nR + nP) {  // agent-carrying unpinned: class from this launch's BFS
+            const int j = q - nE - nR;
+            const unsigned long long x = P.pl_lt[bP + j];
+            const unsigned int s = P.pl_slot[bP + j];
+            if (__ldcg(P.lt + s) != x || xset_has(S, s)) continue;
+            add_member(x, s, B.cls[P.pl_agent[(size_t)par * kPendCap + j]]);
+        } else {  // U: re-read
+            const unsigned int s = S.xset[q - nE - nR - nP];
+            if (s == kNoSlot) continue;
+            const unsigned long long x = __ldcg(P.lt + s);
+            if (x == kFreeTick || __ldcg(P.refs + s) != 0u) continue;
+            const unsigned int ag = __ldcg(P.agent + s);
+            add_member(x, s, ag == kNoAgent ? E : B.cls[ag]);
+        }
     }
     __syncthreads();
+    pstamp(P, 8);
     if (TP < kNoBound && tid < E) S.lcnt[tid] = 1;  // some agent-carrying members unseen: assume present
     const int nx = S.side_n;
     // exclusive prefix of the valid flags of E and R (sorted lists keep their order)
@@ -1474,6 +1552,140 @@ __device__ bool consume_prescan(const DevPool& P, const AdmitArgs& a, const Scan
     return true;
 }
 
+__device__ __forceinline__ bool tset_insert(unsigned int* t, unsigned int s) {
+    unsigned int h = xhash(s);
+    for (int c = 0; c < kTset; ++c) {
+        const unsigned int old = atomicCAS(&t[h], kNoSlot, s);
+        if (old == kNoSlot || old == s) return true;
+        h = (h + 1) & (kTset - 1);
+    }
+    return false;
+}
+
+__device__ __forceinline__ bool tset_has(const unsigned int* t, unsigned int s) {
+    unsigned int h = xhash(s);
+    for (int c = 0; c < kTset; ++c) {
+        const unsigned int k = t[h];
+        if (k == s) return true;
+        if (k == kNoSlot) return false;
+        h = (h + 1) & (kTset - 1);
+    }
+    return false;
+}
+
+// The consumer of a prescan when phase 0 did its loads (es->ok): the previous launch's lists,
+// validated against the pool as this launch found it, minus this launch's phase-0 changes
+// (touched prefix = tset, unpinned = U); writes chunk 0's E and R lists, E's keys and the other
+// classes' non-empty flags straight into the replay view. On-chip only. False: unusable.
+__device__ bool consume_early(const DevPool& P, const EarlySmem& es, ReplaySmem& R, const ScanBufs& B, ScanSmem& S,
+                              RedSmem& Red) {
+    const int tid = threadIdx.x, T = blockDim.x;
+    const int NL = P.n_lists, E = P.e_max, Rl = NL - 1;
+    const unsigned long long TEs = min(es.TE, es.TP), TR = es.TR, TP = es.TP;
+    const int nE = es.nE, nR = es.nR, nP = es.nP;
+    unsigned long long* xl = B.sd_lt;
+    unsigned int* xs = B.sd_slot;
+    unsigned char* ef = B.st_list;  // E flags [0, kPreK), R flags [kPreK, 2 kPreK)
+    if (tid < kMaxLists) S.lcnt[tid] = 0;
+    if (tid == 0) S.side_n = 0;
+    __syncthreads();
+    auto add_member = [&](unsigned long long x, unsigned int s, int c) {
+        if (c == E) {
+            if (x <= TEs) {
+                const int p = atomicAdd(&S.side_n, 1);
+                if (p < kSide) {
+                    xl[p] = x;
+                    xs[p] = s;
+                }
+            }
+        } else {
+            S.lcnt[c] = 1;
+        }
+    };
+    for (int q = tid; q < nE + nR + nP + kXset; q += T) {
+        if (q < nE) {
+            const unsigned int s = es.E_slot[q];
+            ef[q] = (es.E_ok[q] && es.E_lt[q] <= TEs && !xset_has(S, s) && !tset_has(es.tset, s)) ? 1 : 0;
+        } else if (q < nE + nR) {
+            const int j = q - nE;
+            ef[kPreK + j] = (es.R_ok[j] && !tset_has(es.tset, es.R_slot[j])) ? 1 : 0;
+        } else if (q < nE + nR + nP) {
+            const int j = q - nE - nR;
+            const unsigned int s = es.P_slot[j];
+            if (es.P_ok[j] && !xset_has(S, s) && !tset_has(es.tset, s)) add_member(es.P_lt[j], s, B.cls[es.P_agent[j]]);
+        } else {
+            const int j = q - nE - nR - nP;
+            const unsigned int s = S.xset[j];
+            if (s == kNoSlot || !es.U_ok[j] || tset_has(es.tset, s)) continue;
+            const unsigned int ag = es.U_agent[j];
+            add_member(es.U_lt[j], s, ag == kNoAgent ? E : B.cls[ag]);
+        }
+    }
+    __syncthreads();
+    if (TP < kNoBound && tid < E) S.lcnt[tid] = 1;  // some agent-carrying members unseen: assume present
+    const int nx = S.side_n;
+    int fe = 0, fr = 0;
+    {
+        const int q = tid < kPreK ? tid : 0;
+        const long long both = ((long long)(tid < nE ? ef[q] : 0) << 32) | (tid < nR ? ef[kPreK + q] : 0);
+        long long incl = both;
+        for (int o = 1; o < 32; o <<= 1) {
+            const long long y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane_id() >= o) incl += y;
+        }
+        if (lane_id() == 31) Red.v[warp_id()] = incl;
+        __syncthreads();
+        long long off = 0;
+        for (int w = 0; w < warp_id(); ++w) off += Red.v[w];
+        const long long excl = off + incl - both;
+        fe = (int)(excl >> 32);
+        fr = (int)(excl & 0xffffffffll);
+        __syncthreads();
+        if (tid == (int)blockDim.x - 1) Red.u[0] = (unsigned long long)(off + incl);
+        __syncthreads();
+    }
+    const long long tot = (long long)Red.u[0];
+    const int totE = (int)(tot >> 32), totR = (int)(tot & 0xffffffffll);
+    if (!(nx <= kSide && (totR > 0 || TR >= kNoBound))) return false;
+    const int cap = kChunk + 1;
+    if (tid < nR && ef[kPreK + tid] && fr < cap) {
+        R.L_lt[Rl][fr] = es.R_lt[tid];
+        R.L_slot[Rl][fr] = es.R_slot[tid];
+    }
+    if (tid < nE && ef[tid]) {
+        const unsigned long long x = es.E_lt[tid];
+        int r = fe;
+        for (int k = 0; k < nx; ++k) r += xl[k] < x;
+        if (r < cap) {
+            R.L_lt[E][r] = x;
+            R.L_slot[E][r] = es.E_slot[tid];
+            R.E_key[r] = es.E_key[tid];
+            R.E_key_ok[r] = tid < kChunk + 2 ? 1 : 0;
+        }
+    }
+    for (int i = tid; i < nx; i += T) {
+        const unsigned long long x = xl[i];
+        int r = 0;
+        for (int k = 0; k < nx; ++k) r += xl[k] < x;
+        int lo2 = 0, hi2 = nE;
+        while (lo2 < hi2) {
+            const int mid = (lo2 + hi2) >> 1;
+            if (es.E_lt[mid] < x) lo2 = mid + 1;
+            else hi2 = mid;
+        }
+        for (int k = 0; k < lo2; ++k) r += ef[k];
+        if (r < cap) {
+            R.L_lt[E][r] = x;
+            R.L_slot[E][r] = xs[i];
+            R.E_key_ok[r] = 0;  // key loaded by the apply if it is a victim
+        }
+    }
+    if (tid < NL) R.L_n[tid] = tid == E ? min(totE + nx, cap) : tid == Rl ? min(totR, cap) : S.lcnt[tid];
+    if (tid == 0) R.lists_ready = 1;
+    __syncthreads();
+    return true;
+}
+
 // ------------------------------------------------------------------ K5b: replay + apply
 
 __device__ __forceinline__ unsigned int hslot(unsigned int s) { return (s * 2654435761u) >> 23; }  // 9 bits
@@ -1515,6 +1727,7 @@ __device__ void replay_prologue(const DevPool& P, ReplaySmem& R, const AdmSmem& 
         R.n_new_global = 0;
         R.n_reused = 0;
         R.n_ins = 0;
+        R.lists_ready = 0;
         R.ftop = ftop;
         R.res0 = C->resident;
         R.pinned0 = C->pinned;
@@ -1582,7 +1795,7 @@ __device__ void replay_apply(const DevPool& P, const AdmitArgs& a, ReplaySmem& R
     dstamp(P, 0);
 
     // ---- the candidate lists
-    load_lists(P, R, NL, scanned, early);
+    if (!R.lists_ready) load_lists(P, R, NL, scanned, early);
     dstamp(P, 1);
     // Bulk replay (the common case, no serial loop): when the victims are the first n_ev
     // class-E candidates, all inside the dominance prefix (below) and none of them a prompt
@@ -1875,7 +2088,7 @@ __device__ void replay_apply(const DevPool& P, const AdmitArgs& a, ReplaySmem& R
     // victim keys first (a reused victim slot is rewritten below)
     for (int k = tid; k < nv; k += T) {
         const unsigned int v = R.victims[k];
-        R.vkey[k] = P.key[v];
+        R.vkey[k] = (R.lists_ready && R.bulk && R.E_key_ok[k]) ? R.E_key[k] : P.key[v];
         unsigned int h = hslot(v);
         for (int c = 0; c < 512; ++c) {
             if (atomicCAS(&R.vh_key[h], kNoSlot, v) == kNoSlot) break;
@@ -1952,6 +2165,55 @@ __device__ void replay_apply(const DevPool& P, const AdmitArgs& a, ReplaySmem& R
     dstamp(P, 5);
 }
 
+// On-chip overlay of the queued table updates (phase 0): key -> new slot, kSlotTomb (erased) or
+// both (erased, then re-inserted). Open addressing over kOv entries in the (idle) TMA ring.
+constexpr int kOv = 2048;
+constexpr int kOvMax = kOv / 2;
+constexpr unsigned int kOvErase = 0x7FFFFFFFu;  // erased only (slots stay below 2^31 - 16)
+constexpr unsigned int kOvBoth = 0x80000000u;   // slot | kOvBoth: erased, then re-inserted
+constexpr unsigned int kOvSlot = ~kOvBoth;
+
+__device__ __forceinline__ bool ov_both(unsigned int v) {
+    return v != kSlotEmpty && v != kSlotClaim && (v & kOvBoth) != 0u;
+}
+
+// Adds an erase (slot = kOvErase) or an insert of key; order-free: a key seen as both becomes
+// slot | kOvBoth whichever arrives first.
+__device__ __forceinline__ void ov_put(unsigned long long* ovk, unsigned int* ovs, unsigned long long key,
+                                       unsigned int val) {
+    unsigned int h = (unsigned int)(mix64(key) >> 53) & (kOv - 1);
+    for (int c = 0; c < kOv; ++c) {
+        const unsigned int old = atomicCAS(&ovs[h], kSlotEmpty, kSlotClaim);
+        if (old == kSlotEmpty) {
+            ovk[h] = key;
+            __threadfence_block();
+            const unsigned int prev = atomicExch(&ovs[h], val);
+            (void)prev;  // only a claimer writes an unclaimed entry
+            return;
+        }
+        unsigned int cur = old;
+        while (cur == kSlotClaim) cur = *(volatile unsigned int*)&ovs[h];  // a peer is publishing
+        if (*(volatile unsigned long long*)&ovk[h] == key) {
+            if (val == kOvErase) atomicOr(&ovs[h], kOvBoth);  // the insert's slot stays
+            else atomicExch(&ovs[h], val | kOvBoth);
+            return;
+        }
+        h = (h + 1) & (kOv - 1);
+    }
+}
+
+__device__ __forceinline__ unsigned int ov_get(const unsigned long long* ovk, const unsigned int* ovs,
+                                               unsigned long long key) {
+    unsigned int h = (unsigned int)(mix64(key) >> 53) & (kOv - 1);
+    for (int c = 0; c < kOv; ++c) {
+        const unsigned int v = ovs[h];
+        if (v == kSlotEmpty) return kSlotEmpty;
+        if (ovk[h] == key) return v;
+        h = (h + 1) & (kOv - 1);
+    }
+    return kSlotEmpty;
+}
+
 // Applies the block-table updates queued by the previous admission (all threads of one CTA):
 // every erase, then every insert (a key erased and re-admitted in one admission is inserted
 // after its erase; an inserted block is pinned, so no admission erases it again).
@@ -2023,6 +2285,12 @@ __global__ void __launch_bounds__(kThreads + 32, 1) admit_kernel(DevPool P, Admi
     const ScanBufs B = scan_bufs(dsm);
     ReplaySmem& Rp = *reinterpret_cast<ReplaySmem*>(dsm + kOffRing);
     if (tid == 0) P.dbg[blockIdx.x * 16 + 9] = gtimer();  // kernel entry (instrumentation)
+    const int par_prev = (int)((a.seq - 1ull) & 1ull), par_next = (int)(a.seq & 1ull);
+    const bool pre_run = (a.flags & kPrescan) && gridDim.x >= 2;
+    const bool pre_avail = pre_run && (a.flags & kUsePrescan) &&
+                           *(volatile unsigned long long*)&C->pl_seq[par_prev] == a.seq - 1ull &&
+                           *(volatile int*)&C->pl_ok[par_prev] != 0;
+    EarlySmem& es = *reinterpret_cast<EarlySmem*>(dsm + kOffRing + kEarlyOff);
 
     // ---- phase 0 (CTA 0): poll reset, probe, feasibility, dispatch, lookup
     if (blockIdx.x == 0) {
@@ -2045,36 +2313,153 @@ __global__ void __launch_bounds__(kThreads + 32, 1) admit_kernel(DevPool P, Admi
             A.tl = gtimer();
             C->done = 0;
             C->error = 0;
+            es.ok = 0;
+            if (pre_avail) {
+                es.nE = P.pl_n[par_prev * 3 + 0];
+                es.nR = P.pl_n[par_prev * 3 + 1];
+                es.nP = P.pl_n[par_prev * 3 + 2];
+                es.TE = P.pl_T[par_prev * 3 + 0];
+                es.TR = P.pl_T[par_prev * 3 + 1];
+                es.TP = P.pl_T[par_prev * 3 + 2];
+                es.ok = es.nP <= kEarlyP && unpin_total(a, true) <= kXsetMax ? 1 : 0;
+            }
             if (a.flags & kPollReset) {
                 C->step_warmups = 0;
                 C->n_pend = 0;
             }
         }
         __syncthreads();
-        apply_table_queue(P, Red);  // the previous admission's erases / inserts
-        // deferred EngineSim::unpin calls of completed requests (engine.cpp:170-180), in order
-        if (a.n_unpin_ranges > 0) {
-            long long dec = 0;
-#pragma unroll
-            for (int r = 0; r < kMaxUnpinRanges; ++r)
-                if (r < a.n_unpin_ranges)
-                    for (int i = tid; i < a.unpin_n[r]; i += T) {
-                        const unsigned int us = a.unpin_ptr[r][i];
-                        if (us != kNoSlot && atomicSub(&P.refs[us], 1u) == 1u) ++dec;
-                    }
-            dec = block_sum(dec, Red);
-            if (tid == 0) C->pinned -= dec;
-            __syncthreads();
-        }
+        pstamp(P, 0);
         const int n = a.n;
         long long miss_min = n, need = 0;
-        for (int i = tid; i < n; i += T) {
-            const unsigned int s = table_find(P, a.keys[i]);
-            const unsigned int r0 = s == kNoSlot ? 0u : P.refs[s];
-            P.p_slot[i] = s;
-            P.p_refs0[i] = r0;
-            if (s == kNoSlot && i < miss_min) miss_min = i;
-            if (s == kNoSlot || r0 == 0u) ++need;
+        const int ne = C->tq_erase, ni = C->tq_insert;
+        if (ne + ni <= kOvMax) {
+            // The previous admission's table updates run concurrently with this admission's probe:
+            // the probe resolves the queued keys from an on-chip overlay (insert wins: a key erased
+            // and re-admitted is re-inserted), and a table operation on one key never misleads a
+            // find of another (finds skip claimed and erased entries, and an erased entry's key
+            // is cleared first). Erase+insert of one key run in order on one thread.
+            unsigned long long* ovk = reinterpret_cast<unsigned long long*>(dsm + kOffRing);
+            unsigned int* ovs = reinterpret_cast<unsigned int*>(dsm + kOffRing + 8 * kOv);
+            for (int j = tid; j < kOv; j += T) ovs[j] = kSlotEmpty;
+            const bool early = es.ok != 0;
+            if (early) {
+                for (int j = tid; j < kXset; j += T) S.xset[j] = kNoSlot;
+                for (int j = tid; j < kTset; j += T) es.tset[j] = kNoSlot;
+                for (int x = tid; x < a.n_agents; x += T) B.cls[x] = __ldcg(P.cls + x);
+            }
+            __syncthreads();
+            // one round: the overlay of the queued keys, the deferred EngineSim::unpin calls of
+            // completed requests (engine.cpp:170-180) and, feeding a prescan consumer, the set U
+            // of unpinned slots and the early validation of the previous launch's prescan lists
+            long long dec = 0;
+            const int nu = unpin_total(a, false);
+            const int nuv = early ? unpin_total(a, true) : nu;
+            const int nE = early ? es.nE : 0, nR = early ? es.nR : 0, nP = early ? es.nP : 0;
+            const size_t bE = ((size_t)par_prev * 3 + 0) * kPendCap, bR = ((size_t)par_prev * 3 + 1) * kPendCap,
+                         bP = ((size_t)par_prev * 3 + 2) * kPendCap;
+            for (int q = tid; q < ne + ni + nuv + nE + nR + nP; q += T) {
+                if (q < ne) {
+                    ov_put(ovk, ovs, P.tq_key[q], kOvErase);
+                } else if (q < ne + ni) {
+                    ov_put(ovk, ovs, P.tq_key[P.p_cap + (q - ne)], P.tq_slot[q - ne]);
+                } else if (q < ne + ni + nuv) {
+                    const int i = q - ne - ni;
+                    const unsigned int us = unpin_at(a, i);
+                    if (us == kNoSlot) continue;
+                    if (i < nu && atomicSub(&P.refs[us], 1u) == 1u) ++dec;
+                    if (early) xset_insert(S, us);
+                } else if (q < ne + ni + nuv + nE) {
+                    const int j = q - ne - ni - nuv;
+                    const unsigned long long x = P.pl_lt[bE + j];
+                    const unsigned int sl = P.pl_slot[bE + j];
+                    es.E_lt[j] = x;
+                    es.E_slot[j] = sl;
+                    es.E_ok[j] = __ldcg(P.lt + sl) == x ? 1 : 0;
+                    es.E_key[j] = j < kChunk + 2 ? __ldcg(P.key + sl) : 0ull;
+                } else if (q < ne + ni + nuv + nE + nR) {
+                    const int j = q - ne - ni - nuv - nE;
+                    const unsigned long long x = P.pl_lt[bR + j];
+                    const unsigned int sl = P.pl_slot[bR + j];
+                    es.R_lt[j] = x;
+                    es.R_slot[j] = sl;
+                    es.R_ok[j] = __ldcg(P.lt + sl) == x ? 1 : 0;
+                } else {
+                    const int j = q - ne - ni - nuv - nE - nR;
+                    const unsigned long long x = P.pl_lt[bP + j];
+                    const unsigned int sl = P.pl_slot[bP + j];
+                    es.P_lt[j] = x;
+                    es.P_slot[j] = sl;
+                    es.P_agent[j] = P.pl_agent[(size_t)par_prev * kPendCap + j];
+                    es.P_ok[j] = __ldcg(P.lt + sl) == x ? 1 : 0;
+                }
+            }
+            dec = block_sum(dec, Red);  // (its barriers also publish the overlay)
+            if (tid == 0) C->pinned -= dec;
+            pstamp(P, 1);
+            long long reused = 0;
+            const int nxs = early ? kXset : 0;
+            for (int q = tid; q < ne + ni + n + nxs; q += T) {
+                if (q < ne) {
+                    const unsigned long long key = P.tq_key[q];
+                    if (ov_get(ovk, ovs, key) == kOvErase) table_erase(P, key);  // else its insert erases
+                } else if (q < ne + ni) {
+                    const int k = q - ne;
+                    const unsigned long long key = P.tq_key[P.p_cap + k];
+                    if (ov_both(ov_get(ovk, ovs, key))) table_erase(P, key);
+                    reused += table_insert(P, key, P.tq_slot[k]);
+                } else if (q < ne + ni + n) {
+                    const int i = q - ne - ni;
+                    const unsigned long long key = a.keys[i];
+                    const unsigned int ov = ov_get(ovk, ovs, key);
+                    const unsigned int s = ov == kSlotEmpty ? table_find(P, key) : ov == kOvErase ? kNoSlot : (ov & kOvSlot);
+                    const unsigned int r0 = s == kNoSlot ? 0u : P.refs[s];
+                    P.p_slot[i] = s;
+                    P.p_refs0[i] = r0;
+                    if (s == kNoSlot && i < miss_min) miss_min = i;
+                    if (s == kNoSlot || r0 == 0u) ++need;
+                } else {  // U re-read, after every unpin of this launch
+                    const int j = q - ne - ni - n;
+                    const unsigned int us = S.xset[j];
+                    if (us == kNoSlot) continue;
+                    const unsigned long long x = __ldcg(P.lt + us);
+                    es.U_lt[j] = x;
+                    es.U_agent[j] = __ldcg(P.agent + us);
+                    es.U_ok[j] = (x != kFreeTick && __ldcg(P.refs + us) == 0u) ? 1 : 0;
+                }
+            }
+            reused = block_sum(reused, Red);
+            if (tid == 0) {
+                C->tombstones += (long long)ne - reused;
+                C->tq_erase = 0;
+                C->tq_insert = 0;
+            }
+            pstamp(P, 2);
+        } else {
+            if (tid == 0) es.ok = 0;  // (the late prescan consumer re-reads instead)
+            apply_table_queue(P, Red);  // the previous admission's erases / inserts
+            pstamp(P, 1);
+            // deferred EngineSim::unpin calls of completed requests (engine.cpp:170-180), in order
+            if (a.n_unpin_ranges > 0) {
+                long long dec = 0;
+                const int nu = unpin_total(a, false);
+                for (int i = tid; i < nu; i += T) {
+                    const unsigned int us = unpin_at(a, i);
+                    if (us != kNoSlot && atomicSub(&P.refs[us], 1u) == 1u) ++dec;
+                }
+                dec = block_sum(dec, Red);
+                if (tid == 0) C->pinned -= dec;
+                __syncthreads();
+            }
+            pstamp(P, 2);
+            for (int i = tid; i < n; i += T) {
+                const unsigned int s = table_find(P, a.keys[i]);
+                const unsigned int r0 = s == kNoSlot ? 0u : P.refs[s];
+                P.p_slot[i] = s;
+                P.p_refs0[i] = r0;
+                if (s == kNoSlot && i < miss_min) miss_min = i;
+                if (s == kNoSlot || r0 == 0u) ++need;
+            }
         }
         need = block_sum(need, Red);
         miss_min = block_min(miss_min, Red);
@@ -2083,19 +2468,25 @@ __global__ void __launch_bounds__(kThreads + 32, 1) admit_kernel(DevPool P, Admi
             if (tid == 0) A.started = 0;  // try_start_head: wait for in-flight pins to clear
         }
         __syncthreads();
+        pstamp(P, 3);
         if (A.started) {
             if (a.flags & kDispatch) {
                 if (tid == 0) A.tick = A.tick + 1;
                 __syncthreads();
-                observe_dispatch(P, a.prev, a.next, A.tick, a.n_agents, dsm, Red, A);
+                observe_dispatch(P, a.prev, a.next, A.tick, a.n_agents, dsm, Red, A, B.cls);
             }
+            pstamp(P, 4);
             if (a.flags & kLookup) {
                 const int f = (int)miss_min;
                 long long cached = 0;
+                const bool early = es.ok != 0 && f <= kTset / 2;
                 for (int i = tid; i < f; i += T) {
                     cached += a.counts[i];
-                    P.lt[P.p_slot[i]] = A.tick + 1 + (unsigned long long)i;  // EngineSim::touch
+                    const unsigned int ts = P.p_slot[i];
+                    P.lt[ts] = A.tick + 1 + (unsigned long long)i;  // EngineSim::touch
+                    if (early) tset_insert(es.tset, ts);
                 }
+                if (tid == 0 && !early) es.ok = 0;
                 cached = block_sum(cached, Red);
                 if (tid == 0) {
                     A.first_miss = f;
@@ -2118,6 +2509,7 @@ __global__ void __launch_bounds__(kThreads + 32, 1) admit_kernel(DevPool P, Admi
             asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(&C->p0_seq), "l"(a.seq) : "memory");
         }
         stamp(A, 0);
+        pstamp(P, 5);
     }
     if (tid == 0) {
         S.spec = 0;
@@ -2127,11 +2519,6 @@ __global__ void __launch_bounds__(kThreads + 32, 1) admit_kernel(DevPool P, Admi
 
     // ---- prescan: CTAs 1.. stream the pool for the NEXT admission while CTA 0 serves this one
     // from the lists the previous launch's prescan produced (validated, see consume_prescan)
-    const int par_prev = (int)((a.seq - 1ull) & 1ull), par_next = (int)(a.seq & 1ull);
-    const bool pre_run = (a.flags & kPrescan) && gridDim.x >= 2;
-    const bool pre_avail = pre_run && (a.flags & kUsePrescan) &&
-                           *(volatile unsigned long long*)&C->pl_seq[par_prev] == a.seq - 1ull &&
-                           *(volatile int*)&C->pl_ok[par_prev] != 0;
     bool run_loop = true;
     bool pending_rescan = false;  // CTA 0: the last pass must be redone (safe, no hints)
     if (pre_avail) {
@@ -2162,10 +2549,15 @@ __global__ void __launch_bounds__(kThreads + 32, 1) admit_kernel(DevPool P, Admi
             if (A.started && !A.error && A.admit_n > 0) {
                 replay_prologue(P, Rp, A, Red);
                 stamp(A, 1);
+                pstamp(P, 6);
                 const bool need0 = C->resident + Rp.absent > P.cap;
-                const bool ok = need0 ? consume_prescan(P, a, B, S, Red, par_prev) : true;
+                const bool ok = !need0 ? true
+                                : es.ok ? consume_early(P, es, Rp, B, S, Red)
+                                        : consume_prescan(P, a, B, S, Red, par_prev);
                 stamp(A, 3);
+                pstamp(P, 9);
                 if (ok) replay_apply(P, a, Rp, A, NL, need0, Red, true, true);
+                pstamp(P, 10);
                 if (tid == 0) {
                     if (ok && !A.need_full) {
                         A.chunk = 1;
@@ -2416,7 +2808,9 @@ __global__ void __launch_bounds__(kThreads + 32, 1) admit_kernel(DevPool P, Admi
         }
         __syncthreads();
         stamp(A, 5);
+        pstamp(P, 11);
         if (tid == 0) write_status(P, a, A);
+        pstamp(P, 12);
         // per-list scan state for the next launch (a speculative pass starts without a prep)
         if (tid < kMaxLists) {
             P.gbound[tid] = kNoBound;

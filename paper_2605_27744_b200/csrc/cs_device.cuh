@@ -254,10 +254,11 @@ __device__ __forceinline__ int table_insert(const DevPool& P, unsigned long long
         if (s == kSlotEmpty || s == kSlotTomb) {
             unsigned int old = atomicCAS(&P.table[h].slot, s, kSlotClaim);
             if (old == s) {
-                // Concurrent inserters only read slot words (a CLAIM entry is skipped); lookups
-                // run in later phases, ordered by the grid barrier / kernel boundary, so no
-                // fence is needed between the key write and the slot publish.
+                // Concurrent inserters only read slot words (a CLAIM entry is skipped). A find
+                // racing this insert (phase 0) sees CLAIM, or the new slot with the old key
+                // (cleared by the erase, never a probed key), or the new pair.
                 P.table[h].key = key;
+                __threadfence_block();  // the racing finds run in the same CTA (phase 0)
                 atomicExch(&P.table[h].slot, slot);
                 return s == kSlotTomb ? 1 : 0;
             }
@@ -275,6 +276,11 @@ __device__ __forceinline__ void table_erase(const DevPool& P, unsigned long long
         const TableEntry e = P.table[h];
         if (e.slot == kSlotEmpty) return;
         if (e.slot < kSlotClaim && e.key == key) {
+            // clear the key first: a find of another key that races a later reuse of this entry
+            // (phase 0 overlaps the previous admission's table updates with its probe) must
+            // never pair the new slot with the erased key
+            P.table[h].key = ~0ull;
+            __threadfence_block();  // the racing finds run in the same CTA (phase 0)
             P.table[h].slot = kSlotTomb;
             return;
         }

@@ -55,7 +55,7 @@ void cs_pool::create(const cs_pool_cfg& c, long long shard_slots, cs_comm* cm) {
     if (c.window <= 0) throw std::invalid_argument("TransitionLearner: window capacity must be positive");
     if (c.agent_capacity < 1 || c.agent_capacity > csb::kMaxAgents)
         throw CsError(CS_ERR_CAPACITY, "agent_capacity must be in [1, 4096]");
-    if (c.budget_blocks >= (int64_t)0xFFFFFFF0ll) throw CsError(CS_ERR_CAPACITY, "budget exceeds 32-bit slot ids");
+    if (c.budget_blocks >= (int64_t)0x7FFFFFF0ll) throw CsError(CS_ERR_CAPACITY, "budget exceeds 31-bit slot ids");
     const int world = comm ? comm->world : 1;
     if (comm) {
         if (world < 1 || world > csb::kMaxShards) throw std::invalid_argument("sharded pool: 1 <= world <= 8");
@@ -147,7 +147,7 @@ void cs_pool::create(const cs_pool_cfg& c, long long shard_slots, cs_comm* cm) {
     p.gbuf_lt = dmalloc<unsigned long long>((size_t)csb::kMaxLists * p.gcap, "gbuf_lt");
     p.gbuf_slot = dmalloc<unsigned int>((size_t)csb::kMaxLists * p.gcap, "gbuf_slot");
     p.gmin = dmalloc<unsigned long long>((size_t)csb::kMaxLists * lc.grid, "gmin");
-    p.dbg = dmalloc<unsigned long long>((size_t)lc.grid * 16, "dbg");
+    p.dbg = dmalloc<unsigned long long>((size_t)lc.grid * 16 + 64, "dbg");  // + CTA-0 sub-phase stamps
     p.pl_lt = dmalloc<unsigned long long>((size_t)2 * 3 * csb::kPendCap, "pl_lt");
     p.pl_slot = dmalloc<unsigned int>((size_t)2 * 3 * csb::kPendCap, "pl_slot");
     p.pl_agent = dmalloc<unsigned int>((size_t)2 * csb::kPendCap, "pl_agent");
@@ -161,7 +161,7 @@ void cs_pool::create(const cs_pool_cfg& c, long long shard_slots, cs_comm* cm) {
         const unsigned long long h[3] = {csb::kNoBound, csb::kNoBound, csb::kNoBound};
         ck(cudaMemcpy(p.pre_hint, h, sizeof(h), cudaMemcpyHostToDevice), "pre_hint");
     }
-    ck(cudaMemsetAsync(p.dbg, 0, sizeof(unsigned long long) * lc.grid * 16, stream), "memset");
+    ck(cudaMemsetAsync(p.dbg, 0, sizeof(unsigned long long) * (lc.grid * 16 + 64), stream), "memset");
 
     if (comm) {
         p.sh_send2 = dmalloc<csb::ShardLists>(1, "sh_send2");
@@ -796,7 +796,7 @@ int cs_pool_debug(cs_pool_t pool, uint64_t* out, int cap, int* grid) {
     return guard([&] {
         if (!pool || !out) throw std::invalid_argument("cs_pool_debug: null argument");
         pool->sync();
-        const int n = std::min(cap, pool->lc.grid * 16);
+        const int n = std::min(cap, pool->lc.grid * 16 + 64);
         ck(cudaMemcpy(out, pool->P.dbg, 8 * (size_t)n, cudaMemcpyDeviceToHost), "dbg D2H");
         if (grid) *grid = pool->lc.grid;
     });
