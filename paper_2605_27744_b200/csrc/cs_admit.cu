@@ -1101,8 +1101,7 @@ __device__ void finalize_list(const DevPool& P, int l, int NL, int keep, const S
         // few candidates (the common case): every entry's rank directly, one pass (distinct ticks)
         for (int j = tid; j < mf; j += T) {
             const unsigned long long x = src[j];
-            int r = 0;
-            for (int k = 0; k < mf; ++k) r += src[k] < x;
+            const int r = count_below(src, mf, x);
             if (r < kl) {
                 P.fin_lt[(long long)l * (kChunk + 2) + r] = x;
                 P.fin_slot[(long long)l * (kChunk + 2) + r] = srs[j];
@@ -1134,8 +1133,7 @@ __device__ void finalize_list(const DevPool& P, int l, int NL, int keep, const S
     // rank sort of the (at most keep + 1) survivors: distinct ticks, one barrier
     for (int j = tid; j < n; j += T) {
         const unsigned long long x = t_lt[j];
-        int r = 0;
-        for (int k = 0; k < n; ++k) r += t_lt[k] < x;
+        const int r = count_below(t_lt, n, x);
         P.fin_lt[(long long)l * (kChunk + 2) + r] = x;
         P.fin_slot[(long long)l * (kChunk + 2) + r] = t_slot[j];
     }
@@ -1164,12 +1162,13 @@ __device__ __forceinline__ unsigned long long sat_add(unsigned long long a, unsi
     return (a > kNoBound - 1 - b) ? kNoBound : a + b;
 }
 
-// The next acceptance threshold of a list from its sorted kept entries: ~3x the rank reached
-// (the front moves by at most two admissions of victims before the next prescan is consumed).
+// The next acceptance threshold of a list from its sorted kept entries: ~2x the rank reached
+// (the front moves by about one admission of victims before the next prescan reads it). Any
+// threshold is safe: it only sizes the candidate set; completeness is tracked per list.
 __device__ __forceinline__ unsigned long long next_hint(unsigned long long v1, unsigned long long base) {
     if (base >= kNoBound || base < v1) return kNoBound;
     const unsigned long long span = base - v1;
-    return sat_add(v1, sat_add(span, span < (kNoBound >> 2) ? 2 * span : kNoBound));
+    return sat_add(v1, sat_add(span, span));
 }
 
 __device__ void prescan_pass(const DevPool& P, const ScanBufs& B, ScanSmem& S, unsigned char* dsm, int par) {
@@ -1183,9 +1182,6 @@ __device__ void prescan_pass(const DevPool& P, const ScanBufs& B, ScanSmem& S, u
     const long long hi = min(P.cap_scan, lo + per);
     const int ntiles = (int)((hi - lo + TV - 1) / TV);
     unsigned char* ring = dsm + kOffRing;
-    // agent-carrying slots share E's threshold: the E members among them are complete to it,
-    // and the other classes' lists are only needed non-empty (see consume_prescan)
-    const unsigned long long hE = __ldcg(P.pre_hint + 0), hR = __ldcg(P.pre_hint + 1), hP = hE;
     if (tid == 0) {
         S.count = 0;
         S.overflow = 0;
@@ -1197,6 +1193,10 @@ __device__ void prescan_pass(const DevPool& P, const ScanBufs& B, ScanSmem& S, u
         P.dbg[blockIdx.x * 16 + 0] = gtimer();
     }
     __syncthreads();
+    // (the thresholds load while the first tiles are in flight) agent-carrying slots share E's
+    // threshold: the E members among them are complete to it, and the other classes' lists are
+    // only needed non-empty (see consume_prescan)
+    const unsigned long long hE = __ldcg(P.pre_hint + 0), hR = __ldcg(P.pre_hint + 1), hP = hE;
     if (tid >= kThreads) {  // producer warp: one elected thread keeps kRing tiles in flight
         if (lane_id() == 0) {
             for (int t = 0; t < ntiles; ++t) {
@@ -1299,7 +1299,10 @@ __device__ void prescan_barrier(Ctrl* c) {
     __syncthreads();
 }
 
+constexpr int kDirectPre = 1024;  // prescan_finalize ranks up to this many candidates directly
+
 // List l (0 = E, 1 = R) of the prescan: its kPreK oldest, sorted, and the completeness bound.
+// The raw candidates (a few hundred with a good threshold) are staged on chip first.
 __device__ void prescan_finalize(const DevPool& P, const ScanBufs& B, SelectSmem& Sel, int par, int l,
                                  unsigned long long h) {
     Ctrl* C = P.ctrl;
@@ -1307,26 +1310,69 @@ __device__ void prescan_finalize(const DevPool& P, const ScanBufs& B, SelectSmem
     const int m = min(*(volatile int*)&C->pre_cnt[par][l], (int)P.pre_gcap);
     const unsigned long long* g = P.pre_buf_lt + l * P.pre_gcap;
     const unsigned int* gs = P.pre_buf_slot + l * P.pre_gcap;
+    const bool local = m <= kStage;
+    if (tid == 0) {
+        P.dbg[blockIdx.x * 16 + 6] = (unsigned long long)m;
+        P.dbg[blockIdx.x * 16 + 7] = gtimer();
+    }
+    if (local) {
+        for (int j = tid; j < m; j += T) {
+            B.st_lt[j] = __ldcg(g + j);
+            B.st_slot[j] = __ldcg(gs + j);
+        }
+        __syncthreads();
+    }
+    if (tid == 0) P.dbg[blockIdx.x * 16 + 8] = gtimer();
+    const unsigned long long* src = local ? B.st_lt : g;
+    const unsigned int* srs = local ? B.st_slot : gs;
+    const size_t base = ((size_t)par * 3 + l) * kPendCap;
+    if (local && m <= kDirectPre) {
+        // few candidates (the usual case): every entry's rank in one pass, no radix rounds
+        if (tid == 0) Sel.prefix = kNoBound;
+        __syncthreads();
+        unsigned long long vk = kNoBound, v1 = kNoBound;
+        for (int j = tid; j < m; j += T) {
+            const unsigned long long x = src[j];
+            const int r = count_below(src, m, x);
+            if (r < kPreK) {
+                P.pl_lt[base + r] = x;
+                P.pl_slot[base + r] = srs[j];
+            }
+            if (r == kPreK - 1) vk = x;
+            if (r == 0) v1 = x;
+        }
+        if (vk != kNoBound) Sel.prefix = vk;
+        if (v1 != kNoBound) Sel.hmax = v1;
+        __syncthreads();
+        if (tid == 0) {
+            const int n = min(m, kPreK);
+            const unsigned long long Tl = m > kPreK ? Sel.prefix : h;
+            const int bad = *(volatile int*)&C->pre_bad[par];
+            P.pl_n[par * 3 + l] = n;
+            P.pl_T[par * 3 + l] = Tl;
+            P.pre_hint[l] = n == 0 ? kNoBound : bad ? Tl : next_hint(Sel.hmax, Tl);
+        }
+        __syncthreads();
+        return;
+    }
     unsigned long long v = kNoBound;
-    if (m > kPreK) v = block_kth(g, nullptr, 0, m, kPreK, Sel);
+    if (m > kPreK) v = block_kth(src, nullptr, 0, m, kPreK, Sel);
     if (tid == 0) Sel.tmp = 0;
     __syncthreads();
     for (int j = tid; j < m; j += T) {
-        const unsigned long long x = __ldcg(g + j);
+        const unsigned long long x = src[j];
         if (m <= kPreK || x <= v) {
             const int p = atomicAdd(&Sel.tmp, 1);
             B.sd_lt[p] = x;
-            B.sd_slot[p] = __ldcg(gs + j);
+            B.sd_slot[p] = srs[j];
         }
     }
     __syncthreads();
     const int n = Sel.tmp;  // distinct ticks: exactly min(m, kPreK)
-    const size_t base = ((size_t)par * 3 + l) * kPendCap;
     unsigned long long v1 = kNoBound;
     for (int j = tid; j < n; j += T) {
         const unsigned long long x = B.sd_lt[j];
-        int r = 0;
-        for (int k = 0; k < n; ++k) r += B.sd_lt[k] < x;
+        const int r = count_below(B.sd_lt, n, x);
         P.pl_lt[base + r] = x;
         P.pl_slot[base + r] = B.sd_slot[j];
         if (r == 0) v1 = x;
@@ -1344,41 +1390,104 @@ __device__ void prescan_finalize(const DevPool& P, const ScanBufs& B, SelectSmem
     __syncthreads();
 }
 
-// After the barrier: CTA 1 finalizes E and the pending list, CTA 2 (CTA 1 if alone) R; the last
-// finalizer publishes the lists for the next launch.
+// After every prescan CTA's writeout, CTA 1 alone finalizes the prescan (E and R ranked in one
+// on-chip pass) and publishes it for the next launch; the other prescan CTAs only count their
+// arrival. Thread 0's tail is a short chain: one round of counter loads, then plain stores.
 __device__ void prescan_finish(const DevPool& P, const AdmitArgs& a, const ScanBufs& B, SelectSmem& Sel, int par,
                                unsigned long long hE, unsigned long long hR, unsigned long long hP) {
+    __shared__ int cnt[4];                  // candidates of E, R, pending; overflow flag
     Ctrl* C = P.ctrl;
-    const int nfin = gridDim.x >= 3 ? 2 : 1;
-    const int me = (int)blockIdx.x - 1;
-    if (me >= nfin) return;
-    if (me == 0) {
-        prescan_finalize(P, B, Sel, par, 0, hE);
-        if (threadIdx.x == 0) {
-            const int np = *(volatile int*)&C->pre_cnt[par][2];
-            if (np > kPendCap) atomicExch(&C->pre_bad[par], 1);
-            P.pl_n[par * 3 + 2] = min(np, kPendCap);
-            P.pl_T[par * 3 + 2] = hP;
-            if (np > kPendCap || *(volatile int*)&C->pre_bad[par]) C->pre_badcnt += 1;
-        }
-    }
-    if (me == nfin - 1) prescan_finalize(P, B, Sel, par, 1, hR);
-    if (threadIdx.x == 0) {
+    const int tid = threadIdx.x, T = blockDim.x;
+    __syncthreads();
+    if (tid == 0) {
         __threadfence();
-        if (atomicAdd(&C->pre_fin[par], 1u) == (unsigned int)nfin - 1) {
-            __threadfence();
-            C->pl_ok[par] = *(volatile int*)&C->pre_bad[par] ? 0 : 1;
-            C->pre_cnt[par][0] = C->pre_cnt[par][1] = C->pre_cnt[par][2] = 0;
-            C->pre_bad[par] = 0;
-            C->pre_fin[par] = 0u;
-            __threadfence();
-            asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(&C->pl_seq[par]), "l"(a.seq) : "memory");
+        atomicAdd(&C->pre_arrive[par], 1u);  // this CTA's candidates are in global memory
+    }
+    if (blockIdx.x != 1) return;
+    if (tid == 0) {
+        unsigned long long spins = 0;
+        while (ld_acquire(&C->pre_arrive[par]) < (unsigned int)(gridDim.x - 1)) {
+            if (++spins > 65536) __nanosleep(32);
+            if (spins > (1ull << 28)) __trap();
         }
+        __threadfence();
+        cnt[0] = min(*(volatile int*)&C->pre_cnt[par][0], (int)P.pre_gcap);
+        cnt[1] = min(*(volatile int*)&C->pre_cnt[par][1], (int)P.pre_gcap);
+        cnt[2] = *(volatile int*)&C->pre_cnt[par][2];
+        cnt[3] = *(volatile int*)&C->pre_bad[par];
+        P.dbg[blockIdx.x * 16 + 6] = gtimer();
+    }
+    __syncthreads();
+    const int mE = cnt[0], mR = cnt[1], mP = cnt[2];
+    const bool bad = cnt[3] != 0 || mP > kPendCap;
+    const unsigned long long h[2] = {hE, hR};
+    const int oR = ((mE + 1) & ~1);  // R staged 16-B aligned after E
+    if (oR + mR <= kStage && mE <= kDirectPre && mR <= kDirectPre) {
+        // two warp groups (named barriers 1 and 2): group 0 finalizes E, group 1 R, at once
+        __shared__ SelectSmem Sg[2];
+        __shared__ int ng[2];
+        const int nw = (int)blockDim.x >> 5, w0 = (nw + 1) >> 1;
+        const int grp = warp_id() < w0 ? 0 : 1;
+        const int gn = (grp == 0 ? w0 : nw - w0) * 32, gt = tid - (grp == 0 ? 0 : w0 * 32);
+        const int m = grp ? mR : mE, off = grp ? oR : 0;
+        unsigned long long* vl = B.st_lt + off;
+        unsigned int* vs = B.st_slot + off;
+        unsigned long long* tl = B.sd_lt + (grp ? kPreK + 2 : 0);  // selected, kPreK per group
+        unsigned int* ts = B.sd_slot + (grp ? kPreK + 2 : 0);
+        for (int j = gt; j < m; j += gn) {
+            vl[j] = __ldcg(P.pre_buf_lt + grp * P.pre_gcap + j);
+            vs[j] = __ldcg(P.pre_buf_slot + grp * P.pre_gcap + j);
+        }
+        if (gt == 0) ng[grp] = 0;
+        group_sync(1 + grp, gn);
+        if (tid == 0) P.dbg[blockIdx.x * 16 + 7] = gtimer();
+        const unsigned long long v = m > kPreK ? group_kth(vl, m, kPreK, Sg[grp], gt, gn, 1 + grp) : kNoBound;
+        for (int j = gt; j < m; j += gn) {
+            const unsigned long long x = vl[j];
+            if (m <= kPreK || x <= v) {
+                const int p = atomicAdd(&ng[grp], 1);
+                tl[p] = x;
+                ts[p] = vs[j];
+            }
+        }
+        group_sync(1 + grp, gn);
+        if (tid == 0) P.dbg[blockIdx.x * 16 + 8] = gtimer();
+        const int n = ng[grp];  // min(m, kPreK) (distinct ticks)
+        const size_t base = ((size_t)par * 3 + grp) * kPendCap;
+        for (int j = gt; j < n; j += gn) {
+            const unsigned long long x = tl[j];
+            const int r = count_below(tl, n, x);
+            P.pl_lt[base + r] = x;
+            P.pl_slot[base + r] = ts[j];
+            if (r == 0) Sg[grp].hmax = x;
+        }
+        group_sync(1 + grp, gn);
+        if (gt == 0) {
+            const unsigned long long Tl = m > kPreK ? v : h[grp];
+            P.pl_n[par * 3 + grp] = n;
+            P.pl_T[par * 3 + grp] = Tl;
+            P.pre_hint[grp] = n == 0 ? kNoBound : bad ? Tl : next_hint(Sg[grp].hmax, Tl);
+        }
+        __syncthreads();
+    } else {  // many candidates (a loose threshold): radix select per list
+        prescan_finalize(P, B, Sel, par, 0, hE);
+        prescan_finalize(P, B, Sel, par, 1, hR);
+    }
+    if (tid == 0) {
+        P.pl_n[par * 3 + 2] = min(mP, kPendCap);
+        P.pl_T[par * 3 + 2] = hP;
+        if (bad) atomicAdd(reinterpret_cast<unsigned long long*>(&C->pre_badcnt), 1ull);
+        C->pl_ok[par] = bad ? 0 : 1;
+        C->pre_cnt[par][0] = C->pre_cnt[par][1] = C->pre_cnt[par][2] = 0;
+        C->pre_bad[par] = 0;
+        C->pre_arrive[par] = 0u;  // every arrival happened before the wait above ended
+        __threadfence();
+        asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(&C->pl_seq[par]), "l"(a.seq) : "memory");
     }
 }
 
 // Acceptance thresholds for the next prescan from a regular select's lists (CTA 0, thread 0):
-// the keep oldest of E and R extrapolated to ~3 kPreK ranks. Agent-carrying slots are kept whole.
+// the keep oldest of E and R extrapolated to ~2 kPreK ranks. Agent-carrying slots are kept whole.
 __device__ void hints_from_fin(const DevPool& P, int NL, int keep) {
     const int E = P.e_max, Rl = NL - 1;
     const int lists[2] = {E, Rl};
@@ -1391,7 +1500,7 @@ __device__ void hints_from_fin(const DevPool& P, int NL, int keep) {
             const unsigned long long v1 = P.fin_lt[(long long)l * (kChunk + 2)];
             const unsigned long long vk = P.fin_lt[(long long)l * (kChunk + 2) + n - 1];
             const unsigned long long span = vk - v1;
-            const unsigned long long mult = (unsigned long long)((3 * kPreK + n - 1) / n);
+            const unsigned long long mult = (unsigned long long)((2 * kPreK + n - 1) / n);
             h = span > (kNoBound - v1) / (mult + 1) ? kNoBound : v1 + span * mult;
         }
         P.pre_hint[q] = h;
@@ -1516,8 +1625,7 @@ __device__ bool consume_prescan(const DevPool& P, const AdmitArgs& a, const Scan
     // E: merge of the valid agentless entries (sorted) with the extras (unsorted, few)
     if (tid < nE && B.st_list[tid]) {
         const unsigned long long x = B.st_lt[tid];
-        int r = fe;
-        for (int k = 0; k < nx; ++k) r += xl[k] < x;
+        const int r = fe + count_below(xl, nx, x);
         if (r < capE) {
             P.fin_lt[(long long)E * (kChunk + 2) + r] = x;
             P.fin_slot[(long long)E * (kChunk + 2) + r] = B.st_slot[tid];
@@ -1525,8 +1633,7 @@ __device__ bool consume_prescan(const DevPool& P, const AdmitArgs& a, const Scan
     }
     for (int i = tid; i < nx; i += T) {
         const unsigned long long x = xl[i];
-        int r = 0;
-        for (int k = 0; k < nx; ++k) r += xl[k] < x;
+        int r = count_below(xl, nx, x);
         int lo2 = 0, hi2 = nE;  // valid agentless entries below x: binary search + prefix flag count
         while (lo2 < hi2) {
             const int mid = (lo2 + hi2) >> 1;
@@ -1654,8 +1761,7 @@ __device__ bool consume_early(const DevPool& P, const EarlySmem& es, ReplaySmem&
     }
     if (tid < nE && ef[tid]) {
         const unsigned long long x = es.E_lt[tid];
-        int r = fe;
-        for (int k = 0; k < nx; ++k) r += xl[k] < x;
+        const int r = fe + count_below(xl, nx, x);
         if (r < cap) {
             R.L_lt[E][r] = x;
             R.L_slot[E][r] = es.E_slot[tid];
@@ -1665,8 +1771,7 @@ __device__ bool consume_early(const DevPool& P, const EarlySmem& es, ReplaySmem&
     }
     for (int i = tid; i < nx; i += T) {
         const unsigned long long x = xl[i];
-        int r = 0;
-        for (int k = 0; k < nx; ++k) r += xl[k] < x;
+        int r = count_below(xl, nx, x);
         int lo2 = 0, hi2 = nE;
         while (lo2 < hi2) {
             const int mid = (lo2 + hi2) >> 1;
@@ -2525,14 +2630,16 @@ __global__ void __launch_bounds__(kThreads + 32, 1) admit_kernel(DevPool P, Admi
         if (blockIdx.x != 0) {
             const unsigned long long hE = __ldcg(P.pre_hint + 0), hR = __ldcg(P.pre_hint + 1), hP = hE;
             prescan_pass(P, B, S, dsm, par_next);
-            prescan_barrier(C);
+            if (tid == 0) P.dbg[blockIdx.x * 16 + 2] = gtimer();
             prescan_finish(P, a, B, Sel, par_next, hE, hR, hP);
             if (tid == 0) {
+                P.dbg[blockIdx.x * 16 + 4] = gtimer();
                 unsigned long long spins = 0;
                 while (ld_acquire_u64(&C->verdict_seq) != a.seq) {
                     if (++spins > 4096) __nanosleep(128);
                     if (spins > (1ull << 28)) __trap();
                 }
+                P.dbg[blockIdx.x * 16 + 5] = gtimer();
             }
             __syncthreads();
             run_loop = *(volatile int*)&C->verdict == 2;
@@ -2782,7 +2889,6 @@ __global__ void __launch_bounds__(kThreads + 32, 1) admit_kernel(DevPool P, Admi
     if (pre_run && !pre_avail && blockIdx.x != 0) {
         const unsigned long long hE = __ldcg(P.pre_hint + 0), hR = __ldcg(P.pre_hint + 1), hP = hE;
         prescan_pass(P, B, S, dsm, par_next);
-        prescan_barrier(C);
         prescan_finish(P, a, B, Sel, par_next, hE, hR, hP);
         return;
     }

@@ -50,6 +50,25 @@ __device__ __forceinline__ long long block_min(long long x, RedSmem& R) {
     return r;
 }
 
+// Number of v[0, m) below x. v lives in shared memory, 16-byte aligned: 128-bit loads, four
+// independent counters and an unrolled body keep many loads in flight (a plain loop is bound by
+// the shared-memory latency at one CTA per SM).
+__device__ __forceinline__ int count_below(const unsigned long long* v, int m, unsigned long long x) {
+    int r0 = 0, r1 = 0, r2 = 0, r3 = 0;
+    int k = 0;
+#pragma unroll 4
+    for (; k + 4 <= m; k += 4) {
+        const ulonglong2 a = *reinterpret_cast<const ulonglong2*>(v + k);
+        const ulonglong2 b = *reinterpret_cast<const ulonglong2*>(v + k + 2);
+        r0 += a.x < x;
+        r1 += a.y < x;
+        r2 += b.x < x;
+        r3 += b.y < x;
+    }
+    for (; k < m; ++k) r0 += v[k] < x;
+    return r0 + r1 + r2 + r3;
+}
+
 struct SelectSmem {
     unsigned int hist[256];
     unsigned long long acc_or, acc_and;
@@ -140,6 +159,93 @@ __device__ inline unsigned long long block_kth(const unsigned long long* v, cons
         shift -= 8;
     }
     __syncthreads();
+    return prefix;
+}
+
+// Barrier of a warp group of `n` threads (a multiple of 32) on named barrier `id` (1..15).
+__device__ __forceinline__ void group_sync(int id, int n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+// block_kth for a warp group (threads gt = 0..gn-1 of the group, named barrier bar), so two
+// groups of one CTA select from two lists at once. v in shared memory; all values distinct.
+__device__ inline unsigned long long group_kth(const unsigned long long* v, int m, int k, SelectSmem& S, int gt,
+                                               int gn, int bar) {
+    if (gt == 0) {
+        S.acc_or = 0ull;
+        S.acc_and = ~0ull;
+    }
+    group_sync(bar, gn);
+    unsigned long long o = 0ull, a = ~0ull;
+    for (int j = gt; j < m; j += gn) {
+        const unsigned long long x = v[j];
+        o |= x;
+        a &= x;
+    }
+    for (int s = 16; s; s >>= 1) {
+        o |= __shfl_xor_sync(0xffffffffu, o, s);
+        a &= __shfl_xor_sync(0xffffffffu, a, s);
+    }
+    if ((gt & 31) == 0) {
+        atomicOr(&S.acc_or, o);
+        atomicAnd(&S.acc_and, a);
+    }
+    group_sync(bar, gn);
+    const unsigned long long diff = S.acc_or ^ S.acc_and;
+    const unsigned long long same = S.acc_and;
+    if (diff == 0ull) {
+        group_sync(bar, gn);
+        return same;
+    }
+    const int hb = 63 - __clzll((long long)diff);
+    int shift = (hb / 8) * 8;
+    unsigned long long hmask = (shift + 8 >= 64) ? 0ull : ~((1ull << (shift + 8)) - 1ull);
+    unsigned long long prefix = same & hmask;
+    int kk = k;
+    for (;;) {
+        for (int b = gt; b < 256; b += gn) S.hist[b] = 0u;
+        group_sync(bar, gn);
+        for (int j = gt; j < m; j += gn) {
+            const unsigned long long x = v[j];
+            if ((x & hmask) == prefix) atomicAdd(&S.hist[(x >> shift) & 255ull], 1u);
+        }
+        group_sync(bar, gn);
+        if (gt < 32) {
+            const int ln = gt;
+            unsigned int c[8];
+            unsigned int sum = 0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                c[q] = S.hist[ln * 8 + q];
+                sum += c[q];
+            }
+            unsigned int inc = sum;
+            for (int d = 1; d < 32; d <<= 1) {
+                const unsigned int t = __shfl_up_sync(0xffffffffu, inc, d);
+                if (ln >= d) inc += t;
+            }
+            const unsigned int exc = inc - sum;
+            if (exc < (unsigned)kk && (unsigned)kk <= inc) {
+                unsigned int cum = exc;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    if (cum + c[q] >= (unsigned)kk) {
+                        S.prefix = prefix | ((unsigned long long)(ln * 8 + q) << shift);
+                        S.k = kk - (int)cum;
+                        break;
+                    }
+                    cum += c[q];
+                }
+            }
+        }
+        group_sync(bar, gn);
+        prefix = S.prefix;
+        kk = S.k;
+        hmask |= (255ull << shift);
+        if (shift == 0) break;
+        shift -= 8;
+    }
+    group_sync(bar, gn);
     return prefix;
 }
 

@@ -85,6 +85,7 @@ struct Ctrl {
     int pre_cnt[2][3];                  // raw candidates written per list (E, R, pending)
     int pre_bad[2];                     // staging / buffer overflow: the prescan is unusable
     unsigned int pre_fin[2];            // prescan lists finalized
+    unsigned int pre_arrive[2];         // prescan CTAs whose candidates are written
     unsigned long long pl_seq[2];       // AdmitArgs::seq of the launch that produced the lists
     int pl_ok[2];
     unsigned long long verdict_seq;     // CTA 0 -> prescan CTAs: this launch's verdict is out
@@ -94,7 +95,7 @@ struct Ctrl {
 
 // prescan list lengths: E (agentless unpinned) and R (resident) keep the kPreK oldest; the
 // agent-carrying unpinned slots (classified by the consumer, after its BFS) are kept whole
-constexpr int kPreK = 256;
+constexpr int kPreK = 192;  // >= kChunk + 1 list entries plus the front the previous admission evicts
 constexpr int kPendCap = 4096;
 
 // ---------------------------------------------------------------- hash-sharded pool

@@ -19,6 +19,7 @@ spec, seed = bench.rank_workload(40000, pool, 0)
 eng = bench.build_engine(W, spec, pool, 0, False, seed)
 eng.run_timed(100)
 rows = []
+fin = []
 ends = []
 for it in range(40):
     eng.run_timed(1)
@@ -32,10 +33,16 @@ for it in range(40):
     st = d[16 * g:16 * g + 16]
     rows.append((st - ent) / 1e3)
     per = d[:16 * g].reshape(g, 16)
-    ends.append(((per[1:, 1] - ent) / 1e3).max())
+    fin.append([(per[1, c] - ent) / 1e3 for c in (6, 7, 8, 4)])
+    ends.append([((per[1:, c] - ent) / 1e3).max() for c in (0, 1, 2, 3, 4, 5)] + [((per[1:3, 4] - ent) / 1e3).max()])
 r = np.median(np.array(rows), axis=0)
 for k in [0, 1, 2, 3, 13, 14, 4, 5, 6, 7, 8, 9, 10, 11, 12]:
     print(f"{NAMES[k]:>14}: {r[k]:8.2f} us")
-print(f"{'prescan end':>14}: {np.median(ends):8.2f} us (max over CTAs of stream end)")
+e = np.median(np.array(ends), axis=0)
+print("prescan CTAs (max over CTAs): start %.2f stream end %.2f writeout %.2f barrier %.2f finish %.2f (finalizers %.2f) verdict %.2f us"
+      % (e[0], e[1], e[2], e[3], e[4], e[6], e[5]))
 res = eng.result()
 print("admit_ms per launch", res["admit_ms"] / max(res["admissions"], 1) * 1e3)
+
+f = np.median(np.array(fin), axis=0)
+print("finalizer CTA 1: arrivals seen %.2f staged %.2f ranked %.2f published %.2f us" % tuple(f))
