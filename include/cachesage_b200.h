@@ -76,6 +76,13 @@ int cs_hash_prompts(cs_pool_t pool, const uint32_t* tokens, const int64_t* tok_o
                     int32_t* counts_out, uint64_t* agent_ids_out);
 int64_t cs_blocks_for(const int64_t* tok_off, int n_prompts, int block_size, int64_t* blk_off);
 
+/* chain_hash (hashing.cpp:26-35) of n token spans (tok_off[n+1]); has_parent[i] != 0 chains
+ * from parents[i], else from the root (both may be NULL). The reference's Python chain_hash. */
+int cs_chain_hash(const uint64_t* parents, const uint8_t* has_parent, const uint32_t* tokens, const int64_t* tok_off,
+                  int n, uint64_t* out);
+/* derive_agent_identity (cachesage_policy.cpp:9-31) of n block-key lists (key_off[n+1]). */
+int cs_derive_agent_identity(const uint64_t* keys, const int64_t* key_off, int n, int skip, int take, uint64_t* out);
+
 /* K2: EngineSim::lookup (engine.cpp:127-139): longest resident prefix; each hit is touched
  * with ticks tick_base+1, tick_base+2, ... The caller's clock advances by *first_miss. */
 int cs_lookup(cs_pool_t pool, const uint64_t* keys, const int32_t* counts, int n, uint64_t tick_base,
@@ -212,6 +219,32 @@ int64_t cs_engine_evictions(cs_engine_t e, uint64_t* keys, int64_t cap);
 /* drained warmups: step index, target agent id, issued tick */
 int64_t cs_engine_warmups(cs_engine_t e, int64_t* step, uint64_t* target, uint64_t* tick, int64_t cap);
 cs_pool_t cs_engine_pool(cs_engine_t e);
+
+/* ------------------------------------------------------------------ standalone learner
+ *
+ * The reference's TransitionLearner (transition_learner.hpp:19-60; Python binding
+ * py_module.cpp:103-123) on the device: dense counts over agent indices in first-seen order,
+ * the window as an index-pair ring. record = K3 (warp-aggregated atomics), rebuild = K3b,
+ * argmax = K6, and the horizon-k survival oracle (a21). */
+typedef struct cs_learner* cs_learner_t;
+int cs_learner_create(int64_t window, int agent_capacity, int device, cs_learner_t* out);
+int cs_learner_destroy(cs_learner_t learner);
+/* TransitionLearner::record (transition_learner.cpp:22-51) for n pairs, in order. */
+int cs_learner_record(cs_learner_t learner, const uint64_t* prev, const uint64_t* next, int64_t n);
+/* TransitionLearner::prob / row_total (transition_learner.cpp:53-71). */
+int cs_learner_prob(cs_learner_t learner, uint64_t a, uint64_t b, double* p);
+int cs_learner_row_total(cs_learner_t learner, uint64_t a, uint64_t* total);
+/* TransitionLearner::agents (first-seen order); returns the count. */
+int cs_learner_agents(cs_learner_t learner, uint64_t* ids, int cap);
+/* TransitionLearner::state_bytes (transition_learner.cpp:98-106). */
+int cs_learner_state_bytes(cs_learner_t learner, uint64_t* bytes);
+/* rebuild_reachability (reachability.cpp:39-81): hop of every known agent (agents() order). */
+int cs_learner_rebuild(cs_learner_t learner, uint64_t current, double tau, int e_max, int* hops, int cap);
+/* TransitionLearner::argmax_row (transition_learner.cpp:79-96); *found = 0 for an unseen row. */
+int cs_learner_argmax(cs_learner_t learner, uint64_t a, uint64_t* best, double* p, int* found);
+/* oracle::exact_survival_prob (survival_oracle.cpp:9-62): P(the walk from current visits
+ * target within k steps), same fp64 operation order. Alphabet <= 64, 0 <= k <= 32. */
+int cs_exact_survival_prob(cs_learner_t learner, uint64_t target, int k, uint64_t current, double* out);
 
 /* ------------------------------------------------------------------ hash-sharded pool
  *

@@ -327,3 +327,130 @@ class Engine:
         s = np.zeros(max(n, 1), np.float64)
         lib().cso_engine_scores(self.h, _p(k), _p(s), n)
         return k[:n], s[:n]
+
+
+# ---------------------------------------------------------------------------------------------
+# TransitionLearner / rebuild_reachability / exact_survival_prob, restated in Python for small
+# alphabets (test-scale, like the reference's own oracle). Paths relative to /root/reference/proj.
+
+class Learner:
+    """TransitionLearner (transition_learner.cpp:10-96): alphabet in first-seen order, sparse
+    counts and row totals over a sliding window of pairs."""
+
+    def __init__(self, window=1024):
+        if window <= 0:
+            raise ValueError("TransitionLearner: window capacity must be positive")
+        self.cap = window
+        self.alphabet = []
+        self._seen = set()
+        self.window = []
+        self.counts = {}  # a -> {b: n}
+        self.totals = {}
+
+    def note_agent(self, a):  # transition_learner.cpp:16-20
+        if a not in self._seen:
+            self._seen.add(a)
+            self.alphabet.append(a)
+
+    def record(self, a, b):  # transition_learner.cpp:22-51
+        self.note_agent(a)
+        self.note_agent(b)
+        self.window.append((a, b))
+        row = self.counts.setdefault(a, {})
+        row[b] = row.get(b, 0) + 1
+        self.totals[a] = self.totals.get(a, 0) + 1
+        if len(self.window) > self.cap:
+            oa, ob = self.window.pop(0)
+            r = self.counts[oa]
+            r[ob] -= 1
+            if r[ob] == 0:
+                del r[ob]
+            if not r:
+                del self.counts[oa]
+            self.totals[oa] -= 1
+            if self.totals[oa] == 0:
+                del self.totals[oa]
+
+    def prob(self, a, b):  # transition_learner.cpp:53-67
+        t = self.totals.get(a, 0)
+        c = self.counts.get(a, {}).get(b, 0)
+        return 0.0 if t == 0 or c == 0 else float(c) / float(t)
+
+    def row_total(self, a):
+        return self.totals.get(a, 0)
+
+    def argmax_row(self, a):  # transition_learner.cpp:79-96 (ties -> smaller id)
+        r = self.counts.get(a)
+        t = self.totals.get(a, 0)
+        if not r or t == 0:
+            return None
+        best, bc = None, 0
+        for b, c in r.items():
+            if best is None or c > bc or (c == bc and b < best):
+                best, bc = b, c
+        return best, float(bc) / float(t)
+
+    def state_bytes(self):  # transition_learner.cpp:98-106
+        nz = sum(len(r) for r in self.counts.values())
+        return len(self.window) * 4 + nz * 12 + len(self.totals) * 10 + len(self.alphabet) * 8 + 8
+
+
+def rebuild_reachability(learner, current, tau, e_max):
+    """reachability.cpp:39-81: hop per agent (e_max = unreachable)."""
+    if e_max <= 0:
+        raise ValueError("rebuild_reachability: e_max must be positive")
+    hops = {a: e_max for a in learner.alphabet}
+    hops[current] = 0
+    frontier = [current]
+    while frontier:
+        a = frontier.pop(0)
+        d = hops[a]
+        if d + 1 >= e_max:
+            continue
+        row = learner.counts.get(a)
+        if not row:
+            continue
+        total = float(learner.totals[a])
+        for b, c in row.items():
+            if float(c) / total < tau:
+                continue
+            if hops.get(b, e_max) > d + 1:
+                hops[b] = d + 1
+                frontier.append(b)
+    return hops
+
+
+def exact_survival_prob(target, k, learner, current):
+    """survival_oracle.cpp:9-62, fp64 operations in the reference's order."""
+    agents = learner.alphabet
+    if len(agents) > 64:
+        raise ValueError("exact_survival_prob: alphabet too large (test-scale <= 64)")
+    if k > 32:
+        raise ValueError("exact_survival_prob: horizon too deep (test-scale <= 32)")
+    if k < 0:
+        raise ValueError("exact_survival_prob: negative horizon")
+    if target == current:
+        return 1.0
+    index = {a: i for i, a in enumerate(agents)}
+    if target not in index or current not in index:
+        return 0.0
+    n = len(agents)
+    ti = index[target]
+    dist = [0.0] * n
+    dist[index[current]] = 1.0
+    absorbed = 0.0
+    for _ in range(k):
+        nxt = [0.0] * n
+        for i in range(n):
+            if dist[i] == 0.0:
+                continue
+            row = learner.counts.get(agents[i])
+            if not row:
+                continue
+            total = float(learner.totals[agents[i]])
+            for b, c in row.items():
+                nxt[index[b]] += dist[i] * float(c) / total
+        absorbed += nxt[ti]
+        nxt[ti] = 0.0
+        dist = nxt
+    return absorbed

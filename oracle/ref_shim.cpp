@@ -460,4 +460,39 @@ double ref_evict_bench(long N, int n_agents, long n_agent_blocks, long k_warm, l
     }
 }
 
+// The reference TransitionLearner after recording n pairs with window W, as the device learner
+// exposes it (cs_learner_*): the alphabet (first-seen order, <= cap), P(a,b) over it, row
+// totals, state_bytes, argmax_row per row, rebuild_reachability hops from `current`, and
+// exact_survival_prob(agent, k, current) per agent (k < 0: skipped). Returns the alphabet size.
+long ref_learner_eval(long n, const unsigned long long* a, const unsigned long long* b, long window, long cap,
+                      unsigned long long current, double tau, int e_max, int k, unsigned long long* agents,
+                      double* prob, unsigned long long* totals, unsigned long long* state_bytes,
+                      unsigned long long* amax_id, double* amax_p, int* amax_found, int* hops, double* surv) {
+    try {
+        TransitionLearner l((std::size_t)window);
+        for (long i = 0; i < n; ++i) l.record(AgentId{a[i]}, AgentId{b[i]});
+        const auto& al = l.agents();
+        const long A = (long)al.size();
+        if (A > cap) return -2;
+        for (long i = 0; i < A; ++i) {
+            agents[i] = al[i].value;
+            totals[i] = l.row_total(al[i]);
+            for (long j = 0; j < A; ++j) prob[i * A + j] = l.prob(al[i], al[j]);
+            const auto am = l.argmax_row(al[i]);
+            amax_found[i] = am ? 1 : 0;
+            amax_id[i] = am ? am->first.value : 0ull;
+            amax_p[i] = am ? am->second : 0.0;
+        }
+        *state_bytes = l.state_bytes();
+        const ReachabilityState r = rebuild_reachability(l, AgentId{current}, tau, e_max);
+        for (long i = 0; i < A; ++i) hops[i] = r.hop(al[i]);
+        if (k >= 0)
+            for (long i = 0; i < A; ++i) surv[i] = oracle::exact_survival_prob(al[i], k, l, AgentId{current});
+        return A;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
 }  // extern "C"

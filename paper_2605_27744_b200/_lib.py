@@ -116,6 +116,19 @@ SIGNATURES = {
     "cs_pool_create_sharded": (C.c_int, [C.POINTER(PoolCfg), C.c_int64, vp, C.POINTER(vp)]),
     "cs_engine_create_sharded": (C.c_int, [C.POINTER(EngineCfg), C.POINTER(WorkloadSpec), C.c_int64, vp,
                                            C.POINTER(vp)]),
+    "cs_learner_create": (C.c_int, [C.c_int64, C.c_int, C.c_int, C.POINTER(vp)]),
+    "cs_learner_destroy": (C.c_int, [vp]),
+    "cs_learner_record": (C.c_int, [vp, vp, vp, C.c_int64]),
+    "cs_learner_prob": (C.c_int, [vp, C.c_uint64, C.c_uint64, C.POINTER(C.c_double)]),
+    "cs_learner_row_total": (C.c_int, [vp, C.c_uint64, C.POINTER(C.c_uint64)]),
+    "cs_learner_agents": (C.c_int, [vp, vp, C.c_int]),
+    "cs_learner_state_bytes": (C.c_int, [vp, C.POINTER(C.c_uint64)]),
+    "cs_learner_rebuild": (C.c_int, [vp, C.c_uint64, C.c_double, C.c_int, vp, C.c_int]),
+    "cs_learner_argmax": (C.c_int, [vp, C.c_uint64, C.POINTER(C.c_uint64), C.POINTER(C.c_double),
+                                    C.POINTER(C.c_int)]),
+    "cs_exact_survival_prob": (C.c_int, [vp, C.c_uint64, C.c_int, C.c_uint64, C.POINTER(C.c_double)]),
+    "cs_chain_hash": (C.c_int, [vp, vp, vp, vp, C.c_int, vp]),
+    "cs_derive_agent_identity": (C.c_int, [vp, vp, C.c_int, C.c_int, C.c_int, vp]),
     "cs_last_error": (C.c_char_p, []),
     "cs_version": (C.c_char_p, []),
 }

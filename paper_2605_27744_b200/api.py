@@ -169,12 +169,102 @@ def hash_prompts(prompts, block_size=16, skip=4, take=4, pool=None):
 
 
 def chain_hash(parent, tokens):
-    """chain_hash (hashing.cpp:26-35) on the GPU. A parent key is supported by hashing a
-    two-block prompt whose first block is unknown, so only parent=None is accepted here."""
-    if parent is not None:
-        raise ValueError("chain_hash with an explicit parent: use block_keys_for on the full prompt")
-    ks, _, _ = hash_prompts([tokens], block_size=max(len(tokens), 1))
-    return int(ks[0][0])
+    """chain_hash (hashing.cpp:26-35; Python binding py_module.cpp:82-88) on the GPU: parent None
+    chains from the root. Empty token sequences are invalid_argument (ValueError)."""
+    toks = np.ascontiguousarray(tokens, dtype=np.uint32)
+    off = np.array([0, toks.size], np.int64)
+    par = np.array([0 if parent is None else int(parent)], np.uint64)
+    hp = np.array([0 if parent is None else 1], np.uint8)
+    out = np.zeros(1, np.uint64)
+    check(lib().cs_chain_hash(_p(par), _p(hp), _p(toks), _p(off), 1, _p(out)))
+    return int(out[0])
+
+
+def derive_agent_identity(block_keys, skip=4, take=4):
+    """derive_agent_identity (cachesage_policy.cpp:9-31; py_module.cpp:90-101) on the GPU."""
+    k = _u64(block_keys)
+    off = np.array([0, k.size], np.int64)
+    out = np.zeros(1, np.uint64)
+    check(lib().cs_derive_agent_identity(_p(k) if k.size else None, _p(off), 1, skip, take, _p(out)))
+    return int(out[0])
+
+
+class TransitionLearner:
+    """TransitionLearner (transition_learner.hpp:19-60; Python binding py_module.cpp:103-123)
+    on the device: record (K3), prob, row_total, agents, state_bytes, argmax_row (K6) and the
+    reachability rebuild (K3b). Agent ids are the 64-bit AgentId values."""
+
+    def __init__(self, window=1024, agent_capacity=1024, device=0):
+        h = C.c_void_p()
+        check(lib().cs_learner_create(int(window), int(agent_capacity), int(device), C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().cs_learner_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def record(self, prev, nxt):
+        self.record_many([prev], [nxt])
+
+    def record_many(self, prev, nxt):
+        """record() of each (prev[i], next[i]) in order, as one device batch."""
+        a, b = _u64(prev), _u64(nxt)
+        if a.size != b.size:
+            raise ValueError("record_many: prev and next differ in length")
+        check(lib().cs_learner_record(self.h, _p(a), _p(b), a.size))
+
+    def prob(self, a, b):
+        p = C.c_double(0.0)
+        check(lib().cs_learner_prob(self.h, int(a), int(b), C.byref(p)))
+        return p.value
+
+    def row_total(self, a):
+        t = C.c_uint64(0)
+        check(lib().cs_learner_row_total(self.h, int(a), C.byref(t)))
+        return t.value
+
+    def agents(self):
+        n = check(lib().cs_learner_agents(self.h, None, 0))
+        out = np.zeros(max(n, 1), np.uint64)
+        lib().cs_learner_agents(self.h, _p(out), n)
+        return [int(x) for x in out[:n]]
+
+    def state_bytes(self):
+        b = C.c_uint64(0)
+        check(lib().cs_learner_state_bytes(self.h, C.byref(b)))
+        return b.value
+
+    def argmax_row(self, a):
+        """(best successor id, probability), or None for an unseen row (ties -> smaller id)."""
+        best, p, found = C.c_uint64(0), C.c_double(0.0), C.c_int(0)
+        check(lib().cs_learner_argmax(self.h, int(a), C.byref(best), C.byref(p), C.byref(found)))
+        return (best.value, p.value) if found.value else None
+
+    def rebuild_reachability(self, current, tau=0.01, e_max=8):
+        """rebuild_reachability (reachability.cpp:39-81): {agent id: hop} over the known agents
+        (plus `current` at hop 0, as the reference inserts it)."""
+        ids = self.agents()
+        hops = np.zeros(max(len(ids), 1), np.int32)
+        check(lib().cs_learner_rebuild(self.h, int(current), float(tau), int(e_max), _p(hops), len(ids)))
+        out = {a: int(h) for a, h in zip(ids, hops[:len(ids)])}
+        out[int(current)] = 0
+        return out
+
+
+def exact_survival_prob(target, k, matrix, current):
+    """oracle::exact_survival_prob (survival_oracle.cpp:9-62; py_module.cpp:125-131) on the GPU:
+    P(a walk from `current` visits `target` within k steps) on the learner's MLE matrix. Same
+    fp64 operation order as the reference; alphabet <= 64 and k <= 32 (else ValueError)."""
+    out = C.c_double(0.0)
+    check(lib().cs_exact_survival_prob(matrix.h, int(target), int(k), int(current), C.byref(out)))
+    return out.value
 
 
 def block_keys_for(tokens, block_size=16):

@@ -18,7 +18,7 @@ LIB = os.path.join(HERE, "libcachesage_b200.so")
 
 NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-DEVICE_SRCS = ["cs_kernels.cu", "cs_admit.cu"]
+DEVICE_SRCS = ["cs_kernels.cu", "cs_admit.cu", "cs_learner.cu"]
 HOST_SRCS = ["cs_pool.cpp", "cs_engine.cpp", "cs_comm.cpp"]
 DEPS = DEVICE_SRCS + HOST_SRCS + ["cs_device.cuh", "cs_launch.h", "cs_pool.hpp"]
 

@@ -111,6 +111,26 @@ __device__ __forceinline__ unsigned long long identity_of(const unsigned long lo
     return h;
 }
 
+// chain_hash (hashing.cpp:26-35) of one token span per thread, from an explicit parent key or
+// the root (the reference's Python chain_hash(parent, tokens), py_module.cpp:82-88)
+__global__ void chain_hash_kernel(const unsigned long long* parents, const unsigned char* has_parent,
+                                  const unsigned int* tok, const long long* tok_off, int n, unsigned long long* out) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    const bool hp = has_parent && has_parent[p];
+    unsigned long long h = mix64(kHashSeed ^ (hp ? parents[p] : kRootParent));
+    for (long long i = tok_off[p]; i < tok_off[p + 1]; ++i) h = mix64(h ^ ((unsigned long long)tok[i] + kGolden));
+    out[p] = h;
+}
+
+// derive_agent_identity (cachesage_policy.cpp:9-31) of one block-key list per thread
+__global__ void identity_kernel(const unsigned long long* keys, const long long* key_off, int n, int skip, int take,
+                                unsigned long long* out) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    out[p] = identity_of(keys + key_off[p], key_off[p + 1] - key_off[p], skip, take);
+}
+
 // K1 over explicit token streams: one thread per prompt (the chain is sequential within a
 // prompt), tokens read as 128-bit vectors once 16-B aligned.
 __global__ void hash_prompts_kernel(const unsigned int* __restrict__ tok, const long long* __restrict__ tok_off, int n,
@@ -307,6 +327,19 @@ cudaError_t launch_restore(const DevPool& P, const unsigned long long* keys, con
     restore_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(P, keys, lt, agents, refs, n, acc);
     restore_finish_kernel<<<1, 1, 0, s>>>(P, n, acc);
     cudaFreeAsync(acc, s);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_chain_hash(const unsigned long long* parents, const unsigned char* has_parent,
+                              const unsigned int* tok, const long long* tok_off, int n, unsigned long long* out,
+                              cudaStream_t s) {
+    if (n > 0) chain_hash_kernel<<<(n + 127) / 128, 128, 0, s>>>(parents, has_parent, tok, tok_off, n, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_identity(const unsigned long long* keys, const long long* key_off, int n, int skip, int take,
+                            unsigned long long* out, cudaStream_t s) {
+    if (n > 0) identity_kernel<<<(n + 127) / 128, 128, 0, s>>>(keys, key_off, n, skip, take, out);
     return cudaGetLastError();
 }
 

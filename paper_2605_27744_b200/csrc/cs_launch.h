@@ -108,6 +108,11 @@ struct TurnDesc {
 cudaError_t launch_hash_turns(const TurnDesc* turns, int n, int bs, int skip, int take, unsigned int anchor_stride,
                               int hist_pos_bits, unsigned long long* keys, int* counts, unsigned long long* agents,
                               cudaStream_t s);
+cudaError_t launch_chain_hash(const unsigned long long* parents, const unsigned char* has_parent,
+                              const unsigned int* tok, const long long* tok_off, int n, unsigned long long* out,
+                              cudaStream_t s);
+cudaError_t launch_identity(const unsigned long long* keys, const long long* key_off, int n, int skip, int take,
+                            unsigned long long* out, cudaStream_t s);
 cudaError_t launch_unpin(const DevPool& P, const unsigned int* slots, int n, cudaStream_t s);
 cudaError_t launch_restore(const DevPool& P, const unsigned long long* keys, const unsigned long long* lt,
                            const unsigned int* agents, const unsigned int* refs, long long n, cudaStream_t s);

@@ -569,6 +569,64 @@ int cs_hash_prompts(cs_pool_t pool, const uint32_t* tokens, const int64_t* tok_o
     });
 }
 
+static void need_device() {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        throw CsError(CS_ERR_CUDA, "no CUDA device: cachesage_b200 has no CPU fallback");
+}
+
+int cs_chain_hash(const uint64_t* parents, const uint8_t* has_parent, const uint32_t* tokens, const int64_t* tok_off,
+                  int n, uint64_t* out) {
+    return guard([&] {
+        if (n < 0 || (n > 0 && (!tokens || !tok_off || !out))) throw std::invalid_argument("cs_chain_hash: null argument");
+        for (int i = 0; i < n; ++i)
+            if (tok_off[i + 1] <= tok_off[i]) throw std::invalid_argument("chain_hash: token sequence must be nonempty");
+        if (n == 0) return;
+        need_device();
+        const int64_t ntok = tok_off[n] - tok_off[0];
+        csb::DevBuf tk, off, par, hp, o;
+        tk.ensure(4 * (size_t)ntok);
+        off.ensure(8 * (size_t)(n + 1));
+        o.ensure(8 * (size_t)n);
+        std::vector<int64_t> rel(n + 1);
+        for (int i = 0; i <= n; ++i) rel[i] = tok_off[i] - tok_off[0];
+        ck(cudaMemcpy(tk.p, tokens + tok_off[0], 4 * (size_t)ntok, cudaMemcpyHostToDevice), "H2D");
+        ck(cudaMemcpy(off.p, rel.data(), 8 * (size_t)(n + 1), cudaMemcpyHostToDevice), "H2D");
+        if (parents && has_parent) {
+            par.ensure(8 * (size_t)n);
+            hp.ensure((size_t)n);
+            ck(cudaMemcpy(par.p, parents, 8 * (size_t)n, cudaMemcpyHostToDevice), "H2D");
+            ck(cudaMemcpy(hp.p, has_parent, (size_t)n, cudaMemcpyHostToDevice), "H2D");
+        }
+        ck(csb::launch_chain_hash(par.as<unsigned long long>(), hp.as<unsigned char>(), tk.as<unsigned int>(),
+                                  off.as<long long>(), n, o.as<unsigned long long>(), 0),
+           "chain_hash");
+        ck(cudaMemcpy(out, o.p, 8 * (size_t)n, cudaMemcpyDeviceToHost), "D2H");
+    });
+}
+
+int cs_derive_agent_identity(const uint64_t* keys, const int64_t* key_off, int n, int skip, int take, uint64_t* out) {
+    return guard([&] {
+        if (n < 0 || (n > 0 && (!key_off || !out))) throw std::invalid_argument("cs_derive_agent_identity: null argument");
+        if (skip < 0 || take < 1) throw std::invalid_argument("derive_agent_identity: skip >= 0 and take >= 1 required");
+        if (n == 0) return;
+        need_device();
+        const int64_t nk = key_off[n] - key_off[0];
+        csb::DevBuf k, off, o;
+        k.ensure(8 * (size_t)std::max<int64_t>(nk, 1));
+        off.ensure(8 * (size_t)(n + 1));
+        o.ensure(8 * (size_t)n);
+        std::vector<int64_t> rel(n + 1);
+        for (int i = 0; i <= n; ++i) rel[i] = key_off[i] - key_off[0];
+        if (nk > 0) ck(cudaMemcpy(k.p, keys + key_off[0], 8 * (size_t)nk, cudaMemcpyHostToDevice), "H2D");
+        ck(cudaMemcpy(off.p, rel.data(), 8 * (size_t)(n + 1), cudaMemcpyHostToDevice), "H2D");
+        ck(csb::launch_identity(k.as<unsigned long long>(), off.as<long long>(), n, skip, take,
+                                o.as<unsigned long long>(), 0),
+           "derive_agent_identity");
+        ck(cudaMemcpy(out, o.p, 8 * (size_t)n, cudaMemcpyDeviceToHost), "D2H");
+    });
+}
+
 static void stage_prompt(cs_pool_t pool, const uint64_t* keys, const int32_t* counts, int n) {
     pool->d_keys.ensure(sizeof(uint64_t) * std::max(n, 1));
     pool->d_counts.ensure(sizeof(int32_t) * std::max(n, 1));

@@ -84,6 +84,9 @@ def lib():
         _lib.ref_exact_survival.restype = C.c_double
         _lib.ref_exact_survival.argtypes = [C.c_ulonglong, C.c_int, C.c_long, C.c_void_p,
                                             C.c_void_p, C.c_ulonglong]
+        _lib.ref_learner_eval.restype = C.c_long
+        _lib.ref_learner_eval.argtypes = [C.c_long, C.c_void_p, C.c_void_p, C.c_long, C.c_long, C.c_ulonglong,
+                                          C.c_double, C.c_int, C.c_int] + [C.c_void_p] * 9
         _lib.ref_evict_bench.restype = C.c_double
         _lib.ref_evict_bench.argtypes = [C.c_long, C.c_int, C.c_long, C.c_long, C.c_long, C.c_int,
                                          C.POINTER(C.c_double), C.POINTER(C.c_ulonglong)]
@@ -238,3 +241,27 @@ def evict_bench(N, n_agents, n_agent_blocks, k, cachesage=True, k_warm=0):
     if s < 0:
         raise RuntimeError(_err())
     return s, fill.value, int(last.value)
+
+
+def learner_eval(pairs_a, pairs_b, window=1024, current=0, tau=0.01, e_max=8, k=-1, cap=64):
+    """The reference TransitionLearner after recording the pairs (see ref_learner_eval)."""
+    import numpy as np
+
+    a = np.ascontiguousarray(pairs_a, dtype=np.uint64)
+    b = np.ascontiguousarray(pairs_b, dtype=np.uint64)
+    ag = np.zeros(cap, np.uint64)
+    prob = np.zeros(cap * cap, np.float64)
+    tot = np.zeros(cap, np.uint64)
+    sb = np.zeros(1, np.uint64)
+    ai = np.zeros(cap, np.uint64)
+    ap = np.zeros(cap, np.float64)
+    af = np.zeros(cap, np.int32)
+    hops = np.zeros(cap, np.int32)
+    surv = np.zeros(cap, np.float64)
+    n = lib().ref_learner_eval(a.size, _ptr(a), _ptr(b), window, cap, current, tau, e_max, k, _ptr(ag), _ptr(prob),
+                               _ptr(tot), _ptr(sb), _ptr(ai), _ptr(ap), _ptr(af), _ptr(hops), _ptr(surv))
+    if n < 0:
+        raise RuntimeError(_err())
+    return {"agents": [int(x) for x in ag[:n]], "prob": prob[:n * n].reshape(n, n), "totals": tot[:n],
+            "state_bytes": int(sb[0]), "argmax": [(int(i), float(p)) if f else None for i, p, f in zip(ai[:n], ap[:n], af[:n])],
+            "hops": hops[:n], "surv": surv[:n]}
