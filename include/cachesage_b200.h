@@ -175,6 +175,8 @@ typedef struct cs_engine_cfg {
     int timing;       /* record CUDA events around each admission launch */
     int host_inputs;  /* 1: prompt blocks live in pinned host memory and are copied H2D per
                          admission, victims copied D2H per admission (the end-to-end path) */
+    int device_scheduler; /* 1: EXPERIMENTAL device-resident scheduler: whole
+                             EngineSim steps in one persistent launch; see DESIGN.md §4 */
 } cs_engine_cfg;
 
 void cs_engine_cfg_default(cs_engine_cfg* cfg);

@@ -56,6 +56,7 @@ class EngineCfg(C.Structure):
     _fields_ = [
         ("pool", PoolCfg), ("concurrency", C.c_int), ("block_size", C.c_int), ("prefetch", C.c_int),
         ("skip", C.c_int), ("take", C.c_int), ("timing", C.c_int), ("host_inputs", C.c_int),
+        ("device_scheduler", C.c_int),
     ]
 
 

@@ -314,7 +314,8 @@ class Engine:
     """EngineSim (engine.hpp:90-208) with the block pool, learner and eviction on the GPU."""
 
     def __init__(self, spec, policy="cachesage", budget=None, concurrency=None, block_size=16, prefetch=True,
-                 skip=4, take=4, timing=False, host_inputs=False, comm=None, shard_slots=0, **pool_kw):
+                 skip=4, take=4, timing=False, host_inputs=False, comm=None, shard_slots=0,
+                 device_scheduler=False, **pool_kw):
         """comm (shard.Comm): this engine drives ONE shard of a hash-sharded pool of global
         budget `budget`; every shard runs the same trace and reaches the same
         decisions. shard_slots: the shard's physical slots (0 = 1.25 budget / world + 4096)."""
@@ -327,6 +328,7 @@ class Engine:
         cfg.skip, cfg.take = skip, take
         cfg.timing = 1 if timing else 0
         cfg.host_inputs = 1 if host_inputs else 0
+        cfg.device_scheduler = 1 if device_scheduler else 0
         self._spec = spec_struct(spec)
         h = C.c_void_p()
         self.comm = comm

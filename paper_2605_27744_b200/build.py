@@ -39,14 +39,16 @@ def _stale(target, sources):
 def build(verbose: bool = False, force: bool = False) -> str:
     os.makedirs(OUT_DIR, exist_ok=True)
     inc = ["-I", os.path.join(ROOT, "include"), "-I", CSRC]
-    header_deps = [os.path.join(CSRC, h) for h in ("cs_device.cuh", "cs_launch.h", "cs_pool.hpp", "cs_block.cuh", "cs_shard.cuh", "cs_comm.hpp")]
+    header_deps = [os.path.join(CSRC, h) for h in ("cs_device.cuh", "cs_launch.h", "cs_pool.hpp", "cs_block.cuh", "cs_shard.cuh", "cs_comm.hpp", "cs_engine_state.h", "cs_engine_dev.cuh")]
     header_deps.append(os.path.join(ROOT, "include", "cachesage_b200.h"))
     objs = []
     for src in DEVICE_SRCS:
         s = os.path.join(CSRC, src)
         o = os.path.join(OUT_DIR, src + ".o")
         if force or _stale(o, [s] + header_deps):
-            _run([NVCC, "-O3", "-lineinfo", "-std=c++17", *ARCH, "-fmad=false", "-Xptxas", "-v",
+            # -dlcm=cg: global loads default to L2 (not L1). The persistent kernels read state other
+            # SMs wrote since a previous admission; only a kernel boundary would clean a stale L1.
+            _run([NVCC, "-O3", "-lineinfo", "-std=c++17", *ARCH, "-fmad=false", "-Xptxas", "-v,-dlcm=cg",
                   "-Xcompiler", "-fPIC,-ffp-contract=off", *inc, "-c", s, "-o", o], verbose)
         objs.append(o)
     for src in HOST_SRCS:

@@ -23,6 +23,7 @@
 #include <algorithm>
 
 #include "cs_block.cuh"
+#include "cs_engine_state.h"
 #include "cs_launch.h"
 
 namespace csb {
@@ -514,6 +515,13 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* m, unsigned int pa
         : "memory");
 }
 
+// Cross-proxy ordering for the TMA stream, global and shared: (1) the pool slots the previous
+// admission wrote with generic stores (on CTA 0, made visible by a grid barrier or a kernel
+// boundary) must be what the async-proxy bulk reads see; (2) this CTA's earlier generic accesses
+// to the ring (which doubles as the replay view, the prescan select buffer and the scheduler's
+// staging area) must precede the async-proxy writes into it. Issued after a __syncthreads.
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async;" ::: "memory"); }
+
 // 1-D bulk copy global -> this CTA's shared memory, completion counted on mbarrier m. The pool
 // stream is read once per pass: it is marked evict-first in L2, so it does not flush the small
 // hot state CTA 0's serial chain works on (block table entries, prescan lists, learner).
@@ -521,6 +529,13 @@ __device__ __forceinline__ unsigned long long l2_evict_first() {
     unsigned long long pol;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
     return pol;
+}
+
+__device__ __forceinline__ void bulk_g2s_plain(void* dst, const void* src, unsigned int bytes, unsigned long long* m) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(m))
+                 : "memory");
 }
 
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned int bytes, unsigned long long* m) {
@@ -664,6 +679,37 @@ __device__ __forceinline__ unsigned int unpin_at(const AdmitArgs& a, int i) {
         }
     }
     return kNoSlot;
+}
+
+// The same 4 slots straight from global memory (L2, 128-bit loads): the persistent engine kernel
+// streams this way (kFreeTick / no agent / pinned past the range end).
+__device__ __forceinline__ void load4(const DevPool& P, long long i0, bool valid, unsigned long long (&x4)[kV],
+                                      unsigned int (&a4)[kV], unsigned int (&r4)[kV]) {
+    if (valid) {
+        const ulonglong2 l01 = __ldcg(reinterpret_cast<const ulonglong2*>(P.lt + i0));
+        const ulonglong2 l23 = __ldcg(reinterpret_cast<const ulonglong2*>(P.lt + i0 + 2));
+        const uint4 aa = __ldcg(reinterpret_cast<const uint4*>(P.agent + i0));
+        const uint4 rr = __ldcg(reinterpret_cast<const uint4*>(P.refs + i0));
+        x4[0] = l01.x;
+        x4[1] = l01.y;
+        x4[2] = l23.x;
+        x4[3] = l23.y;
+        a4[0] = aa.x;
+        a4[1] = aa.y;
+        a4[2] = aa.z;
+        a4[3] = aa.w;
+        r4[0] = rr.x;
+        r4[1] = rr.y;
+        r4[2] = rr.z;
+        r4[3] = rr.w;
+    } else {
+#pragma unroll
+        for (int k = 0; k < kV; ++k) {
+            x4[k] = kFreeTick;
+            a4[k] = kNoAgent;
+            r4[k] = 1u;
+        }
+    }
 }
 
 // ---- speculative pass support: the set of slots phase 0 may change (the prompt's resident
@@ -861,6 +907,7 @@ __device__ void scan_pass(const DevPool& P, int NL, int keep, const ScanBufs& B,
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+    fence_proxy_async_smem();
     if (tid == 0) {  // an unclassified agent slot may land in any survival class
         unsigned long long m = 0ull;
         for (int c = 0; c + 1 < NL; ++c) m = max(m, S.thr[c]);
@@ -884,7 +931,7 @@ __device__ void scan_pass(const DevPool& P, int NL, int keep, const ScanBufs& B,
     volatile unsigned long long* thr = S.thr;
     const bool consumer = tid < kThreads;
 
-    if (fast) {
+    if (fast && !P.stream_generic) {
         if (!consumer) {  // producer warp
             if (lane_id() == 0) {
                 for (int t = 0; t < ntiles; ++t) {
@@ -922,7 +969,7 @@ __device__ void scan_pass(const DevPool& P, int NL, int keep, const ScanBufs& B,
             return;  // the caller redoes this pass in safe mode
         }
     } else {
-        if (tid == 0)
+        if (tid == 0 && !P.stream_generic)
             for (int t = 0; t < kRing && t < ntiles; ++t) issue(t);
         unsigned long long gbn = ~0ull;
         for (int t = 0; t < ntiles; ++t) {
@@ -933,16 +980,20 @@ __device__ void scan_pass(const DevPool& P, int NL, int keep, const ScanBufs& B,
             }
             const long long i0 = lo + (long long)t * TV + (long long)tid * kV;
             const unsigned char* st = ring + (size_t)s * kRingStage;
-            mbar_wait(&S.mbar[s], (unsigned int)((t / kRing) & 1));
             unsigned long long x4[kV];
             unsigned int a4[kV], r4[kV];
-            read4(st, tid, consumer && i0 + kV <= hi, x4, a4, r4);
+            if (P.stream_generic) {
+                load4(P, i0, consumer && i0 + kV <= hi, x4, a4, r4);
+            } else {
+                mbar_wait(&S.mbar[s], (unsigned int)((t / kRing) & 1));
+                read4(st, tid, consumer && i0 + kV <= hi, x4, a4, r4);
+            }
             int cl[kV];
             unsigned int acc = classify4(x4, a4, r4, thr[R], thr[E], thr, cls, E, cl);
             const int maxpos = append4(acc, x4, cl, i0, R, B, S, false);
             // every thread is done with stage s: refill it with tile t + kRing
             const int need_flush = __syncthreads_or(maxpos >= kFlushAt);
-            if (tid == 0 && t + kRing < ntiles) issue(t + kRing);
+            if (tid == 0 && t + kRing < ntiles && !P.stream_generic) issue(t + kRing);
             if (need_flush) {
                 ensure_cls(P, a, B, S);
                 stage_flush(P, NL, keep, B, S, Sel, false);
@@ -1171,7 +1222,8 @@ __device__ __forceinline__ unsigned long long next_hint(unsigned long long v1, u
     return sat_add(v1, sat_add(span, span));
 }
 
-__device__ void prescan_pass(const DevPool& P, const ScanBufs& B, ScanSmem& S, unsigned char* dsm, int par) {
+__device__ void prescan_pass(const DevPool& P, const ScanBufs& B, ScanSmem& S, unsigned char* dsm, int par,
+                             const AdmitArgs* dbg_args) {
     Ctrl* C = P.ctrl;
     const int tid = threadIdx.x, T = blockDim.x;
     const long long TV = kTile;
@@ -1193,11 +1245,47 @@ __device__ void prescan_pass(const DevPool& P, const ScanBufs& B, ScanSmem& S, u
         P.dbg[blockIdx.x * 16 + 0] = gtimer();
     }
     __syncthreads();
+    fence_proxy_async_smem();
     // (the thresholds load while the first tiles are in flight) agent-carrying slots share E's
     // threshold: the E members among them are complete to it, and the other classes' lists are
     // only needed non-empty (see consume_prescan)
     const unsigned long long hE = __ldcg(P.pre_hint + 0), hR = __ldcg(P.pre_hint + 1), hP = hE;
-    if (tid >= kThreads) {  // producer warp: one elected thread keeps kRing tiles in flight
+    // list ids: 0 = E (agentless unpinned), 1 = R (resident), 2 = pending (agent, unpinned)
+    auto classify_append = [&](const unsigned long long (&x4)[kV], const unsigned int (&a4)[kV],
+                               const unsigned int (&r4)[kV], long long i0) {
+        unsigned int acc = 0u;
+        int cl[kV];
+#pragma unroll
+        for (int k = 0; k < kV; ++k) {
+            const unsigned long long x = x4[k];
+            acc |= (unsigned int)(x <= hR) << k;
+            const bool agentless = a4[k] == kNoAgent;
+            cl[k] = agentless ? 0 : 2;
+            acc |= (unsigned int)(r4[k] == 0u && x <= (agentless ? hE : hP)) << (kV + k);
+        }
+        if (!S.overflow) append4(acc, x4, cl, i0, 1, B, S, true);
+    };
+    if (P.stream_generic) {
+        // persistent engine kernel: L2-coherent 128-bit loads, one tile prefetched in registers
+        if (tid < kThreads) {
+            unsigned long long nx[kV];
+            unsigned int na[kV], nr[kV];
+            long long i0 = lo + (long long)tid * kV;
+            load4(P, i0, i0 + kV <= hi, nx, na, nr);
+            for (int t = 0; t < ntiles; ++t, i0 += TV) {
+                unsigned long long x4[kV];
+                unsigned int a4[kV], r4[kV];
+#pragma unroll
+                for (int k = 0; k < kV; ++k) {
+                    x4[k] = nx[k];
+                    a4[k] = na[k];
+                    r4[k] = nr[k];
+                }
+                if (t + 1 < ntiles) load4(P, i0 + TV, i0 + TV + kV <= hi, nx, na, nr);
+                classify_append(x4, a4, r4, i0);
+            }
+        }
+    } else if (tid >= kThreads) {  // producer warp: one elected thread keeps kRing tiles in flight
         if (lane_id() == 0) {
             for (int t = 0; t < ntiles; ++t) {
                 const int s = t % kRing;
@@ -1221,20 +1309,10 @@ __device__ void prescan_pass(const DevPool& P, const ScanBufs& B, ScanSmem& S, u
             unsigned long long x4[kV];
             unsigned int a4[kV], r4[kV];
             read4(st, tid, i0 + kV <= hi, x4, a4, r4);
+            if (P.dbg_check == 2 && i0 + kV <= hi) load4(P, i0, true, x4, a4, r4);  // debug: L2 values
             __syncwarp();
             if (lane_id() == 0) mbar_arrive(&S.mbar_empty[s]);
-            // list ids: 0 = E (agentless unpinned), 1 = R (resident), 2 = pending (agent, unpinned)
-            unsigned int acc = 0u;
-            int cl[kV];
-#pragma unroll
-            for (int k = 0; k < kV; ++k) {
-                const unsigned long long x = x4[k];
-                acc |= (unsigned int)(x <= hR) << k;
-                const bool agentless = a4[k] == kNoAgent;
-                cl[k] = agentless ? 0 : 2;
-                acc |= (unsigned int)(r4[k] == 0u && x <= (agentless ? hE : hP)) << (kV + k);
-            }
-            if (!S.overflow) append4(acc, x4, cl, i0, 1, B, S, true);
+            classify_append(x4, a4, r4, i0);
         }
     }
     __syncthreads();
@@ -1424,10 +1502,12 @@ __device__ void prescan_finish(const DevPool& P, const AdmitArgs& a, const ScanB
     const int oR = ((mE + 1) & ~1);  // R staged 16-B aligned after E
     if (oR + mR <= kStage && mE <= kDirectPre && mR <= kDirectPre) {
         // two warp groups (named barriers 1 and 2): group 0 finalizes E, group 1 R, at once
-        __shared__ SelectSmem Sg[2];
         __shared__ int ng[2];
         const int nw = (int)blockDim.x >> 5, w0 = (nw + 1) >> 1;
         const int grp = warp_id() < w0 ? 0 : 1;
+        // group 0 selects with the CTA's SelectSmem, group 1 with one in the (drained) TMA ring
+        SelectSmem& Sgr =
+            grp == 0 ? Sel : *reinterpret_cast<SelectSmem*>(reinterpret_cast<unsigned char*>(B.st_lt) + kOffRing);
         const int gn = (grp == 0 ? w0 : nw - w0) * 32, gt = tid - (grp == 0 ? 0 : w0 * 32);
         const int m = grp ? mR : mE, off = grp ? oR : 0;
         unsigned long long* vl = B.st_lt + off;
@@ -1441,7 +1521,7 @@ __device__ void prescan_finish(const DevPool& P, const AdmitArgs& a, const ScanB
         if (gt == 0) ng[grp] = 0;
         group_sync(1 + grp, gn);
         if (tid == 0) P.dbg[blockIdx.x * 16 + 7] = gtimer();
-        const unsigned long long v = m > kPreK ? group_kth(vl, m, kPreK, Sg[grp], gt, gn, 1 + grp) : kNoBound;
+        const unsigned long long v = m > kPreK ? group_kth(vl, m, kPreK, Sgr, gt, gn, 1 + grp) : kNoBound;
         for (int j = gt; j < m; j += gn) {
             const unsigned long long x = vl[j];
             if (m <= kPreK || x <= v) {
@@ -1459,14 +1539,14 @@ __device__ void prescan_finish(const DevPool& P, const AdmitArgs& a, const ScanB
             const int r = count_below(tl, n, x);
             P.pl_lt[base + r] = x;
             P.pl_slot[base + r] = ts[j];
-            if (r == 0) Sg[grp].hmax = x;
+            if (r == 0) Sgr.hmax = x;
         }
         group_sync(1 + grp, gn);
         if (gt == 0) {
             const unsigned long long Tl = m > kPreK ? v : h[grp];
             P.pl_n[par * 3 + grp] = n;
             P.pl_T[par * 3 + grp] = Tl;
-            P.pre_hint[grp] = n == 0 ? kNoBound : bad ? Tl : next_hint(Sg[grp].hmax, Tl);
+            P.pre_hint[grp] = n == 0 ? kNoBound : bad ? Tl : next_hint(Sgr.hmax, Tl);
         }
         __syncthreads();
     } else {  // many candidates (a loose threshold): radix select per list
@@ -1789,6 +1869,47 @@ __device__ bool consume_early(const DevPool& P, const EarlySmem& es, ReplaySmem&
     if (tid == 0) R.lists_ready = 1;
     __syncthreads();
     return true;
+}
+
+// Debug (P.dbg_check, small pools): every true E member below the last listed E entry must be
+// listed. Records misses (slot, lt, refs, agent, in U, touched, in the prescan list and its flag)
+// at dbg[grid*16 + 16 ...].
+__device__ void debug_check_e(const DevPool& P, const EarlySmem& es, const ReplaySmem& R, const ScanBufs& B,
+                              const ScanSmem& S, const AdmitArgs& a) {
+    const int E = P.e_max;
+    const int n = R.L_n[E];
+    if (n <= 0) return;
+    const unsigned long long last = R.L_lt[E][n - 1];
+    unsigned long long* out = P.dbg + gridDim.x * 16 + 16;
+    for (long long s = threadIdx.x; s < P.cap; s += blockDim.x) {
+        const unsigned long long x = __ldcg(P.lt + s);
+        if (x == kFreeTick || x > last || __ldcg(P.refs + s) != 0u) continue;
+        const unsigned int ag = __ldcg(P.agent + s);
+        const int c = ag == kNoAgent ? E : B.cls[ag];
+        if (c != E) continue;
+        int lo = 0, hi = n;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (R.L_lt[E][mid] < x) lo = mid + 1;
+            else hi = mid;
+        }
+        if (lo < n && R.L_lt[E][lo] == x) continue;
+        int inpl = -1;
+        for (int j = 0; j < es.nE; ++j)
+            if (es.E_slot[j] == (unsigned int)s) inpl = j;
+        const unsigned long long k = atomicAdd(out, 1ull);
+        if (k < 8) {
+            unsigned long long* r = out + 1 + k * 6;
+            r[0] = (unsigned long long)s;
+            r[1] = x;
+            r[2] = ((unsigned long long)ag << 32) | (unsigned long long)xset_has(S, (unsigned int)s) << 1 |
+                   (unsigned long long)tset_has(es.tset, (unsigned int)s);
+            r[3] = (unsigned long long)(long long)inpl | (inpl >= 0 ? (unsigned long long)es.E_ok[inpl] << 40 : 0ull);
+            r[4] = a.seq;
+            r[5] = P.dbg_unpin ? P.dbg_unpin[s] : 0ull;
+        }
+    }
+    __syncthreads();
 }
 
 // ------------------------------------------------------------------ K5b: replay + apply
@@ -2378,12 +2499,10 @@ __device__ void write_status(const DevPool& P, const AdmitArgs& a, const AdmSmem
     // no system fence: the host reads the mapped record only after the launch completes
 }
 
-__global__ void __launch_bounds__(kThreads + 32, 1) admit_kernel(DevPool P, AdmitArgs a) {
-    extern __shared__ __align__(16) unsigned char dsm[];
-    __shared__ ScanSmem S;
-    __shared__ SelectSmem Sel;
-    __shared__ RedSmem Red;
-    __shared__ AdmSmem A;
+// One admission (the body of admit_kernel; the device-resident engine kernel runs it in a loop).
+// Every CTA of the cooperative grid calls it; a CTA returns when its part is done.
+__device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a, unsigned char* dsm, ScanSmem& S,
+                                        SelectSmem& Sel, RedSmem& Red, AdmSmem& A) {
     Ctrl* C = P.ctrl;
     const int tid = threadIdx.x, T = blockDim.x;
     const int NL = P.n_lists;
@@ -2472,7 +2591,10 @@ __global__ void __launch_bounds__(kThreads + 32, 1) admit_kernel(DevPool P, Admi
                     const int i = q - ne - ni;
                     const unsigned int us = unpin_at(a, i);
                     if (us == kNoSlot) continue;
-                    if (i < nu && atomicSub(&P.refs[us], 1u) == 1u) ++dec;
+                    if (i < nu && atomicSub(&P.refs[us], 1u) == 1u) {
+                        ++dec;
+                        if (P.dbg_unpin) P.dbg_unpin[us] = (a.seq << 8) | 1u;
+                    }
                     if (early) xset_insert(S, us);
                 } else if (q < ne + ni + nuv + nE) {
                     const int j = q - ne - ni - nuv;
@@ -2550,7 +2672,10 @@ __global__ void __launch_bounds__(kThreads + 32, 1) admit_kernel(DevPool P, Admi
                 const int nu = unpin_total(a, false);
                 for (int i = tid; i < nu; i += T) {
                     const unsigned int us = unpin_at(a, i);
-                    if (us != kNoSlot && atomicSub(&P.refs[us], 1u) == 1u) ++dec;
+                    if (us != kNoSlot && atomicSub(&P.refs[us], 1u) == 1u) {
+                        ++dec;
+                        if (P.dbg_unpin) P.dbg_unpin[us] = (a.seq << 8) | 2u;
+                    }
                 }
                 dec = block_sum(dec, Red);
                 if (tid == 0) C->pinned -= dec;
@@ -2629,7 +2754,7 @@ __global__ void __launch_bounds__(kThreads + 32, 1) admit_kernel(DevPool P, Admi
     if (pre_avail) {
         if (blockIdx.x != 0) {
             const unsigned long long hE = __ldcg(P.pre_hint + 0), hR = __ldcg(P.pre_hint + 1), hP = hE;
-            prescan_pass(P, B, S, dsm, par_next);
+            prescan_pass(P, B, S, dsm, par_next, &a);
             if (tid == 0) P.dbg[blockIdx.x * 16 + 2] = gtimer();
             prescan_finish(P, a, B, Sel, par_next, hE, hR, hP);
             if (tid == 0) {
@@ -2661,6 +2786,7 @@ __global__ void __launch_bounds__(kThreads + 32, 1) admit_kernel(DevPool P, Admi
                 const bool ok = !need0 ? true
                                 : es.ok ? consume_early(P, es, Rp, B, S, Red)
                                         : consume_prescan(P, a, B, S, Red, par_prev);
+                if (ok && need0 && es.ok && P.dbg_check) debug_check_e(P, es, Rp, B, S, a);
                 stamp(A, 3);
                 pstamp(P, 9);
                 if (ok) replay_apply(P, a, Rp, A, NL, need0, Red, true, true);
@@ -2888,7 +3014,7 @@ __global__ void __launch_bounds__(kThreads + 32, 1) admit_kernel(DevPool P, Admi
     // ---- no usable prescan came in: CTAs 1.. now prescan for the next admission
     if (pre_run && !pre_avail && blockIdx.x != 0) {
         const unsigned long long hE = __ldcg(P.pre_hint + 0), hR = __ldcg(P.pre_hint + 1), hP = hE;
-        prescan_pass(P, B, S, dsm, par_next);
+        prescan_pass(P, B, S, dsm, par_next, &a);
         prescan_finish(P, a, B, Sel, par_next, hE, hR, hP);
         return;
     }
@@ -2906,7 +3032,10 @@ __global__ void __launch_bounds__(kThreads + 32, 1) admit_kernel(DevPool P, Admi
                 const unsigned int s = P.p_slot[i];
                 if (a.pins_out) a.pins_out[i] = s;
                 if (a.flags & kUnpinAfter) {
-                    if (atomicSub(&P.refs[s], 1u) == 1u) ++dec;
+                    if (atomicSub(&P.refs[s], 1u) == 1u) {
+                        ++dec;
+                        if (P.dbg_unpin) P.dbg_unpin[s] = (a.seq << 8) | 3u;
+                    }
                 }
             }
             dec = block_sum(dec, Red);
@@ -2915,7 +3044,7 @@ __global__ void __launch_bounds__(kThreads + 32, 1) admit_kernel(DevPool P, Admi
         __syncthreads();
         stamp(A, 5);
         pstamp(P, 11);
-        if (tid == 0) write_status(P, a, A);
+        if (tid == 0 && a.status) write_status(P, a, A);
         pstamp(P, 12);
         // per-list scan state for the next launch (a speculative pass starts without a prep)
         if (tid < kMaxLists) {
@@ -2930,9 +3059,22 @@ __global__ void __launch_bounds__(kThreads + 32, 1) admit_kernel(DevPool P, Admi
     }
 }
 
+__global__ void __launch_bounds__(kThreads + 32, 1) admit_kernel(DevPool P, AdmitArgs a) {
+    extern __shared__ __align__(16) unsigned char dsm[];
+    __shared__ ScanSmem S;
+    __shared__ SelectSmem Sel;
+    __shared__ RedSmem Red;
+    __shared__ AdmSmem A;
+    admit_body(P, a, dsm, S, Sel, Red, A);
+}
+
 // ------------------------------------------------------------------ hash-sharded pool
 
 #include "cs_shard.cuh"
+
+// ------------------------------------------------------------------ device-resident scheduler
+
+#include "cs_engine_dev.cuh"
 
 // ------------------------------------------------------------------ host side
 

@@ -208,6 +208,9 @@ struct DevPool {
     unsigned int* pre_buf_slot;
     long long pre_gcap;
     unsigned long long* pre_hint;
+    int dbg_check;  // debug: brute-force check of the prescan consumer's list E (small pools)
+    int stream_generic;  // stream the pool with L2 loads instead of TMA (the persistent engine kernel)
+    unsigned long long* dbg_unpin;  // debug: per slot (admission seq << 8 | source) of its last unpin
 
     // hash-sharded mode (world > 1 or an explicit shard): this shard's rank, the shard count,
     // the GLOBAL budget, the exchange buffers and the replicated admission state

@@ -12,6 +12,8 @@
 //   complete_earliest              engine.cpp:353-370   -> unpin_kernel
 //   drain_and_run_warmups          engine.cpp:197-238   -> admit_kernel (lookup + room + unpin)
 #include <algorithm>
+#include <climits>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <deque>
@@ -20,6 +22,7 @@
 #include <unordered_map>
 #include <vector>
 
+#include "cs_engine_state.h"
 #include "cs_pool.hpp"
 
 using csb::ck;
@@ -228,8 +231,23 @@ struct cs_engine {
     }
 
     void build(const cs_engine_cfg& c, const cs_workload_spec* ws, long long shard_slots = 0, cs_comm* comm = nullptr);
+    // device-resident scheduler (cs_engine_dev.cuh): whole steps in one persistent launch
+    bool dev = false;
+    csb::EngState hs{};  // authoritative between launches
+    csb::DevBuf d_state, d_reqs, d_soff, d_sreqs, d_spos, d_cat, d_tc, d_tp, d_ts, d_te, d_td, d_ws, d_wt, d_wk,
+        d_args, d_cmd;
+    long long w_cap = 0;
+    void dev_setup();
+    void dev_run(long long stop_at, long long max_steps);
+    void dev_pull_outputs();
+    long long max_nb = 1;
+    // admissions per persistent launch: the eviction log (drained between launches) must not wrap
+    long long dev_chunk() const { return std::max(1ll, (long long)pool->P.evlog_cap / (2 * std::max(1ll, max_nb))); }
     void drain_evictions(bool force);
-    bool done() const { return loaded && in_flight.empty() && ready.empty() && pending_sessions.empty(); }
+    bool done() const {
+        if (dev) return hs.n_flight == 0 && hs.ready_n == 0 && hs.next_session >= hs.n_sessions;
+        return loaded && in_flight.empty() && ready.empty() && pending_sessions.empty();
+    }
     void arrive(int64_t idx);
     void activate_sessions();
     bool try_start_head();
@@ -370,6 +388,173 @@ void cs_engine::build(const cs_engine_cfg& c, const cs_workload_spec* ws, long l
     t_end.assign(nt, 0.0);
     t_done.assign(nt, 0);
     loaded = true;
+    dev_setup();
+}
+
+void cs_engine::dev_setup() {
+    const char* env = std::getenv("CS_DEVICE_SCHED");  // tools: overrides the config either way
+    const char* env2 = std::getenv("CS_USE_PRESCAN");  // A/B switch (tools): prescans run, never consumed
+    const bool want = env ? std::atoi(env) != 0 : cfg.device_scheduler != 0;
+    if (!want || cfg.host_inputs || pool->comm || conc > csb::kMaxConc) return;
+    const int64_t nt = (int64_t)reqs.size();
+    // sessions in ascending id order (the std::map order of the host scheduler)
+    std::vector<int> soff(1, 0), sreqs;
+    std::unordered_map<int, int> slot;
+    for (const auto& kv : by_session) {
+        slot[kv.first] = (int)soff.size() - 1;
+        for (int64_t r : kv.second) sreqs.push_back((int)r);
+        soff.push_back((int)sreqs.size());
+    }
+    std::vector<csb::EngReq> er(std::max<int64_t>(nt, 1));
+    int max_nb = 1;
+    for (int64_t i = 0; i < nt; ++i) {
+        const Req& r = reqs[i];
+        csb::EngReq& q = er[i];
+        q.blk_off = r.blk_off;
+        q.prompt_tokens = r.prompt_tokens;
+        q.session = slot[r.session];
+        q.agent = r.agent;
+        q.nb = r.nb;
+        q.anchor_blocks = r.anchor_blocks;
+        q.decode = r.decode;
+        q.pad = 0;
+        max_nb = std::max(max_nb, r.nb);
+    }
+    std::vector<csb::EngCat> cat(pool->P.a_cap);
+    for (auto& c : cat) c = csb::EngCat{0, 0, 0, 0};
+    for (const auto& kv : catalog) {
+        cat[kv.first] = csb::EngCat{kv.second.blk_off, kv.second.prompt_tokens, kv.second.nb, 0};
+        max_nb = std::max(max_nb, kv.second.nb);
+    }
+    pool->ensure_prompt_scratch(max_nb);
+    this->max_nb = max_nb;
+    const int bps = std::max(1, pool->cfg.budget_per_step);
+    w_cap = (2 * nt + 64) * bps;
+    auto up = [&](csb::DevBuf& b, const void* src, size_t bytes) {
+        b.ensure(std::max<size_t>(bytes, 8));
+        if (bytes) ck(cudaMemcpy(b.p, src, bytes, cudaMemcpyHostToDevice), "H2D");
+    };
+    up(d_reqs, er.data(), sizeof(csb::EngReq) * er.size());
+    up(d_soff, soff.data(), 4 * soff.size());
+    up(d_sreqs, sreqs.data(), 4 * std::max<size_t>(sreqs.size(), 1));
+    d_spos.ensure(4 * std::max<size_t>(soff.size(), 1));
+    up(d_cat, cat.data(), sizeof(csb::EngCat) * cat.size());
+    d_tc.ensure(8 * std::max<int64_t>(nt, 1));
+    d_tp.ensure(8 * std::max<int64_t>(nt, 1));
+    d_ts.ensure(8 * std::max<int64_t>(nt, 1));
+    d_te.ensure(8 * std::max<int64_t>(nt, 1));
+    d_td.ensure(std::max<int64_t>(nt, 1));
+    ck(cudaMemset(d_td.p, 0, std::max<int64_t>(nt, 1)), "memset");
+    d_ws.ensure(8 * w_cap);
+    d_wt.ensure(8 * w_cap);
+    d_wk.ensure(8 * w_cap);
+    d_args.ensure(sizeof(csb::AdmitArgs));
+    d_cmd.ensure(8);
+    d_state.ensure(sizeof(csb::EngState));
+    std::memset(&hs, 0, sizeof(hs));
+    hs.conc = conc;
+    hs.budget = budget;
+    hs.prefetch = cfg.prefetch ? 1 : 0;
+    hs.speculate = pool->speculate ? 1 : 0;
+    hs.prescan = pool->prescan ? 1 : 0;
+    hs.use_prescan = (env2 && std::atoi(env2) == 0) ? 0 : 1;
+    hs.n_sessions = (int)soff.size() - 1;
+    hs.last_dispatched = -1;
+    hs.phase = 0;
+    dev = true;
+}
+
+void cs_engine::dev_run(long long stop_at, long long max_steps) {
+    pool->flush_unpins();  // (host-queued unpins: none while the device schedules)
+    hs.tick = tick;
+    hs.seq = pool->seq;
+    hs.pre_ok = pool->pre_ok ? 1 : 0;
+    hs.poll_reset_pending = pool->poll_reset_pending ? 1 : 0;
+    ck(cudaMemcpyAsync(d_state.p, &hs, sizeof(hs), cudaMemcpyHostToDevice, pool->stream), "H2D");
+    csb::EngDev E{};
+    E.st = d_state.as<csb::EngState>();
+    E.reqs = d_reqs.as<csb::EngReq>();
+    E.sess_off = d_soff.as<int>();
+    E.sess_reqs = d_sreqs.as<int>();
+    E.session_pos = d_spos.as<int>();
+    E.cat = d_cat.as<csb::EngCat>();
+    E.keys = d_keys.as<unsigned long long>();
+    E.counts = d_counts.as<int>();
+    E.pins = d_pins.as<unsigned int>();
+    E.agent_ids = pool->P.agent_ids;
+    E.t_cached = d_tc.as<long long>();
+    E.t_prompt = d_tp.as<long long>();
+    E.t_start = d_ts.as<double>();
+    E.t_end = d_te.as<double>();
+    E.t_done = d_td.as<unsigned char>();
+    E.w_step = d_ws.as<long long>();
+    E.w_target = d_wt.as<unsigned long long>();
+    E.w_tick = d_wk.as<unsigned long long>();
+    E.w_cap = w_cap;
+    E.args = d_args.as<csb::AdmitArgs>();
+    E.cmd = d_cmd.as<int>();
+    csb::Ctrl c0;
+    ck(cudaMemcpyAsync(&c0, pool->P.ctrl, sizeof(c0), cudaMemcpyDeviceToHost, pool->stream), "ctrl D2H");
+    if (pool->timing) ck(cudaEventRecord(pool->ev0, pool->stream), "cudaEventRecord");
+    ck(csb::launch_engine(pool->P, E, stop_at, max_steps, pool->n_agents, pool->lc, pool->stream), "engine_kernel");
+    ++pool->launches;
+    if (pool->timing) ck(cudaEventRecord(pool->ev1, pool->stream), "cudaEventRecord");
+    ck(cudaMemcpyAsync(&hs, d_state.p, sizeof(hs), cudaMemcpyDeviceToHost, pool->stream), "D2H");
+    csb::Ctrl c;
+    ck(cudaMemcpyAsync(&c, pool->P.ctrl, sizeof(c), cudaMemcpyDeviceToHost, pool->stream), "ctrl D2H");
+    pool->sync();
+    if (pool->timing) {
+        float ms = 0.f;
+        ck(cudaEventElapsedTime(&ms, pool->ev0, pool->ev1), "cudaEventElapsedTime");
+        pool->admit_ms += ms;
+        const long long sc = c.scans - c0.scans;
+        if (sc > 0) {  // one persistent launch covers many scoring passes: timed per pass
+            pool->scan_launch_ms += ms;
+            pool->scan_launches += sc;
+        }
+        pool->admit_launches += hs.admissions - admissions;
+    }
+    tick = hs.tick;
+    sim_now = hs.sim_now;
+    admissions = hs.admissions;
+    steps = hs.steps;
+    completed = hs.completed;
+    truncated = hs.truncated;
+    warm_exec = hs.warm_exec;
+    warm_drop = hs.warm_drop;
+    tot_prompt = hs.tot_prompt;
+    tot_cached = hs.tot_cached;
+    pool->seq = hs.seq;
+    pool->pre_ok = hs.pre_ok != 0;
+    pool->poll_reset_pending = hs.poll_reset_pending != 0;
+    pool->resident = c.resident;
+    pool->pinned = c.pinned;
+    pool->ev_total = c.n_ev;
+    if (hs.error == 1) throw std::runtime_error("scheduler stalled with an idle engine");
+    if (hs.error == 2) throw std::runtime_error("evict_one: all resident blocks are pinned");
+    if (hs.error == 3) throw CsError(CS_ERR_CAPACITY, "device scheduler: warmup output capacity exceeded");
+    if (hs.error) throw std::runtime_error("device scheduler error");
+    drain_evictions(false);
+}
+
+void cs_engine::dev_pull_outputs() {
+    const int64_t nt = (int64_t)reqs.size();
+    if (nt > 0) {
+        ck(cudaMemcpy(t_cached.data(), d_tc.p, 8 * nt, cudaMemcpyDeviceToHost), "D2H");
+        ck(cudaMemcpy(t_prompt.data(), d_tp.p, 8 * nt, cudaMemcpyDeviceToHost), "D2H");
+        ck(cudaMemcpy(t_start.data(), d_ts.p, 8 * nt, cudaMemcpyDeviceToHost), "D2H");
+        ck(cudaMemcpy(t_end.data(), d_te.p, 8 * nt, cudaMemcpyDeviceToHost), "D2H");
+        ck(cudaMemcpy(t_done.data(), d_td.p, nt, cudaMemcpyDeviceToHost), "D2H");
+    }
+    const long long nw = hs.n_warm;
+    w_step.resize(nw);
+    w_target.resize(nw);
+    w_tick.resize(nw);
+    if (nw > 0) {
+        ck(cudaMemcpy(w_step.data(), d_ws.p, 8 * nw, cudaMemcpyDeviceToHost), "D2H");
+        ck(cudaMemcpy(w_target.data(), d_wt.p, 8 * nw, cudaMemcpyDeviceToHost), "D2H");
+        ck(cudaMemcpy(w_tick.data(), d_wk.p, 8 * nw, cudaMemcpyDeviceToHost), "D2H");
+    }
 }
 
 void cs_engine::drain_evictions(bool force) {
@@ -579,6 +764,7 @@ void cs_engine_cfg_default(cs_engine_cfg* c) {
     c->take = 4;
     c->timing = 0;
     c->host_inputs = 0;
+    c->device_scheduler = 0;
 }
 
 int cs_engine_create(const cs_engine_cfg* cfg, const cs_workload_spec* spec, cs_engine_t* out) {
@@ -639,7 +825,11 @@ int cs_engine_destroy(cs_engine_t e) {
 int cs_engine_step(cs_engine_t e, int* done) {
     return eguard([&] {
         if (!e) throw std::invalid_argument("cs_engine_step: null engine");
-        e->step();
+        if (e->dev) {
+            if (!e->done()) e->dev_run(LLONG_MAX, 1);
+        } else {
+            e->step();
+        }
         if (done) *done = e->done() ? 1 : 0;
     });
 }
@@ -647,7 +837,11 @@ int cs_engine_step(cs_engine_t e, int* done) {
 int cs_engine_run(cs_engine_t e) {
     return eguard([&] {
         if (!e) throw std::invalid_argument("cs_engine_run: null engine");
-        while (!e->done()) e->step();
+        if (e->dev) {
+            while (!e->done()) e->dev_run(e->admissions + e->dev_chunk(), LLONG_MAX);
+        } else {
+            while (!e->done()) e->step();
+        }
         e->pool->flush_unpins();
         e->drain_evictions(true);
     });
@@ -657,7 +851,11 @@ int cs_engine_run_for(cs_engine_t e, int64_t max_adm, int* done) {
     return eguard([&] {
         if (!e) throw std::invalid_argument("cs_engine_run_for: null engine");
         const int64_t stop = e->admissions + max_adm;
-        while (!e->done() && e->admissions < stop) e->step();
+        if (e->dev) {
+            while (!e->done() && e->admissions < stop) e->dev_run(std::min<int64_t>(stop, e->admissions + e->dev_chunk()), LLONG_MAX);
+        } else {
+            while (!e->done() && e->admissions < stop) e->step();
+        }
         if (done) *done = e->done() ? 1 : 0;
     });
 }
@@ -676,7 +874,7 @@ int cs_engine_result_get(cs_engine_t e, cs_engine_result* o) {
         o->truncated = e->truncated;
         o->warmups_executed = e->warm_exec;
         o->warmups_dropped = e->warm_drop;
-        o->warmups_issued = (int64_t)e->w_target.size();
+        o->warmups_issued = e->dev ? (int64_t)e->hs.n_warm : (int64_t)e->w_target.size();
         o->sim_us = e->sim_now;
         o->steps = e->steps;
         o->admissions = e->admissions;
@@ -703,7 +901,11 @@ int cs_engine_run_timed(cs_engine_t e, int64_t max_adm, double* device_ms, int* 
         e->pool->sync();
         ck(cudaEventRecord(a, e->pool->stream), "cudaEventRecord");
         const int64_t stop = e->admissions + max_adm;
-        while (!e->done() && e->admissions < stop) e->step();
+        if (e->dev) {
+            while (!e->done() && e->admissions < stop) e->dev_run(std::min<int64_t>(stop, e->admissions + e->dev_chunk()), LLONG_MAX);
+        } else {
+            while (!e->done() && e->admissions < stop) e->step();
+        }
         ck(cudaEventRecord(b, e->pool->stream), "cudaEventRecord");
         ck(cudaEventSynchronize(b), "cudaEventSynchronize");
         float ms = 0.f;
@@ -751,6 +953,7 @@ int cs_engine_agents(cs_engine_t e, uint64_t* ids, int cap) {
 int cs_engine_turns(cs_engine_t e, int64_t* cached, int64_t* prompt, double* start_us, double* end_us, int64_t cap) {
     return eguard([&] {
         if (!e) throw std::invalid_argument("cs_engine_turns: null engine");
+        if (e->dev) e->dev_pull_outputs();
         const int64_t n = std::min<int64_t>(cap, (int64_t)e->reqs.size());
         for (int64_t i = 0; i < n; ++i) {
             if (cached) cached[i] = e->t_cached[i];
@@ -776,6 +979,14 @@ int64_t cs_engine_evictions(cs_engine_t e, uint64_t* keys, int64_t cap) {
 
 int64_t cs_engine_warmups(cs_engine_t e, int64_t* step, uint64_t* target, uint64_t* tick, int64_t cap) {
     if (!e) return CS_ERR_INVALID_ARGUMENT;
+    if (e->dev) {
+        try {
+            e->dev_pull_outputs();
+        } catch (const std::exception& ex) {
+            cs_set_error(ex.what());
+            return CS_ERR_CUDA;
+        }
+    }
     const int64_t n = (int64_t)e->w_target.size();
     for (int64_t i = 0; i < n && i < cap; ++i) {
         if (step) step[i] = e->w_step[i];

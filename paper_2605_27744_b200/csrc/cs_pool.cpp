@@ -147,7 +147,12 @@ void cs_pool::create(const cs_pool_cfg& c, long long shard_slots, cs_comm* cm) {
     p.gbuf_lt = dmalloc<unsigned long long>((size_t)csb::kMaxLists * p.gcap, "gbuf_lt");
     p.gbuf_slot = dmalloc<unsigned int>((size_t)csb::kMaxLists * p.gcap, "gbuf_slot");
     p.gmin = dmalloc<unsigned long long>((size_t)csb::kMaxLists * lc.grid, "gmin");
-    p.dbg = dmalloc<unsigned long long>((size_t)lc.grid * 16 + 64, "dbg");  // + CTA-0 sub-phase stamps
+    p.dbg = dmalloc<unsigned long long>((size_t)lc.grid * 16 + 192, "dbg");  // + CTA-0 stamps, debug records
+    if (const char* e = std::getenv("CS_DEBUG_PRESCAN")) p.dbg_check = std::atoi(e);
+    if (p.dbg_check) {
+        p.dbg_unpin = dmalloc<unsigned long long>(p.cap_scan, "dbg_unpin");
+        ck(cudaMemset(p.dbg_unpin, 0, 8 * p.cap_scan), "memset");
+    }
     p.pl_lt = dmalloc<unsigned long long>((size_t)2 * 3 * csb::kPendCap, "pl_lt");
     p.pl_slot = dmalloc<unsigned int>((size_t)2 * 3 * csb::kPendCap, "pl_slot");
     p.pl_agent = dmalloc<unsigned int>((size_t)2 * csb::kPendCap, "pl_agent");
@@ -161,7 +166,7 @@ void cs_pool::create(const cs_pool_cfg& c, long long shard_slots, cs_comm* cm) {
         const unsigned long long h[3] = {csb::kNoBound, csb::kNoBound, csb::kNoBound};
         ck(cudaMemcpy(p.pre_hint, h, sizeof(h), cudaMemcpyHostToDevice), "pre_hint");
     }
-    ck(cudaMemsetAsync(p.dbg, 0, sizeof(unsigned long long) * (lc.grid * 16 + 64), stream), "memset");
+    ck(cudaMemsetAsync(p.dbg, 0, sizeof(unsigned long long) * (lc.grid * 16 + 192), stream), "memset");
 
     if (comm) {
         p.sh_send2 = dmalloc<csb::ShardLists>(1, "sh_send2");
@@ -334,7 +339,11 @@ const csb::AdmitStatus& cs_pool::admit(const csb::AdmitArgs& in, int n_for_grid)
     // No eviction is possible when every block could be inserted without reaching the budget:
     // one CTA then suffices (the grid barrier degenerates), saving the cooperative launch.
     const bool may_evict = (a.flags & csb::kAdmit) && resident + n_for_grid > P.cap;
-    const int grid = may_evict ? lc.grid : 1;
+    static const bool full_grid = [] {
+        const char* e = std::getenv("CS_FULL_GRID");  // A/B switch (tools): every admission cooperative
+        return e && std::atoi(e) != 0;
+    }();
+    const int grid = (may_evict || full_grid) ? lc.grid : 1;
     // queued unpins run first inside this launch (they fit the change set of a speculative pass)
     if ((int)unpin_q.size() > csb::kMaxUnpinRanges) flush_unpins();
     a.n_unpin_ranges = 0;
@@ -854,7 +863,7 @@ int cs_pool_debug(cs_pool_t pool, uint64_t* out, int cap, int* grid) {
     return guard([&] {
         if (!pool || !out) throw std::invalid_argument("cs_pool_debug: null argument");
         pool->sync();
-        const int n = std::min(cap, pool->lc.grid * 16 + 64);
+        const int n = std::min(cap, pool->lc.grid * 16 + 192);
         ck(cudaMemcpy(out, pool->P.dbg, 8 * (size_t)n, cudaMemcpyDeviceToHost), "dbg D2H");
         if (grid) *grid = pool->lc.grid;
     });

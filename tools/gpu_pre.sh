@@ -1,1 +1,2 @@
-timeout 1200 python -m pytest tests -m gpu -x -q --timeout 300 2>&1 | tail -5
+timeout 1500 python -m pytest tests -m gpu -q --timeout 300 2>&1 | tail -4
+timeout 600 python bench.py --no-cpu-baseline 2>&1 | tail -1
