@@ -212,8 +212,16 @@ typedef struct cs_engine_result {
     int64_t scan_launches;    /* admission launches that ran at least one scan pass */
     int64_t h2d_bytes, d2h_bytes; /* host<->device bytes moved by admissions (host_inputs=1) */
     int64_t gpu_launches;         /* kernels launched by the engine so far */
+    int64_t warmup_prompt_tokens; /* EngineSim::warmup_prompt_tokens_ (engine.cpp:222) */
 } cs_engine_result;
 int cs_engine_result_get(cs_engine_t e, cs_engine_result* out);
+/* An engine over an explicit trace (turns7 rows as cs_generate_trace writes them, e.g. a trace
+ * read back from JSONL, trace_io.cpp:87-136); the spec supplies agents, template, budget and
+ * concurrency. run_cell (experiment.cpp:355-379) for a given Trace. */
+int cs_engine_create_from_turns(const cs_engine_cfg* cfg, const cs_workload_spec* spec, const int64_t* turns7,
+                                int64_t n_turns, cs_engine_t* out);
+/* per-turn arrival time (simulated us), TurnMetrics::arrival_us (engine.cpp:316) */
+int cs_engine_turn_arrivals(cs_engine_t e, double* arrival_us, int64_t cap);
 /* per-turn (by turn id) cached/prompt tokens and start/end simulated us; any may be NULL */
 int cs_engine_turns(cs_engine_t e, int64_t* cached, int64_t* prompt, double* start_us, double* end_us,
                     int64_t cap);

@@ -14,6 +14,7 @@
 // Nothing here re-implements reference logic; it only marshals arguments.
 
 #include <chrono>
+#include <sstream>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
@@ -24,6 +25,7 @@
 #include "cachesage/baselines.hpp"
 #include "cachesage/cachesage_policy.hpp"
 #include "cachesage/engine.hpp"
+#include "cachesage/experiment.hpp"
 #include "cachesage/hashing.hpp"
 #include "cachesage/reachability.hpp"
 #include "cachesage/runtime.hpp"
@@ -489,6 +491,54 @@ long ref_learner_eval(long n, const unsigned long long* a, const unsigned long l
         if (k >= 0)
             for (long i = 0; i < A; ++i) surv[i] = oracle::exact_survival_prob(al[i], k, l, AgentId{current});
         return A;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
+// The reference's Python surface (py_module.cpp:134-183): generate_trace(preset, sessions, seed)
+// -> Trace.to_jsonl(), and run_sim(read_trace_jsonl(text), policy, budget, concurrency,
+// block_size, prefetch) -> its metrics. Marshalling only.
+long ref_preset_trace_jsonl(const char* preset, int sessions, long long seed, char* buf, long cap) {
+    try {
+        WorkloadSpec spec = preset_by_name(preset);
+        if (sessions > 0) spec.sessions = sessions;
+        if (seed >= 0) spec.seed = (std::uint64_t)seed;
+        std::ostringstream out;
+        write_trace_jsonl(generate_trace(spec), out);
+        const std::string t = out.str();
+        if (buf && cap > 0) std::memcpy(buf, t.data(), std::min<long>(cap, (long)t.size()));
+        return (long)t.size();
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
+// out: hit_rate, mean_ttft_ms, mean_latency_ms, throughput_turns_per_s, sim_duration_ms, turns,
+// total_prompt_tokens, total_cached_tokens, evictions, truncated_admissions, warmups_executed,
+// warmup_prompt_tokens (metrics_to_py order, py_module.cpp:48-63)
+int ref_run_sim_jsonl(const char* jsonl, const char* policy, int budget, int concurrency, int block_size, int prefetch,
+                      double* out) {
+    try {
+        std::istringstream in(jsonl);
+        const Trace trace = read_trace_jsonl(in);
+        RunConfig config;
+        config.policies = {policy};
+        if (budget > 0) config.budget_blocks = budget;
+        if (concurrency > 0) config.concurrency = concurrency;
+        config.block_size = block_size;
+        config.prefetch = prefetch != 0;
+        const RunResult r = run_cell(trace, policy, config);
+        const RunMetrics& m = r.aggregate;
+        const double v[12] = {m.hit_rate, m.mean_ttft_us / 1000.0, m.mean_latency_us / 1000.0,
+                              m.throughput_turns_per_s, m.sim_duration_us / 1000.0, (double)m.turns,
+                              (double)m.total_prompt_tokens, (double)m.total_cached_tokens, (double)m.evictions,
+                              (double)m.truncated_admissions, (double)m.warmups_executed,
+                              (double)m.warmup_prompt_tokens};
+        std::memcpy(out, v, sizeof(v));
+        return 0;
     } catch (const std::exception& e) {
         g_err = e.what();
         return -1;

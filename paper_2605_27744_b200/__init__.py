@@ -7,12 +7,14 @@ package is the Python mirror of the reference's API over that ABI. No CPU fallba
 from . import workloads
 from ._lib import CacheSageError, lib
 from .api import (Engine, Pool, TransitionLearner, block_keys_for, chain_hash, derive_agent_identity,
-                  derive_agent_identity_of_prompt, exact_survival_prob, generate_trace, hash_prompts, run_sim)
+                  derive_agent_identity_of_prompt, exact_survival_prob, generate_trace_rows, hash_prompts, run_sim_spec)
+from .trace import Trace, generate_trace, read_trace_jsonl, run_sim
 from .workloads import preset_by_name, preset_names, preset_workloads
 
 __all__ = [
     "CacheSageError", "Engine", "Pool", "TransitionLearner", "block_keys_for", "chain_hash", "derive_agent_identity",
-    "derive_agent_identity_of_prompt", "exact_survival_prob",
+    "derive_agent_identity_of_prompt", "exact_survival_prob", "Trace", "read_trace_jsonl", "generate_trace_rows",
+    "run_sim_spec",
     "generate_trace", "hash_prompts", "lib", "preset_by_name", "preset_names", "preset_workloads", "run_sim",
     "workloads",
 ]

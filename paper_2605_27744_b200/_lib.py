@@ -69,7 +69,7 @@ class EngineResult(C.Structure):
         ("steps", C.c_int64), ("admissions", C.c_int64), ("scans", C.c_int64),
         ("scanned_slots", C.c_int64), ("tick", C.c_uint64), ("scan_ms", C.c_double),
         ("admit_ms", C.c_double), ("scan_launches", C.c_int64), ("h2d_bytes", C.c_int64),
-        ("d2h_bytes", C.c_int64), ("gpu_launches", C.c_int64),
+        ("d2h_bytes", C.c_int64), ("gpu_launches", C.c_int64), ("warmup_prompt_tokens", C.c_int64),
     ]
 
 
@@ -129,6 +129,9 @@ SIGNATURES = {
                                     C.POINTER(C.c_int)]),
     "cs_exact_survival_prob": (C.c_int, [vp, C.c_uint64, C.c_int, C.c_uint64, C.POINTER(C.c_double)]),
     "cs_chain_hash": (C.c_int, [vp, vp, vp, vp, C.c_int, vp]),
+    "cs_engine_create_from_turns": (C.c_int, [C.POINTER(EngineCfg), C.POINTER(WorkloadSpec), vp, C.c_int64,
+                                              C.POINTER(vp)]),
+    "cs_engine_turn_arrivals": (C.c_int, [vp, vp, C.c_int64]),
     "cs_derive_agent_identity": (C.c_int, [vp, vp, C.c_int, C.c_int, C.c_int, vp]),
     "cs_last_error": (C.c_char_p, []),
     "cs_version": (C.c_char_p, []),

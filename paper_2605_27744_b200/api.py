@@ -300,9 +300,9 @@ def spec_struct(spec):
     return s
 
 
-def generate_trace(spec):
+def generate_trace_rows(spec):
     """generate_trace (workload.cpp:156-182): rows (session, turn, agent, anchor, history,
-    prompt, decode). Host code (no GPU needed)."""
+    prompt, decode). Host code (no GPU needed). The reference's Trace API: trace.generate_trace."""
     s = spec_struct(spec)
     n = check(lib().cs_generate_trace(C.byref(s), None, 0))
     out = np.zeros((max(n, 1), 7), np.int64)
@@ -421,8 +421,9 @@ class Engine:
         return st[:n], tg[:n], tk[:n]
 
 
-def run_sim(spec, policy="cachesage", budget=None, concurrency=None, block_size=16, prefetch=True, **kw):
-    """py_module.cpp run_sim: one (trace, policy) simulation; aggregate metrics dict."""
+def run_sim_spec(spec, policy="cachesage", budget=None, concurrency=None, block_size=16, prefetch=True, **kw):
+    """One (spec, policy) simulation; the engine's own result dict (see trace.run_sim for the
+    reference's metrics dict)."""
     if isinstance(spec, str):
         spec = workloads.preset_by_name(spec)
     eng = Engine(spec, policy=policy, budget=budget, concurrency=concurrency, block_size=block_size,

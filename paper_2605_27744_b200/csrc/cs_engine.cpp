@@ -230,12 +230,14 @@ struct cs_engine {
         return a.end_us > b.end_us || (a.end_us == b.end_us && a.seq > b.seq);
     }
 
-    void build(const cs_engine_cfg& c, const cs_workload_spec* ws, long long shard_slots = 0, cs_comm* comm = nullptr);
+    void build(const cs_engine_cfg& c, const cs_workload_spec* ws, long long shard_slots = 0, cs_comm* comm = nullptr,
+               const int64_t* turns7 = nullptr, int64_t n_turns = -1);
+    int64_t warm_prompt = 0;  // EngineSim::warmup_prompt_tokens_ (engine.cpp:222)
     // device-resident scheduler (cs_engine_dev.cuh): whole steps in one persistent launch
     bool dev = false;
     csb::EngState hs{};  // authoritative between launches
-    csb::DevBuf d_state, d_reqs, d_soff, d_sreqs, d_spos, d_cat, d_tc, d_tp, d_ts, d_te, d_td, d_ws, d_wt, d_wk,
-        d_args, d_cmd;
+    csb::DevBuf d_state, d_reqs, d_soff, d_sreqs, d_spos, d_cat, d_tc, d_tp, d_ts, d_te, d_td, d_ta, d_ws, d_wt,
+        d_wk, d_args, d_cmd;
     long long w_cap = 0;
     void dev_setup();
     void dev_run(long long stop_at, long long max_steps);
@@ -257,7 +259,8 @@ struct cs_engine {
     void step();
 };
 
-void cs_engine::build(const cs_engine_cfg& c, const cs_workload_spec* ws, long long shard_slots, cs_comm* comm) {
+void cs_engine::build(const cs_engine_cfg& c, const cs_workload_spec* ws, long long shard_slots, cs_comm* comm,
+                      const int64_t* turns7, int64_t n_turns) {
     cfg = c;
     spec = to_spec(ws);
     bs = c.block_size;
@@ -267,7 +270,19 @@ void cs_engine::build(const cs_engine_cfg& c, const cs_workload_spec* ws, long l
     conc = c.concurrency > 0 ? c.concurrency : spec.concurrency;
     if (budget < 1 || conc < 1) throw std::invalid_argument("EngineSim: budget, block size, and concurrency must be positive");
 
-    const std::vector<Turn> turns = generate(spec);
+    // the spec's generated trace, or an explicit one (a trace read back from JSONL, run_sim)
+    std::vector<Turn> turns;
+    if (turns7) {
+        turns.resize(n_turns);
+        for (int64_t i = 0; i < n_turns; ++i) {
+            std::memcpy(turns[i].v, turns7 + 7 * i, sizeof(turns[i].v));
+            if (turns[i].v[2] < 0 || turns[i].v[2] >= spec.n_agents)
+                throw std::invalid_argument("trace: agent index out of range");
+            if (turns[i].v[5] <= 0) throw std::invalid_argument("trace: prompt must be non-empty");
+        }
+    } else {
+        turns = generate(spec);
+    }
     const int64_t nt = (int64_t)turns.size();
     // materialize_requests on the device: K1 over synthesised token ids
     std::vector<csb::TurnDesc> desc(nt + spec.n_agents);
@@ -444,6 +459,7 @@ void cs_engine::dev_setup() {
     d_ts.ensure(8 * std::max<int64_t>(nt, 1));
     d_te.ensure(8 * std::max<int64_t>(nt, 1));
     d_td.ensure(std::max<int64_t>(nt, 1));
+    d_ta.ensure(8 * std::max<int64_t>(nt, 1));
     ck(cudaMemset(d_td.p, 0, std::max<int64_t>(nt, 1)), "memset");
     d_ws.ensure(8 * w_cap);
     d_wt.ensure(8 * w_cap);
@@ -487,6 +503,7 @@ void cs_engine::dev_run(long long stop_at, long long max_steps) {
     E.t_start = d_ts.as<double>();
     E.t_end = d_te.as<double>();
     E.t_done = d_td.as<unsigned char>();
+    E.t_arrival = d_ta.as<double>();
     E.w_step = d_ws.as<long long>();
     E.w_target = d_wt.as<unsigned long long>();
     E.w_tick = d_wk.as<unsigned long long>();
@@ -545,6 +562,7 @@ void cs_engine::dev_pull_outputs() {
         ck(cudaMemcpy(t_start.data(), d_ts.p, 8 * nt, cudaMemcpyDeviceToHost), "D2H");
         ck(cudaMemcpy(t_end.data(), d_te.p, 8 * nt, cudaMemcpyDeviceToHost), "D2H");
         ck(cudaMemcpy(t_done.data(), d_td.p, nt, cudaMemcpyDeviceToHost), "D2H");
+        ck(cudaMemcpy(arrival_us.data(), d_ta.p, 8 * nt, cudaMemcpyDeviceToHost), "D2H");
     }
     const long long nw = hs.n_warm;
     w_step.resize(nw);
@@ -704,6 +722,7 @@ void cs_engine::execute_warmup(int target) {
     ++admissions;
     tick = st.tick_after;
     ++warm_exec;
+    warm_prompt += c.prompt_tokens;
     fetch_victims(ev_before);
 }
 
@@ -782,6 +801,35 @@ int cs_engine_create(const cs_engine_cfg* cfg, const cs_workload_spec* spec, cs_
             throw;
         }
         *out = e;
+    });
+}
+
+int cs_engine_create_from_turns(const cs_engine_cfg* cfg, const cs_workload_spec* spec, const int64_t* turns7,
+                                int64_t n_turns, cs_engine_t* out) {
+    return eguard([&] {
+        if (!cfg || !spec || !out || n_turns < 0 || (n_turns > 0 && !turns7))
+            throw std::invalid_argument("cs_engine_create_from_turns: null argument");
+        auto* e = new cs_engine();
+        try {
+            e->build(*cfg, spec, 0, nullptr, turns7, n_turns);
+        } catch (...) {
+            if (e->pool) {
+                e->pool->destroy();
+                delete e->pool;
+            }
+            delete e;
+            throw;
+        }
+        *out = e;
+    });
+}
+
+int cs_engine_turn_arrivals(cs_engine_t e, double* arrival_us, int64_t cap) {
+    return eguard([&] {
+        if (!e) throw std::invalid_argument("cs_engine_turn_arrivals: null engine");
+        if (e->dev) e->dev_pull_outputs();
+        const int64_t n = std::min<int64_t>(cap, (int64_t)e->reqs.size());
+        for (int64_t i = 0; i < n && arrival_us; ++i) arrival_us[i] = e->arrival_us[i];
     });
 }
 
@@ -889,6 +937,7 @@ int cs_engine_result_get(cs_engine_t e, cs_engine_result* o) {
         o->h2d_bytes = e->h2d_bytes;
         o->d2h_bytes = e->d2h_bytes;
         o->gpu_launches = e->pool->launches;
+        o->warmup_prompt_tokens = e->dev ? e->hs.warm_prompt : e->warm_prompt;
     });
 }
 

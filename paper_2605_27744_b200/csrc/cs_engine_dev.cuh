@@ -45,6 +45,7 @@ __device__ EngFlight heap_pop(EngState& s) {
 }
 
 __device__ void eng_arrive(const EngDev& E, EngState& s, int idx) {  // cs_engine::arrive
+    E.t_arrival[idx] = s.sim_now;
     ++s.tick;  // emit(RequestArrival)
     s.ready[(s.ready_head + s.ready_n) % (kMaxConc + 1)] = idx;
     ++s.ready_n;
@@ -284,6 +285,7 @@ __device__ int eng_schedule(const DevPool& P, const EngDev& E, EngState& s, cons
             case kPhWarmResult: {
                 s.tick = A.tick;
                 ++s.warm_exec;
+                s.warm_prompt += E.cat[s.fx[s.warm_i]].prompt_tokens;
                 ++s.warm_i;
                 s.phase = kPhWarm;
                 break;

@@ -35,7 +35,8 @@ struct EngState {
     unsigned long long flight_seq, tick, seq;
     double sim_now;
     int last_dispatched;
-    long long completed, truncated, warm_exec, warm_drop, steps, admissions, tot_prompt, tot_cached, n_warm;
+    long long completed, truncated, warm_exec, warm_drop, steps, admissions, tot_prompt, tot_cached, n_warm,
+        warm_prompt;
     int poll_reset_pending;
     // the pool driver's bookkeeping (cs_pool::admit): deferred unpins, prescan reuse
     int n_unpin, unpin_slots;
@@ -68,6 +69,7 @@ struct EngDev {
     double* t_start;
     double* t_end;
     unsigned char* t_done;
+    double* t_arrival;
     long long* w_step;
     unsigned long long* w_target;
     unsigned long long* w_tick;

@@ -87,6 +87,10 @@ def lib():
         _lib.ref_learner_eval.restype = C.c_long
         _lib.ref_learner_eval.argtypes = [C.c_long, C.c_void_p, C.c_void_p, C.c_long, C.c_long, C.c_ulonglong,
                                           C.c_double, C.c_int, C.c_int] + [C.c_void_p] * 9
+        _lib.ref_preset_trace_jsonl.restype = C.c_long
+        _lib.ref_preset_trace_jsonl.argtypes = [C.c_char_p, C.c_int, C.c_longlong, C.c_char_p, C.c_long]
+        _lib.ref_run_sim_jsonl.restype = C.c_int
+        _lib.ref_run_sim_jsonl.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p]
         _lib.ref_evict_bench.restype = C.c_double
         _lib.ref_evict_bench.argtypes = [C.c_long, C.c_int, C.c_long, C.c_long, C.c_long, C.c_int,
                                          C.POINTER(C.c_double), C.POINTER(C.c_ulonglong)]
@@ -265,3 +269,32 @@ def learner_eval(pairs_a, pairs_b, window=1024, current=0, tau=0.01, e_max=8, k=
     return {"agents": [int(x) for x in ag[:n]], "prob": prob[:n * n].reshape(n, n), "totals": tot[:n],
             "state_bytes": int(sb[0]), "argmax": [(int(i), float(p)) if f else None for i, p, f in zip(ai[:n], ap[:n], af[:n])],
             "hops": hops[:n], "surv": surv[:n]}
+
+
+def preset_trace_jsonl(preset, sessions=None, seed=None):
+    """The reference's generate_trace(preset, sessions, seed).to_jsonl()."""
+    n = lib().ref_preset_trace_jsonl(preset.encode(), sessions or -1, -1 if seed is None else seed, None, 0)
+    if n < 0:
+        raise RuntimeError(_err())
+    buf = C.create_string_buffer(n)
+    lib().ref_preset_trace_jsonl(preset.encode(), sessions or -1, -1 if seed is None else seed, buf, n)
+    return buf.raw[:n].decode()
+
+
+METRIC_KEYS = ["hit_rate", "mean_ttft_ms", "mean_latency_ms", "throughput_turns_per_s", "sim_duration_ms", "turns",
+               "total_prompt_tokens", "total_cached_tokens", "evictions", "truncated_admissions", "warmups_executed",
+               "warmup_prompt_tokens"]
+
+
+def run_sim_jsonl(jsonl, policy="cachesage", budget=None, concurrency=None, block_size=16, prefetch=True):
+    """The reference's run_sim(read_trace_jsonl(jsonl), ...) metrics dict."""
+    import numpy as np
+
+    out = np.zeros(12, np.float64)
+    if lib().ref_run_sim_jsonl(jsonl.encode(), policy.encode(), budget or 0, concurrency or 0, block_size,
+                               1 if prefetch else 0, _ptr(out)) != 0:
+        raise RuntimeError(_err())
+    d = dict(zip(METRIC_KEYS, out.tolist()))
+    for k in METRIC_KEYS[5:]:
+        d[k] = int(d[k])
+    return d

@@ -62,7 +62,7 @@ def test_rank_partitions_generate_different_traces():
 
     a, _ = bench.rank_workload(30, 4096, 0)
     b, _ = bench.rank_workload(30, 4096, 1)
-    ta, tb = api.generate_trace(a), api.generate_trace(b)
+    ta, tb = api.generate_trace_rows(a), api.generate_trace_rows(b)
     assert not (ta.shape == tb.shape and np.array_equal(ta, tb))
 
 

@@ -126,7 +126,7 @@ def test_generator_matches_reference_golden():
     gens = json.load(open(os.path.join(ROOT, "tests", "golden", "generator.json")))
     import refshim
     for g in gens:
-        t = api.generate_trace(g["spec"])
+        t = api.generate_trace_rows(g["spec"])
         assert t.shape[0] == g["n"], g["name"]
         assert hex(refshim.fnv1a64(t.astype(np.uint64).reshape(-1))) == g["fnv"], g["name"]
 
@@ -136,11 +136,11 @@ def test_generator_rejects_bad_specs():
     s = dict(preset_by_name("supervisor-a"))
     s["turns_min"], s["turns_max"] = 5, 2
     with pytest.raises(ValueError):
-        api.generate_trace(s)
+        api.generate_trace_rows(s)
     s = dict(preset_by_name("supervisor-a"))
     s["transition"] = [[0.0] * len(s["anchor_tokens"])] * len(s["anchor_tokens"])
     with pytest.raises(ValueError):
-        api.generate_trace(s)
+        api.generate_trace_rows(s)
 
 
 def test_null_arguments_are_rejected():
@@ -160,4 +160,4 @@ def test_no_device_fails_loudly():
         api.hash_prompts([[1, 2, 3]])
     from paper_2605_27744_b200.workloads import preset_by_name
     with pytest.raises(_lib.CacheSageError):
-        api.run_sim(preset_by_name("supervisor-a"))
+        api.run_sim_spec(preset_by_name("supervisor-a"))
