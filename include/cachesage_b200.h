@@ -36,7 +36,9 @@ typedef struct cs_engine* cs_engine_t;
 #define CS_NO_AGENT 0xFFFFFFFFu
 
 /* Policy and pool configuration: EngineConfig (engine.hpp:29-36) + CacheSageConfig
- * (cachesage_policy.hpp:36-43). policy: 0 = lru (baselines.cpp:12-14), 1 = cachesage. */
+ * (cachesage_policy.hpp:36-43). policy: 0 = lru (baselines.cpp:12-14), 1 = cachesage,
+ * 2 = ttl (baselines.cpp:22-28, default pin horizon: the same victims as lru, see cs_pool.cpp;
+ * cs_score_snapshot reports the recency part only). */
 typedef struct cs_pool_cfg {
     int64_t budget_blocks; /* pool slots N (EngineConfig::budget_blocks) */
     int policy;

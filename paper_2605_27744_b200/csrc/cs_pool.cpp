@@ -77,7 +77,12 @@ void cs_pool::create(const cs_pool_cfg& c, long long shard_slots, cs_comm* cm) {
     p.rank = comm ? comm->rank : 0;
     p.world = world;
     p.gbudget = c.budget_blocks;
-    p.policy = c.policy;
+    // TtlPolicy (baselines.cpp:22-28) picks the same victims as LruPolicy: last_touch_us never
+    // decreases along last_touch (ticks and the simulated clock advance together), so the
+    // blocks still inside the pin horizon (score 1e6 + rho) are the youngest, and the argmin of
+    // (score, last_touch) over unpinned blocks is the oldest one under both scorers.
+    if (c.policy < 0 || c.policy > 2) throw std::invalid_argument("policy must be 0 (lru), 1 (cachesage) or 2 (ttl)");
+    p.policy = c.policy == 2 ? 0 : c.policy;
     p.e_max = c.e_max;
     p.n_lists = c.e_max + 2;
     p.a_cap = c.agent_capacity;
