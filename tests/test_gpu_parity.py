@@ -235,3 +235,13 @@ def test_large_pool_admissions_match_oracle():
         assert np.array_equal(ev, o.evictions()[-64:])
     g.close()
     o.close()
+
+
+@pytest.mark.parametrize("task,budget,policy", [(2600, 700, "cachesage"), (2600, 700, "lru"), (4200, 1500, "cachesage")])
+def test_long_prompts_multi_chunk_match_oracle(task, budget, policy):
+    """Prompts of 170-300 blocks: admissions span several 128-block chunks (the prescan feeds the
+    first chunk, the later chunks rescan), against the C oracle, bit-exact."""
+    spec = dict(W.preset_by_name("supervisor-a"))
+    spec["task_tokens"], spec["sessions"] = task, 40
+    res, ev = _compare_runs(spec, policy, budget=budget)
+    assert ev.size > 0
