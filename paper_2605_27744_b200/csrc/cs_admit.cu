@@ -164,7 +164,7 @@ struct EarlySmem {
     unsigned char U_ok[kXset];
     unsigned int tset[kTset];
     unsigned long long TE, TR, TP;
-    int nE, nR, nP, ok;
+    int nE, nR, nP, ok, valid;
 };
 constexpr size_t kEarlyOff = 64 * 1024;
 static_assert(sizeof(ReplaySmem) <= kEarlyOff, "replay view must stay below the early-validation view");
@@ -1223,7 +1223,7 @@ __device__ __forceinline__ unsigned long long next_hint(unsigned long long v1, u
 }
 
 __device__ void prescan_pass(const DevPool& P, const ScanBufs& B, ScanSmem& S, unsigned char* dsm, int par,
-                             const AdmitArgs* dbg_args) {
+                             bool after_writes) {
     Ctrl* C = P.ctrl;
     const int tid = threadIdx.x, T = blockDim.x;
     const long long TV = kTile;
@@ -1245,7 +1245,7 @@ __device__ void prescan_pass(const DevPool& P, const ScanBufs& B, ScanSmem& S, u
         P.dbg[blockIdx.x * 16 + 0] = gtimer();
     }
     __syncthreads();
-    fence_proxy_async_smem();
+    if (after_writes) fence_proxy_async_smem();  // pool slots written earlier in this launch
     // (the thresholds load while the first tiles are in flight) agent-carrying slots share E's
     // threshold: the E members among them are complete to it, and the other classes' lists are
     // only needed non-empty (see consume_prescan)
@@ -1561,8 +1561,9 @@ __device__ void prescan_finish(const DevPool& P, const AdmitArgs& a, const ScanB
         C->pre_cnt[par][0] = C->pre_cnt[par][1] = C->pre_cnt[par][2] = 0;
         C->pre_bad[par] = 0;
         C->pre_arrive[par] = 0u;  // every arrival happened before the wait above ended
-        __threadfence();
-        asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(&C->pl_seq[par]), "l"(a.seq) : "memory");
+        // the consumer is the next admission: a kernel boundary (or the engine kernel's grid
+        // barrier) orders these stores before its reads
+        C->pl_seq[par] = a.seq;
     }
 }
 
@@ -2511,9 +2512,9 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
     if (tid == 0) P.dbg[blockIdx.x * 16 + 9] = gtimer();  // kernel entry (instrumentation)
     const int par_prev = (int)((a.seq - 1ull) & 1ull), par_next = (int)(a.seq & 1ull);
     const bool pre_run = (a.flags & kPrescan) && gridDim.x >= 2;
-    const bool pre_avail = pre_run && (a.flags & kUsePrescan) &&
-                           *(volatile unsigned long long*)&C->pl_seq[par_prev] == a.seq - 1ull &&
-                           *(volatile int*)&C->pl_ok[par_prev] != 0;
+    // The host asks for the previous prescan's lists (kUsePrescan): the prescan CTAs start the
+    // next stream at once; CTA 0 checks the lists are there and usable (else it scans as before).
+    const bool pre_avail = pre_run && (a.flags & kUsePrescan);
     EarlySmem& es = *reinterpret_cast<EarlySmem*>(dsm + kOffRing + kEarlyOff);
 
     // ---- phase 0 (CTA 0): poll reset, probe, feasibility, dispatch, lookup
@@ -2538,7 +2539,9 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
             C->done = 0;
             C->error = 0;
             es.ok = 0;
-            if (pre_avail) {
+            es.valid = pre_avail && *(volatile unsigned long long*)&C->pl_seq[par_prev] == a.seq - 1ull &&
+                       *(volatile int*)&C->pl_ok[par_prev] != 0;
+            if (es.valid) {
                 es.nE = P.pl_n[par_prev * 3 + 0];
                 es.nR = P.pl_n[par_prev * 3 + 1];
                 es.nP = P.pl_n[par_prev * 3 + 2];
@@ -2754,7 +2757,7 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
     if (pre_avail) {
         if (blockIdx.x != 0) {
             const unsigned long long hE = __ldcg(P.pre_hint + 0), hR = __ldcg(P.pre_hint + 1), hP = hE;
-            prescan_pass(P, B, S, dsm, par_next, &a);
+            prescan_pass(P, B, S, dsm, par_next, P.stream_generic != 0);
             if (tid == 0) P.dbg[blockIdx.x * 16 + 2] = gtimer();
             prescan_finish(P, a, B, Sel, par_next, hE, hR, hP);
             if (tid == 0) {
@@ -2784,6 +2787,7 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
                 pstamp(P, 6);
                 const bool need0 = C->resident + Rp.absent > P.cap;
                 const bool ok = !need0 ? true
+                                : !es.valid ? false
                                 : es.ok ? consume_early(P, es, Rp, B, S, Red)
                                         : consume_prescan(P, a, B, S, Red, par_prev);
                 if (ok && need0 && es.ok && P.dbg_check) debug_check_e(P, es, Rp, B, S, a);
@@ -3014,7 +3018,7 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
     // ---- no usable prescan came in: CTAs 1.. now prescan for the next admission
     if (pre_run && !pre_avail && blockIdx.x != 0) {
         const unsigned long long hE = __ldcg(P.pre_hint + 0), hR = __ldcg(P.pre_hint + 1), hP = hE;
-        prescan_pass(P, B, S, dsm, par_next, &a);
+        prescan_pass(P, B, S, dsm, par_next, true);
         prescan_finish(P, a, B, Sel, par_next, hE, hR, hP);
         return;
     }
