@@ -187,6 +187,12 @@ struct cs_engine {
     // host_inputs: prompt blocks in pinned host memory, staged per admission
     uint64_t* h_keys = nullptr;
     int* h_counts = nullptr;
+    // host_inputs: per request one pinned blob [keys (8 nb) | counts (4 nb)] at byte 12 * blk_off,
+    // so an admission's inputs are ONE H2D copy; victims land in h_vict (pinned) by a D2H copy
+    // queued right behind the admission kernel (one stream sync for the whole admission)
+    unsigned char* h_blob = nullptr;
+    unsigned long long* h_vict = nullptr;
+    int h_vict_cap = 0;
     csb::DevBuf d_stage_keys, d_stage_counts;
     int64_t h2d_bytes = 0, d2h_bytes = 0;
     void stage(csb::AdmitArgs& a, int64_t blk_off, int nb);
@@ -389,6 +395,18 @@ void cs_engine::build(const cs_engine_cfg& c, const cs_workload_spec* ws, long l
         ck(cudaMallocHost(reinterpret_cast<void**>(&h_counts), 4 * total_blocks), "cudaMallocHost");
         ck(cudaMemcpy(h_keys, d_keys.p, 8 * total_blocks, cudaMemcpyDeviceToHost), "D2H");
         ck(cudaMemcpy(h_counts, d_counts.p, 4 * total_blocks, cudaMemcpyDeviceToHost), "D2H");
+        ck(cudaMallocHost(reinterpret_cast<void**>(&h_blob), 12 * std::max<int64_t>(total_blocks, 1)), "cudaMallocHost");
+        int max_nb = 1;
+        auto pack = [&](int64_t off, int nb) {
+            std::memcpy(h_blob + 12 * off, h_keys + off, 8 * (size_t)nb);
+            std::memcpy(h_blob + 12 * off + 8 * (size_t)nb, h_counts + off, 4 * (size_t)nb);
+            max_nb = std::max(max_nb, nb);
+        };
+        for (int64_t i = 0; i < nt; ++i) pack(desc[i].blk_off, (int)((turns[i].v[5] + bs - 1) / bs));
+        for (int ag = 0; ag < spec.n_agents; ++ag)
+            pack(desc[nt + ag].blk_off, (int)((spec.template_tokens + spec.anchor[ag] + 1 + bs - 1) / bs));
+        h_vict_cap = max_nb;
+        ck(cudaMallocHost(reinterpret_cast<void**>(&h_vict), 8 * (size_t)h_vict_cap), "cudaMallocHost");
         d_keys.release();
         d_counts.release();
     }
@@ -591,15 +609,15 @@ void cs_engine::stage(csb::AdmitArgs& a, int64_t blk_off, int nb) {
         a.counts = d_counts.as<int>() + blk_off;
         return;
     }
-    d_stage_keys.ensure(8 * (size_t)std::max(nb, 1));
-    d_stage_counts.ensure(4 * (size_t)std::max(nb, 1));
-    ck(cudaMemcpyAsync(d_stage_keys.p, h_keys + blk_off, 8 * (size_t)nb, cudaMemcpyHostToDevice, pool->stream),
-       "H2D");
-    ck(cudaMemcpyAsync(d_stage_counts.p, h_counts + blk_off, 4 * (size_t)nb, cudaMemcpyHostToDevice, pool->stream),
+    d_stage_keys.ensure(12 * (size_t)std::max(nb, 1));
+    ck(cudaMemcpyAsync(d_stage_keys.p, h_blob + 12 * blk_off, 12 * (size_t)nb, cudaMemcpyHostToDevice, pool->stream),
        "H2D");
     h2d_bytes += 12 * (int64_t)nb;
     a.keys = d_stage_keys.as<unsigned long long>();
-    a.counts = d_stage_counts.as<int>();
+    a.counts = reinterpret_cast<int*>(d_stage_keys.as<unsigned char>() + 8 * (size_t)nb);
+    // the victims (at most one per prompt block) come back behind the kernel, same stream
+    pool->vpref = h_vict;
+    pool->vpref_n = nb;
 }
 
 // host_inputs: the admission's result (victim keys) is read back immediately
@@ -611,13 +629,18 @@ void cs_engine::fetch_victims(unsigned long long before) {
     const unsigned long long tot = pool->ev_total;
     if (tot > ev_drained) {
         const size_t base = evictions.size();
-        evictions.resize(base + (tot - ev_drained));
-        pool->copy_victims(ev_drained, tot, evictions.data() + base);
-        d2h_bytes += 8 * (int64_t)(tot - ev_drained);
+        const unsigned long long n = tot - ev_drained;
+        evictions.resize(base + n);
+        if (ev_drained == before && n <= (unsigned long long)pool->vpref_done) {
+            std::memcpy(evictions.data() + base, h_vict, 8 * n);
+        } else {  // (not this admission's window alone: read the log)
+            pool->copy_victims(ev_drained, tot, evictions.data() + base);
+            d2h_bytes += 8 * (int64_t)n;
+        }
         ev_drained = tot;
     }
+    pool->vpref_done = 0;
     d2h_bytes += (int64_t)sizeof(csb::AdmitStatus);  // the mapped status record
-    (void)before;
 }
 
 void cs_engine::arrive(int64_t idx) {
@@ -654,6 +677,7 @@ bool cs_engine::try_start_head() {
     a.pins_out = d_pins.as<unsigned int>() + r.blk_off;
     const unsigned long long ev_before = pool->ev_total;
     const csb::AdmitStatus& st = pool->admit(a, r.nb);
+    d2h_bytes += 8 * (int64_t)pool->vpref_done;  // the victim window copied behind the kernel
     ++admissions;
     if (cfg.host_inputs) d2h_bytes += (int64_t)sizeof(csb::AdmitStatus);
     if (!st.started) return false;  // wait for in-flight pins to clear
@@ -719,6 +743,7 @@ void cs_engine::execute_warmup(int target) {
     a.pins_out = d_pins.as<unsigned int>() + c.blk_off;
     const unsigned long long ev_before = pool->ev_total;
     const csb::AdmitStatus& st = pool->admit(a, c.nb);
+    d2h_bytes += 8 * (int64_t)pool->vpref_done;
     ++admissions;
     tick = st.tick_after;
     ++warm_exec;
@@ -861,6 +886,8 @@ int cs_engine_destroy(cs_engine_t e) {
         e->d_stage_keys.release();
         e->d_stage_counts.release();
         if (e->h_keys) cudaFreeHost(e->h_keys);
+        if (e->h_blob) cudaFreeHost(e->h_blob);
+        if (e->h_vict) cudaFreeHost(e->h_vict);
         if (e->h_counts) cudaFreeHost(e->h_counts);
         if (e->pool) {
             e->pool->destroy();

@@ -380,6 +380,17 @@ const csb::AdmitStatus& cs_pool::admit(const csb::AdmitArgs& in, int n_for_grid)
     ck(csb::launch_admit(P, a, lc, grid, stream), "admit_kernel launch");
     ++launches;
     if (timing) ck(cudaEventRecord(ev1, stream), "cudaEventRecord");
+    vpref_done = 0;
+    if (vpref && vpref_n > 0) {  // this admission's victims (<= one per block) behind the kernel
+        const unsigned long long cap = (unsigned long long)P.evlog_cap, off = ev_total % cap;
+        const unsigned long long n1 = std::min<unsigned long long>((unsigned long long)vpref_n, cap - off);
+        ck(cudaMemcpyAsync(vpref, P.evlog + off, 8 * n1, cudaMemcpyDeviceToHost, stream), "victims D2H");
+        if (n1 < (unsigned long long)vpref_n)
+            ck(cudaMemcpyAsync(vpref + n1, P.evlog, 8 * (vpref_n - n1), cudaMemcpyDeviceToHost, stream), "victims D2H");
+        vpref_done = vpref_n;
+    }
+    vpref = nullptr;
+    vpref_n = 0;
     ck(cudaStreamSynchronize(stream), "admit_kernel");
     poll_reset_pending = false;
     const long long scans_before = scans_total;

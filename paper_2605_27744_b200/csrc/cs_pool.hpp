@@ -81,6 +81,10 @@ struct cs_pool {
     // prescan: every cooperative launch streams the pool for the NEXT admission (kPrescan); the
     // next launch may use those lists (kUsePrescan) unless the pool changed out of band since
     bool prescan = true;
+    // the next admission's victims land here (pinned) by a D2H copy queued behind the kernel:
+    // vpref_n log entries from the pre-admission log end; vpref_done = entries copied
+    unsigned long long* vpref = nullptr;
+    int vpref_n = 0, vpref_done = 0;
     bool pre_ok = false;
     std::vector<std::pair<const unsigned int*, int>> prev_ranges;  // slots the last launch unpinned
     int prev_slots = 0;

@@ -119,3 +119,32 @@ def test_policy_trace_golden_on_device(p):
             assert got[int(kk)] == want
     finally:
         pool.close()
+
+
+HOST_INPUT_RUNS = [g for g in RUNS if g["name"] in ("supervisor-a", "synthetic-chain", "cfg1@128", "oversized-mixed",
+                                                    "supervisor-a-conc8", "pins-defer")]
+
+
+@pytest.mark.parametrize("g", HOST_INPUT_RUNS, ids=[g["name"] + "-" + g["kw"]["policy"] for g in HOST_INPUT_RUNS])
+def test_engine_host_inputs_golden(g):
+    """The end-to-end path bench.py times (prompt blocks H2D per admission from pinned memory,
+    the victims D2H behind each admission kernel) gives the reference's run bit-exactly."""
+    from paper_2605_27744_b200 import api
+
+    kw = dict(g["kw"])
+    ekw = {k: kw.pop(k) for k in list(kw) if k in ENGINE_KW}
+    pol = kw.pop("policy")
+    eng = api.Engine(g["spec"], policy=pol, agent_capacity=1024, host_inputs=True, **ekw, **kw)
+    try:
+        res = eng.run()
+        t = eng.turns()
+        ev = eng.evictions()
+        ws, wt, wk = eng.warmups()
+        r = eng.result()
+    finally:
+        eng.close()
+    assert repr(res["hit_rate"]) == g["hit_rate"]
+    assert fnv(ev) == g["evictions_fnv"]
+    assert fnv(t["cached_tokens"]) == g["cached_fnv"]
+    assert fnv(wt) == g["warmups_fnv"]
+    assert r["h2d_bytes"] > 0 and r["d2h_bytes"] > 0
