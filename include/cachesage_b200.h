@@ -38,7 +38,9 @@ typedef struct cs_engine* cs_engine_t;
 /* Policy and pool configuration: EngineConfig (engine.hpp:29-36) + CacheSageConfig
  * (cachesage_policy.hpp:36-43). policy: 0 = lru (baselines.cpp:12-14), 1 = cachesage,
  * 2 = ttl (baselines.cpp:22-28, default pin horizon: the same victims as lru, see cs_pool.cpp;
- * cs_score_snapshot reports the recency part only). */
+ * cs_score_snapshot reports the recency part only), 3 = belady (baselines.cpp:34-70: needs the
+ * request stream, so only engines run it — cs_engine_create*; admissions on a bare pool fail
+ * with CS_ERR_INVALID_ARGUMENT; not with a hash-sharded pool). */
 typedef struct cs_pool_cfg {
     int64_t budget_blocks; /* pool slots N (EngineConfig::budget_blocks) */
     int policy;

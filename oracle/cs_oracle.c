@@ -231,6 +231,13 @@ typedef struct {
     uint64_t* pend_tick;
     long n_pend, pend_cap;
     uint64_t rebuilds;
+    /* BeladyPolicy (baselines.cpp:34-46): every request block as (key, request id, chain
+     * position), sorted, and the cursor (highest arrived request id, :48-52) */
+    uint64_t* bel_key;
+    uint64_t* bel_req;
+    int* bel_pos;
+    long bel_n;
+    uint64_t cursor;
 } policy;
 
 /* TransitionLearner::record, transition_learner.cpp:22-51 (note_agent :16-20 is the alphabet,
@@ -307,7 +314,7 @@ static int argmax_row(const policy* p, long a, long* best, double* prob) {
 /* CacheSagePolicy::observe(AgentDispatch), cachesage_policy.cpp:57-72, with maybe_prefetch
  * :109-123. LRU (baselines.cpp:10) observes nothing. */
 static void observe_dispatch(policy* p, long prev, long next, uint64_t tick) {
-    if (p->cfg.policy == 0) return;
+    if (p->cfg.policy != 1) return; /* LruPolicy / TtlPolicy / BeladyPolicy ignore dispatches */
     if (prev >= 0) learner_record(p, prev, next);
     const int changed = p->current < 0 || p->current != next;
     p->current = next;
@@ -344,6 +351,27 @@ static double recency(uint64_t lt, uint64_t now, uint64_t old) {
 
 /* CacheSagePolicy::score, cachesage_policy.cpp:79-85 (+ ReachabilityState::survival,
  * reachability.cpp:12-20); LruPolicy::score, baselines.cpp:12-14 */
+/* BeladyPolicy::score, baselines.cpp:54-70 */
+static double belady_score(const policy* p, uint64_t key) {
+    long lo = 0, hi = p->bel_n;
+    while (lo < hi) { /* first entry of the key */
+        long m = (lo + hi) / 2;
+        if (p->bel_key[m] < key) lo = m + 1;
+        else hi = m;
+    }
+    if (lo == p->bel_n || p->bel_key[lo] != key) return 0.0;
+    const int depth = p->bel_pos[lo]; /* depth_.emplace: the first occurrence */
+    long j = lo, e = p->bel_n;
+    while (j < e) { /* std::upper_bound of the cursor in the key's request ids (:60) */
+        long m = (j + e) / 2;
+        if (p->bel_key[m] < key || (p->bel_key[m] == key && p->bel_req[m] <= p->cursor)) j = m + 1;
+        else e = m;
+    }
+    if (j == p->bel_n || p->bel_key[j] != key) return 0.0; /* never referenced again */
+    const double nudge = 1e-10 * (double)depth;
+    return 1.0 / (1.0 + (double)(p->bel_req[j] - p->cursor)) - nudge;
+}
+
 static double score(const policy* p, long agent, uint64_t lt, uint64_t now, uint64_t old) {
     const double rho = recency(lt, now, old);
     if (p->cfg.policy == 0) return rho;
@@ -466,6 +494,9 @@ void cso_engine_free(cso_engine* e) {
     free(e->pol.hops);
     free(e->pol.pend_target);
     free(e->pol.pend_tick);
+    free(e->pol.bel_key);
+    free(e->pol.bel_req);
+    free(e->pol.bel_pos);
     free(e);
 }
 
@@ -487,7 +518,15 @@ static int evict_one(cso_engine* e) {
     for (long i = 0; i < e->n_ent_cap; ++i) {
         const entry* x = &e->ent[i];
         if (!x->used || x->refs > 0) continue;
-        const double s = score(&e->pol, x->agent, x->lt, e->tick, old);
+        double s;
+        if (e->pol.cfg.policy == 3) {
+            s = belady_score(&e->pol, x->key);
+        } else if (e->pol.cfg.policy == 2) { /* TtlPolicy::score, baselines.cpp:22-28 */
+            const double rho = recency(x->lt, e->tick, old);
+            s = e->sim_now - x->lt_us < 5000000.0 ? 1.0e6 + rho : rho;
+        } else {
+            s = score(&e->pol, x->agent, x->lt, e->tick, old);
+        }
         if (v < 0 || s < vs ||
             (s == vs && (x->lt < e->ent[v].lt || (x->lt == e->ent[v].lt && x->key < e->ent[v].key)))) {
             v = i;
@@ -718,6 +757,19 @@ static void push_u64(uint64_t** a, long* n, long* cap, uint64_t v) {
     (*a)[(*n)++] = v;
 }
 
+typedef struct {
+    uint64_t key, req;
+    int pos;
+} bel_t;
+
+static int bel_cmp(const void* x, const void* y) {
+    const bel_t* a = (const bel_t*)x;
+    const bel_t* b = (const bel_t*)y;
+    if (a->key != b->key) return a->key < b->key ? -1 : 1;
+    if (a->req != b->req) return a->req < b->req ? -1 : 1;
+    return a->pos < b->pos ? -1 : a->pos > b->pos;
+}
+
 /* run_cell (experiment.cpp:355-379) -> EngineSim::run (engine.cpp:415-421): load (:240-255),
  * step (:372-392), activate/arrive (:262-276), try_start_head (:325-351), start_request
  * (:278-323), complete_earliest (:353-370), drain_and_run_warmups/execute_warmup (:197-238). */
@@ -787,6 +839,31 @@ int cso_run(const cso_spec* s, const cso_cfg* cfg_in, cso_run_out* out) {
         free(tmp.tab);
     }
     cso_engine* e = cso_engine_new(&cfg, distinct + 1);
+    if (cfg.policy == 3) {
+        long nb = 0;
+        for (long i = 0; i < nt; ++i) nb += rq[i].nb;
+        bel_t* t = (bel_t*)malloc(sizeof(bel_t) * (size_t)(nb > 0 ? nb : 1));
+        long k = 0;
+        for (long i = 0; i < nt; ++i)
+            for (long b = 0; b < rq[i].nb; ++b) {
+                t[k].key = rq[i].keys[b];
+                t[k].req = (uint64_t)i;
+                t[k].pos = (int)b;
+                ++k;
+            }
+        qsort(t, (size_t)nb, sizeof(bel_t), bel_cmp);
+        policy* p = &e->pol;
+        p->bel_n = nb;
+        p->bel_key = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)(nb > 0 ? nb : 1));
+        p->bel_req = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)(nb > 0 ? nb : 1));
+        p->bel_pos = (int*)malloc(sizeof(int) * (size_t)(nb > 0 ? nb : 1));
+        for (long i = 0; i < nb; ++i) {
+            p->bel_key[i] = t[i].key;
+            p->bel_req[i] = t[i].req;
+            p->bel_pos[i] = t[i].pos;
+        }
+        free(t);
+    }
 
     /* sessions ascending (std::map order); requests per session in trace order */
     int max_sess = 0;
@@ -836,7 +913,8 @@ int cso_run(const cso_spec* s, const cso_cfg* cfg_in, cso_run_out* out) {
             sess_pos[sid] = 0;
             long idx = sess_req[sess_cnt[sid]];
             arrival[idx] = e->sim_now;
-            ++e->tick; /* RequestArrival: note_agent only */
+            ++e->tick; /* RequestArrival: note_agent only; BeladyPolicy::observe moves the cursor */
+            if ((uint64_t)idx > e->pol.cursor) e->pol.cursor = (uint64_t)idx;
             agent_index(e, rq[idx].agent);
             ready[rd_tail++] = idx;
         }
@@ -897,6 +975,7 @@ int cso_run(const cso_spec* s, const cso_cfg* cfg_in, cso_run_out* out) {
                     long nx = sess_req[sess_cnt[sid] + sess_pos[sid]];
                     arrival[nx] = e->sim_now;
                     ++e->tick;
+                    if ((uint64_t)nx > e->pol.cursor) e->pol.cursor = (uint64_t)nx;
                     agent_index(e, rq[nx].agent);
                     ready[rd_tail++] = nx;
                 } else {

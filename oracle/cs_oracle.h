@@ -36,7 +36,7 @@ typedef struct cso_spec {
 
 /* RunConfig subset + CacheSageConfig (experiment.hpp:28-44, cachesage_policy.hpp:17-43). */
 typedef struct cso_cfg {
-    int policy; /* 0 = lru, 1 = cachesage */
+    int policy; /* 0 = lru, 1 = cachesage, 2 = ttl, 3 = belady (cso_run only) */
     int budget_blocks, concurrency, block_size, prefetch;
     int skip, take;
     double tau;

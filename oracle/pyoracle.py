@@ -187,7 +187,7 @@ def turn_tokens(spec, turn7):
     return out[:n]
 
 
-POLICY_IDS = {"lru": 0, "cachesage": 1}
+POLICY_IDS = {"lru": 0, "cachesage": 1, "ttl": 2, "belady": 3}
 
 
 def cfg_struct(policy="cachesage", budget=None, concurrency=None, block_size=16, prefetch=True,

@@ -84,7 +84,7 @@ typedef struct ref_spec {
 } ref_spec;
 
 typedef struct ref_run_cfg {
-    int policy;  // 0 = lru, 1 = cachesage, 2 = ttl
+    int policy;  // 0 = lru, 1 = cachesage, 2 = ttl, 3 = belady
     int budget_blocks;  // <= 0: the spec's pairing
     int concurrency;    // <= 0: the spec's pairing
     int block_size;
@@ -284,6 +284,8 @@ int ref_run(const ref_spec* s, const ref_run_cfg* c, ref_run_out* out) {
             rec->inner = std::make_shared<LruPolicy>();
         } else if (c->policy == 2) {
             rec->inner = std::make_shared<TtlPolicy>();
+        } else if (c->policy == 3) {
+            rec->inner = std::make_shared<BeladyPolicy>(requests);
         } else {
             rec->inner = std::make_shared<CacheSagePolicy>(to_cs_cfg(c));
         }

@@ -14,7 +14,7 @@ from . import workloads
 from ._lib import (CS_NO_AGENT, EngineCfg, EngineResult, PoolCfg, PoolStats, WorkloadSpec, check,
                    lib)
 
-POLICIES = {"lru": 0, "cachesage": 1, "ttl": 2}
+POLICIES = {"lru": 0, "cachesage": 1, "ttl": 2, "belady": 3}
 
 
 def _p(a):

@@ -18,7 +18,7 @@ LIB = os.path.join(HERE, "libcachesage_b200.so")
 
 NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-DEVICE_SRCS = ["cs_kernels.cu", "cs_admit.cu", "cs_learner.cu"]
+DEVICE_SRCS = ["cs_kernels.cu", "cs_admit.cu", "cs_learner.cu", "cs_belady.cu"]
 HOST_SRCS = ["cs_pool.cpp", "cs_engine.cpp", "cs_comm.cpp"]
 DEPS = DEVICE_SRCS + HOST_SRCS + ["cs_device.cuh", "cs_launch.h", "cs_pool.hpp"]
 
@@ -39,7 +39,7 @@ def _stale(target, sources):
 def build(verbose: bool = False, force: bool = False) -> str:
     os.makedirs(OUT_DIR, exist_ok=True)
     inc = ["-I", os.path.join(ROOT, "include"), "-I", CSRC]
-    header_deps = [os.path.join(CSRC, h) for h in ("cs_device.cuh", "cs_launch.h", "cs_pool.hpp", "cs_block.cuh", "cs_shard.cuh", "cs_comm.hpp", "cs_engine_state.h", "cs_engine_dev.cuh")]
+    header_deps = [os.path.join(CSRC, h) for h in ("cs_device.cuh", "cs_launch.h", "cs_pool.hpp", "cs_block.cuh", "cs_shard.cuh", "cs_comm.hpp", "cs_engine_state.h", "cs_engine_dev.cuh", "cs_belady.cuh")]
     header_deps.append(os.path.join(ROOT, "include", "cachesage_b200.h"))
     objs = []
     for src in DEVICE_SRCS:

@@ -3076,6 +3076,10 @@ __global__ void __launch_bounds__(kThreads + 32, 1) admit_kernel(DevPool P, Admi
 
 #include "cs_shard.cuh"
 
+// ------------------------------------------------------------------ Belady baseline (policy 3)
+
+#include "cs_belady.cuh"
+
 // ------------------------------------------------------------------ device-resident scheduler
 
 #include "cs_engine_dev.cuh"

@@ -134,10 +134,35 @@ struct ShardState {
     int started, error, first_miss, admit_n, anchor, needed, warm_issued, chunk, need_scan, scans;
 };
 
+// ---------------------------------------------------------------- Belady (policy 3)
+// BeladyPolicy (baselines.cpp:34-70): a block's score depends on the next request that
+// references it, so the pool keeps per slot that request id (kNoRef: never again) and the key's
+// index into a CSR of request ids per unique key, built once from the materialized requests.
+constexpr unsigned int kNoRef = 0xFFFFFFFFu;
+constexpr int kBelCand = 4096;   // candidates one selection pass hands to the replay
+constexpr int kBelPasses = 16;   // 8-bit digits of the (score, last_touch) composite
+
+struct BelCand {
+    unsigned long long hi, lo;  // order-preserving score bits, last_touch
+    unsigned int slot, pad;
+};
+
+struct BelCtl {
+    unsigned long long hi_or, hi_and, lo_or, lo_and;  // over this pass's candidates
+    unsigned long long m;                             // candidates (resident, unpinned)
+    int n_cand;                                       // compacted
+    int pos;                                          // next prompt block of the replay
+    int more;                                         // 1: the replay needs another pass
+    int started, error, first_miss, admit_n, anchor, needed, scans;
+    long long cached, n_ev_adm;
+    unsigned long long tick;                          // before admit_pinned's touches
+    unsigned int hist[kBelPasses][256];
+};
+
 struct DevPool {
     long long cap;            // slots == EngineConfig::budget_blocks
     long long cap_scan;       // cap rounded up to 64: the SoA tail is padded with free slots
-    int policy;               // 0 lru, 1 cachesage
+    int policy;               // 0 lru, 1 cachesage, 3 belady
     int e_max;
     int n_lists;              // e_max + 2 (classes 0..e_max, resident list last)
     int a_cap;
@@ -223,6 +248,19 @@ struct DevPool {
     ShardState* sh_state;
     unsigned int* sh_gslot;    // [p_cap] replicated prompt position -> gslot (kNoSlot: absent)
     unsigned int* sh_grefs0;   // [p_cap]
+
+    // Belady (policy 3; cs_belady.cuh)
+    unsigned int* bel_nu;             // [cap] next request id that references the slot's block
+    unsigned int* bel_kid;            // [cap] unique-key index of the slot's block
+    unsigned int* bel_kid_slot;       // [n_kids] slot holding that key (kNoSlot: not resident)
+    const unsigned int* bel_ref;      // [n_flat] request ids per key, ascending (CSR)
+    const long long* bel_ref_off;     // [n_kids + 1]
+    const int* bel_depth;             // [n_kids] chain position of the key's first occurrence
+    const unsigned int* bel_kid_of;   // [n_flat] key index of every request block
+    unsigned long long* bel_hi;       // [cap] per-pass composite (score bits)
+    unsigned long long* bel_lo;       // [cap] per-pass composite (last_touch)
+    BelCand* bel_cand;                // [kBelCand]
+    BelCtl* bel_ctl;
 };
 
 #ifdef __CUDACC__

@@ -218,6 +218,17 @@ struct cs_engine {
     bool loaded = false;
 
     uint64_t tick = 0;
+    // Belady: BeladyPolicy::cursor_ (highest arrived request id) and its value at the last launch
+    unsigned long long bel_cursor = 0, bel_cursor_dev = 0;
+    std::vector<long long> bel_off;  // request block offsets (n_req + 1)
+    void belady_args(csb::AdmitArgs& a, int64_t blk_off) {
+        if (pool->P.policy != 3) return;
+        a.kids = pool->bel_kid_of() + blk_off;
+        a.cursor = bel_cursor;
+        a.adv_lo = bel_off[bel_cursor_dev + 1 < bel_off.size() ? bel_cursor_dev + 1 : bel_off.size() - 1];
+        a.adv_hi = bel_off[bel_cursor + 1 < bel_off.size() ? bel_cursor + 1 : bel_off.size() - 1];
+        if (a.adv_hi < a.adv_lo) a.adv_hi = a.adv_lo;
+    }
     double sim_now = 0.0;
     int last_dispatched = -1;
 
@@ -388,7 +399,14 @@ void cs_engine::build(const cs_engine_cfg& c, const cs_workload_spec* ws, long l
     pool->agent_ids = order;
     pool->n_agents = (int)order.size();
     pool->sync();
-    (void)req_blocks;
+    if (pool->P.policy == 3) {
+        // BeladyPolicy(requests) (baselines.cpp:34-46): the next-use index over the request blocks
+        std::vector<long long> offs(nt + 1);
+        for (int64_t i = 0; i < nt; ++i) offs[i] = desc[i].blk_off;
+        offs[nt] = req_blocks;
+        pool->belady_index(d_keys.as<unsigned long long>(), req_blocks, offs);
+        bel_off = std::move(offs);
+    }
     if (c.host_inputs) {
         // the end-to-end path: prompt blocks live on the host and cross PCIe per admission
         ck(cudaMallocHost(reinterpret_cast<void**>(&h_keys), 8 * total_blocks), "cudaMallocHost");
@@ -428,7 +446,8 @@ void cs_engine::dev_setup() {
     const char* env = std::getenv("CS_DEVICE_SCHED");  // tools: overrides the config either way
     const char* env2 = std::getenv("CS_USE_PRESCAN");  // A/B switch (tools): prescans run, never consumed
     const bool want = env ? std::atoi(env) != 0 : cfg.device_scheduler != 0;
-    if (!want || cfg.host_inputs || pool->comm || conc > csb::kMaxConc) return;
+    // (the Belady baseline runs on the host scheduler: its admissions are a different kernel)
+    if (!want || cfg.host_inputs || pool->comm || conc > csb::kMaxConc || pool->P.policy == 3) return;
     const int64_t nt = (int64_t)reqs.size();
     // sessions in ascending id order (the std::map order of the host scheduler)
     std::vector<int> soff(1, 0), sreqs;
@@ -646,6 +665,7 @@ void cs_engine::fetch_victims(unsigned long long before) {
 void cs_engine::arrive(int64_t idx) {
     arrival_us[idx] = sim_now;
     ++tick;  // emit(RequestArrival): note_agent only (no decision depends on alphabet order)
+    if ((unsigned long long)idx > bel_cursor) bel_cursor = (unsigned long long)idx;  // BeladyPolicy::observe
     ready.push_back(idx);
 }
 
@@ -675,8 +695,10 @@ bool cs_engine::try_start_head() {
     a.anchor = r.anchor_blocks;
     a.tick_base = tick;
     a.pins_out = d_pins.as<unsigned int>() + r.blk_off;
+    belady_args(a, r.blk_off);
     const unsigned long long ev_before = pool->ev_total;
     const csb::AdmitStatus& st = pool->admit(a, r.nb);
+    bel_cursor_dev = bel_cursor;
     d2h_bytes += 8 * (int64_t)pool->vpref_done;  // the victim window copied behind the kernel
     ++admissions;
     if (cfg.host_inputs) d2h_bytes += (int64_t)sizeof(csb::AdmitStatus);

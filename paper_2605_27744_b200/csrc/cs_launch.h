@@ -73,6 +73,12 @@ struct AdmitArgs {
     const unsigned int* prev_ptr[kMaxUnpinRanges + 1];
     int prev_n[kMaxUnpinRanges + 1];
     int n_prev_ranges;
+    // Belady (policy 3): the prompt blocks' key indices, BeladyPolicy::cursor_ (the highest
+    // request id arrived so far) and the request blocks [adv_lo, adv_hi) whose next use the
+    // cursor passed since the previous admission launch
+    const unsigned int* kids;
+    unsigned long long cursor;
+    long long adv_lo, adv_hi;
 };
 
 struct LaunchCfg {
@@ -87,6 +93,15 @@ struct LaunchCfg {
 LaunchCfg admit_launch_config(const DevPool& P, int device, int want_grid);
 cudaError_t launch_admit(const DevPool& P, const AdmitArgs& a, const LaunchCfg& lc, int grid,
                          cudaStream_t s);
+
+// Belady admission (cs_belady.cuh): one cooperative launch per admission.
+LaunchCfg belady_launch_config(const DevPool& P, int device);
+cudaError_t launch_belady_admit(const DevPool& P, const AdmitArgs& a, const LaunchCfg& lc, int grid, cudaStream_t s);
+// Next-use index over the materialized requests (cs_belady.cu): keys[0, n_flat) are the request
+// blocks, blk_off[0, n_req] their offsets. Fills ref/ref_off/depth/kid_of (device buffers the
+// caller sized n_flat, n_flat + 1, n_flat, n_flat) and returns the unique-key count.
+long long build_belady_index(const unsigned long long* keys, long long n_flat, const long long* blk_off, long long n_req,
+                             unsigned int* ref, long long* ref_off, int* depth, unsigned int* kid_of, cudaStream_t s);
 
 // Hash-sharded admission (cs_shard.cuh): probe -> exchange 1 -> decide -> per chunk
 // [scan -> exchange 2] -> replay.

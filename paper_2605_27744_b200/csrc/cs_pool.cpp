@@ -81,7 +81,9 @@ void cs_pool::create(const cs_pool_cfg& c, long long shard_slots, cs_comm* cm) {
     // decreases along last_touch (ticks and the simulated clock advance together), so the
     // blocks still inside the pin horizon (score 1e6 + rho) are the youngest, and the argmin of
     // (score, last_touch) over unpinned blocks is the oldest one under both scorers.
-    if (c.policy < 0 || c.policy > 2) throw std::invalid_argument("policy must be 0 (lru), 1 (cachesage) or 2 (ttl)");
+    if (c.policy < 0 || c.policy > 3)
+        throw std::invalid_argument("policy must be 0 (lru), 1 (cachesage), 2 (ttl) or 3 (belady)");
+    if (c.policy == 3 && comm) throw std::invalid_argument("belady: the hash-sharded pool runs lru / ttl / cachesage");
     p.policy = c.policy == 2 ? 0 : c.policy;
     p.e_max = c.e_max;
     p.n_lists = c.e_max + 2;
@@ -180,6 +182,17 @@ void cs_pool::create(const cs_pool_cfg& c, long long shard_slots, cs_comm* cm) {
         ck(cudaMallocHost(reinterpret_cast<void**>(&hstate), sizeof(csb::ShardState)), "cudaMallocHost");
         ensure_prompt_scratch(8192);
     }
+    if (p.policy == 3) {
+        p.bel_nu = dmalloc<unsigned int>(p.cap, "bel_nu");
+        p.bel_kid = dmalloc<unsigned int>(p.cap, "bel_kid");
+        p.bel_hi = dmalloc<unsigned long long>(p.cap, "bel_hi");
+        p.bel_lo = dmalloc<unsigned long long>(p.cap, "bel_lo");
+        p.bel_cand = dmalloc<csb::BelCand>(csb::kBelCand, "bel_cand");
+        p.bel_ctl = dmalloc<csb::BelCtl>(1, "bel_ctl");
+        ck(cudaMemsetAsync(p.bel_ctl, 0, sizeof(csb::BelCtl), stream), "memset");
+        blc = csb::belady_launch_config(p, device);
+        if (blc.grid <= 0) throw CsError(CS_ERR_CUDA, "belady kernel: no launch configuration fits this device");
+    }
     ck(cudaHostAlloc(reinterpret_cast<void**>(&st), sizeof(csb::AdmitStatus), cudaHostAllocMapped), "cudaHostAlloc");
     std::memset(st, 0, sizeof(*st));
     ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(&st_dev), st, 0), "cudaHostGetDevicePointer");
@@ -193,7 +206,9 @@ void cs_pool::destroy() {
                     p.win_a, p.win_b, p.hop, p.cls, p.agent_ids, p.ctrl, p.gbound, p.gcount, p.fin_lt, p.fin_slot,
                     p.fin_n, p.p_slot, p.p_refs0, p.gbuf_lt, p.gbuf_slot, p.ghint, p.gmaxk, p.grej, p.dbg, p.gsmall, p.gmin, p.tq_key, p.tq_slot,
                     p.sh_send1, p.sh_recv1, p.sh_send2, p.sh_recv2, p.sh_state, p.sh_gslot, p.sh_grefs0,
-                    p.pl_lt, p.pl_slot, p.pl_agent, p.pl_n, p.pl_T, p.pre_buf_lt, p.pre_buf_slot, p.pre_hint};
+                    p.pl_lt, p.pl_slot, p.pl_agent, p.pl_n, p.pl_T, p.pre_buf_lt, p.pre_buf_slot, p.pre_hint,
+                    p.bel_nu, p.bel_kid, p.bel_kid_slot, (void*)p.bel_ref, (void*)p.bel_ref_off, (void*)p.bel_depth,
+                    (void*)p.bel_kid_of, p.bel_hi, p.bel_lo, p.bel_cand, p.bel_ctl};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     d_keys.release();
@@ -334,8 +349,97 @@ const csb::AdmitStatus& cs_pool::admit_sharded_once(const csb::AdmitArgs& in) {
     return *st;
 }
 
+void cs_pool::belady_index(const unsigned long long* keys, long long n_flat, const std::vector<long long>& blk_off) {
+    if (P.policy != 3) throw std::logic_error("belady_index: not a belady pool");
+    const long long n_req = (long long)blk_off.size() - 1;
+    const long long nf = std::max(1ll, n_flat);
+    P.bel_ref = dmalloc<unsigned int>(nf, "bel_ref");
+    P.bel_ref_off = dmalloc<long long>(nf + 1, "bel_ref_off");
+    P.bel_depth = dmalloc<int>(nf, "bel_depth");
+    P.bel_kid_of = dmalloc<unsigned int>(nf, "bel_kid_of");
+    long long* d_off = dmalloc<long long>(blk_off.size(), "blk_off");
+    ck(cudaMemcpyAsync(d_off, blk_off.data(), 8 * blk_off.size(), cudaMemcpyHostToDevice, stream), "H2D");
+    bel_kids = csb::build_belady_index(keys, n_flat, d_off, n_req, const_cast<unsigned int*>(P.bel_ref),
+                                       const_cast<long long*>(P.bel_ref_off), const_cast<int*>(P.bel_depth),
+                                       const_cast<unsigned int*>(P.bel_kid_of), stream);
+    cudaFree(d_off);
+    if (bel_kids < 0) throw CsError(CS_ERR_CUDA, "belady: next-use index build failed");
+    P.bel_kid_slot = dmalloc<unsigned int>(std::max(1ll, bel_kids), "bel_kid_slot");
+    ck(cudaMemsetAsync(P.bel_kid_slot, 0xff, 4 * (size_t)std::max(1ll, bel_kids), stream), "memset");
+    launches += 5;
+    sync();
+}
+
+// One Belady admission launch (cs_belady.cuh); same contract as admit().
+const csb::AdmitStatus& cs_pool::admit_belady(const csb::AdmitArgs& in, int n_for_grid) {
+    if (bel_kids < 0 || !in.kids) throw std::invalid_argument("belady: the pool needs the request stream (cs_engine)");
+    csb::AdmitArgs a = in;
+    ensure_prompt_scratch(std::max(1, a.n));
+    a.status = st_dev;
+    a.n_agents = n_agents;
+    const bool may_evict = (a.flags & csb::kAdmit) && resident + n_for_grid > P.cap;
+    // one CTA per 16K slots: the selection passes are short, the grid barriers are not free
+    const char* ge = std::getenv("CS_BELADY_CTAS");  // tests: force a grid (multi-CTA select on small pools)
+    const int grid_env = ge ? std::atoi(ge) : 0;
+    int grid = may_evict ? (int)std::max(1ll, std::min<long long>(blc.grid, (P.cap + 16383) / 16384)) : 1;
+    if (may_evict && grid_env > 0) grid = std::min(grid_env, blc.grid);
+    if ((int)unpin_q.size() > csb::kMaxUnpinRanges) flush_unpins();
+    a.n_unpin_ranges = 0;
+    for (const auto& u : unpin_q) {
+        a.unpin_ptr[a.n_unpin_ranges] = u.first;
+        a.unpin_n[a.n_unpin_ranges] = u.second;
+        ++a.n_unpin_ranges;
+    }
+    unpin_q.clear();
+    unpin_q_slots = 0;
+    a.n_prev_ranges = 0;
+    a.seq = ++seq;
+    st->started = -1;
+    if (timing) ck(cudaEventRecord(ev0, stream), "cudaEventRecord");
+    ck(csb::launch_belady_admit(P, a, blc, grid, stream), "belady_admit_kernel launch");
+    ++launches;
+    if (timing) ck(cudaEventRecord(ev1, stream), "cudaEventRecord");
+    vpref_done = 0;
+    if (vpref && vpref_n > 0) {
+        const unsigned long long cap = (unsigned long long)P.evlog_cap, off = ev_total % cap;
+        const unsigned long long n1 = std::min<unsigned long long>((unsigned long long)vpref_n, cap - off);
+        ck(cudaMemcpyAsync(vpref, P.evlog + off, 8 * n1, cudaMemcpyDeviceToHost, stream), "victims D2H");
+        if (n1 < (unsigned long long)vpref_n)
+            ck(cudaMemcpyAsync(vpref + n1, P.evlog, 8 * (vpref_n - n1), cudaMemcpyDeviceToHost, stream), "victims D2H");
+        vpref_done = vpref_n;
+    }
+    vpref = nullptr;
+    vpref_n = 0;
+    ck(cudaStreamSynchronize(stream), "belady_admit_kernel");
+    poll_reset_pending = false;
+    if (timing) {
+        float ms = 0.f;
+        ck(cudaEventElapsedTime(&ms, ev0, ev1), "cudaEventElapsedTime");
+        admit_ms += ms;
+        ++admit_launches;
+        if (st->scans > 0) {
+            scan_launch_ms += ms;
+            ++scan_launches;
+        }
+    }
+    if (st->started < 0) throw CsError(CS_ERR_CUDA, "belady kernel did not report a status");
+    resident = st->resident;
+    pinned = st->pinned;
+    ev_total = st->ev_total;
+    pending_targets.clear();
+    pending_ticks.clear();
+    if (st->error) throw std::runtime_error("evict_one: all resident blocks are pinned");
+    if ((unsigned long long)(st->resident + st->tombstones) > (P.tmask + 1) / 2) {
+        ck(csb::launch_table_rebuild(P, stream), "table rebuild");
+        ++table_rebuilds;
+        launches += 2;
+    }
+    return *st;
+}
+
 const csb::AdmitStatus& cs_pool::admit(const csb::AdmitArgs& in, int n_for_grid) {
     if (comm) return admit_sharded(in);
+    if (P.policy == 3) return admit_belady(in, n_for_grid);
     csb::AdmitArgs a = in;
     ensure_prompt_scratch(std::max(1, a.n));
     a.status = st_dev;

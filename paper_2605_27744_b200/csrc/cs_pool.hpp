@@ -96,6 +96,15 @@ struct cs_pool {
     cs_comm* comm = nullptr;
     csb::ShardState* hstate = nullptr;  // pinned host copy of the replicated admission state
 
+    // Belady (policy 3): launch shape and the next-use index over the request stream
+    csb::LaunchCfg blc{};
+    long long bel_kids = -1;  // unique keys of the installed index (-1: none)
+    // Builds the index from the request blocks keys[0, n_flat) (device) with request offsets
+    // blk_off[0, n_req] (host); kid_of() then gives every request block's key index.
+    void belady_index(const unsigned long long* keys, long long n_flat, const std::vector<long long>& blk_off);
+    const unsigned int* bel_kid_of() const { return P.bel_kid_of; }
+    const csb::AdmitStatus& admit_belady(const csb::AdmitArgs& args_in, int n_for_grid);
+
     // shard_slots > 0 or comm: one shard of a pool of global budget c.budget_blocks
     void create(const cs_pool_cfg& c, long long shard_slots = 0, cs_comm* comm = nullptr);
     const csb::AdmitStatus& admit_sharded(const csb::AdmitArgs& args_in);

@@ -83,6 +83,19 @@ def run_cases():
     cases.append(("supervisor-a-bs8", sa, {"policy": "cachesage", "block_size": 8}))
     ch = W.preset_by_name("synthetic-chain")
     cases.append(("chain-budget120", ch, {"policy": "cachesage", "budget": 120}))
+    # the Belady baseline (baselines.cpp:34-70) on the same pool: every preset, tight budgets,
+    # oversized prompts, pins, concurrency
+    for s in W.preset_workloads():
+        cases.append((s["name"], s, {"policy": "belady"}))
+    for b in (128, 256, 4096, 16384, 65536):  # (the last two run the radix select over > kBelCand slots)
+        cases.append((f"cfg1@{b}", W.cfg1(b), {"policy": "belady", "budget": b}))
+    cases.append(("tiny-alternation-belady", t, {"policy": "belady", "prefetch": False}))
+    cases.append(("oversized-solo", o, {"policy": "belady"}))
+    cases.append(("oversized-mixed", o2, {"policy": "belady"}))
+    cases.append(("pins-defer", p, {"policy": "belady"}))
+    cases.append(("supervisor-a-conc8", sa, {"policy": "belady", "concurrency": 8}))
+    cases.append(("supervisor-a-budget60", sa, {"policy": "belady", "budget": 60}))
+    cases.append(("chain-budget120", ch, {"policy": "belady", "budget": 120}))
     return cases
 
 

@@ -182,7 +182,7 @@ def turn_tokens(spec, idx, cap=1 << 20):
     return out[:n]
 
 
-POLICY_IDS = {"lru": 0, "cachesage": 1, "ttl": 2}
+POLICY_IDS = {"lru": 0, "cachesage": 1, "ttl": 2, "belady": 3}
 
 
 def run_cfg(policy="cachesage", budget=None, concurrency=None, block_size=16, prefetch=True,

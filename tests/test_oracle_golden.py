@@ -99,12 +99,16 @@ def _check_run(r, g):
 
 @pytest.mark.parametrize("g", RUNS, ids=[g["name"] + "-" + g["kw"]["policy"] for g in RUNS])
 def test_oracle_run_golden(g):
+    if g["kw"]["policy"] == "belady" and g["kw"].get("budget", 0) >= 4096:
+        pytest.skip("O(N) per eviction at N >= 4096 takes minutes on CPU; the GPU tests check these fixtures")
     _check_run(O.run(g["spec"], **g["kw"]), g)
 
 
 # SURVEY.md Appendix A.1 (hit rates of the five presets under the two policies)
 SURVEY_A1 = {
     ("supervisor-a", "cachesage"): 0.41240476693085648,
+    ("supervisor-a", "belady"): 0.42184651403788215,
+    ("supervisor-b", "belady"): 0.48052231635950737,
 }
 
 
