@@ -234,6 +234,18 @@ int64_t cs_engine_evictions(cs_engine_t e, uint64_t* keys, int64_t cap);
 int64_t cs_engine_warmups(cs_engine_t e, int64_t* step, uint64_t* target, uint64_t* tick, int64_t cap);
 cs_pool_t cs_engine_pool(cs_engine_t e);
 
+/* Output writers: run_experiment's per-cell files (experiment.cpp:94-183,
+ * 424-440), byte-identical to the reference's for the same cell:
+ *   <dir>/metrics.json  metrics_to_json(...).dump(2)
+ *   <dir>/turns.csv     write_turns_csv
+ *   <dir>/events.jsonl  write_events_jsonl (write_events = 1; needs cs_engine_record_events)
+ * workload / policy / seed / labels are the cell's names as run_experiment reports them (the
+ * workload display name, the policy name, the trace seed, the workload's agent labels in spec
+ * order). The run must be finished. */
+int cs_engine_record_events(cs_engine_t e, int on); /* before the first step; host scheduler only */
+int cs_engine_write_outputs(cs_engine_t e, const char* dir, const char* workload, const char* policy, uint64_t seed,
+                            const char* const* labels, int n_labels, int write_events);
+
 /* ------------------------------------------------------------------ standalone learner
  *
  * The reference's TransitionLearner (transition_learner.hpp:19-60; Python binding

@@ -547,4 +547,20 @@ int ref_run_sim_jsonl(const char* jsonl, const char* policy, int budget, int con
     }
 }
 
+// The reference's experiment driver over a config text (experiment.cpp:238-330 parse, :380-495
+// run_experiment): writes <out.dir>/<workload>/<policy>/{metrics.json,turns.csv,events.jsonl}
+// and summary.json. Marshalling only.
+int ref_run_experiment_text(const char* config_text) {
+    try {
+        RunConfig config = parse_run_config_text(config_text, "<config>");
+        config.force = true;
+        std::ostringstream summary;
+        run_experiment(config, summary);
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
 }  // extern "C"

@@ -132,6 +132,8 @@ SIGNATURES = {
     "cs_engine_create_from_turns": (C.c_int, [C.POINTER(EngineCfg), C.POINTER(WorkloadSpec), vp, C.c_int64,
                                               C.POINTER(vp)]),
     "cs_engine_turn_arrivals": (C.c_int, [vp, vp, C.c_int64]),
+    "cs_engine_record_events": (C.c_int, [vp, C.c_int]),
+    "cs_engine_write_outputs": (C.c_int, [vp, C.c_char_p, C.c_char_p, C.c_char_p, C.c_uint64, vp, C.c_int, C.c_int]),
     "cs_derive_agent_identity": (C.c_int, [vp, vp, C.c_int, C.c_int, C.c_int, vp]),
     "cs_last_error": (C.c_char_p, []),
     "cs_version": (C.c_char_p, []),

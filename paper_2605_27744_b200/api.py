@@ -330,6 +330,8 @@ class Engine:
         cfg.host_inputs = 1 if host_inputs else 0
         cfg.device_scheduler = 1 if device_scheduler else 0
         self._spec = spec_struct(spec)
+        self._spec_dict = spec
+        self._policy = policy
         h = C.c_void_p()
         self.comm = comm
         if comm is None:
@@ -411,6 +413,27 @@ class Engine:
         out = np.zeros(max(n, 1), np.uint64)
         lib().cs_engine_evictions(self.h, _p(out), n)
         return out[:n]
+
+    def record_events(self, on=True):
+        """Record EngineSim's event stream (engine.cpp:72-88) for write_outputs' events.jsonl;
+        call before the first step (host scheduler only)."""
+        check(lib().cs_engine_record_events(self.h, 1 if on else 0))
+
+    def write_outputs(self, out_dir, workload=None, policy=None, seed=None, labels=None, events=True):
+        """run_experiment's per-cell files (experiment.cpp:94-183, 424-440) for this finished run:
+        <out_dir>/metrics.json, turns.csv and (events) events.jsonl, byte-identical to the
+        reference's. Defaults come from the spec this engine was built from."""
+        import os
+
+        spec = self._spec_dict
+        workload = workload if workload is not None else spec.get("name", "custom")
+        policy = policy if policy is not None else self._policy
+        seed = int(seed if seed is not None else spec.get("seed", 0))
+        labels = list(labels if labels is not None else spec.get("labels", []))
+        os.makedirs(out_dir, exist_ok=True)
+        arr = (C.c_char_p * max(1, len(labels)))(*[x.encode() for x in labels])
+        check(lib().cs_engine_write_outputs(self.h, str(out_dir).encode(), workload.encode(), policy.encode(), seed,
+                                            C.cast(arr, C.c_void_p), len(labels), 1 if events else 0))
 
     def warmups(self):
         n = check(lib().cs_engine_warmups(self.h, None, None, None, 0))

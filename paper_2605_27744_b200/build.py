@@ -9,17 +9,21 @@ from __future__ import annotations
 import os
 import shutil
 import subprocess
+import sysconfig
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT_DIR = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libcachesage_b200.so")
+# nlohmann/json 3.11.3 (the reference's serializer; shipped in the image with cudnn_frontend):
+# the output writers format through it so metrics.json / events.jsonl match byte for byte
+JSON_DIR = os.path.join(sysconfig.get_paths()["purelib"], "include", "cudnn_frontend", "thirdparty", "nlohmann")
 
 NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 DEVICE_SRCS = ["cs_kernels.cu", "cs_admit.cu", "cs_learner.cu", "cs_belady.cu"]
-HOST_SRCS = ["cs_pool.cpp", "cs_engine.cpp", "cs_comm.cpp"]
+HOST_SRCS = ["cs_pool.cpp", "cs_engine.cpp", "cs_comm.cpp", "cs_output.cpp"]
 DEPS = DEVICE_SRCS + HOST_SRCS + ["cs_device.cuh", "cs_launch.h", "cs_pool.hpp"]
 
 
@@ -39,7 +43,7 @@ def _stale(target, sources):
 def build(verbose: bool = False, force: bool = False) -> str:
     os.makedirs(OUT_DIR, exist_ok=True)
     inc = ["-I", os.path.join(ROOT, "include"), "-I", CSRC]
-    header_deps = [os.path.join(CSRC, h) for h in ("cs_device.cuh", "cs_launch.h", "cs_pool.hpp", "cs_block.cuh", "cs_shard.cuh", "cs_comm.hpp", "cs_engine_state.h", "cs_engine_dev.cuh", "cs_belady.cuh")]
+    header_deps = [os.path.join(CSRC, h) for h in ("cs_device.cuh", "cs_launch.h", "cs_pool.hpp", "cs_block.cuh", "cs_shard.cuh", "cs_comm.hpp", "cs_engine_state.h", "cs_engine_dev.cuh", "cs_belady.cuh", "cs_output.hpp")]
     header_deps.append(os.path.join(ROOT, "include", "cachesage_b200.h"))
     objs = []
     for src in DEVICE_SRCS:
@@ -55,7 +59,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
         s = os.path.join(CSRC, src)
         o = os.path.join(OUT_DIR, src + ".o")
         if force or _stale(o, [s] + header_deps):
-            _run([NVCC, "-O2", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off,-Wall", *inc, "-c", s,
+            _run([NVCC, "-O2", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off,-Wall", *inc, "-I", JSON_DIR, "-c", s,
                   "-o", o], verbose)
         objs.append(o)
     if force or _stale(LIB, objs):

@@ -2717,6 +2717,7 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
                     cached += a.counts[i];
                     const unsigned int ts = P.p_slot[i];
                     P.lt[ts] = A.tick + 1 + (unsigned long long)i;  // EngineSim::touch
+                    if (a.touch_agent) a.touch_agent[i] = P.agent[ts];
                     if (early) tset_insert(es.tset, ts);
                 }
                 if (tid == 0 && !early) es.ok = 0;

@@ -396,7 +396,10 @@ __global__ void __launch_bounds__(kBelThreads, 1) belady_admit_kernel(DevPool P,
             const int f = B->first_miss, pre = min(f, B->admit_n);
             const unsigned long long t0 = B->tick;
             long long cached = 0, pinc = 0;
-            for (int i = tid; i < f; i += T) cached += a.counts[i];
+            for (int i = tid; i < f; i += T) {
+                cached += a.counts[i];
+                if (a.touch_agent) a.touch_agent[i] = P.agent[P.p_slot[i]];  // BlockTouch{key, agent}
+            }
             for (int i = tid; i < pre; i += T) {  // admit_pinned over the resident prefix
                 const unsigned int s = P.p_slot[i];
                 P.lt[s] = t0 + 1 + (unsigned long long)i;

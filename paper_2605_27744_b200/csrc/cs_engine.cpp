@@ -23,6 +23,7 @@
 #include <vector>
 
 #include "cs_engine_state.h"
+#include "cs_output.hpp"
 #include "cs_pool.hpp"
 
 using csb::ck;
@@ -174,6 +175,7 @@ struct cs_engine {
         int anchor_blocks;
         int64_t prompt_tokens;
         int decode;
+        int spec_agent;  // workload agent (its label in turns.csv)
     };
     std::vector<Req> reqs;
     struct Cat {
@@ -241,6 +243,42 @@ struct cs_engine {
     std::vector<int64_t> w_step;
     std::vector<uint64_t> w_target, w_tick;
     int64_t completed = 0, truncated = 0, warm_exec = 0, warm_drop = 0, steps = 0, admissions = 0;
+    int64_t warm_uncached = 0;     // EngineSim::warmup_uncached_tokens_ (engine.cpp:223)
+    double warm_time_us = 0.0;     // EngineSim::warmup_time_us_ (engine.cpp:224-227)
+    // recorded event stream (events.jsonl): EngineSim::events_ (engine.cpp:72-88)
+    bool rec_events = false;
+    std::vector<csb::EventRec> events;
+    csb::DevBuf d_touch;
+    std::vector<unsigned int> h_touch;
+    std::vector<unsigned long long> h_tkeys;
+    void ev_push(uint64_t tick_, uint8_t kind, uint64_t a, uint64_t b, bool has_a = true, bool has_b = true) {
+        csb::EventRec e{};
+        e.tick = tick_;
+        e.kind = kind;
+        e.a = a;
+        e.b = b;
+        e.has_a = has_a;
+        e.has_b = has_b;
+        events.push_back(e);
+    }
+    // BlockTouch events of a lookup that touched the first f prompt blocks from tick t0 + 1 on
+    void ev_touches(const csb::AdmitArgs& a, int f, uint64_t t0) {
+        if (!rec_events || f <= 0) return;
+        h_touch.resize(f);
+        h_tkeys.resize(f);
+        ck(cudaMemcpy(h_touch.data(), a.touch_agent, 4 * (size_t)f, cudaMemcpyDeviceToHost), "D2H");
+        ck(cudaMemcpy(h_tkeys.data(), a.keys, 8 * (size_t)f, cudaMemcpyDeviceToHost), "D2H");
+        for (int i = 0; i < f; ++i) {
+            const unsigned int ag = h_touch[i];
+            const bool has = ag != csb::kNoAgent;
+            ev_push(t0 + 1 + (uint64_t)i, csb::EventRec::kBlockTouch, h_tkeys[i], has ? pool->agent_ids[ag] : 0, true, has);
+        }
+    }
+    void ev_prepare(csb::AdmitArgs& a, int nb) {
+        if (!rec_events) return;
+        d_touch.ensure(4 * (size_t)std::max(nb, 1));
+        a.touch_agent = d_touch.as<unsigned int>();
+    }
     int64_t tot_prompt = 0, tot_cached = 0;
 
     static bool later(const Flight& a, const Flight& b) {
@@ -382,6 +420,7 @@ void cs_engine::build(const cs_engine_cfg& c, const cs_workload_spec* ws, long l
         r.anchor_blocks = (int)((spec.template_tokens + t.v[3]) / bs);
         r.prompt_tokens = t.v[5];
         r.decode = (int)t.v[6];
+        r.spec_agent = (int)t.v[2];
     }
     for (int a = 0; a < spec.n_agents; ++a) {
         const int k = idx_of(ids[nt + a]);
@@ -666,6 +705,7 @@ void cs_engine::arrive(int64_t idx) {
     arrival_us[idx] = sim_now;
     ++tick;  // emit(RequestArrival): note_agent only (no decision depends on alphabet order)
     if ((unsigned long long)idx > bel_cursor) bel_cursor = (unsigned long long)idx;  // BeladyPolicy::observe
+    if (rec_events) ev_push(tick, csb::EventRec::kRequestArrival, (uint64_t)idx, pool->agent_ids[reqs[idx].agent]);
     ready.push_back(idx);
 }
 
@@ -696,9 +736,15 @@ bool cs_engine::try_start_head() {
     a.tick_base = tick;
     a.pins_out = d_pins.as<unsigned int>() + r.blk_off;
     belady_args(a, r.blk_off);
+    ev_prepare(a, r.nb);
     const unsigned long long ev_before = pool->ev_total;
     const csb::AdmitStatus& st = pool->admit(a, r.nb);
     bel_cursor_dev = bel_cursor;
+    if (rec_events && st.started) {
+        ev_push(tick + 1, csb::EventRec::kAgentDispatch, last_dispatched >= 0 ? pool->agent_ids[last_dispatched] : 0,
+                pool->agent_ids[r.agent], last_dispatched >= 0, true);
+        if (!oversized) ev_touches(a, st.first_miss, tick + 1);
+    }
     d2h_bytes += 8 * (int64_t)pool->vpref_done;  // the victim window copied behind the kernel
     ++admissions;
     if (cfg.host_inputs) d2h_bytes += (int64_t)sizeof(csb::AdmitStatus);
@@ -727,6 +773,7 @@ void cs_engine::complete_earliest() {
     in_flight.pop_back();
     sim_now = f.end_us;
     ++tick;  // emit(TurnComplete)
+    if (rec_events) ev_push(tick, csb::EventRec::kTurnComplete, (uint64_t)f.req, 0);
     const Req& r = reqs[f.req];
     pool->defer_unpin(d_pins.as<unsigned int>() + r.blk_off, f.npins);  // runs inside the next admission launch
     const int sid = r.session;
@@ -763,13 +810,18 @@ void cs_engine::execute_warmup(int target) {
     a.anchor = -1;
     a.tick_base = tick;
     a.pins_out = d_pins.as<unsigned int>() + c.blk_off;
+    ev_prepare(a, c.nb);
     const unsigned long long ev_before = pool->ev_total;
     const csb::AdmitStatus& st = pool->admit(a, c.nb);
     d2h_bytes += 8 * (int64_t)pool->vpref_done;
     ++admissions;
+    ev_touches(a, st.first_miss, tick);
     tick = st.tick_after;
     ++warm_exec;
     warm_prompt += c.prompt_tokens;
+    // engine.cpp:223-227
+    warm_uncached += c.prompt_tokens - st.cached;
+    warm_time_us += 1000.0 + 50.0 * (double)(c.prompt_tokens - st.cached) + 20000.0 * 1;
     fetch_victims(ev_before);
 }
 
@@ -1059,6 +1111,80 @@ int cs_engine_turns(cs_engine_t e, int64_t* cached, int64_t* prompt, double* sta
             if (start_us) start_us[i] = e->t_start[i];
             if (end_us) end_us[i] = e->t_end[i];
         }
+    });
+}
+
+int cs_engine_record_events(cs_engine_t e, int on) {
+    return eguard([&] {
+        if (!e) throw std::invalid_argument("cs_engine_record_events: null engine");
+        if (on && (e->dev || e->pool->comm))
+            throw std::invalid_argument("events: recorded by the host scheduler on one pool (no device scheduler, no shards)");
+        if (on && (e->admissions > 0 || e->steps > 0)) throw std::logic_error("events: enable before the first step");
+        e->rec_events = on != 0;
+    });
+}
+
+int cs_engine_write_outputs(cs_engine_t e, const char* dir, const char* workload, const char* policy, uint64_t seed,
+                            const char* const* labels, int n_labels, int write_events) {
+    return eguard([&] {
+        if (!e || !dir || !workload || !policy) throw std::invalid_argument("cs_engine_write_outputs: null argument");
+        if (e->dev) e->dev_pull_outputs();
+        if (!e->done()) throw std::logic_error("cs_engine_write_outputs: the run is not finished");
+        if (write_events && !e->rec_events) throw std::logic_error("events were not recorded (cs_engine_record_events)");
+        e->drain_evictions(true);
+        csb::CellOut c;
+        c.workload = workload;
+        c.policy = policy;
+        c.seed = seed;
+        for (int i = 0; i < n_labels; ++i) c.labels.emplace_back(labels && labels[i] ? labels[i] : "");
+        c.budget_blocks = e->budget;
+        c.block_size = e->bs;
+        c.concurrency = e->conc;
+        c.prefetch = e->cfg.prefetch != 0;
+        c.prefill_per_token_us = 50.0;
+        c.prefill_base_us = 1000.0;
+        c.decode_per_token_us = 20000.0;
+        const cs_pool_cfg& pc = e->cfg.pool;
+        c.skip = e->cfg.skip;
+        c.take = e->cfg.take;
+        c.tau = pc.tau;
+        c.e_max = pc.e_max;
+        c.w_pred = pc.w_pred;
+        c.window = (uint64_t)pc.window;
+        c.min_confidence = pc.min_confidence;
+        c.min_row_count = (uint64_t)pc.min_row_count;
+        c.budget_per_step = pc.budget_per_step;
+        c.ttl_pin_horizon_us = 5000000.0;  // TtlConfig default (baselines.hpp:25)
+        const int64_t nt = (int64_t)e->reqs.size();
+        c.turns.reserve(nt);
+        for (int64_t i = 0; i < nt; ++i) {
+            if (!e->t_done[i]) continue;
+            const auto& r = e->reqs[i];
+            csb::TurnRec t{};
+            t.turn_id = (uint64_t)i;
+            t.session = r.session;
+            t.turn_index = r.turn_index;
+            t.agent = e->pool->agent_ids[r.agent];
+            t.label = r.spec_agent;
+            t.prompt_tokens = (long)e->t_prompt[i];
+            t.cached_tokens = (long)e->t_cached[i];
+            t.ttft_us = 1000.0 + 50.0 * (double)(r.prompt_tokens - e->t_cached[i]);  // engine.cpp:300-302
+            t.arrival_us = e->arrival_us[i];
+            t.start_us = e->t_start[i];
+            t.end_us = e->t_end[i];
+            t.latency_us = t.end_us - t.arrival_us;
+            c.turns.push_back(t);
+        }
+        c.sim_duration_us = e->sim_now;
+        c.evictions = e->evictions.size();
+        c.truncated = (uint64_t)e->truncated;
+        c.warmups_executed = (uint64_t)e->warm_exec;
+        c.warmups_dropped = (uint64_t)e->warm_drop;
+        c.warmup_prompt_tokens = (long)e->warm_prompt;
+        c.warmup_uncached_tokens = (long)e->warm_uncached;
+        c.warmup_time_us = e->warm_time_us;
+        c.events = write_events ? &e->events : nullptr;
+        csb::write_cell(c, dir);
     });
 }
 

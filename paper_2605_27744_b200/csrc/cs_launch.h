@@ -79,6 +79,9 @@ struct AdmitArgs {
     const unsigned int* kids;
     unsigned long long cursor;
     long long adv_lo, adv_hi;
+    // recorded runs (events.jsonl): per looked-up prompt position < first_miss, the touched
+    // block's agent index (BlockTouch{key, agent}, engine.cpp:79-88); null: not recorded
+    unsigned int* touch_agent;
 };
 
 struct LaunchCfg {

@@ -89,6 +89,8 @@ def lib():
                                           C.c_double, C.c_int, C.c_int] + [C.c_void_p] * 9
         _lib.ref_preset_trace_jsonl.restype = C.c_long
         _lib.ref_preset_trace_jsonl.argtypes = [C.c_char_p, C.c_int, C.c_longlong, C.c_char_p, C.c_long]
+        _lib.ref_run_experiment_text.restype = C.c_int
+        _lib.ref_run_experiment_text.argtypes = [C.c_char_p]
         _lib.ref_run_sim_jsonl.restype = C.c_int
         _lib.ref_run_sim_jsonl.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p]
         _lib.ref_evict_bench.restype = C.c_double
@@ -298,3 +300,17 @@ def run_sim_jsonl(jsonl, policy="cachesage", budget=None, concurrency=None, bloc
     for k in METRIC_KEYS[5:]:
         d[k] = int(d[k])
     return d
+
+
+def run_experiment(config):
+    """The reference's run_experiment over a config dict (the `cachesage run` config schema,
+    experiment.cpp:238-330); files land under config["output"]["dir"]. Runs oracle/_ref/
+    ref_experiment in a child process (its std::filesystem clashes with the interpreter's
+    libstdc++ in-process)."""
+    import json as _json
+    import subprocess
+
+    exe = os.path.join(os.path.dirname(LIB_PATH), "ref_experiment")
+    r = subprocess.run([exe], input=_json.dumps(config).encode(), capture_output=True)
+    if r.returncode != 0:
+        raise RuntimeError(r.stderr.decode())
