@@ -541,6 +541,7 @@ void cs_engine::dev_setup() {
     d_wt.ensure(8 * w_cap);
     d_wk.ensure(8 * w_cap);
     d_args.ensure(sizeof(csb::AdmitArgs));
+    ck(cudaMemset(d_args.p, 0, sizeof(csb::AdmitArgs)), "memset");  // fields eng_issue never sets stay null
     d_cmd.ensure(8);
     d_state.ensure(sizeof(csb::EngState));
     std::memset(&hs, 0, sizeof(hs));
