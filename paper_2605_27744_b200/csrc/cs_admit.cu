@@ -2329,6 +2329,7 @@ __device__ void replay_apply(const DevPool& P, const AdmitArgs& a, ReplaySmem& R
         const unsigned long long kk = R.vkey[k];
         P.tq_key[q_e + k] = kk;
         P.evlog[(ev0 + k) % (unsigned long long)P.evlog_cap] = kk;  // ring; the host drains it
+        if (a.vict_host && A.n_ev_adm + k < a.vict_cap) a.vict_host[A.n_ev_adm + k] = kk;  // mapped host memory
         if (k >= R.n_reused) {  // victims[0, n_reused) are overwritten by new blocks below
             const unsigned int v = R.victims[k];
             P.lt[v] = kFreeTick;
@@ -3049,7 +3050,11 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
         __syncthreads();
         stamp(A, 5);
         pstamp(P, 11);
-        if (tid == 0 && a.status) write_status(P, a, A);
+        if (tid == 0 && a.status) {
+            write_status(P, a, A);
+            __threadfence_system();  // status and victims reach the host before the flag
+            *(volatile unsigned long long*)&a.status->done_seq = a.seq;
+        }
         pstamp(P, 12);
         // per-list scan state for the next launch (a speculative pass starts without a prep)
         if (tid < kMaxLists) {

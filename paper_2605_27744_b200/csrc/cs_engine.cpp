@@ -379,6 +379,9 @@ void cs_engine::build(const cs_engine_cfg& c, const cs_workload_spec* ws, long l
         throw;
     }
     pool->timing = c.timing != 0;
+    // the scheduler needs only the status of an admission: it enqueues the next one while the
+    // previous launch's prescan CTAs finish (cs_pool::wait_status)
+    pool->early_status = comm == nullptr;
     d_keys.ensure(8 * total_blocks);
     d_counts.ensure(4 * total_blocks);
     d_pins.ensure(4 * total_blocks);

@@ -48,6 +48,9 @@ struct AdmitStatus {
     unsigned long long phase_ns[kPhases];
     int pend_target[kMaxPending];
     unsigned long long pend_tick[kMaxPending];
+    // AdmitArgs::seq once every field above (and AdmitArgs::vict_host) is written: CTA 0 sets
+    // it behind a system-scope fence, so the host continues while the prescan CTAs finish
+    unsigned long long done_seq;
 };
 
 struct AdmitArgs {
@@ -82,6 +85,10 @@ struct AdmitArgs {
     // recorded runs (events.jsonl): per looked-up prompt position < first_miss, the touched
     // block's agent index (BlockTouch{key, agent}, engine.cpp:79-88); null: not recorded
     unsigned int* touch_agent;
+    // the end-to-end path: this admission's victim keys, written by CTA 0 straight into pinned
+    // host memory (mapped) before done_seq; at most vict_cap
+    unsigned long long* vict_host;
+    int vict_cap;
 };
 
 struct LaunchCfg {

@@ -480,34 +480,37 @@ const csb::AdmitStatus& cs_pool::admit(const csb::AdmitArgs& in, int n_for_grid)
     }
     pre_ok = false;
     st->started = -1;
-    if (timing) ck(cudaEventRecord(ev0, stream), "cudaEventRecord");
+    // the end-to-end path: CTA 0 writes this admission's victims (<= one per block) into the
+    // caller's pinned buffer itself, before the status flag
+    a.vict_host = nullptr;
+    a.vict_cap = 0;
+    if (vpref && vpref_n > 0) {
+        unsigned long long* dp = nullptr;
+        ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dp), vpref, 0), "cudaHostGetDevicePointer(victims)");
+        a.vict_host = dp;
+        a.vict_cap = vpref_n;
+    }
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (timing) {
+        e0 = take_event();
+        e1 = take_event();
+        ck(cudaEventRecord(e0, stream), "cudaEventRecord");
+    }
     ck(csb::launch_admit(P, a, lc, grid, stream), "admit_kernel launch");
     ++launches;
-    if (timing) ck(cudaEventRecord(ev1, stream), "cudaEventRecord");
-    vpref_done = 0;
-    if (vpref && vpref_n > 0) {  // this admission's victims (<= one per block) behind the kernel
-        const unsigned long long cap = (unsigned long long)P.evlog_cap, off = ev_total % cap;
-        const unsigned long long n1 = std::min<unsigned long long>((unsigned long long)vpref_n, cap - off);
-        ck(cudaMemcpyAsync(vpref, P.evlog + off, 8 * n1, cudaMemcpyDeviceToHost, stream), "victims D2H");
-        if (n1 < (unsigned long long)vpref_n)
-            ck(cudaMemcpyAsync(vpref + n1, P.evlog, 8 * (vpref_n - n1), cudaMemcpyDeviceToHost, stream), "victims D2H");
-        vpref_done = vpref_n;
-    }
+    if (timing) ck(cudaEventRecord(e1, stream), "cudaEventRecord");
+    // The status flag is set by CTA 0 while the prescan CTAs still stream the next admission's
+    // pass: the host prepares and enqueues the next launch behind this one instead of waiting
+    // for the kernel's end (stream order keeps every later device operation behind it).
+    wait_status(a.seq, "admit_kernel");
+    if (!early_status) ck(cudaStreamSynchronize(stream), "admit_kernel");
+    vpref_done = (vpref && vpref_n > 0) ? (int)std::min<long long>(st->n_evicted, vpref_n) : 0;
     vpref = nullptr;
     vpref_n = 0;
-    ck(cudaStreamSynchronize(stream), "admit_kernel");
     poll_reset_pending = false;
-    const long long scans_before = scans_total;
-    (void)scans_before;
     if (timing) {
-        float ms = 0.f;
-        ck(cudaEventElapsedTime(&ms, ev0, ev1), "cudaEventElapsedTime");
-        admit_ms += ms;
-        ++admit_launches;
-        if (st->scans > 0) {
-            scan_launch_ms += ms;
-            ++scan_launches;
-        }
+        t_pending.push_back({e0, e1, st->scans > 0});
+        resolve_timing(false);
     }
     if (st->started < 0) throw CsError(CS_ERR_CUDA, "admit kernel did not report a status");
     // the slots this launch unpinned, for the next launch's use of this launch's prescan
@@ -536,6 +539,52 @@ const csb::AdmitStatus& cs_pool::admit(const csb::AdmitArgs& in, int n_for_grid)
         launches += 2;
     }
     return *st;
+}
+
+cudaEvent_t cs_pool::take_event() {
+    if (!t_free.empty()) {
+        cudaEvent_t e = t_free.back();
+        t_free.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    ck(cudaEventCreate(&e), "cudaEventCreate");
+    return e;
+}
+
+void cs_pool::resolve_timing(bool wait) {
+    size_t k = 0;
+    for (; k < t_pending.size(); ++k) {
+        const TimedLaunch& t = t_pending[k];
+        if (wait) ck(cudaEventSynchronize(t.e1), "cudaEventSynchronize");
+        else if (cudaEventQuery(t.e1) != cudaSuccess) break;
+        float ms = 0.f;
+        ck(cudaEventElapsedTime(&ms, t.e0, t.e1), "cudaEventElapsedTime");
+        admit_ms += ms;
+        ++admit_launches;
+        if (t.scan) {
+            scan_launch_ms += ms;
+            ++scan_launches;
+        }
+        t_free.push_back(t.e0);
+        t_free.push_back(t.e1);
+    }
+    t_pending.erase(t_pending.begin(), t_pending.begin() + k);
+}
+
+void cs_pool::wait_status(unsigned long long seq, const char* what) {
+    volatile unsigned long long* flag = &st->done_seq;
+    for (unsigned long long spin = 0;; ++spin) {
+        if (*flag == seq) return;
+        if ((spin & 1023) == 1023) {
+            const cudaError_t e = cudaStreamQuery(stream);
+            if (e == cudaSuccess) {  // the kernel has ended: its flag write is visible by now
+                if (*flag == seq) return;
+                throw CsError(CS_ERR_CUDA, std::string(what) + ": no status from the kernel");
+            }
+            if (e != cudaErrorNotReady) ck(e, what);
+        }
+    }
 }
 
 void cs_pool::defer_unpin(const unsigned int* dev_slots, int n) {
@@ -859,6 +908,7 @@ int cs_admit_pinned(cs_pool_t pool, const uint64_t* keys, const int32_t* counts,
 int cs_unpin_slots(cs_pool_t pool, const uint32_t* slots, int n) {
     return guard([&] {
         if (!pool || n < 0 || (n > 0 && !slots)) throw std::invalid_argument("cs_unpin_slots: null argument");
+        pool->sync();  // (an engine's last admission may still be finishing its prescan)
         pool->flush_unpins();
         pool->pre_ok = false;
         pool->d_aux.ensure(sizeof(uint32_t) * std::max(n, 1));
@@ -932,6 +982,7 @@ int cs_restore(cs_pool_t pool, const uint64_t* keys, const uint64_t* lt, const u
 int cs_score_snapshot(cs_pool_t pool, uint64_t now_tick, uint64_t* keys, double* scores, int64_t cap, int64_t* n) {
     return guard([&] {
         if (!pool) throw std::invalid_argument("cs_score_snapshot: null pool");
+        pool->sync();  // (an engine's last admission may still be finishing its prescan)
         pool->flush_unpins();
         const long long N = pool->P.cap;
         csb::DevBuf k, s, cnt, scr;
@@ -955,6 +1006,7 @@ int cs_score_snapshot(cs_pool_t pool, uint64_t now_tick, uint64_t* keys, double*
 int cs_hops(cs_pool_t pool, int* hops, int n) {
     return guard([&] {
         if (!pool || !hops || n < 0 || n > pool->P.a_cap) throw std::invalid_argument("cs_hops: bad argument");
+        pool->sync();  // (an engine's last admission may still be finishing its prescan)
         csb::Ctrl c;
         ck(cudaMemcpy(&c, pool->P.ctrl, sizeof(c), cudaMemcpyDeviceToHost), "ctrl D2H");
         std::vector<unsigned char> h(std::max(n, 1));
@@ -966,6 +1018,7 @@ int cs_hops(cs_pool_t pool, int* hops, int n) {
 int cs_poll_actions(cs_pool_t pool, int* targets, uint64_t* ticks, int cap, int* n) {
     return guard([&] {
         if (!pool || !n) throw std::invalid_argument("cs_poll_actions: null argument");
+        pool->sync();  // (an engine's last admission may still be finishing its prescan)
         const int m = (int)pool->pending_targets.size();
         for (int i = 0; i < m && i < cap; ++i) {
             if (targets) targets[i] = pool->pending_targets[i];

@@ -72,6 +72,20 @@ struct cs_pool {
     // timing (CUDA events around each admission launch)
     bool timing = false;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // per-admission timing without a sync: event pairs resolved once they complete
+    struct TimedLaunch {
+        cudaEvent_t e0, e1;
+        bool scan;
+    };
+    std::vector<TimedLaunch> t_pending;
+    std::vector<cudaEvent_t> t_free;
+    cudaEvent_t take_event();
+    void resolve_timing(bool wait);
+    // waits for this launch's status (AdmitStatus::done_seq), not for the kernel's end
+    void wait_status(unsigned long long seq, const char* what);
+    // engine loop only: admit() returns at the status flag, not at the kernel's end (every
+    // public pool entry point syncs first)
+    bool early_status = false;
     double admit_ms = 0.0, scan_launch_ms = 0.0;
     long long admit_launches = 0, scan_launches = 0, scans_total = 0, table_rebuilds = 0;
     long long launches = 0;  // every kernel this handle launched (the bench's gpu_launches)
@@ -124,5 +138,8 @@ struct cs_pool {
     void flush_unpins();
     // Applies queued block-table updates (admissions defer them to the next launch's phase 0).
     void flush_table();
-    void sync() { csb::ck(cudaStreamSynchronize(stream), "cudaStreamSynchronize"); }
+    void sync() {
+        csb::ck(cudaStreamSynchronize(stream), "cudaStreamSynchronize");
+        resolve_timing(true);
+    }
 };
