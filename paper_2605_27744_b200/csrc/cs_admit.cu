@@ -1222,6 +1222,16 @@ __device__ __forceinline__ unsigned long long next_hint(unsigned long long v1, u
     return sat_add(v1, sat_add(span, span));
 }
 
+// The same target (about 2 kPreK candidates next pass) from the density just below the kPreK-th
+// value: the span of the upper half of the list, doubled past it. A list whose oldest entries are
+// far older than the rest (old snapshot blocks ahead of recently unpinned ones) would make the
+// v1-based estimate overshoot by orders of magnitude. Any hint is safe; it only sizes the pass.
+__device__ __forceinline__ unsigned long long next_hint_mid(unsigned long long vmid, unsigned long long base) {
+    if (base >= kNoBound || vmid >= kNoBound || base < vmid) return kNoBound;
+    const unsigned long long span = base - vmid;
+    return sat_add(base, sat_add(span, span));
+}
+
 __device__ void prescan_pass(const DevPool& P, const ScanBufs& B, ScanSmem& S, unsigned char* dsm, int par,
                              bool after_writes) {
     Ctrl* C = P.ctrl;
@@ -1406,7 +1416,10 @@ __device__ void prescan_finalize(const DevPool& P, const ScanBufs& B, SelectSmem
     const size_t base = ((size_t)par * 3 + l) * kPendCap;
     if (local && m <= kDirectPre) {
         // few candidates (the usual case): every entry's rank in one pass, no radix rounds
-        if (tid == 0) Sel.prefix = kNoBound;
+        if (tid == 0) {
+            Sel.prefix = kNoBound;
+            Sel.acc_or = kNoBound;
+        }
         __syncthreads();
         unsigned long long vk = kNoBound, v1 = kNoBound;
         for (int j = tid; j < m; j += T) {
@@ -1418,6 +1431,7 @@ __device__ void prescan_finalize(const DevPool& P, const ScanBufs& B, SelectSmem
             }
             if (r == kPreK - 1) vk = x;
             if (r == 0) v1 = x;
+            if (r == kPreK / 2 - 1) Sel.acc_or = x;
         }
         if (vk != kNoBound) Sel.prefix = vk;
         if (v1 != kNoBound) Sel.hmax = v1;
@@ -1428,7 +1442,7 @@ __device__ void prescan_finalize(const DevPool& P, const ScanBufs& B, SelectSmem
             const int bad = *(volatile int*)&C->pre_bad[par];
             P.pl_n[par * 3 + l] = n;
             P.pl_T[par * 3 + l] = Tl;
-            P.pre_hint[l] = n == 0 ? kNoBound : bad ? Tl : next_hint(Sel.hmax, Tl);
+            P.pre_hint[l] = n == 0 ? kNoBound : bad ? Tl : n == kPreK ? next_hint_mid(Sel.acc_or, Tl) : next_hint(Sel.hmax, Tl);
         }
         __syncthreads();
         return;
@@ -1447,6 +1461,8 @@ __device__ void prescan_finalize(const DevPool& P, const ScanBufs& B, SelectSmem
     }
     __syncthreads();
     const int n = Sel.tmp;  // distinct ticks: exactly min(m, kPreK)
+    if (tid == 0) Sel.acc_or = kNoBound;
+    __syncthreads();
     unsigned long long v1 = kNoBound;
     for (int j = tid; j < n; j += T) {
         const unsigned long long x = B.sd_lt[j];
@@ -1454,6 +1470,7 @@ __device__ void prescan_finalize(const DevPool& P, const ScanBufs& B, SelectSmem
         P.pl_lt[base + r] = x;
         P.pl_slot[base + r] = B.sd_slot[j];
         if (r == 0) v1 = x;
+        if (r == kPreK / 2 - 1) Sel.acc_or = x;
     }
     if (v1 != kNoBound) Sel.prefix = v1;  // the unique rank-0 entry
     __syncthreads();
@@ -1463,7 +1480,10 @@ __device__ void prescan_finalize(const DevPool& P, const ScanBufs& B, SelectSmem
         P.pl_n[par * 3 + l] = n;
         P.pl_T[par * 3 + l] = Tl;
         // an overflowed pass staged a subset: its kPreK-th is a tighter, safe next threshold
-        P.pre_hint[l] = n == 0 ? kNoBound : bad ? (m > kPreK ? v : h) : next_hint(Sel.prefix, Tl);
+        P.pre_hint[l] = n == 0 ? kNoBound
+                        : bad ? (m > kPreK ? v : h)
+                        : n == kPreK ? next_hint_mid(Sel.acc_or, Tl)
+                                     : next_hint(Sel.prefix, Tl);
     }
     __syncthreads();
 }
@@ -1534,19 +1554,25 @@ __device__ void prescan_finish(const DevPool& P, const AdmitArgs& a, const ScanB
         if (tid == 0) P.dbg[blockIdx.x * 16 + 8] = gtimer();
         const int n = ng[grp];  // min(m, kPreK) (distinct ticks)
         const size_t base = ((size_t)par * 3 + grp) * kPendCap;
+        if (gt == 0) Sgr.acc_or = kNoBound;  // (free after the select) rank kPreK / 2 - 1
+        group_sync(1 + grp, gn);
         for (int j = gt; j < n; j += gn) {
             const unsigned long long x = tl[j];
             const int r = count_below(tl, n, x);
             P.pl_lt[base + r] = x;
             P.pl_slot[base + r] = ts[j];
             if (r == 0) Sgr.hmax = x;
+            if (r == kPreK / 2 - 1) Sgr.acc_or = x;
         }
         group_sync(1 + grp, gn);
         if (gt == 0) {
             const unsigned long long Tl = m > kPreK ? v : h[grp];
             P.pl_n[par * 3 + grp] = n;
             P.pl_T[par * 3 + grp] = Tl;
-            P.pre_hint[grp] = n == 0 ? kNoBound : bad ? Tl : next_hint(Sgr.hmax, Tl);
+            P.pre_hint[grp] = n == 0 ? kNoBound
+                              : bad ? Tl
+                              : n == kPreK ? next_hint_mid(Sgr.acc_or, Tl)
+                                           : next_hint(Sgr.hmax, Tl);
         }
         __syncthreads();
     } else {  // many candidates (a loose threshold): radix select per list

@@ -17,7 +17,7 @@ NAMES = {0: "p0 start", 1: "table queue", 2: "unpins", 3: "probe", 13: "record",
 pool = 16 << 20
 spec, seed = bench.rank_workload(40000, pool, 0)
 eng = bench.build_engine(W, spec, pool, 0, False, seed)
-eng.run_timed(100)
+eng.run_timed(int(sys.argv[1]) if len(sys.argv) > 1 else 100)
 rows = []
 fin = []
 ends = []
