@@ -30,8 +30,8 @@ namespace csb {
 
 constexpr int kThreads = 512;            // one CTA per SM (cooperative grid)
 constexpr int kV = 4;                    // slots per thread per tile (2 x LDG.128 + 2 x LDG.128)
-constexpr int kTile = kThreads * kV;     // 2048 slots = 32 KiB of SoA per tile
-constexpr int kRing = 3;                 // TMA stages (32 KiB of SoA each) per CTA
+constexpr int kTile = kThreads * kV;     // 2048 slots = 16 KiB of packed scan words per tile
+constexpr int kRing = 6;                 // TMA stages (16 KiB of packed words each) per CTA
 constexpr int kStage = 6144;             // staged candidates per CTA (all lists share it)
 constexpr int kFlushAt = kStage - 2 * kTile;  // a tile appends at most 2 entries per slot
 constexpr int kSide = kMaxLists * (kChunk + 1);
@@ -94,8 +94,7 @@ constexpr size_t kOffSdSlot = kOffSdLt + 8ull * kSide;
 constexpr size_t kOffSdList = kOffSdSlot + 4ull * kSide;
 constexpr size_t kOffCls = (kOffSdList + kSide + 15) & ~size_t(15);
 constexpr size_t kOffRing = (kOffCls + kMaxAgents + 127) & ~size_t(127);  // TMA ring (128-B aligned)
-constexpr size_t kRingLt = 8ull * kTile, kRingAg = 4ull * kTile, kRingRf = 4ull * kTile;
-constexpr size_t kRingStage = kRingLt + kRingAg + kRingRf;  // 32 KiB
+constexpr size_t kRingStage = 8ull * kTile;  // 16 KiB: one packed word (pk) per slot
 constexpr size_t kDynSmem = kOffRing + kRing * kRingStage;
 
 __device__ __forceinline__ ScanBufs scan_bufs(unsigned char* d) {
@@ -548,7 +547,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned in
 
 // One streaming pass over this CTA's contiguous slot range: 16 B per slot read exactly once.
 // The SoA arrives through a kRing-stage TMA ring (cp.async.bulk into shared memory, one
-// elected thread issues, mbarrier transaction counts complete), so kRing-1 tiles of 32 KiB
+// elected thread issues, mbarrier transaction counts complete), so kRing-1 tiles of 16 KiB
 // are in flight independently of the threads' progress and no registers hold in-flight data.
 // Survivors go to a staging pool flushed (exact per-list select) only when it could overflow.
 __device__ __forceinline__ void mbar_arrive(unsigned long long* m) {
@@ -624,22 +623,12 @@ __device__ __forceinline__ int append4(unsigned int acc, const unsigned long lon
 __device__ __forceinline__ void read4(const unsigned char* st, int tid, bool valid, unsigned long long (&x4)[kV],
                                       unsigned int (&a4)[kV], unsigned int (&r4)[kV]) {
     if (valid) {
-        const ulonglong2 l01 = *reinterpret_cast<const ulonglong2*>(st + (size_t)tid * 32);
-        const ulonglong2 l23 = *reinterpret_cast<const ulonglong2*>(st + (size_t)tid * 32 + 16);
-        const uint4 aa = *reinterpret_cast<const uint4*>(st + kRingLt + (size_t)tid * 16);
-        const uint4 rr = *reinterpret_cast<const uint4*>(st + kRingLt + kRingAg + (size_t)tid * 16);
-        x4[0] = l01.x;
-        x4[1] = l01.y;
-        x4[2] = l23.x;
-        x4[3] = l23.y;
-        a4[0] = aa.x;
-        a4[1] = aa.y;
-        a4[2] = aa.z;
-        a4[3] = aa.w;
-        r4[0] = rr.x;
-        r4[1] = rr.y;
-        r4[2] = rr.z;
-        r4[3] = rr.w;
+        const ulonglong2 w01 = *reinterpret_cast<const ulonglong2*>(st + (size_t)tid * 32);
+        const ulonglong2 w23 = *reinterpret_cast<const ulonglong2*>(st + (size_t)tid * 32 + 16);
+        pk_decode(w01.x, x4[0], a4[0], r4[0]);
+        pk_decode(w01.y, x4[1], a4[1], r4[1]);
+        pk_decode(w23.x, x4[2], a4[2], r4[2]);
+        pk_decode(w23.y, x4[3], a4[3], r4[3]);
     } else {
 #pragma unroll
         for (int k = 0; k < kV; ++k) {
@@ -686,22 +675,12 @@ __device__ __forceinline__ unsigned int unpin_at(const AdmitArgs& a, int i) {
 __device__ __forceinline__ void load4(const DevPool& P, long long i0, bool valid, unsigned long long (&x4)[kV],
                                       unsigned int (&a4)[kV], unsigned int (&r4)[kV]) {
     if (valid) {
-        const ulonglong2 l01 = __ldcg(reinterpret_cast<const ulonglong2*>(P.lt + i0));
-        const ulonglong2 l23 = __ldcg(reinterpret_cast<const ulonglong2*>(P.lt + i0 + 2));
-        const uint4 aa = __ldcg(reinterpret_cast<const uint4*>(P.agent + i0));
-        const uint4 rr = __ldcg(reinterpret_cast<const uint4*>(P.refs + i0));
-        x4[0] = l01.x;
-        x4[1] = l01.y;
-        x4[2] = l23.x;
-        x4[3] = l23.y;
-        a4[0] = aa.x;
-        a4[1] = aa.y;
-        a4[2] = aa.z;
-        a4[3] = aa.w;
-        r4[0] = rr.x;
-        r4[1] = rr.y;
-        r4[2] = rr.z;
-        r4[3] = rr.w;
+        const ulonglong2 w01 = __ldcg(reinterpret_cast<const ulonglong2*>(P.pk + i0));
+        const ulonglong2 w23 = __ldcg(reinterpret_cast<const ulonglong2*>(P.pk + i0 + 2));
+        pk_decode(w01.x, x4[0], a4[0], r4[0]);
+        pk_decode(w01.y, x4[1], a4[1], r4[1]);
+        pk_decode(w23.x, x4[2], a4[2], r4[2]);
+        pk_decode(w23.y, x4[3], a4[3], r4[3]);
     } else {
 #pragma unroll
         for (int k = 0; k < kV; ++k) {
@@ -919,10 +898,8 @@ __device__ void scan_pass(const DevPool& P, int NL, int keep, const ScanBufs& B,
         const long long b0 = lo + (long long)t * TV;
         const unsigned int nsl = (unsigned int)min(TV, hi - b0);
         unsigned char* st = ring + (size_t)s * kRingStage;
-        mbar_expect_tx(&S.mbar[s], nsl * 16u);
-        bulk_g2s(st, P.lt + b0, nsl * 8u, &S.mbar[s]);
-        bulk_g2s(st + kRingLt, P.agent + b0, nsl * 4u, &S.mbar[s]);
-        bulk_g2s(st + kRingLt + kRingAg, P.refs + b0, nsl * 4u, &S.mbar[s]);
+        mbar_expect_tx(&S.mbar[s], nsl * 8u);
+        bulk_g2s(st, P.pk + b0, nsl * 8u, &S.mbar[s]);  // the packed scan words
     };
     if (tid == 0) {
         P.dbg[blockIdx.x * 16 + 0] = gtimer();
@@ -1303,10 +1280,8 @@ __device__ void prescan_pass(const DevPool& P, const ScanBufs& B, ScanSmem& S, u
                 const long long b0 = lo + (long long)t * TV;
                 const unsigned int nsl = (unsigned int)min(TV, hi - b0);
                 unsigned char* st = ring + (size_t)s * kRingStage;
-                mbar_expect_tx(&S.mbar[s], nsl * 16u);
-                bulk_g2s(st, P.lt + b0, nsl * 8u, &S.mbar[s]);
-                bulk_g2s(st + kRingLt, P.agent + b0, nsl * 4u, &S.mbar[s]);
-                bulk_g2s(st + kRingLt + kRingAg, P.refs + b0, nsl * 4u, &S.mbar[s]);
+                mbar_expect_tx(&S.mbar[s], nsl * 8u);
+                bulk_g2s(st, P.pk + b0, nsl * 8u, &S.mbar[s]);  // the packed scan words
             }
         }
         __syncwarp();
@@ -2361,6 +2336,7 @@ __device__ void replay_apply(const DevPool& P, const AdmitArgs& a, ReplaySmem& R
             P.lt[v] = kFreeTick;
             P.refs[v] = 0u;
             P.agent[v] = kNoAgent;
+            P.pk[v] = kPkFreeWord;
         }
     }
     // A serial chunk may evict a later prompt block and re-admit it into the victim's slot:
@@ -2373,15 +2349,18 @@ __device__ void replay_apply(const DevPool& P, const AdmitArgs& a, ReplaySmem& R
             const int gi = lo + i;
             P.key[s] = a.keys[gi];
             P.tokens[s] = a.counts[gi];
-            P.agent[s] = (a.agent != kNoAgent && gi < A.anchor) ? a.agent : kNoAgent;
+            const unsigned int ag = (a.agent != kNoAgent && gi < A.anchor) ? a.agent : kNoAgent;
+            P.agent[s] = ag;
             P.lt[s] = R.out_lt[i];
             P.refs[s] = 1u;
+            P.pk[s] = pk_make(R.out_lt[i], ag, true);
             const int q = q_i + atomicAdd(&R.n_ins, 1);
             P.tq_key[P.p_cap + q] = a.keys[gi];
             P.tq_slot[q] = s;
         } else {
             P.lt[s] = R.out_lt[i];
             atomicAdd(&P.refs[s], 1u);
+            P.pk[s] = pk_make(R.out_lt[i], P.agent[s], true);
         }
         P.p_slot[lo + i] = s;
     }
@@ -2622,6 +2601,7 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
                     const unsigned int us = unpin_at(a, i);
                     if (us == kNoSlot) continue;
                     if (i < nu && atomicSub(&P.refs[us], 1u) == 1u) {
+                        pk_unpinned(P, us);
                         ++dec;
                         if (P.dbg_unpin) P.dbg_unpin[us] = (a.seq << 8) | 1u;
                     }
@@ -2703,6 +2683,7 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
                 for (int i = tid; i < nu; i += T) {
                     const unsigned int us = unpin_at(a, i);
                     if (us != kNoSlot && atomicSub(&P.refs[us], 1u) == 1u) {
+                        pk_unpinned(P, us);
                         ++dec;
                         if (P.dbg_unpin) P.dbg_unpin[us] = (a.seq << 8) | 2u;
                     }
@@ -2744,6 +2725,7 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
                     cached += a.counts[i];
                     const unsigned int ts = P.p_slot[i];
                     P.lt[ts] = A.tick + 1 + (unsigned long long)i;  // EngineSim::touch
+                    pk_touch(P, ts, A.tick + 1 + (unsigned long long)i);
                     if (a.touch_agent) a.touch_agent[i] = P.agent[ts];
                     if (early) tset_insert(es.tset, ts);
                 }
@@ -3065,6 +3047,7 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
                 if (a.pins_out) a.pins_out[i] = s;
                 if (a.flags & kUnpinAfter) {
                     if (atomicSub(&P.refs[s], 1u) == 1u) {
+                        pk_unpinned(P, s);
                         ++dec;
                         if (P.dbg_unpin) P.dbg_unpin[s] = (a.seq << 8) | 3u;
                     }

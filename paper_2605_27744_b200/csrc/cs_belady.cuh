@@ -283,6 +283,7 @@ __device__ void bel_replay(const DevPool& P, const AdmitArgs& a, unsigned char* 
                     P.bel_kid_slot[P.bel_kid[v]] = kNoSlot;
                     P.lt[v] = kFreeTick;
                     P.agent[v] = kNoAgent;
+                    P.pk[v] = kPkFreeWord;
                     P.free_stack[top++] = v;
                     --res;
                 }
@@ -297,6 +298,7 @@ __device__ void bel_replay(const DevPool& P, const AdmitArgs& a, unsigned char* 
                 P.agent[s] = (a.agent != kNoAgent && i < anchor) ? a.agent : kNoAgent;  // engine.cpp:155-157
                 P.lt[s] = t0 + 1 + (unsigned long long)i;
                 P.refs[s] = 1u;
+                P.pk[s] = pk_make(t0 + 1 + (unsigned long long)i, P.agent[s], true);
                 ++pin;
                 ++res;
                 reused += table_insert(P, key, s);
@@ -307,6 +309,7 @@ __device__ void bel_replay(const DevPool& P, const AdmitArgs& a, unsigned char* 
             } else {
                 P.lt[s] = t0 + 1 + (unsigned long long)i;  // EngineSim::touch
                 if (P.refs[s]++ == 0u) ++pin;
+                P.pk[s] = pk_make(t0 + 1 + (unsigned long long)i, P.agent[s], true);
             }
             if (a.pins_out) a.pins_out[i] = s;
         }
@@ -360,7 +363,10 @@ __global__ void __launch_bounds__(kBelThreads, 1) belady_admit_kernel(DevPool P,
         const int nu = unpin_total(a, false);
         for (int i = tid; i < nu; i += T) {  // EngineSim::unpin of completed requests (engine.cpp:170-180)
             const unsigned int us = unpin_at(a, i);
-            if (us != kNoSlot && atomicSub(&P.refs[us], 1u) == 1u) ++dec;
+            if (us != kNoSlot && atomicSub(&P.refs[us], 1u) == 1u) {
+                ++dec;
+                pk_unpinned(P, us);
+            }
         }
         dec = block_sum(dec, S.red);
         if (tid == 0) C->pinned -= dec;
@@ -404,6 +410,7 @@ __global__ void __launch_bounds__(kBelThreads, 1) belady_admit_kernel(DevPool P,
                 const unsigned int s = P.p_slot[i];
                 P.lt[s] = t0 + 1 + (unsigned long long)i;
                 if (atomicAdd(&P.refs[s], 1u) == 0u) ++pinc;
+                P.pk[s] = pk_make(t0 + 1 + (unsigned long long)i, P.agent[s], true);
                 if (a.pins_out) a.pins_out[i] = s;
             }
             cached = block_sum(cached, S.red);
@@ -433,7 +440,10 @@ __global__ void __launch_bounds__(kBelThreads, 1) belady_admit_kernel(DevPool P,
         if (B->started && !B->error && (a.flags & kUnpinAfter) && a.pins_out) {
             long long dec = 0;
             for (int i = tid; i < an; i += T)
-                if (atomicSub(&P.refs[a.pins_out[i]], 1u) == 1u) ++dec;
+                if (atomicSub(&P.refs[a.pins_out[i]], 1u) == 1u) {
+                    ++dec;
+                    pk_unpinned(P, a.pins_out[i]);
+                }
             dec = block_sum(dec, S.red);
             if (tid == 0) C->pinned -= dec;
         }

@@ -173,7 +173,9 @@ struct DevPool {
     long long window;
     unsigned long long tmask;
 
-    // SoA pool: the scan reads lt/agent/refs = 16 B per slot
+    // SoA pool (the exact state) + the packed scan word of every slot (pk_make): the scan
+    // streams 8 B per slot instead of lt/agent/refs' 16 B
+    unsigned long long* pk;
     unsigned long long* lt;
     unsigned int* agent;
     unsigned int* refs;
@@ -263,6 +265,32 @@ struct DevPool {
     BelCtl* bel_ctl;
 };
 
+// ---------------------------------------------------------------- packed scan word
+// bits 0..39 last_touch (kPkFree: free slot), 40..52 agent index (kPkNoAgent: none), 63 pinned
+// (refs > 0). Ticks stay below 2^40 - 1 (the host checks), so the scan's decoded last_touch is
+// the exact tick. Every writer of lt / agent / a refs 0 <-> 1 transition keeps it in step.
+constexpr unsigned long long kPkLtMask = (1ull << 40) - 1ull;
+constexpr unsigned long long kPkFree = kPkLtMask;
+constexpr unsigned long long kPkNoAgent = 0x1FFFull;
+constexpr unsigned long long kPkPin = 1ull << 63;
+constexpr unsigned long long kPkFreeWord = kPkFree | (kPkNoAgent << 40);
+constexpr unsigned long long kMaxTick = kPkLtMask - 1ull;
+
+__host__ __device__ __forceinline__ unsigned long long pk_make(unsigned long long lt, unsigned int agent, bool pinned) {
+    const unsigned long long l = lt == kFreeTick ? kPkFree : (lt & kPkLtMask);
+    const unsigned long long a = agent == kNoAgent ? kPkNoAgent : (unsigned long long)(agent & 0x1FFFu);
+    return l | (a << 40) | (pinned ? kPkPin : 0ull);
+}
+
+__host__ __device__ __forceinline__ void pk_decode(unsigned long long w, unsigned long long& lt, unsigned int& agent,
+                                                   unsigned int& pinned) {
+    const unsigned long long l = w & kPkLtMask;
+    const unsigned long long a = (w >> 40) & kPkNoAgent;
+    lt = l == kPkFree ? kFreeTick : l;
+    agent = a == kPkNoAgent ? kNoAgent : (unsigned int)a;
+    pinned = (unsigned int)(w >> 63);
+}
+
 #ifdef __CUDACC__
 // ---------------------------------------------------------------- block table
 
@@ -329,6 +357,13 @@ __device__ __forceinline__ void table_erase(const DevPool& P, unsigned long long
         h = (h + 1) & P.tmask;
     }
     __trap();
+}
+
+__device__ __forceinline__ void pk_unpinned(const DevPool& P, unsigned int s) { atomicAnd(P.pk + s, ~kPkPin); }
+
+// a touch of a resident block (EngineSim::touch): last_touch changes, agent and pin bit do not
+__device__ __forceinline__ void pk_touch(const DevPool& P, unsigned int s, unsigned long long lt) {
+    P.pk[s] = (P.pk[s] & ~kPkLtMask) | (lt & kPkLtMask);
 }
 
 // ---------------------------------------------------------------- exact fp64 scoring

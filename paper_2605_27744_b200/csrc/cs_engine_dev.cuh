@@ -73,6 +73,7 @@ __device__ void eng_complete(const DevPool& P, const EngDev& E, EngState& s) {  
                 for (int i = 0; i < s.unpin_n[k]; ++i) {
                     const unsigned int us = s.unpin_ptr[k][i];
                     if (us != kNoSlot && atomicSub(&P.refs[us], 1u) == 1u) {
+                        pk_unpinned(P, us);
                         ++dec;
                         if (P.dbg_unpin) P.dbg_unpin[us] = (s.seq << 8) | 4u;
                     }

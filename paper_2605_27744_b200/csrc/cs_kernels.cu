@@ -27,6 +27,7 @@ __global__ void init_pool_kernel(DevPool P) {
         P.lt[s] = kFreeTick;
         P.agent[s] = kNoAgent;
         P.refs[s] = 0u;
+        P.pk[s] = kPkFreeWord;
     }
     for (long long e = i; e <= (long long)P.tmask; e += stride) {
         P.table[e].key = 0ull;
@@ -195,7 +196,10 @@ __global__ void unpin_kernel(DevPool P, const unsigned int* slots, int n) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     int dec = 0;
     if (i < n && slots[i] != kNoSlot) {  // kNoSlot: a position another shard owns
-        if (atomicSub(&P.refs[slots[i]], 1u) == 1u) dec = 1;
+        if (atomicSub(&P.refs[slots[i]], 1u) == 1u) {
+            dec = 1;
+            pk_unpinned(P, slots[i]);
+        }
     }
     dec = __reduce_add_sync(0xffffffffu, dec);
     if (lane_id() == 0 && dec) atomicAdd(reinterpret_cast<unsigned long long*>(&P.ctrl->pinned),
@@ -214,6 +218,7 @@ __global__ void restore_kernel(DevPool P, const unsigned long long* keys, const 
     P.agent[s] = agents ? agents[i] : kNoAgent;
     const unsigned int r = refs ? refs[i] : 0u;
     P.refs[s] = r;
+    P.pk[s] = pk_make(lt[i], agents ? agents[i] : kNoAgent, r != 0u);
     P.tokens[s] = 16;
     const int reused = table_insert(P, keys[i], s);
     if (r) atomicAdd(acc, 1ull);

@@ -99,6 +99,7 @@ void cs_pool::create(const cs_pool_cfg& c, long long shard_slots, cs_comm* cm) {
     p.tmask = tcap - 1;
 
     p.cap_scan = (p.cap + 63) & ~63ll;  // bulk copies move whole 16-B granules
+    p.pk = dmalloc<unsigned long long>(p.cap_scan, "pk");
     p.lt = dmalloc<unsigned long long>(p.cap_scan, "lt");
     p.agent = dmalloc<unsigned int>(p.cap_scan, "agent");
     p.refs = dmalloc<unsigned int>(p.cap_scan, "refs");
@@ -202,7 +203,7 @@ void cs_pool::create(const cs_pool_cfg& c, long long shard_slots, cs_comm* cm) {
 
 void cs_pool::destroy() {
     csb::DevPool& p = P;
-    void* ptrs[] = {p.lt, p.agent, p.refs, p.key, p.tokens, p.table, p.free_stack, p.evlog, p.counts, p.totals,
+    void* ptrs[] = {p.pk, p.lt, p.agent, p.refs, p.key, p.tokens, p.table, p.free_stack, p.evlog, p.counts, p.totals,
                     p.win_a, p.win_b, p.hop, p.cls, p.agent_ids, p.ctrl, p.gbound, p.gcount, p.fin_lt, p.fin_slot,
                     p.fin_n, p.p_slot, p.p_refs0, p.gbuf_lt, p.gbuf_slot, p.ghint, p.gmaxk, p.grej, p.dbg, p.gsmall, p.gmin, p.tq_key, p.tq_slot,
                     p.sh_send1, p.sh_recv1, p.sh_send2, p.sh_recv2, p.sh_state, p.sh_gslot, p.sh_grefs0,
@@ -438,6 +439,9 @@ const csb::AdmitStatus& cs_pool::admit_belady(const csb::AdmitArgs& in, int n_fo
 }
 
 const csb::AdmitStatus& cs_pool::admit(const csb::AdmitArgs& in, int n_for_grid) {
+    // the packed scan word keeps 40 bits of last_touch (cs_device.cuh)
+    if (in.tick_base + 2ull * (unsigned long long)std::max(in.n, 0) + 16ull > csb::kMaxTick)
+        throw CsError(CS_ERR_CAPACITY, "tick space exhausted (last_touch must stay below 2^40 - 1)");
     if (comm) return admit_sharded(in);
     if (P.policy == 3) return admit_belady(in, n_for_grid);
     csb::AdmitArgs a = in;
@@ -925,6 +929,8 @@ int cs_restore(cs_pool_t pool, const uint64_t* keys, const uint64_t* lt, const u
                int64_t n) {
     return guard([&] {
         if (!pool || n < 0 || (n > 0 && (!keys || !lt))) throw std::invalid_argument("cs_restore: null argument");
+        for (int64_t i = 0; i < n; ++i)
+            if (lt[i] >= csb::kMaxTick) throw std::invalid_argument("cs_restore: last_touch must stay below 2^40 - 1");
         pool->flush_unpins();
         pool->flush_table();
         pool->pre_ok = false;

@@ -43,7 +43,10 @@ __device__ void shard_unpins(const DevPool& P, const AdmitArgs& a, RedSmem& Red)
         if (r < a.n_unpin_ranges)
             for (int i = threadIdx.x; i < a.unpin_n[r]; i += blockDim.x) {
                 const unsigned int us = a.unpin_ptr[r][i];
-                if (us != kNoSlot && atomicSub(&P.refs[us], 1u) == 1u) ++dec;
+                if (us != kNoSlot && atomicSub(&P.refs[us], 1u) == 1u) {
+                    ++dec;
+                    pk_unpinned(P, us);
+                }
             }
     dec = block_sum(dec, Red);
     if (threadIdx.x == 0) P.ctrl->pinned -= dec;
@@ -179,7 +182,10 @@ __global__ void __launch_bounds__(512, 1) shard_decide_kernel(DevPool P, AdmitAr
             for (int i = tid; i < f; i += T) {
                 cached += a.counts[i];
                 const unsigned int gs = P.sh_gslot[i];
-                if (own_gslot(P, gs)) P.lt[gs & kShardMask] = A.tick + 1 + (unsigned long long)i;  // EngineSim::touch
+                if (own_gslot(P, gs)) {  // EngineSim::touch
+                    P.lt[gs & kShardMask] = A.tick + 1 + (unsigned long long)i;
+                    pk_touch(P, gs & kShardMask, A.tick + 1 + (unsigned long long)i);
+                }
             }
             cached = block_sum(cached, Red);
             if (tid == 0) {
@@ -618,6 +624,7 @@ __global__ void __launch_bounds__(512, 1) shard_replay_kernel(DevPool P, AdmitAr
                 P.lt[ls] = kFreeTick;
                 P.refs[ls] = 0u;
                 P.agent[ls] = kNoAgent;
+                P.pk[ls] = kPkFreeWord;
             }
         }
     }
@@ -635,6 +642,7 @@ __global__ void __launch_bounds__(512, 1) shard_replay_kernel(DevPool P, AdmitAr
                 P.agent[ls] = (a.agent != kNoAgent && gi < A.anchor) ? a.agent : kNoAgent;
                 P.lt[ls] = R.out_lt[i];
                 P.refs[ls] = 1u;
+                P.pk[ls] = pk_make(R.out_lt[i], P.agent[ls], true);
                 const int q = q_i + atomicAdd(&R.n_ins, 1);
                 P.tq_key[P.p_cap + q] = a.keys[gi];
                 P.tq_slot[q] = ls;
@@ -645,6 +653,7 @@ __global__ void __launch_bounds__(512, 1) shard_replay_kernel(DevPool P, AdmitAr
             const unsigned int ls = s & kShardMask;
             P.lt[ls] = R.out_lt[i];
             if (atomicAdd(&P.refs[ls], 1u) == 0u) ++own_pin;
+            P.pk[ls] = pk_make(R.out_lt[i], P.agent[ls], true);
         }
         P.sh_gslot[lo + i] = s;
     }
@@ -699,7 +708,10 @@ __global__ void __launch_bounds__(512, 1) shard_replay_kernel(DevPool P, AdmitAr
                 // the block's pin count drops back to its value before this admission: it becomes
                 // unpinned iff it was new or unpinned then (decidable on every shard)
                 if (P.sh_grefs0[i] == 0u) ++dec_g;  // new blocks were absent at the probe: refs0 0
-                if (own && atomicSub(&P.refs[s & kShardMask], 1u) == 1u) ++dec_own;
+                if (own && atomicSub(&P.refs[s & kShardMask], 1u) == 1u) {
+                    ++dec_own;
+                    pk_unpinned(P, s & kShardMask);
+                }
             }
         }
     }
