@@ -545,7 +545,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned in
         : "memory");
 }
 
-// One streaming pass over this CTA's contiguous slot range: 16 B per slot read exactly once.
+// One streaming pass over this CTA's contiguous slot range: one 8-B packed word per slot, read once.
 // The SoA arrives through a kRing-stage TMA ring (cp.async.bulk into shared memory, one
 // elected thread issues, mbarrier transaction counts complete), so kRing-1 tiles of 16 KiB
 // are in flight independently of the threads' progress and no registers hold in-flight data.
@@ -839,7 +839,7 @@ __device__ void producer_prep(const DevPool& P, const AdmitArgs& a, const ScanBu
     if (lane == 0) S.prep_done = 1;
 }
 
-// One streaming pass over this CTA's contiguous slot range: 16 B per slot read exactly once.
+// One streaming pass over this CTA's contiguous slot range: one 8-B packed word per slot, read once.
 // The SoA arrives through a kRing-stage TMA ring (cp.async.bulk into shared memory, mbarrier
 // transaction counts), so the loads are independent of the threads' progress.
 //   fast: warp-specialized. A producer warp refills a stage as soon as the 16 consumer warps
