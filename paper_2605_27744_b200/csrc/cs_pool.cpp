@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <thread>
 
 using csb::ck;
 using csb::CsError;
@@ -580,6 +581,7 @@ void cs_pool::wait_status(unsigned long long seq, const char* what) {
     volatile unsigned long long* flag = &st->done_seq;
     for (unsigned long long spin = 0;; ++spin) {
         if (*flag == seq) return;
+        if (spin >= 256) std::this_thread::yield();  // a long wait: let other host threads run
         if ((spin & 1023) == 1023) {
             const cudaError_t e = cudaStreamQuery(stream);
             if (e == cudaSuccess) {  // the kernel has ended: its flag write is visible by now
