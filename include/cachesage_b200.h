@@ -146,6 +146,11 @@ typedef struct cs_pool_stats {
 int cs_pool_get_stats(cs_pool_t pool, cs_pool_stats* out);
 /* Instrumentation: per-CTA scan timestamps of the last admission (grid x 8 u64). */
 int cs_pool_debug(cs_pool_t pool, uint64_t* out, int cap, int* grid);
+/* Pool invariants (tests): out[0] = slots whose packed scan word disagrees with the exact
+ * last_touch / agent / pin state, out[1] = resident slots minus the pool's resident count,
+ * out[2] = pinned slots minus its pinned count, out[3] = resident slots the block table does not
+ * map back. All zero on a consistent pool. */
+int cs_pool_check(cs_pool_t pool, int64_t* out4);
 
 /* ------------------------------------------------------------------ engine (EngineSim) */
 

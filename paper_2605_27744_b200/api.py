@@ -414,6 +414,13 @@ class Engine:
         lib().cs_engine_evictions(self.h, _p(out), n)
         return out[:n]
 
+    def check(self):
+        """Pool invariants (cs_pool_check): all zero on a consistent pool."""
+        out = np.zeros(4, np.int64)
+        check(lib().cs_pool_check(lib().cs_engine_pool(self.h), _p(out)))
+        return {"pk_mismatch": int(out[0]), "resident_delta": int(out[1]), "pinned_delta": int(out[2]),
+                "table_mismatch": int(out[3])}
+
     def record_events(self, on=True):
         """Record EngineSim's event stream (engine.cpp:72-88) for write_outputs' events.jsonl;
         call before the first step (host scheduler only)."""

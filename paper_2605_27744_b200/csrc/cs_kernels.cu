@@ -363,6 +363,34 @@ cudaError_t launch_scores(const DevPool& P, unsigned long long now, unsigned lon
     return cudaGetLastError();
 }
 
+// Pool invariants (debug / tests): out[0] = slots whose packed scan word disagrees with
+// lt / agent / refs, out[1] = resident slots, out[2] = pinned slots, out[3] = resident slots the
+// block table does not map back to themselves.
+__global__ void check_pool_kernel(DevPool P, unsigned long long* out) {
+    unsigned long long bad = 0, res = 0, pin = 0, tab = 0;
+    for (long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x; s < P.cap_scan;
+         s += (long long)gridDim.x * blockDim.x) {
+        const unsigned long long lt = P.lt[s];
+        const unsigned int r = P.refs[s];
+        const unsigned long long want = lt == kFreeTick ? kPkFreeWord : pk_make(lt, P.agent[s], r != 0u);
+        bad += P.pk[s] != want;
+        if (lt != kFreeTick) {
+            ++res;
+            pin += r != 0u;
+            tab += table_find(P, P.key[s]) != (unsigned int)s;
+        }
+    }
+    atomicAdd(out + 0, bad);
+    atomicAdd(out + 1, res);
+    atomicAdd(out + 2, pin);
+    atomicAdd(out + 3, tab);
+}
+
+cudaError_t launch_check_pool(const DevPool& P, unsigned long long* out, cudaStream_t s) {
+    check_pool_kernel<<<592, 256, 0, s>>>(P, out);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_table_rebuild(const DevPool& P, cudaStream_t s) {
     table_clear_kernel<<<1184, 256, 0, s>>>(P);
     table_fill_kernel<<<1184, 256, 0, s>>>(P);

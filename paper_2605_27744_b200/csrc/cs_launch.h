@@ -145,6 +145,7 @@ cudaError_t launch_probe(const DevPool& P, const unsigned long long* keys, int n
 cudaError_t launch_scores(const DevPool& P, unsigned long long now, unsigned long long* keys, double* scores,
                           long long* n_out, unsigned long long* scratch, cudaStream_t s);
 cudaError_t launch_table_rebuild(const DevPool& P, cudaStream_t s);
+cudaError_t launch_check_pool(const DevPool& P, unsigned long long* out, cudaStream_t s);  // out[4], zeroed
 // Applies the block-table updates the last admission queued (before any other table user).
 cudaError_t launch_table_flush(const DevPool& P, cudaStream_t s);
 

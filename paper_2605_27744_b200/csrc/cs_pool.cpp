@@ -1040,6 +1040,30 @@ int cs_poll_actions(cs_pool_t pool, int* targets, uint64_t* ticks, int cap, int*
 }
 
 /* Instrumentation: per-CTA timestamps of the last scan (grid x 8 u64, globaltimer ns). */
+int cs_pool_check(cs_pool_t pool, int64_t* out4) {
+    return guard([&] {
+        if (!pool || !out4) throw std::invalid_argument("cs_pool_check: null argument");
+        pool->flush_unpins();
+        pool->flush_table();
+        pool->sync();
+        unsigned long long* d = nullptr;
+        ck(cudaMalloc(&d, 32), "cudaMalloc");
+        ck(cudaMemset(d, 0, 32), "memset");
+        unsigned long long h[4] = {0, 0, 0, 0};
+        cudaError_t e = csb::launch_check_pool(pool->P, d, pool->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(pool->stream);
+        if (e == cudaSuccess) e = cudaMemcpy(h, d, 32, cudaMemcpyDeviceToHost);
+        cudaFree(d);
+        ck(e, "check_pool_kernel");
+        csb::Ctrl c;
+        ck(cudaMemcpy(&c, pool->P.ctrl, sizeof(c), cudaMemcpyDeviceToHost), "ctrl D2H");
+        out4[0] = (int64_t)h[0];
+        out4[1] = (int64_t)h[1] - c.resident;  // 0 when the count matches the pool's scalar
+        out4[2] = (int64_t)h[2] - c.pinned;
+        out4[3] = (int64_t)h[3];
+    });
+}
+
 int cs_pool_debug(cs_pool_t pool, uint64_t* out, int cap, int* grid) {
     return guard([&] {
         if (!pool || !out) throw std::invalid_argument("cs_pool_debug: null argument");
