@@ -127,6 +127,10 @@ int cs_score_snapshot(cs_pool_t pool, uint64_t now_tick, uint64_t* keys, double*
 
 /* ReachabilityState::hop per agent index (-1 before the first rebuild). */
 int cs_hops(cs_pool_t pool, int* hops, int n);
+/* Installs reachability hops computed elsewhere (e.g. cs_learner_rebuild, or an external
+ * learner): hop per agent index, survival class min(hop, e_max) (reachability.cpp:12-20); the
+ * pool scores with them until its own observe rebuilds. SURVEY §8b cs_set_hops. */
+int cs_set_hops(cs_pool_t pool, const uint8_t* hops, int n);
 
 /* CacheSagePolicy::poll_actions (cachesage_policy.cpp:125-130): drains queued warmups
  * (agent indices, issue ticks) and resets the per-step budget. */

@@ -94,6 +94,7 @@ SIGNATURES = {
     "cs_pool_get_stats": (C.c_int, [vp, C.POINTER(PoolStats)]),
     "cs_pool_debug": (C.c_int, [vp, vp, C.c_int, C.POINTER(C.c_int)]),
     "cs_pool_check": (C.c_int, [vp, vp]),
+    "cs_set_hops": (C.c_int, [vp, vp, C.c_int]),
     "cs_generate_trace": (C.c_int64, [C.POINTER(WorkloadSpec), vp, C.c_int64]),
     "cs_engine_cfg_default": (None, [C.POINTER(EngineCfg)]),
     "cs_engine_create": (C.c_int, [C.POINTER(EngineCfg), C.POINTER(WorkloadSpec), C.POINTER(vp)]),

@@ -120,6 +120,11 @@ class Pool:
         check(lib().cs_score_snapshot(self.h, now_tick, _p(k), _p(s), cap, C.byref(n)))
         return k[:n.value], s[:n.value]
 
+    def set_hops(self, hops):
+        """Install externally computed reachability hops (cs_set_hops), per agent index."""
+        h = np.ascontiguousarray(hops, dtype=np.uint8)
+        check(lib().cs_set_hops(self.h, _p(h), h.size))
+
     def hops(self, n):
         h = np.zeros(max(n, 1), np.int32)
         check(lib().cs_hops(self.h, _p(h), n))

@@ -2,6 +2,7 @@
 #include "cs_pool.hpp"
 
 #include <algorithm>
+#include <cstddef>
 #include <cstdlib>
 #include <cstring>
 #include <thread>
@@ -1008,6 +1009,31 @@ int cs_score_snapshot(cs_pool_t pool, uint64_t now_tick, uint64_t* keys, double*
         const long long c = std::min<long long>(m, cap);
         if (c > 0 && keys) ck(cudaMemcpy(keys, k.p, 8 * c, cudaMemcpyDeviceToHost), "D2H");
         if (c > 0 && scores) ck(cudaMemcpy(scores, s.p, 8 * c, cudaMemcpyDeviceToHost), "D2H");
+    });
+}
+
+int cs_set_hops(cs_pool_t pool, const uint8_t* hops, int n) {
+    return guard([&] {
+        if (!pool || (n > 0 && !hops) || n < 0 || n > pool->P.a_cap) throw std::invalid_argument("cs_set_hops: bad argument");
+        pool->flush_unpins();
+        pool->sync();
+        // ReachabilityState as rebuild_reachability would leave it (reachability.cpp:39-81): the
+        // survival class of an agent is its hop count, capped at e_max (reachability.cpp:12-20)
+        std::vector<unsigned char> h(std::max(n, 1)), c(std::max(n, 1));
+        for (int i = 0; i < n; ++i) {
+            h[i] = hops[i];
+            c[i] = (unsigned char)std::min<int>(hops[i], pool->P.e_max);
+        }
+        if (n > 0) {
+            ck(cudaMemcpyAsync(pool->P.hop, h.data(), n, cudaMemcpyHostToDevice, pool->stream), "hop H2D");
+            ck(cudaMemcpyAsync(pool->P.cls, c.data(), n, cudaMemcpyHostToDevice, pool->stream), "cls H2D");
+        }
+        const int one = 1;
+        ck(cudaMemcpyAsync(reinterpret_cast<char*>(pool->P.ctrl) + offsetof(csb::Ctrl, reach_built), &one, sizeof(int),
+                           cudaMemcpyHostToDevice, pool->stream),
+           "reach_built H2D");
+        pool->pre_ok = false;  // classes changed out of band: no prescan reuse
+        pool->sync();
     });
 }
 
