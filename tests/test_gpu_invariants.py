@@ -54,3 +54,21 @@ def test_invariants_on_a_restored_snapshot():
         assert eng.check() == ZERO
     finally:
         eng.close()
+
+
+def test_tick_space_guard():
+    """The packed scan word keeps 40 bits of last_touch: ticks at or past 2^40 - 1 are refused
+    loudly (restore: invalid argument; an admission: capacity) instead of aliasing."""
+    from paper_2605_27744_b200 import api
+
+    p = api.Pool(64, policy="cachesage")
+    try:
+        with pytest.raises(Exception, match="2\\^40"):
+            p.restore(np.array([5], np.uint64), np.array([(1 << 40) - 1], np.uint64))
+        keys = np.arange(1, 4, dtype=np.uint64)
+        with pytest.raises(Exception, match="tick space"):
+            p.admit_pinned(keys, np.full(3, 16, np.int32), tick_base=(1 << 40) - 8)
+        ev, pins = p.admit_pinned(keys, np.full(3, 16, np.int32), tick_base=(1 << 40) - 64)
+        assert ev.size == 0 and pins.size == 3
+    finally:
+        p.close()
