@@ -381,10 +381,10 @@ const csb::AdmitStatus& cs_pool::admit_belady(const csb::AdmitArgs& in, int n_fo
     a.status = st_dev;
     a.n_agents = n_agents;
     const bool may_evict = (a.flags & csb::kAdmit) && resident + n_for_grid > P.cap;
-    // one CTA per 16K slots: the selection passes are short, the grid barriers are not free
+    // one CTA per 4K slots: the selection passes are short, the grid barriers are not free
     const char* ge = std::getenv("CS_BELADY_CTAS");  // tests: force a grid (multi-CTA select on small pools)
     const int grid_env = ge ? std::atoi(ge) : 0;
-    int grid = may_evict ? (int)std::max(1ll, std::min<long long>(blc.grid, (P.cap + 16383) / 16384)) : 1;
+    int grid = may_evict ? (int)std::max(1ll, std::min<long long>(blc.grid, (P.cap + 4095) / 4096)) : 1;
     if (may_evict && grid_env > 0) grid = std::min(grid_env, blc.grid);
     if ((int)unpin_q.size() > csb::kMaxUnpinRanges) flush_unpins();
     a.n_unpin_ranges = 0;
