@@ -1252,6 +1252,27 @@ __device__ void prescan_pass(const DevPool& P, const ScanBufs& B, ScanSmem& S, u
         }
         if (!S.overflow) append4(acc, x4, cl, i0, 1, B, S, true);
     };
+    // The same classification straight on the packed words (the TMA stream's hot loop, issue-
+    // bound): thresholds clamped below the free tick, so a free slot never passes a compare
+    static_assert(kV == 4, "the packed consumer reads two 16-B vectors per thread");
+    const unsigned long long cE = min(hE, kPkFree - 1ull), cR = min(hR, kPkFree - 1ull), cP = cE;
+    auto classify_append_pk = [&](const ulonglong2 w01, const ulonglong2 w23, bool valid, long long i0) {
+        const unsigned long long w[kV] = {w01.x, w01.y, w23.x, w23.y};
+        unsigned long long x4[kV];
+        int cl[kV];
+        unsigned int acc = 0u;
+#pragma unroll
+        for (int k = 0; k < kV; ++k) {
+            const unsigned long long x = w[k] & kPkLtMask;
+            x4[k] = x;
+            const bool agentless = ((w[k] >> 40) & kPkNoAgent) == kPkNoAgent;
+            cl[k] = agentless ? 0 : 2;
+            acc |= (unsigned int)(x <= cR) << k;
+            acc |= (unsigned int)((long long)w[k] >= 0 && x <= (agentless ? cE : cP)) << (kV + k);
+        }
+        if (!valid) acc = 0u;
+        if (!S.overflow) append4(acc, x4, cl, i0, 1, B, S, true);
+    };
     if (P.stream_generic) {
         // persistent engine kernel: L2-coherent 128-bit loads, one tile prefetched in registers
         if (tid < kThreads) {
@@ -1291,13 +1312,21 @@ __device__ void prescan_pass(const DevPool& P, const ScanBufs& B, ScanSmem& S, u
             const long long i0 = lo + (long long)t * TV + (long long)tid * kV;
             const unsigned char* st = ring + (size_t)s * kRingStage;
             mbar_wait(&S.mbar[s], (unsigned int)((t / kRing) & 1));
-            unsigned long long x4[kV];
-            unsigned int a4[kV], r4[kV];
-            read4(st, tid, i0 + kV <= hi, x4, a4, r4);
-            if (P.dbg_check == 2 && i0 + kV <= hi) load4(P, i0, true, x4, a4, r4);  // debug: L2 values
+            if (P.dbg_check == 2) {
+                unsigned long long x4[kV];
+                unsigned int a4[kV], r4[kV];
+                read4(st, tid, i0 + kV <= hi, x4, a4, r4);
+                if (i0 + kV <= hi) load4(P, i0, true, x4, a4, r4);  // debug: L2 values
+                __syncwarp();
+                if (lane_id() == 0) mbar_arrive(&S.mbar_empty[s]);
+                classify_append(x4, a4, r4, i0);
+                continue;
+            }
+            const ulonglong2 w01 = *reinterpret_cast<const ulonglong2*>(st + (size_t)tid * 32);
+            const ulonglong2 w23 = *reinterpret_cast<const ulonglong2*>(st + (size_t)tid * 32 + 16);
             __syncwarp();
             if (lane_id() == 0) mbar_arrive(&S.mbar_empty[s]);
-            classify_append(x4, a4, r4, i0);
+            classify_append_pk(w01, w23, i0 + kV <= hi, i0);
         }
     }
     __syncthreads();
