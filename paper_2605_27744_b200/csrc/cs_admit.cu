@@ -38,6 +38,7 @@ constexpr int kSide = kMaxLists * (kChunk + 1);
 
 // ------------------------------------------------------------------ shared state
 
+constexpr int kBfsPre = 2048;  // window pairs phase 0 can prefetch for the BFS
 constexpr int kPend = kMaxLists;  // staged agent-carrying slot whose class phase 0 has not fixed yet
 
 struct ScanSmem {
@@ -70,6 +71,8 @@ struct AdmSmem {
     int need_full; // a prescan-fed chunk needs the serial replay (every class list): scan instead
     double wsurv[kMaxLists];  // P.wsurv staged on chip (indexed kernel-parameter loads are slow)
     unsigned long long ph[kPhases], tl;  // phase timestamps (CTA 0, thread 0)
+    long long pf_head, pf_size;  // the learner window at launch (BFS prefetch)
+    int pf_on;
 };
 
 // Dynamic shared memory, phase by phase (the regions alias across phases):
@@ -174,6 +177,11 @@ struct BfsSmem {
     unsigned short wb[8192];
     unsigned char edge[8192];
     unsigned char hop[kMaxAgents];
+    // prefetched by admit_body's phase 0 (window pairs in window order, their counts and row
+    // totals before this admission's record): the BFS then runs without global round trips
+    unsigned int pc[kBfsPre], pt[kBfsPre];
+    int pf_size;
+    unsigned int rec_c, rec_t;  // the record's counts[prev][next] and totals[prev] before it
 };
 static_assert(sizeof(BfsSmem) <= kOffCls, "BFS view must fit the scan region");
 
@@ -210,7 +218,8 @@ __device__ __forceinline__ void fstamp(const DevPool& P, int k) {
 
 // CacheSagePolicy::observe(AgentDispatch) (cachesage_policy.cpp:57-72). CTA 0, all threads.
 __device__ void observe_dispatch(const DevPool& P, int prev, int next, unsigned long long tick, int n_agents,
-                                 unsigned char* dsm, RedSmem& Red, AdmSmem& A, unsigned char* cls_smem = nullptr) {
+                                 unsigned char* dsm, RedSmem& Red, AdmSmem& A, unsigned char* cls_smem = nullptr,
+                                 bool prefetched = false) {
     Ctrl* C = P.ctrl;
     const int tid = threadIdx.x, T = blockDim.x;
     const long long W = P.window;
@@ -219,8 +228,14 @@ __device__ void observe_dispatch(const DevPool& P, int prev, int next, unsigned 
     // K3: TransitionLearner::record (transition_learner.cpp:22-51): one pair per dispatch
     if (prev >= 0 && tid == 0) {
         const long long head = C->win_head, size = C->win_size;
-        atomicAdd(&P.counts[(long long)prev * Acap + next], 1u);  // fire-and-forget (RED)
-        atomicAdd(&P.totals[prev], 1u);
+        if (prefetched) {  // the new pair's count and row total (the BFS below needs them)
+            BfsSmem& Bq = *reinterpret_cast<BfsSmem*>(dsm);
+            Bq.rec_c = atomicAdd(&P.counts[(long long)prev * Acap + next], 1u);
+            Bq.rec_t = atomicAdd(&P.totals[prev], 1u);
+        } else {
+            atomicAdd(&P.counts[(long long)prev * Acap + next], 1u);  // fire-and-forget (RED)
+            atomicAdd(&P.totals[prev], 1u);
+        }
         if (size == W) {
             const int oa = P.win_a[head], ob = P.win_b[head];
             P.win_a[head] = prev;
@@ -240,7 +255,61 @@ __device__ void observe_dispatch(const DevPool& P, int prev, int next, unsigned 
     const bool changed = C->cur_agent != next;
     __syncthreads();
     if (tid == 0) C->cur_agent = next;
-    if (changed) {
+    if (changed && prefetched) {
+        // K3b from the prefetched window: the record's effect applied on chip. The record pushed
+        // (prev, next) and, with a full window, pushed out the oldest pair (oa, ob): counts and
+        // row totals move by +-1 exactly there (transition_learner.cpp:22-51).
+        const int e = P.e_max;
+        BfsSmem& B = *reinterpret_cast<BfsSmem*>(dsm);
+        const int sz0 = B.pf_size;
+        const bool popped = prev >= 0 && (long long)sz0 == W;
+        const int oa = popped ? (int)B.wa[0] : -1, ob = popped ? (int)B.wb[0] : -1;
+        const int jlo = popped ? 1 : 0, jhi = sz0 + (prev >= 0 ? 1 : 0);
+        for (int x = tid; x < n_agents; x += T) B.hop[x] = (unsigned char)e;
+        for (int j = jlo + tid; j < jhi; j += T) {
+            int aj, bj;
+            unsigned int c, t;
+            if (j < sz0) {
+                aj = B.wa[j];
+                bj = B.wb[j];
+                c = B.pc[j] + (aj == prev && bj == next ? 1u : 0u) - (aj == oa && bj == ob ? 1u : 0u);
+                t = B.pt[j] + (aj == prev ? 1u : 0u) - (aj == oa ? 1u : 0u);
+            } else {  // the pair this record appended
+                aj = prev;
+                bj = next;
+                B.wa[j] = (unsigned short)aj;
+                B.wb[j] = (unsigned short)bj;
+                c = B.rec_c + 1u - (aj == oa && bj == ob ? 1u : 0u);
+                t = B.rec_t + 1u - (aj == oa ? 1u : 0u);
+            }
+            B.edge[j] = __ddiv_rn((double)c, (double)t) < P.tau ? 0 : 1;
+        }
+        __syncthreads();
+        if (tid == 0) B.hop[next] = 0;
+        __syncthreads();
+        for (int d = 0; d + 1 < e; ++d) {
+            int any = 0;
+            for (int j = jlo + tid; j < jhi; j += T) {
+                const int aj = B.wa[j], bj = B.wb[j];
+                if (!B.edge[j] || B.hop[aj] != d) continue;
+                if (B.hop[bj] > d + 1) {
+                    B.hop[bj] = (unsigned char)(d + 1);
+                    any = 1;
+                }
+            }
+            if (!__syncthreads_or(any)) break;
+        }
+        for (int x = tid; x < n_agents; x += T) {
+            P.hop[x] = B.hop[x];
+            P.cls[x] = B.hop[x];
+            if (cls_smem) cls_smem[x] = B.hop[x];
+        }
+        if (tid == 0) {
+            C->rebuilds += 1ull;
+            C->reach_built = 1;
+        }
+        __syncthreads();
+    } else if (changed) {
         // K3b: rebuild_reachability (reachability.cpp:39-81), level-synchronous over the
         // window's pairs (every positive count cell is a window pair). Edge iff
         // !(count/total < tau) in fp64; depth d expands only while d + 1 < e_max.
@@ -2574,6 +2643,13 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
             C->done = 0;
             C->error = 0;
             es.ok = 0;
+            {  // (thread 0 waits for this round of loads anyway)
+                const long long wh = C->win_head, wsz = C->win_size;
+                A.pf_head = wh;
+                A.pf_size = wsz;
+                A.pf_on = (a.flags & kDispatch) && P.policy != 0 && a.next >= 0 && C->cur_agent != a.next &&
+                          wsz <= 2 * (long long)blockDim.x && wsz <= kBfsPre;
+            }
             es.valid = pre_avail && *(volatile unsigned long long*)&C->pl_seq[par_prev] == a.seq - 1ull &&
                        *(volatile int*)&C->pl_ok[par_prev] != 0;
             if (es.valid) {
@@ -2595,6 +2671,34 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
         const int n = a.n;
         long long miss_min = n, need = 0;
         const int ne = C->tq_erase, ni = C->tq_insert;
+        // BFS inputs of observe(AgentDispatch), issued now so their round trips overlap the two
+        // table rounds: the window pairs (here), their counts and row totals (round 2)
+        const long long W_ = P.window, pf_head = A.pf_head, pf_size = A.pf_size;
+        const bool pf = A.pf_on != 0;
+        int pf_a[2] = {0, 0}, pf_b[2] = {0, 0};
+        unsigned int pf_c[2] = {0u, 0u}, pf_t[2] = {0u, 0u};
+        if (pf) {
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                const long long j = tid + (long long)k * T;
+                if (j < pf_size) {
+                    const long long q = (pf_head + j) % W_;
+                    pf_a[k] = P.win_a[q];
+                    pf_b[k] = P.win_b[q];
+                }
+            }
+        }
+        auto pf_issue2 = [&]() {
+            if (!pf) return;
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                const long long j = tid + (long long)k * T;
+                if (j < pf_size) {
+                    pf_c[k] = __ldcg(P.counts + (long long)pf_a[k] * P.a_cap + pf_b[k]);
+                    pf_t[k] = __ldcg(P.totals + pf_a[k]);
+                }
+            }
+        };
         if (ne + ni <= kOvMax) {
             // The previous admission's table updates run concurrently with this admission's probe:
             // the probe resolves the queued keys from an on-chip overlay (insert wins: a key erased
@@ -2663,6 +2767,7 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
             dec = block_sum(dec, Red);  // (its barriers also publish the overlay)
             if (tid == 0) C->pinned -= dec;
             pstamp(P, 1);
+            pf_issue2();
             long long reused = 0;
             const int nxs = early ? kXset : 0;
             for (int q = tid; q < ne + ni + n + nxs; q += T) {
@@ -2705,6 +2810,7 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
             if (tid == 0) es.ok = 0;  // (the late prescan consumer re-reads instead)
             apply_table_queue(P, Red);  // the previous admission's erases / inserts
             pstamp(P, 1);
+            pf_issue2();
             // deferred EngineSim::unpin calls of completed requests (engine.cpp:170-180), in order
             if (a.n_unpin_ranges > 0) {
                 long long dec = 0;
@@ -2731,6 +2837,20 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
                 if (s == kNoSlot || r0 == 0u) ++need;
             }
         }
+        if (pf) {  // (the BFS view is free until observe_dispatch)
+            BfsSmem& Bf = *reinterpret_cast<BfsSmem*>(dsm);
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                const long long j = tid + (long long)k * T;
+                if (j < pf_size) {
+                    Bf.wa[j] = (unsigned short)pf_a[k];
+                    Bf.wb[j] = (unsigned short)pf_b[k];
+                    Bf.pc[j] = pf_c[k];
+                    Bf.pt[j] = pf_t[k];
+                }
+            }
+            if (tid == 0) Bf.pf_size = (int)pf_size;
+        }
         need = block_sum(need, Red);
         miss_min = block_min(miss_min, Red);
         if (tid == 0) A.needed = (int)need;
@@ -2743,7 +2863,7 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
             if (a.flags & kDispatch) {
                 if (tid == 0) A.tick = A.tick + 1;
                 __syncthreads();
-                observe_dispatch(P, a.prev, a.next, A.tick, a.n_agents, dsm, Red, A, B.cls);
+                observe_dispatch(P, a.prev, a.next, A.tick, a.n_agents, dsm, Red, A, B.cls, pf);
             }
             pstamp(P, 4);
             if (a.flags & kLookup) {
