@@ -2930,7 +2930,13 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
             }
             __syncthreads();
             run_loop = *(volatile int*)&C->verdict == 2;
-            if (!run_loop) return;
+            if (!run_loop) {
+                // This admission's table updates are queued (CTA 0's apply precedes the verdict) and
+                // CTA 0 no longer reads the table: the prescan CTAs apply them now, off the next
+                // admission's phase 0 (which then finds an empty queue)
+                if (!P.stream_generic && blockIdx.x == 1) apply_table_queue(P, Red);
+                return;
+            }
         } else {
             if (tid == 0) {  // this launch's scoring pass is the prescan
                 A.scans += 1;
