@@ -2461,6 +2461,7 @@ __device__ void replay_apply(const DevPool& P, const AdmitArgs& a, ReplaySmem& R
             P.pk[s] = pk_make(R.out_lt[i], P.agent[s], true);
         }
         P.p_slot[lo + i] = s;
+        if (a.pins_out) a.pins_out[lo + i] = s;  // final: later chunks only re-resolve positions >= hi
     }
     // blocks of later chunks evicted here are absent when reached
     if (nv > 0) {
@@ -3195,12 +3196,11 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
 
     // ---- epilogue (CTA 0): EngineSim::admit unpins at once; pins out; status
     if (blockIdx.x == 0) {
-        if (A.started && !A.error) {
+        if (A.started && !A.error && (a.flags & kUnpinAfter)) {  // (pins_out was written by apply)
             long long dec = 0;
             for (int i = tid; i < A.admit_n; i += T) {
                 const unsigned int s = P.p_slot[i];
-                if (a.pins_out) a.pins_out[i] = s;
-                if (a.flags & kUnpinAfter) {
+                {
                     if (atomicSub(&P.refs[s], 1u) == 1u) {
                         pk_unpinned(P, s);
                         ++dec;
