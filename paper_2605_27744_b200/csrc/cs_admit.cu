@@ -2935,7 +2935,10 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
                 // This admission's table updates are queued (CTA 0's apply precedes the verdict) and
                 // CTA 0 no longer reads the table: the prescan CTAs apply them now, off the next
                 // admission's phase 0 (which then finds an empty queue)
-                if (!P.stream_generic && blockIdx.x == 1) apply_table_queue(P, Red);
+                if (!P.stream_generic && blockIdx.x == 1) {
+                    apply_table_queue(P, Red);
+                    if (tid == 0) P.dbg[blockIdx.x * 16 + 11] = gtimer();  // instrumentation
+                }
                 return;
             }
         } else {

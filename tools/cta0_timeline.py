@@ -33,7 +33,7 @@ for it in range(40):
     st = d[16 * g:16 * g + 16]
     rows.append((st - ent) / 1e3)
     per = d[:16 * g].reshape(g, 16)
-    fin.append([(per[1, c] - ent) / 1e3 for c in (6, 7, 8, 4)])
+    fin.append([(per[1, c] - ent) / 1e3 for c in (6, 7, 8, 4, 11)])
     ends.append([((per[1:, c] - ent) / 1e3).max() for c in (0, 1, 2, 3, 4, 5)] + [((per[1:3, 4] - ent) / 1e3).max()])
 r = np.median(np.array(rows), axis=0)
 for k in [0, 1, 2, 3, 13, 14, 4, 5, 6, 7, 8, 9, 10, 11, 12]:
@@ -45,4 +45,4 @@ res = eng.result()
 print("admit_ms per launch", res["admit_ms"] / max(res["admissions"], 1) * 1e3)
 
 f = np.median(np.array(fin), axis=0)
-print("finalizer CTA 1: arrivals seen %.2f staged %.2f ranked %.2f published %.2f us" % tuple(f))
+print("finalizer CTA 1: arrivals seen %.2f staged %.2f ranked %.2f published %.2f us; table queue applied %.2f us" % tuple(f))
