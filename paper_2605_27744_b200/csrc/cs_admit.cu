@@ -2423,10 +2423,14 @@ __device__ void replay_apply(const DevPool& P, const AdmitArgs& a, ReplaySmem& R
     }
     __syncthreads();
     dstamp(P, 4);
-    const int q_e = C->tq_erase, q_i = C->tq_insert;  // table updates are queued for the next launch
+    // Inserts are queued (the next launch's phase 0, or CTA 1 at the end of a pipelined launch,
+    // applies them); the victims' erases run here, one chain per thread: nothing reads the table
+    // for the rest of this admission, and a block this admission inserted is pinned, so it is
+    // never among its own victims (an erase always precedes any re-insert of the same key).
+    const int q_e = C->tq_erase, q_i = C->tq_insert;
     for (int k = tid; k < nv; k += T) {
         const unsigned long long kk = R.vkey[k];
-        P.tq_key[q_e + k] = kk;
+        table_erase(P, kk);
         P.evlog[(ev0 + k) % (unsigned long long)P.evlog_cap] = kk;  // ring; the host drains it
         if (a.vict_host && A.n_ev_adm + k < a.vict_cap) a.vict_host[A.n_ev_adm + k] = kk;  // mapped host memory
         if (k >= R.n_reused) {  // victims[0, n_reused) are overwritten by new blocks below
@@ -2488,7 +2492,8 @@ __device__ void replay_apply(const DevPool& P, const AdmitArgs& a, ReplaySmem& R
         C->pinned = A.pinned;
         C->free_top = top;
         C->n_ev = ev0 + nv;
-        C->tq_erase = q_e + nv;
+        C->tq_erase = q_e;
+        C->tombstones += nv;  // (an erase leaves a tombstone; an insert may reuse it later)
         C->tq_insert = q_i + R.n_ins;
         A.n_ev_adm += nv;
     }
