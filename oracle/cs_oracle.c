@@ -220,6 +220,11 @@ typedef struct {
     long A;            /* capacity */
     uint64_t* counts;  /* A*A */
     uint64_t* totals;  /* A */
+    /* per row, its nonzero columns (any order; hops and argmax are order-independent):
+     * nz[a*A + k], k < nnz[a]; nzpos[a*A + b] = k */
+    long* nz;
+    long* nzpos;
+    long* nnz;
     long* win_a;       /* ring */
     long* win_b;
     long win_head, win_size, win_cap;
@@ -240,6 +245,25 @@ typedef struct {
     uint64_t cursor;
 } policy;
 
+static void cell_inc(policy* p, long a, long b) {
+    if (p->counts[a * p->A + b]++ == 0) {
+        p->nzpos[a * p->A + b] = p->nnz[a];
+        p->nz[a * p->A + p->nnz[a]++] = b;
+    }
+    p->totals[a]++;
+}
+
+/* erase zero cells (transition_learner.cpp:40-47) */
+static void cell_dec(policy* p, long a, long b) {
+    p->totals[a]--;
+    if (--p->counts[a * p->A + b] == 0) {
+        const long k = p->nzpos[a * p->A + b];
+        const long last = p->nz[a * p->A + --p->nnz[a]];
+        p->nz[a * p->A + k] = last;
+        p->nzpos[a * p->A + last] = k;
+    }
+}
+
 /* TransitionLearner::record, transition_learner.cpp:22-51 (note_agent :16-20 is the alphabet,
  * which does not influence any decision; indices come from the agent map). */
 static void learner_record(policy* p, long a, long b) {
@@ -249,18 +273,15 @@ static void learner_record(policy* p, long a, long b) {
         long oa = p->win_a[p->win_head], ob = p->win_b[p->win_head];
         p->win_a[p->win_head] = a;
         p->win_b[p->win_head] = b;
-        p->counts[a * p->A + b]++;
-        p->totals[a]++;
-        p->counts[oa * p->A + ob]--;
-        p->totals[oa]--;
+        cell_inc(p, a, b);
+        cell_dec(p, oa, ob);
         p->win_head = (p->win_head + 1) % p->win_cap;
         return;
     }
     p->win_a[pos] = a;
     p->win_b[pos] = b;
     p->win_size++;
-    p->counts[a * p->A + b]++;
-    p->totals[a]++;
+    cell_inc(p, a, b);
 }
 
 /* rebuild_reachability, reachability.cpp:39-81: FIFO BFS from current over edges with
@@ -278,9 +299,9 @@ static void rebuild(policy* p, long cur) {
         if (d + 1 >= e) continue;
         if (p->totals[a] == 0) continue;
         const double total = (double)p->totals[a];
-        for (long b = 0; b < p->am.n; ++b) {
+        for (long k = 0; k < p->nnz[a]; ++k) {
+            const long b = p->nz[a * p->A + k];
             uint64_t c = p->counts[a * p->A + b];
-            if (c == 0) continue;
             if ((double)c / total < p->cfg.tau) continue;
             if (p->hops[b] > d + 1) {
                 p->hops[b] = d + 1;
@@ -297,9 +318,9 @@ static int argmax_row(const policy* p, long a, long* best, double* prob) {
     if (p->totals[a] == 0) return 0;
     uint64_t bc = 0;
     long bi = -1;
-    for (long b = 0; b < p->am.n; ++b) {
+    for (long k = 0; k < p->nnz[a]; ++k) {
+        const long b = p->nz[a * p->A + k];
         uint64_t c = p->counts[a * p->A + b];
-        if (c == 0) continue;
         if (bi < 0 || c > bc || (c == bc && p->am.ids[b] < p->am.ids[bi])) {
             bi = b;
             bc = c;
@@ -409,6 +430,12 @@ struct cso_engine {
     uint64_t* ev;
     long n_ev, ev_cap;
     int error;
+    /* fast_evict index (see lheap below): grp[g] holds the unpinned resident blocks of agent
+     * index g (g = A: agentless) keyed by last_touch; all holds every resident block. */
+    int fast;
+    struct lheap* grp;
+    long n_grp;
+    struct lheap* all;
 };
 
 static long tab_find(const cso_engine* e, uint64_t key) {
@@ -448,6 +475,133 @@ static void tab_erase(cso_engine* e, uint64_t key) {
     e->tab[hole] = 0;
 }
 
+/* ---------------------------------------------------------------- indexed evict_one
+ *
+ * The class-head lemma: a block's score is f(survival(hop(agent)), rho(lt)) with
+ * rho monotone in last_touch (runtime.cpp:23-32) and fp64 rounding monotone, so among the
+ * unpinned blocks of ONE agent the reference's argmin (engine.cpp:106-118, tie on
+ * (score, last_touch, key)) is the one with the smallest last_touch. evict_one therefore only
+ * needs each agent's oldest unpinned block: it scores those heads with the same score() and
+ * picks the (score, last_touch, key) minimum — the reference's own comparison over a subset
+ * that provably contains its victim. oldest_live_touch (engine.cpp:90-96) is the top of a heap
+ * of every resident block. This is an independent derivation from the GPU's (one scan per
+ * admission, per-class lists, dominance replay); both must agree with the O(N) argmin, which
+ * the tests check on every golden fixture.
+ *
+ * Lazy heaps: an entry (lt, idx) is live iff ent[idx] is resident with that last_touch (and,
+ * for the group heaps, unpinned). last_touch values are never reused, so a stale entry can
+ * never become live again. Heaps are compacted when stale entries outnumber live ones. */
+typedef struct {
+    uint64_t lt;
+    long idx;
+} hnode;
+
+typedef struct lheap {
+    hnode* a;
+    long n, cap, live;
+    /* cached live top (group heaps): valid unless dirty; hidx < 0 = empty */
+    uint64_t hlt;
+    long hidx;
+    int dirty;
+} lheap;
+
+static void lh_push_raw(lheap* h, uint64_t lt, long idx) {
+    if (h->n == h->cap) {
+        h->cap = h->cap ? h->cap * 2 : 16;
+        h->a = (hnode*)realloc(h->a, sizeof(hnode) * (size_t)h->cap);
+    }
+    h->a[h->n].lt = lt;
+    h->a[h->n].idx = idx;
+    h->n++;
+}
+
+static void lh_down(lheap* h, long i) {
+    const hnode x = h->a[i];
+    for (;;) {
+        long l = 2 * i + 1;
+        if (l >= h->n) break;
+        if (l + 1 < h->n && h->a[l + 1].lt < h->a[l].lt) ++l;
+        if (h->a[l].lt >= x.lt) break;
+        h->a[i] = h->a[l];
+        i = l;
+    }
+    h->a[i] = x;
+}
+
+static void lh_up(lheap* h, long i) {
+    const hnode x = h->a[i];
+    while (i > 0) {
+        long p = (i - 1) / 2;
+        if (h->a[p].lt <= x.lt) break;
+        h->a[i] = h->a[p];
+        i = p;
+    }
+    h->a[i] = x;
+}
+
+static void lh_heapify(lheap* h) {
+    for (long i = h->n / 2 - 1; i >= 0; --i) lh_down(h, i);
+}
+
+static void lh_pop(lheap* h) {
+    h->a[0] = h->a[--h->n];
+    if (h->n > 0) lh_down(h, 0);
+}
+
+static int live_all(const cso_engine* e, const hnode* x) {
+    return e->ent[x->idx].used && e->ent[x->idx].lt == x->lt;
+}
+
+static int live_grp(const cso_engine* e, const hnode* x) {
+    return live_all(e, x) && e->ent[x->idx].refs == 0;
+}
+
+static void lh_compact(cso_engine* e, lheap* h, int grp) {
+    long m = 0;
+    for (long i = 0; i < h->n; ++i)
+        if (grp ? live_grp(e, &h->a[i]) : live_all(e, &h->a[i])) h->a[m++] = h->a[i];
+    h->n = m;
+    lh_heapify(h);
+    h->dirty = 1;
+}
+
+static void lh_push(cso_engine* e, lheap* h, uint64_t lt, long idx, int grp) {
+    lh_push_raw(h, lt, idx);
+    lh_up(h, h->n - 1);
+    h->live++;
+    h->dirty = 1;
+    if (h->n > 2 * h->live + 64) lh_compact(e, h, grp);
+}
+
+static lheap* grp_of(cso_engine* e, long idx) {
+    const long a = e->ent[idx].agent;
+    return &e->grp[a >= 0 ? a : e->n_grp - 1];
+}
+
+/* hooks: the index follows every change of (resident, last_touch, refs == 0) */
+static void ix_touched(cso_engine* e, long idx, int was_resident) {
+    if (!e->fast) return;
+    if (was_resident) e->all->live--; /* the previous (lt, idx) entry went stale */
+    lh_push(e, e->all, e->ent[idx].lt, idx, 0);
+}
+
+static void ix_join_grp(cso_engine* e, long idx) { /* unpinned member at its current last_touch */
+    if (e->fast) lh_push(e, grp_of(e, idx), e->ent[idx].lt, idx, 1);
+}
+
+static void ix_leave_grp(cso_engine* e, long idx) { /* pinned, touched, or evicted while unpinned */
+    if (!e->fast) return;
+    lheap* h = grp_of(e, idx);
+    h->live--;
+    if (h->hidx == idx) h->dirty = 1;
+}
+
+static void ix_evicted(cso_engine* e, long idx) {
+    if (!e->fast) return;
+    e->all->live--;
+    if (e->ent[idx].refs == 0) ix_leave_grp(e, idx);
+}
+
 cso_engine* cso_engine_new(const cso_cfg* cfg, long agent_cap) {
     cso_engine* e = (cso_engine*)calloc(1, sizeof(cso_engine));
     e->cfg = *cfg;
@@ -471,11 +625,21 @@ cso_engine* cso_engine_new(const cso_cfg* cfg, long agent_cap) {
     p->am.tab = (long*)calloc((size_t)p->am.tcap, sizeof(long));
     p->counts = (uint64_t*)calloc((size_t)(agent_cap * agent_cap), sizeof(uint64_t));
     p->totals = (uint64_t*)calloc((size_t)agent_cap, sizeof(uint64_t));
+    p->nz = (long*)malloc(sizeof(long) * (size_t)(agent_cap * agent_cap));
+    p->nzpos = (long*)malloc(sizeof(long) * (size_t)(agent_cap * agent_cap));
+    p->nnz = (long*)calloc((size_t)agent_cap, sizeof(long));
     p->win_cap = cfg->window > 0 ? cfg->window : 1024;
     p->win_a = (long*)malloc(sizeof(long) * (size_t)p->win_cap);
     p->win_b = (long*)malloc(sizeof(long) * (size_t)p->win_cap);
     p->hops = (int*)calloc((size_t)agent_cap, sizeof(int));
     p->current = -1;
+    e->fast = cfg->fast_evict && cfg->policy != 3;
+    if (e->fast) {
+        e->n_grp = agent_cap + 1;
+        e->grp = (lheap*)calloc((size_t)e->n_grp, sizeof(lheap));
+        for (long g = 0; g < e->n_grp; ++g) e->grp[g].dirty = 1;
+        e->all = (lheap*)calloc(1, sizeof(lheap));
+    }
     return e;
 }
 
@@ -489,6 +653,9 @@ void cso_engine_free(cso_engine* e) {
     free(e->pol.am.tab);
     free(e->pol.counts);
     free(e->pol.totals);
+    free(e->pol.nz);
+    free(e->pol.nzpos);
+    free(e->pol.nnz);
     free(e->pol.win_a);
     free(e->pol.win_b);
     free(e->pol.hops);
@@ -497,19 +664,96 @@ void cso_engine_free(cso_engine* e) {
     free(e->pol.bel_key);
     free(e->pol.bel_req);
     free(e->pol.bel_pos);
+    if (e->fast) {
+        for (long g = 0; g < e->n_grp; ++g) free(e->grp[g].a);
+        free(e->grp);
+        free(e->all->a);
+        free(e->all);
+    }
     free(e);
 }
 
 static long agent_index(cso_engine* e, uint64_t id) { return amap_get(&e->pol.am, id, 1); }
 
-/* EngineSim::touch, engine.cpp:79-88 (BlockTouch events are no-ops for both policies) */
-static void touch(cso_engine* e, long idx) {
+
+/* EngineSim::touch, engine.cpp:79-88 (BlockTouch events are no-ops for both policies).
+ * was_resident = 0 for a block admit_pinned just inserted. */
+static void touch(cso_engine* e, long idx, int was_resident) {
     e->ent[idx].lt = ++e->tick;
     e->ent[idx].lt_us = e->sim_now;
+    ix_touched(e, idx, was_resident);
+}
+
+/* the fast_evict victim: the (score, last_touch, key) minimum over each agent group's oldest
+ * unpinned block (see the lemma above); -1 when every resident block is pinned. Groups that
+ * share a survival value score by the same function of last_touch, so only the oldest head per
+ * survival class is scored (LRU and TTL scores do not depend on the agent: one class). */
+static long fast_victim(cso_engine* e) {
+    uint64_t old = e->tick;
+    lheap* all = e->all;
+    while (all->n > 0 && !live_all(e, &all->a[0])) lh_pop(all);
+    if (all->n > 0 && all->a[0].lt < old) old = all->a[0].lt;
+    const policy* p = &e->pol;
+    const int cs = p->cfg.policy == 1 && p->reach_built;
+    const int emax = p->cfg.e_max;
+    long cand[65];
+    const int ncls = cs ? (emax < 64 ? emax : 64) + 1 : 1;
+    for (int c = 0; c < ncls; ++c) cand[c] = -1;
+    for (long g = 0; g < e->n_grp; ++g) {
+        lheap* h = &e->grp[g];
+        if (h->dirty) {
+            while (h->n > 0 && !live_grp(e, &h->a[0])) lh_pop(h);
+            h->hidx = h->n > 0 ? h->a[0].idx : -1;
+            h->hlt = h->n > 0 ? h->a[0].lt : 0;
+            h->dirty = 0;
+        }
+        if (h->hidx < 0) continue;
+        int c = 0;
+        if (cs) {
+            const int hop = g < e->n_grp - 1 ? p->hops[g] : emax;
+            c = hop < emax ? hop : emax;
+            if (c > 64) c = 64;
+        }
+        if (cand[c] < 0 || h->hlt < e->ent[cand[c]].lt) cand[c] = h->hidx;
+    }
+    long v = -1;
+    double vs = 0.0;
+    for (int c = 0; c < ncls; ++c) {
+        if (cand[c] < 0) continue;
+        const entry* x = &e->ent[cand[c]];
+        double s;
+        if (p->cfg.policy == 2) { /* TtlPolicy::score, baselines.cpp:22-28 */
+            const double rho = recency(x->lt, e->tick, old);
+            s = e->sim_now - x->lt_us < 5000000.0 ? 1.0e6 + rho : rho;
+        } else {
+            s = score(p, x->agent, x->lt, e->tick, old);
+        }
+        if (v < 0 || s < vs ||
+            (s == vs && (x->lt < e->ent[v].lt || (x->lt == e->ent[v].lt && x->key < e->ent[v].key)))) {
+            v = cand[c];
+            vs = s;
+        }
+    }
+    return v;
 }
 
 /* EngineSim::evict_one, engine.cpp:102-125 with score_context/oldest_live_touch :90-100 */
 static int evict_one(cso_engine* e) {
+    if (e->fast) {
+        const long v = fast_victim(e);
+        if (v < 0) return -1; /* "evict_one: all resident blocks are pinned" */
+        ix_evicted(e, v);
+        tab_erase(e, e->ent[v].key);
+        if (e->n_ev == e->ev_cap) {
+            e->ev_cap = e->ev_cap ? e->ev_cap * 2 : 1024;
+            e->ev = (uint64_t*)realloc(e->ev, sizeof(uint64_t) * (size_t)e->ev_cap);
+        }
+        e->ev[e->n_ev++] = e->ent[v].key;
+        e->ent[v].used = 0;
+        e->free_stack[e->n_free++] = v;
+        e->resident--;
+        return 0;
+    }
     uint64_t old = e->tick;
     for (long i = 0; i < e->n_ent_cap; ++i)
         if (e->ent[i].used && e->ent[i].lt < old) old = e->ent[i].lt;
@@ -553,7 +797,10 @@ long cso_engine_lookup(cso_engine* e, const uint64_t* keys, const int32_t* count
         long idx = tab_find(e, keys[i]);
         if (idx < 0) break;
         cached += counts[i];
-        touch(e, idx);
+        const int unpinned = e->ent[idx].refs == 0;
+        if (unpinned) ix_leave_grp(e, idx);
+        touch(e, idx, 1);
+        if (unpinned) ix_join_grp(e, idx);
     }
     if (first_miss) *first_miss = i;
     return cached;
@@ -573,6 +820,7 @@ static long admit_pinned(cso_engine* e, const uint64_t* keys, const int32_t* cou
                          int anchor, long* pins) {
     for (long i = 0; i < n; ++i) {
         long idx = tab_find(e, keys[i]);
+        const int fresh = idx < 0;
         if (idx < 0) {
             while (e->resident >= e->cfg.budget_blocks) {
                 if (evict_one(e) != 0) {
@@ -590,7 +838,8 @@ static long admit_pinned(cso_engine* e, const uint64_t* keys, const int32_t* cou
             tab_insert(e, keys[i], idx);
             e->resident++;
         }
-        touch(e, idx);
+        if (!fresh && e->ent[idx].refs == 0) ix_leave_grp(e, idx);
+        touch(e, idx, !fresh);
         if (e->ent[idx].refs++ == 0) e->pinned++;
         if (pins) pins[i] = idx;
     }
@@ -606,7 +855,10 @@ int cso_engine_admit_pinned(cso_engine* e, const uint64_t* keys, const int32_t* 
 /* EngineSim::unpin, engine.cpp:170-180 */
 static int unpin_idx(cso_engine* e, const long* idx, long n) {
     for (long i = 0; i < n; ++i)
-        if (--e->ent[idx[i]].refs == 0) e->pinned--;
+        if (--e->ent[idx[i]].refs == 0) {
+            e->pinned--;
+            ix_join_grp(e, idx[i]);
+        }
     return 0;
 }
 
@@ -614,7 +866,10 @@ int cso_engine_unpin(cso_engine* e, const uint64_t* keys, long n) {
     for (long i = 0; i < n; ++i) {
         long idx = tab_find(e, keys[i]);
         if (idx < 0) return -1; /* "unpin: block vanished while referenced" */
-        if (--e->ent[idx].refs == 0) e->pinned--;
+        if (--e->ent[idx].refs == 0) {
+            e->pinned--;
+            ix_join_grp(e, idx);
+        }
     }
     return 0;
 }
@@ -635,6 +890,10 @@ int cso_engine_restore(cso_engine* e, const uint64_t* keys, const uint64_t* lt, 
         if (x->refs > 0) e->pinned++;
         tab_insert(e, keys[i], idx);
         e->resident++;
+        if (e->fast) {
+            lh_push(e, e->all, x->lt, idx, 0);
+            if (x->refs == 0) ix_join_grp(e, idx);
+        }
     }
     if (tick > e->tick) e->tick = tick;
     return 0;
@@ -747,6 +1006,7 @@ static flight_t heap_pop(flight_t* h, long* n) {
     return top;
 }
 
+/* CostModel defaults, engine.hpp:20-24 */
 static const double kPrefillPerTok = 50.0, kPrefillBase = 1000.0, kDecodePerTok = 20000.0;
 
 static void push_u64(uint64_t** a, long* n, long* cap, uint64_t v) {
@@ -774,10 +1034,20 @@ static int bel_cmp(const void* x, const void* y) {
  * step (:372-392), activate/arrive (:262-276), try_start_head (:325-351), start_request
  * (:278-323), complete_earliest (:353-370), drain_and_run_warmups/execute_warmup (:197-238). */
 int cso_run(const cso_spec* s, const cso_cfg* cfg_in, cso_run_out* out) {
+    return cso_run_ex(s, cfg_in, NULL, -1, out);
+}
+
+int cso_run_ex(const cso_spec* s, const cso_cfg* cfg_in, const cso_snapshot* snap, long max_steps,
+               cso_run_out* out) {
     memset(out, 0, sizeof(*out));
     cso_cfg cfg = *cfg_in;
     if (cfg.budget_blocks <= 0) cfg.budget_blocks = s->budget_blocks;
     if (cfg.concurrency <= 0) cfg.concurrency = s->concurrency;
+    /* EngineSim ctor validation, engine.cpp:57-63 (0 selects the CostModel default) */
+    const double c_base = cfg.prefill_base_us != 0.0 ? cfg.prefill_base_us : kPrefillBase;
+    const double c_tok = cfg.prefill_per_token_us != 0.0 ? cfg.prefill_per_token_us : kPrefillPerTok;
+    const double c_dec = cfg.decode_per_token_us != 0.0 ? cfg.decode_per_token_us : kDecodePerTok;
+    if (c_base <= 0.0 || c_tok <= 0.0 || c_dec <= 0.0) return -3; /* invalid_argument */
     const int bs = cfg.block_size;
     const long nt = cso_generate(s, NULL, 0);
     int64_t* t7 = (int64_t*)malloc(sizeof(int64_t) * 7 * (size_t)(nt > 0 ? nt : 1));
@@ -839,6 +1109,16 @@ int cso_run(const cso_spec* s, const cso_cfg* cfg_in, cso_run_out* out) {
         free(tmp.tab);
     }
     cso_engine* e = cso_engine_new(&cfg, distinct + 1);
+    int rc = 0;
+    if (snap && snap->n > 0) {
+        uint64_t mx = 0;
+        for (long i = 0; i < snap->n; ++i)
+            if (snap->last_touch[i] > mx) mx = snap->last_touch[i];
+        if (snap->n > cfg.budget_blocks ||
+            cso_engine_restore(e, snap->keys, snap->last_touch, snap->has_agent, snap->agents, snap->refs, snap->n,
+                               mx) != 0)
+            rc = -4; /* invalid snapshot */
+    }
     if (cfg.policy == 3) {
         long nb = 0;
         for (long i = 0; i < nt; ++i) nb += rq[i].nb;
@@ -897,13 +1177,15 @@ int cso_run(const cso_spec* s, const cso_cfg* cfg_in, cso_run_out* out) {
     long w_cap = 0, w_n = 0;
     uint64_t *w_target = NULL, *w_tick = NULL, *w_step = NULL;
     long wt_cap = 0, wt_n = 0, ws_cap = 0, ws_n = 0;
+    out->completed = (uint8_t*)calloc((size_t)(nt > 0 ? nt : 1), 1);
     long long tot_prompt = 0, tot_cached = 0;
     long steps = 0, completed = 0;
-    int rc = 0;
+    if (rc != 0) goto done;
     (void)w_cap;
     (void)w_n;
 
     for (;;) {
+        if (max_steps >= 0 && steps >= max_steps) break;
         /* done() */
         if (nheap == 0 && rd_head == rd_tail && np_head == np_tail) break;
         /* activate_sessions */
@@ -956,8 +1238,9 @@ int cso_run(const cso_spec* s, const cso_cfg* cfg_in, cso_run_out* out) {
                 rc = -1;
                 goto done;
             }
-            const double ttft = kPrefillBase + kPrefillPerTok * (double)(r->prompt_tokens - cached);
-            f.end_us = e->sim_now + ttft + kDecodePerTok * r->decode_tokens;
+            out->n_admissions++;
+            const double ttft = c_base + c_tok * (double)(r->prompt_tokens - cached);
+            f.end_us = e->sim_now + ttft + c_dec * r->decode_tokens;
             f.cached = cached;
             f.start_us = e->sim_now;
             heap_push(heap, &nheap, f);
@@ -985,6 +1268,7 @@ int cso_run(const cso_spec* s, const cso_cfg* cfg_in, cso_run_out* out) {
                 out->prompt_tokens[f.req] = rq[f.req].prompt_tokens;
                 out->start_us[f.req] = f.start_us;
                 out->end_us[f.req] = f.end_us;
+                out->completed[f.req] = 1;
                 tot_prompt += rq[f.req].prompt_tokens;
                 tot_cached += f.cached;
                 ++completed;
@@ -1032,6 +1316,7 @@ int cso_run(const cso_spec* s, const cso_cfg* cfg_in, cso_run_out* out) {
                     unpin_idx(e, pins, admit_n);
                     free(pins);
                     out->warmups_executed++;
+                    out->n_admissions++;
                 }
             }
             free(fx);
@@ -1084,5 +1369,6 @@ void cso_free_run(cso_run_out* o) {
     free(o->warmup_step);
     free(o->warmup_target);
     free(o->warmup_tick);
+    free(o->completed);
     memset(o, 0, sizeof(*o));
 }

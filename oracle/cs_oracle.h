@@ -46,6 +46,13 @@ typedef struct cso_cfg {
     double min_confidence;
     uint64_t min_row_count;
     int budget_per_step;
+    /* 1: the indexed evict_one (per-agent heaps of unpinned blocks by last_touch + a heap of all
+     * resident blocks), exact by the class-head lemma; 0: the reference's O(N) argmin. Belady
+     * always uses the O(N) argmin (its score is not monotone in last_touch). */
+    int fast_evict;
+    /* CostModel (engine.hpp:20-24, experiment.cpp:272-279); 0 = the reference defaults
+     * 1000 / 50 / 20000 us. */
+    double prefill_base_us, prefill_per_token_us, decode_per_token_us;
 } cso_cfg;
 
 typedef struct cso_run_out {
@@ -64,6 +71,8 @@ typedef struct cso_run_out {
     long truncated, warmups_executed, warmups_dropped;
     double sim_us;
     long n_steps;
+    long n_admissions; /* start_request + executed warmups */
+    uint8_t* completed; /* per turn: 1 once complete_earliest retired it */
 } cso_run_out;
 
 uint64_t cso_mix64(uint64_t x);
@@ -77,6 +86,23 @@ long cso_generate(const cso_spec* spec, int64_t* turns7, long cap);
 long cso_turn_tokens(const cso_spec* spec, const int64_t* turn7, uint32_t* out, long cap);
 
 int cso_run(const cso_spec* spec, const cso_cfg* cfg, cso_run_out* out);
+
+/* A resident-pool snapshot installed before the first scheduler step (as cs_engine_restore):
+ * agents are 64-bit AgentIds (has_agent = 0: none); the engine clock becomes max(last_touch). */
+typedef struct cso_snapshot {
+    long n;
+    const uint64_t* keys;
+    const uint64_t* last_touch;
+    const int32_t* has_agent;
+    const uint64_t* agents;
+    const int32_t* refs; /* NULL: all unpinned */
+} cso_snapshot;
+
+/* cso_run from an optional snapshot, stopping after max_steps scheduler steps (< 0: run to the
+ * end). out->n_turns counts every request; turns not completed keep cached/end = 0 and are
+ * flagged by out->completed[i] = 0. */
+int cso_run_ex(const cso_spec* spec, const cso_cfg* cfg, const cso_snapshot* snap, long max_steps,
+               cso_run_out* out);
 void cso_free_run(cso_run_out* out);
 
 /* Engine-level primitives (EngineSim public surface + the start_request hot path). */

@@ -34,7 +34,16 @@ class Cfg(C.Structure):
         ("block_size", C.c_int), ("prefetch", C.c_int), ("skip", C.c_int), ("take", C.c_int),
         ("tau", C.c_double), ("e_max", C.c_int), ("w_pred", C.c_double), ("window", C.c_long),
         ("min_confidence", C.c_double), ("min_row_count", C.c_uint64),
-        ("budget_per_step", C.c_int),
+        ("budget_per_step", C.c_int), ("fast_evict", C.c_int),
+        ("prefill_base_us", C.c_double), ("prefill_per_token_us", C.c_double),
+        ("decode_per_token_us", C.c_double),
+    ]
+
+
+class Snapshot(C.Structure):
+    _fields_ = [
+        ("n", C.c_long), ("keys", C.c_void_p), ("last_touch", C.c_void_p), ("has_agent", C.c_void_p),
+        ("agents", C.c_void_p), ("refs", C.c_void_p),
     ]
 
 
@@ -47,7 +56,8 @@ class RunOut(C.Structure):
         ("warmup_step", C.POINTER(C.c_long)), ("warmup_target", C.POINTER(C.c_uint64)),
         ("warmup_tick", C.POINTER(C.c_uint64)), ("hit_rate", C.c_double),
         ("truncated", C.c_long), ("warmups_executed", C.c_long), ("warmups_dropped", C.c_long),
-        ("sim_us", C.c_double), ("n_steps", C.c_long),
+        ("sim_us", C.c_double), ("n_steps", C.c_long), ("n_admissions", C.c_long),
+        ("completed", C.POINTER(C.c_uint8)),
     ]
 
 
@@ -78,6 +88,8 @@ def lib():
         L.cso_turn_tokens.argtypes = [C.POINTER(Spec), vp, vp, C.c_long]
         L.cso_run.restype = C.c_int
         L.cso_run.argtypes = [C.POINTER(Spec), C.POINTER(Cfg), C.POINTER(RunOut)]
+        L.cso_run_ex.restype = C.c_int
+        L.cso_run_ex.argtypes = [C.POINTER(Spec), C.POINTER(Cfg), C.POINTER(Snapshot), C.c_long, C.POINTER(RunOut)]
         L.cso_free_run.argtypes = [C.POINTER(RunOut)]
         L.cso_engine_new.restype = vp
         L.cso_engine_new.argtypes = [C.POINTER(Cfg), C.c_long]
@@ -192,7 +204,9 @@ POLICY_IDS = {"lru": 0, "cachesage": 1, "ttl": 2, "belady": 3}
 
 def cfg_struct(policy="cachesage", budget=None, concurrency=None, block_size=16, prefetch=True,
                skip=4, take=4, tau=0.01, e_max=8, w_pred=1.0, window=1024, min_confidence=0.5,
-               min_row_count=5, budget_per_step=1):
+               min_row_count=5, budget_per_step=1, fast=False, cost=None):
+    """fast: the indexed evict_one (exact by the class-head lemma; see cs_oracle.c). cost:
+    (prefill_base_us, prefill_per_token_us, decode_per_token_us), None = the reference defaults."""
     c = Cfg()
     c.policy = POLICY_IDS[policy]
     c.budget_blocks = budget or 0
@@ -202,18 +216,37 @@ def cfg_struct(policy="cachesage", budget=None, concurrency=None, block_size=16,
     c.skip, c.take, c.tau, c.e_max, c.w_pred = skip, take, tau, e_max, w_pred
     c.window, c.min_confidence, c.min_row_count = window, min_confidence, min_row_count
     c.budget_per_step = budget_per_step
+    c.fast_evict = 1 if fast else 0
+    if cost is not None:
+        c.prefill_base_us, c.prefill_per_token_us, c.decode_per_token_us = (float(x) for x in cost)
     return c
 
 
-def run(spec, **kw):
+def run(spec, snapshot=None, max_steps=-1, **kw):
+    """cso_run_ex: one simulation cell; snapshot = (keys, last_touch, agent ids or None per slot
+    as a u64 array with has_agent mask, refs) installed before the first step; max_steps bounds
+    the scheduler steps (-1: to the end)."""
     s = spec_struct(spec)
     c = cfg_struct(**kw)
     o = RunOut()
-    rc = lib().cso_run(C.byref(s), C.byref(c), C.byref(o))
+    snp = None
+    if snapshot is not None:
+        keys, lt, has, ids, refs = (np.ascontiguousarray(snapshot[0], np.uint64),
+                                    np.ascontiguousarray(snapshot[1], np.uint64),
+                                    np.ascontiguousarray(snapshot[2], np.int32),
+                                    np.ascontiguousarray(snapshot[3], np.uint64),
+                                    None if snapshot[4] is None else np.ascontiguousarray(snapshot[4], np.int32))
+        snp = Snapshot(keys.size, keys.ctypes.data, lt.ctypes.data, has.ctypes.data, ids.ctypes.data,
+                       None if refs is None else refs.ctypes.data)
+        snp._keep = (keys, lt, has, ids, refs)
+    rc = lib().cso_run_ex(C.byref(s), C.byref(c), None if snp is None else C.byref(snp), int(max_steps),
+                          C.byref(o))
     try:
         if rc != 0:
             raise RuntimeError({-1: "evict_one: all resident blocks are pinned",
-                                -2: "scheduler stalled with an idle engine"}.get(rc, str(rc)))
+                                -2: "scheduler stalled with an idle engine",
+                                -3: "EngineSim: cost model parameters must be positive",
+                                -4: "snapshot: duplicate keys or larger than the budget"}.get(rc, str(rc)))
         nt, ne, nw = o.n_turns, o.n_evictions, o.n_warmups
         arr = lambda p, n, dt: (np.ctypeslib.as_array(p, (n,)).copy().astype(dt) if n > 0
                                else np.zeros(0, dt))
@@ -228,7 +261,8 @@ def run(spec, **kw):
             "warmup_tick": arr(o.warmup_tick, nw, np.uint64),
             "hit_rate": o.hit_rate, "truncated": o.truncated,
             "warmups_executed": o.warmups_executed, "warmups_dropped": o.warmups_dropped,
-            "sim_us": o.sim_us, "n_steps": o.n_steps,
+            "sim_us": o.sim_us, "n_steps": o.n_steps, "n_admissions": o.n_admissions,
+            "completed": arr(o.completed, nt, np.uint8).astype(bool),
         }
     finally:
         lib().cso_free_run(C.byref(o))
