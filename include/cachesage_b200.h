@@ -112,8 +112,50 @@ int cs_admit_pinned(cs_pool_t pool, const uint64_t* keys, const int32_t* counts,
                     int anchor_blocks, uint64_t tick_base, uint64_t* evicted, int64_t cap,
                     int64_t* n_evicted, uint32_t* pins);
 
-/* EngineSim::unpin (engine.cpp:170-180) by pinned slot (as returned by cs_admit_pinned). */
+/* EngineSim::unpin (engine.cpp:170-180): one pin released per key, in order (flight.pins are
+ * the BlockKeys admit_pinned returned, engine.hpp:144-152). A key that is not resident (or holds
+ * no pin) is CS_ERR_LOGIC "unpin: block vanished while referenced" after the keys before it were
+ * unpinned, as the reference throws mid-loop. */
+int cs_unpin(cs_pool_t pool, const uint64_t* keys, int n);
+/* The same by pinned slot (as cs_admit_pinned returns them): no table probe. */
 int cs_unpin_slots(cs_pool_t pool, const uint32_t* slots, int n);
+
+/* Event kinds of the observe stream (types.hpp:51-82). */
+typedef enum cs_event_kind {
+    CS_EV_BLOCK_TOUCH = 0,     /* BlockTouch{key, agent}: ignored by every policy's observe */
+    CS_EV_REQUEST_ARRIVAL = 1, /* RequestArrival{request, agent}: note_agent; Belady's cursor */
+    CS_EV_AGENT_DISPATCH = 2,  /* AgentDispatch{prev, next}: the full observe (cs_observe_dispatch) */
+    CS_EV_TOOL_RETURN = 3,     /* ToolReturn{agent}: note_agent */
+    CS_EV_TURN_COMPLETE = 4    /* TurnComplete{request}: ignored */
+} cs_event_kind;
+
+typedef struct cs_event {
+    uint64_t tick;    /* Event::tick: nondecreasing over the stream */
+    int kind;         /* cs_event_kind */
+    int agent;        /* arrival / tool-return agent, dispatch `next` (dense agent index) */
+    int prev;         /* dispatch `prev` (-1 = std::nullopt) */
+    uint64_t request; /* arrival / turn-complete RequestId */
+} cs_event;
+
+/* Runtime::dispatch_event (runtime.cpp:59-69) -> Policy::observe (cachesage_policy.cpp:50-77):
+ * CS_ERR_RUNTIME "dispatch_event: tick regression" when ev->tick is below the last event's tick
+ * (equal ticks allowed). *warmup_target = agent index of a warmup this dispatch issued, or -1. */
+int cs_dispatch_event(cs_pool_t pool, const cs_event* ev, int* warmup_target);
+
+/* CacheSagePolicy::predict(horizon) (current < 0: the policy's current agent) and
+ * predict_next(current, horizon) (cachesage_policy.cpp:87-107): the full MLE row, count / row
+ * total in fp64. The entries come ranked for prefetch: descending probability, ties to the
+ * smaller AgentId (argmax_row's order, transition_learner.cpp:79-96), so entry 0 is the
+ * warmup candidate maybe_prefetch gates. ids / probs / idx (dense agent index) may be NULL;
+ * *n = the row's support (an empty Forecast: 0). Baseline policies forecast nothing. */
+int cs_predict(cs_pool_t pool, int horizon, int current, uint64_t* ids, double* probs, int* idx, int cap, int* n);
+
+/* Policy::serialize_state().dump() (cachesage_policy.cpp:139-153; baselines.cpp:16, 30-32,
+ * 72-74): the documented JSON shape, byte-identical to the reference's for the same observe
+ * stream. *len = bytes (without the NUL); buf gets min(cap - 1, len) bytes + NUL (may be NULL). */
+int cs_serialize_state(cs_pool_t pool, char* buf, size_t cap, size_t* len);
+/* CacheSagePolicy::state_bytes (cachesage_policy.cpp:133-138). */
+int cs_policy_state_bytes(cs_pool_t pool, uint64_t* bytes);
 
 /* Pool snapshot restore (stress inputs): resident blocks with explicit
  * last_touch / agent index (CS_NO_AGENT = none) / refs. Keys must be new and distinct. */
@@ -190,6 +232,11 @@ typedef struct cs_engine_cfg {
                          admission, victims copied D2H per admission (the end-to-end path) */
     int device_scheduler; /* 1: EXPERIMENTAL device-resident scheduler: whole
                              EngineSim steps in one persistent launch; see DESIGN.md §4 */
+    /* CostModel (engine.hpp:22-26; experiment.cpp:270-280 reads it from the cell config): ttft =
+     * prefill_base_us + prefill_per_token_us * uncached tokens, decode = decode_per_token_us per
+     * token. They set completion order, hence unpin order, hence the victims. All must be > 0
+     * (engine.cpp:60-63); cs_engine_cfg_default sets 50 / 1000 / 20000. */
+    double prefill_per_token_us, prefill_base_us, decode_per_token_us;
 } cs_engine_cfg;
 
 void cs_engine_cfg_default(cs_engine_cfg* cfg);

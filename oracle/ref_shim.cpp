@@ -13,6 +13,7 @@
 //   - ref_evict_bench                                  -> EngineSim::admit / evict_one timing at pool N
 // Nothing here re-implements reference logic; it only marshals arguments.
 
+#include <algorithm>
 #include <chrono>
 #include <sstream>
 #include <cstdint>
@@ -31,12 +32,14 @@
 #include "cachesage/runtime.hpp"
 #include "cachesage/survival_oracle.hpp"
 #include "cachesage/workload.hpp"
+#include "ref_shim.h"
 
 using namespace cachesage;
 
 namespace {
 
 thread_local std::string g_err;
+thread_local std::string g_state;  // the last ref_run's final Policy::serialize_state().dump()
 
 struct RecordingPolicy : Policy {
     std::shared_ptr<Policy> inner;
@@ -73,54 +76,10 @@ T* dup(const std::vector<T>& v) {
 
 extern "C" {
 
-typedef struct ref_spec {
-    int n_agents;
-    const int* anchor_tokens;   // [n_agents]
-    const double* transition;   // [n_agents * n_agents], row-major
-    int supervisor;             // -1 = none
-    int turns_min, turns_max, sessions, task_tokens, history_growth, decode_tokens;
-    int template_tokens, concurrency, budget_blocks;
-    unsigned long long seed;
-} ref_spec;
 
-typedef struct ref_run_cfg {
-    int policy;  // 0 = lru, 1 = cachesage, 2 = ttl, 3 = belady
-    int budget_blocks;  // <= 0: the spec's pairing
-    int concurrency;    // <= 0: the spec's pairing
-    int block_size;
-    int prefetch;
-    int skip, take;
-    double tau;
-    int e_max;
-    double w_pred;
-    long window;
-    double min_confidence;
-    unsigned long long min_row_count;
-    int budget_per_step;
-} ref_run_cfg;
-
-typedef struct ref_run_out {
-    long n_turns;
-    long* cached_tokens;   // by turn id
-    long* prompt_tokens;
-    double* start_us;
-    double* end_us;
-    long n_evictions;
-    unsigned long long* evictions;
-    long n_warmups;  // drained side effects (executed or dropped)
-    long* warmup_step;
-    unsigned long long* warmup_target;
-    unsigned long long* warmup_tick;
-    double hit_rate;
-    long truncated;
-    long warmups_executed;
-    long warmups_dropped;
-    double sim_us;
-    long n_steps;
-    long events;
-} ref_run_out;
 
 const char* ref_last_error(void) { return g_err.c_str(); }
+const char* ref_last_state(void) { return g_state.c_str(); }
 
 unsigned long long ref_chain_hash(int has_parent, unsigned long long parent, const std::uint32_t* tokens,
                                   size_t n) {
@@ -269,7 +228,15 @@ static CacheSageConfig to_cs_cfg(const ref_run_cfg* c) {
     return cs;
 }
 
-int ref_run(const ref_spec* s, const ref_run_cfg* c, ref_run_out* out) {
+}  // extern "C"
+
+WorkloadSpec ref_to_spec(const ref_spec* s) { return to_spec(s); }
+
+// ref_run with the scoring policy supplied by `make` (nullptr: the reference's own, by
+// c->policy): the unmodified EngineSim / Runtime drive whatever Policy it returns. Used by
+// adapter_check.cpp to run the reference engine over the B200 drop-in policy.
+int ref_run_with(const ref_spec* s, const ref_run_cfg* c, ref_run_out* out,
+                 std::shared_ptr<Policy> (*make)(const CacheSageConfig&, void*), void* ctx) {
     try {
         const Trace trace = generate_trace(to_spec(s));
         EngineConfig ec;
@@ -278,9 +245,14 @@ int ref_run(const ref_spec* s, const ref_run_cfg* c, ref_run_out* out) {
         ec.block_size = c->block_size;
         ec.identity = IdentityConfig{c->skip, c->take};
         ec.prefetch_enabled = c->prefetch != 0;
+        if (c->prefill_base_us != 0.0) ec.cost.prefill_base_us = c->prefill_base_us;
+        if (c->prefill_per_token_us != 0.0) ec.cost.prefill_per_token_us = c->prefill_per_token_us;
+        if (c->decode_per_token_us != 0.0) ec.cost.decode_per_token_us = c->decode_per_token_us;
         const auto requests = materialize_requests(trace, ec.block_size, ec.identity);
         auto rec = std::make_shared<RecordingPolicy>();
-        if (c->policy == 0) {
+        if (make) {
+            rec->inner = make(to_cs_cfg(c), ctx);
+        } else if (c->policy == 0) {
             rec->inner = std::make_shared<LruPolicy>();
         } else if (c->policy == 2) {
             rec->inner = std::make_shared<TtlPolicy>();
@@ -300,6 +272,7 @@ int ref_run(const ref_spec* s, const ref_run_cfg* c, ref_run_out* out) {
             ++steps;
         }
         RunResult r = engine.finalize();
+        g_state = rec->inner->serialize_state().dump();
         std::vector<long> cached, prompt;
         std::vector<double> st, en;
         for (const TurnMetrics& t : r.turns) {
@@ -336,6 +309,10 @@ int ref_run(const ref_spec* s, const ref_run_cfg* c, ref_run_out* out) {
         return -1;
     }
 }
+
+extern "C" {
+
+int ref_run(const ref_spec* s, const ref_run_cfg* c, ref_run_out* out) { return ref_run_with(s, c, out, nullptr, nullptr); }
 
 void ref_free_run(ref_run_out* o) {
     std::free(o->cached_tokens);
@@ -392,6 +369,86 @@ int ref_policy_trace(const ref_run_cfg* c, long n, const int* has_prev, const un
         }
         *state_bytes = pol.state_bytes();
         return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
+// Drives the reference Runtime + a policy (policy: 0 lru, 1 cachesage, 2 ttl) with a general
+// event stream (types.hpp:51-82): kind[i] 0 BlockTouch, 1 RequestArrival, 2 AgentDispatch,
+// 3 ToolReturn, 4 TurnComplete; agent[i] = the arrival/tool/dispatch-next AgentId, prev[i] with
+// has_prev[i] for dispatches, request[i]. After event i with drain[i]: drain_side_effects. After
+// event i with ckpt[i]: a checkpoint object {"i", "state": serialize_state().dump(),
+// "predict": predict(1) as [[hex id, p] ...] ranked (p desc, id asc), "next": {hex a:
+// predict_next(a) ranked} for every learner agent, "drained": [[hex target, tick] ...]}.
+// Writes the JSON array of checkpoints into out; returns its length, or -1 (message in
+// ref_last_error; *fail_at = the event index that threw).
+long ref_policy_events(const ref_run_cfg* c, long n, const int* kind, const unsigned long long* tick,
+                       const unsigned long long* agent, const int* has_prev, const unsigned long long* prev,
+                       const unsigned long long* request, const unsigned char* drain, const unsigned char* ckpt,
+                       char* out, long cap, long* fail_at) {
+    *fail_at = -1;
+    try {
+        std::shared_ptr<Policy> pol;
+        std::shared_ptr<CacheSagePolicy> cs;
+        if (c->policy == 0) {
+            pol = std::make_shared<LruPolicy>();
+        } else if (c->policy == 2) {
+            pol = std::make_shared<TtlPolicy>();
+        } else {
+            cs = std::make_shared<CacheSagePolicy>(to_cs_cfg(c));
+            pol = cs;
+        }
+        Runtime rt;
+        rt.register_policy(pol);
+        auto ranked = [](const Forecast& f) {
+            std::vector<std::pair<AgentId, double>> v(f.distribution.begin(), f.distribution.end());
+            std::sort(v.begin(), v.end(), [](const auto& x, const auto& y) {
+                return x.second > y.second || (x.second == y.second && x.first < y.first);
+            });
+            json a = json::array();
+            for (const auto& [id, p] : v) a.push_back(json::array({to_hex(id.value), p}));
+            return a;
+        };
+        json cps = json::array();
+        json drained = json::array();
+        for (long i = 0; i < n; ++i) {
+            Event e;
+            e.tick = tick[i];
+            switch (kind[i]) {
+                case 0: e.payload = BlockTouch{BlockKey{request[i]}, AgentId{agent[i]}}; break;
+                case 1: e.payload = RequestArrival{request[i], AgentId{agent[i]}}; break;
+                case 2: {
+                    std::optional<AgentId> p;
+                    if (has_prev[i]) p = AgentId{prev[i]};
+                    e.payload = AgentDispatch{p, AgentId{agent[i]}};
+                    break;
+                }
+                case 3: e.payload = ToolReturn{AgentId{agent[i]}}; break;
+                default: e.payload = TurnComplete{request[i]}; break;
+            }
+            *fail_at = i;
+            rt.dispatch_event(e);
+            *fail_at = -1;
+            if (drain[i])
+                for (const SideEffect& fx : rt.drain_side_effects())
+                    drained.push_back(json::array({to_hex(fx.target.value), fx.issued_tick}));
+            if (ckpt[i]) {
+                json next = json::object();
+                if (cs)
+                    for (AgentId a : cs->learner().agents()) next[to_hex(a.value)] = ranked(cs->predict_next(a, 1));
+                cps.push_back(json{{"i", i},
+                                   {"state", pol->serialize_state().dump()},
+                                   {"predict", ranked(rt.consult_forecast(1))},
+                                   {"next", std::move(next)},
+                                   {"drained", drained}});
+                drained = json::array();
+            }
+        }
+        const std::string d = cps.dump();
+        if ((long)d.size() < cap) std::memcpy(out, d.c_str(), d.size() + 1);
+        return (long)d.size();
     } catch (const std::exception& e) {
         g_err = e.what();
         return -1;

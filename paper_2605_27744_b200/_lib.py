@@ -22,6 +22,15 @@ CS_NO_AGENT = 0xFFFFFFFF
 vp = C.c_void_p
 
 
+class Event(C.Structure):
+    """cs_event: one observe-stream Event (types.hpp:51-82)."""
+    _fields_ = [("tick", C.c_uint64), ("kind", C.c_int), ("agent", C.c_int), ("prev", C.c_int),
+                ("request", C.c_uint64)]
+
+
+EV_BLOCK_TOUCH, EV_REQUEST_ARRIVAL, EV_AGENT_DISPATCH, EV_TOOL_RETURN, EV_TURN_COMPLETE = range(5)
+
+
 class PoolCfg(C.Structure):
     _fields_ = [
         ("budget_blocks", C.c_int64), ("policy", C.c_int), ("e_max", C.c_int), ("tau", C.c_double),
@@ -56,7 +65,8 @@ class EngineCfg(C.Structure):
     _fields_ = [
         ("pool", PoolCfg), ("concurrency", C.c_int), ("block_size", C.c_int), ("prefetch", C.c_int),
         ("skip", C.c_int), ("take", C.c_int), ("timing", C.c_int), ("host_inputs", C.c_int),
-        ("device_scheduler", C.c_int),
+        ("device_scheduler", C.c_int), ("prefill_per_token_us", C.c_double),
+        ("prefill_base_us", C.c_double), ("decode_per_token_us", C.c_double),
     ]
 
 
@@ -87,6 +97,11 @@ SIGNATURES = {
     "cs_admit_pinned": (C.c_int, [vp, vp, vp, C.c_int, C.c_uint32, C.c_int, C.c_uint64, vp, C.c_int64,
                                   C.POINTER(C.c_int64), vp]),
     "cs_unpin_slots": (C.c_int, [vp, vp, C.c_int]),
+    "cs_unpin": (C.c_int, [vp, vp, C.c_int]),
+    "cs_dispatch_event": (C.c_int, [vp, C.POINTER(Event), C.POINTER(C.c_int)]),
+    "cs_predict": (C.c_int, [vp, C.c_int, C.c_int, vp, vp, vp, C.c_int, C.POINTER(C.c_int)]),
+    "cs_serialize_state": (C.c_int, [vp, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
+    "cs_policy_state_bytes": (C.c_int, [vp, C.POINTER(C.c_uint64)]),
     "cs_restore": (C.c_int, [vp, vp, vp, vp, vp, C.c_int64]),
     "cs_score_snapshot": (C.c_int, [vp, C.c_uint64, vp, vp, C.c_int64, C.POINTER(C.c_int64)]),
     "cs_hops": (C.c_int, [vp, vp, C.c_int]),

@@ -11,8 +11,13 @@ import ctypes as C
 import numpy as np
 
 from . import workloads
-from ._lib import (CS_NO_AGENT, EngineCfg, EngineResult, PoolCfg, PoolStats, WorkloadSpec, check,
+from ._lib import (CS_NO_AGENT, EV_AGENT_DISPATCH, EV_BLOCK_TOUCH, EV_REQUEST_ARRIVAL, EV_TOOL_RETURN,
+                   EV_TURN_COMPLETE, EngineCfg, EngineResult, Event, PoolCfg, PoolStats, WorkloadSpec, check,
                    lib)
+
+EVENT_KINDS = {"block_touch": EV_BLOCK_TOUCH, "request_arrival": EV_REQUEST_ARRIVAL,
+               "agent_dispatch": EV_AGENT_DISPATCH, "tool_return": EV_TOOL_RETURN,
+               "turn_complete": EV_TURN_COMPLETE}
 
 POLICIES = {"lru": 0, "cachesage": 1, "ttl": 2, "belady": 3}
 
@@ -100,9 +105,47 @@ class Pool:
                                     anchor, tick_base, _p(ev), ev.size, C.byref(ne), _p(pins)))
         return ev[:ne.value].copy(), pins[:n].copy()
 
-    def unpin(self, slots):
+    def unpin(self, keys):
+        """EngineSim::unpin (engine.cpp:170-180): one pin per BlockKey; a key that is not resident
+        raises RuntimeError (logic_error "unpin: block vanished while referenced")."""
+        k = _u64(keys)
+        check(lib().cs_unpin(self.h, _p(k), k.size))
+
+    def unpin_slots(self, slots):
+        """The same by the pinned slots admit_pinned returned (no table probe)."""
         s = np.ascontiguousarray(slots, dtype=np.uint32)
         check(lib().cs_unpin_slots(self.h, _p(s), s.size))
+
+    def dispatch_event(self, tick, kind, agent=-1, prev=None, request=0):
+        """Runtime::dispatch_event (runtime.cpp:59-69) -> observe. kind: a key of EVENT_KINDS.
+        A tick below the previous event's raises RuntimeError (tick regression). Returns the
+        agent index of a warmup the dispatch issued, or None."""
+        ev = Event(int(tick), EVENT_KINDS[kind], int(agent), -1 if prev is None else int(prev), int(request))
+        w = C.c_int(-1)
+        check(lib().cs_dispatch_event(self.h, C.byref(ev), C.byref(w)))
+        return None if w.value < 0 else w.value
+
+    def predict(self, horizon=1, current=None):
+        """CacheSagePolicy::predict(horizon) / predict_next(current, horizon)
+        (cachesage_policy.cpp:87-107): [(agent_id, probability, agent_index)] ranked by
+        probability (ties: smaller AgentId first). The Forecast's distribution is
+        {id: p for id, p, _ in result}."""
+        cap = max(self.stats()["n_agents"], 1)
+        ids, pr, ix = np.zeros(cap, np.uint64), np.zeros(cap, np.float64), np.zeros(cap, np.int32)
+        n = C.c_int(0)
+        check(lib().cs_predict(self.h, int(horizon), -1 if current is None else int(current), _p(ids), _p(pr),
+                               _p(ix), cap, C.byref(n)))
+        return [(int(ids[i]), float(pr[i]), int(ix[i])) for i in range(n.value)]
+
+    def serialize_state(self):
+        """Policy::serialize_state().dump() (cachesage_policy.cpp:139-153), as a str."""
+        return serialize_state(self.h)
+
+    def state_bytes(self):
+        """CacheSagePolicy::state_bytes (cachesage_policy.cpp:133-138)."""
+        b = C.c_uint64(0)
+        check(lib().cs_policy_state_bytes(self.h, C.byref(b)))
+        return b.value
 
     def restore(self, keys, last_touch, agents=None, refs=None):
         keys, lt = _u64(keys), _u64(last_touch)
@@ -143,6 +186,14 @@ class Pool:
         d = {f: getattr(s, f) for f, _ in PoolStats._fields_}
         d["phase_ns"] = list(s.phase_ns)
         return d
+
+
+def serialize_state(pool_handle):
+    n = C.c_size_t(0)
+    check(lib().cs_serialize_state(pool_handle, None, 0, C.byref(n)))
+    buf = C.create_string_buffer(n.value + 1)
+    check(lib().cs_serialize_state(pool_handle, buf, n.value + 1, C.byref(n)))
+    return buf.value.decode()
 
 
 def hash_prompts(prompts, block_size=16, skip=4, take=4, pool=None):
@@ -320,10 +371,12 @@ class Engine:
 
     def __init__(self, spec, policy="cachesage", budget=None, concurrency=None, block_size=16, prefetch=True,
                  skip=4, take=4, timing=False, host_inputs=False, comm=None, shard_slots=0,
-                 device_scheduler=False, **pool_kw):
+                 device_scheduler=False, cost_model=None, **pool_kw):
         """comm (shard.Comm): this engine drives ONE shard of a hash-sharded pool of global
         budget `budget`; every shard runs the same trace and reaches the same
-        decisions. shard_slots: the shard's physical slots (0 = 1.25 budget / world + 4096)."""
+        decisions. shard_slots: the shard's physical slots (0 = 1.25 budget / world + 4096).
+        cost_model: dict with any of prefill_per_token_us / prefill_base_us / decode_per_token_us
+        (CostModel, engine.hpp:22-26; the experiment config's "cost_model", experiment.cpp:270-280)."""
         cfg = EngineCfg()
         lib().cs_engine_cfg_default(C.byref(cfg))
         cfg.pool = pool_cfg(budget or 0, policy=policy, **pool_kw)
@@ -334,6 +387,10 @@ class Engine:
         cfg.timing = 1 if timing else 0
         cfg.host_inputs = 1 if host_inputs else 0
         cfg.device_scheduler = 1 if device_scheduler else 0
+        for k, v in (cost_model or {}).items():
+            if k not in ("prefill_per_token_us", "prefill_base_us", "decode_per_token_us"):
+                raise ValueError(f"unknown cost_model key {k!r}")
+            setattr(cfg, k, float(v))
         self._spec = spec_struct(spec)
         self._spec_dict = spec
         self._policy = policy
@@ -412,6 +469,10 @@ class Engine:
         en = np.zeros(max(n, 1), np.float64)
         check(lib().cs_engine_turns(self.h, _p(cached), _p(prompt), _p(st), _p(en), n))
         return {"cached_tokens": cached[:n], "prompt_tokens": prompt[:n], "start_us": st[:n], "end_us": en[:n]}
+
+    def serialize_state(self):
+        """The engine policy's Policy::serialize_state().dump() (cachesage_policy.cpp:139-153)."""
+        return serialize_state(lib().cs_engine_pool(self.h))
 
     def evictions(self):
         n = check(lib().cs_engine_evictions(self.h, None, 0))

@@ -23,7 +23,7 @@ JSON_DIR = os.path.join(sysconfig.get_paths()["purelib"], "include", "cudnn_fron
 NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 DEVICE_SRCS = ["cs_kernels.cu", "cs_admit.cu", "cs_learner.cu", "cs_belady.cu"]
-HOST_SRCS = ["cs_pool.cpp", "cs_engine.cpp", "cs_comm.cpp", "cs_output.cpp"]
+HOST_SRCS = ["cs_pool.cpp", "cs_state.cpp", "cs_engine.cpp", "cs_comm.cpp", "cs_output.cpp"]
 DEPS = DEVICE_SRCS + HOST_SRCS + ["cs_device.cuh", "cs_launch.h", "cs_pool.hpp"]
 
 

@@ -68,6 +68,9 @@ struct AdmSmem {
     long long cached, n_ev_adm, resident, pinned, free_top;
     int first_miss, admit_n, anchor, chunk, started, error, needed, warm_issued, scans;
     int fin_want;  // lists finalized by CTAs other than 0 in the current pass
+    int tomb_snap; // tomb_hi is the status's tombstone count (CTA 1 applies the table queue concurrently)
+    long long tomb_hi;  // tombstones + queued erases when the verdict went out: CTA 1's apply can only
+                        // lower it, so the host's rebuild decision is deterministic and conservative
     int need_full; // a prescan-fed chunk needs the serial replay (every class list): scan instead
     double wsurv[kMaxLists];  // P.wsurv staged on chip (indexed kernel-parameter loads are slow)
     unsigned long long ph[kPhases], tl;  // phase timestamps (CTA 0, thread 0)
@@ -228,6 +231,7 @@ __device__ void observe_dispatch(const DevPool& P, int prev, int next, unsigned 
     // K3: TransitionLearner::record (transition_learner.cpp:22-51): one pair per dispatch
     if (prev >= 0 && tid == 0) {
         const long long head = C->win_head, size = C->win_size;
+        C->recorded += 1ull;
         if (prefetched) {  // the new pair's count and row total (the BFS below needs them)
             BfsSmem& Bq = *reinterpret_cast<BfsSmem*>(dsm);
             Bq.rec_c = atomicAdd(&P.counts[(long long)prev * Acap + next], 1u);
@@ -2600,7 +2604,7 @@ __device__ void write_status(const DevPool& P, const AdmitArgs& a, const AdmSmem
     st->warm_issued = A.warm_issued;
     st->needed = A.needed;
     st->scans = A.scans;
-    st->tombstones = C->tombstones;
+    st->tombstones = A.tomb_snap ? A.tomb_hi : C->tombstones;
     for (int k = 0; k < kPhases; ++k) st->phase_ns[k] = A.ph[k];
     st->n_pend = C->n_pend;
     for (int k = 0; k < C->n_pend && k < kMaxPending; ++k) {
@@ -2640,6 +2644,7 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
             A.needed = 0;
             A.warm_issued = -1;
             A.scans = 0;
+            A.tomb_snap = 0;
             A.first_touch = ~0ull;
             A.tick = a.tick_base;
             for (int k = 0; k < kPhases; ++k) A.ph[k] = 0;
@@ -2983,6 +2988,8 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
             }
             if (tid == 0) {
                 C->verdict = need_loop ? 2 : 1;
+                A.tomb_hi = C->tombstones + (long long)C->tq_erase;  // (before CTA 1 may touch either)
+                A.tomb_snap = need_loop ? 0 : 1;
                 __threadfence();
                 asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(&C->verdict_seq), "l"(a.seq) : "memory");
             }

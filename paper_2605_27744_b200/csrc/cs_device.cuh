@@ -57,6 +57,7 @@ struct Ctrl {
     long long scanned_slots;
     unsigned long long rebuilds;
     long long win_head, win_size;
+    unsigned long long recorded;  // TransitionLearner::recorded_ (transitions_recorded)
     int cur_agent;           // CacheSagePolicy::current_ (-1 = none)
     int reach_built;         // !reach_.empty()
     int step_warmups;

@@ -324,6 +324,9 @@ void cs_engine::build(const cs_engine_cfg& c, const cs_workload_spec* ws, long l
     budget = c.pool.budget_blocks > 0 ? (int)c.pool.budget_blocks : spec.budget_blocks;
     conc = c.concurrency > 0 ? c.concurrency : spec.concurrency;
     if (budget < 1 || conc < 1) throw std::invalid_argument("EngineSim: budget, block size, and concurrency must be positive");
+    // CostModel validation (engine.cpp:60-63)
+    if (!(c.prefill_per_token_us > 0.0) || !(c.prefill_base_us > 0.0) || !(c.decode_per_token_us > 0.0))
+        throw std::invalid_argument("EngineSim: cost model parameters must be positive");
 
     // the spec's generated trace, or an explicit one (a trace read back from JSONL, run_sim)
     std::vector<Turn> turns;
@@ -550,6 +553,9 @@ void cs_engine::dev_setup() {
     std::memset(&hs, 0, sizeof(hs));
     hs.conc = conc;
     hs.budget = budget;
+    hs.cost_base = cfg.prefill_base_us;
+    hs.cost_tok = cfg.prefill_per_token_us;
+    hs.cost_dec = cfg.decode_per_token_us;
     hs.prefetch = cfg.prefetch ? 1 : 0;
     hs.speculate = pool->speculate ? 1 : 0;
     hs.prescan = pool->prescan ? 1 : 0;
@@ -558,6 +564,7 @@ void cs_engine::dev_setup() {
     hs.last_dispatched = -1;
     hs.phase = 0;
     dev = true;
+    pool->mirror_ok = false;  // arrivals and dispatches happen on the device from here on
 }
 
 void cs_engine::dev_run(long long stop_at, long long max_steps) {
@@ -708,7 +715,9 @@ void cs_engine::fetch_victims(unsigned long long before) {
 void cs_engine::arrive(int64_t idx) {
     arrival_us[idx] = sim_now;
     ++tick;  // emit(RequestArrival): note_agent only (no decision depends on alphabet order)
+    if (pool->P.policy == 1) pool->note_agent(reqs[idx].agent);  // for serialize_state's alphabet
     if ((unsigned long long)idx > bel_cursor) bel_cursor = (unsigned long long)idx;  // BeladyPolicy::observe
+    pool->bel_cursor = bel_cursor;
     if (rec_events) ev_push(tick, csb::EventRec::kRequestArrival, (uint64_t)idx, pool->agent_ids[reqs[idx].agent]);
     ready.push_back(idx);
 }
@@ -754,6 +763,7 @@ bool cs_engine::try_start_head() {
     if (cfg.host_inputs) d2h_bytes += (int64_t)sizeof(csb::AdmitStatus);
     if (!st.started) return false;  // wait for in-flight pins to clear
     ready.pop_front();
+    pool->note_dispatch(last_dispatched, r.agent);
     last_dispatched = r.agent;
     tick = st.tick_after;
     if (oversized) ++truncated;
@@ -763,8 +773,9 @@ bool cs_engine::try_start_head() {
     f.npins = st.admit_n;
     f.cached = oversized ? 0 : st.cached;
     f.start_us = sim_now;
-    const double ttft = 1000.0 + 50.0 * (double)(r.prompt_tokens - f.cached);
-    f.end_us = sim_now + ttft + 20000.0 * r.decode;
+    // engine.cpp:302-305: ttft = base + per_token * uncached; end = now + ttft + decode * tokens
+    const double ttft = cfg.prefill_base_us + cfg.prefill_per_token_us * (double)(r.prompt_tokens - f.cached);
+    f.end_us = sim_now + ttft + cfg.decode_per_token_us * r.decode;
     in_flight.push_back(f);
     std::push_heap(in_flight.begin(), in_flight.end(), later);
     fetch_victims(ev_before);
@@ -825,7 +836,8 @@ void cs_engine::execute_warmup(int target) {
     warm_prompt += c.prompt_tokens;
     // engine.cpp:223-227
     warm_uncached += c.prompt_tokens - st.cached;
-    warm_time_us += 1000.0 + 50.0 * (double)(c.prompt_tokens - st.cached) + 20000.0 * 1;
+    warm_time_us += cfg.prefill_base_us + cfg.prefill_per_token_us * (double)(c.prompt_tokens - st.cached) +
+                    cfg.decode_per_token_us * 1;
     fetch_victims(ev_before);
 }
 
@@ -887,6 +899,9 @@ void cs_engine_cfg_default(cs_engine_cfg* c) {
     c->timing = 0;
     c->host_inputs = 0;
     c->device_scheduler = 0;
+    c->prefill_per_token_us = 50.0;  // CostModel defaults (engine.hpp:22-26)
+    c->prefill_base_us = 1000.0;
+    c->decode_per_token_us = 20000.0;
 }
 
 int cs_engine_create(const cs_engine_cfg* cfg, const cs_workload_spec* spec, cs_engine_t* out) {
@@ -1145,9 +1160,9 @@ int cs_engine_write_outputs(cs_engine_t e, const char* dir, const char* workload
         c.block_size = e->bs;
         c.concurrency = e->conc;
         c.prefetch = e->cfg.prefetch != 0;
-        c.prefill_per_token_us = 50.0;
-        c.prefill_base_us = 1000.0;
-        c.decode_per_token_us = 20000.0;
+        c.prefill_per_token_us = e->cfg.prefill_per_token_us;
+        c.prefill_base_us = e->cfg.prefill_base_us;
+        c.decode_per_token_us = e->cfg.decode_per_token_us;
         const cs_pool_cfg& pc = e->cfg.pool;
         c.skip = e->cfg.skip;
         c.take = e->cfg.take;
@@ -1172,7 +1187,8 @@ int cs_engine_write_outputs(cs_engine_t e, const char* dir, const char* workload
             t.label = r.spec_agent;
             t.prompt_tokens = (long)e->t_prompt[i];
             t.cached_tokens = (long)e->t_cached[i];
-            t.ttft_us = 1000.0 + 50.0 * (double)(r.prompt_tokens - e->t_cached[i]);  // engine.cpp:300-302
+            t.ttft_us = e->cfg.prefill_base_us +
+                        e->cfg.prefill_per_token_us * (double)(r.prompt_tokens - e->t_cached[i]);  // engine.cpp:302-304
             t.arrival_us = e->arrival_us[i];
             t.start_us = e->t_start[i];
             t.end_us = e->t_end[i];

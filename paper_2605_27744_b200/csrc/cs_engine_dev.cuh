@@ -223,8 +223,9 @@ __device__ int eng_schedule(const DevPool& P, const EngDev& E, EngState& s, cons
                 f.npins = A.admit_n;
                 f.cached = oversized ? 0 : A.cached;
                 f.start_us = s.sim_now;
-                const double ttft = __dadd_rn(1000.0, __dmul_rn(50.0, (double)(r.prompt_tokens - f.cached)));
-                f.end_us = __dadd_rn(__dadd_rn(s.sim_now, ttft), __dmul_rn(20000.0, (double)r.decode));
+                const double ttft =
+                    __dadd_rn(s.cost_base, __dmul_rn(s.cost_tok, (double)(r.prompt_tokens - f.cached)));
+                f.end_us = __dadd_rn(__dadd_rn(s.sim_now, ttft), __dmul_rn(s.cost_dec, (double)r.decode));
                 f.pad = 0;
                 heap_push(s, f);
                 s.progressed = 1;

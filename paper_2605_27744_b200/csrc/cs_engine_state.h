@@ -27,6 +27,7 @@ struct EngFlight {
 // lives in device memory between launches and in CTA 0's shared memory during one.
 struct EngState {
     int conc, budget, prefetch, speculate, prescan, use_prescan, n_sessions;
+    double cost_base, cost_tok, cost_dec;  // CostModel (engine.hpp:22-26)
     int active_sessions, next_session;
     int ready_head, ready_n;
     int ready[kMaxConc + 1];

@@ -55,6 +55,7 @@ __global__ void init_pool_kernel(DevPool P) {
         C->rebuilds = 0;
         C->win_head = 0;
         C->win_size = 0;
+        C->recorded = 0;
         C->cur_agent = -1;
         C->reach_built = 0;
         C->step_warmups = 0;
@@ -244,6 +245,58 @@ __global__ void probe_kernel(DevPool P, const unsigned long long* keys, int n, i
     if (lane_id() == 0 && c) atomicAdd(needed, c);
 }
 
+// EngineSim::unpin by key (engine.cpp:170-180), step 1: the slot of every key. The reference
+// throws "unpin: block vanished while referenced" at the first key that is not resident, after
+// unpinning the keys before it; *first_bad is the smallest such index (n: none). A resident key
+// with no pin left (the reference would drive refs negative) is reported the same way.
+__global__ void unpin_find_kernel(DevPool P, const unsigned long long* keys, int n, unsigned int* slots,
+                                  int* first_bad) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const unsigned int s = table_find(P, keys[i]);
+    slots[i] = s;
+    if (s == kNoSlot || P.refs[s] == 0u) atomicMin(first_bad, i);
+}
+
+// CacheSagePolicy::predict_next (cachesage_policy.cpp:94-107): the full MLE row of `cur`,
+// count / row_total in fp64, ranked for prefetch (the warmup candidates of maybe_prefetch,
+// :109-123): descending count, ties to the smaller 64-bit AgentId exactly as argmax_row breaks
+// them (transition_learner.cpp:79-96), so entry 0 is the argmax. One CTA; the row (A <= 4096
+// u32 counts) is read once and its non-zero cells ranked in shared memory.
+__global__ void __launch_bounds__(1024) forecast_kernel(DevPool P, int cur, int n_agents, int* out_idx,
+                                                       double* out_p, int* out_n) {
+    __shared__ int nz;
+    __shared__ int z_idx[kMaxAgents];
+    __shared__ unsigned int z_cnt[kMaxAgents];
+    const int tid = threadIdx.x, T = blockDim.x;
+    if (tid == 0) nz = 0;
+    __syncthreads();
+    const unsigned int* row = P.counts + (long long)cur * P.a_cap;
+    for (int b = tid; b < n_agents; b += T) {
+        const unsigned int c = row[b];
+        if (c) {
+            const int k = atomicAdd(&nz, 1);
+            z_idx[k] = b;
+            z_cnt[k] = c;
+        }
+    }
+    __syncthreads();
+    const int m = nz;
+    const double total = (double)P.totals[cur];
+    for (int k = tid; k < m; k += T) {
+        const unsigned int c = z_cnt[k];
+        const unsigned long long id = P.agent_ids[z_idx[k]];
+        int rank = 0;
+        for (int j = 0; j < m; ++j) {
+            const unsigned int cj = z_cnt[j];
+            rank += (cj > c || (cj == c && P.agent_ids[z_idx[j]] < id)) ? 1 : 0;
+        }
+        out_idx[rank] = z_idx[k];
+        out_p[rank] = __ddiv_rn((double)c, total);
+    }
+    if (tid == 0) *out_n = m;
+}
+
 __global__ void min_lt_kernel(DevPool P, unsigned long long* out) {
     unsigned long long m = ~0ull;
     for (long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x; s < P.cap;
@@ -345,6 +398,18 @@ cudaError_t launch_chain_hash(const unsigned long long* parents, const unsigned 
 cudaError_t launch_identity(const unsigned long long* keys, const long long* key_off, int n, int skip, int take,
                             unsigned long long* out, cudaStream_t s) {
     if (n > 0) identity_kernel<<<(n + 127) / 128, 128, 0, s>>>(keys, key_off, n, skip, take, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_unpin_find(const DevPool& P, const unsigned long long* keys, int n, unsigned int* slots,
+                              int* first_bad, cudaStream_t s) {
+    if (n > 0) unpin_find_kernel<<<(n + 255) / 256, 256, 0, s>>>(P, keys, n, slots, first_bad);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_forecast(const DevPool& P, int cur, int n_agents, int* out_idx, double* out_p, int* out_n,
+                            cudaStream_t s) {
+    forecast_kernel<<<1, 1024, 0, s>>>(P, cur, n_agents, out_idx, out_p, out_n);
     return cudaGetLastError();
 }
 

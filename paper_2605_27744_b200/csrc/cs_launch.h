@@ -142,6 +142,12 @@ cudaError_t launch_unpin(const DevPool& P, const unsigned int* slots, int n, cud
 cudaError_t launch_restore(const DevPool& P, const unsigned long long* keys, const unsigned long long* lt,
                            const unsigned int* agents, const unsigned int* refs, long long n, cudaStream_t s);
 cudaError_t launch_probe(const DevPool& P, const unsigned long long* keys, int n, int* needed, cudaStream_t s);
+// EngineSim::unpin by key, step 1 (slot per key; *first_bad = first missing/unpinned index)
+cudaError_t launch_unpin_find(const DevPool& P, const unsigned long long* keys, int n, unsigned int* slots,
+                              int* first_bad, cudaStream_t s);
+// CacheSagePolicy::predict_next: the MLE row of cur, ranked (count desc, AgentId asc)
+cudaError_t launch_forecast(const DevPool& P, int cur, int n_agents, int* out_idx, double* out_p, int* out_n,
+                            cudaStream_t s);
 cudaError_t launch_scores(const DevPool& P, unsigned long long now, unsigned long long* keys, double* scores,
                           long long* n_out, unsigned long long* scratch, cudaStream_t s);
 cudaError_t launch_table_rebuild(const DevPool& P, cudaStream_t s);

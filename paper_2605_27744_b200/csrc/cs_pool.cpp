@@ -442,7 +442,9 @@ const csb::AdmitStatus& cs_pool::admit_belady(const csb::AdmitArgs& in, int n_fo
 
 const csb::AdmitStatus& cs_pool::admit(const csb::AdmitArgs& in, int n_for_grid) {
     // the packed scan word keeps 40 bits of last_touch (cs_device.cuh)
-    if (in.tick_base + 2ull * (unsigned long long)std::max(in.n, 0) + 16ull > csb::kMaxTick)
+    // (no wrap: a caller-supplied tick_base near 2^64 must not pass; a dispatch-only call writes
+    // no last_touch, so any event tick is fine there)
+    if (in.n > 0 && in.tick_base > csb::kMaxTick - (2ull * (unsigned long long)in.n + 16ull))
         throw CsError(CS_ERR_CAPACITY, "tick space exhausted (last_touch must stay below 2^40 - 1)");
     if (comm) return admit_sharded(in);
     if (P.policy == 3) return admit_belady(in, n_for_grid);
@@ -865,6 +867,7 @@ int cs_observe_dispatch(cs_pool_t pool, int prev, int next, uint64_t tick, int* 
     return guard([&] {
         if (!pool || next < 0 || next >= pool->n_agents || prev >= pool->n_agents)
             throw std::invalid_argument("cs_observe_dispatch: agent index out of range");
+        pool->check_tick(tick);  // Runtime::dispatch_event (runtime.cpp:59-64)
         csb::AdmitArgs a{};
         a.keys = nullptr;
         a.counts = nullptr;
@@ -875,6 +878,7 @@ int cs_observe_dispatch(cs_pool_t pool, int prev, int next, uint64_t tick, int* 
         a.agent = CS_NO_AGENT;
         a.tick_base = tick - 1;  // the kernel assigns tick_base + 1 to the dispatch
         const auto& st = pool->admit(a, 0);
+        pool->note_dispatch(prev, next);
         if (warmup_target) *warmup_target = st.warm_issued;
     });
 }
@@ -1033,6 +1037,7 @@ int cs_set_hops(cs_pool_t pool, const uint8_t* hops, int n) {
                            cudaMemcpyHostToDevice, pool->stream),
            "reach_built H2D");
         pool->pre_ok = false;  // classes changed out of band: no prescan reuse
+        pool->reach_known = (size_t)n;
         pool->sync();
     });
 }

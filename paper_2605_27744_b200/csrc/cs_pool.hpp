@@ -67,6 +67,23 @@ struct cs_pool {
     unsigned long long ev_total = 0;     // evictions logged so far
     std::vector<int> pending_targets;
     std::vector<unsigned long long> pending_ticks;
+    // Host mirror of what the reference keeps outside the counts (cs_state.cpp):
+    // Runtime::last_tick_ (runtime.cpp:59-64), TransitionLearner::alphabet_ in note_agent order
+    // (transition_learner.cpp:16-20), |ReachabilityState::hops| of the last rebuild
+    // (reachability.cpp:48-51: every agent known then), BeladyPolicy::cursor_.
+    bool has_last_tick = false;
+    unsigned long long last_tick = 0;
+    std::vector<int> alphabet;
+    std::vector<unsigned char> noted;
+    size_t reach_known = 0;
+    int host_cur = -1;
+    unsigned long long bel_cursor = 0;
+    bool mirror_ok = true;  // false once a device-resident scheduler observes events on the device
+    void note_agent(int a);
+    // AgentDispatch{prev, next} as CacheSagePolicy::observe notes it (cachesage_policy.cpp:57-66)
+    void note_dispatch(int prev, int next);
+    // Runtime::dispatch_event's tick check (runtime.cpp:59-64): CS_ERR_RUNTIME on a regression
+    void check_tick(unsigned long long tick);
     // scratch
     csb::DevBuf d_keys, d_counts, d_pins, d_aux, d_aux2, d_aux3;
     // timing (CUDA events around each admission launch)

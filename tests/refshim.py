@@ -36,7 +36,8 @@ class RefRunCfg(C.Structure):
         ("block_size", C.c_int), ("prefetch", C.c_int), ("skip", C.c_int), ("take", C.c_int),
         ("tau", C.c_double), ("e_max", C.c_int), ("w_pred", C.c_double), ("window", C.c_long),
         ("min_confidence", C.c_double), ("min_row_count", C.c_ulonglong),
-        ("budget_per_step", C.c_int),
+        ("budget_per_step", C.c_int), ("prefill_base_us", C.c_double),
+        ("prefill_per_token_us", C.c_double), ("decode_per_token_us", C.c_double),
     ]
 
 
@@ -189,7 +190,8 @@ POLICY_IDS = {"lru": 0, "cachesage": 1, "ttl": 2, "belady": 3}
 
 def run_cfg(policy="cachesage", budget=None, concurrency=None, block_size=16, prefetch=True,
             skip=4, take=4, tau=0.01, e_max=8, w_pred=1.0, window=1024, min_confidence=0.5,
-            min_row_count=5, budget_per_step=1):
+            min_row_count=5, budget_per_step=1, cost=None):
+    """cost = (prefill_base_us, prefill_per_token_us, decode_per_token_us) or None (defaults)."""
     c = RefRunCfg()
     c.policy = POLICY_IDS[policy]
     c.budget_blocks = budget or 0
@@ -199,6 +201,8 @@ def run_cfg(policy="cachesage", budget=None, concurrency=None, block_size=16, pr
     c.skip, c.take, c.tau, c.e_max, c.w_pred = skip, take, tau, e_max, w_pred
     c.window, c.min_confidence, c.min_row_count = window, min_confidence, min_row_count
     c.budget_per_step = budget_per_step
+    if cost is not None:
+        c.prefill_base_us, c.prefill_per_token_us, c.decode_per_token_us = cost
     return c
 
 
@@ -226,6 +230,13 @@ def run(spec, **kw):
     finally:
         lib().ref_free_run(C.byref(o))
     return res
+
+
+def last_state():
+    """The final Policy::serialize_state().dump() of the last run() on this thread."""
+    f = lib().ref_last_state
+    f.restype = C.c_char_p
+    return f().decode()
 
 
 def fnv1a64(keys) -> int:
@@ -314,3 +325,33 @@ def run_experiment(config):
     r = subprocess.run([exe], input=_json.dumps(config).encode(), capture_output=True)
     if r.returncode != 0:
         raise RuntimeError(r.stderr.decode())
+
+
+def policy_events(events, **kw):
+    """ref_policy_events: the reference Runtime + policy over an event stream. events: list of
+    dicts {kind (0..4), tick, agent, prev (None or id), request, drain (bool), ckpt (bool)}.
+    Returns (checkpoints, None) or (None, (fail_index, message))."""
+    import json
+
+    c = run_cfg(**kw)
+    n = len(events)
+    kind = np.array([e["kind"] for e in events], np.int32)
+    tick = np.array([e["tick"] for e in events], np.uint64)
+    agent = np.array([e.get("agent", 0) for e in events], np.uint64)
+    has_prev = np.array([e.get("prev") is not None for e in events], np.int32)
+    prev = np.array([e.get("prev") or 0 for e in events], np.uint64)
+    req = np.array([e.get("request", 0) for e in events], np.uint64)
+    drain = np.array([1 if e.get("drain") else 0 for e in events], np.uint8)
+    ckpt = np.array([1 if e.get("ckpt") else 0 for e in events], np.uint8)
+    fail = C.c_long(-1)
+    L = lib()
+    f = L.ref_policy_events
+    f.restype = C.c_long
+    f.argtypes = [C.POINTER(RefRunCfg), C.c_long] + [C.c_void_p] * 8 + [C.c_char_p, C.c_long, C.POINTER(C.c_long)]
+    args = [C.byref(c), n] + [_ptr(a) for a in (kind, tick, agent, has_prev, prev, req, drain, ckpt)]
+    m = f(*args, None, 0, C.byref(fail))
+    if m < 0:
+        return None, (fail.value, _err())
+    buf = C.create_string_buffer(m + 1)
+    f(*args, buf, m + 1, C.byref(fail))
+    return json.loads(buf.value.decode()), None

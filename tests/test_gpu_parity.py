@@ -181,7 +181,10 @@ def test_admissions_on_snapshots_match_oracle(seed, n, n_agents, pinned, policy)
         pins_g.append((pins, prompt))
         if len(pins_g) > 3:  # complete the oldest flight
             pslots, pkeys = pins_g.pop(0)
-            g.unpin(pslots)
+            if step % 2:  # EngineSim::unpin by BlockKey (cs_unpin) and by slot (cs_unpin_slots)
+                g.unpin(pkeys)
+            else:
+                g.unpin_slots(pslots)
             o.unpin(pkeys)
         if w is not None:
             tg, _ = g.poll_actions()

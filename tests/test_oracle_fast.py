@@ -8,11 +8,13 @@ generators and on pre-filled snapshots, and (3) oracle/_ref itself on random spe
 """
 import json
 import os
+import sys
 
 import numpy as np
 import pytest
 
 from oracle import pyoracle as O
+from paper_2605_27744_b200 import workloads as W
 import refshim
 
 GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
@@ -124,3 +126,31 @@ def test_fast_oracle_vs_reference_random(seed):
         for f in ("cached_tokens", "evictions", "warmup_step", "warmup_target", "warmup_tick"):
             assert np.array_equal(np.asarray(ref[f]), np.asarray(mine[f])), f
         assert ref["n_steps"] == mine["n_steps"]
+
+
+@pytest.mark.skipif(not refshim.available(), reason="oracle/_ref not built (needs /root/reference)")
+@pytest.mark.parametrize("cost", [(500.0, 20.0, 9000.0), (3000.0, 7.5, 41000.0)])
+def test_cost_model_matches_reference(cost):
+    """A non-default CostModel (experiment.cpp:270-280) moves completion times and so the pin
+    release order: the oracle follows the reference bit for bit (end_us bits, victims)."""
+    for name, budget in (("cfg1", 256), ("cfg1", 128), ("supervisor-a", 60)):
+        spec = W.cfg1(budget) if name == "cfg1" else W.preset_by_name(name)
+        ref = refshim.run(spec, policy="cachesage", budget=budget, cost=cost)
+        mine = O.run(spec, fast=True, policy="cachesage", budget=budget, cost=cost)
+        assert np.array_equal(ref["end_us"].view(np.uint64), mine["end_us"].view(np.uint64))
+        assert np.array_equal(ref["evictions"], mine["evictions"])
+        assert np.array_equal(ref["cached_tokens"], mine["cached_tokens"])
+
+
+@pytest.mark.skipif(not refshim.available(), reason="oracle/_ref not built (needs /root/reference)")
+def test_policy_state_fixture_is_the_reference():
+    """tests/golden/policy_state.json (the GPU serialize_state / predict / event-stream parity
+    fixture) is what the reference produces for the same streams today."""
+    sys.path.insert(0, GOLD)
+    import make_policy_state as M
+
+    gold = json.load(open(os.path.join(GOLD, "policy_state.json")))["cases"]
+    for (name, seed, na, ne, kw), g in zip(M.CASES, gold):
+        _, ev = M.stream(seed, na, ne)
+        cps, err = refshim.policy_events(ev, **kw)
+        assert err is None and cps == g["checkpoints"], name

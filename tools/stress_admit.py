@@ -42,7 +42,7 @@ for it in range(args.iters):
     ev, pins = g.admit_pinned(prompt, np.full(args.k, 16, np.int32), agent=a, anchor=8, tick_base=tick)
     times.append(time.perf_counter() - t0)
     tick += args.k
-    g.unpin(pins)
+    g.unpin_slots(pins)
 st1 = g.stats()
 ph = np.array(st1["phase_ns"], dtype=np.float64) - np.array(st0["phase_ns"], dtype=np.float64)
 n = args.iters
