@@ -68,9 +68,7 @@ struct AdmSmem {
     long long cached, n_ev_adm, resident, pinned, free_top;
     int first_miss, admit_n, anchor, chunk, started, error, needed, warm_issued, scans;
     int fin_want;  // lists finalized by CTAs other than 0 in the current pass
-    int tomb_snap; // tomb_hi is the status's tombstone count (CTA 1 applies the table queue concurrently)
-    long long tomb_hi;  // tombstones + queued erases when the verdict went out: CTA 1's apply can only
-                        // lower it, so the host's rebuild decision is deterministic and conservative
+    int q_deleg;   // CTA kSvcQ applies the previous queue: wait for it before touching the counters
     int need_full; // a prescan-fed chunk needs the serial replay (every class list): scan instead
     double wsurv[kMaxLists];  // P.wsurv staged on chip (indexed kernel-parameter loads are slow)
     unsigned long long ph[kPhases], tl;  // phase timestamps (CTA 0, thread 0)
@@ -150,9 +148,9 @@ struct ReplaySmem {
 // speculative pass, so CTA 0 prepares the prologue while the other CTAs still stream.
 static_assert(sizeof(ReplaySmem) <= kRing * kRingStage, "replay view must fit the TMA ring");
 
-// Early prescan validation (CTA 0, pre path): loaded during phase 0's two load rounds, so the
-// consumer of a prescan works on chip. Lives in the TMA ring above the replay view.
-constexpr int kEarlyP = 256;  // agent-carrying entries validated early (more: the late consumer)
+// The prescan consumer's view (CTA 0, pipelined launch): the list service's E and R lists, the
+// set U re-read in phase 0 and the slots this launch's lookup touched. Lives in the TMA ring
+// above the replay view.
 constexpr int kTset = 1024;   // slots touched by this launch's lookup (hash)
 struct EarlySmem {
     unsigned long long E_lt[kPreK], E_key[kPreK];
@@ -161,9 +159,6 @@ struct EarlySmem {
     unsigned long long R_lt[kPreK];
     unsigned int R_slot[kPreK];
     unsigned char R_ok[kPreK];
-    unsigned long long P_lt[kEarlyP];
-    unsigned int P_slot[kEarlyP], P_agent[kEarlyP];
-    unsigned char P_ok[kEarlyP];
     unsigned long long U_lt[kXset];  // U re-read after the unpins, by xset position
     unsigned int U_agent[kXset];
     unsigned char U_ok[kXset];
@@ -187,6 +182,7 @@ struct BfsSmem {
     unsigned int rec_c, rec_t;  // the record's counts[prev][next] and totals[prev] before it
 };
 static_assert(sizeof(BfsSmem) <= kOffCls, "BFS view must fit the scan region");
+static_assert(sizeof(SelectSmem) <= 4096, "service_lists keeps its per-CTA offsets after a SelectSmem in the ring");
 
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
@@ -1283,11 +1279,10 @@ __device__ __forceinline__ unsigned long long next_hint_mid(unsigned long long v
 }
 
 __device__ void prescan_pass(const DevPool& P, const ScanBufs& B, ScanSmem& S, unsigned char* dsm, int par,
-                             bool after_writes) {
-    Ctrl* C = P.ctrl;
+                             bool after_writes, unsigned long long seq) {
     const int tid = threadIdx.x, T = blockDim.x;
     const long long TV = kTile;
-    const int nscan = (int)gridDim.x - 1, me = (int)blockIdx.x - 1;
+    const int nscan = (int)gridDim.x - kStream0, me = (int)blockIdx.x - kStream0;
     long long per = (P.cap_scan + nscan - 1) / nscan;
     per = (per + kV - 1) / kV * kV;
     const long long lo = min(P.cap_scan, (long long)me * per);
@@ -1308,8 +1303,9 @@ __device__ void prescan_pass(const DevPool& P, const ScanBufs& B, ScanSmem& S, u
     if (after_writes) fence_proxy_async_smem();  // pool slots written earlier in this launch
     // (the thresholds load while the first tiles are in flight) agent-carrying slots share E's
     // threshold: the E members among them are complete to it, and the other classes' lists are
-    // only needed non-empty (see consume_prescan)
-    const unsigned long long hE = __ldcg(P.pre_hint + 0), hR = __ldcg(P.pre_hint + 1), hP = hE;
+    // only needed non-empty (see consume_svc). This launch's parity slot: the list service of the
+    // previous launch wrote it, the one of this launch writes the other slot.
+    const unsigned long long hE = __ldcg(P.pre_hint + par * 3 + 0), hR = __ldcg(P.pre_hint + par * 3 + 1), hP = hE;
     // list ids: 0 = E (agentless unpinned), 1 = R (resident), 2 = pending (agent, unpinned)
     auto classify_append = [&](const unsigned long long (&x4)[kV], const unsigned int (&a4)[kV],
                                const unsigned int (&r4)[kV], long long i0) {
@@ -1404,41 +1400,26 @@ __device__ void prescan_pass(const DevPool& P, const ScanBufs& B, ScanSmem& S, u
     }
     __syncthreads();
     if (tid == 0) P.dbg[blockIdx.x * 16 + 1] = gtimer();
-    if (S.overflow) {
-        if (tid == 0) atomicExch(&C->pre_bad[par], 1);
-        return;
-    }
-    // every staged candidate to global memory: E and R raw (selected after the barrier), the
-    // agent-carrying ones straight into the output list with their agent
-    const int m = S.count;
-    for (int j0 = 0; j0 < m; j0 += T) {
-        const int j = j0 + tid;
-        const unsigned int act = __ballot_sync(0xffffffffu, j < m);
-        if (j >= m) continue;
+    // this CTA's staged candidates, as staged, into its own raw region (no global atomics, no
+    // cross-CTA wait): the next launch's list service gathers and finalizes them
+    const size_t base = ((size_t)par * P.raw_grid + me) * kRawCap;
+    // (an overflowed pass keeps what it staged: a subset, from which the service derives a
+    // tighter threshold for the next prescan; the lists themselves are then unusable)
+    const int m = min(S.count, kRawCap);
+    for (int j = tid; j < m; j += T) {
         const unsigned int l = B.st_list[j];
-        const unsigned int peers = __match_any_sync(act, l);
-        const int leader = __ffs(peers) - 1;
-        int base = 0;
-        if (lane_id() == leader) base = atomicAdd(&C->pre_cnt[par][l], __popc(peers));
-        base = __shfl_sync(peers, base, leader);
-        const int pos = base + __popc(peers & ((1u << lane_id()) - 1u));
-        const unsigned long long x = B.st_lt[j];
         const unsigned int s = B.st_slot[j];
-        if (l < 2) {
-            if (pos < P.pre_gcap) {
-                P.pre_buf_lt[l * P.pre_gcap + pos] = x;
-                P.pre_buf_slot[l * P.pre_gcap + pos] = s;
-            } else {
-                atomicExch(&C->pre_bad[par], 1);
-            }
-        } else if (pos < kPendCap) {
-            const size_t o = ((size_t)par * 3 + 2) * kPendCap + pos;
-            P.pl_lt[o] = x;
-            P.pl_slot[o] = s;
-            P.pl_agent[(size_t)par * kPendCap + pos] = __ldcg(P.agent + s);
-        } else {
-            atomicExch(&C->pre_bad[par], 1);
-        }
+        P.raw_lt[base + j] = B.st_lt[j];
+        P.raw_slot[base + j] = s;
+        P.raw_list[base + j] = (unsigned char)l;
+        if (l == 2) P.raw_agent[base + j] = __ldcg(P.agent + s);  // agent-carrying: its agent index
+    }
+    if (tid == 0) {
+        RawHdr h;
+        h.seq = seq;
+        h.n = m;
+        h.bad = S.overflow ? 1 : 0;
+        P.raw_hdr[(size_t)par * P.raw_grid + me] = h;  // (a kernel boundary orders it before the reader)
     }
 }
 
@@ -1464,215 +1445,202 @@ __device__ void prescan_barrier(Ctrl* c) {
     __syncthreads();
 }
 
-constexpr int kDirectPre = 1024;  // prescan_finalize ranks up to this many candidates directly
-
-// List l (0 = E, 1 = R) of the prescan: its kPreK oldest, sorted, and the completeness bound.
-// The raw candidates (a few hundred with a good threshold) are staged on chip first.
-__device__ void prescan_finalize(const DevPool& P, const ScanBufs& B, SelectSmem& Sel, int par, int l,
-                                 unsigned long long h) {
+// The table service (CTA kSvcQ of a pipelined launch): applies the block-table updates the
+// previous admission queued (every erase, then every insert: a key erased and re-admitted in one
+// admission is inserted after its erase), concurrently with CTA 0's probe, which resolves the
+// queued keys from its on-chip overlay (a table operation on one key never misleads a find of
+// another: finds skip claimed and erased entries, and an erased entry's key is cleared first).
+// CTA 0 owns the queue counters: it resets them once it has seen svc_q_seq.
+__device__ void service_queue(const DevPool& P, const AdmitArgs& a, RedSmem& Red) {
     Ctrl* C = P.ctrl;
     const int tid = threadIdx.x, T = blockDim.x;
-    const int m = min(*(volatile int*)&C->pre_cnt[par][l], (int)P.pre_gcap);
-    const unsigned long long* g = P.pre_buf_lt + l * P.pre_gcap;
-    const unsigned int* gs = P.pre_buf_slot + l * P.pre_gcap;
-    const bool local = m <= kStage;
+    const int ne = C->tq_erase, ni = C->tq_insert;
+    if (tid == 0) P.dbg[blockIdx.x * 16 + 6] = gtimer();
+    for (int k = tid; k < ne; k += T) table_erase(P, P.tq_key[k]);
+    __syncthreads();
+    long long reused = 0;
+    for (int i = tid; i < ni; i += T) reused += table_insert(P, P.tq_key[P.p_cap + i], P.tq_slot[i]);
+    reused = block_sum(reused, Red);
     if (tid == 0) {
-        P.dbg[blockIdx.x * 16 + 6] = (unsigned long long)m;
+        C->tombstones += (long long)ne - reused;
+        __threadfence();
+        asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(&C->svc_q_seq), "l"(a.seq) : "memory");
         P.dbg[blockIdx.x * 16 + 7] = gtimer();
     }
-    if (local) {
-        for (int j = tid; j < m; j += T) {
-            B.st_lt[j] = __ldcg(g + j);
-            B.st_slot[j] = __ldcg(gs + j);
-        }
-        __syncthreads();
-    }
-    if (tid == 0) P.dbg[blockIdx.x * 16 + 8] = gtimer();
-    const unsigned long long* src = local ? B.st_lt : g;
-    const unsigned int* srs = local ? B.st_slot : gs;
-    const size_t base = ((size_t)par * 3 + l) * kPendCap;
-    if (local && m <= kDirectPre) {
-        // few candidates (the usual case): every entry's rank in one pass, no radix rounds
-        if (tid == 0) {
-            Sel.prefix = kNoBound;
-            Sel.acc_or = kNoBound;
-        }
-        __syncthreads();
-        unsigned long long vk = kNoBound, v1 = kNoBound;
-        for (int j = tid; j < m; j += T) {
-            const unsigned long long x = src[j];
-            const int r = count_below(src, m, x);
-            if (r < kPreK) {
-                P.pl_lt[base + r] = x;
-                P.pl_slot[base + r] = srs[j];
-            }
-            if (r == kPreK - 1) vk = x;
-            if (r == 0) v1 = x;
-            if (r == kPreK / 2 - 1) Sel.acc_or = x;
-        }
-        if (vk != kNoBound) Sel.prefix = vk;
-        if (v1 != kNoBound) Sel.hmax = v1;
-        __syncthreads();
-        if (tid == 0) {
-            const int n = min(m, kPreK);
-            const unsigned long long Tl = m > kPreK ? Sel.prefix : h;
-            const int bad = *(volatile int*)&C->pre_bad[par];
-            P.pl_n[par * 3 + l] = n;
-            P.pl_T[par * 3 + l] = Tl;
-            P.pre_hint[l] = n == 0 ? kNoBound : bad ? Tl : n == kPreK ? next_hint_mid(Sel.acc_or, Tl) : next_hint(Sel.hmax, Tl);
-        }
-        __syncthreads();
-        return;
-    }
-    unsigned long long v = kNoBound;
-    if (m > kPreK) v = block_kth(src, nullptr, 0, m, kPreK, Sel);
-    if (tid == 0) Sel.tmp = 0;
-    __syncthreads();
-    for (int j = tid; j < m; j += T) {
-        const unsigned long long x = src[j];
-        if (m <= kPreK || x <= v) {
-            const int p = atomicAdd(&Sel.tmp, 1);
-            B.sd_lt[p] = x;
-            B.sd_slot[p] = srs[j];
-        }
-    }
-    __syncthreads();
-    const int n = Sel.tmp;  // distinct ticks: exactly min(m, kPreK)
-    if (tid == 0) Sel.acc_or = kNoBound;
-    __syncthreads();
-    unsigned long long v1 = kNoBound;
-    for (int j = tid; j < n; j += T) {
-        const unsigned long long x = B.sd_lt[j];
-        const int r = count_below(B.sd_lt, n, x);
-        P.pl_lt[base + r] = x;
-        P.pl_slot[base + r] = B.sd_slot[j];
-        if (r == 0) v1 = x;
-        if (r == kPreK / 2 - 1) Sel.acc_or = x;
-    }
-    if (v1 != kNoBound) Sel.prefix = v1;  // the unique rank-0 entry
-    __syncthreads();
-    if (tid == 0) {
-        const unsigned long long Tl = m > kPreK ? v : h;
-        const int bad = *(volatile int*)&C->pre_bad[par];
-        P.pl_n[par * 3 + l] = n;
-        P.pl_T[par * 3 + l] = Tl;
-        // an overflowed pass staged a subset: its kPreK-th is a tighter, safe next threshold
-        P.pre_hint[l] = n == 0 ? kNoBound
-                        : bad ? (m > kPreK ? v : h)
-                        : n == kPreK ? next_hint_mid(Sel.acc_or, Tl)
-                                     : next_hint(Sel.prefix, Tl);
-    }
-    __syncthreads();
 }
 
-// After every prescan CTA's writeout, CTA 1 alone finalizes the prescan (E and R ranked in one
-// on-chip pass) and publishes it for the next launch; the other prescan CTAs only count their
-// arrival. Thread 0's tail is a short chain: one round of counter loads, then plain stores.
-__device__ void prescan_finish(const DevPool& P, const AdmitArgs& a, const ScanBufs& B, SelectSmem& Sel, int par,
-                               unsigned long long hE, unsigned long long hR, unsigned long long hP) {
-    __shared__ int cnt[4];                  // candidates of E, R, pending; overflow flag
+// Block-wide exclusive prefix sum of one int per thread; *total = the sum (all threads).
+__device__ __forceinline__ int block_excl_scan(int v, RedSmem& Red, int* total) {
+    int incl = v;
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane_id() >= o) incl += y;
+    }
+    __syncthreads();
+    if (lane_id() == 31) Red.v[warp_id()] = incl;
+    __syncthreads();
+    int off = 0;
+    const int nw = (int)blockDim.x >> 5;
+    for (int w = 0; w < warp_id(); ++w) off += (int)Red.v[w];
+    int tot = 0;
+    for (int w = 0; w < nw; ++w) tot += (int)Red.v[w];
+    *total = tot;
+    __syncthreads();
+    return off + incl - v;
+}
+
+constexpr int kSvcStage = kStage / 2;  // E and R candidates the list service stages on chip, each
+
+// The list service (CTA kSvcL of a pipelined launch, all threads): the previous launch's prescan
+// (parity par) for this launch's CTA 0. Gathers the raw candidates every streaming CTA wrote;
+// keeps per list E (agentless unpinned) and R (resident) the kPreK oldest, sorted, with the
+// completeness bound T_l (every member of the state the prescan read at or below T_l is among
+// the candidates); keeps every agent-carrying unpinned candidate (pending, complete to E's
+// threshold); validates each entry against the pool as this launch found it (its last_touch is
+// unchanged: DESIGN.md §5.6; CTA 0 filters this launch's own touches and unpins) and loads the
+// keys of E's head. Publishes through svc_l_seq; writes the acceptance thresholds of the next
+// launch's prescan (the parity slot this prescan used).
+__device__ void service_lists(const DevPool& P, const AdmitArgs& a, const ScanBufs& B, SelectSmem& Sel, RedSmem& Red,
+                              unsigned char* dsm, int par) {
+    int* off = reinterpret_cast<int*>(dsm + kOffRing + 4096);  // per streaming CTA (the ring is idle here)
+    __shared__ int cntL[3];
+    __shared__ int okf;
+    __shared__ unsigned long long hused[2];
+    __shared__ int ng[2];
     Ctrl* C = P.ctrl;
     const int tid = threadIdx.x, T = blockDim.x;
-    __syncthreads();
+    const int ns = (int)gridDim.x - kStream0;
     if (tid == 0) {
-        __threadfence();
-        atomicAdd(&C->pre_arrive[par], 1u);  // this CTA's candidates are in global memory
-    }
-    if (blockIdx.x != 1) return;
-    if (tid == 0) {
-        unsigned long long spins = 0;
-        while (ld_acquire(&C->pre_arrive[par]) < (unsigned int)(gridDim.x - 1)) {
-            if (++spins > 65536) __nanosleep(32);
-            if (spins > (1ull << 28)) __trap();
-        }
-        __threadfence();
-        cnt[0] = min(*(volatile int*)&C->pre_cnt[par][0], (int)P.pre_gcap);
-        cnt[1] = min(*(volatile int*)&C->pre_cnt[par][1], (int)P.pre_gcap);
-        cnt[2] = *(volatile int*)&C->pre_cnt[par][2];
-        cnt[3] = *(volatile int*)&C->pre_bad[par];
         P.dbg[blockIdx.x * 16 + 6] = gtimer();
+        okf = 1;
+        cntL[0] = cntL[1] = cntL[2] = 0;
+        hused[0] = __ldcg(P.pre_hint + par * 3 + 0);
+        hused[1] = __ldcg(P.pre_hint + par * 3 + 1);
     }
+    int nc = 0;
+    bool mine_ok = true, mine_full = true;
+    if (tid < ns) {
+        const RawHdr h = P.raw_hdr[(size_t)par * P.raw_grid + tid];
+        mine_ok = h.seq == a.seq - 1ull;
+        mine_full = !h.bad;
+        nc = mine_ok ? h.n : 0;
+    }
+    int M = 0;
+    const int ex = block_excl_scan(nc, Red, &M);
+    if (tid <= ns) off[tid] = ex;  // off[ns] = M (nc = 0 there)
+    // produced: every streaming CTA of the previous launch wrote its candidates; overflowed:
+    // some staged only a subset (the lists are unusable, the next threshold tightens)
+    const bool produced = !__syncthreads_or(tid < ns && !mine_ok);
+    const bool overflowed = __syncthreads_or(tid < ns && !mine_full);
+    if (tid == 0 && (!produced || overflowed)) okf = 0;
     __syncthreads();
-    const int mE = cnt[0], mR = cnt[1], mP = cnt[2];
-    const bool bad = cnt[3] != 0 || mP > kPendCap;
-    const unsigned long long h[2] = {hE, hR};
-    const int oR = ((mE + 1) & ~1);  // R staged 16-B aligned after E
-    if (oR + mR <= kStage && mE <= kDirectPre && mR <= kDirectPre) {
-        // two warp groups (named barriers 1 and 2): group 0 finalizes E, group 1 R, at once
-        __shared__ int ng[2];
-        const int nw = (int)blockDim.x >> 5, w0 = (nw + 1) >> 1;
-        const int grp = warp_id() < w0 ? 0 : 1;
-        // group 0 selects with the CTA's SelectSmem, group 1 with one in the (drained) TMA ring
-        SelectSmem& Sgr =
-            grp == 0 ? Sel : *reinterpret_cast<SelectSmem*>(reinterpret_cast<unsigned char*>(B.st_lt) + kOffRing);
-        const int gn = (grp == 0 ? w0 : nw - w0) * 32, gt = tid - (grp == 0 ? 0 : w0 * 32);
-        const int m = grp ? mR : mE, off = grp ? oR : 0;
-        unsigned long long* vl = B.st_lt + off;
-        unsigned int* vs = B.st_slot + off;
-        unsigned long long* tl = B.sd_lt + (grp ? kPreK + 2 : 0);  // selected, kPreK per group
-        unsigned int* ts = B.sd_slot + (grp ? kPreK + 2 : 0);
-        for (int j = gt; j < m; j += gn) {
-            vl[j] = __ldcg(P.pre_buf_lt + grp * P.pre_gcap + j);
-            vs[j] = __ldcg(P.pre_buf_slot + grp * P.pre_gcap + j);
+    // gather: E and R staged on chip, pending written out validated
+    unsigned long long* eL = B.st_lt;
+    unsigned int* eS = B.st_slot;
+    unsigned long long* rL = B.st_lt + kSvcStage;
+    unsigned int* rS = B.st_slot + kSvcStage;
+    for (int g = tid; g < M; g += T) {
+        int lo = 0, hi = ns;  // the CTA whose range holds g: off[c] <= g < off[c + 1]
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (off[mid] <= g) lo = mid;
+            else hi = mid;
         }
-        if (gt == 0) ng[grp] = 0;
-        group_sync(1 + grp, gn);
-        if (tid == 0) P.dbg[blockIdx.x * 16 + 7] = gtimer();
-        const unsigned long long v = m > kPreK ? group_kth(vl, m, kPreK, Sgr, gt, gn, 1 + grp) : kNoBound;
-        for (int j = gt; j < m; j += gn) {
-            const unsigned long long x = vl[j];
-            if (m <= kPreK || x <= v) {
-                const int p = atomicAdd(&ng[grp], 1);
-                tl[p] = x;
-                ts[p] = vs[j];
+        const size_t idx = ((size_t)par * P.raw_grid + lo) * kRawCap + (g - off[lo]);
+        const unsigned int l = P.raw_list[idx];
+        const unsigned long long x = P.raw_lt[idx];
+        const unsigned int sl = P.raw_slot[idx];
+        if (l < 2) {
+            const int p = atomicAdd(&cntL[l], 1);
+            if (p < kSvcStage) {
+                (l ? rL : eL)[p] = x;
+                (l ? rS : eS)[p] = sl;
+            } else {
+                okf = 0;
+            }
+        } else {
+            const int p = atomicAdd(&cntL[2], 1);
+            if (p < kPendCap) {
+                const size_t o = (size_t)2 * kPendCap + p;
+                P.pl_lt[o] = x;
+                P.pl_slot[o] = sl;
+                P.pl_agent[p] = P.raw_agent[idx];
+                P.pl_ok[o] = __ldcg(P.lt + sl) == x ? 1 : 0;
+            } else {
+                okf = 0;
             }
         }
-        group_sync(1 + grp, gn);
-        if (tid == 0) P.dbg[blockIdx.x * 16 + 8] = gtimer();
-        const int n = ng[grp];  // min(m, kPreK) (distinct ticks)
-        const size_t base = ((size_t)par * 3 + grp) * kPendCap;
-        if (gt == 0) Sgr.acc_or = kNoBound;  // (free after the select) rank kPreK / 2 - 1
-        group_sync(1 + grp, gn);
-        for (int j = gt; j < n; j += gn) {
-            const unsigned long long x = tl[j];
-            const int r = count_below(tl, n, x);
-            P.pl_lt[base + r] = x;
-            P.pl_slot[base + r] = ts[j];
-            if (r == 0) Sgr.hmax = x;
-            if (r == kPreK / 2 - 1) Sgr.acc_or = x;
-        }
-        group_sync(1 + grp, gn);
-        if (gt == 0) {
-            const unsigned long long Tl = m > kPreK ? v : h[grp];
-            P.pl_n[par * 3 + grp] = n;
-            P.pl_T[par * 3 + grp] = Tl;
-            P.pre_hint[grp] = n == 0 ? kNoBound
-                              : bad ? Tl
-                              : n == kPreK ? next_hint_mid(Sgr.acc_or, Tl)
-                                           : next_hint(Sgr.hmax, Tl);
-        }
-        __syncthreads();
-    } else {  // many candidates (a loose threshold): radix select per list
-        prescan_finalize(P, B, Sel, par, 0, hE);
-        prescan_finalize(P, B, Sel, par, 1, hR);
     }
+    __syncthreads();
+    if (tid == 0) P.dbg[blockIdx.x * 16 + 7] = gtimer();
+    const int mE = min(cntL[0], kSvcStage), mR = min(cntL[1], kSvcStage);
+    const bool bad = okf == 0;
+    // two warp groups (named barriers 1 and 2): group 0 finalizes E, group 1 R, at once
+    const int nw = (int)blockDim.x >> 5, w0 = (nw + 1) >> 1;
+    const int grp = warp_id() < w0 ? 0 : 1;
+    // group 0 selects with the CTA's SelectSmem, group 1 with one in the (idle) TMA ring
+    SelectSmem& Sgr =
+        grp == 0 ? Sel : *reinterpret_cast<SelectSmem*>(reinterpret_cast<unsigned char*>(B.st_lt) + kOffRing);
+    const int gn = (grp == 0 ? w0 : nw - w0) * 32, gt = tid - (grp == 0 ? 0 : w0 * 32);
+    const int m = grp ? mR : mE;
+    const unsigned long long* vl = grp ? rL : eL;
+    const unsigned int* vs = grp ? rS : eS;
+    unsigned long long* tl = B.sd_lt + (grp ? kPreK + 2 : 0);  // selected, kPreK per group
+    unsigned int* ts = B.sd_slot + (grp ? kPreK + 2 : 0);
+    if (gt == 0) ng[grp] = 0;
+    group_sync(1 + grp, gn);
+    const unsigned long long v = m > kPreK ? group_kth(vl, m, kPreK, Sgr, gt, gn, 1 + grp) : kNoBound;
+    for (int j = gt; j < m; j += gn) {
+        const unsigned long long x = vl[j];
+        if (m <= kPreK || x <= v) {
+            const int p = atomicAdd(&ng[grp], 1);
+            tl[p] = x;
+            ts[p] = vs[j];
+        }
+    }
+    group_sync(1 + grp, gn);
+    const int n = ng[grp];  // min(m, kPreK) (distinct ticks)
+    if (gt == 0) Sgr.acc_or = kNoBound;  // (free after the select) rank kPreK / 2 - 1
+    group_sync(1 + grp, gn);
+    const size_t base = (size_t)grp * kPendCap;
+    for (int j = gt; j < n; j += gn) {
+        const unsigned long long x = tl[j];
+        const unsigned int sl = ts[j];
+        const int r = count_below(tl, n, x);
+        P.pl_lt[base + r] = x;
+        P.pl_slot[base + r] = sl;
+        P.pl_ok[base + r] = __ldcg(P.lt + sl) == x ? 1 : 0;  // validation: last_touch unchanged
+        if (grp == 0 && r < kChunk + 2) P.pl_key[r] = __ldcg(P.key + sl);
+        if (r == 0) Sgr.hmax = x;
+        if (r == kPreK / 2 - 1) Sgr.acc_or = x;
+    }
+    group_sync(1 + grp, gn);
+    if (gt == 0) {
+        const unsigned long long Tl = m > kPreK ? v : hused[grp];
+        P.pl_n[grp] = n;
+        P.pl_T[grp] = Tl;
+        // (a seq mismatch: nothing was read; the old threshold stays)
+        if (produced)
+            P.pre_hint[par * 3 + grp] = n == 0 ? kNoBound
+                                        : bad ? Tl
+                                        : n == kPreK ? next_hint_mid(Sgr.acc_or, Tl)
+                                                     : next_hint(Sgr.hmax, Tl);
+    }
+    __syncthreads();
     if (tid == 0) {
-        P.pl_n[par * 3 + 2] = min(mP, kPendCap);
-        P.pl_T[par * 3 + 2] = hP;
+        P.pl_n[2] = min(cntL[2], kPendCap);
+        P.pl_T[2] = hused[0];  // pending shares E's acceptance threshold
+        P.pl_n[3] = bad ? 0 : 1;
         if (bad) atomicAdd(reinterpret_cast<unsigned long long*>(&C->pre_badcnt), 1ull);
-        C->pl_ok[par] = bad ? 0 : 1;
-        C->pre_cnt[par][0] = C->pre_cnt[par][1] = C->pre_cnt[par][2] = 0;
-        C->pre_bad[par] = 0;
-        C->pre_arrive[par] = 0u;  // every arrival happened before the wait above ended
-        // the consumer is the next admission: a kernel boundary (or the engine kernel's grid
-        // barrier) orders these stores before its reads
-        C->pl_seq[par] = a.seq;
+        __threadfence();
+        asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(&C->svc_l_seq), "l"(a.seq) : "memory");
+        P.dbg[blockIdx.x * 16 + 8] = gtimer();
     }
 }
 
 // Acceptance thresholds for the next prescan from a regular select's lists (CTA 0, thread 0):
 // the keep oldest of E and R extrapolated to ~2 kPreK ranks. Agent-carrying slots are kept whole.
-__device__ void hints_from_fin(const DevPool& P, int NL, int keep) {
+__device__ void hints_from_fin(const DevPool& P, int NL, int keep, int par) {
     const int E = P.e_max, Rl = NL - 1;
     const int lists[2] = {E, Rl};
     for (int q = 0; q < 2; ++q) {
@@ -1687,160 +1655,11 @@ __device__ void hints_from_fin(const DevPool& P, int NL, int keep) {
             const unsigned long long mult = (unsigned long long)((2 * kPreK + n - 1) / n);
             h = span > (kNoBound - v1) / (mult + 1) ? kNoBound : v1 + span * mult;
         }
-        P.pre_hint[q] = h;
+        P.pre_hint[par * 3 + q] = h;
+        P.pre_hint[(par ^ 1) * 3 + q] = h;  // (the next pipelined launch's prescan reads the other slot)
     }
-    P.pre_hint[2] = kNoBound;
-}
-
-// CTA 0, after phase 0: chunk 0's E and R lists (exact, sorted) and the other classes'
-// non-empty flags from the previous launch's prescan (parity par). False: unusable.
-__device__ bool consume_prescan(const DevPool& P, const AdmitArgs& a, const ScanBufs& B, ScanSmem& S, RedSmem& Red,
-                                int par) {
-    const int tid = threadIdx.x, T = blockDim.x;
-    const int NL = P.n_lists, E = P.e_max, Rl = NL - 1;
-    // U: the slots unpinned since the prescan may have read them (see above)
-    for (int j = tid; j < kXset; j += T) S.xset[j] = kNoSlot;
-    for (int x = tid; x < a.n_agents; x += T) B.cls[x] = __ldcg(P.cls + x);
-    if (tid < kMaxLists) S.lcnt[tid] = 0;
-    if (tid == 0) S.side_n = 0;
-    __syncthreads();
-    {
-        const int nu = unpin_total(a, true);
-        for (int i = tid; i < nu; i += T) {
-            const unsigned int us = unpin_at(a, i);
-            if (us != kNoSlot) xset_insert(S, us);
-        }
-    }
-    __syncthreads();
-    pstamp(P, 7);
-    const unsigned long long TE = P.pl_T[par * 3 + 0], TR = P.pl_T[par * 3 + 1], TP = P.pl_T[par * 3 + 2];
-    const unsigned long long TEs = min(TE, TP);  // agentless E members complete to TE, agent-carrying to TP
-    const int nE = P.pl_n[par * 3 + 0], nR = P.pl_n[par * 3 + 1], nP = P.pl_n[par * 3 + 2];
-    const size_t bE = ((size_t)par * 3 + 0) * kPendCap, bR = ((size_t)par * 3 + 1) * kPendCap,
-                 bP = ((size_t)par * 3 + 2) * kPendCap;
-    // staging view: [0, kPreK) E entries + valid flag, [kPreK, 2 kPreK) R entries + flag,
-    // extras (E members outside the agentless list) in the side buffers
-    unsigned long long* xl = B.sd_lt;
-    unsigned int* xs = B.sd_slot;
-    auto add_member = [&](unsigned long long x, unsigned int s, int c) {
-        if (c == E) {
-            if (x <= TEs) {
-                const int p = atomicAdd(&S.side_n, 1);
-                if (p < kSide) {
-                    xl[p] = x;
-                    xs[p] = s;
-                }
-            }
-        } else {
-            S.lcnt[c] = 1;
-        }
-    };
-    // one flat pass (independent loads): E entries, R entries, pending entries, U re-reads
-    const int nall = nE + nR + nP + kXset;
-    for (int q = tid; q < nall; q += T) {
-        if (q < nE) {
-            const unsigned long long x = P.pl_lt[bE + q];
-            const unsigned int s = P.pl_slot[bE + q];
-            B.st_lt[q] = x;
-            B.st_slot[q] = s;
-            B.st_list[q] = (__ldcg(P.lt + s) == x && x <= TEs && !xset_has(S, s)) ? 1 : 0;
-        } else if (q < nE + nR) {
-            const int j = q - nE;
-            const unsigned long long x = P.pl_lt[bR + j];
-            const unsigned int s = P.pl_slot[bR + j];
-            B.st_lt[kPreK + j] = x;
-            B.st_slot[kPreK + j] = s;
-            B.st_list[kPreK + j] = __ldcg(P.lt + s) == x ? 1 : 0;
-        } else if (q < nE + nR + nP) {  // agent-carrying unpinned: class from this launch's BFS
-            const int j = q - nE - nR;
-            const unsigned long long x = P.pl_lt[bP + j];
-            const unsigned int s = P.pl_slot[bP + j];
-            if (__ldcg(P.lt + s) != x || xset_has(S, s)) continue;
-            add_member(x, s, B.cls[P.pl_agent[(size_t)par * kPendCap + j]]);
-        } else {  // U: re-read
-            const unsigned int s = S.xset[q - nE - nR - nP];
-            if (s == kNoSlot) continue;
-            const unsigned long long x = __ldcg(P.lt + s);
-            if (x == kFreeTick || __ldcg(P.refs + s) != 0u) continue;
-            const unsigned int ag = __ldcg(P.agent + s);
-            add_member(x, s, ag == kNoAgent ? E : B.cls[ag]);
-        }
-    }
-    __syncthreads();
-    pstamp(P, 8);
-    if (TP < kNoBound && tid < E) S.lcnt[tid] = 1;  // some agent-carrying members unseen: assume present
-    const int nx = S.side_n;
-    // exclusive prefix of the valid flags of E and R (sorted lists keep their order)
-    int fe = 0, fr = 0;
-    {
-        const int q = tid < kPreK ? tid : 0;
-        const int ve = tid < nE ? B.st_list[q] : 0;
-        const int vr = tid < nR ? B.st_list[kPreK + q] : 0;
-        const long long both = ((long long)ve << 32) | vr;
-        // block-wide exclusive scan over 256 entries (kPreK <= blockDim)
-        long long incl = both;
-        for (int o = 1; o < 32; o <<= 1) {
-            const long long y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane_id() >= o) incl += y;
-        }
-        if (lane_id() == 31) Red.v[warp_id()] = incl;
-        __syncthreads();
-        long long off = 0;
-        for (int w = 0; w < warp_id(); ++w) off += Red.v[w];
-        const long long excl = off + incl - both;
-        fe = (int)(excl >> 32);
-        fr = (int)(excl & 0xffffffffll);
-        __syncthreads();
-        if (tid == (int)blockDim.x - 1) {
-            Red.u[0] = (unsigned long long)(off + incl);  // totals
-        }
-        __syncthreads();
-    }
-    const long long tot = (long long)Red.u[0];
-    const int totE = (int)(tot >> 32), totR = (int)(tot & 0xffffffffll);
-    const bool ok = nx <= kSide && (totR > 0 || TR >= kNoBound);
-    if (!ok) return false;
-    const int capE = kChunk + 1, capR = kChunk + 1;
-    // R: the valid entries in order
-    if (tid < nR && B.st_list[kPreK + tid] && fr < capR) {
-        P.fin_lt[(long long)Rl * (kChunk + 2) + fr] = B.st_lt[kPreK + tid];
-        P.fin_slot[(long long)Rl * (kChunk + 2) + fr] = B.st_slot[kPreK + tid];
-    }
-    // E: merge of the valid agentless entries (sorted) with the extras (unsorted, few)
-    if (tid < nE && B.st_list[tid]) {
-        const unsigned long long x = B.st_lt[tid];
-        const int r = fe + count_below(xl, nx, x);
-        if (r < capE) {
-            P.fin_lt[(long long)E * (kChunk + 2) + r] = x;
-            P.fin_slot[(long long)E * (kChunk + 2) + r] = B.st_slot[tid];
-        }
-    }
-    for (int i = tid; i < nx; i += T) {
-        const unsigned long long x = xl[i];
-        int r = count_below(xl, nx, x);
-        int lo2 = 0, hi2 = nE;  // valid agentless entries below x: binary search + prefix flag count
-        while (lo2 < hi2) {
-            const int mid = (lo2 + hi2) >> 1;
-            if (B.st_lt[mid] < x) lo2 = mid + 1;
-            else hi2 = mid;
-        }
-        int cnt = 0;
-        for (int k = 0; k < lo2; ++k) cnt += B.st_list[k];
-        r += cnt;
-        if (r < capE) {
-            P.fin_lt[(long long)E * (kChunk + 2) + r] = x;
-            P.fin_slot[(long long)E * (kChunk + 2) + r] = xs[i];
-        }
-    }
-    if (tid == 0) {
-        P.fin_n[E] = min(totE + nx, capE);
-        P.fin_n[Rl] = min(totR, capR);
-    }
-    for (int c = tid; c < NL; c += T)
-        if (c != E && c != Rl) P.gcount[c] = S.lcnt[c];
-    __threadfence_block();
-    __syncthreads();
-    return true;
+    P.pre_hint[par * 3 + 2] = kNoBound;
+    P.pre_hint[(par ^ 1) * 3 + 2] = kNoBound;
 }
 
 __device__ __forceinline__ bool tset_insert(unsigned int* t, unsigned int s) {
@@ -1864,16 +1683,49 @@ __device__ __forceinline__ bool tset_has(const unsigned int* t, unsigned int s) 
     return false;
 }
 
-// The consumer of a prescan when phase 0 did its loads (es->ok): the previous launch's lists,
-// validated against the pool as this launch found it, minus this launch's phase-0 changes
-// (touched prefix = tset, unpinned = U); writes chunk 0's E and R lists, E's keys and the other
-// classes' non-empty flags straight into the replay view. On-chip only. False: unusable.
-__device__ bool consume_early(const DevPool& P, const EarlySmem& es, ReplaySmem& R, const ScanBufs& B, ScanSmem& S,
-                              RedSmem& Red) {
+// The consumer of the previous launch's prescan (CTA 0, after phase 0): the list service's
+// output (service_lists: sorted, validated against the pool as this launch found it) minus this
+// launch's phase-0 changes (touched prefix = tset, unpinned = U, re-read in phase 0); writes
+// chunk 0's E and R lists, E's keys and the other classes' non-empty flags straight into the
+// replay view. False: unusable (the admission scans instead).
+__device__ bool consume_svc(const DevPool& P, const AdmitArgs& a, EarlySmem& es, ReplaySmem& R, const ScanBufs& B,
+                            ScanSmem& S, RedSmem& Red) {
+    Ctrl* C = P.ctrl;
     const int tid = threadIdx.x, T = blockDim.x;
     const int NL = P.n_lists, E = P.e_max, Rl = NL - 1;
+    if (tid == 0) {
+        unsigned long long spins = 0;
+        while (ld_acquire_u64(&C->svc_l_seq) != a.seq) {
+            if (++spins > 4096) __nanosleep(64);
+            if (spins > (1ull << 28)) __trap();
+        }
+        es.nE = __ldcg(P.pl_n + 0);
+        es.nR = __ldcg(P.pl_n + 1);
+        es.nP = __ldcg(P.pl_n + 2);
+        es.valid = __ldcg(P.pl_n + 3);
+        es.TE = __ldcg(P.pl_T + 0);
+        es.TR = __ldcg(P.pl_T + 1);
+        es.TP = __ldcg(P.pl_T + 2);
+    }
+    __syncthreads();
+    pstamp(P, 7);
+    if (!es.valid) return false;
     const unsigned long long TEs = min(es.TE, es.TP), TR = es.TR, TP = es.TP;
     const int nE = es.nE, nR = es.nR, nP = es.nP;
+    for (int q = tid; q < nE + nR; q += T) {  // one round of (L2-resident) loads
+        if (q < nE) {
+            es.E_lt[q] = __ldcg(P.pl_lt + q);
+            es.E_slot[q] = __ldcg(P.pl_slot + q);
+            es.E_ok[q] = __ldcg(P.pl_ok + q);
+            if (q < kChunk + 2) es.E_key[q] = __ldcg(P.pl_key + q);
+        } else {
+            const int j = q - nE;
+            es.R_lt[j] = __ldcg(P.pl_lt + kPendCap + j);
+            es.R_slot[j] = __ldcg(P.pl_slot + kPendCap + j);
+            es.R_ok[j] = __ldcg(P.pl_ok + kPendCap + j);
+        }
+    }
+    __syncthreads();
     unsigned long long* xl = B.sd_lt;
     unsigned int* xs = B.sd_slot;
     unsigned char* ef = B.st_list;  // E flags [0, kPreK), R flags [kPreK, 2 kPreK)
@@ -1900,10 +1752,12 @@ __device__ bool consume_early(const DevPool& P, const EarlySmem& es, ReplaySmem&
         } else if (q < nE + nR) {
             const int j = q - nE;
             ef[kPreK + j] = (es.R_ok[j] && !tset_has(es.tset, es.R_slot[j])) ? 1 : 0;
-        } else if (q < nE + nR + nP) {
+        } else if (q < nE + nR + nP) {  // agent-carrying unpinned: class from this launch's BFS
             const int j = q - nE - nR;
-            const unsigned int s = es.P_slot[j];
-            if (es.P_ok[j] && !xset_has(S, s) && !tset_has(es.tset, s)) add_member(es.P_lt[j], s, B.cls[es.P_agent[j]]);
+            const size_t o = (size_t)2 * kPendCap + j;
+            const unsigned int s = __ldcg(P.pl_slot + o);
+            if (__ldcg(P.pl_ok + o) && !xset_has(S, s) && !tset_has(es.tset, s))
+                add_member(__ldcg(P.pl_lt + o), s, B.cls[__ldcg(P.pl_agent + j)]);
         } else {
             const int j = q - nE - nR - nP;
             const unsigned int s = S.xset[j];
@@ -2106,6 +1960,25 @@ __device__ void load_lists(const DevPool& P, ReplaySmem& R, int NL, bool scanned
             R.L_lt[l][j] = P.fin_lt[q];
             R.L_slot[l][j] = P.fin_slot[q];
         }
+    }
+    __syncthreads();
+}
+
+// CTA 0, all threads: the queue counters are CTA 0's again. In a pipelined launch CTA kSvcQ
+// applies the previous admission's queue (service_queue); wait for it, then start the new queue.
+__device__ void queue_ready(const DevPool& P, const AdmitArgs& a, AdmSmem& A) {
+    if (!A.q_deleg) return;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        Ctrl* C = P.ctrl;
+        unsigned long long spins = 0;
+        while (ld_acquire_u64(&C->svc_q_seq) != a.seq) {
+            if (++spins > 4096) __nanosleep(64);
+            if (spins > (1ull << 28)) __trap();
+        }
+        C->tq_erase = 0;
+        C->tq_insert = 0;
+        A.q_deleg = 0;
     }
     __syncthreads();
 }
@@ -2413,7 +2286,8 @@ __device__ void replay_apply(const DevPool& P, const AdmitArgs& a, ReplaySmem& R
     stamp(A, 7);
     const bool err = A.error != 0;
     const int nv = R.n_vict;
-    // ---- apply: victims first (erase key, free slot), then inserts and touches
+    // ---- apply: victims first (queue the erase, free slot), then inserts and touches
+    queue_ready(P, a, A);
     const unsigned long long ev0 = C->n_ev;
     // victim keys first (a reused victim slot is rewritten below)
     for (int k = tid; k < nv; k += T) {
@@ -2427,14 +2301,15 @@ __device__ void replay_apply(const DevPool& P, const AdmitArgs& a, ReplaySmem& R
     }
     __syncthreads();
     dstamp(P, 4);
-    // Inserts are queued (the next launch's phase 0, or CTA 1 at the end of a pipelined launch,
-    // applies them); the victims' erases run here, one chain per thread: nothing reads the table
-    // for the rest of this admission, and a block this admission inserted is pinned, so it is
-    // never among its own victims (an erase always precedes any re-insert of the same key).
+    // The table updates are queued, erases and inserts, and applied by the next launch (its
+    // CTA kSvcQ concurrently with its probe, or its phase 0): nothing reads the table for the rest
+    // of this admission (later chunks re-resolve through the victim set), and a block this
+    // admission inserted is pinned, so it is never among its own victims (the queue applies every
+    // erase before every insert).
     const int q_e = C->tq_erase, q_i = C->tq_insert;
     for (int k = tid; k < nv; k += T) {
         const unsigned long long kk = R.vkey[k];
-        table_erase(P, kk);
+        P.tq_key[q_e + k] = kk;
         P.evlog[(ev0 + k) % (unsigned long long)P.evlog_cap] = kk;  // ring; the host drains it
         if (a.vict_host && A.n_ev_adm + k < a.vict_cap) a.vict_host[A.n_ev_adm + k] = kk;  // mapped host memory
         if (k >= R.n_reused) {  // victims[0, n_reused) are overwritten by new blocks below
@@ -2496,8 +2371,7 @@ __device__ void replay_apply(const DevPool& P, const AdmitArgs& a, ReplaySmem& R
         C->pinned = A.pinned;
         C->free_top = top;
         C->n_ev = ev0 + nv;
-        C->tq_erase = q_e;
-        C->tombstones += nv;  // (an erase leaves a tombstone; an insert may reuse it later)
+        C->tq_erase = q_e + nv;
         C->tq_insert = q_i + R.n_ins;
         A.n_ev_adm += nv;
     }
@@ -2604,7 +2478,10 @@ __device__ void write_status(const DevPool& P, const AdmitArgs& a, const AdmSmem
     st->warm_issued = A.warm_issued;
     st->needed = A.needed;
     st->scans = A.scans;
-    st->tombstones = A.tomb_snap ? A.tomb_hi : C->tombstones;
+    // after queue_ready: nothing else changes either until the next launch applies the queue;
+    // the queued erases leave tombstones then (an insert may reuse some): an upper bound, so the
+    // host's rebuild decision is deterministic and conservative
+    st->tombstones = C->tombstones + (long long)C->tq_erase;
     for (int k = 0; k < kPhases; ++k) st->phase_ns[k] = A.ph[k];
     st->n_pend = C->n_pend;
     for (int k = 0; k < C->n_pend && k < kMaxPending; ++k) {
@@ -2625,7 +2502,7 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
     ReplaySmem& Rp = *reinterpret_cast<ReplaySmem*>(dsm + kOffRing);
     if (tid == 0) P.dbg[blockIdx.x * 16 + 9] = gtimer();  // kernel entry (instrumentation)
     const int par_prev = (int)((a.seq - 1ull) & 1ull), par_next = (int)(a.seq & 1ull);
-    const bool pre_run = (a.flags & kPrescan) && gridDim.x >= 2;
+    const bool pre_run = (a.flags & kPrescan) && gridDim.x > kStream0;
     // The host asks for the previous prescan's lists (kUsePrescan): the prescan CTAs start the
     // next stream at once; CTA 0 checks the lists are there and usable (else it scans as before).
     const bool pre_avail = pre_run && (a.flags & kUsePrescan);
@@ -2644,7 +2521,7 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
             A.needed = 0;
             A.warm_issued = -1;
             A.scans = 0;
-            A.tomb_snap = 0;
+            A.q_deleg = 0;
             A.first_touch = ~0ull;
             A.tick = a.tick_base;
             for (int k = 0; k < kPhases; ++k) A.ph[k] = 0;
@@ -2661,17 +2538,9 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
                 A.pf_on = (a.flags & kDispatch) && P.policy != 0 && a.next >= 0 && C->cur_agent != a.next &&
                           wsz <= 2 * (long long)blockDim.x && wsz <= kBfsPre;
             }
-            es.valid = pre_avail && *(volatile unsigned long long*)&C->pl_seq[par_prev] == a.seq - 1ull &&
-                       *(volatile int*)&C->pl_ok[par_prev] != 0;
-            if (es.valid) {
-                es.nE = P.pl_n[par_prev * 3 + 0];
-                es.nR = P.pl_n[par_prev * 3 + 1];
-                es.nP = P.pl_n[par_prev * 3 + 2];
-                es.TE = P.pl_T[par_prev * 3 + 0];
-                es.TR = P.pl_T[par_prev * 3 + 1];
-                es.TP = P.pl_T[par_prev * 3 + 2];
-                es.ok = es.nP <= kEarlyP && unpin_total(a, true) <= kXsetMax ? 1 : 0;
-            }
+            // a pipelined launch: the list service validates the previous prescan concurrently;
+            // phase 0 tracks this launch's own changes (U, touched) for its consumer
+            es.ok = pre_avail && unpin_total(a, true) <= kXsetMax ? 1 : 0;
             if (a.flags & kPollReset) {
                 C->step_warmups = 0;
                 C->n_pend = 0;
@@ -2682,6 +2551,9 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
         const int n = a.n;
         long long miss_min = n, need = 0;
         const int ne = C->tq_erase, ni = C->tq_insert;
+        // a pipelined launch: CTA kSvcQ applies the queued table updates (service_queue)
+        const bool deleg = pre_avail;
+        if (tid == 0) A.q_deleg = deleg ? 1 : 0;
         // BFS inputs of observe(AgentDispatch), issued now so their round trips overlap the two
         // table rounds: the window pairs (here), their counts and row totals (round 2)
         const long long W_ = P.window, pf_head = A.pf_head, pf_size = A.pf_size;
@@ -2715,7 +2587,8 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
             // the probe resolves the queued keys from an on-chip overlay (insert wins: a key erased
             // and re-admitted is re-inserted), and a table operation on one key never misleads a
             // find of another (finds skip claimed and erased entries, and an erased entry's key
-            // is cleared first). Erase+insert of one key run in order on one thread.
+            // is cleared first). In a pipelined launch CTA kSvcQ applies them (service_queue);
+            // otherwise this CTA does, erase+insert of one key in order on one thread.
             unsigned long long* ovk = reinterpret_cast<unsigned long long*>(dsm + kOffRing);
             unsigned int* ovs = reinterpret_cast<unsigned int*>(dsm + kOffRing + 8 * kOv);
             for (int j = tid; j < kOv; j += T) ovs[j] = kSlotEmpty;
@@ -2728,19 +2601,16 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
             __syncthreads();
             // one round: the overlay of the queued keys, the deferred EngineSim::unpin calls of
             // completed requests (engine.cpp:170-180) and, feeding a prescan consumer, the set U
-            // of unpinned slots and the early validation of the previous launch's prescan lists
+            // of unpinned slots (this launch's and the previous launch's)
             long long dec = 0;
             const int nu = unpin_total(a, false);
             const int nuv = early ? unpin_total(a, true) : nu;
-            const int nE = early ? es.nE : 0, nR = early ? es.nR : 0, nP = early ? es.nP : 0;
-            const size_t bE = ((size_t)par_prev * 3 + 0) * kPendCap, bR = ((size_t)par_prev * 3 + 1) * kPendCap,
-                         bP = ((size_t)par_prev * 3 + 2) * kPendCap;
-            for (int q = tid; q < ne + ni + nuv + nE + nR + nP; q += T) {
+            for (int q = tid; q < ne + ni + nuv; q += T) {
                 if (q < ne) {
                     ov_put(ovk, ovs, P.tq_key[q], kOvErase);
                 } else if (q < ne + ni) {
                     ov_put(ovk, ovs, P.tq_key[P.p_cap + (q - ne)], P.tq_slot[q - ne]);
-                } else if (q < ne + ni + nuv) {
+                } else {
                     const int i = q - ne - ni;
                     const unsigned int us = unpin_at(a, i);
                     if (us == kNoSlot) continue;
@@ -2750,29 +2620,6 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
                         if (P.dbg_unpin) P.dbg_unpin[us] = (a.seq << 8) | 1u;
                     }
                     if (early) xset_insert(S, us);
-                } else if (q < ne + ni + nuv + nE) {
-                    const int j = q - ne - ni - nuv;
-                    const unsigned long long x = P.pl_lt[bE + j];
-                    const unsigned int sl = P.pl_slot[bE + j];
-                    es.E_lt[j] = x;
-                    es.E_slot[j] = sl;
-                    es.E_ok[j] = __ldcg(P.lt + sl) == x ? 1 : 0;
-                    es.E_key[j] = j < kChunk + 2 ? __ldcg(P.key + sl) : 0ull;
-                } else if (q < ne + ni + nuv + nE + nR) {
-                    const int j = q - ne - ni - nuv - nE;
-                    const unsigned long long x = P.pl_lt[bR + j];
-                    const unsigned int sl = P.pl_slot[bR + j];
-                    es.R_lt[j] = x;
-                    es.R_slot[j] = sl;
-                    es.R_ok[j] = __ldcg(P.lt + sl) == x ? 1 : 0;
-                } else {
-                    const int j = q - ne - ni - nuv - nE - nR;
-                    const unsigned long long x = P.pl_lt[bP + j];
-                    const unsigned int sl = P.pl_slot[bP + j];
-                    es.P_lt[j] = x;
-                    es.P_slot[j] = sl;
-                    es.P_agent[j] = P.pl_agent[(size_t)par_prev * kPendCap + j];
-                    es.P_ok[j] = __ldcg(P.lt + sl) == x ? 1 : 0;
                 }
             }
             dec = block_sum(dec, Red);  // (its barriers also publish the overlay)
@@ -2781,17 +2628,18 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
             pf_issue2();
             long long reused = 0;
             const int nxs = early ? kXset : 0;
-            for (int q = tid; q < ne + ni + n + nxs; q += T) {
-                if (q < ne) {
+            const int nq = deleg ? 0 : ne + ni;  // queued table updates this CTA applies
+            for (int q = tid; q < nq + n + nxs; q += T) {
+                if (q < nq && q < ne) {
                     const unsigned long long key = P.tq_key[q];
                     if (ov_get(ovk, ovs, key) == kOvErase) table_erase(P, key);  // else its insert erases
-                } else if (q < ne + ni) {
+                } else if (q < nq) {
                     const int k = q - ne;
                     const unsigned long long key = P.tq_key[P.p_cap + k];
                     if (ov_both(ov_get(ovk, ovs, key))) table_erase(P, key);
                     reused += table_insert(P, key, P.tq_slot[k]);
-                } else if (q < ne + ni + n) {
-                    const int i = q - ne - ni;
+                } else if (q < nq + n) {
+                    const int i = q - nq;
                     const unsigned long long key = a.keys[i];
                     const unsigned int ov = ov_get(ovk, ovs, key);
                     const unsigned int s = ov == kSlotEmpty ? table_find(P, key) : ov == kOvErase ? kNoSlot : (ov & kOvSlot);
@@ -2801,7 +2649,7 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
                     if (s == kNoSlot && i < miss_min) miss_min = i;
                     if (s == kNoSlot || r0 == 0u) ++need;
                 } else {  // U re-read, after every unpin of this launch
-                    const int j = q - ne - ni - n;
+                    const int j = q - nq - n;
                     const unsigned int us = S.xset[j];
                     if (us == kNoSlot) continue;
                     const unsigned long long x = __ldcg(P.lt + us);
@@ -2811,15 +2659,18 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
                 }
             }
             reused = block_sum(reused, Red);
-            if (tid == 0) {
+            if (tid == 0 && !deleg) {
                 C->tombstones += (long long)ne - reused;
                 C->tq_erase = 0;
                 C->tq_insert = 0;
             }
             pstamp(P, 2);
-        } else {
-            if (tid == 0) es.ok = 0;  // (the late prescan consumer re-reads instead)
-            apply_table_queue(P, Red);  // the previous admission's erases / inserts
+        } else {  // too many queued keys for the overlay: the probe waits for the table
+            if (tid == 0) es.ok = 0;  // (no consumer: the admission scans)
+            if (deleg)
+                queue_ready(P, a, A);
+            else
+                apply_table_queue(P, Red);  // the previous admission's erases / inserts
             pstamp(P, 1);
             pf_issue2();
             // deferred EngineSim::unpin calls of completed requests (engine.cpp:170-180), in order
@@ -2920,16 +2771,19 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
     }
     __syncthreads();
 
-    // ---- prescan: CTAs 1.. stream the pool for the NEXT admission while CTA 0 serves this one
-    // from the lists the previous launch's prescan produced (validated, see consume_prescan)
+    // ---- pipelined launch: CTAs kStream0.. stream the pool for the NEXT admission while CTA 0
+    // serves this one from the previous launch's prescan, which CTA kSvcL finalizes and validates
+    // meanwhile (service_lists); CTA kSvcQ applies the previous admission's table updates
     bool run_loop = true;
     bool pending_rescan = false;  // CTA 0: the last pass must be redone (safe, no hints)
     if (pre_avail) {
         if (blockIdx.x != 0) {
-            const unsigned long long hE = __ldcg(P.pre_hint + 0), hR = __ldcg(P.pre_hint + 1), hP = hE;
-            prescan_pass(P, B, S, dsm, par_next, P.stream_generic != 0);
-            if (tid == 0) P.dbg[blockIdx.x * 16 + 2] = gtimer();
-            prescan_finish(P, a, B, Sel, par_next, hE, hR, hP);
+            if (blockIdx.x == kSvcQ)
+                service_queue(P, a, Red);
+            else if (blockIdx.x == kSvcL)
+                service_lists(P, a, B, Sel, Red, dsm, par_prev);
+            else
+                prescan_pass(P, B, S, dsm, par_next, P.stream_generic != 0, a.seq);
             if (tid == 0) {
                 P.dbg[blockIdx.x * 16 + 4] = gtimer();
                 unsigned long long spins = 0;
@@ -2941,16 +2795,7 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
             }
             __syncthreads();
             run_loop = *(volatile int*)&C->verdict == 2;
-            if (!run_loop) {
-                // This admission's table updates are queued (CTA 0's apply precedes the verdict) and
-                // CTA 0 no longer reads the table: the prescan CTAs apply them now, off the next
-                // admission's phase 0 (which then finds an empty queue)
-                if (!P.stream_generic && blockIdx.x == 1) {
-                    apply_table_queue(P, Red);
-                    if (tid == 0) P.dbg[blockIdx.x * 16 + 11] = gtimer();  // instrumentation
-                }
-                return;
-            }
+            if (!run_loop) return;
         } else {
             if (tid == 0) {  // this launch's scoring pass is the prescan
                 A.scans += 1;
@@ -2965,10 +2810,7 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
                 stamp(A, 1);
                 pstamp(P, 6);
                 const bool need0 = C->resident + Rp.absent > P.cap;
-                const bool ok = !need0 ? true
-                                : !es.valid ? false
-                                : es.ok ? consume_early(P, es, Rp, B, S, Red)
-                                        : consume_prescan(P, a, B, S, Red, par_prev);
+                const bool ok = !need0 ? true : es.ok ? consume_svc(P, a, es, Rp, B, S, Red) : false;
                 if (ok && need0 && es.ok && P.dbg_check) debug_check_e(P, es, Rp, B, S, a);
                 stamp(A, 3);
                 pstamp(P, 9);
@@ -2988,8 +2830,6 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
             }
             if (tid == 0) {
                 C->verdict = need_loop ? 2 : 1;
-                A.tomb_hi = C->tombstones + (long long)C->tq_erase;  // (before CTA 1 may touch either)
-                A.tomb_snap = need_loop ? 0 : 1;
                 __threadfence();
                 asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(&C->verdict_seq), "l"(a.seq) : "memory");
             }
@@ -3098,7 +2938,7 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
             if (stop) {
                 if (tid == 0) {
                     C->done = 1;
-                    if (pre_run && !pre_avail) hints_from_fin(P, NL, C->keep);  // for the prescan below
+                    if (pre_run && !pre_avail) hints_from_fin(P, NL, C->keep, par_next);  // for the prescan below
                 }
             } else if (pending_rescan) {
                 // a hint was too tight (or the fast pass overflowed): same chunk, safe pass
@@ -3196,11 +3036,9 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
         }
     }
 
-    // ---- no usable prescan came in: CTAs 1.. now prescan for the next admission
+    // ---- no usable prescan came in: CTAs kStream0.. now prescan for the next admission
     if (pre_run && !pre_avail && blockIdx.x != 0) {
-        const unsigned long long hE = __ldcg(P.pre_hint + 0), hR = __ldcg(P.pre_hint + 1), hP = hE;
-        prescan_pass(P, B, S, dsm, par_next, true);
-        prescan_finish(P, a, B, Sel, par_next, hE, hR, hP);
+        if (blockIdx.x >= kStream0) prescan_pass(P, B, S, dsm, par_next, true, a.seq);
         return;
     }
     if (pre_run && !pre_avail && blockIdx.x == 0 && tid == 0) {
@@ -3227,6 +3065,7 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
             if (tid == 0) C->pinned -= dec;
         }
         __syncthreads();
+        queue_ready(P, a, A);  // (an admission that applied nothing: the counters are reset here)
         stamp(A, 5);
         pstamp(P, 11);
         if (tid == 0 && a.status) {

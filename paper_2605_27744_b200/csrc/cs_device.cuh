@@ -83,12 +83,9 @@ struct Ctrl {
     // prescan: the next admission's scoring pass, run by CTAs 1.. of this launch while CTA 0
     // serves this admission; double-buffered by launch-sequence parity
     unsigned int pbar_count, pbar_gen;  // barrier of the prescan CTAs
-    int pre_cnt[2][3];                  // raw candidates written per list (E, R, pending)
-    int pre_bad[2];                     // staging / buffer overflow: the prescan is unusable
-    unsigned int pre_fin[2];            // prescan lists finalized
-    unsigned int pre_arrive[2];         // prescan CTAs whose candidates are written
-    unsigned long long pl_seq[2];       // AdmitArgs::seq of the launch that produced the lists
-    int pl_ok[2];
+    // service CTAs of a pipelined launch -> CTA 0 (AdmitArgs::seq, release/acquire):
+    unsigned long long svc_q_seq;       // CTA kSvcQ applied the previous admission's table queue
+    unsigned long long svc_l_seq;       // CTA kSvcL published the validated prescan lists
     unsigned long long verdict_seq;     // CTA 0 -> prescan CTAs: this launch's verdict is out
     int verdict;                        // 1: done, 2: everyone joins the command loop
     long long pre_used, pre_fallbacks, pre_badcnt;  // instrumentation
@@ -98,6 +95,17 @@ struct Ctrl {
 // agent-carrying unpinned slots (classified by the consumer, after its BFS) are kept whole
 constexpr int kPreK = 192;  // >= kChunk + 1 list entries plus the front the previous admission evicts
 constexpr int kPendCap = 4096;
+// Roles in a pipelined launch (admit_kernel): CTA 0 serves this admission; CTA kSvcQ applies the
+// previous admission's queued block-table updates; CTA kSvcL finalizes and validates the previous
+// launch's prescan for CTA 0; CTAs kStream0.. stream the pool for the next admission.
+constexpr int kSvcQ = 1, kSvcL = 2, kStream0 = 3;
+constexpr int kRawCap = 6144;  // raw prescan candidates per streaming CTA (its staging capacity)
+// header of one streaming CTA's raw prescan output
+struct RawHdr {
+    unsigned long long seq;  // AdmitArgs::seq of the launch that wrote it
+    int n;                   // staged candidates (every list, staging order)
+    int bad;                 // staging overflowed: the prescan is unusable
+};
 
 // ---------------------------------------------------------------- hash-sharded pool
 // A pool of budget N split over G GPUs: a block lives on shard owner(key) = (key >> 40) % G.
@@ -224,18 +232,25 @@ struct DevPool {
 
     Ctrl* ctrl;
 
-    // prescan output [parity][list E, R, pending][kPendCap] (E and R use the first kPreK),
-    // its completeness thresholds [parity][3], the raw per-list candidates [3][pre_gcap] and
-    // the acceptance thresholds of the next prescan [3]
+    // raw prescan output, per launch parity and streaming CTA: the CTA's staged candidates in
+    // staging order ([2][raw_grid][kRawCap] lt / slot / list id / agent) and its header
+    unsigned long long* raw_lt;
+    unsigned int* raw_slot;
+    unsigned char* raw_list;
+    unsigned int* raw_agent;
+    RawHdr* raw_hdr;  // [2][raw_grid]
+    int raw_grid;
+    // the list service's output for this launch's CTA 0: [list E, R, pending][kPendCap] (E and
+    // R sorted, the first kPreK), validity against the pool at launch start, E keys, counts
+    // pl_n[0..2] + usable flag pl_n[3], completeness thresholds pl_T[0..2]
     unsigned long long* pl_lt;
     unsigned int* pl_slot;
     unsigned int* pl_agent;
+    unsigned char* pl_ok;
+    unsigned long long* pl_key;
     int* pl_n;
     unsigned long long* pl_T;
-    unsigned long long* pre_buf_lt;
-    unsigned int* pre_buf_slot;
-    long long pre_gcap;
-    unsigned long long* pre_hint;
+    unsigned long long* pre_hint;  // [parity][3]: acceptance thresholds of the prescan of a launch of that parity
     int dbg_check;  // debug: brute-force check of the prescan consumer's list E (small pools)
     int stream_generic;  // stream the pool with L2 loads instead of TMA (the persistent engine kernel)
     unsigned long long* dbg_unpin;  // debug: per slot (admission seq << 8 | source) of its last unpin

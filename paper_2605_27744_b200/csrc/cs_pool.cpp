@@ -163,17 +163,27 @@ void cs_pool::create(const cs_pool_cfg& c, long long shard_slots, cs_comm* cm) {
         p.dbg_unpin = dmalloc<unsigned long long>(p.cap_scan, "dbg_unpin");
         ck(cudaMemset(p.dbg_unpin, 0, 8 * p.cap_scan), "memset");
     }
-    p.pl_lt = dmalloc<unsigned long long>((size_t)2 * 3 * csb::kPendCap, "pl_lt");
-    p.pl_slot = dmalloc<unsigned int>((size_t)2 * 3 * csb::kPendCap, "pl_slot");
-    p.pl_agent = dmalloc<unsigned int>((size_t)2 * csb::kPendCap, "pl_agent");
-    p.pl_n = dmalloc<int>(6, "pl_n");
-    p.pl_T = dmalloc<unsigned long long>(6, "pl_T");
-    p.pre_gcap = (long long)lc.grid * 6144;  // every CTA's staging pool
-    p.pre_buf_lt = dmalloc<unsigned long long>((size_t)2 * p.pre_gcap, "pre_buf_lt");
-    p.pre_buf_slot = dmalloc<unsigned int>((size_t)2 * p.pre_gcap, "pre_buf_slot");
-    p.pre_hint = dmalloc<unsigned long long>(3, "pre_hint");
+    p.raw_grid = lc.grid;
     {
-        const unsigned long long h[3] = {csb::kNoBound, csb::kNoBound, csb::kNoBound};
+        const size_t nraw = (size_t)2 * lc.grid * csb::kRawCap;
+        p.raw_lt = dmalloc<unsigned long long>(nraw, "raw_lt");
+        p.raw_slot = dmalloc<unsigned int>(nraw, "raw_slot");
+        p.raw_list = dmalloc<unsigned char>(nraw, "raw_list");
+        p.raw_agent = dmalloc<unsigned int>(nraw, "raw_agent");
+        p.raw_hdr = dmalloc<csb::RawHdr>((size_t)2 * lc.grid, "raw_hdr");
+        ck(cudaMemset(p.raw_hdr, 0, sizeof(csb::RawHdr) * 2 * lc.grid), "memset");  // seq 0: nothing written
+    }
+    p.pl_lt = dmalloc<unsigned long long>((size_t)3 * csb::kPendCap, "pl_lt");
+    p.pl_slot = dmalloc<unsigned int>((size_t)3 * csb::kPendCap, "pl_slot");
+    p.pl_agent = dmalloc<unsigned int>((size_t)csb::kPendCap, "pl_agent");
+    p.pl_ok = dmalloc<unsigned char>((size_t)3 * csb::kPendCap, "pl_ok");
+    p.pl_key = dmalloc<unsigned long long>((size_t)csb::kPreK, "pl_key");
+    p.pl_n = dmalloc<int>(4, "pl_n");
+    p.pl_T = dmalloc<unsigned long long>(3, "pl_T");
+    p.pre_hint = dmalloc<unsigned long long>(6, "pre_hint");
+    {
+        const unsigned long long h[6] = {csb::kNoBound, csb::kNoBound, csb::kNoBound,
+                                         csb::kNoBound, csb::kNoBound, csb::kNoBound};
         ck(cudaMemcpy(p.pre_hint, h, sizeof(h), cudaMemcpyHostToDevice), "pre_hint");
     }
     ck(cudaMemsetAsync(p.dbg, 0, sizeof(unsigned long long) * (lc.grid * 16 + 192), stream), "memset");
@@ -209,7 +219,8 @@ void cs_pool::destroy() {
                     p.win_a, p.win_b, p.hop, p.cls, p.agent_ids, p.ctrl, p.gbound, p.gcount, p.fin_lt, p.fin_slot,
                     p.fin_n, p.p_slot, p.p_refs0, p.gbuf_lt, p.gbuf_slot, p.ghint, p.gmaxk, p.grej, p.dbg, p.gsmall, p.gmin, p.tq_key, p.tq_slot,
                     p.sh_send1, p.sh_recv1, p.sh_send2, p.sh_recv2, p.sh_state, p.sh_gslot, p.sh_grefs0,
-                    p.pl_lt, p.pl_slot, p.pl_agent, p.pl_n, p.pl_T, p.pre_buf_lt, p.pre_buf_slot, p.pre_hint,
+                    p.pl_lt, p.pl_slot, p.pl_agent, p.pl_ok, p.pl_key, p.pl_n, p.pl_T, p.pre_hint,
+                    p.raw_lt, p.raw_slot, p.raw_list, p.raw_agent, p.raw_hdr,
                     p.bel_nu, p.bel_kid, p.bel_kid_slot, (void*)p.bel_ref, (void*)p.bel_ref_off, (void*)p.bel_depth,
                     (void*)p.bel_kid_of, p.bel_hi, p.bel_lo, p.bel_cand, p.bel_ctl};
     for (void* q : ptrs)
@@ -475,7 +486,7 @@ const csb::AdmitStatus& cs_pool::admit(const csb::AdmitArgs& in, int n_for_grid)
     unpin_q_slots = 0;
     a.seq = ++seq;
     if (speculate && grid > 1 && xn <= csb::kXsetMax) a.flags |= csb::kSpeculate;
-    if (prescan && grid > 1) a.flags |= csb::kPrescan;
+    if (prescan && grid > csb::kStream0) a.flags |= csb::kPrescan;
     a.n_prev_ranges = 0;
     if ((a.flags & csb::kPrescan) && pre_ok && cur_unpins + prev_slots <= csb::kXsetMax &&
         (int)prev_ranges.size() <= csb::kMaxUnpinRanges + 1) {

@@ -12,14 +12,14 @@ from paper_2605_27744_b200 import workloads as W  # noqa: E402
 from paper_2605_27744_b200._lib import lib  # noqa: E402
 
 NAMES = {0: "p0 start", 1: "table queue", 2: "unpins", 3: "probe", 13: "record", 14: "bfs", 4: "observe",
-         5: "phase0 end", 6: "prologue", 7: "U set", 8: "validate", 9: "consume end", 10: "replay_apply",
+         5: "phase0 end", 6: "prologue", 7: "lists seen", 8: "validate", 9: "consume end", 10: "replay_apply",
          11: "epilogue", 12: "status"}
 pool = 16 << 20
 spec, seed = bench.rank_workload(40000, pool, 0)
 eng = bench.build_engine(W, spec, pool, 0, False, seed)
 eng.run_timed(int(sys.argv[1]) if len(sys.argv) > 1 else 100)
 rows = []
-fin = []
+svc = []
 ends = []
 for it in range(40):
     eng.run_timed(1)
@@ -33,16 +33,18 @@ for it in range(40):
     st = d[16 * g:16 * g + 16]
     rows.append((st - ent) / 1e3)
     per = d[:16 * g].reshape(g, 16)
-    fin.append([(per[1, c] - ent) / 1e3 for c in (6, 7, 8, 4, 11)])
-    ends.append([((per[1:, c] - ent) / 1e3).max() for c in (0, 1, 2, 3, 4, 5)] + [((per[1:3, 4] - ent) / 1e3).max()])
+    # service CTAs: 1 = table queue (start, done), 2 = list service (start, gathered, published)
+    svc.append([(per[1, 6] - ent) / 1e3, (per[1, 7] - ent) / 1e3, (per[2, 6] - ent) / 1e3, (per[2, 7] - ent) / 1e3,
+                (per[2, 8] - ent) / 1e3])
+    # streaming CTAs 3..: start, stream end, writeout end (= verdict wait start), verdict seen
+    ends.append([((per[3:, c] - ent) / 1e3).max() for c in (0, 1, 4, 5)])
 r = np.median(np.array(rows), axis=0)
-for k in [0, 1, 2, 3, 13, 14, 4, 5, 6, 7, 8, 9, 10, 11, 12]:
+for k in [0, 1, 2, 3, 13, 14, 4, 5, 6, 7, 9, 10, 11, 12]:
     print(f"{NAMES[k]:>14}: {r[k]:8.2f} us")
 e = np.median(np.array(ends), axis=0)
-print("prescan CTAs (max over CTAs): start %.2f stream end %.2f writeout %.2f barrier %.2f finish %.2f (finalizers %.2f) verdict %.2f us"
-      % (e[0], e[1], e[2], e[3], e[4], e[6], e[5]))
+print("streaming CTAs (max over CTAs): start %.2f stream end %.2f writeout %.2f verdict seen %.2f us" % tuple(e))
+sv = np.median(np.array(svc), axis=0)
+print("service CTA 1 (table queue): start %.2f done %.2f us; CTA 2 (lists): start %.2f gathered %.2f published %.2f us"
+      % tuple(sv))
 res = eng.result()
 print("admit_ms per launch", res["admit_ms"] / max(res["admissions"], 1) * 1e3)
-
-f = np.median(np.array(fin), axis=0)
-print("finalizer CTA 1: arrivals seen %.2f staged %.2f ranked %.2f published %.2f us; table queue applied %.2f us" % tuple(f))
