@@ -16,6 +16,10 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT_DIR = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libcachesage_b200.so")
+# Only the C ABI is exported, and every symbol binds at load time (-z now): a library loaded
+# later in the same process (the reference library in the tests exports its own inline
+# libstdc++ instantiations) can never capture one of our lazily bound calls.
+EXPORTS = os.path.join(CSRC, "exports.map")
 # nlohmann/json 3.11.3 (the reference's serializer; shipped in the image with cudnn_frontend):
 # the output writers format through it so metrics.json / events.jsonl match byte for byte
 JSON_DIR = os.path.join(sysconfig.get_paths()["purelib"], "include", "cudnn_frontend", "thirdparty", "nlohmann")
@@ -59,11 +63,12 @@ def build(verbose: bool = False, force: bool = False) -> str:
         s = os.path.join(CSRC, src)
         o = os.path.join(OUT_DIR, src + ".o")
         if force or _stale(o, [s] + header_deps):
-            _run([NVCC, "-O2", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off,-Wall", *inc, "-I", JSON_DIR, "-c", s,
+            _run([NVCC, "-O2", "-std=c++17", "-Wno-deprecated-gpu-targets", "-Xcompiler", "-fPIC,-ffp-contract=off,-Wall", *inc, "-I", JSON_DIR, "-c", s,
                   "-o", o], verbose)
         objs.append(o)
-    if force or _stale(LIB, objs):
-        _run([NVCC, "-shared", *ARCH, "-o", LIB, *objs, "-lcudart", "-ldl"], verbose)
+    if force or _stale(LIB, objs + [EXPORTS]):
+        _run([NVCC, "-shared", *ARCH, "-Xlinker", "--version-script=" + EXPORTS, "-Xlinker", "-z,now", "-o", LIB, *objs, "-lcudart",
+              "-ldl"], verbose)
     return LIB
 
 

@@ -21,6 +21,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstddef>
 
 #include "cs_block.cuh"
 #include "cs_engine_state.h"
@@ -52,6 +53,7 @@ struct ScanSmem {
     unsigned long long hint[kMaxLists];
     unsigned long long lmin[kMaxLists];
     int overflow;
+    int ovf_base;   // staging positions [0, ovf_base) were all written before an overflow
     int spec;       // speculative pass: phase 0 runs concurrently on CTA 0
     int hc, dc;     // ensure_cls compaction counters
     int prep_done;  // the producer warp already loaded the classes and built the change set
@@ -74,6 +76,9 @@ struct AdmSmem {
     unsigned long long ph[kPhases], tl;  // phase timestamps (CTA 0, thread 0)
     long long pf_head, pf_size;  // the learner window at launch (BFS prefetch)
     int pf_on;
+    unsigned long long srv_t0;  // admission server: when CTA 0 picked this admission up (else 0)
+    int st_done;  // the status went out early (st_early -> CTA kSvcQ), not in the epilogue
+    int svc_b;    // observe(AgentDispatch) comes from the learner service (commit_observe)
 };
 
 // Dynamic shared memory, phase by phase (the regions alias across phases):
@@ -190,6 +195,12 @@ __device__ __forceinline__ unsigned long long gtimer() {
     return t;
 }
 
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
 __device__ __forceinline__ void stamp(AdmSmem& A, int k) {
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         const unsigned long long t = gtimer();
@@ -216,6 +227,56 @@ __device__ __forceinline__ void fstamp(const DevPool& P, int k) {
 // ------------------------------------------------------------------ K3 / K3b / K6
 
 // CacheSagePolicy::observe(AgentDispatch) (cachesage_policy.cpp:57-72). CTA 0, all threads.
+// K3b from a prefetched window (BfsSmem: pairs wa/wb, their counts pc and row totals pt before
+// this dispatch's record, pf_size pairs, rec_c / rec_t = counts[prev][next] / totals[prev]
+// before it): rebuild_reachability (reachability.cpp:39-81) on the learner state the record
+// leaves. The record pushed (prev, next) and, with a full window, pushed out the oldest pair
+// (oa, ob): counts and row totals move by +-1 exactly there (transition_learner.cpp:22-51).
+// Writes B.hop[0, n_agents). All threads of the CTA.
+__device__ void bfs_prefetched(const DevPool& P, BfsSmem& B, int prev, int next, int n_agents) {
+    const int tid = threadIdx.x, T = blockDim.x;
+    const long long W = P.window;
+    const int e = P.e_max;
+    const int sz0 = B.pf_size;
+    const bool popped = prev >= 0 && (long long)sz0 == W;
+    const int oa = popped ? (int)B.wa[0] : -1, ob = popped ? (int)B.wb[0] : -1;
+    const int jlo = popped ? 1 : 0, jhi = sz0 + (prev >= 0 ? 1 : 0);
+    for (int x = tid; x < n_agents; x += T) B.hop[x] = (unsigned char)e;
+    for (int j = jlo + tid; j < jhi; j += T) {
+        int aj, bj;
+        unsigned int c, t;
+        if (j < sz0) {
+            aj = B.wa[j];
+            bj = B.wb[j];
+            c = B.pc[j] + (aj == prev && bj == next ? 1u : 0u) - (aj == oa && bj == ob ? 1u : 0u);
+            t = B.pt[j] + (aj == prev ? 1u : 0u) - (aj == oa ? 1u : 0u);
+        } else {  // the pair this record appended
+            aj = prev;
+            bj = next;
+            B.wa[j] = (unsigned short)aj;
+            B.wb[j] = (unsigned short)bj;
+            c = B.rec_c + 1u - (aj == oa && bj == ob ? 1u : 0u);
+            t = B.rec_t + 1u - (aj == oa ? 1u : 0u);
+        }
+        B.edge[j] = __ddiv_rn((double)c, (double)t) < P.tau ? 0 : 1;
+    }
+    __syncthreads();
+    if (tid == 0) B.hop[next] = 0;
+    __syncthreads();
+    for (int d = 0; d + 1 < e; ++d) {
+        int any = 0;
+        for (int j = jlo + tid; j < jhi; j += T) {
+            const int aj = B.wa[j], bj = B.wb[j];
+            if (!B.edge[j] || B.hop[aj] != d) continue;
+            if (B.hop[bj] > d + 1) {
+                B.hop[bj] = (unsigned char)(d + 1);
+                any = 1;
+            }
+        }
+        if (!__syncthreads_or(any)) break;
+    }
+}
+
 __device__ void observe_dispatch(const DevPool& P, int prev, int next, unsigned long long tick, int n_agents,
                                  unsigned char* dsm, RedSmem& Red, AdmSmem& A, unsigned char* cls_smem = nullptr,
                                  bool prefetched = false) {
@@ -256,49 +317,8 @@ __device__ void observe_dispatch(const DevPool& P, int prev, int next, unsigned 
     __syncthreads();
     if (tid == 0) C->cur_agent = next;
     if (changed && prefetched) {
-        // K3b from the prefetched window: the record's effect applied on chip. The record pushed
-        // (prev, next) and, with a full window, pushed out the oldest pair (oa, ob): counts and
-        // row totals move by +-1 exactly there (transition_learner.cpp:22-51).
-        const int e = P.e_max;
         BfsSmem& B = *reinterpret_cast<BfsSmem*>(dsm);
-        const int sz0 = B.pf_size;
-        const bool popped = prev >= 0 && (long long)sz0 == W;
-        const int oa = popped ? (int)B.wa[0] : -1, ob = popped ? (int)B.wb[0] : -1;
-        const int jlo = popped ? 1 : 0, jhi = sz0 + (prev >= 0 ? 1 : 0);
-        for (int x = tid; x < n_agents; x += T) B.hop[x] = (unsigned char)e;
-        for (int j = jlo + tid; j < jhi; j += T) {
-            int aj, bj;
-            unsigned int c, t;
-            if (j < sz0) {
-                aj = B.wa[j];
-                bj = B.wb[j];
-                c = B.pc[j] + (aj == prev && bj == next ? 1u : 0u) - (aj == oa && bj == ob ? 1u : 0u);
-                t = B.pt[j] + (aj == prev ? 1u : 0u) - (aj == oa ? 1u : 0u);
-            } else {  // the pair this record appended
-                aj = prev;
-                bj = next;
-                B.wa[j] = (unsigned short)aj;
-                B.wb[j] = (unsigned short)bj;
-                c = B.rec_c + 1u - (aj == oa && bj == ob ? 1u : 0u);
-                t = B.rec_t + 1u - (aj == oa ? 1u : 0u);
-            }
-            B.edge[j] = __ddiv_rn((double)c, (double)t) < P.tau ? 0 : 1;
-        }
-        __syncthreads();
-        if (tid == 0) B.hop[next] = 0;
-        __syncthreads();
-        for (int d = 0; d + 1 < e; ++d) {
-            int any = 0;
-            for (int j = jlo + tid; j < jhi; j += T) {
-                const int aj = B.wa[j], bj = B.wb[j];
-                if (!B.edge[j] || B.hop[aj] != d) continue;
-                if (B.hop[bj] > d + 1) {
-                    B.hop[bj] = (unsigned char)(d + 1);
-                    any = 1;
-                }
-            }
-            if (!__syncthreads_or(any)) break;
-        }
+        bfs_prefetched(P, B, prev, next, n_agents);
         for (int x = tid; x < n_agents; x += T) {
             P.hop[x] = B.hop[x];
             P.cls[x] = B.hop[x];
@@ -428,6 +448,200 @@ __device__ void observe_dispatch(const DevPool& P, int prev, int next, unsigned 
         }
         __syncthreads();
     }
+}
+
+// The learner service (CTA kSvcB of a pipelined launch): CacheSagePolicy::observe(AgentDispatch
+// {prev, next}) (cachesage_policy.cpp:50-77) computed speculatively, concurrently with CTA 0's
+// probe, on the learner state this dispatch's record will leave (the record's +-1 applied on
+// chip): the rebuilt reachability (K3b) when the agent changes and the prefetch gate's
+// argmax_row(next) (K6, transition_learner.cpp:79-96). Nothing of the policy's state is written;
+// CTA 0 commits it (commit_observe) only if the request starts, so a request that waits commits
+// nothing. Runs only when CTA 0 uses it (the same predicate, evaluated on the same inputs).
+__device__ void service_learner(const DevPool& P, const AdmitArgs& a, unsigned char* dsm, RedSmem& Red) {
+    Ctrl* C = P.ctrl;
+    const int tid = threadIdx.x, T = blockDim.x;
+    const long long W = P.window;
+    const int Acap = P.a_cap, n_agents = a.n_agents, prev = a.prev, next = a.next;
+    BfsSmem& B = *reinterpret_cast<BfsSmem*>(dsm);
+    __shared__ long long s_head, s_size;
+    __shared__ int s_changed;
+    if (tid == 0) {
+        s_head = __ldcg(&C->win_head);
+        s_size = __ldcg(&C->win_size);
+        s_changed = __ldcg(&C->cur_agent) != next ? 1 : 0;
+    }
+    // row `next` and the ids for the argmax: independent of the window, issued first
+    unsigned long long best_c = 0ull, best_id = ~0ull;
+    int best_b = -1;
+    unsigned int rc[8];
+    unsigned long long rid[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const int b = tid + k * T;
+        rc[k] = b < n_agents ? __ldcg(P.counts + (long long)next * Acap + b) : 0u;
+        rid[k] = b < n_agents ? __ldcg(P.agent_ids + b) : 0ull;
+    }
+    __syncthreads();
+    const long long head = s_head, size = s_size;
+    const bool changed = s_changed != 0;
+    // the window's pairs, then their counts and row totals (two dependent rounds), and the
+    // record's own cell
+    for (long long j = tid; j < size; j += T) {
+        const long long q = (head + j) % W;
+        const int aj = __ldcg(P.win_a + q), bj = __ldcg(P.win_b + q);
+        B.wa[j] = (unsigned short)aj;
+        B.wb[j] = (unsigned short)bj;
+        B.pc[j] = __ldcg(P.counts + (long long)aj * Acap + bj);
+        B.pt[j] = __ldcg(P.totals + aj);
+    }
+    unsigned int tot_next = 0u;
+    if (tid == 0) {
+        B.pf_size = (int)size;
+        if (prev >= 0) {
+            B.rec_c = __ldcg(P.counts + (long long)prev * Acap + next);
+            B.rec_t = __ldcg(P.totals + prev);
+        }
+        tot_next = __ldcg(P.totals + next);
+    }
+    __syncthreads();
+    const bool popped = prev >= 0 && size == W;
+    const int oa = popped ? (int)B.wa[0] : -1, ob = popped ? (int)B.wb[0] : -1;
+    if (changed) bfs_prefetched(P, B, prev, next, n_agents);
+    // argmax_row(next) after the record: +1 at [next][next] when prev == next, -1 at [oa][ob]
+    // when oa == next (the popped pair); ties -> the smaller 64-bit AgentId
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const int b = tid + k * T;
+        if (b >= n_agents) continue;
+        const unsigned int c = rc[k] + (prev >= 0 && prev == next && b == next ? 1u : 0u) -
+                               (oa == next && b == ob ? 1u : 0u);
+        if (c == 0u) continue;
+        if (best_b < 0 || c > best_c || (c == best_c && rid[k] < best_id)) {
+            best_c = c;
+            best_id = rid[k];
+            best_b = b;
+        }
+    }
+    for (int o = 16; o; o >>= 1) {
+        const unsigned long long oc = __shfl_xor_sync(0xffffffffu, best_c, o);
+        const unsigned long long oi = __shfl_xor_sync(0xffffffffu, best_id, o);
+        const int ob2 = __shfl_xor_sync(0xffffffffu, best_b, o);
+        if (ob2 >= 0 && (best_b < 0 || oc > best_c || (oc == best_c && oi < best_id))) {
+            best_c = oc;
+            best_id = oi;
+            best_b = ob2;
+        }
+    }
+    __syncthreads();
+    if (lane_id() == 0) {
+        Red.u[warp_id()] = best_c;
+        Red.v[warp_id()] = (long long)best_b;
+        Red.w[warp_id()] = best_id;
+    }
+    if (changed)
+        for (int x = tid; x < n_agents; x += T) P.spec_hop[x] = B.hop[x];
+    __syncthreads();
+    if (tid == 0) {
+        const int nw = (T + 31) >> 5;
+        best_c = 0;
+        best_b = -1;
+        best_id = ~0ull;
+        for (int w = 0; w < nw; ++w) {
+            const int b = (int)Red.v[w];
+            if (b < 0) continue;
+            const unsigned long long c = Red.u[w], id = Red.w[w];
+            if (best_b < 0 || c > best_c || (c == best_c && id < best_id)) {
+                best_c = c;
+                best_id = id;
+                best_b = b;
+            }
+        }
+        LearnSpec* sp = P.spec;
+        sp->changed = changed ? 1 : 0;
+        sp->oa = oa;
+        sp->ob = ob;
+        sp->best_b = best_b;
+        sp->best_c = (unsigned int)best_c;
+        sp->total_next = tot_next + (prev >= 0 && prev == next ? 1u : 0u) - (oa == next ? 1u : 0u);
+    }
+    __syncthreads();  // (every thread's spec_hop stores before the release)
+    if (tid == 0) {
+        __threadfence();
+        asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(&C->svc_b_seq), "l"(a.seq) : "memory");
+    }
+}
+
+// CTA 0: commits the learner service's observe(AgentDispatch{prev, next}) for a request that
+// starts, exactly as observe_dispatch would have applied it: TransitionLearner::record (the
+// count cells and the window ring, transition_learner.cpp:22-51), the rebuilt hops when the agent
+// changed, and the prefetch gate (cachesage_policy.cpp:109-123).
+__device__ void commit_observe(const DevPool& P, const AdmitArgs& a, unsigned long long tick, AdmSmem& A,
+                               unsigned char* cls_smem) {
+    Ctrl* C = P.ctrl;
+    const int tid = threadIdx.x, T = blockDim.x;
+    const long long W = P.window;
+    const int Acap = P.a_cap, prev = a.prev, next = a.next, n_agents = a.n_agents;
+    __shared__ LearnSpec sp;
+    if (tid == 0) {
+        unsigned long long spins = 0;
+        while (ld_acquire_u64(&C->svc_b_seq) != a.seq) {
+            if (++spins > 4096) __nanosleep(64);
+            if (spins > (1ull << 28)) __trap();
+        }
+        sp = *P.spec;
+    }
+    __syncthreads();
+    pstamp(P, 13);
+    if (sp.changed) {
+        for (int x = tid; x < n_agents; x += T) {
+            const unsigned char h = __ldcg(P.spec_hop + x);
+            P.hop[x] = h;
+            P.cls[x] = h;
+            if (cls_smem) cls_smem[x] = h;
+        }
+    }
+    if (tid == 0) {
+        if (prev >= 0) {  // record: fire-and-forget count updates, the window ring
+            const long long head = A.pf_head, size = A.pf_size;
+            C->recorded += 1ull;
+            atomicAdd(&P.counts[(long long)prev * Acap + next], 1u);
+            atomicAdd(&P.totals[prev], 1u);
+            if (size == W) {
+                P.win_a[head] = prev;
+                P.win_b[head] = next;
+                atomicSub(&P.counts[(long long)sp.oa * Acap + sp.ob], 1u);
+                atomicSub(&P.totals[sp.oa], 1u);
+                C->win_head = head + 1 == W ? 0 : head + 1;
+            } else {
+                const long long pos = (head + size) % W;
+                P.win_a[pos] = prev;
+                P.win_b[pos] = next;
+                C->win_size = size + 1;
+            }
+        }
+        C->cur_agent = next;
+        if (sp.changed) {
+            C->rebuilds += 1ull;
+            C->reach_built = 1;
+        }
+        // maybe_prefetch on argmax_row(next) of the recorded learner
+        const unsigned int total = sp.total_next;
+        if (C->step_warmups < P.budget_per_step && (unsigned long long)total >= P.min_row && total > 0u &&
+            sp.best_b >= 0) {
+            const double p = __ddiv_rn((double)sp.best_c, (double)total);
+            if (!(p < P.min_conf)) {
+                C->step_warmups += 1;
+                if (C->n_pend < kMaxPending) {
+                    C->pend_target[C->n_pend] = sp.best_b;
+                    C->pend_tick[C->n_pend] = tick;
+                    C->n_pend += 1;
+                }
+                A.warm_issued = sp.best_b;
+            }
+        }
+    }
+    __syncthreads();
+    pstamp(P, 14);
 }
 
 // ------------------------------------------------------------------ K4: the pool scan
@@ -665,6 +879,9 @@ __device__ __forceinline__ int append4(unsigned int acc, const unsigned long lon
     if (lane_id() == 31) base = atomicAdd(&S.count, wtot);
     base = __shfl_sync(0xffffffffu, base, 31);
     if (bounded && base + wtot > kStage) {
+        // this warp's reservation [base, base + wtot) stays unwritten, and so does every later
+        // one: only [0, ovf_base) holds staged entries
+        if (lane_id() == 31) atomicMin(&S.ovf_base, base);
         S.overflow = 1;
         return kStage;
     }
@@ -805,11 +1022,6 @@ __device__ void build_xset(const DevPool& P, const AdmitArgs& a, ScanSmem& S) {
     __syncthreads();
 }
 
-__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
-    unsigned long long v;
-    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
 
 // All threads of a scanning CTA, before its first flush (no bound has used a staged entry
 // yet): waits for this launch's phase 0, loads the survival classes it fixed, drops the staged
@@ -945,6 +1157,7 @@ __device__ void scan_pass(const DevPool& P, int NL, int keep, const ScanBufs& B,
     if (tid == 0) {
         S.count = 0;
         S.overflow = 0;
+        S.ovf_base = kStage;
         S.prep_done = 0;
         S.flush_ns = 0;
         S.flushes = 0;
@@ -1292,6 +1505,7 @@ __device__ void prescan_pass(const DevPool& P, const ScanBufs& B, ScanSmem& S, u
     if (tid == 0) {
         S.count = 0;
         S.overflow = 0;
+        S.ovf_base = kStage;
         for (int s = 0; s < kRing; ++s) {
             mbar_init(&S.mbar[s], 1u);
             mbar_init(&S.mbar_empty[s], (unsigned int)(kThreads / 32));
@@ -1364,6 +1578,9 @@ __device__ void prescan_pass(const DevPool& P, const ScanBufs& B, ScanSmem& S, u
         }
     } else if (tid >= kThreads) {  // producer warp: one elected thread keeps kRing tiles in flight
         if (lane_id() == 0) {
+            // generic-proxy writes to the pool that this thread has observed (a kernel boundary,
+            // or the admission server's grid barrier) before the async-proxy bulk reads
+            asm volatile("fence.proxy.async.global;" ::: "memory");
             for (int t = 0; t < ntiles; ++t) {
                 const int s = t % kRing;
                 if (t >= kRing) mbar_wait(&S.mbar_empty[s], (unsigned int)(((t / kRing) - 1) & 1));
@@ -1405,7 +1622,7 @@ __device__ void prescan_pass(const DevPool& P, const ScanBufs& B, ScanSmem& S, u
     const size_t base = ((size_t)par * P.raw_grid + me) * kRawCap;
     // (an overflowed pass keeps what it staged: a subset, from which the service derives a
     // tighter threshold for the next prescan; the lists themselves are then unusable)
-    const int m = min(S.count, kRawCap);
+    const int m = min(min(S.count, S.ovf_base), kRawCap);
     for (int j = tid; j < m; j += T) {
         const unsigned int l = B.st_list[j];
         const unsigned int s = B.st_slot[j];
@@ -1983,6 +2200,9 @@ __device__ void queue_ready(const DevPool& P, const AdmitArgs& a, AdmSmem& A) {
     __syncthreads();
 }
 
+__device__ void fill_status(AdmitStatus* st, const DevPool& P, const AdmSmem& A, long long n_evicted,
+                            long long resident, long long pinned, unsigned long long ev_total, long long tombstones);
+
 // early: only lists E and R are final (CTA 0 finalized E, CTA 1 signalled R); the other
 // lists are awaited only if the bulk test fails.
 __device__ void replay_apply(const DevPool& P, const AdmitArgs& a, ReplaySmem& R, AdmSmem& A, int NL, bool scanned,
@@ -2307,17 +2527,31 @@ __device__ void replay_apply(const DevPool& P, const AdmitArgs& a, ReplaySmem& R
     // admission inserted is pinned, so it is never among its own victims (the queue applies every
     // erase before every insert).
     const int q_e = C->tq_erase, q_i = C->tq_insert;
+    // This chunk completes a plain admission served from a prescan: its status is final now
+    // (publish_early_status); CTA kSvcQ copies it and the victims out while the apply runs.
+    const bool early_st = pre && R.bulk && !err && hi >= A.admit_n && !(a.flags & kUnpinAfter) && a.status != nullptr;
     for (int k = tid; k < nv; k += T) {
         const unsigned long long kk = R.vkey[k];
         P.tq_key[q_e + k] = kk;
         P.evlog[(ev0 + k) % (unsigned long long)P.evlog_cap] = kk;  // ring; the host drains it
-        if (a.vict_host && A.n_ev_adm + k < a.vict_cap) a.vict_host[A.n_ev_adm + k] = kk;  // mapped host memory
+        if (!early_st && a.vict_host && A.n_ev_adm + k < a.vict_cap)
+            a.vict_host[A.n_ev_adm + k] = kk;  // mapped host memory
         if (k >= R.n_reused) {  // victims[0, n_reused) are overwritten by new blocks below
             const unsigned int v = R.victims[k];
             P.lt[v] = kFreeTick;
             P.refs[v] = 0u;
             P.agent[v] = kNoAgent;
             P.pk[v] = kPkFreeWord;
+        }
+    }
+    if (early_st) {
+        __syncthreads();  // every victim key is in the eviction log
+        if (tid == T - 1) {  // (a thread the apply below leaves idle: len <= kChunk < T - 1)
+            fill_status(P.st_early, P, A, A.n_ev_adm + nv, A.resident, A.pinned, ev0 + nv,
+                        C->tombstones + (long long)(q_e + nv));
+            __threadfence();
+            asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(&C->st_seq), "l"(a.seq) : "memory");
+            A.st_done = 1;
         }
     }
     // A serial chunk may evict a later prompt block and re-admit it into the victim's slot:
@@ -2462,33 +2696,85 @@ cudaError_t launch_table_flush(const DevPool& P, cudaStream_t s) {
 
 // ------------------------------------------------------------------ the admission kernel
 
-__device__ void write_status(const DevPool& P, const AdmitArgs& a, const AdmSmem& A) {
+__device__ void fill_status(AdmitStatus* st, const DevPool& P, const AdmSmem& A, long long n_evicted,
+                            long long resident, long long pinned, unsigned long long ev_total, long long tombstones) {
     Ctrl* C = P.ctrl;
-    AdmitStatus* st = a.status;
     st->started = A.started;
     st->error = A.error;
     st->first_miss = A.first_miss;
     st->admit_n = A.admit_n;
     st->cached = A.cached;
-    st->n_evicted = A.n_ev_adm;
-    st->resident = C->resident;
-    st->pinned = C->pinned;
+    st->n_evicted = n_evicted;
+    st->resident = resident;
+    st->pinned = pinned;
     st->tick_after = A.tick;
-    st->ev_total = C->n_ev;
+    st->ev_total = ev_total;
     st->warm_issued = A.warm_issued;
     st->needed = A.needed;
     st->scans = A.scans;
-    // after queue_ready: nothing else changes either until the next launch applies the queue;
-    // the queued erases leave tombstones then (an insert may reuse some): an upper bound, so the
-    // host's rebuild decision is deterministic and conservative
-    st->tombstones = C->tombstones + (long long)C->tq_erase;
+    st->tombstones = tombstones;
     for (int k = 0; k < kPhases; ++k) st->phase_ns[k] = A.ph[k];
+    st->srv_t0 = A.srv_t0;
     st->n_pend = C->n_pend;
     for (int k = 0; k < C->n_pend && k < kMaxPending; ++k) {
         st->pend_target[k] = C->pend_target[k];
         st->pend_tick[k] = C->pend_tick[k];
     }
-    // no system fence: the host reads the mapped record only after the launch completes
+}
+
+__device__ void write_status(const DevPool& P, const AdmitArgs& a, const AdmSmem& A) {
+    Ctrl* C = P.ctrl;
+    // after queue_ready: nothing else changes either until the next launch applies the queue;
+    // the queued erases leave tombstones then (an insert may reuse some): an upper bound, so the
+    // host's rebuild decision is deterministic and conservative
+    fill_status(a.status, P, A, A.n_ev_adm, C->resident, C->pinned, C->n_ev, C->tombstones + (long long)C->tq_erase);
+}
+
+// CTA kSvcQ of a pipelined launch, after its table service: when CTA 0 published this
+// admission's final status early (Ctrl::st_seq, set after the replay's decisions, before the
+// apply), copy it and the admission's victims (from the eviction log) into the host-mapped
+// records and raise done_seq, so the host schedules the next admission while CTA 0 still applies
+// this one. If CTA 0's verdict comes first without it, CTA 0 writes the status itself.
+__device__ void publish_early_status(const DevPool& P, const AdmitArgs& a) {
+    Ctrl* C = P.ctrl;
+    const int tid = threadIdx.x, T = blockDim.x;
+    __shared__ int pub;
+    if (tid == 0) {
+        unsigned long long spins = 0;
+        for (;;) {
+            if (ld_acquire_u64(&C->st_seq) == a.seq) {
+                pub = 1;
+                break;
+            }
+            if (ld_acquire_u64(&C->verdict_seq) == a.seq) {
+                pub = ld_acquire_u64(&C->st_seq) == a.seq ? 1 : 0;
+                break;
+            }
+            if (++spins > 4096) __nanosleep(64);
+            if (spins > (1ull << 28)) __trap();
+        }
+    }
+    __syncthreads();
+    if (!pub) return;
+    const AdmitStatus* src = P.st_early;
+    AdmitStatus* dst = a.status;
+    constexpr int kW = (int)(offsetof(AdmitStatus, done_seq) / 8);
+    static_assert(offsetof(AdmitStatus, done_seq) % 8 == 0, "AdmitStatus is copied as 64-bit words");
+    for (int i = tid; i < kW; i += T)
+        reinterpret_cast<unsigned long long*>(dst)[i] = __ldcg(reinterpret_cast<const unsigned long long*>(src) + i);
+    if (tid == 0) dst->srv_t0 = __ldcg(&src->srv_t0);
+    if (a.vict_host) {
+        const long long n = __ldcg(&src->n_evicted);
+        const unsigned long long e0 = __ldcg(&src->ev_total) - (unsigned long long)n;
+        for (long long k = tid; k < n && k < a.vict_cap; k += T)
+            a.vict_host[k] = __ldcg(P.evlog + (e0 + (unsigned long long)k) % (unsigned long long)P.evlog_cap);
+    }
+    __threadfence_system();  // every thread's record words before the flag
+    __syncthreads();
+    if (tid == 0) {
+        *(volatile unsigned long long*)&dst->done_seq = a.seq;
+        P.dbg[blockIdx.x * 16 + 8] = gtimer();  // (instrumentation: when the host could see it)
+    }
 }
 
 // One admission (the body of admit_kernel; the device-resident engine kernel runs it in a loop).
@@ -2522,6 +2808,7 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
             A.warm_issued = -1;
             A.scans = 0;
             A.q_deleg = 0;
+            A.st_done = 0;
             A.first_touch = ~0ull;
             A.tick = a.tick_base;
             for (int k = 0; k < kPhases; ++k) A.ph[k] = 0;
@@ -2535,7 +2822,11 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
                 const long long wh = C->win_head, wsz = C->win_size;
                 A.pf_head = wh;
                 A.pf_size = wsz;
-                A.pf_on = (a.flags & kDispatch) && P.policy != 0 && a.next >= 0 && C->cur_agent != a.next &&
+                // a pipelined launch: CTA kSvcB computes the dispatch's observe concurrently
+                // (service_learner evaluates the same predicate on the same inputs)
+                A.svc_b = pre_avail && gridDim.x > kSvcB && (a.flags & kDispatch) && P.policy == 1 && a.next >= 0 &&
+                          wsz <= kBfsPre;
+                A.pf_on = !A.svc_b && (a.flags & kDispatch) && P.policy != 0 && a.next >= 0 && C->cur_agent != a.next &&
                           wsz <= 2 * (long long)blockDim.x && wsz <= kBfsPre;
             }
             // a pipelined launch: the list service validates the previous prescan concurrently;
@@ -2725,7 +3016,10 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
             if (a.flags & kDispatch) {
                 if (tid == 0) A.tick = A.tick + 1;
                 __syncthreads();
-                observe_dispatch(P, a.prev, a.next, A.tick, a.n_agents, dsm, Red, A, B.cls, pf);
+                if (A.svc_b)
+                    commit_observe(P, a, A.tick, A, B.cls);
+                else
+                    observe_dispatch(P, a.prev, a.next, A.tick, a.n_agents, dsm, Red, A, B.cls, pf);
             }
             pstamp(P, 4);
             if (a.flags & kLookup) {
@@ -2778,10 +3072,16 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
     bool pending_rescan = false;  // CTA 0: the last pass must be redone (safe, no hints)
     if (pre_avail) {
         if (blockIdx.x != 0) {
-            if (blockIdx.x == kSvcQ)
+            if (blockIdx.x == kSvcQ) {
                 service_queue(P, a, Red);
+                if (a.status) publish_early_status(P, a);
+            }
             else if (blockIdx.x == kSvcL)
                 service_lists(P, a, B, Sel, Red, dsm, par_prev);
+            else if (blockIdx.x == kSvcB) {
+                if ((a.flags & kDispatch) && P.policy == 1 && a.next >= 0 && __ldcg(&C->win_size) <= kBfsPre)
+                    service_learner(P, a, dsm, Red);
+            }
             else
                 prescan_pass(P, B, S, dsm, par_next, P.stream_generic != 0, a.seq);
             if (tid == 0) {
@@ -3068,7 +3368,7 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
         queue_ready(P, a, A);  // (an admission that applied nothing: the counters are reset here)
         stamp(A, 5);
         pstamp(P, 11);
-        if (tid == 0 && a.status) {
+        if (tid == 0 && a.status && !A.st_done) {
             write_status(P, a, A);
             __threadfence_system();  // status and victims reach the host before the flag
             *(volatile unsigned long long*)&a.status->done_seq = a.seq;
@@ -3093,6 +3393,7 @@ __global__ void __launch_bounds__(kThreads + 32, 1) admit_kernel(DevPool P, Admi
     __shared__ SelectSmem Sel;
     __shared__ RedSmem Red;
     __shared__ AdmSmem A;
+    if (threadIdx.x == 0) A.srv_t0 = 0;
     admit_body(P, a, dsm, S, Sel, Red, A);
 }
 
@@ -3107,6 +3408,101 @@ __global__ void __launch_bounds__(kThreads + 32, 1) admit_kernel(DevPool P, Admi
 // ------------------------------------------------------------------ device-resident scheduler
 
 #include "cs_engine_dev.cuh"
+
+// ------------------------------------------------------------------ admission server
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// One persistent cooperative launch serves every admission the host scheduler posts: CTA 0 polls
+// the host-mapped mailbox, relays the arguments (and, on the end-to-end path, copies the
+// admission's prompt blocks from pinned host memory into device scratch), one grid barrier
+// orders everything the previous admission wrote, and every CTA runs admit_body exactly as
+// admit_kernel would. The host's scheduler loop is unchanged; what disappears per admission is
+// the cooperative launch itself and the host's enqueue behind the previous kernel.
+__global__ void __launch_bounds__(kThreads + 32, 1) server_kernel(DevPool P, SrvMailbox* mb, AdmitArgs* dargs,
+                                                                  unsigned long long seq0) {
+    extern __shared__ __align__(16) unsigned char dsm[];
+    __shared__ ScanSmem S;
+    __shared__ SelectSmem Sel;
+    __shared__ RedSmem Red;
+    __shared__ AdmSmem A;
+    __shared__ AdmitArgs a;
+    const int tid = threadIdx.x, T = blockDim.x;
+    constexpr int kWords = (int)(sizeof(AdmitArgs) / 4);
+    static_assert(sizeof(AdmitArgs) % 4 == 0, "AdmitArgs is relayed as 32-bit words");
+    unsigned long long t_exit = 0;  // (CTA 0, thread 0: when the previous admission's work ended)
+    for (unsigned long long seq = seq0;; ++seq) {
+        if (blockIdx.x == 0) {
+            if (tid == 0) {
+                // the host posts within microseconds while its scheduler loop runs (a process
+                // that dies takes its context, and this kernel, with it)
+                unsigned long long spins = 0;
+                while (ld_acquire_sys_u64(&mb->seq) != seq)
+                    if (++spins > 256) __nanosleep(200);
+                A.srv_t0 = gtimer();
+                // instrumentation (tools/cta0_timeline.py): this pickup, the previous admission's
+                // CTA-0 end and its early status publication (CTA kSvcQ)
+                P.dbg[kSvcB * 16 + 10] = A.srv_t0;
+                P.dbg[kSvcB * 16 + 11] = t_exit;
+                P.dbg[kSvcB * 16 + 12] = P.dbg[kSvcQ * 16 + 8];
+            }
+            __syncthreads();
+            const unsigned int* src = reinterpret_cast<const unsigned int*>(&mb->args);
+            unsigned int* d0 = reinterpret_cast<unsigned int*>(&a);
+            unsigned int* d1 = reinterpret_cast<unsigned int*>(dargs);
+            for (int i = tid; i < kWords; i += T) {
+                const unsigned int v = __ldcv(src + i);
+                d0[i] = v;
+                d1[i] = v;
+            }
+            __syncthreads();
+            if (a.stage_src != nullptr && !(a.flags & kSrvStop)) {  // host -> device prompt blocks
+                const unsigned int* hs = reinterpret_cast<const unsigned int*>(a.stage_src);
+                unsigned int* dk = reinterpret_cast<unsigned int*>(const_cast<unsigned long long*>(a.keys));
+                for (int i = tid; i < 3 * a.n; i += T) dk[i] = __ldcv(hs + i);
+            }
+        }
+        grid_barrier(P.ctrl);  // publishes dargs and the staged blocks; orders the last admission
+        if (blockIdx.x != 0) {
+            unsigned int* d0 = reinterpret_cast<unsigned int*>(&a);
+            const unsigned int* d1 = reinterpret_cast<const unsigned int*>(dargs);
+            for (int i = tid; i < kWords; i += T) d0[i] = __ldcg(d1 + i);
+            __syncthreads();
+        }
+        if (a.flags & kSrvStop) {
+            if (blockIdx.x == 0 && tid == 0 && a.status) {
+                a.status->srv_t0 = A.srv_t0;
+                __threadfence_system();
+                *(volatile unsigned long long*)&a.status->done_seq = a.seq;
+            }
+            return;
+        }
+        admit_body(P, a, dsm, S, Sel, Red, A);
+        __syncthreads();
+        if (blockIdx.x == 0 && tid == 0) t_exit = gtimer();
+        fence_proxy_async_smem();  // this admission's generic shared-memory use before the next TMA writes
+    }
+}
+
+cudaError_t launch_server(const DevPool& P, SrvMailbox* mb_dev, AdmitArgs* args_dev, unsigned long long first_seq,
+                          const LaunchCfg& lc, cudaStream_t s) {
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(server_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lc.smem);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    DevPool p = P;
+    SrvMailbox* m = mb_dev;
+    AdmitArgs* d = args_dev;
+    unsigned long long q = first_seq;
+    void* args[] = {&p, &m, &d, &q};
+    return cudaLaunchCooperativeKernel((const void*)server_kernel, dim3(lc.grid), dim3(lc.threads), args, lc.smem, s);
+}
 
 // ------------------------------------------------------------------ host side
 

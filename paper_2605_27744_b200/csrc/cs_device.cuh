@@ -89,6 +89,10 @@ struct Ctrl {
     unsigned long long verdict_seq;     // CTA 0 -> prescan CTAs: this launch's verdict is out
     int verdict;                        // 1: done, 2: everyone joins the command loop
     long long pre_used, pre_fallbacks, pre_badcnt;  // instrumentation
+    // CTA 0 -> CTA kSvcQ: this admission's final status record is in DevPool::st_early (and its
+    // victims in the eviction log); CTA kSvcQ publishes it to the host while CTA 0 applies
+    unsigned long long st_seq;
+    unsigned long long svc_b_seq;  // CTA kSvcB -> CTA 0: LearnSpec / spec_hop are this admission's
 };
 
 // prescan list lengths: E (agentless unpinned) and R (resident) keep the kPreK oldest; the
@@ -98,7 +102,18 @@ constexpr int kPendCap = 4096;
 // Roles in a pipelined launch (admit_kernel): CTA 0 serves this admission; CTA kSvcQ applies the
 // previous admission's queued block-table updates; CTA kSvcL finalizes and validates the previous
 // launch's prescan for CTA 0; CTAs kStream0.. stream the pool for the next admission.
-constexpr int kSvcQ = 1, kSvcL = 2, kStream0 = 3;
+// CTA kSvcB runs this admission's observe(AgentDispatch) speculatively (the learner service).
+constexpr int kSvcQ = 1, kSvcL = 2, kSvcB = 3, kStream0 = 4;
+
+// The learner service's result for CTA 0 (service_learner): observe(AgentDispatch{prev, next})
+// computed on the learner state as this dispatch's record will leave it, committed by CTA 0 only
+// if the request starts. The BFS hops go to DevPool::spec_hop.
+struct LearnSpec {
+    int changed;              // CacheSagePolicy::current_ != next: the reachability was rebuilt
+    int oa, ob;               // the window pair the record pushes out of a full window (else -1)
+    int best_b;               // argmax_row(next) after the record (-1: no positive count)
+    unsigned int best_c, total_next;
+};
 constexpr int kRawCap = 6144;  // raw prescan candidates per streaming CTA (its staging capacity)
 // header of one streaming CTA's raw prescan output
 struct RawHdr {
@@ -168,6 +183,8 @@ struct BelCtl {
     unsigned int hist[kBelPasses][256];
 };
 
+struct AdmitStatus;
+
 struct DevPool {
     long long cap;            // slots == EngineConfig::budget_blocks
     long long cap_scan;       // cap rounded up to 64: the SoA tail is padded with free slots
@@ -231,6 +248,9 @@ struct DevPool {
     unsigned int* tq_slot;
 
     Ctrl* ctrl;
+    AdmitStatus* st_early;  // device copy of an admission's status, published early (Ctrl::st_seq)
+    LearnSpec* spec;        // the learner service's speculative observe (Ctrl::svc_b_seq)
+    unsigned char* spec_hop;  // [a_cap] its BFS hops
 
     // raw prescan output, per launch parity and streaming CTA: the CTA's staged candidates in
     // staging order ([2][raw_grid][kRawCap] lt / slot / list id / agent) and its header

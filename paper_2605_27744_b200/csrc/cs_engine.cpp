@@ -276,6 +276,7 @@ struct cs_engine {
     }
     void ev_prepare(csb::AdmitArgs& a, int nb) {
         if (!rec_events) return;
+        if (4 * (size_t)std::max(nb, 1) > d_touch.n) pool->server_stop();  // (never while it runs)
         d_touch.ensure(4 * (size_t)std::max(nb, 1));
         a.touch_agent = d_touch.as<unsigned int>();
     }
@@ -470,6 +471,8 @@ void cs_engine::build(const cs_engine_cfg& c, const cs_workload_spec* ws, long l
             pack(desc[nt + ag].blk_off, (int)((spec.template_tokens + spec.anchor[ag] + 1 + bs - 1) / bs));
         h_vict_cap = max_nb;
         ck(cudaMallocHost(reinterpret_cast<void**>(&h_vict), 8 * (size_t)h_vict_cap), "cudaMallocHost");
+        d_stage_keys.ensure(12 * (size_t)max_nb);  // sized once: no allocation inside the engine loop
+        pool->ensure_prompt_scratch(max_nb);
         d_keys.release();
         d_counts.release();
     }
@@ -678,9 +681,17 @@ void cs_engine::stage(csb::AdmitArgs& a, int64_t blk_off, int nb) {
         a.counts = d_counts.as<int>() + blk_off;
         return;
     }
+    if (12 * (size_t)std::max(nb, 1) > d_stage_keys.n) pool->server_stop();  // (never while it runs)
     d_stage_keys.ensure(12 * (size_t)std::max(nb, 1));
-    ck(cudaMemcpyAsync(d_stage_keys.p, h_blob + 12 * blk_off, 12 * (size_t)nb, cudaMemcpyHostToDevice, pool->stream),
-       "H2D");
+    if (pool->uses_server()) {  // the admission server's CTA 0 reads them from pinned host memory
+        unsigned char* dp = nullptr;
+        ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dp), h_blob, 0), "cudaHostGetDevicePointer(prompts)");
+        a.stage_src = dp + 12 * blk_off;
+    } else {
+        ck(cudaMemcpyAsync(d_stage_keys.p, h_blob + 12 * blk_off, 12 * (size_t)nb, cudaMemcpyHostToDevice,
+                           pool->stream),
+           "H2D");
+    }
     h2d_bytes += 12 * (int64_t)nb;
     a.keys = d_stage_keys.as<unsigned long long>();
     a.counts = reinterpret_cast<int*>(d_stage_keys.as<unsigned char>() + 8 * (size_t)nb);
@@ -990,9 +1001,24 @@ int cs_engine_destroy(cs_engine_t e) {
     });
 }
 
+namespace {
+// Engine loops leave no admission server running behind them (csb::server_kernel): the next
+// pool or engine call may need the stream.
+struct ServerScope {
+    cs_pool* pool;
+    ~ServerScope() {
+        try {
+            pool->server_stop();
+        } catch (...) {  // (the loop's own error, if any, is the one reported)
+        }
+    }
+};
+}  // namespace
+
 int cs_engine_step(cs_engine_t e, int* done) {
     return eguard([&] {
         if (!e) throw std::invalid_argument("cs_engine_step: null engine");
+        ServerScope scope{e->pool};
         if (e->dev) {
             if (!e->done()) e->dev_run(LLONG_MAX, 1);
         } else {
@@ -1005,6 +1031,7 @@ int cs_engine_step(cs_engine_t e, int* done) {
 int cs_engine_run(cs_engine_t e) {
     return eguard([&] {
         if (!e) throw std::invalid_argument("cs_engine_run: null engine");
+        ServerScope scope{e->pool};
         if (e->dev) {
             while (!e->done()) e->dev_run(e->admissions + e->dev_chunk(), LLONG_MAX);
         } else {
@@ -1018,6 +1045,7 @@ int cs_engine_run(cs_engine_t e) {
 int cs_engine_run_for(cs_engine_t e, int64_t max_adm, int* done) {
     return eguard([&] {
         if (!e) throw std::invalid_argument("cs_engine_run_for: null engine");
+        ServerScope scope{e->pool};
         const int64_t stop = e->admissions + max_adm;
         if (e->dev) {
             while (!e->done() && e->admissions < stop) e->dev_run(std::min<int64_t>(stop, e->admissions + e->dev_chunk()), LLONG_MAX);
@@ -1070,10 +1098,15 @@ int cs_engine_run_timed(cs_engine_t e, int64_t max_adm, double* device_ms, int* 
         e->pool->sync();
         ck(cudaEventRecord(a, e->pool->stream), "cudaEventRecord");
         const int64_t stop = e->admissions + max_adm;
-        if (e->dev) {
-            while (!e->done() && e->admissions < stop) e->dev_run(std::min<int64_t>(stop, e->admissions + e->dev_chunk()), LLONG_MAX);
-        } else {
-            while (!e->done() && e->admissions < stop) e->step();
+        {
+            ServerScope scope{e->pool};
+            if (e->dev) {
+                while (!e->done() && e->admissions < stop)
+                    e->dev_run(std::min<int64_t>(stop, e->admissions + e->dev_chunk()), LLONG_MAX);
+            } else {
+                while (!e->done() && e->admissions < stop) e->step();
+            }
+            e->pool->server_stop();  // (inside the timed region: the server's exit is part of it)
         }
         ck(cudaEventRecord(b, e->pool->stream), "cudaEventRecord");
         ck(cudaEventSynchronize(b), "cudaEventSynchronize");

@@ -18,7 +18,8 @@ enum AdmitFlags : int {
     kAdmit = 128,      // run admit_pinned at all (lookup-only / observe-only calls clear it)
     kSpeculate = 256,  // scan chunk 0 concurrently with phase 0 (cooperative grid only)
     kPrescan = 512,    // CTAs 1.. run the NEXT admission's scoring pass in this launch
-    kUsePrescan = 1024 // chunk 0 may use the lists the previous launch's prescan produced
+    kUsePrescan = 1024, // chunk 0 may use the lists the previous launch's prescan produced
+    kSrvStop = 2048     // admission server (server_kernel): the host's stop command, no admission
 };
 
 constexpr int kMaxUnpinRanges = 8;  // deferred EngineSim::unpin calls folded into one launch
@@ -51,6 +52,8 @@ struct AdmitStatus {
     // AdmitArgs::seq once every field above (and AdmitArgs::vict_host) is written: CTA 0 sets
     // it behind a system-scope fence, so the host continues while the prescan CTAs finish
     unsigned long long done_seq;
+    // admission server: %globaltimer when CTA 0 picked this admission (or the stop) up
+    unsigned long long srv_t0;
 };
 
 struct AdmitArgs {
@@ -89,6 +92,18 @@ struct AdmitArgs {
     // host memory (mapped) before done_seq; at most vict_cap
     unsigned long long* vict_host;
     int vict_cap;
+    // the end-to-end path of the admission server: this admission's [keys (8 n) | counts (4 n)]
+    // in pinned host memory; CTA 0 copies them into keys/counts (device) before phase 0
+    const unsigned char* stage_src;
+};
+
+// The admission server's mailbox (server_kernel): pinned, host-mapped memory the host writes
+// and CTA 0 polls. The host writes args, then seq (x86 stores stay in order); CTA 0 waits for
+// seq == the admission it expects, then reads args.
+struct SrvMailbox {
+    unsigned long long seq;
+    unsigned long long pad[15];  // args start on their own 128-B line
+    AdmitArgs args;
 };
 
 struct LaunchCfg {
@@ -103,6 +118,11 @@ struct LaunchCfg {
 LaunchCfg admit_launch_config(const DevPool& P, int device, int want_grid);
 cudaError_t launch_admit(const DevPool& P, const AdmitArgs& a, const LaunchCfg& lc, int grid,
                          cudaStream_t s);
+// The admission server: ONE persistent cooperative launch that runs admit_body for every
+// admission the host posts in the mailbox (seq first_seq, first_seq + 1, ...) until a kSrvStop
+// post. args_dev (device) relays each admission's arguments from CTA 0 to the other CTAs.
+cudaError_t launch_server(const DevPool& P, SrvMailbox* mb_dev, AdmitArgs* args_dev, unsigned long long first_seq,
+                          const LaunchCfg& lc, cudaStream_t s);
 
 // Belady admission (cs_belady.cuh): one cooperative launch per admission.
 LaunchCfg belady_launch_config(const DevPool& P, int device);

@@ -1,6 +1,8 @@
 // cs_pool: device allocation, the admission driver, and the pool-level C ABI.
 #include "cs_pool.hpp"
 
+#include <atomic>
+
 #include <algorithm>
 #include <cstddef>
 #include <cstdlib>
@@ -209,11 +211,24 @@ void cs_pool::create(const cs_pool_cfg& c, long long shard_slots, cs_comm* cm) {
     ck(cudaHostAlloc(reinterpret_cast<void**>(&st), sizeof(csb::AdmitStatus), cudaHostAllocMapped), "cudaHostAlloc");
     std::memset(st, 0, sizeof(*st));
     ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(&st_dev), st, 0), "cudaHostGetDevicePointer");
+    ck(cudaHostAlloc(reinterpret_cast<void**>(&mb), sizeof(csb::SrvMailbox), cudaHostAllocMapped), "cudaHostAlloc");
+    std::memset(mb, 0, sizeof(*mb));
+    ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(&mb_dev), mb, 0), "cudaHostGetDevicePointer");
+    d_srv_args = dmalloc<csb::AdmitArgs>(1, "server args");
+    P.st_early = dmalloc<csb::AdmitStatus>(1, "early status");
+    P.spec = dmalloc<csb::LearnSpec>(1, "learner service");
+    P.spec_hop = dmalloc<unsigned char>(P.a_cap, "learner service hops");
+    if (const char* e = std::getenv("CS_SERVER")) server = std::atoi(e) != 0;
+    if (const char* e = std::getenv("CS_SERVER_GENERIC")) server_generic = std::atoi(e) != 0;
     ck(csb::launch_init_pool(p, stream), "init_pool");
     sync();
 }
 
 void cs_pool::destroy() {
+    try {
+        server_stop();
+    } catch (...) {
+    }
     csb::DevPool& p = P;
     void* ptrs[] = {p.pk, p.lt, p.agent, p.refs, p.key, p.tokens, p.table, p.free_stack, p.evlog, p.counts, p.totals,
                     p.win_a, p.win_b, p.hop, p.cls, p.agent_ids, p.ctrl, p.gbound, p.gcount, p.fin_lt, p.fin_slot,
@@ -221,7 +236,7 @@ void cs_pool::destroy() {
                     p.sh_send1, p.sh_recv1, p.sh_send2, p.sh_recv2, p.sh_state, p.sh_gslot, p.sh_grefs0,
                     p.pl_lt, p.pl_slot, p.pl_agent, p.pl_ok, p.pl_key, p.pl_n, p.pl_T, p.pre_hint,
                     p.raw_lt, p.raw_slot, p.raw_list, p.raw_agent, p.raw_hdr,
-                    p.bel_nu, p.bel_kid, p.bel_kid_slot, (void*)p.bel_ref, (void*)p.bel_ref_off, (void*)p.bel_depth,
+                    (void*)p.st_early, (void*)p.spec, p.spec_hop, p.bel_nu, p.bel_kid, p.bel_kid_slot, (void*)p.bel_ref, (void*)p.bel_ref_off, (void*)p.bel_depth,
                     (void*)p.bel_kid_of, p.bel_hi, p.bel_lo, p.bel_cand, p.bel_ctl};
     for (void* q : ptrs)
         if (q) cudaFree(q);
@@ -232,6 +247,8 @@ void cs_pool::destroy() {
     d_aux2.release();
     d_aux3.release();
     if (st) cudaFreeHost(st);
+    if (mb) cudaFreeHost(mb);
+    if (d_srv_args) cudaFree(d_srv_args);
     if (hstate) cudaFreeHost(hstate);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
@@ -253,6 +270,7 @@ void cs_pool::ensure_prompt_scratch(long long n) {
         n = c;
     }
     long long c = std::max<long long>(n, P.p_cap * 2);
+    server_stop();  // (the scratch is the server's: never reallocated under it)
     if (P.p_slot) {
         ck(csb::launch_table_flush(P, stream), "table flush");  // the queue lives in this scratch
         ++launches;
@@ -471,7 +489,8 @@ const csb::AdmitStatus& cs_pool::admit(const csb::AdmitArgs& in, int n_for_grid)
         const char* e = std::getenv("CS_FULL_GRID");  // A/B switch (tools): every admission cooperative
         return e && std::atoi(e) != 0;
     }();
-    const int grid = (may_evict || full_grid) ? lc.grid : 1;
+    const bool srv = uses_server();
+    const int grid = (srv || may_evict || full_grid) ? lc.grid : 1;
     // queued unpins run first inside this launch (they fit the change set of a speculative pass)
     if ((int)unpin_q.size() > csb::kMaxUnpinRanges) flush_unpins();
     a.n_unpin_ranges = 0;
@@ -510,24 +529,43 @@ const csb::AdmitStatus& cs_pool::admit(const csb::AdmitArgs& in, int n_for_grid)
         a.vict_cap = vpref_n;
     }
     cudaEvent_t e0 = nullptr, e1 = nullptr;
-    if (timing) {
-        e0 = take_event();
-        e1 = take_event();
-        ck(cudaEventRecord(e0, stream), "cudaEventRecord");
+    if (srv) {
+        // the server must run on the current pool arguments (scratch may have been reallocated)
+        csb::DevPool want = P;
+        want.stream_generic = server_generic ? 1 : 0;
+        if (srv_running && std::memcmp(&want, &srv_P, sizeof(want)) != 0) server_stop();
+        if (!srv_running) {
+            srv_P = want;
+            ck(csb::launch_server(srv_P, mb_dev, d_srv_args, a.seq, lc, stream), "server_kernel launch");
+            ++launches;
+            ++server_launches;
+            srv_running = true;
+            srv_have_t0 = false;
+        }
+        server_post(a);
+    } else {
+        if (timing) {
+            e0 = take_event();
+            e1 = take_event();
+            ck(cudaEventRecord(e0, stream), "cudaEventRecord");
+        }
+        ck(csb::launch_admit(P, a, lc, grid, stream), "admit_kernel launch");
+        ++launches;
+        if (timing) ck(cudaEventRecord(e1, stream), "cudaEventRecord");
     }
-    ck(csb::launch_admit(P, a, lc, grid, stream), "admit_kernel launch");
-    ++launches;
-    if (timing) ck(cudaEventRecord(e1, stream), "cudaEventRecord");
     // The status flag is set by CTA 0 while the prescan CTAs still stream the next admission's
     // pass: the host prepares and enqueues the next launch behind this one instead of waiting
     // for the kernel's end (stream order keeps every later device operation behind it).
-    wait_status(a.seq, "admit_kernel");
+    wait_status(a.seq, srv ? "server_kernel" : "admit_kernel");
     if (!early_status) ck(cudaStreamSynchronize(stream), "admit_kernel");
     vpref_done = (vpref && vpref_n > 0) ? (int)std::min<long long>(st->n_evicted, vpref_n) : 0;
     vpref = nullptr;
     vpref_n = 0;
     poll_reset_pending = false;
-    if (timing) {
+    if (timing && srv) {
+        server_account(st->srv_t0);
+        srv_last_scan = st->scans > 0;
+    } else if (timing) {
         t_pending.push_back({e0, e1, st->scans > 0});
         resolve_timing(false);
     }
@@ -553,11 +591,50 @@ const csb::AdmitStatus& cs_pool::admit(const csb::AdmitArgs& in, int n_for_grid)
     if (st->error) throw std::runtime_error("evict_one: all resident blocks are pinned");
     // erased entries become tombstones; rebuild before live + tombstones pass half the table
     if ((unsigned long long)(st->resident + st->tombstones) > (P.tmask + 1) / 2) {
+        server_stop();
         ck(csb::launch_table_rebuild(P, stream), "table rebuild");
         ++table_rebuilds;
         launches += 2;
     }
     return *st;
+}
+
+void cs_pool::server_post(const csb::AdmitArgs& a) {
+    std::memcpy(&mb->args, &a, sizeof(a));
+    std::atomic_thread_fence(std::memory_order_seq_cst);  // the arguments before the sequence number
+    *reinterpret_cast<volatile unsigned long long*>(&mb->seq) = a.seq;
+}
+
+void cs_pool::server_account(unsigned long long t_next) {
+    if (srv_have_t0 && t_next >= srv_last_t0) {
+        const double ms = (double)(t_next - srv_last_t0) / 1e6;
+        admit_ms += ms;
+        ++admit_launches;
+        if (srv_last_scan) {
+            scan_launch_ms += ms;
+            ++scan_launches;
+        }
+    }
+    srv_last_t0 = t_next;
+    srv_have_t0 = true;
+}
+
+void cs_pool::server_stop() {
+    if (!srv_running) return;
+    srv_running = false;
+    // The stop takes the next sequence number without consuming it: the next admission reuses
+    // it, so the prescan parity (AdmitArgs::seq & 1) of the last admission before the stop and
+    // of the first one after it stay consecutive and the next admission can use that prescan.
+    csb::AdmitArgs a{};
+    a.flags = csb::kSrvStop;
+    a.status = st_dev;
+    a.seq = seq + 1;
+    server_post(a);
+    ck(cudaStreamSynchronize(stream), "server_kernel");
+    if (st->done_seq != a.seq) throw CsError(CS_ERR_CUDA, "server_kernel: no stop acknowledgement");
+    st->done_seq = 0;  // (the next admission waits for this number again)
+    if (timing) server_account(st->srv_t0);
+    srv_have_t0 = false;
 }
 
 cudaEvent_t cs_pool::take_event() {
@@ -615,7 +692,9 @@ void cs_pool::defer_unpin(const unsigned int* dev_slots, int n) {
 }
 
 void cs_pool::flush_unpins() {
-    if (!unpin_q.empty()) pre_ok = false;  // unpins outside an admission launch: no prescan reuse
+    if (unpin_q.empty()) return;
+    server_stop();
+    pre_ok = false;  // unpins outside an admission launch: no prescan reuse
     for (const auto& u : unpin_q) {
         ck(csb::launch_unpin(P, u.first, u.second, stream), "unpin");
         ++launches;

@@ -156,7 +156,30 @@ struct cs_pool {
     // Applies queued block-table updates (admissions defer them to the next launch's phase 0).
     void flush_table();
     void sync() {
+        server_stop();  // (the admission server occupies the stream until it is told to stop)
         csb::ck(cudaStreamSynchronize(stream), "cudaStreamSynchronize");
         resolve_timing(true);
     }
+
+    // Admission server (csb::server_kernel): inside an engine loop (early_status) every admission
+    // is posted to ONE persistent cooperative launch through a host-mapped mailbox instead of
+    // launching admit_kernel. Anything else that needs the stream stops it first (sync(),
+    // flush_unpins, the table rebuild); the next admission starts it again.
+    bool server = true;           // use the server where it applies (A/B switch: CS_SERVER=0)
+    bool server_generic = false;  // stream the pool with L2 loads instead of TMA in the server
+    bool srv_running = false;
+    csb::SrvMailbox* mb = nullptr;      // pinned, mapped
+    csb::SrvMailbox* mb_dev = nullptr;
+    csb::AdmitArgs* d_srv_args = nullptr;
+    csb::DevPool srv_P{};
+    long long server_launches = 0;
+    // per-admission device time from the server's pickup stamps: admission k's time is the
+    // interval to admission k+1's pickup (the host's turnaround included)
+    bool srv_have_t0 = false, srv_last_scan = false;
+    unsigned long long srv_last_t0 = 0;
+    bool uses_server() const { return server && early_status && !comm && P.policy != 3 && lc.grid > csb::kStream0; }
+    void server_post(const csb::AdmitArgs& a);
+    void server_start();
+    void server_stop();
+    void server_account(unsigned long long t_next);
 };

@@ -216,6 +216,33 @@ def cfg4_mixed(sessions=400_000, budget=16 << 20, seed=2608):
     }
 
 
+def cfg5_stress(agents, sessions=40_000, budget=16 << 20, seed=2609):
+    """cfg5 stress trace over A agents: every agent has 4 distinct successors
+    with Dirichlet(1) weights (seeded), sessions start at agent 0 (the supervisor), so the BFS from
+    the current agent spreads the survival classes over 0..e_max. anchor_stride shrinks with A so
+    A x stride stays within the generator's 24-bit anchor space (A <= 1024)."""
+    import numpy as np
+
+    A = int(agents)
+    rng = np.random.default_rng(seed + A)
+    T = [[0.0] * A for _ in range(A)]
+    for i in range(A):
+        k = min(4, A - 1)
+        succ = rng.choice([j for j in range(A) if j != i], size=k, replace=False)
+        w = rng.dirichlet(np.ones(k))
+        for j, x in zip(succ, w):
+            T[i][int(j)] = float(x)
+    return {
+        "name": f"cfg5-stress-{A}",
+        "anchor_tokens": [176] * A,
+        "transition": T, "supervisor": 0,
+        "turns_min": 6, "turns_max": 14, "sessions": sessions,
+        "task_tokens": 160, "history_growth": 8, "decode_tokens": 32, "template_tokens": 16,
+        "concurrency": 4, "budget_blocks": budget, "seed": seed,
+        "anchor_stride": min(0x10000, (1 << 24) // A), "hist_pos_bits": 11, "prefetch": True,
+    }
+
+
 def _splitmix(x):
     import numpy as np
 

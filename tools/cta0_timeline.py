@@ -21,8 +21,9 @@ eng.run_timed(int(sys.argv[1]) if len(sys.argv) > 1 else 100)
 rows = []
 svc = []
 ends = []
+srv = []
 for it in range(40):
-    eng.run_timed(1)
+    eng.run_timed(2)  # (the admission server: the second admission's pickup follows the first one)
     buf = (C.c_uint64 * (16 * 1024))()
     grid = C.c_int(0)
     rc = lib().cs_pool_debug(lib().cs_engine_pool(eng.h), buf, 16 * 1024, C.byref(grid))
@@ -36,8 +37,13 @@ for it in range(40):
     # service CTAs: 1 = table queue (start, done), 2 = list service (start, gathered, published)
     svc.append([(per[1, 6] - ent) / 1e3, (per[1, 7] - ent) / 1e3, (per[2, 6] - ent) / 1e3, (per[2, 7] - ent) / 1e3,
                 (per[2, 8] - ent) / 1e3])
-    # streaming CTAs 3..: start, stream end, writeout end (= verdict wait start), verdict seen
-    ends.append([((per[3:, c] - ent) / 1e3).max() for c in (0, 1, 4, 5)])
+    # streaming CTAs 4..: start, stream end, writeout end (= verdict wait start), verdict seen
+    ends.append([((per[4:, c] - ent) / 1e3).max() for c in (0, 1, 4, 5)])
+    # admission server (row 3): this pickup, the previous admission's CTA-0 end and its early
+    # status publication, relative to this pickup
+    pk = per[3, 10]
+    if pk > 0 and per[3, 11] > 0:
+        srv.append([(per[3, 11] - pk) / 1e3, (per[3, 12] - pk) / 1e3, (ent - pk) / 1e3])
 r = np.median(np.array(rows), axis=0)
 for k in [0, 1, 2, 3, 13, 14, 4, 5, 6, 7, 9, 10, 11, 12]:
     print(f"{NAMES[k]:>14}: {r[k]:8.2f} us")
@@ -46,5 +52,9 @@ print("streaming CTAs (max over CTAs): start %.2f stream end %.2f writeout %.2f 
 sv = np.median(np.array(svc), axis=0)
 print("service CTA 1 (table queue): start %.2f done %.2f us; CTA 2 (lists): start %.2f gathered %.2f published %.2f us"
       % tuple(sv))
+if srv:
+    v = np.median(np.array(srv), axis=0)
+    print("server: previous admission's CTA 0 ended %.2f us and its status went out %.2f us before this pickup; "
+          "admit_body entry %.2f us after it" % (-v[0], -v[1], v[2]))
 res = eng.result()
 print("admit_ms per launch", res["admit_ms"] / max(res["admissions"], 1) * 1e3)
