@@ -77,7 +77,7 @@ struct AdmSmem {
     long long pf_head, pf_size;  // the learner window at launch (BFS prefetch)
     int pf_on;
     unsigned long long srv_t0;  // admission server: when CTA 0 picked this admission up (else 0)
-    int st_done;  // the status went out early (st_early -> CTA kSvcQ), not in the epilogue
+    int st_done;  // the status went out early (from the apply's idle warp), not in the epilogue
     int svc_b;    // observe(AgentDispatch) comes from the learner service (commit_observe)
 };
 
@@ -209,6 +209,13 @@ __device__ __forceinline__ void stamp(AdmSmem& A, int k) {
     }
 }
 
+// The admission server's trace ring (instrumentation, tools/cta0_timeline.py): per admission
+// (seq % 8) 8 %globaltimer stamps: 0 pickup, 1 admit_body entry, 2 phase 0 end, 3 early status
+// ready (CTA 0), 4 status published (CTA kSvcQ), 5 CTA 0 done, 6 streamers' verdict seen (CTA 4)
+__device__ __forceinline__ void tstamp(const DevPool& P, unsigned long long seq, int k) {
+    P.dbg[(size_t)gridDim.x * 16 + 192 + (seq & 7ull) * 8 + k] = gtimer();
+}
+
 // CTA-0 serial-chain timestamps (%globaltimer), after the per-CTA rows (instrumentation)
 __device__ __forceinline__ void pstamp(const DevPool& P, int k) {
     if (blockIdx.x == 0 && threadIdx.x == 0) P.dbg[gridDim.x * 16 + k] = gtimer();
@@ -216,7 +223,7 @@ __device__ __forceinline__ void pstamp(const DevPool& P, int k) {
 
 // CTA-0 sub-phase timestamps of the replay (instrumentation row 0, columns 10..15)
 __device__ __forceinline__ void dstamp(const DevPool& P, int k) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) P.dbg[10 + k] = clock64();
+    if (blockIdx.x == 0 && threadIdx.x == 0) P.dbg[10 + k] = gtimer();
 }
 
 // CTA-0 sub-phase SM-clock stamps of finalize_list (instrumentation row 2, columns 10..15)
@@ -2527,8 +2534,9 @@ __device__ void replay_apply(const DevPool& P, const AdmitArgs& a, ReplaySmem& R
     // admission inserted is pinned, so it is never among its own victims (the queue applies every
     // erase before every insert).
     const int q_e = C->tq_erase, q_i = C->tq_insert;
-    // This chunk completes a plain admission served from a prescan: its status is final now
-    // (publish_early_status); CTA kSvcQ copies it and the victims out while the apply runs.
+    // This chunk completes a plain admission served from a prescan: its status is final once the
+    // victims are known, so the apply's idle warp publishes it (and the victims) to the host while
+    // the other warps apply; the host schedules the next admission meanwhile.
     const bool early_st = pre && R.bulk && !err && hi >= A.admit_n && !(a.flags & kUnpinAfter) && a.status != nullptr;
     for (int k = tid; k < nv; k += T) {
         const unsigned long long kk = R.vkey[k];
@@ -2544,14 +2552,20 @@ __device__ void replay_apply(const DevPool& P, const AdmitArgs& a, ReplaySmem& R
             P.pk[v] = kPkFreeWord;
         }
     }
-    if (early_st) {
-        __syncthreads();  // every victim key is in the eviction log
-        if (tid == T - 1) {  // (a thread the apply below leaves idle: len <= kChunk < T - 1)
-            fill_status(P.st_early, P, A, A.n_ev_adm + nv, A.resident, A.pinned, ev0 + nv,
+    if (early_st && warp_id() == (T >> 5) - 1) {  // (the apply below leaves it idle: len <= kChunk)
+        const int lane = lane_id();
+        tstamp(P, a.seq, 3);
+        if (lane == 0)
+            fill_status(a.status, P, A, A.n_ev_adm + nv, A.resident, A.pinned, ev0 + nv,
                         C->tombstones + (long long)(q_e + nv));
-            __threadfence();
-            asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(&C->st_seq), "l"(a.seq) : "memory");
+        if (a.vict_host)
+            for (int k = lane; k < nv && A.n_ev_adm + k < a.vict_cap; k += 32) a.vict_host[A.n_ev_adm + k] = R.vkey[k];
+        __threadfence_system();  // each lane's record words and victims before the flag
+        __syncwarp();
+        if (lane == 0) {
+            *(volatile unsigned long long*)&a.status->done_seq = a.seq;
             A.st_done = 1;
+            tstamp(P, a.seq, 4);
         }
     }
     // A serial chunk may evict a later prompt block and re-admit it into the victim's slot:
@@ -2618,6 +2632,11 @@ __device__ void replay_apply(const DevPool& P, const AdmitArgs& a, ReplaySmem& R
 // both (erased, then re-inserted). Open addressing over kOv entries in the (idle) TMA ring.
 constexpr int kOv = 2048;
 constexpr int kOvMax = kOv / 2;
+// phase 0's early table finds: slots and keys of up to kFindMax prompt blocks, in the TMA ring
+// after the overlay (below the early-validation view)
+constexpr int kFindMax = 2048;
+constexpr size_t kFindOff = 12ull * kOv;
+static_assert(kFindOff + 12ull * kFindMax <= kEarlyOff, "early finds must stay below the early-validation view");
 constexpr unsigned int kOvErase = 0x7FFFFFFFu;  // erased only (slots stay below 2^31 - 16)
 constexpr unsigned int kOvBoth = 0x80000000u;   // slot | kOvBoth: erased, then re-inserted
 constexpr unsigned int kOvSlot = ~kOvBoth;
@@ -2730,52 +2749,6 @@ __device__ void write_status(const DevPool& P, const AdmitArgs& a, const AdmSmem
     fill_status(a.status, P, A, A.n_ev_adm, C->resident, C->pinned, C->n_ev, C->tombstones + (long long)C->tq_erase);
 }
 
-// CTA kSvcQ of a pipelined launch, after its table service: when CTA 0 published this
-// admission's final status early (Ctrl::st_seq, set after the replay's decisions, before the
-// apply), copy it and the admission's victims (from the eviction log) into the host-mapped
-// records and raise done_seq, so the host schedules the next admission while CTA 0 still applies
-// this one. If CTA 0's verdict comes first without it, CTA 0 writes the status itself.
-__device__ void publish_early_status(const DevPool& P, const AdmitArgs& a) {
-    Ctrl* C = P.ctrl;
-    const int tid = threadIdx.x, T = blockDim.x;
-    __shared__ int pub;
-    if (tid == 0) {
-        unsigned long long spins = 0;
-        for (;;) {
-            if (ld_acquire_u64(&C->st_seq) == a.seq) {
-                pub = 1;
-                break;
-            }
-            if (ld_acquire_u64(&C->verdict_seq) == a.seq) {
-                pub = ld_acquire_u64(&C->st_seq) == a.seq ? 1 : 0;
-                break;
-            }
-            if (++spins > 4096) __nanosleep(64);
-            if (spins > (1ull << 28)) __trap();
-        }
-    }
-    __syncthreads();
-    if (!pub) return;
-    const AdmitStatus* src = P.st_early;
-    AdmitStatus* dst = a.status;
-    constexpr int kW = (int)(offsetof(AdmitStatus, done_seq) / 8);
-    static_assert(offsetof(AdmitStatus, done_seq) % 8 == 0, "AdmitStatus is copied as 64-bit words");
-    for (int i = tid; i < kW; i += T)
-        reinterpret_cast<unsigned long long*>(dst)[i] = __ldcg(reinterpret_cast<const unsigned long long*>(src) + i);
-    if (tid == 0) dst->srv_t0 = __ldcg(&src->srv_t0);
-    if (a.vict_host) {
-        const long long n = __ldcg(&src->n_evicted);
-        const unsigned long long e0 = __ldcg(&src->ev_total) - (unsigned long long)n;
-        for (long long k = tid; k < n && k < a.vict_cap; k += T)
-            a.vict_host[k] = __ldcg(P.evlog + (e0 + (unsigned long long)k) % (unsigned long long)P.evlog_cap);
-    }
-    __threadfence_system();  // every thread's record words before the flag
-    __syncthreads();
-    if (tid == 0) {
-        *(volatile unsigned long long*)&dst->done_seq = a.seq;
-        P.dbg[blockIdx.x * 16 + 8] = gtimer();  // (instrumentation: when the host could see it)
-    }
-}
 
 // One admission (the body of admit_kernel; the device-resident engine kernel runs it in a loop).
 // Every CTA of the cooperative grid calls it; a CTA returns when its part is done.
@@ -2787,6 +2760,7 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
     const ScanBufs B = scan_bufs(dsm);
     ReplaySmem& Rp = *reinterpret_cast<ReplaySmem*>(dsm + kOffRing);
     if (tid == 0) P.dbg[blockIdx.x * 16 + 9] = gtimer();  // kernel entry (instrumentation)
+    if (tid == 0 && blockIdx.x == 0) tstamp(P, a.seq, 1);
     const int par_prev = (int)((a.seq - 1ull) & 1ull), par_next = (int)(a.seq & 1ull);
     const bool pre_run = (a.flags & kPrescan) && gridDim.x > kStream0;
     // The host asks for the previous prescan's lists (kUsePrescan): the prescan CTAs start the
@@ -2893,16 +2867,23 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
             // one round: the overlay of the queued keys, the deferred EngineSim::unpin calls of
             // completed requests (engine.cpp:170-180) and, feeding a prescan consumer, the set U
             // of unpinned slots (this launch's and the previous launch's)
+            // The prompt's table finds run in this round too (their slots and keys kept on chip):
+            // a find never depends on the overlay or the unpins (a queued key is resolved from the
+            // overlay in the next round, and a find of any other key is exact while the queue is
+            // applied, see above), so the next round only reads the pins.
             long long dec = 0;
             const int nu = unpin_total(a, false);
             const int nuv = early ? unpin_total(a, true) : nu;
-            for (int q = tid; q < ne + ni + nuv; q += T) {
-                if (q < ne) {
-                    ov_put(ovk, ovs, P.tq_key[q], kOvErase);
-                } else if (q < ne + ni) {
-                    ov_put(ovk, ovs, P.tq_key[P.p_cap + (q - ne)], P.tq_slot[q - ne]);
-                } else {
-                    const int i = q - ne - ni;
+            const int nf = n <= kFindMax ? n : 0;
+            unsigned int* f_slot = reinterpret_cast<unsigned int*>(dsm + kOffRing + kFindOff);
+            unsigned long long* f_key = reinterpret_cast<unsigned long long*>(dsm + kOffRing + kFindOff + 4 * kFindMax);
+            for (int q = tid; q < nf + nuv + ne + ni; q += T) {
+                if (q < nf) {
+                    const unsigned long long key = a.keys[q];
+                    f_key[q] = key;
+                    f_slot[q] = table_find(P, key);
+                } else if (q < nf + nuv) {
+                    const int i = q - nf;
                     const unsigned int us = unpin_at(a, i);
                     if (us == kNoSlot) continue;
                     if (i < nu && atomicSub(&P.refs[us], 1u) == 1u) {
@@ -2911,6 +2892,11 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
                         if (P.dbg_unpin) P.dbg_unpin[us] = (a.seq << 8) | 1u;
                     }
                     if (early) xset_insert(S, us);
+                } else if (q < nf + nuv + ne) {
+                    ov_put(ovk, ovs, P.tq_key[q - nf - nuv], kOvErase);
+                } else {
+                    const int k = q - nf - nuv - ne;
+                    ov_put(ovk, ovs, P.tq_key[P.p_cap + k], P.tq_slot[k]);
                 }
             }
             dec = block_sum(dec, Red);  // (its barriers also publish the overlay)
@@ -2931,9 +2917,10 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
                     reused += table_insert(P, key, P.tq_slot[k]);
                 } else if (q < nq + n) {
                     const int i = q - nq;
-                    const unsigned long long key = a.keys[i];
+                    const unsigned long long key = nf ? f_key[i] : a.keys[i];
                     const unsigned int ov = ov_get(ovk, ovs, key);
-                    const unsigned int s = ov == kSlotEmpty ? table_find(P, key) : ov == kOvErase ? kNoSlot : (ov & kOvSlot);
+                    const unsigned int s = ov == kSlotEmpty ? (nf ? f_slot[i] : table_find(P, key))
+                                                            : ov == kOvErase ? kNoSlot : (ov & kOvSlot);
                     const unsigned int r0 = s == kNoSlot ? 0u : P.refs[s];
                     P.p_slot[i] = s;
                     P.p_refs0[i] = r0;
@@ -3058,6 +3045,7 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
         }
         stamp(A, 0);
         pstamp(P, 5);
+        if (tid == 0) tstamp(P, a.seq, 2);
     }
     if (tid == 0) {
         S.spec = 0;
@@ -3072,10 +3060,8 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
     bool pending_rescan = false;  // CTA 0: the last pass must be redone (safe, no hints)
     if (pre_avail) {
         if (blockIdx.x != 0) {
-            if (blockIdx.x == kSvcQ) {
+            if (blockIdx.x == kSvcQ)
                 service_queue(P, a, Red);
-                if (a.status) publish_early_status(P, a);
-            }
             else if (blockIdx.x == kSvcL)
                 service_lists(P, a, B, Sel, Red, dsm, par_prev);
             else if (blockIdx.x == kSvcB) {
@@ -3092,6 +3078,7 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
                     if (spins > (1ull << 28)) __trap();
                 }
                 P.dbg[blockIdx.x * 16 + 5] = gtimer();
+                if (blockIdx.x == kStream0) tstamp(P, a.seq, 6);
             }
             __syncthreads();
             run_loop = *(volatile int*)&C->verdict == 2;
@@ -3411,11 +3398,6 @@ __global__ void __launch_bounds__(kThreads + 32, 1) admit_kernel(DevPool P, Admi
 
 // ------------------------------------------------------------------ admission server
 
-__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
-    unsigned long long v;
-    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
 
 // One persistent cooperative launch serves every admission the host scheduler posts: CTA 0 polls
 // the host-mapped mailbox, relays the arguments (and, on the end-to-end path, copies the
@@ -3424,7 +3406,7 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned 
 // admit_kernel would. The host's scheduler loop is unchanged; what disappears per admission is
 // the cooperative launch itself and the host's enqueue behind the previous kernel.
 __global__ void __launch_bounds__(kThreads + 32, 1) server_kernel(DevPool P, SrvMailbox* mb, AdmitArgs* dargs,
-                                                                  unsigned long long seq0) {
+                                                                  unsigned long long post0) {
     extern __shared__ __align__(16) unsigned char dsm[];
     __shared__ ScanSmem S;
     __shared__ SelectSmem Sel;
@@ -3433,33 +3415,38 @@ __global__ void __launch_bounds__(kThreads + 32, 1) server_kernel(DevPool P, Srv
     __shared__ AdmitArgs a;
     const int tid = threadIdx.x, T = blockDim.x;
     constexpr int kWords = (int)(sizeof(AdmitArgs) / 4);
-    static_assert(sizeof(AdmitArgs) % 4 == 0, "AdmitArgs is relayed as 32-bit words");
-    unsigned long long t_exit = 0;  // (CTA 0, thread 0: when the previous admission's work ended)
-    for (unsigned long long seq = seq0;; ++seq) {
+    for (unsigned long long post = post0;; ++post) {
         if (blockIdx.x == 0) {
+            // the host posts within microseconds while its scheduler loop runs (a process that
+            // dies takes its context, and this kernel, with it). The first kArgWords threads poll
+            // the tagged pairs; one round that sees every tag == post carries the arguments too.
+            static_assert(kArgWords <= kThreads, "one tagged pair per polling thread");
+            unsigned long long spins = 0;
+            for (;;) {
+                int mine = 1;
+                unsigned long long w = 0;
+                if (tid < kArgWords) {
+                    unsigned long long t;
+                    asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];"
+                                 : "=l"(t), "=l"(w)
+                                 : "l"(&mb->pair[tid])
+                                 : "memory");
+                    mine = t == post ? 1 : 0;
+                }
+                if (__syncthreads_and(mine)) {
+                    if (tid < kArgWords) {
+                        reinterpret_cast<unsigned long long*>(&a)[tid] = w;
+                        reinterpret_cast<unsigned long long*>(dargs)[tid] = w;
+                    }
+                    break;
+                }
+                if (++spins > 64) __nanosleep(100);
+            }
+            __syncthreads();
             if (tid == 0) {
-                // the host posts within microseconds while its scheduler loop runs (a process
-                // that dies takes its context, and this kernel, with it)
-                unsigned long long spins = 0;
-                while (ld_acquire_sys_u64(&mb->seq) != seq)
-                    if (++spins > 256) __nanosleep(200);
                 A.srv_t0 = gtimer();
-                // instrumentation (tools/cta0_timeline.py): this pickup, the previous admission's
-                // CTA-0 end and its early status publication (CTA kSvcQ)
-                P.dbg[kSvcB * 16 + 10] = A.srv_t0;
-                P.dbg[kSvcB * 16 + 11] = t_exit;
-                P.dbg[kSvcB * 16 + 12] = P.dbg[kSvcQ * 16 + 8];
+                tstamp(P, a.seq, 0);
             }
-            __syncthreads();
-            const unsigned int* src = reinterpret_cast<const unsigned int*>(&mb->args);
-            unsigned int* d0 = reinterpret_cast<unsigned int*>(&a);
-            unsigned int* d1 = reinterpret_cast<unsigned int*>(dargs);
-            for (int i = tid; i < kWords; i += T) {
-                const unsigned int v = __ldcv(src + i);
-                d0[i] = v;
-                d1[i] = v;
-            }
-            __syncthreads();
             if (a.stage_src != nullptr && !(a.flags & kSrvStop)) {  // host -> device prompt blocks
                 const unsigned int* hs = reinterpret_cast<const unsigned int*>(a.stage_src);
                 unsigned int* dk = reinterpret_cast<unsigned int*>(const_cast<unsigned long long*>(a.keys));
@@ -3483,12 +3470,12 @@ __global__ void __launch_bounds__(kThreads + 32, 1) server_kernel(DevPool P, Srv
         }
         admit_body(P, a, dsm, S, Sel, Red, A);
         __syncthreads();
-        if (blockIdx.x == 0 && tid == 0) t_exit = gtimer();
+        if (blockIdx.x == 0 && tid == 0) tstamp(P, a.seq, 5);
         fence_proxy_async_smem();  // this admission's generic shared-memory use before the next TMA writes
     }
 }
 
-cudaError_t launch_server(const DevPool& P, SrvMailbox* mb_dev, AdmitArgs* args_dev, unsigned long long first_seq,
+cudaError_t launch_server(const DevPool& P, SrvMailbox* mb_dev, AdmitArgs* args_dev, unsigned long long first_post,
                           const LaunchCfg& lc, cudaStream_t s) {
     static bool attr = false;
     if (!attr) {
@@ -3499,7 +3486,7 @@ cudaError_t launch_server(const DevPool& P, SrvMailbox* mb_dev, AdmitArgs* args_
     DevPool p = P;
     SrvMailbox* m = mb_dev;
     AdmitArgs* d = args_dev;
-    unsigned long long q = first_seq;
+    unsigned long long q = first_post;
     void* args[] = {&p, &m, &d, &q};
     return cudaLaunchCooperativeKernel((const void*)server_kernel, dim3(lc.grid), dim3(lc.threads), args, lc.smem, s);
 }

@@ -89,9 +89,6 @@ struct Ctrl {
     unsigned long long verdict_seq;     // CTA 0 -> prescan CTAs: this launch's verdict is out
     int verdict;                        // 1: done, 2: everyone joins the command loop
     long long pre_used, pre_fallbacks, pre_badcnt;  // instrumentation
-    // CTA 0 -> CTA kSvcQ: this admission's final status record is in DevPool::st_early (and its
-    // victims in the eviction log); CTA kSvcQ publishes it to the host while CTA 0 applies
-    unsigned long long st_seq;
     unsigned long long svc_b_seq;  // CTA kSvcB -> CTA 0: LearnSpec / spec_hop are this admission's
 };
 
@@ -183,8 +180,6 @@ struct BelCtl {
     unsigned int hist[kBelPasses][256];
 };
 
-struct AdmitStatus;
-
 struct DevPool {
     long long cap;            // slots == EngineConfig::budget_blocks
     long long cap_scan;       // cap rounded up to 64: the SoA tail is padded with free slots
@@ -248,7 +243,6 @@ struct DevPool {
     unsigned int* tq_slot;
 
     Ctrl* ctrl;
-    AdmitStatus* st_early;  // device copy of an admission's status, published early (Ctrl::st_seq)
     LearnSpec* spec;        // the learner service's speculative observe (Ctrl::svc_b_seq)
     unsigned char* spec_hop;  // [a_cap] its BFS hops
 

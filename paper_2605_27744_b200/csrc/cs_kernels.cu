@@ -68,7 +68,6 @@ __global__ void init_pool_kernel(DevPool P) {
         C->p0_seq = 0ull;
         C->tq_erase = 0;
         C->tq_insert = 0;
-        C->st_seq = 0ull;
         C->svc_b_seq = 0ull;
     }
 }

@@ -98,12 +98,17 @@ struct AdmitArgs {
 };
 
 // The admission server's mailbox (server_kernel): pinned, host-mapped memory the host writes
-// and CTA 0 polls. The host writes args, then seq (x86 stores stay in order); CTA 0 waits for
-// seq == the admission it expects, then reads args.
+// and CTA 0 polls. Every 8-byte word of the arguments travels in a 16-byte pair with the post
+// number it belongs to: the host writes the word, then its tag (one cache line, x86 stores stay
+// in order); CTA 0 reads all pairs in one round of 16-byte loads (each one atomic over PCIe)
+// and accepts when every tag equals the post it waits for, so one PCIe round trip both detects
+// the post and delivers the arguments. Posts count admissions and stop commands alike.
+constexpr int kArgWords = (int)(sizeof(AdmitArgs) / 8);
+static_assert(sizeof(AdmitArgs) % 8 == 0, "AdmitArgs travels as 64-bit words");
 struct SrvMailbox {
-    unsigned long long seq;
-    unsigned long long pad[15];  // args start on their own 128-B line
-    AdmitArgs args;
+    struct Pair {
+        unsigned long long tag, word;
+    } pair[kArgWords];
 };
 
 struct LaunchCfg {
@@ -119,9 +124,9 @@ LaunchCfg admit_launch_config(const DevPool& P, int device, int want_grid);
 cudaError_t launch_admit(const DevPool& P, const AdmitArgs& a, const LaunchCfg& lc, int grid,
                          cudaStream_t s);
 // The admission server: ONE persistent cooperative launch that runs admit_body for every
-// admission the host posts in the mailbox (seq first_seq, first_seq + 1, ...) until a kSrvStop
-// post. args_dev (device) relays each admission's arguments from CTA 0 to the other CTAs.
-cudaError_t launch_server(const DevPool& P, SrvMailbox* mb_dev, AdmitArgs* args_dev, unsigned long long first_seq,
+// admission the host posts in the mailbox (posts first_post, first_post + 1, ...) until a
+// kSrvStop post. args_dev (device) relays each admission's arguments from CTA 0 to the other CTAs.
+cudaError_t launch_server(const DevPool& P, SrvMailbox* mb_dev, AdmitArgs* args_dev, unsigned long long first_post,
                           const LaunchCfg& lc, cudaStream_t s);
 
 // Belady admission (cs_belady.cuh): one cooperative launch per admission.

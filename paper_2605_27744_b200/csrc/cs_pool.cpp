@@ -159,7 +159,8 @@ void cs_pool::create(const cs_pool_cfg& c, long long shard_slots, cs_comm* cm) {
     p.gbuf_lt = dmalloc<unsigned long long>((size_t)csb::kMaxLists * p.gcap, "gbuf_lt");
     p.gbuf_slot = dmalloc<unsigned int>((size_t)csb::kMaxLists * p.gcap, "gbuf_slot");
     p.gmin = dmalloc<unsigned long long>((size_t)csb::kMaxLists * lc.grid, "gmin");
-    p.dbg = dmalloc<unsigned long long>((size_t)lc.grid * 16 + 192, "dbg");  // + CTA-0 stamps, debug records
+    // per-CTA rows + CTA-0 stamps + debug records + the admission server's trace ring (8 x 8)
+    p.dbg = dmalloc<unsigned long long>((size_t)lc.grid * 16 + 256, "dbg");
     if (const char* e = std::getenv("CS_DEBUG_PRESCAN")) p.dbg_check = std::atoi(e);
     if (p.dbg_check) {
         p.dbg_unpin = dmalloc<unsigned long long>(p.cap_scan, "dbg_unpin");
@@ -215,7 +216,6 @@ void cs_pool::create(const cs_pool_cfg& c, long long shard_slots, cs_comm* cm) {
     std::memset(mb, 0, sizeof(*mb));
     ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(&mb_dev), mb, 0), "cudaHostGetDevicePointer");
     d_srv_args = dmalloc<csb::AdmitArgs>(1, "server args");
-    P.st_early = dmalloc<csb::AdmitStatus>(1, "early status");
     P.spec = dmalloc<csb::LearnSpec>(1, "learner service");
     P.spec_hop = dmalloc<unsigned char>(P.a_cap, "learner service hops");
     if (const char* e = std::getenv("CS_SERVER")) server = std::atoi(e) != 0;
@@ -236,7 +236,7 @@ void cs_pool::destroy() {
                     p.sh_send1, p.sh_recv1, p.sh_send2, p.sh_recv2, p.sh_state, p.sh_gslot, p.sh_grefs0,
                     p.pl_lt, p.pl_slot, p.pl_agent, p.pl_ok, p.pl_key, p.pl_n, p.pl_T, p.pre_hint,
                     p.raw_lt, p.raw_slot, p.raw_list, p.raw_agent, p.raw_hdr,
-                    (void*)p.st_early, (void*)p.spec, p.spec_hop, p.bel_nu, p.bel_kid, p.bel_kid_slot, (void*)p.bel_ref, (void*)p.bel_ref_off, (void*)p.bel_depth,
+                    (void*)p.spec, p.spec_hop, p.bel_nu, p.bel_kid, p.bel_kid_slot, (void*)p.bel_ref, (void*)p.bel_ref_off, (void*)p.bel_depth,
                     (void*)p.bel_kid_of, p.bel_hi, p.bel_lo, p.bel_cand, p.bel_ctl};
     for (void* q : ptrs)
         if (q) cudaFree(q);
@@ -536,7 +536,7 @@ const csb::AdmitStatus& cs_pool::admit(const csb::AdmitArgs& in, int n_for_grid)
         if (srv_running && std::memcmp(&want, &srv_P, sizeof(want)) != 0) server_stop();
         if (!srv_running) {
             srv_P = want;
-            ck(csb::launch_server(srv_P, mb_dev, d_srv_args, a.seq, lc, stream), "server_kernel launch");
+            ck(csb::launch_server(srv_P, mb_dev, d_srv_args, srv_post + 1, lc, stream), "server_kernel launch");
             ++launches;
             ++server_launches;
             srv_running = true;
@@ -600,9 +600,17 @@ const csb::AdmitStatus& cs_pool::admit(const csb::AdmitArgs& in, int n_for_grid)
 }
 
 void cs_pool::server_post(const csb::AdmitArgs& a) {
-    std::memcpy(&mb->args, &a, sizeof(a));
-    std::atomic_thread_fence(std::memory_order_seq_cst);  // the arguments before the sequence number
-    *reinterpret_cast<volatile unsigned long long*>(&mb->seq) = a.seq;
+    // every word, then its tag, in the same 16-byte pair (csb::SrvMailbox): a device load that
+    // sees the new tag sees the new word
+    const unsigned long long tag = ++srv_post;
+    unsigned long long w[csb::kArgWords];
+    std::memcpy(w, &a, sizeof(a));
+    for (int i = 0; i < csb::kArgWords; ++i) {
+        volatile csb::SrvMailbox::Pair* p = &mb->pair[i];
+        p->word = w[i];
+        std::atomic_signal_fence(std::memory_order_release);  // (compiler order: word, then tag)
+        p->tag = tag;
+    }
 }
 
 void cs_pool::server_account(unsigned long long t_next) {
@@ -1189,7 +1197,7 @@ int cs_pool_debug(cs_pool_t pool, uint64_t* out, int cap, int* grid) {
     return guard([&] {
         if (!pool || !out) throw std::invalid_argument("cs_pool_debug: null argument");
         pool->sync();
-        const int n = std::min(cap, pool->lc.grid * 16 + 192);
+        const int n = std::min(cap, pool->lc.grid * 16 + 256);
         ck(cudaMemcpy(out, pool->P.dbg, 8 * (size_t)n, cudaMemcpyDeviceToHost), "dbg D2H");
         if (grid) *grid = pool->lc.grid;
     });

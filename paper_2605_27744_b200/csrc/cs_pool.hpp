@@ -173,6 +173,7 @@ struct cs_pool {
     csb::AdmitArgs* d_srv_args = nullptr;
     csb::DevPool srv_P{};
     long long server_launches = 0;
+    unsigned long long srv_post = 0;  // mailbox posts so far (admissions and stops)
     // per-admission device time from the server's pickup stamps: admission k's time is the
     // interval to admission k+1's pickup (the host's turnaround included)
     bool srv_have_t0 = false, srv_last_scan = false;

@@ -19,11 +19,11 @@ spec, seed = bench.rank_workload(40000, pool, 0)
 eng = bench.build_engine(W, spec, pool, 0, False, seed)
 eng.run_timed(int(sys.argv[1]) if len(sys.argv) > 1 else 100)
 rows = []
+dsub = []
 svc = []
 ends = []
-srv = []
 for it in range(40):
-    eng.run_timed(2)  # (the admission server: the second admission's pickup follows the first one)
+    eng.run_timed(1)
     buf = (C.c_uint64 * (16 * 1024))()
     grid = C.c_int(0)
     rc = lib().cs_pool_debug(lib().cs_engine_pool(eng.h), buf, 16 * 1024, C.byref(grid))
@@ -35,16 +35,32 @@ for it in range(40):
     rows.append((st - ent) / 1e3)
     per = d[:16 * g].reshape(g, 16)
     # service CTAs: 1 = table queue (start, done), 2 = list service (start, gathered, published)
+    dsub.append(((per[0, 10:16] - ent) / 1e3))
     svc.append([(per[1, 6] - ent) / 1e3, (per[1, 7] - ent) / 1e3, (per[2, 6] - ent) / 1e3, (per[2, 7] - ent) / 1e3,
                 (per[2, 8] - ent) / 1e3])
     # streaming CTAs 4..: start, stream end, writeout end (= verdict wait start), verdict seen
     ends.append([((per[4:, c] - ent) / 1e3).max() for c in (0, 1, 4, 5)])
-    # admission server (row 3): this pickup, the previous admission's CTA-0 end and its early
-    # status publication, relative to this pickup
-    pk = per[3, 10]
-    if pk > 0 and per[3, 11] > 0:
-        srv.append([(per[3, 11] - pk) / 1e3, (per[3, 12] - pk) / 1e3, (ent - pk) / 1e3])
+# the admission server's trace ring over runs of 8 consecutive admissions (one server launch)
+srv = []
+for it in range(10):
+    eng.run_timed(8)
+    buf = (C.c_uint64 * (16 * 1024))()
+    grid = C.c_int(0)
+    lib().cs_pool_debug(lib().cs_engine_pool(eng.h), buf, 16 * 1024, C.byref(grid))
+    g = grid.value
+    ring = np.array(buf[16 * g + 192:16 * g + 256], dtype=np.int64).reshape(8, 8)
+    order = np.argsort(ring[:, 0])
+    ring = ring[order]
+    for k in range(7):
+        a, b = ring[k], ring[k + 1]
+        if a[0] <= 0 or b[0] <= a[0]:
+            continue
+        srv.append([(a[1] - a[0]) / 1e3, (a[2] - a[0]) / 1e3, (a[3] - a[0]) / 1e3, (a[4] - a[0]) / 1e3,
+                    (a[5] - a[0]) / 1e3, (a[6] - a[0]) / 1e3, (b[0] - a[0]) / 1e3])
 r = np.median(np.array(rows), axis=0)
+ds = np.median(np.array(dsub), axis=0)
+print("replay_apply sub-phases (us from CTA 0 entry): start %.2f lists %.2f bulk decided %.2f prep %.2f victim keys %.2f end %.2f"
+      % tuple(ds))
 for k in [0, 1, 2, 3, 13, 14, 4, 5, 6, 7, 9, 10, 11, 12]:
     print(f"{NAMES[k]:>14}: {r[k]:8.2f} us")
 e = np.median(np.array(ends), axis=0)
@@ -54,7 +70,9 @@ print("service CTA 1 (table queue): start %.2f done %.2f us; CTA 2 (lists): star
       % tuple(sv))
 if srv:
     v = np.median(np.array(srv), axis=0)
-    print("server: previous admission's CTA 0 ended %.2f us and its status went out %.2f us before this pickup; "
-          "admit_body entry %.2f us after it" % (-v[0], -v[1], v[2]))
+    print("admission server, us after the pickup (median over %d consecutive pairs):" % len(srv))
+    for name, x in zip(["admit_body entry", "phase 0 end", "early status ready (CTA 0)", "status published (CTA 1)",
+                        "CTA 0 done", "streamers saw the verdict", "NEXT admission picked up"], v):
+        print("  %28s: %8.2f" % (name, x))
 res = eng.result()
 print("admit_ms per launch", res["admit_ms"] / max(res["admissions"], 1) * 1e3)
