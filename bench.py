@@ -382,6 +382,9 @@ def run_ours(args, dist):
                      "avg_launch_us": avg_scan_launch_s * 1e6, "algorithmic_bytes_per_launch": BYTES_PER_SLOT * pool},
         "clocks": clk.summary(),
         "phases_us_per_scan_launch": _phases(p0, p1, scan_launches),
+        "server": {"launches": ps1["server_launches"] - ps0["server_launches"],
+                   "host_turnaround_us": ((ps1["host_turnaround_ns"] - ps0["host_turnaround_ns"]) / 1e3 /
+                                          max(ps1["host_turnarounds"] - ps0["host_turnarounds"], 1))},
         "prescan": {"used": ps1["prescan_used"] - ps0["prescan_used"],
                     "fallbacks": ps1["prescan_fallbacks"] - ps0["prescan_fallbacks"],
                     "unusable": ps1["prescan_unusable"] - ps0["prescan_unusable"]},

@@ -188,6 +188,10 @@ typedef struct cs_pool_stats {
     /* admissions whose chunk 0 used the previous launch's prescan / fell back to a scan;
      * prescans that overflowed (unusable) */
     int64_t prescan_used, prescan_fallbacks, prescan_unusable;
+    /* admission server: launches, and the host's turnaround (status seen -> next admission
+     * posted) summed over the admissions that followed another one in the same launch */
+    int64_t server_launches, host_turnarounds;
+    uint64_t host_turnaround_ns;
 } cs_pool_stats;
 int cs_pool_get_stats(cs_pool_t pool, cs_pool_stats* out);
 /* Instrumentation: per-CTA scan timestamps of the last admission (grid x 8 u64). */

@@ -46,6 +46,7 @@ class PoolStats(C.Structure):
         ("tombstones", C.c_int64), ("scans", C.c_int64), ("scanned_slots", C.c_int64),
         ("rebuilds", C.c_uint64), ("n_agents", C.c_int), ("phase_ns", C.c_uint64 * 16),
         ("prescan_used", C.c_int64), ("prescan_fallbacks", C.c_int64), ("prescan_unusable", C.c_int64),
+        ("server_launches", C.c_int64), ("host_turnarounds", C.c_int64), ("host_turnaround_ns", C.c_uint64),
     ]
 
 

@@ -167,6 +167,8 @@ struct EarlySmem {
     unsigned long long U_lt[kXset];  // U re-read after the unpins, by xset position
     unsigned int U_agent[kXset];
     unsigned char U_ok[kXset];
+    unsigned short xl[kXset];  // the xset positions phase 0 filled (U), in insertion order
+    int xn;
     unsigned int tset[kTset];
     unsigned long long TE, TR, TP;
     int nE, nR, nP, ok, valid;
@@ -593,7 +595,7 @@ __device__ void commit_observe(const DevPool& P, const AdmitArgs& a, unsigned lo
         unsigned long long spins = 0;
         while (ld_acquire_u64(&C->svc_b_seq) != a.seq) {
             if (++spins > 4096) __nanosleep(64);
-            if (spins > (1ull << 28)) __trap();
+            if (spins > (1ull << 28)) trap_at(101);
         }
         sp = *P.spec;
     }
@@ -1000,6 +1002,18 @@ __device__ __forceinline__ bool xset_insert(ScanSmem& S, unsigned int s) {
     return false;  // unreachable: at most kXsetMax entries
 }
 
+// The same, returning the hash position of a newly inserted slot (-1: already present).
+__device__ __forceinline__ int xset_insert_pos(ScanSmem& S, unsigned int s) {
+    unsigned int h = xhash(s);
+    for (int c = 0; c < kXset; ++c) {
+        const unsigned int old = atomicCAS(&S.xset[h], kNoSlot, s);
+        if (old == kNoSlot) return (int)h;
+        if (old == s) return -1;
+        h = (h + 1) & (kXset - 1);
+    }
+    return -1;  // unreachable: at most kXsetMax entries
+}
+
 __device__ __forceinline__ bool xset_has(const ScanSmem& S, unsigned int s) {
     unsigned int h = xhash(s);
     for (int c = 0; c < kXset; ++c) {
@@ -1042,7 +1056,7 @@ __device__ void ensure_cls(const DevPool& P, const AdmitArgs& a, const ScanBufs&
             unsigned long long spins = 0;
             while (ld_acquire_u64(&P.ctrl->p0_seq) != a.seq) {
                 if (++spins > 1024) __nanosleep(128);
-                if (spins > (1ull << 27)) __trap();
+                if (spins > (1ull << 27)) trap_at(102);
             }
         }
         __syncthreads();
@@ -1107,7 +1121,7 @@ __device__ void producer_prep(const DevPool& P, const AdmitArgs& a, const ScanBu
         unsigned long long spins = 0;
         while (ld_acquire_u64(&P.ctrl->p0_seq) != a.seq) {
             if (++spins > 1024) __nanosleep(128);
-            if (spins > (1ull << 27)) __trap();
+            if (spins > (1ull << 27)) trap_at(103);
         }
     }
     __syncwarp();
@@ -1661,7 +1675,7 @@ __device__ void prescan_barrier(Ctrl* c) {
             unsigned long long spins = 0;
             while (ld_acquire(&c->pbar_gen) == gen) {
                 if (++spins > 4096) __nanosleep(64);
-                if (spins > (1ull << 27)) __trap();
+                if (spins > (1ull << 27)) trap_at(104);
             }
         }
         __threadfence();
@@ -1921,7 +1935,7 @@ __device__ bool consume_svc(const DevPool& P, const AdmitArgs& a, EarlySmem& es,
         unsigned long long spins = 0;
         while (ld_acquire_u64(&C->svc_l_seq) != a.seq) {
             if (++spins > 4096) __nanosleep(64);
-            if (spins > (1ull << 28)) __trap();
+            if (spins > (1ull << 28)) trap_at(105);
         }
         es.nE = __ldcg(P.pl_n + 0);
         es.nR = __ldcg(P.pl_n + 1);
@@ -1969,7 +1983,8 @@ __device__ bool consume_svc(const DevPool& P, const AdmitArgs& a, EarlySmem& es,
             S.lcnt[c] = 1;
         }
     };
-    for (int q = tid; q < nE + nR + nP + kXset; q += T) {
+    const int nU = es.xn;
+    for (int q = tid; q < nE + nR + nP + nU; q += T) {
         if (q < nE) {
             const unsigned int s = es.E_slot[q];
             ef[q] = (es.E_ok[q] && es.E_lt[q] <= TEs && !xset_has(S, s) && !tset_has(es.tset, s)) ? 1 : 0;
@@ -1983,9 +1998,9 @@ __device__ bool consume_svc(const DevPool& P, const AdmitArgs& a, EarlySmem& es,
             if (__ldcg(P.pl_ok + o) && !xset_has(S, s) && !tset_has(es.tset, s))
                 add_member(__ldcg(P.pl_lt + o), s, B.cls[__ldcg(P.pl_agent + j)]);
         } else {
-            const int j = q - nE - nR - nP;
+            const int j = es.xl[q - nE - nR - nP];
             const unsigned int s = S.xset[j];
-            if (s == kNoSlot || !es.U_ok[j] || tset_has(es.tset, s)) continue;
+            if (!es.U_ok[j] || tset_has(es.tset, s)) continue;
             const unsigned int ag = es.U_agent[j];
             add_member(es.U_lt[j], s, ag == kNoAgent ? E : B.cls[ag]);
         }
@@ -2198,7 +2213,7 @@ __device__ void queue_ready(const DevPool& P, const AdmitArgs& a, AdmSmem& A) {
         unsigned long long spins = 0;
         while (ld_acquire_u64(&C->svc_q_seq) != a.seq) {
             if (++spins > 4096) __nanosleep(64);
-            if (spins > (1ull << 28)) __trap();
+            if (spins > (1ull << 28)) trap_at(106);
         }
         C->tq_erase = 0;
         C->tq_insert = 0;
@@ -2209,6 +2224,39 @@ __device__ void queue_ready(const DevPool& P, const AdmitArgs& a, AdmSmem& A) {
 
 __device__ void fill_status(AdmitStatus* st, const DevPool& P, const AdmSmem& A, long long n_evicted,
                             long long resident, long long pinned, unsigned long long ev_total, long long tombstones);
+
+// The early status record (fill_status) written by one warp: lane 0 the scalars, the lanes the
+// phase timers and the pending warmups.
+__device__ void warp_fill_status(AdmitStatus* st, const DevPool& P, const AdmSmem& A, long long n_evicted,
+                                 long long resident, long long pinned, unsigned long long ev_total,
+                                 long long tombstones) {
+    Ctrl* C = P.ctrl;
+    const int lane = lane_id();
+    const int np = min(__ldcg(&C->n_pend), kMaxPending);
+    if (lane == 0) {
+        st->started = A.started;
+        st->error = A.error;
+        st->first_miss = A.first_miss;
+        st->admit_n = A.admit_n;
+        st->cached = A.cached;
+        st->n_evicted = n_evicted;
+        st->resident = resident;
+        st->pinned = pinned;
+        st->tick_after = A.tick;
+        st->ev_total = ev_total;
+        st->warm_issued = A.warm_issued;
+        st->needed = A.needed;
+        st->scans = A.scans;
+        st->tombstones = tombstones;
+        st->srv_t0 = A.srv_t0;
+        st->n_pend = np;
+    }
+    if (lane < kPhases) st->phase_ns[lane] = A.ph[lane];
+    for (int k = lane; k < np; k += 32) {
+        st->pend_target[k] = __ldcg(&C->pend_target[k]);
+        st->pend_tick[k] = __ldcg(&C->pend_tick[k]);
+    }
+}
 
 // early: only lists E and R are final (CTA 0 finalized E, CTA 1 signalled R); the other
 // lists are awaited only if the bulk test fails.
@@ -2327,7 +2375,7 @@ __device__ void replay_apply(const DevPool& P, const AdmitArgs& a, ReplaySmem& R
             unsigned long long spins = 0;
             while (ld_acquire(&C->fin_done) < (unsigned int)A.fin_want) {
                 if (++spins > 4096) __nanosleep(64);
-                if (spins > (1ull << 27)) __trap();
+                if (spins > (1ull << 27)) trap_at(107);
             }
             __threadfence();
         }
@@ -2555,9 +2603,8 @@ __device__ void replay_apply(const DevPool& P, const AdmitArgs& a, ReplaySmem& R
     if (early_st && warp_id() == (T >> 5) - 1) {  // (the apply below leaves it idle: len <= kChunk)
         const int lane = lane_id();
         tstamp(P, a.seq, 3);
-        if (lane == 0)
-            fill_status(a.status, P, A, A.n_ev_adm + nv, A.resident, A.pinned, ev0 + nv,
-                        C->tombstones + (long long)(q_e + nv));
+        warp_fill_status(a.status, P, A, A.n_ev_adm + nv, A.resident, A.pinned, ev0 + nv,
+                         C->tombstones + (long long)(q_e + nv));
         if (a.vict_host)
             for (int k = lane; k < nv && A.n_ev_adm + k < a.vict_cap; k += 32) a.vict_host[A.n_ev_adm + k] = R.vkey[k];
         __threadfence_system();  // each lane's record words and victims before the flag
@@ -2760,6 +2807,7 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
     const ScanBufs B = scan_bufs(dsm);
     ReplaySmem& Rp = *reinterpret_cast<ReplaySmem*>(dsm + kOffRing);
     if (tid == 0) P.dbg[blockIdx.x * 16 + 9] = gtimer();  // kernel entry (instrumentation)
+    progress(a.seq, 2);
     if (tid == 0 && blockIdx.x == 0) tstamp(P, a.seq, 1);
     const int par_prev = (int)((a.seq - 1ull) & 1ull), par_next = (int)(a.seq & 1ull);
     const bool pre_run = (a.flags & kPrescan) && gridDim.x > kStream0;
@@ -2858,10 +2906,18 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
             unsigned int* ovs = reinterpret_cast<unsigned int*>(dsm + kOffRing + 8 * kOv);
             for (int j = tid; j < kOv; j += T) ovs[j] = kSlotEmpty;
             const bool early = es.ok != 0;
+            // the class table for the consumer, stored on chip after the first round (its loads
+            // complete meanwhile instead of holding the barrier below)
+            unsigned char cls_r[kMaxAgents / kThreads + 1];
             if (early) {
                 for (int j = tid; j < kXset; j += T) S.xset[j] = kNoSlot;
                 for (int j = tid; j < kTset; j += T) es.tset[j] = kNoSlot;
-                for (int x = tid; x < a.n_agents; x += T) B.cls[x] = __ldcg(P.cls + x);
+#pragma unroll
+                for (int k = 0; k < kMaxAgents / kThreads + 1; ++k) {
+                    const int x = tid + k * T;
+                    cls_r[k] = x < a.n_agents ? __ldcg(P.cls + x) : (unsigned char)0;
+                }
+                if (tid == 0) es.xn = 0;
             }
             __syncthreads();
             // one round: the overlay of the queued keys, the deferred EngineSim::unpin calls of
@@ -2879,9 +2935,22 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
             unsigned long long* f_key = reinterpret_cast<unsigned long long*>(dsm + kOffRing + kFindOff + 4 * kFindMax);
             for (int q = tid; q < nf + nuv + ne + ni; q += T) {
                 if (q < nf) {
+                    const unsigned long long t0 = P.dbg_warps ? gtimer() : 0ull;
                     const unsigned long long key = a.keys[q];
                     f_key[q] = key;
-                    f_slot[q] = table_find(P, key);
+                    const unsigned long long t1 = P.dbg_warps ? (key != 0ull ? gtimer() : 0ull) : 0ull;
+                    f_slot[q] = table_find_line(P, key);
+                    if (P.dbg_warps && (q & 31) == 0 && q < 96) {  // (instrumentation: lane 0 of warps 0-2)
+                        const unsigned long long t2 = f_slot[q] != 0xFFFFFFFEu ? gtimer() : 0ull;
+                        unsigned long long* o = P.dbg + (size_t)gridDim.x * 16 + 100 + (q >> 5) * 4;
+                        o[0] = t0;
+                        o[1] = t1;
+                        o[2] = t2;
+                        const unsigned long long h = table_home(key, P.tmask);
+                        unsigned long long n = 0;
+                        while (n < 4096 && P.table[(h + n) & P.tmask].key != key && P.table[(h + n) & P.tmask].slot != kSlotEmpty) ++n;
+                        o[3] = (n << 32) | (f_slot[q] == kNoSlot ? 1ull : 0ull);
+                    }
                 } else if (q < nf + nuv) {
                     const int i = q - nf;
                     const unsigned int us = unpin_at(a, i);
@@ -2891,7 +2960,10 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
                         ++dec;
                         if (P.dbg_unpin) P.dbg_unpin[us] = (a.seq << 8) | 1u;
                     }
-                    if (early) xset_insert(S, us);
+                    if (early) {
+                        const int pos = xset_insert_pos(S, us);
+                        if (pos >= 0) es.xl[atomicAdd(&es.xn, 1)] = (unsigned short)pos;
+                    }
                 } else if (q < nf + nuv + ne) {
                     ov_put(ovk, ovs, P.tq_key[q - nf - nuv], kOvErase);
                 } else {
@@ -2899,12 +2971,20 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
                     ov_put(ovk, ovs, P.tq_key[P.p_cap + k], P.tq_slot[k]);
                 }
             }
-            dec = block_sum(dec, Red);  // (its barriers also publish the overlay)
+            if (P.dbg_warps && lane_id() == 0) P.dbg[(size_t)gridDim.x * 16 + 48 + warp_id()] = gtimer();
+            if (early) {
+#pragma unroll
+                for (int k = 0; k < kMaxAgents / kThreads + 1; ++k) {
+                    const int x = tid + k * T;
+                    if (x < a.n_agents) B.cls[x] = cls_r[k];
+                }
+            }
+            dec = block_sum(dec, Red);  // (its barriers also publish the overlay and the U list)
             if (tid == 0) C->pinned -= dec;
             pstamp(P, 1);
             pf_issue2();
             long long reused = 0;
-            const int nxs = early ? kXset : 0;
+            const int nxs = early ? es.xn : 0;  // U: one entry per distinct unpinned slot
             const int nq = deleg ? 0 : ne + ni;  // queued table updates this CTA applies
             for (int q = tid; q < nq + n + nxs; q += T) {
                 if (q < nq && q < ne) {
@@ -2927,15 +3007,15 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
                     if (s == kNoSlot && i < miss_min) miss_min = i;
                     if (s == kNoSlot || r0 == 0u) ++need;
                 } else {  // U re-read, after every unpin of this launch
-                    const int j = q - nq - n;
+                    const int j = es.xl[q - nq - n];
                     const unsigned int us = S.xset[j];
-                    if (us == kNoSlot) continue;
                     const unsigned long long x = __ldcg(P.lt + us);
                     es.U_lt[j] = x;
                     es.U_agent[j] = __ldcg(P.agent + us);
                     es.U_ok[j] = (x != kFreeTick && __ldcg(P.refs + us) == 0u) ? 1 : 0;
                 }
             }
+            if (P.dbg_warps && lane_id() == 0) P.dbg[(size_t)gridDim.x * 16 + 48 + 24 + warp_id()] = gtimer();
             reused = block_sum(reused, Red);
             if (tid == 0 && !deleg) {
                 C->tombstones += (long long)ne - reused;
@@ -3068,20 +3148,32 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
                 if ((a.flags & kDispatch) && P.policy == 1 && a.next >= 0 && __ldcg(&C->win_size) <= kBfsPre)
                     service_learner(P, a, dsm, Red);
             }
-            else
+            else {
+                if (P.dbg_warps > 1) {  // experiment (CS_DEBUG_WARPS=us): start the stream later
+                    const unsigned long long t = gtimer();
+                    while (gtimer() - t < 1000ull * (unsigned long long)P.dbg_warps) __nanosleep(500);
+                }
                 prescan_pass(P, B, S, dsm, par_next, P.stream_generic != 0, a.seq);
+            }
+            // The verdict word is (seq << 2) | verdict. A later admission's verdict means this
+            // one's was "done": a "join the command loop" verdict holds CTA 0 in this admission
+            // until every CTA joined (the admission server lets CTA 0 run ahead otherwise).
+            __shared__ int join;
+            progress(a.seq, 4);
             if (tid == 0) {
                 P.dbg[blockIdx.x * 16 + 4] = gtimer();
-                unsigned long long spins = 0;
-                while (ld_acquire_u64(&C->verdict_seq) != a.seq) {
+                unsigned long long spins = 0, w;
+                while (((w = ld_acquire_u64(&C->verdict_w)) >> 2) < a.seq) {
                     if (++spins > 4096) __nanosleep(128);
-                    if (spins > (1ull << 28)) __trap();
+                    if (spins > (1ull << 28)) trap_at(108);
                 }
+                join = (w >> 2) == a.seq && (w & 3ull) == 2ull ? 1 : 0;
                 P.dbg[blockIdx.x * 16 + 5] = gtimer();
                 if (blockIdx.x == kStream0) tstamp(P, a.seq, 6);
             }
             __syncthreads();
-            run_loop = *(volatile int*)&C->verdict == 2;
+            run_loop = join != 0;
+            progress(a.seq, run_loop ? 6 : 5);
             if (!run_loop) return;
         } else {
             if (tid == 0) {  // this launch's scoring pass is the prescan
@@ -3116,9 +3208,9 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
                 need_loop = A.chunk * kChunk < A.admit_n;
             }
             if (tid == 0) {
-                C->verdict = need_loop ? 2 : 1;
+                const unsigned long long w = (a.seq << 2) | (need_loop ? 2ull : 1ull);
                 __threadfence();
-                asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(&C->verdict_seq), "l"(a.seq) : "memory");
+                asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(&C->verdict_w), "l"(w) : "memory");
             }
             run_loop = need_loop;
         }
@@ -3186,7 +3278,7 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
                 unsigned long long spins = 0;
                 while (ld_acquire_u64(&C->r_seq) != a.seq) {
                     if (++spins > 4096) __nanosleep(64);
-                    if (spins > (1ull << 27)) __trap();
+                    if (spins > (1ull << 27)) trap_at(109);
                 }
                 __threadfence();
                 A.ph[15] += gtimer() - tw;  // instrumentation: CTA 0 waiting for the resident list
@@ -3207,7 +3299,7 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
                 unsigned long long spins = 0;
                 while (ld_acquire(&C->fin_done) < (unsigned int)A.fin_want) {
                     if (++spins > 4096) __nanosleep(64);
-                    if (spins > (1ull << 27)) __trap();
+                    if (spins > (1ull << 27)) trap_at(110);
                 }
             }
             __syncthreads();
@@ -3219,6 +3311,7 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
     // ---- command loop. CTA 0 decides the next step (scan pass of a chunk, or done); every CTA
     // scans; CTAs 0..NL-1 select one list each; only CTA 0 consumes the lists, so it waits on
     // a counter instead of a grid barrier; CTA 0 replays. Per chunk: 2 grid barriers.
+    const bool looped = run_loop;
     for (; run_loop;) {
         if (blockIdx.x == 0) {
             const bool stop = !A.started || A.error || A.chunk * kChunk >= A.admit_n;
@@ -3305,7 +3398,7 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
                     unsigned long long spins = 0;
                     while (ld_acquire(&C->fin_done) < want) {
                         if (++spins > 4096) __nanosleep(64);
-                        if (spins > (1ull << 27)) __trap();
+                        if (spins > (1ull << 27)) trap_at(111);
                     }
                     __threadfence();
                 }
@@ -3322,6 +3415,9 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
             stamp(A, 4);
         }
     }
+    // Every CTA has read C->done before CTA 0 can reset the loop's control words: in the admission
+    // server CTA 0 starts the next admission (its phase 0 resets them) without a grid barrier.
+    if (looped) grid_barrier(C);
 
     // ---- no usable prescan came in: CTAs kStream0.. now prescan for the next admission
     if (pre_run && !pre_avail && blockIdx.x != 0) {
@@ -3414,33 +3510,36 @@ __global__ void __launch_bounds__(kThreads + 32, 1) server_kernel(DevPool P, Srv
     __shared__ AdmSmem A;
     __shared__ AdmitArgs a;
     const int tid = threadIdx.x, T = blockDim.x;
-    constexpr int kWords = (int)(sizeof(AdmitArgs) / 4);
+    Ctrl* C = P.ctrl;
     for (unsigned long long post = post0;; ++post) {
+        AdmitArgs* dslot = dargs + (post & 1ull);  // (double-buffered: never rewritten while read)
         if (blockIdx.x == 0) {
             // the host posts within microseconds while its scheduler loop runs (a process that
             // dies takes its context, and this kernel, with it). The first kArgWords threads poll
-            // the tagged pairs; one round that sees every tag == post carries the arguments too.
+            // the tagged pairs: one round that sees every tag == post carries the arguments too.
             static_assert(kArgWords <= kThreads, "one tagged pair per polling thread");
-            unsigned long long spins = 0;
-            for (;;) {
-                int mine = 1;
-                unsigned long long w = 0;
-                if (tid < kArgWords) {
-                    unsigned long long t;
-                    asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];"
-                                 : "=l"(t), "=l"(w)
-                                 : "l"(&mb->pair[tid])
-                                 : "memory");
-                    mine = t == post ? 1 : 0;
-                }
-                if (__syncthreads_and(mine)) {
+            {
+                unsigned long long spins = 0;
+                for (;;) {
+                    int mine = 1;
+                    unsigned long long w = 0;
                     if (tid < kArgWords) {
-                        reinterpret_cast<unsigned long long*>(&a)[tid] = w;
-                        reinterpret_cast<unsigned long long*>(dargs)[tid] = w;
+                        unsigned long long t;
+                        asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];"
+                                     : "=l"(t), "=l"(w)
+                                     : "l"(&mb->pair[tid])
+                                     : "memory");
+                        mine = t == post ? 1 : 0;
                     }
-                    break;
+                    if (__syncthreads_and(mine)) {
+                        if (tid < kArgWords) {
+                            reinterpret_cast<unsigned long long*>(&a)[tid] = w;
+                            reinterpret_cast<unsigned long long*>(dslot)[tid] = w;
+                        }
+                        break;
+                    }
+                    if (++spins > 64) __nanosleep(100);
                 }
-                if (++spins > 64) __nanosleep(100);
             }
             __syncthreads();
             if (tid == 0) {
@@ -3452,12 +3551,26 @@ __global__ void __launch_bounds__(kThreads + 32, 1) server_kernel(DevPool P, Srv
                 unsigned int* dk = reinterpret_cast<unsigned int*>(const_cast<unsigned long long*>(a.keys));
                 for (int i = tid; i < 3 * a.n; i += T) dk[i] = __ldcv(hs + i);
             }
-        }
-        grid_barrier(P.ctrl);  // publishes dargs and the staged blocks; orders the last admission
-        if (blockIdx.x != 0) {
-            unsigned int* d0 = reinterpret_cast<unsigned int*>(&a);
-            const unsigned int* d1 = reinterpret_cast<const unsigned int*>(dargs);
-            for (int i = tid; i < kWords; i += T) d0[i] = __ldcg(d1 + i);
+            // hand the admission to the other CTAs without waiting for them: they finished the
+            // previous one among themselves (prescan_barrier below), and everything CTA 0 wrote
+            // in it is ordered before this release
+            __syncthreads();
+            if (tid == 0) {
+                __threadfence();
+                asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(&C->srv_go), "l"(post) : "memory");
+            }
+        } else {
+            progress(post, 9);
+            prescan_barrier(C);  // CTAs 1..: every one of them finished the previous admission
+            progress(post, 10);
+            if (tid == 0) {
+                unsigned long long spins = 0;
+                while (ld_acquire_u64(&C->srv_go) != post)
+                    if (++spins > 64) __nanosleep(100);
+            }
+            __syncthreads();
+            for (int i = tid; i < kArgWords; i += T)
+                reinterpret_cast<unsigned long long*>(&a)[i] = __ldcg(reinterpret_cast<const unsigned long long*>(dslot) + i);
             __syncthreads();
         }
         if (a.flags & kSrvStop) {
@@ -3492,6 +3605,12 @@ cudaError_t launch_server(const DevPool& P, SrvMailbox* mb_dev, AdmitArgs* args_
 }
 
 // ------------------------------------------------------------------ host side
+
+cudaError_t set_trap_word(unsigned long long* host_mapped, int progress_on) {
+    const cudaError_t e = cudaMemcpyToSymbol(cs_trap_host, &host_mapped, sizeof(host_mapped));
+    if (e != cudaSuccess) return e;
+    return cudaMemcpyToSymbol(cs_progress_on, &progress_on, sizeof(progress_on));
+}
 
 LaunchCfg admit_launch_config(const DevPool& P, int device, int want_grid) {
     LaunchCfg lc{0, 0, 0, 0};

@@ -86,10 +86,12 @@ struct Ctrl {
     // service CTAs of a pipelined launch -> CTA 0 (AdmitArgs::seq, release/acquire):
     unsigned long long svc_q_seq;       // CTA kSvcQ applied the previous admission's table queue
     unsigned long long svc_l_seq;       // CTA kSvcL published the validated prescan lists
-    unsigned long long verdict_seq;     // CTA 0 -> prescan CTAs: this launch's verdict is out
-    int verdict;                        // 1: done, 2: everyone joins the command loop
+    // CTA 0 -> prescan CTAs: (AdmitArgs::seq << 2) | verdict (1: done, 2: everyone joins the
+    // command loop), one word so a reader never pairs one admission's seq with another's verdict
+    unsigned long long verdict_w;
     long long pre_used, pre_fallbacks, pre_badcnt;  // instrumentation
     unsigned long long svc_b_seq;  // CTA kSvcB -> CTA 0: LearnSpec / spec_hop are this admission's
+    unsigned long long srv_go;     // admission server: CTA 0 -> CTAs 1..: the arguments of this post
 };
 
 // prescan list lengths: E (agentless unpinned) and R (resident) keep the kPreK oldest; the
@@ -232,6 +234,7 @@ struct DevPool {
     int* fin_n;
 
     unsigned long long* dbg;      // [grid * 8] per-CTA instrumentation timestamps
+    int dbg_warps;                // CS_DEBUG_WARPS: CTA 0's per-warp phase-0 round ends (tools)
 
     // per-admission prompt scratch (grown by the host)
     unsigned int* p_slot;
@@ -322,6 +325,24 @@ __host__ __device__ __forceinline__ void pk_decode(unsigned long long w, unsigne
 }
 
 #ifdef __CUDACC__
+// A watchdog that fires (a wait that never ends, a corrupted table) records where before it
+// traps: the site code and CTA go to host-mapped memory (cs_trap_word), which outlives the
+// context the trap takes down, so the host can name the site in its error.
+static __device__ unsigned long long* cs_trap_host;  // (per translation unit; set for cs_admit.cu)
+static __device__ int cs_progress_on;  // CS_DEBUG_PROGRESS: per-CTA progress marks in cs_trap_host[1 + cta]
+__device__ __forceinline__ void progress(unsigned long long seq, int stage) {
+    if (cs_progress_on && threadIdx.x == 0)
+        *(volatile unsigned long long*)(cs_trap_host + 1 + blockIdx.x) = (seq << 8) | (unsigned long long)stage;
+}
+static __device__ __noinline__ void trap_at(int code) {
+    unsigned long long* w = cs_trap_host;
+    if (w) {
+        *(volatile unsigned long long*)w = ((unsigned long long)code << 32) | (unsigned long long)blockIdx.x;
+        __threadfence_system();
+    }
+    __trap();
+}
+
 // ---------------------------------------------------------------- block table
 
 __device__ __forceinline__ unsigned long long table_home(unsigned long long key, unsigned long long mask) {
@@ -340,7 +361,34 @@ __device__ __forceinline__ unsigned int table_find(const DevPool& P, unsigned lo
         if (e.slot < kSlotClaim && e.key == key) return e.slot;
         h = (h + 1) & P.tmask;
     }
-    __trap();
+    trap_at(201);
+    return kNoSlot;
+}
+
+// The same answer with one round trip per 128-byte line instead of per entry, for the
+// latency-critical probe of an admission (phase 0): all entries of the line from h on are loaded
+// together (L2-coherent 16-byte loads, each an atomic {key, slot} pair) and scanned in probe
+// order. Entries may change while they are read (the block-table queue is applied concurrently,
+// csrc/cs_admit.cu phase 0); a find of a key the queue does not touch is exact under any
+// interleaving (the key's entry precedes every EMPTY on its path and is never moved), and queued
+// keys are resolved by the caller's overlay.
+__device__ __forceinline__ unsigned int table_find_line(const DevPool& P, unsigned long long key) {
+    unsigned long long h = table_home(key, P.tmask);
+    for (unsigned long long n = 0; n <= P.tmask; n += 8) {
+        const unsigned long long base = h & ~7ull;
+        ulonglong2 e[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) e[k] = __ldcg(reinterpret_cast<const ulonglong2*>(P.table + base + k));
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            if (base + k < h) continue;
+            const unsigned int slot = (unsigned int)e[k].y;
+            if (slot == kSlotEmpty) return kNoSlot;
+            if (slot < kSlotClaim && e[k].x == key) return slot;
+        }
+        h = (base + 8) & P.tmask;
+    }
+    trap_at(202);
     return kNoSlot;
 }
 
@@ -366,7 +414,7 @@ __device__ __forceinline__ int table_insert(const DevPool& P, unsigned long long
         }
         h = (h + 1) & P.tmask;
     }
-    __trap();
+    trap_at(203);
     return 0;
 }
 
@@ -386,7 +434,7 @@ __device__ __forceinline__ void table_erase(const DevPool& P, unsigned long long
         }
         h = (h + 1) & P.tmask;
     }
-    __trap();
+    trap_at(204);
 }
 
 __device__ __forceinline__ void pk_unpinned(const DevPool& P, unsigned int s) { atomicAnd(P.pk + s, ~kPkPin); }
@@ -454,7 +502,7 @@ __device__ __forceinline__ void grid_barrier(Ctrl* c) {
             unsigned long long spins = 0;
             while (ld_acquire(&c->bar_gen) == gen) {
                 if (++spins > 4096) __nanosleep(64);  // hot spin first: barriers are short
-                if (spins > (1ull << 27)) __trap();
+                if (spins > (1ull << 27)) trap_at(205);
             }
         }
         __threadfence();

@@ -195,7 +195,8 @@ struct cs_engine {
     unsigned char* h_blob = nullptr;
     unsigned long long* h_vict = nullptr;
     int h_vict_cap = 0;
-    csb::DevBuf d_stage_keys, d_stage_counts;
+    csb::DevBuf d_stage_keys, d_stage_keys2, d_stage_counts;
+    bool stage_flip = false;
     int64_t h2d_bytes = 0, d2h_bytes = 0;
     void stage(csb::AdmitArgs& a, int64_t blk_off, int nb);
     void fetch_victims(unsigned long long before);
@@ -472,6 +473,7 @@ void cs_engine::build(const cs_engine_cfg& c, const cs_workload_spec* ws, long l
         h_vict_cap = max_nb;
         ck(cudaMallocHost(reinterpret_cast<void**>(&h_vict), 8 * (size_t)h_vict_cap), "cudaMallocHost");
         d_stage_keys.ensure(12 * (size_t)max_nb);  // sized once: no allocation inside the engine loop
+        d_stage_keys2.ensure(12 * (size_t)max_nb);
         pool->ensure_prompt_scratch(max_nb);
         d_keys.release();
         d_counts.release();
@@ -666,8 +668,11 @@ void cs_engine::dev_pull_outputs() {
 }
 
 void cs_engine::drain_evictions(bool force) {
-    const unsigned long long tot = pool->ev_total;
-    if (tot == ev_drained) return;
+    // a forced drain follows a sync (every entry is in the log); inside the engine loop the last
+    // admission's entries may still be being written (its status goes out before its apply)
+    if (force) pool->sync();
+    const unsigned long long tot = force ? pool->ev_total : pool->ev_safe;
+    if (tot <= ev_drained) return;
     if (!force && tot - ev_drained < (unsigned long long)pool->P.evlog_cap / 2) return;
     const size_t base = evictions.size();
     evictions.resize(base + (tot - ev_drained));
@@ -681,20 +686,23 @@ void cs_engine::stage(csb::AdmitArgs& a, int64_t blk_off, int nb) {
         a.counts = d_counts.as<int>() + blk_off;
         return;
     }
-    if (12 * (size_t)std::max(nb, 1) > d_stage_keys.n) pool->server_stop();  // (never while it runs)
-    d_stage_keys.ensure(12 * (size_t)std::max(nb, 1));
-    if (pool->uses_server()) {  // the admission server's CTA 0 reads them from pinned host memory
+    // the admission server may copy the next admission's blocks while this one is still being
+    // applied (its look-ahead fetch): consecutive admissions alternate between two buffers
+    const bool srv = pool->uses_server();
+    csb::DevBuf& buf = (srv && (stage_flip = !stage_flip)) ? d_stage_keys2 : d_stage_keys;
+    if (12 * (size_t)std::max(nb, 1) > buf.n) pool->server_stop();  // (never while it runs)
+    buf.ensure(12 * (size_t)std::max(nb, 1));
+    if (srv) {  // the admission server's CTA 0 reads them from pinned host memory
         unsigned char* dp = nullptr;
         ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dp), h_blob, 0), "cudaHostGetDevicePointer(prompts)");
         a.stage_src = dp + 12 * blk_off;
     } else {
-        ck(cudaMemcpyAsync(d_stage_keys.p, h_blob + 12 * blk_off, 12 * (size_t)nb, cudaMemcpyHostToDevice,
-                           pool->stream),
+        ck(cudaMemcpyAsync(buf.p, h_blob + 12 * blk_off, 12 * (size_t)nb, cudaMemcpyHostToDevice, pool->stream),
            "H2D");
     }
     h2d_bytes += 12 * (int64_t)nb;
-    a.keys = d_stage_keys.as<unsigned long long>();
-    a.counts = reinterpret_cast<int*>(d_stage_keys.as<unsigned char>() + 8 * (size_t)nb);
+    a.keys = buf.as<unsigned long long>();
+    a.counts = reinterpret_cast<int*>(buf.as<unsigned char>() + 8 * (size_t)nb);
     // the victims (at most one per prompt block) come back behind the kernel, same stream
     pool->vpref = h_vict;
     pool->vpref_n = nb;
@@ -713,7 +721,8 @@ void cs_engine::fetch_victims(unsigned long long before) {
         evictions.resize(base + n);
         if (ev_drained == before && n <= (unsigned long long)pool->vpref_done) {
             std::memcpy(evictions.data() + base, h_vict, 8 * n);
-        } else {  // (not this admission's window alone: read the log)
+        } else {  // (not this admission's window alone: read the log, once it is all written)
+            pool->sync();
             pool->copy_victims(ev_drained, tot, evictions.data() + base);
             d2h_bytes += 8 * (int64_t)n;
         }
@@ -988,6 +997,7 @@ int cs_engine_destroy(cs_engine_t e) {
         e->d_counts.release();
         e->d_pins.release();
         e->d_stage_keys.release();
+        e->d_stage_keys2.release();
         e->d_stage_counts.release();
         if (e->h_keys) cudaFreeHost(e->h_keys);
         if (e->h_blob) cudaFreeHost(e->h_blob);

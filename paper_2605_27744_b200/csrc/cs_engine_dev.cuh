@@ -334,7 +334,10 @@ __global__ void __launch_bounds__(kThreads + 32, 1) engine_kernel(DevPool P, Eng
     // dynamic shared memory); CTA 0 stages it on chip, in the TMA ring, around each decision.
     EngState& es = *reinterpret_cast<EngState*>(dsm + kOffRing);
     static_assert(sizeof(EngState) <= kRing * kRingStage, "scheduler state must fit the TMA ring");
-    if (blockIdx.x == 0 && tid == 0) steps0 = E.st->steps;
+    if (blockIdx.x == 0 && tid == 0) {
+        steps0 = E.st->steps;
+        A.srv_t0 = 0;
+    }
     bool have_last = false;
     for (;;) {
         if (blockIdx.x == 0) {

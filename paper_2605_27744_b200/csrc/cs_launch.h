@@ -126,6 +126,8 @@ cudaError_t launch_admit(const DevPool& P, const AdmitArgs& a, const LaunchCfg& 
 // The admission server: ONE persistent cooperative launch that runs admit_body for every
 // admission the host posts in the mailbox (posts first_post, first_post + 1, ...) until a
 // kSrvStop post. args_dev (device) relays each admission's arguments from CTA 0 to the other CTAs.
+// Where a device watchdog records its site before it traps (host-mapped u64; see trap_at).
+cudaError_t set_trap_word(unsigned long long* host_mapped, int progress_on);
 cudaError_t launch_server(const DevPool& P, SrvMailbox* mb_dev, AdmitArgs* args_dev, unsigned long long first_post,
                           const LaunchCfg& lc, cudaStream_t s);
 

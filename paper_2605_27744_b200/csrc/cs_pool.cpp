@@ -2,6 +2,7 @@
 #include "cs_pool.hpp"
 
 #include <atomic>
+#include <chrono>
 
 #include <algorithm>
 #include <cstddef>
@@ -162,6 +163,7 @@ void cs_pool::create(const cs_pool_cfg& c, long long shard_slots, cs_comm* cm) {
     // per-CTA rows + CTA-0 stamps + debug records + the admission server's trace ring (8 x 8)
     p.dbg = dmalloc<unsigned long long>((size_t)lc.grid * 16 + 256, "dbg");
     if (const char* e = std::getenv("CS_DEBUG_PRESCAN")) p.dbg_check = std::atoi(e);
+    if (const char* e = std::getenv("CS_DEBUG_WARPS")) p.dbg_warps = std::atoi(e);
     if (p.dbg_check) {
         p.dbg_unpin = dmalloc<unsigned long long>(p.cap_scan, "dbg_unpin");
         ck(cudaMemset(p.dbg_unpin, 0, 8 * p.cap_scan), "memset");
@@ -189,7 +191,7 @@ void cs_pool::create(const cs_pool_cfg& c, long long shard_slots, cs_comm* cm) {
                                          csb::kNoBound, csb::kNoBound, csb::kNoBound};
         ck(cudaMemcpy(p.pre_hint, h, sizeof(h), cudaMemcpyHostToDevice), "pre_hint");
     }
-    ck(cudaMemsetAsync(p.dbg, 0, sizeof(unsigned long long) * (lc.grid * 16 + 192), stream), "memset");
+    ck(cudaMemsetAsync(p.dbg, 0, sizeof(unsigned long long) * (lc.grid * 16 + 256), stream), "memset");
 
     if (comm) {
         p.sh_send2 = dmalloc<csb::ShardLists>(1, "sh_send2");
@@ -215,7 +217,20 @@ void cs_pool::create(const cs_pool_cfg& c, long long shard_slots, cs_comm* cm) {
     ck(cudaHostAlloc(reinterpret_cast<void**>(&mb), sizeof(csb::SrvMailbox), cudaHostAllocMapped), "cudaHostAlloc");
     std::memset(mb, 0, sizeof(*mb));
     ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(&mb_dev), mb, 0), "cudaHostGetDevicePointer");
-    d_srv_args = dmalloc<csb::AdmitArgs>(1, "server args");
+    d_srv_args = dmalloc<csb::AdmitArgs>(2, "server args");  // (double-buffered by post parity)
+    {  // the device watchdogs' trap site (one per process, host-mapped)
+        static unsigned long long* trap_word = nullptr;
+        if (!trap_word) {
+            ck(cudaHostAlloc(reinterpret_cast<void**>(&trap_word), 8 * 4096, cudaHostAllocMapped | cudaHostAllocPortable),
+               "cudaHostAlloc(trap word)");
+            std::memset(trap_word, 0, 8 * 4096);
+            unsigned long long* dp = nullptr;
+            ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dp), trap_word, 0), "cudaHostGetDevicePointer");
+            const char* pe = std::getenv("CS_DEBUG_PROGRESS");
+            ck(csb::set_trap_word(dp, pe ? std::atoi(pe) : 0), "set_trap_word");
+        }
+        trap_word_host = trap_word;
+    }
     P.spec = dmalloc<csb::LearnSpec>(1, "learner service");
     P.spec_hop = dmalloc<unsigned char>(P.a_cap, "learner service hops");
     if (const char* e = std::getenv("CS_SERVER")) server = std::atoi(e) != 0;
@@ -367,6 +382,7 @@ const csb::AdmitStatus& cs_pool::admit_sharded_once(const csb::AdmitArgs& in) {
     if (st->started < 0) throw CsError(CS_ERR_CUDA, "shard kernels did not report a status");
     resident = st->resident;
     pinned = st->pinned;
+    ev_safe = ev_total;  // (this admission's own log entries may still be in flight: early status)
     ev_total = st->ev_total;
     pending_targets.assign(st->pend_target, st->pend_target + std::min(st->n_pend, csb::kMaxPending));
     pending_ticks.assign(st->pend_tick, st->pend_tick + std::min(st->n_pend, csb::kMaxPending));
@@ -457,6 +473,7 @@ const csb::AdmitStatus& cs_pool::admit_belady(const csb::AdmitArgs& in, int n_fo
     if (st->started < 0) throw CsError(CS_ERR_CUDA, "belady kernel did not report a status");
     resident = st->resident;
     pinned = st->pinned;
+    ev_safe = ev_total;  // (this admission's own log entries may still be in flight: early status)
     ev_total = st->ev_total;
     pending_targets.clear();
     pending_ticks.clear();
@@ -542,6 +559,11 @@ const csb::AdmitStatus& cs_pool::admit(const csb::AdmitArgs& in, int n_for_grid)
             srv_running = true;
             srv_have_t0 = false;
         }
+        if (srv_status_seen) {  // instrumentation: the host's part of the turnaround
+            host_turnaround_ns += (unsigned long long)std::chrono::duration_cast<std::chrono::nanoseconds>(
+                                      std::chrono::steady_clock::now() - srv_status_t).count();
+            ++host_turnarounds;
+        }
         server_post(a);
     } else {
         if (timing) {
@@ -557,6 +579,10 @@ const csb::AdmitStatus& cs_pool::admit(const csb::AdmitArgs& in, int n_for_grid)
     // pass: the host prepares and enqueues the next launch behind this one instead of waiting
     // for the kernel's end (stream order keeps every later device operation behind it).
     wait_status(a.seq, srv ? "server_kernel" : "admit_kernel");
+    if (srv) {
+        srv_status_t = std::chrono::steady_clock::now();
+        srv_status_seen = true;
+    }
     if (!early_status) ck(cudaStreamSynchronize(stream), "admit_kernel");
     vpref_done = (vpref && vpref_n > 0) ? (int)std::min<long long>(st->n_evicted, vpref_n) : 0;
     vpref = nullptr;
@@ -584,6 +610,7 @@ const csb::AdmitStatus& cs_pool::admit(const csb::AdmitArgs& in, int n_for_grid)
     pre_ok = (a.flags & csb::kPrescan) != 0 && !st->error;
     resident = st->resident;
     pinned = st->pinned;
+    ev_safe = ev_total;  // (this admission's own log entries may still be in flight: early status)
     ev_total = st->ev_total;
     for (int k = 0; k < csb::kPhases; ++k) phase_ns[k] += st->phase_ns[k];
     pending_targets.assign(st->pend_target, st->pend_target + std::min(st->n_pend, csb::kMaxPending));
@@ -597,6 +624,23 @@ const csb::AdmitStatus& cs_pool::admit(const csb::AdmitArgs& in, int n_for_grid)
         launches += 2;
     }
     return *st;
+}
+
+void cs_pool::ck_trap(cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return;
+    std::string m = std::string(what) + ": " + cudaGetErrorString(e);
+    if (trap_word_host && *trap_word_host) {
+        const unsigned long long w = *trap_word_host;
+        m += " (device watchdog site " + std::to_string(w >> 32) + ", CTA " + std::to_string(w & 0xffffffffull) + ")";
+        if (std::getenv("CS_DEBUG_PROGRESS")) {  // each CTA's last progress mark: (seq << 8) | stage
+            m += " progress:";
+            for (int c = 0; c < lc.grid; ++c) {
+                const unsigned long long v = trap_word_host[1 + c];
+                m += " " + std::to_string(c) + ":" + std::to_string(v >> 8) + "/" + std::to_string(v & 0xff);
+            }
+        }
+    }
+    throw CsError(CS_ERR_CUDA, m);
 }
 
 void cs_pool::server_post(const csb::AdmitArgs& a) {
@@ -638,8 +682,9 @@ void cs_pool::server_stop() {
     a.status = st_dev;
     a.seq = seq + 1;
     server_post(a);
-    ck(cudaStreamSynchronize(stream), "server_kernel");
+    ck_trap(cudaStreamSynchronize(stream), "server_kernel");
     if (st->done_seq != a.seq) throw CsError(CS_ERR_CUDA, "server_kernel: no stop acknowledgement");
+    srv_status_seen = false;
     st->done_seq = 0;  // (the next admission waits for this number again)
     if (timing) server_account(st->srv_t0);
     srv_have_t0 = false;
@@ -687,7 +732,7 @@ void cs_pool::wait_status(unsigned long long seq, const char* what) {
                 if (*flag == seq) return;
                 throw CsError(CS_ERR_CUDA, std::string(what) + ": no status from the kernel");
             }
-            if (e != cudaErrorNotReady) ck(e, what);
+            if (e != cudaErrorNotReady) ck_trap(e, what);
         }
     }
 }
@@ -1222,6 +1267,9 @@ int cs_pool_get_stats(cs_pool_t pool, cs_pool_stats* out) {
         out->prescan_used = c.pre_used;
         out->prescan_fallbacks = c.pre_fallbacks;
         out->prescan_unusable = c.pre_badcnt;
+        out->server_launches = pool->server_launches;
+        out->host_turnarounds = pool->host_turnarounds;
+        out->host_turnaround_ns = pool->host_turnaround_ns;
     });
 }
 

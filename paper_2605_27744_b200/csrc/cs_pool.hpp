@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <chrono>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -65,6 +66,7 @@ struct cs_pool {
     bool poll_reset_pending = false;
     long long resident = 0, pinned = 0;  // mirrors of the last status
     unsigned long long ev_total = 0;     // evictions logged so far
+    unsigned long long ev_safe = 0;      // ... of which surely in the log (all but the last admission's)
     std::vector<int> pending_targets;
     std::vector<unsigned long long> pending_ticks;
     // Host mirror of what the reference keeps outside the counts (cs_state.cpp):
@@ -174,6 +176,10 @@ struct cs_pool {
     csb::DevPool srv_P{};
     long long server_launches = 0;
     unsigned long long srv_post = 0;  // mailbox posts so far (admissions and stops)
+    long long host_turnarounds = 0;   // instrumentation: status seen -> next post, on the host
+    unsigned long long host_turnaround_ns = 0;
+    bool srv_status_seen = false;
+    std::chrono::steady_clock::time_point srv_status_t;
     // per-admission device time from the server's pickup stamps: admission k's time is the
     // interval to admission k+1's pickup (the host's turnaround included)
     bool srv_have_t0 = false, srv_last_scan = false;
@@ -183,4 +189,6 @@ struct cs_pool {
     void server_start();
     void server_stop();
     void server_account(unsigned long long t_next);
+    unsigned long long* trap_word_host = nullptr;  // the device watchdogs' last trap site
+    void ck_trap(cudaError_t e, const char* what);   // ck() that names a watchdog's site
 };

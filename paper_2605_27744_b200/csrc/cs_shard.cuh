@@ -295,7 +295,7 @@ __global__ void __launch_bounds__(kThreads + 32, 1) shard_scan_kernel(DevPool P,
                 unsigned long long spins = 0;
                 while (ld_acquire(&C->fin_done) < want) {
                     if (++spins > 4096) __nanosleep(64);
-                    if (spins > (1ull << 27)) __trap();
+                    if (spins > (1ull << 27)) trap_at(301);
                 }
                 __threadfence();
                 C->done = (pass == 0 && *(volatile int*)&C->rescan) ? 0 : 1;

@@ -2,6 +2,7 @@
 %globaltimer offsets (us) of the sub-phase stamps (pstamp) over steady-state scoring launches,
 plus the prescan CTAs' stream end."""
 import ctypes as C
+import os
 import sys
 
 import numpy as np
@@ -19,6 +20,8 @@ spec, seed = bench.rank_workload(40000, pool, 0)
 eng = bench.build_engine(W, spec, pool, 0, False, seed)
 eng.run_timed(int(sys.argv[1]) if len(sys.argv) > 1 else 100)
 rows = []
+wr = []
+fnd = []
 dsub = []
 svc = []
 ends = []
@@ -36,6 +39,11 @@ for it in range(40):
     per = d[:16 * g].reshape(g, 16)
     # service CTAs: 1 = table queue (start, done), 2 = list service (start, gathered, published)
     dsub.append(((per[0, 10:16] - ent) / 1e3))
+    if os.environ.get("CS_DEBUG_WARPS"):
+        full = np.array(buf[:16 * g + 256], dtype=np.int64)
+        fnd.append([(full[16 * g + 100 + 4 * w + k] - ent) / 1e3 for w in range(3) for k in range(3)] +
+                   [full[16 * g + 100 + 4 * w + 3] >> 32 for w in range(3)] + [full[16 * g + 100 + 4 * w + 3] & 1 for w in range(3)])
+        wr.append(np.concatenate([(full[16 * g + 48:16 * g + 65] - ent) / 1e3, (full[16 * g + 72:16 * g + 89] - ent) / 1e3]))
     svc.append([(per[1, 6] - ent) / 1e3, (per[1, 7] - ent) / 1e3, (per[2, 6] - ent) / 1e3, (per[2, 7] - ent) / 1e3,
                 (per[2, 8] - ent) / 1e3])
     # streaming CTAs 4..: start, stream end, writeout end (= verdict wait start), verdict seen
@@ -59,6 +67,16 @@ for it in range(10):
                     (a[5] - a[0]) / 1e3, (a[6] - a[0]) / 1e3, (b[0] - a[0]) / 1e3])
 r = np.median(np.array(rows), axis=0)
 ds = np.median(np.array(dsub), axis=0)
+if wr:
+    w = np.median(np.array(wr), axis=0)
+    print("phase 0 round 1, per warp end (us):", " ".join("%.1f" % x for x in w[:17]))
+    print("phase 0 round 2, per warp end (us):", " ".join("%.1f" % x for x in w[17:]))
+    f = np.array(fnd)
+    print("finds (lane 0 of warps 0-2): start / key loaded / found (us), probe distance, miss:")
+    for k in range(3):
+        print("  warp %d: %.2f %.2f %.2f  dist median %.0f max %.0f  miss frac %.2f" % (
+            k, np.median(f[:, 3 * k]), np.median(f[:, 3 * k + 1]), np.median(f[:, 3 * k + 2]),
+            np.median(f[:, 9 + k]), f[:, 9 + k].max(), f[:, 12 + k].mean()))
 print("replay_apply sub-phases (us from CTA 0 entry): start %.2f lists %.2f bulk decided %.2f prep %.2f victim keys %.2f end %.2f"
       % tuple(ds))
 for k in [0, 1, 2, 3, 13, 14, 4, 5, 6, 7, 9, 10, 11, 12]:
@@ -74,5 +92,9 @@ if srv:
     for name, x in zip(["admit_body entry", "phase 0 end", "early status ready (CTA 0)", "status published (CTA 1)",
                         "CTA 0 done", "streamers saw the verdict", "NEXT admission picked up"], v):
         print("  %28s: %8.2f" % (name, x))
+ps = eng.pool_stats()
+if ps["host_turnarounds"]:
+    print("host turnaround (status seen -> next post): %.2f us mean over %d" % (
+        ps["host_turnaround_ns"] / ps["host_turnarounds"] / 1e3, ps["host_turnarounds"]))
 res = eng.result()
 print("admit_ms per launch", res["admit_ms"] / max(res["admissions"], 1) * 1e3)
