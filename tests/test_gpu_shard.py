@@ -217,3 +217,55 @@ def test_torch_gloo_processes_share_one_gpu():
         assert ev_fnv == g["evictions_fnv"], (rank, hr)
         assert hr == g["hit_rate"]
         assert cached == g["cached_fnv"]
+
+
+def _nccl_worker(rank, world, uid, name, q):
+    try:
+        from paper_2605_27744_b200 import api, shard
+
+        g = RUNS[name]
+        ekw, pol, kw = _kw(g)
+        comm = shard.NcclComm(uid, rank, world, rank)  # one GPU per rank
+        eng = api.Engine(g["spec"], policy=pol, agent_capacity=1024, comm=comm, device=rank, **ekw, **kw)
+        res = eng.run()
+        q.put((rank, fnv(eng.evictions()), repr(res["hit_rate"]), fnv(eng.turns()["cached_tokens"])))
+        eng.close()
+        comm.close()
+    except Exception as e:  # noqa: BLE001
+        q.put((rank, "error", repr(e), ""))
+
+
+def _visible_gpus():
+    import ctypes
+
+    try:
+        n = ctypes.c_int(0)
+        cu = ctypes.CDLL("libcudart.so.12")
+        return n.value if cu.cudaGetDeviceCount(ctypes.byref(n)) == 0 else 0
+    except OSError:
+        return 0
+
+
+@pytest.mark.skipif(_visible_gpus() < 2, reason="needs two GPUs: NCCL runs one rank per device")
+def test_nccl_world2_processes_two_gpus():
+    """The production exchange at world 2: two processes, one GPU and one shard each, ncclAllGather
+    over NVLink; both ranks must reproduce the reference fixture."""
+    import multiprocessing as mp
+
+    from paper_2605_27744_b200 import shard
+
+    name = "supervisor-a-cachesage"
+    g = RUNS[name]
+    uid = shard.nccl_unique_id()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_nccl_worker, args=(r, 2, uid, name, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    got = [q.get(timeout=600) for _ in ps]
+    for p in ps:
+        p.join(timeout=60)
+    for rank, ev_fnv, hr, cached in got:
+        assert ev_fnv == g["evictions_fnv"], (rank, hr)
+        assert hr == g["hit_rate"]
+        assert cached == g["cached_fnv"]
