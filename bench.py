@@ -18,7 +18,7 @@ so no flush is needed between steps.
 Multi-GPU (torchrun, one process per GPU; default --parallel auto = sharded when N > 1): ONE
 pool of N x 16M slots hash-partitioned over the N GPUs; every rank runs the same
 global trace, scans its own shard and the ranks exchange per-shard candidates each admission
-(NCCL allgather over NVLink). --parallel replicas: N independent pools and trace partitions
+(the fused peer-memory exchange over NVLink, or --comm nccl). --parallel replicas: N independent pools and trace partitions
 (no data-path collective). Either way per-GPU work is fixed as N grows ("scaling": weak).
 Timing: CUDA events on the engine's stream, barrier + max over ranks.
 
@@ -243,14 +243,36 @@ def build_engine(W, spec, pool, device, host_inputs, seed, comm=None):
 SHARD_SLACK = 8192
 
 
-def make_comm(dist):
-    """NCCL shard exchange over NVLink: rank 0 makes the id, torch.distributed broadcasts it."""
+def make_comm(dist, kind="peer"):
+    """The shard exchange. 'peer' (default): the fused exchange, each shard's bytes stored into
+    its peers' windows over NVLink / NVSwitch by one kernel (CUDA IPC handles exchanged once
+    through torch.distributed); every rank falls back to NCCL together when any of them cannot
+    map its peers. 'nccl': ncclAllGather (rank 0 makes the id, torch.distributed broadcasts it)."""
     from paper_2605_27744_b200 import shard
 
+    if kind == "peer":
+        def allgather_bytes(b):
+            if dist.world == 1:
+                return [b]
+            out = [None] * dist.world
+            dist.td.all_gather_object(out, b)
+            return out
+
+        comm, err = None, None
+        try:
+            comm = shard.PeerComm(dist.rank, dist.world, dist.local, allgather_bytes)
+        except Exception as e:  # noqa: BLE001
+            err = e
+        if dist.max(1.0 if err is not None else 0.0) == 0.0:
+            return comm, "peer"
+        if comm is not None:
+            comm.close()
+        if dist.rank == 0:
+            print(f"peer exchange unavailable on some rank ({err}); using NCCL", file=sys.stderr)
     uid = [shard.nccl_unique_id() if dist.rank == 0 else None]
     if dist.world > 1:
         dist.td.broadcast_object_list(uid, src=0)
-    return shard.NcclComm(uid[0], dist.rank, dist.world, dist.local)
+    return shard.NcclComm(uid[0], dist.rank, dist.world, dist.local), "nccl"
 
 
 def rank_workload(sessions, pool, rank):
@@ -282,7 +304,7 @@ def run_ours(args, dist):
 
     pool = args.pool
     sharded = args.parallel == "sharded" or (args.parallel == "auto" and dist.world > 1)
-    comm = make_comm(dist) if sharded else None
+    comm, comm_kind = make_comm(dist, args.comm) if sharded else (None, None)
     if sharded:  # one global trace and pool, hash-partitioned: every rank runs the same trace
         spec = W.cfg4_mixed(sessions=args.sessions, budget=pool * dist.world, seed=2608)
         snap_seed = 11
@@ -358,7 +380,9 @@ def run_ours(args, dist):
                    "trace_sessions_per_gpu": args.sessions, "admissions_per_step": R,
                    "policy": "cachesage",
                    "parallelism": (f"hash-sharded{dist.world} (pool of {dist.world} x {pool} slots, owner = "
-                                   "(key >> 40) % N, NCCL allgather of per-shard candidates)") if sharded
+                                   f"(key >> 40) % N, per-shard candidates exchanged by "
+                                   f"{'peer-memory stores (fused exchange kernel)' if comm_kind == 'peer' else 'NCCL allgather'})")
+                   if sharded
                    else f"replicas{dist.world} (sessions partitioned)",
                    "l2": "no flush: each pass streams 134 MB of packed scan words (> 126 MB L2) with an L2 evict-first policy; ncu DRAM reads = 1.003x the streamed bytes per launch"},
         "evictions_per_s": evicted / (tot_ms / 1e3), "admissions_per_s": adm / (tot_ms / 1e3),
@@ -527,6 +551,8 @@ def main():
     ap.add_argument("--sessions", type=int, default=40_000)
     ap.add_argument("--admissions-per-step", type=int, default=32)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--comm", default="peer", choices=["peer", "nccl"],
+                    help="sharded pool: the fused peer-memory exchange (default) or ncclAllGather")
     ap.add_argument("--parallel", default="auto", choices=["auto", "sharded", "replicas"],
                     help="N>1: hash-sharded pool (auto) or independent replicas; 'sharded' also at N=1")
     args = ap.parse_args()

@@ -355,6 +355,20 @@ int cs_comm_callback(int rank, int world, cs_allgather_fn fn, void* ctx, cs_comm
  * the caller broadcasts its 128 bytes; libnccl.so.2 is loaded at run time (CS_NCCL_LIB). */
 int cs_nccl_unique_id(uint8_t* id128);
 int cs_comm_nccl(const uint8_t* id128, int rank, int world, int device, cs_comm_t* out);
+/* Peer memory (the fused exchange): each shard's contribution is stored straight into every
+ * peer's window over NVLink / NVSwitch by one stream-ordered kernel that then waits on the peers'
+ * flags (no NCCL, no host round trip). cap: the largest exchange in bytes per rank (the shard
+ * lists are 74,400 B; 262,144 fits prompts of up to 32,766 blocks).
+ *   cs_comm_peer_group   world shards of this process (devices[r], NULL = all on device 0);
+ *                        peer access is enabled between distinct devices.
+ *   cs_comm_peer_create  one shard per process: returns this rank's 128-byte handle (CUDA IPC
+ *                        handles of its window and flags); the caller allgathers the handles
+ *                        (rank order) and passes all world * 128 bytes to cs_comm_peer_connect. */
+int cs_comm_peer_group(int world, const int* devices, size_t cap, cs_comm_t* comms_out);
+int cs_comm_peer_create(int rank, int world, int device, size_t cap, uint8_t* handle128_out, cs_comm_t* out);
+int cs_comm_peer_connect(cs_comm_t comm, const uint8_t* handles);
+/* One exchange from host buffers (tests, diagnostics): recv[r * bytes ..) = rank r's send. */
+int cs_comm_allgather_host(cs_comm_t comm, const void* send, void* recv, size_t bytes);
 int cs_comm_destroy(cs_comm_t comm);
 /* The shard that owns a block key. */
 int cs_shard_owner(uint64_t key, int world);
@@ -368,6 +382,8 @@ int cs_engine_create_sharded(const cs_engine_cfg* cfg, const cs_workload_spec* s
                              cs_comm_t comm, cs_engine_t* out);
 
 const char* cs_last_error(void);
+/* Diagnostics: the last device watchdog that fired, (site << 32) | CTA, or 0. */
+uint64_t cs_debug_trap_word(void);
 const char* cs_version(void);
 
 #ifdef __cplusplus

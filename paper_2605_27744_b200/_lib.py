@@ -131,6 +131,10 @@ SIGNATURES = {
     "cs_nccl_unique_id": (C.c_int, [vp]),
     "cs_comm_nccl": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.POINTER(vp)]),
     "cs_comm_destroy": (C.c_int, [vp]),
+    "cs_comm_peer_group": (C.c_int, [C.c_int, vp, C.c_size_t, vp]),
+    "cs_comm_peer_create": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_size_t, vp, C.POINTER(vp)]),
+    "cs_comm_peer_connect": (C.c_int, [vp, vp]),
+    "cs_comm_allgather_host": (C.c_int, [vp, vp, vp, C.c_size_t]),
     "cs_shard_owner": (C.c_int, [C.c_uint64, C.c_int]),
     "cs_pool_create_sharded": (C.c_int, [C.POINTER(PoolCfg), C.c_int64, vp, C.POINTER(vp)]),
     "cs_engine_create_sharded": (C.c_int, [C.POINTER(EngineCfg), C.POINTER(WorkloadSpec), C.c_int64, vp,
@@ -154,6 +158,7 @@ SIGNATURES = {
     "cs_engine_write_outputs": (C.c_int, [vp, C.c_char_p, C.c_char_p, C.c_char_p, C.c_uint64, vp, C.c_int, C.c_int]),
     "cs_derive_agent_identity": (C.c_int, [vp, vp, C.c_int, C.c_int, C.c_int, vp]),
     "cs_last_error": (C.c_char_p, []),
+    "cs_debug_trap_word": (C.c_uint64, []),
     "cs_version": (C.c_char_p, []),
 }
 

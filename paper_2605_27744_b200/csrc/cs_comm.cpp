@@ -4,6 +4,7 @@
 #include <dlfcn.h>
 
 #include <chrono>
+#include <cstdio>
 #include <condition_variable>
 #include <cstdlib>
 #include <cstring>
@@ -122,6 +123,83 @@ struct CallbackComm : cs_comm {
     }
 };
 
+// ------------------------------------------------------------------ peer memory (fused exchange)
+// Each rank owns a window (2 parity slots x world x cap bytes) and world flag words on its own
+// device; every rank maps every peer's window and flags (same process: plain pointers with peer
+// access enabled between distinct devices; other processes: CUDA IPC handles). An exchange is one
+// stream-ordered kernel (csb::launch_peer_allgather): no host round trip, no NCCL.
+struct PeerComm : cs_comm {
+    int device = 0;
+    size_t cap = 0;
+    unsigned long long seq = 0;
+    unsigned char* my_win = nullptr;         // owned
+    unsigned long long* my_flags = nullptr;  // owned
+    csb::PeerTable t{};
+    std::vector<void*> ipc_opened;           // peers' mappings to close
+    bool connected = false;
+    // Shards that are threads of one process share one CUDA context (and, in the tests, one
+    // GPU): a device-wide synchronizing call of one thread (cudaFree, ...) would wait for another
+    // shard's exchange kernel, itself waiting for the first thread's next exchange, and a
+    // cooperative grid queued behind one shard's exchange kernel can hold back the dispatch of a
+    // peer's exchange kernel on the shared GPU. Those shards drain their own stream and meet at a
+    // host rendezvous before each exchange kernel is enqueued, and drain it again after, so the
+    // group's exchange kernels always run together with nothing queued behind them. Shards in
+    // different processes (one per GPU in deployment) need none: their exchange is fully
+    // stream-ordered on the device.
+    std::shared_ptr<LocalGroup> g;
+    const char* kind() const override { return "peer"; }
+    void allgather(const void* dsend, void* drecv, size_t bytes, cudaStream_t s) override {
+        if (!connected) throw CsError(CS_ERR_LOGIC, "peer exchange: not connected");
+        if (bytes > cap) throw CsError(CS_ERR_CAPACITY, "peer exchange: message exceeds the window capacity");
+        if (g) {
+            ck(cudaStreamSynchronize(s), "peer exchange: send ready");
+            g->barrier();
+        }
+        ++seq;
+        static const bool trace = std::getenv("CS_DEBUG_PEER") != nullptr;
+        if (trace) std::fprintf(stderr, "[peer] rank %d seq %llu bytes %zu\n", rank, seq, bytes);
+        ck(csb::launch_peer_allgather(dsend, drecv, bytes, t, rank, world, seq, cap, s), "peer allgather");
+        if (g) ck(cudaStreamSynchronize(s), "peer exchange");
+    }
+    // a failing shard must not leave its peers spinning: poison its flag in every peer (their
+    // exchange kernels then trap with an error instead of waiting forever)
+    void abort() override {
+        if (g) {
+            std::lock_guard<std::mutex> lk(g->m);
+            g->broken = true;
+            g->cv.notify_all();
+        }
+        if (!connected) return;
+        const unsigned long long poison = ~0ull;
+        for (int p = 0; p < world; ++p)
+            if (t.flags[p]) cudaMemcpy(t.flags[p] + rank, &poison, 8, cudaMemcpyHostToDevice);
+    }
+    ~PeerComm() override {
+        for (void* q : ipc_opened) cudaIpcCloseMemHandle(q);
+        if (my_win) cudaFree(my_win);
+        if (my_flags) cudaFree(my_flags);
+    }
+};
+
+PeerComm* peer_new(int rank, int world, int device, size_t cap) {
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    auto* c = new PeerComm();
+    c->rank = rank;
+    c->world = world;
+    c->device = device;
+    c->cap = (cap + 15) & ~size_t(15);
+    try {
+        ck(cudaMalloc(reinterpret_cast<void**>(&c->my_win), 2 * (size_t)world * c->cap), "cudaMalloc(peer window)");
+        ck(cudaMalloc(reinterpret_cast<void**>(&c->my_flags), 8 * (size_t)csb::kMaxShards), "cudaMalloc(peer flags)");
+        ck(cudaMemset(c->my_flags, 0, 8 * (size_t)csb::kMaxShards), "memset");
+        ck(cudaDeviceSynchronize(), "peer window");
+    } catch (...) {
+        delete c;
+        throw;
+    }
+    return c;
+}
+
 // ------------------------------------------------------------------ NCCL (loaded at run time)
 typedef struct {
     char internal[128];
@@ -238,6 +316,114 @@ int cs_comm_nccl(const uint8_t* id128, int rank, int world, int device, cs_comm_
             throw;
         }
         *out = c;
+    });
+}
+
+int cs_comm_peer_group(int world, const int* devices, size_t cap, cs_comm_t* out) {
+    return cguard([&] {
+        if (world < 1 || world > csb::kMaxShards || !out || cap == 0)
+            throw std::invalid_argument("cs_comm_peer_group: bad argument");
+        std::vector<PeerComm*> cs;
+        try {
+            auto grp = std::make_shared<LocalGroup>(world);
+            for (int r = 0; r < world; ++r) {
+                cs.push_back(peer_new(r, world, devices ? devices[r] : 0, cap));
+                cs.back()->g = grp;
+            }
+            for (int r = 0; r < world; ++r) {
+                ck(cudaSetDevice(cs[r]->device), "cudaSetDevice");
+                for (int p = 0; p < world; ++p) {
+                    if (cs[p]->device != cs[r]->device) {
+                        int can = 0;
+                        ck(cudaDeviceCanAccessPeer(&can, cs[r]->device, cs[p]->device), "cudaDeviceCanAccessPeer");
+                        if (!can) throw CsError(CS_ERR_CUDA, "peer exchange: no peer access between the shards' GPUs");
+                        const cudaError_t e = cudaDeviceEnablePeerAccess(cs[p]->device, 0);
+                        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) ck(e, "cudaDeviceEnablePeerAccess");
+                        cudaGetLastError();
+                    }
+                    cs[r]->t.win[p] = cs[p]->my_win;
+                    cs[r]->t.flags[p] = cs[p]->my_flags;
+                }
+                cs[r]->connected = true;
+            }
+        } catch (...) {
+            for (auto* c : cs) delete c;
+            throw;
+        }
+        for (int r = 0; r < world; ++r) out[r] = cs[r];
+    });
+}
+
+int cs_comm_peer_create(int rank, int world, int device, size_t cap, uint8_t* handle_out, cs_comm_t* out) {
+    return cguard([&] {
+        if (world < 1 || world > csb::kMaxShards || rank < 0 || rank >= world || !handle_out || !out || cap == 0)
+            throw std::invalid_argument("cs_comm_peer_create: bad argument");
+        PeerComm* c = peer_new(rank, world, device, cap);
+        try {
+            cudaIpcMemHandle_t hw, hf;
+            ck(cudaIpcGetMemHandle(&hw, c->my_win), "cudaIpcGetMemHandle(window)");
+            ck(cudaIpcGetMemHandle(&hf, c->my_flags), "cudaIpcGetMemHandle(flags)");
+            static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+            std::memcpy(handle_out, &hw, 64);
+            std::memcpy(handle_out + 64, &hf, 64);
+        } catch (...) {
+            delete c;
+            throw;
+        }
+        *out = c;
+    });
+}
+
+int cs_comm_peer_connect(cs_comm_t comm, const uint8_t* handles) {
+    return cguard([&] {
+        auto* c = dynamic_cast<PeerComm*>(comm);
+        if (!c || !handles) throw std::invalid_argument("cs_comm_peer_connect: not a peer comm");
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        for (int p = 0; p < c->world; ++p) {
+            if (p == c->rank) {
+                c->t.win[p] = c->my_win;
+                c->t.flags[p] = c->my_flags;
+                continue;
+            }
+            cudaIpcMemHandle_t hw, hf;
+            std::memcpy(&hw, handles + 128 * (size_t)p, 64);
+            std::memcpy(&hf, handles + 128 * (size_t)p + 64, 64);
+            void* w = nullptr;
+            void* f = nullptr;
+            ck(cudaIpcOpenMemHandle(&w, hw, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle(window)");
+            c->ipc_opened.push_back(w);
+            ck(cudaIpcOpenMemHandle(&f, hf, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle(flags)");
+            c->ipc_opened.push_back(f);
+            c->t.win[p] = static_cast<unsigned char*>(w);
+            c->t.flags[p] = static_cast<unsigned long long*>(f);
+        }
+        c->connected = true;
+    });
+}
+
+int cs_comm_allgather_host(cs_comm_t comm, const void* send, void* recv, size_t bytes) {
+    return cguard([&] {
+        if (!comm || !send || !recv) throw std::invalid_argument("cs_comm_allgather_host: null argument");
+        cudaStream_t s;
+        ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
+        void* ds = nullptr;
+        void* dr = nullptr;
+        try {
+            ck(cudaMalloc(&ds, bytes), "cudaMalloc");
+            ck(cudaMalloc(&dr, bytes * (size_t)comm->world), "cudaMalloc");
+            ck(cudaMemcpyAsync(ds, send, bytes, cudaMemcpyHostToDevice, s), "H2D");
+            comm->allgather(ds, dr, bytes, s);
+            ck(cudaMemcpyAsync(recv, dr, bytes * (size_t)comm->world, cudaMemcpyDeviceToHost, s), "D2H");
+            ck(cudaStreamSynchronize(s), "allgather");
+        } catch (...) {
+            cudaFree(ds);
+            cudaFree(dr);
+            cudaStreamDestroy(s);
+            throw;
+        }
+        cudaFree(ds);
+        cudaFree(dr);
+        cudaStreamDestroy(s);
     });
 }
 

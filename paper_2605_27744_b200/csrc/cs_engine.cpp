@@ -479,6 +479,15 @@ void cs_engine::build(const cs_engine_cfg& c, const cs_workload_spec* ws, long l
         d_counts.release();
     }
 
+    {  // size the per-admission scratch once for the largest prompt: nothing is (re)allocated
+       // inside the engine loop (cudaMalloc / cudaFree synchronize the whole device, which would
+       // deadlock shards sharing one GPU whose exchanges wait on each other on the device)
+        long long mx = 1;
+        for (int64_t i = 0; i < nt; ++i) mx = std::max<long long>(mx, (turns[i].v[5] + bs - 1) / bs);
+        for (const auto& kv : catalog) mx = std::max<long long>(mx, kv.second.nb);
+        pool->ensure_prompt_scratch(mx);
+    }
+
     // load (engine.cpp:240-255)
     for (int64_t i = 0; i < nt; ++i) by_session[reqs[i].session].push_back(i);
     for (const auto& kv : by_session) pending_sessions.push_back(kv.first);

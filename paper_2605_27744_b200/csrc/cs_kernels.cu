@@ -457,6 +457,72 @@ cudaError_t launch_check_pool(const DevPool& P, unsigned long long* out, cudaStr
     return cudaGetLastError();
 }
 
+// ---- the peer-memory allgather (PeerTable). One CTA per rank p of the group: push this rank's
+// bytes into p's window slot [seq & 1][rank], release p's flag for this rank (system scope:
+// the window is on another GPU), then wait for p's contribution in this rank's own window and
+// copy it to drecv + p * bytes. Windows are double-buffered by exchange parity: a rank can start
+// exchange k + 2 only after every peer finished exchange k + 1, so after every peer read slot
+// k & 1 (all ranks run the same sequence of exchanges).
+// (128 threads, few registers: a CTA of it fits beside a cooperative scan CTA on one SM, so
+// shards that share a GPU in the tests never starve each other's cooperative launches)
+__global__ void __launch_bounds__(128) peer_allgather_kernel(const unsigned char* __restrict__ src, unsigned char* __restrict__ dst,
+                                      size_t bytes, PeerTable t, int rank, unsigned long long seq, size_t cap) {
+    const int p = blockIdx.x;
+    const int tid = threadIdx.x, T = blockDim.x;
+    const int world = gridDim.x;
+    const size_t slot = (size_t)(seq & 1ull) * (size_t)world * cap;
+    const bool vec = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst) | bytes | cap) & 15u) == 0;
+    {
+        unsigned char* d = t.win[p] + slot + (size_t)rank * cap;
+        if (vec) {
+            const uint4* s4 = reinterpret_cast<const uint4*>(src);
+            uint4* d4 = reinterpret_cast<uint4*>(d);
+            for (size_t i = tid; i < bytes / 16; i += T) d4[i] = s4[i];
+        } else {
+            for (size_t i = tid; i < bytes; i += T) d[i] = src[i];
+        }
+    }
+    __syncthreads();
+    if (tid == 0) {
+        __threadfence_system();
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(t.flags[p] + rank), "l"(seq) : "memory");
+        const unsigned long long* mine = t.flags[rank] + p;
+        unsigned long long spins = 0, v;
+        for (;;) {
+            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(mine) : "memory");
+            if (v == ~0ull) trap_at(402);  // the peer aborted its admission (PeerComm::abort)
+            if (v >= seq) break;
+            if (++spins > 64) __nanosleep(100);
+            if (spins > (1ull << 27)) trap_at(401);
+        }
+    }
+    __syncthreads();
+    {
+        const unsigned char* w = t.win[rank] + slot + (size_t)p * cap;
+        unsigned char* d = dst + (size_t)p * bytes;
+        if (vec) {
+            const uint4* w4 = reinterpret_cast<const uint4*>(w);
+            uint4* d4 = reinterpret_cast<uint4*>(d);
+            for (size_t i = tid; i < bytes / 16; i += T) d4[i] = __ldcg(w4 + i);
+        } else {
+            for (size_t i = tid; i < bytes; i += T) d[i] = __ldcg(w + i);
+        }
+    }
+}
+
+cudaError_t launch_peer_allgather(const void* dsend, void* drecv, size_t bytes, const PeerTable& t, int rank,
+                                  int world, unsigned long long seq, size_t cap, cudaStream_t s) {
+    static bool attr = false;
+    if (!attr) {  // keep the SM's carve-out at max shared memory: never evicts a scan CTA's layout
+        cudaFuncSetAttribute(peer_allgather_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             cudaSharedmemCarveoutMaxShared);
+        attr = true;
+    }
+    peer_allgather_kernel<<<world, 128, 0, s>>>(static_cast<const unsigned char*>(dsend),
+                                                static_cast<unsigned char*>(drecv), bytes, t, rank, seq, cap);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_table_rebuild(const DevPool& P, cudaStream_t s) {
     table_clear_kernel<<<1184, 256, 0, s>>>(P);
     table_fill_kernel<<<1184, 256, 0, s>>>(P);

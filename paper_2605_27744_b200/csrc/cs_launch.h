@@ -178,6 +178,15 @@ cudaError_t launch_forecast(const DevPool& P, int cur, int n_agents, int* out_id
 cudaError_t launch_scores(const DevPool& P, unsigned long long now, unsigned long long* keys, double* scores,
                           long long* n_out, unsigned long long* scratch, cudaStream_t s);
 cudaError_t launch_table_rebuild(const DevPool& P, cudaStream_t s);
+// The peer-memory shard exchange (cs_comm.cpp PeerComm): every rank pushes its bytes into every
+// peer's window over NVLink / NVSwitch (or the same device's memory), raises a flag in that
+// peer's memory, then gathers the peers' contributions from its own window into drecv.
+struct PeerTable {
+    unsigned char* win[kMaxShards];          // each rank's window, as addressable from this device
+    unsigned long long* flags[kMaxShards];   // each rank's flags (one word per source rank)
+};
+cudaError_t launch_peer_allgather(const void* dsend, void* drecv, size_t bytes, const PeerTable& t, int rank,
+                                  int world, unsigned long long seq, size_t cap, cudaStream_t s);
 cudaError_t launch_check_pool(const DevPool& P, unsigned long long* out, cudaStream_t s);  // out[4], zeroed
 // Applies the block-table updates the last admission queued (before any other table user).
 cudaError_t launch_table_flush(const DevPool& P, cudaStream_t s);

@@ -49,6 +49,10 @@ extern "C" const char* cs_version(void) { return "cachesage_b200 0.1 (sm_100a)";
 
 void cs_set_error(const std::string& m) { g_err = m; }
 
+// the device watchdogs' trap word (host-mapped, one per process; see csb::trap_at)
+static unsigned long long* g_trap_word = nullptr;
+extern "C" uint64_t cs_debug_trap_word(void) { return g_trap_word ? *g_trap_word : 0; }
+
 void cs_pool::create(const cs_pool_cfg& c, long long shard_slots, cs_comm* cm) {
     cfg = c;
     comm = cm;
@@ -219,7 +223,7 @@ void cs_pool::create(const cs_pool_cfg& c, long long shard_slots, cs_comm* cm) {
     ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(&mb_dev), mb, 0), "cudaHostGetDevicePointer");
     d_srv_args = dmalloc<csb::AdmitArgs>(2, "server args");  // (double-buffered by post parity)
     {  // the device watchdogs' trap site (one per process, host-mapped)
-        static unsigned long long* trap_word = nullptr;
+        unsigned long long*& trap_word = g_trap_word;
         if (!trap_word) {
             ck(cudaHostAlloc(reinterpret_cast<void**>(&trap_word), 8 * 4096, cudaHostAllocMapped | cudaHostAllocPortable),
                "cudaHostAlloc(trap word)");

@@ -10,6 +10,8 @@ their probe results and per-class candidate lists and replay the same exact evic
                 shards may share one GPU, which is how the single-GPU tests exercise G > 1
   TorchComm     host allgather through a torch.distributed group (gloo): G processes that may
                 share one GPU
+  peer_group /  the fused exchange over peer memory (NVLink / NVSwitch stores + flags, one kernel
+  PeerComm      per exchange): G threads of one process, or one process per GPU via CUDA IPC
 """
 from __future__ import annotations
 
@@ -67,6 +69,32 @@ def NcclComm(uid, rank, world, device):
     h = C.c_void_p()
     check(lib().cs_comm_nccl(buf, rank, world, device, C.byref(h)))
     return Comm(h, rank, world)
+
+
+PEER_CAP = 1 << 18  # bytes per rank and exchange (the shard lists are 74,400 B)
+
+
+def peer_group(world, devices=None, cap=PEER_CAP):
+    """world Comms over peer memory for world shards driven by world threads of this process
+    (the fused exchange: one kernel stores each shard's bytes into its peers' windows)."""
+    hs = (C.c_void_p * world)()
+    devs = None if devices is None else (C.c_int * world)(*devices)
+    check(lib().cs_comm_peer_group(world, devs, cap, hs))
+    return [Comm(C.c_void_p(hs[r]), r, world) for r in range(world)]
+
+
+def PeerComm(rank, world, device, allgather_bytes, cap=PEER_CAP):
+    """Peer-memory transport for one shard per process. allgather_bytes(b: bytes) -> list of
+    every rank's bytes in rank order (e.g. torch.distributed.all_gather_object): exchanges the
+    ranks' CUDA IPC handles once."""
+    h = C.c_void_p()
+    mine = (C.c_uint8 * 128)()
+    check(lib().cs_comm_peer_create(rank, world, device, cap, mine, C.byref(h)))
+    comm = Comm(h, rank, world)
+    allh = allgather_bytes(bytes(mine))
+    buf = (C.c_uint8 * (128 * world)).from_buffer_copy(b"".join(allh))
+    check(lib().cs_comm_peer_connect(comm.h, buf))
+    return comm
 
 
 def CallbackComm(rank, world, allgather):

@@ -143,14 +143,16 @@ def test_bench_configuration_matches_fast_oracle(mode, host_inputs):
 
 
 @pytest.mark.slow
-def test_bench_configuration_four_shards_match_fast_oracle():
+@pytest.mark.parametrize("transport", ["local", "peer"])
+def test_bench_configuration_four_shards_match_fast_oracle(transport):
     """The same 16M-slot configuration hash-sharded over 4 shards (threads sharing this GPU),
-    checked against the oracle — not against the single pool."""
+    checked against the oracle — not against the single pool — with the device-to-device copy
+    exchange and with the fused peer-memory exchange."""
     from paper_2605_27744_b200 import api, shard, workloads as W
 
     spec = _bench_spec()
     world = 4
-    comms = shard.local_group(world)
+    comms = shard.local_group(world) if transport == "local" else shard.peer_group(world)
     out = [None] * world
     err = []
     snap = {}
@@ -158,7 +160,7 @@ def test_bench_configuration_four_shards_match_fast_oracle():
     def work(r):
         try:
             eng = api.Engine(spec, policy="cachesage", budget=BENCH_POOL, agent_capacity=1024, comm=comms[r],
-                             grid_ctas=148 // world, prefetch=True)
+                             grid_ctas=148 // world - (4 if transport == "peer" else 0), prefetch=True)
             try:
                 if r == 0:
                     snap["agents"] = eng.agents()

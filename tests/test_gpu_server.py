@@ -15,14 +15,14 @@ pytestmark = pytest.mark.gpu
 POOL = 1 << 20
 
 
-def _run(server, host_inputs=False, chunks=(400,), mode="realistic"):
+def _run(server, host_inputs=False, chunks=(400,), mode="realistic", sessions=4000, by_steps=False):
     import paper_2605_27744_b200 as cb
     from paper_2605_27744_b200 import workloads as W
 
     old = os.environ.get("CS_SERVER")
     os.environ["CS_SERVER"] = "1" if server else "0"
     try:
-        spec = W.cfg4_mixed(sessions=4000, budget=POOL, seed=2608)
+        spec = W.cfg4_mixed(sessions=sessions, budget=POOL, seed=2608)
         eng = cb.Engine(spec, policy="cachesage", budget=POOL, host_inputs=host_inputs, agent_capacity=1024,
                         prefetch=True)
     finally:
@@ -33,8 +33,12 @@ def _run(server, host_inputs=False, chunks=(400,), mode="realistic"):
     try:
         keys, lt, agents, refs = W.pool_snapshot(POOL, len(eng.agents()), seed=11, mode=mode)
         eng.restore(keys, lt, agents=agents, refs=refs)
-        for c in chunks:
-            eng.run_for(c)
+        if by_steps:  # one engine call (one server launch and stop) per scheduler step, to the end
+            while not eng.step():
+                pass
+        else:
+            for c in chunks:
+                eng.run_for(c)
         t = eng.turns()
         ws, wt, wk = eng.warmups()
         out = {"ev": eng.evictions(), "cached": t["cached_tokens"], "end": t["end_us"].view(np.uint64),
@@ -65,11 +69,13 @@ def test_server_equals_per_admission_launches(mode):
 
 
 def test_server_segmentation_does_not_matter():
-    """One engine call per admission (a server launch and a stop each) against one call."""
-    a = _run(True, chunks=(1,) * 60 + (340,))
-    b = _run(True, chunks=(400,))
+    """One engine call per scheduler step (a server launch and a stop each) against one call,
+    over a whole trace."""
+    a = _run(True, sessions=200, by_steps=True)
+    b = _run(True, sessions=200, chunks=(10**9,))
     _same(a, b)
     assert a["ps"]["server_launches"] > b["ps"]["server_launches"]
+    assert a["ev"].size > 100
 
 
 def test_server_end_to_end_path():

@@ -36,12 +36,15 @@ def _kw(g):
     return ekw, kw.pop("policy"), kw
 
 
-def _run_shards(g, world, grid=None, shard_slots=0):
+def _run_shards(g, world, grid=None, shard_slots=0, transport="local"):
     from paper_2605_27744_b200 import api, shard
 
     ekw, pol, kw = _kw(g)
-    comms = shard.local_group(world)
-    grid = grid or max(1, 148 // world)  # the G cooperative scan grids must be co-resident
+    comms = shard.local_group(world) if transport == "local" else shard.peer_group(world)
+    # the G cooperative scan grids must be co-resident; with the peer exchange the shards' streams
+    # also run concurrently, and an exchange kernel waiting for a peer must never hold the SM a
+    # peer's cooperative scan needs (one GPU per shard in deployment): leave SMs free for them
+    grid = grid or max(1, 148 // world - (4 if transport == "peer" else 0))
     out = [None] * world
     err = []
 
@@ -97,6 +100,69 @@ def test_sharded_engine_matches_reference(name, world):
     assert sum(residents) <= g["kw"].get("budget", 10**12)
     if world > 1:
         assert min(residents) > 0
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("name", ["supervisor-a-cachesage", "cfg1@128-cachesage", "pins-defer-lru",
+                                  "supervisor-a-emax3-cachesage"])
+def test_sharded_engine_peer_exchange(name, world):
+    """The fused exchange (peer-memory stores + flags, one kernel per exchange, no NCCL, no host
+    round trip): every shard reproduces the reference run bit-exactly."""
+    g = RUNS[name]
+    for res, t, ev, w, ps in _run_shards(g, world, transport="peer"):
+        _check_golden(g, res, t, ev, w)
+
+
+def _peer_worker(rank, world, port, name, q):
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2605_27744_b200 import api, shard
+
+        def allgather_bytes(b):
+            out = [None] * world
+            dist.all_gather_object(out, b)
+            return out
+
+        g = RUNS[name]
+        ekw, pol, kw = _kw(g)
+        comm = shard.PeerComm(rank, world, 0, allgather_bytes)
+        eng = api.Engine(g["spec"], policy=pol, agent_capacity=1024, comm=comm, grid_ctas=148 // world - 4, **ekw,
+                         **kw)
+        res = eng.run()
+        q.put((rank, fnv(eng.evictions()), repr(res["hit_rate"]), fnv(eng.turns()["cached_tokens"])))
+        eng.close()
+        comm.close()
+    except Exception as e:  # noqa: BLE001
+        q.put((rank, "error", repr(e), ""))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_exchange_processes_cuda_ipc():
+    """One shard per process, the windows shared through CUDA IPC handles (the multi-GPU
+    deployment's wiring; here both processes share this box's GPU)."""
+    import multiprocessing as mp
+    import random
+
+    name = "supervisor-b-cachesage"
+    g = RUNS[name]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = random.randint(20000, 40000)
+    ps = [ctx.Process(target=_peer_worker, args=(r, 2, port, name, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    got = [q.get(timeout=600) for _ in ps]
+    for p in ps:
+        p.join(timeout=60)
+    for rank, ev_fnv, hr, cached in got:
+        assert ev_fnv == g["evictions_fnv"], (rank, hr)
+        assert hr == g["hit_rate"]
+        assert cached == g["cached_fnv"]
 
 
 def test_sharded_tight_shards_error_loudly():
@@ -269,3 +335,42 @@ def test_nccl_world2_processes_two_gpus():
         assert ev_fnv == g["evictions_fnv"], (rank, hr)
         assert hr == g["hit_rate"]
         assert cached == g["cached_fnv"]
+
+
+@pytest.mark.parametrize("transport", ["local", "peer"])
+@pytest.mark.parametrize("world", [1, 2, 4])
+def test_exchange_transport_allgather(transport, world):
+    """The exchange itself, outside any admission: world threads, many rounds of odd and
+    16-byte-multiple sizes, every rank must receive every rank's bytes in rank order."""
+    import ctypes as C
+
+    from paper_2605_27744_b200 import shard
+    from paper_2605_27744_b200._lib import check, lib
+
+    comms = shard.local_group(world) if transport == "local" else shard.peer_group(world)
+    err = []
+
+    def work(r):
+        try:
+            rng = np.random.default_rng(r)
+            for it in range(40):
+                nb = [8, 16, 808, 74400, 1000][it % 5]
+                mine = ((np.arange(nb) * 7 + it * 131 + r * 17) % 251).astype(np.uint8)
+                out = np.zeros(nb * world, np.uint8)
+                check(lib().cs_comm_allgather_host(comms[r].h, mine.ctypes.data, out.ctypes.data, nb))
+                for p in range(world):
+                    want = ((np.arange(nb) * 7 + it * 131 + p * 17) % 251).astype(np.uint8)
+                    assert np.array_equal(out[p * nb:(p + 1) * nb], want), (r, it, p)
+                rng.random()
+        except Exception as e:  # noqa: BLE001
+            err.append(e)
+
+    th = [threading.Thread(target=work, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for c in comms:
+        c.close()
+    if err:
+        raise err[0]
