@@ -2131,7 +2131,7 @@ __device__ void replay_prologue(const DevPool& P, ReplaySmem& R, const AdmSmem& 
         R.ph_key[j] = kNoSlot;
         R.vh_key[j] = kNoSlot;
     }
-    const long long ftop = C->free_top;
+    const long long ftop = A.free_top;  // (CTA 0 keeps it: loaded at admission start, updated by every apply)
     int absent = 0, pre_unpinned = 0;
     for (int i = tid; i < len; i += T) {
         const unsigned int sl = P.p_slot[lo + i];
@@ -2665,6 +2665,7 @@ __device__ void replay_apply(const DevPool& P, const AdmitArgs& a, ReplaySmem& R
         C->resident = A.resident;
         C->pinned = A.pinned;
         C->free_top = top;
+        A.free_top = top;
         C->n_ev = ev0 + nv;
         C->tq_erase = q_e + nv;
         C->tq_insert = q_i + R.n_ins;
@@ -2683,7 +2684,8 @@ constexpr int kOvMax = kOv / 2;
 // after the overlay (below the early-validation view)
 constexpr int kFindMax = 2048;
 constexpr size_t kFindOff = 12ull * kOv;
-static_assert(kFindOff + 12ull * kFindMax <= kEarlyOff, "early finds must stay below the early-validation view");
+// per prompt position: slot (the find, then the resolved slot), key, token count, pins before
+static_assert(kFindOff + 20ull * kFindMax <= kEarlyOff, "early finds must stay below the early-validation view");
 constexpr unsigned int kOvErase = 0x7FFFFFFFu;  // erased only (slots stay below 2^31 - 16)
 constexpr unsigned int kOvBoth = 0x80000000u;   // slot | kOvBoth: erased, then re-inserted
 constexpr unsigned int kOvSlot = ~kOvBoth;
@@ -2833,6 +2835,7 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
             A.st_done = 0;
             A.first_touch = ~0ull;
             A.tick = a.tick_base;
+            A.free_top = C->free_top;  // (the replay prologue's free-stack reads need it: one round earlier)
             for (int k = 0; k < kPhases; ++k) A.ph[k] = 0;
 #pragma unroll
             for (int c = 0; c < kMaxLists; ++c) A.wsurv[c] = P.wsurv[c];  // constant indices
@@ -2933,8 +2936,10 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
             const int nf = n <= kFindMax ? n : 0;
             unsigned int* f_slot = reinterpret_cast<unsigned int*>(dsm + kOffRing + kFindOff);
             unsigned long long* f_key = reinterpret_cast<unsigned long long*>(dsm + kOffRing + kFindOff + 4 * kFindMax);
+            int* f_cnt = reinterpret_cast<int*>(dsm + kOffRing + kFindOff + 12 * kFindMax);
             for (int q = tid; q < nf + nuv + ne + ni; q += T) {
                 if (q < nf) {
+                    f_cnt[q] = a.counts[q];  // (for the lookup: issued with the key, used much later)
                     const unsigned long long t0 = P.dbg_warps ? gtimer() : 0ull;
                     const unsigned long long key = a.keys[q];
                     f_key[q] = key;
@@ -3004,6 +3009,7 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
                     const unsigned int r0 = s == kNoSlot ? 0u : P.refs[s];
                     P.p_slot[i] = s;
                     P.p_refs0[i] = r0;
+                    if (nf) f_slot[i] = s;  // (the lookup below reads the resolved slot on chip)
                     if (s == kNoSlot && i < miss_min) miss_min = i;
                     if (s == kNoSlot || r0 == 0u) ++need;
                 } else {  // U re-read, after every unpin of this launch
@@ -3083,19 +3089,23 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
             if (a.flags & kDispatch) {
                 if (tid == 0) A.tick = A.tick + 1;
                 __syncthreads();
-                if (A.svc_b)
-                    commit_observe(P, a, A.tick, A, B.cls);
-                else
-                    observe_dispatch(P, a.prev, a.next, A.tick, a.n_agents, dsm, Red, A, B.cls, pf);
+                // the learner service's observe is committed after the lookup (below): nothing
+                // until the consumer reads the classes, so the service has that much longer
+                if (!A.svc_b) observe_dispatch(P, a.prev, a.next, A.tick, a.n_agents, dsm, Red, A, B.cls, pf);
             }
+            const unsigned long long dispatch_tick = A.tick;
             pstamp(P, 4);
             if (a.flags & kLookup) {
                 const int f = (int)miss_min;
                 long long cached = 0;
                 const bool early = es.ok != 0 && f <= kTset / 2;
+                // the resolved slots and token counts are on chip when phase 0 ran its early finds
+                const bool onchip = ne + ni <= kOvMax && n <= kFindMax;
+                const unsigned int* f_slot = reinterpret_cast<const unsigned int*>(dsm + kOffRing + kFindOff);
+                const int* f_cnt = reinterpret_cast<const int*>(dsm + kOffRing + kFindOff + 12 * kFindMax);
                 for (int i = tid; i < f; i += T) {
-                    cached += a.counts[i];
-                    const unsigned int ts = P.p_slot[i];
+                    cached += onchip ? f_cnt[i] : a.counts[i];
+                    const unsigned int ts = onchip ? f_slot[i] : P.p_slot[i];
                     P.lt[ts] = A.tick + 1 + (unsigned long long)i;  // EngineSim::touch
                     pk_touch(P, ts, A.tick + 1 + (unsigned long long)i);
                     if (a.touch_agent) a.touch_agent[i] = P.agent[ts];
@@ -3117,6 +3127,7 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
                 A.admit_n = an;
                 A.anchor = a.anchor < 0 ? an : a.anchor;
             }
+            if ((a.flags & kDispatch) && A.svc_b) commit_observe(P, a, dispatch_tick, A, B.cls);
         }
         __syncthreads();
         if (tid == 0) {  // phase 0 is complete: publish for the speculative scanners
