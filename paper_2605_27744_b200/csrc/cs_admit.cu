@@ -79,6 +79,10 @@ struct AdmSmem {
     unsigned long long srv_t0;  // admission server: when CTA 0 picked this admission up (else 0)
     int st_done;  // the status went out early (from the apply's idle warp), not in the epilogue
     int svc_b;    // observe(AgentDispatch) comes from the learner service (commit_observe)
+    // CTA 0's own counters, kept on chip (their Ctrl copies are written through): the eviction
+    // log length and the block-table queue lengths
+    unsigned long long n_ev_c;
+    int tq_e, tq_i;
 };
 
 // Dynamic shared memory, phase by phase (the regions alias across phases):
@@ -169,6 +173,7 @@ struct EarlySmem {
     unsigned char U_ok[kXset];
     unsigned short xl[kXset];  // the xset positions phase 0 filled (U), in insertion order
     int xn;
+    int efx[kPreK + 1];        // exclusive prefix count of the surviving E entries
     unsigned int tset[kTset];
     unsigned long long TE, TR, TP;
     int nE, nR, nP, ok, valid;
@@ -1937,6 +1942,22 @@ __device__ bool consume_svc(const DevPool& P, const AdmitArgs& a, EarlySmem& es,
             if (++spins > 4096) __nanosleep(64);
             if (spins > (1ull << 28)) trap_at(105);
         }
+    }
+    __syncthreads();
+    // one round of (L2-resident) loads: the counts and bounds, and the first kPreK entries of E
+    // and of R whatever their counts (the lists hold at most kPreK each; unused entries ignored)
+    static_assert(2 * kPreK < kThreads, "one E or R entry per thread");
+    if (tid < kPreK) {
+        es.E_lt[tid] = __ldcg(P.pl_lt + tid);
+        es.E_slot[tid] = __ldcg(P.pl_slot + tid);
+        es.E_ok[tid] = __ldcg(P.pl_ok + tid);
+        if (tid < kChunk + 2) es.E_key[tid] = __ldcg(P.pl_key + tid);
+    } else if (tid < 2 * kPreK) {
+        const int j = tid - kPreK;
+        es.R_lt[j] = __ldcg(P.pl_lt + kPendCap + j);
+        es.R_slot[j] = __ldcg(P.pl_slot + kPendCap + j);
+        es.R_ok[j] = __ldcg(P.pl_ok + kPendCap + j);
+    } else if (tid == 2 * kPreK) {
         es.nE = __ldcg(P.pl_n + 0);
         es.nR = __ldcg(P.pl_n + 1);
         es.nP = __ldcg(P.pl_n + 2);
@@ -1950,20 +1971,6 @@ __device__ bool consume_svc(const DevPool& P, const AdmitArgs& a, EarlySmem& es,
     if (!es.valid) return false;
     const unsigned long long TEs = min(es.TE, es.TP), TR = es.TR, TP = es.TP;
     const int nE = es.nE, nR = es.nR, nP = es.nP;
-    for (int q = tid; q < nE + nR; q += T) {  // one round of (L2-resident) loads
-        if (q < nE) {
-            es.E_lt[q] = __ldcg(P.pl_lt + q);
-            es.E_slot[q] = __ldcg(P.pl_slot + q);
-            es.E_ok[q] = __ldcg(P.pl_ok + q);
-            if (q < kChunk + 2) es.E_key[q] = __ldcg(P.pl_key + q);
-        } else {
-            const int j = q - nE;
-            es.R_lt[j] = __ldcg(P.pl_lt + kPendCap + j);
-            es.R_slot[j] = __ldcg(P.pl_slot + kPendCap + j);
-            es.R_ok[j] = __ldcg(P.pl_ok + kPendCap + j);
-        }
-    }
-    __syncthreads();
     unsigned long long* xl = B.sd_lt;
     unsigned int* xs = B.sd_slot;
     unsigned char* ef = B.st_list;  // E flags [0, kPreK), R flags [kPreK, 2 kPreK)
@@ -2024,12 +2031,15 @@ __device__ bool consume_svc(const DevPool& P, const AdmitArgs& a, EarlySmem& es,
         const long long excl = off + incl - both;
         fe = (int)(excl >> 32);
         fr = (int)(excl & 0xffffffffll);
+        if (tid < nE) es.efx[tid] = fe;
         __syncthreads();
         if (tid == (int)blockDim.x - 1) Red.u[0] = (unsigned long long)(off + incl);
         __syncthreads();
     }
     const long long tot = (long long)Red.u[0];
     const int totE = (int)(tot >> 32), totR = (int)(tot & 0xffffffffll);
+    if (tid == 0) es.efx[nE] = totE;
+    __syncthreads();
     if (!(nx <= kSide && (totR > 0 || TR >= kNoBound))) return false;
     const int cap = kChunk + 1;
     if (tid < nR && ef[kPreK + tid] && fr < cap) {
@@ -2055,7 +2065,7 @@ __device__ bool consume_svc(const DevPool& P, const AdmitArgs& a, EarlySmem& es,
             if (es.E_lt[mid] < x) lo2 = mid + 1;
             else hi2 = mid;
         }
-        for (int k = 0; k < lo2; ++k) r += ef[k];
+        r += es.efx[lo2];  // the surviving E entries before position lo2
         if (r < cap) {
             R.L_lt[E][r] = x;
             R.L_slot[E][r] = xs[i];
@@ -2121,9 +2131,19 @@ __device__ __forceinline__ unsigned int hslot(unsigned int s) { return (s * 2654
 // prompt slots and their pins, free slots, the slot -> prompt index hash, pool counters.
 // Depends only on phase 0 and earlier chunks, so a speculative pass runs it before the lists
 // exist.
-__device__ void replay_prologue(const DevPool& P, ReplaySmem& R, const AdmSmem& A, RedSmem& Red) {
+__device__ void replay_prologue(const DevPool& P, ReplaySmem& R, AdmSmem& A, RedSmem& Red,
+                                unsigned long long seq) {
     Ctrl* C = P.ctrl;
     const int tid = threadIdx.x, T = blockDim.x;
+    // the table service usually finished long ago: hand the queue counters back to CTA 0 now
+    // (this round of loads), so the apply's queue_ready finds nothing to wait for
+    if (tid == 0 && A.q_deleg && ld_acquire_u64(&C->svc_q_seq) == seq) {
+        C->tq_erase = 0;
+        C->tq_insert = 0;
+        A.tq_e = 0;
+        A.tq_i = 0;
+        A.q_deleg = 0;
+    }
     const int lo = A.chunk * kChunk;
     const int hi = min(A.admit_n, lo + kChunk);
     const int len = hi - lo;
@@ -2217,6 +2237,8 @@ __device__ void queue_ready(const DevPool& P, const AdmitArgs& a, AdmSmem& A) {
         }
         C->tq_erase = 0;
         C->tq_insert = 0;
+        A.tq_e = 0;
+        A.tq_i = 0;
         A.q_deleg = 0;
     }
     __syncthreads();
@@ -2563,7 +2585,7 @@ __device__ void replay_apply(const DevPool& P, const AdmitArgs& a, ReplaySmem& R
     const int nv = R.n_vict;
     // ---- apply: victims first (queue the erase, free slot), then inserts and touches
     queue_ready(P, a, A);
-    const unsigned long long ev0 = C->n_ev;
+    const unsigned long long ev0 = A.n_ev_c;
     // victim keys first (a reused victim slot is rewritten below)
     for (int k = tid; k < nv; k += T) {
         const unsigned int v = R.victims[k];
@@ -2581,7 +2603,7 @@ __device__ void replay_apply(const DevPool& P, const AdmitArgs& a, ReplaySmem& R
     // of this admission (later chunks re-resolve through the victim set), and a block this
     // admission inserted is pinned, so it is never among its own victims (the queue applies every
     // erase before every insert).
-    const int q_e = C->tq_erase, q_i = C->tq_insert;
+    const int q_e = A.tq_e, q_i = A.tq_i;
     // This chunk completes a plain admission served from a prescan: its status is final once the
     // victims are known, so the apply's idle warp publishes it (and the victims) to the host while
     // the other warps apply; the host schedules the next admission meanwhile.
@@ -2669,6 +2691,9 @@ __device__ void replay_apply(const DevPool& P, const AdmitArgs& a, ReplaySmem& R
         C->n_ev = ev0 + nv;
         C->tq_erase = q_e + nv;
         C->tq_insert = q_i + R.n_ins;
+        A.n_ev_c = ev0 + nv;
+        A.tq_e = q_e + nv;
+        A.tq_i = q_i + R.n_ins;
         A.n_ev_adm += nv;
     }
     __syncthreads();
@@ -2836,6 +2861,9 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
             A.first_touch = ~0ull;
             A.tick = a.tick_base;
             A.free_top = C->free_top;  // (the replay prologue's free-stack reads need it: one round earlier)
+            A.n_ev_c = C->n_ev;
+            A.tq_e = C->tq_erase;
+            A.tq_i = C->tq_insert;
             for (int k = 0; k < kPhases; ++k) A.ph[k] = 0;
 #pragma unroll
             for (int c = 0; c < kMaxLists; ++c) A.wsurv[c] = P.wsurv[c];  // constant indices
@@ -2866,7 +2894,7 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
         pstamp(P, 0);
         const int n = a.n;
         long long miss_min = n, need = 0;
-        const int ne = C->tq_erase, ni = C->tq_insert;
+        const int ne = A.tq_e, ni = A.tq_i;
         // a pipelined launch: CTA kSvcQ applies the queued table updates (service_queue)
         const bool deleg = pre_avail;
         if (tid == 0) A.q_deleg = deleg ? 1 : 0;
@@ -3027,6 +3055,8 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
                 C->tombstones += (long long)ne - reused;
                 C->tq_erase = 0;
                 C->tq_insert = 0;
+                A.tq_e = 0;
+                A.tq_i = 0;
             }
             pstamp(P, 2);
         } else {  // too many queued keys for the overlay: the probe waits for the table
@@ -3035,6 +3065,10 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
                 queue_ready(P, a, A);
             else
                 apply_table_queue(P, Red);  // the previous admission's erases / inserts
+            if (tid == 0 && !deleg) {
+                A.tq_e = 0;
+                A.tq_i = 0;
+            }
             pstamp(P, 1);
             pf_issue2();
             // deferred EngineSim::unpin calls of completed requests (engine.cpp:170-180), in order
@@ -3196,7 +3230,7 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
             __syncthreads();
             bool need_loop = false;
             if (A.started && !A.error && A.admit_n > 0) {
-                replay_prologue(P, Rp, A, Red);
+                replay_prologue(P, Rp, A, Red, a.seq);
                 stamp(A, 1);
                 pstamp(P, 6);
                 const bool need0 = C->resident + Rp.absent > P.cap;
@@ -3254,7 +3288,7 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
         }
         if (tid < NL) S.hinted[tid] = P.ghint[tid] < kNoBound ? 1 : 0;  // before any finalizer rewrites it
         const int slow = __syncthreads_or(tid < NL && !(P.ghint[tid] < kNoBound) && !P.gsmall[tid]);
-        if (blockIdx.x == 0) replay_prologue(P, Rp, A, Red);  // the lists are not needed for it
+        if (blockIdx.x == 0) replay_prologue(P, Rp, A, Red, a.seq);  // the lists are not needed for it
         stamp(A, 1);
         scan_pass(P, NL, keep0, B, S, Sel, dsm, !slow, a);
         grid_barrier(C);
@@ -3419,7 +3453,7 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
             }
         }
         if (blockIdx.x == 0 && !pending_rescan) {
-            replay_prologue(P, Rp, A, Red);
+            replay_prologue(P, Rp, A, Red, a.seq);
             replay_apply(P, a, Rp, A, NL, need_scan != 0, Red);
             if (tid == 0) A.chunk += 1;
             __syncthreads();
