@@ -83,6 +83,7 @@ struct AdmSmem {
     // log length and the block-table queue lengths
     unsigned long long n_ev_c;
     int tq_e, tq_i;
+    long long pin_c;  // pinned_count_ (its Ctrl copy written through)
 };
 
 // Dynamic shared memory, phase by phase (the regions alias across phases):
@@ -480,6 +481,7 @@ __device__ void service_learner(const DevPool& P, const AdmitArgs& a, unsigned c
     __shared__ long long s_head, s_size;
     __shared__ int s_changed;
     if (tid == 0) {
+        P.dbg[blockIdx.x * 16 + 6] = gtimer();  // (instrumentation: service start / loads / BFS / done)
         s_head = __ldcg(&C->win_head);
         s_size = __ldcg(&C->win_size);
         s_changed = __ldcg(&C->cur_agent) != next ? 1 : 0;
@@ -520,7 +522,9 @@ __device__ void service_learner(const DevPool& P, const AdmitArgs& a, unsigned c
     __syncthreads();
     const bool popped = prev >= 0 && size == W;
     const int oa = popped ? (int)B.wa[0] : -1, ob = popped ? (int)B.wb[0] : -1;
+    if (tid == 0) P.dbg[blockIdx.x * 16 + 7] = gtimer();
     if (changed) bfs_prefetched(P, B, prev, next, n_agents);
+    if (tid == 0) P.dbg[blockIdx.x * 16 + 8] = gtimer();
     // argmax_row(next) after the record: +1 at [next][next] when prev == next, -1 at [oa][ob]
     // when oa == next (the popped pair); ties -> the smaller 64-bit AgentId
 #pragma unroll
@@ -553,7 +557,13 @@ __device__ void service_learner(const DevPool& P, const AdmitArgs& a, unsigned c
         Red.w[warp_id()] = best_id;
     }
     if (changed)
-        for (int x = tid; x < n_agents; x += T) P.spec_hop[x] = B.hop[x];
+        for (int w = tid; w * 8 < n_agents; w += T) {
+            unsigned long long h8 = 0ull;
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                if (w * 8 + k < n_agents) h8 |= (unsigned long long)B.hop[w * 8 + k] << (8 * k);
+            P.spec_hop[w] = make_ulonglong2(a.seq, h8);
+        }
     __syncthreads();
     if (tid == 0) {
         const int nw = (T + 31) >> 5;
@@ -570,18 +580,23 @@ __device__ void service_learner(const DevPool& P, const AdmitArgs& a, unsigned c
                 best_b = b;
             }
         }
-        LearnSpec* sp = P.spec;
-        sp->changed = changed ? 1 : 0;
-        sp->oa = oa;
-        sp->ob = ob;
-        sp->best_b = best_b;
-        sp->best_c = (unsigned int)best_c;
-        sp->total_next = tot_next + (prev >= 0 && prev == next ? 1u : 0u) - (oa == next ? 1u : 0u);
+        LearnSpec sp;
+        sp.seq0 = sp.seq1 = sp.seq2 = a.seq;
+        sp.changed = changed ? 1 : 0;
+        sp.oa = oa;
+        sp.ob = ob;
+        sp.best_b = best_b;
+        sp.best_c = (unsigned int)best_c;
+        sp.total_next = tot_next + (prev >= 0 && prev == next ? 1u : 0u) - (oa == next ? 1u : 0u);
+        const ulonglong2* src = reinterpret_cast<const ulonglong2*>(&sp);
+        ulonglong2* dst = reinterpret_cast<ulonglong2*>(P.spec);
+        for (int k = 0; k < 3; ++k) dst[k] = src[k];  // (16-byte stores: each word with its seq)
     }
     __syncthreads();  // (every thread's spec_hop stores before the release)
     if (tid == 0) {
         __threadfence();
         asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(&C->svc_b_seq), "l"(a.seq) : "memory");
+        P.dbg[blockIdx.x * 16 + 9] = gtimer();
     }
 }
 
@@ -595,23 +610,36 @@ __device__ void commit_observe(const DevPool& P, const AdmitArgs& a, unsigned lo
     const int tid = threadIdx.x, T = blockDim.x;
     const long long W = P.window;
     const int Acap = P.a_cap, prev = a.prev, next = a.next, n_agents = a.n_agents;
-    __shared__ LearnSpec sp;
-    if (tid == 0) {
-        unsigned long long spins = 0;
-        while (ld_acquire_u64(&C->svc_b_seq) != a.seq) {
-            if (++spins > 4096) __nanosleep(64);
-            if (spins > (1ull << 28)) trap_at(101);
+    __shared__ __align__(16) LearnSpec sp;
+    // one round of 16-byte loads: the result and the hops, each word tagged with its admission;
+    // only a service that has not finished yet costs a wait (then the words are read again)
+    const int nw = (n_agents + 7) / 8;
+    ulonglong2 hw = make_ulonglong2(0ull, 0ull);
+    for (unsigned long long spins = 0;; ++spins) {
+        int ok = 1;
+        if (tid < 3) {
+            const ulonglong2 v = __ldcg(reinterpret_cast<const ulonglong2*>(P.spec) + tid);
+            reinterpret_cast<ulonglong2*>(&sp)[tid] = v;
+            ok = v.x == a.seq;
+        } else if (tid - 3 < nw && tid - 3 < kMaxAgents / 8) {
+            hw = __ldcg(P.spec_hop + (tid - 3));
         }
-        sp = *P.spec;
+        // (the hops are this admission's only if the BFS ran: checked once `changed` is known)
+        if (__syncthreads_and(ok)) {
+            const int need_hops = sp.changed;
+            if (!need_hops || __syncthreads_and(!(tid >= 3 && tid - 3 < nw) || hw.x == a.seq)) break;
+        }
+        if (++spins > 64) __nanosleep(100);
+        if (spins > (1ull << 28)) trap_at(101);
     }
-    __syncthreads();
     pstamp(P, 13);
-    if (sp.changed) {
-        for (int x = tid; x < n_agents; x += T) {
-            const unsigned char h = __ldcg(P.spec_hop + x);
-            P.hop[x] = h;
-            P.cls[x] = h;
-            if (cls_smem) cls_smem[x] = h;
+    if (sp.changed && tid >= 3 && tid - 3 < nw) {
+        const int w = tid - 3;
+        for (int k = 0; k < 8 && w * 8 + k < n_agents; ++k) {
+            const unsigned char h = (unsigned char)(hw.y >> (8 * k));
+            P.hop[w * 8 + k] = h;
+            P.cls[w * 8 + k] = h;
+            if (cls_smem) cls_smem[w * 8 + k] = h;
         }
     }
     if (tid == 0) {
@@ -2173,7 +2201,7 @@ __device__ void replay_prologue(const DevPool& P, ReplaySmem& R, AdmSmem& A, Red
         R.lists_ready = 0;
         R.ftop = ftop;
         R.res0 = C->resident;
-        R.pinned0 = C->pinned;
+        R.pinned0 = A.pin_c;
     }
     const long long both = block_sum(((long long)absent << 32) | (long long)pre_unpinned, Red);
     // slot -> prompt index of this chunk's resident blocks
@@ -2686,6 +2714,7 @@ __device__ void replay_apply(const DevPool& P, const AdmitArgs& a, ReplaySmem& R
         for (int k = R.n_reused; k < nv; ++k) P.free_stack[top++] = R.victims[k];
         C->resident = A.resident;
         C->pinned = A.pinned;
+        A.pin_c = A.pinned;
         C->free_top = top;
         A.free_top = top;
         C->n_ev = ev0 + nv;
@@ -2862,6 +2891,7 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
             A.tick = a.tick_base;
             A.free_top = C->free_top;  // (the replay prologue's free-stack reads need it: one round earlier)
             A.n_ev_c = C->n_ev;
+            A.pin_c = C->pinned;
             A.tq_e = C->tq_erase;
             A.tq_i = C->tq_insert;
             for (int k = 0; k < kPhases; ++k) A.ph[k] = 0;
@@ -2979,10 +3009,9 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
                         o[0] = t0;
                         o[1] = t1;
                         o[2] = t2;
-                        const unsigned long long h = table_home(key, P.tmask);
-                        unsigned long long n = 0;
-                        while (n < 4096 && P.table[(h + n) & P.tmask].key != key && P.table[(h + n) & P.tmask].slot != kSlotEmpty) ++n;
-                        o[3] = (n << 32) | (f_slot[q] == kNoSlot ? 1ull : 0ull);
+                        // the same find again (now an L2 hit): its time against the first one's
+                        const unsigned int s2 = table_find_line(P, key);
+                        o[3] = s2 != 0xFFFFFFFEu ? gtimer() : 0ull;
                     }
                 } else if (q < nf + nuv) {
                     const int i = q - nf;
@@ -3013,7 +3042,10 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
                 }
             }
             dec = block_sum(dec, Red);  // (its barriers also publish the overlay and the U list)
-            if (tid == 0) C->pinned -= dec;
+            if (tid == 0) {
+                C->pinned -= dec;
+                A.pin_c -= dec;
+            }
             pstamp(P, 1);
             pf_issue2();
             long long reused = 0;
@@ -3084,7 +3116,10 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
                     }
                 }
                 dec = block_sum(dec, Red);
-                if (tid == 0) C->pinned -= dec;
+                if (tid == 0) {
+                C->pinned -= dec;
+                A.pin_c -= dec;
+            }
                 __syncthreads();
             }
             pstamp(P, 2);
@@ -3114,7 +3149,7 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
         need = block_sum(need, Red);
         miss_min = block_min(miss_min, Red);
         if (tid == 0) A.needed = (int)need;
-        if ((a.flags & kFeasible) && C->pinned + need > P.cap) {
+        if ((a.flags & kFeasible) && A.pin_c + need > P.cap) {
             if (tid == 0) A.started = 0;  // try_start_head: wait for in-flight pins to clear
         }
         __syncthreads();
@@ -3155,7 +3190,7 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
             }
             if (tid == 0) {
                 int an = (a.flags & kAdmit) ? n : 0;
-                const long long room = P.cap - C->pinned;
+                const long long room = P.cap - A.pin_c;
                 if (a.flags & kTruncate) an = (int)room;
                 if (a.flags & kWarmupRoom) an = (int)min((long long)n, room);
                 A.admit_n = an;
@@ -3490,7 +3525,10 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
                 }
             }
             dec = block_sum(dec, Red);
-            if (tid == 0) C->pinned -= dec;
+            if (tid == 0) {
+                C->pinned -= dec;
+                A.pin_c -= dec;
+            }
         }
         __syncthreads();
         queue_ready(P, a, A);  // (an admission that applied nothing: the counters are reset here)

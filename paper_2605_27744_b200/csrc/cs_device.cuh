@@ -107,12 +107,19 @@ constexpr int kSvcQ = 1, kSvcL = 2, kSvcB = 3, kStream0 = 4;
 // The learner service's result for CTA 0 (service_learner): observe(AgentDispatch{prev, next})
 // computed on the learner state as this dispatch's record will leave it, committed by CTA 0 only
 // if the request starts. The BFS hops go to DevPool::spec_hop.
+// Every 16-byte word carries the admission's seq next to its payload, so CTA 0 reads the whole
+// result in one round of 16-byte loads and knows it is this admission's (no flag round trip).
 struct LearnSpec {
+    unsigned long long seq0;
     int changed;              // CacheSagePolicy::current_ != next: the reachability was rebuilt
-    int oa, ob;               // the window pair the record pushes out of a full window (else -1)
+    int oa;
+    unsigned long long seq1;
+    int ob;                   // (oa, ob): the window pair the record pushes out of a full window
     int best_b;               // argmax_row(next) after the record (-1: no positive count)
+    unsigned long long seq2;
     unsigned int best_c, total_next;
 };
+static_assert(sizeof(LearnSpec) == 48, "three tagged 16-byte words");
 constexpr int kRawCap = 6144;  // raw prescan candidates per streaming CTA (its staging capacity)
 // header of one streaming CTA's raw prescan output
 struct RawHdr {
@@ -247,7 +254,7 @@ struct DevPool {
 
     Ctrl* ctrl;
     LearnSpec* spec;        // the learner service's speculative observe (Ctrl::svc_b_seq)
-    unsigned char* spec_hop;  // [a_cap] its BFS hops
+    ulonglong2* spec_hop;     // [a_cap / 8]: {seq, 8 BFS hops} per 16-byte word
 
     // raw prescan output, per launch parity and streaming CTA: the CTA's staged candidates in
     // staging order ([2][raw_grid][kRawCap] lt / slot / list id / agent) and its header

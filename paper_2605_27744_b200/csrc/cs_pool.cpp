@@ -236,7 +236,9 @@ void cs_pool::create(const cs_pool_cfg& c, long long shard_slots, cs_comm* cm) {
         trap_word_host = trap_word;
     }
     P.spec = dmalloc<csb::LearnSpec>(1, "learner service");
-    P.spec_hop = dmalloc<unsigned char>(P.a_cap, "learner service hops");
+    P.spec_hop = dmalloc<ulonglong2>((P.a_cap + 7) / 8, "learner service hops");
+    ck(cudaMemset(P.spec, 0, sizeof(csb::LearnSpec)), "memset");
+    ck(cudaMemset(P.spec_hop, 0, sizeof(ulonglong2) * ((P.a_cap + 7) / 8)), "memset");
     if (const char* e = std::getenv("CS_SERVER")) server = std::atoi(e) != 0;
     if (const char* e = std::getenv("CS_SERVER_GENERIC")) server_generic = std::atoi(e) != 0;
     ck(csb::launch_init_pool(p, stream), "init_pool");
@@ -255,7 +257,7 @@ void cs_pool::destroy() {
                     p.sh_send1, p.sh_recv1, p.sh_send2, p.sh_recv2, p.sh_state, p.sh_gslot, p.sh_grefs0,
                     p.pl_lt, p.pl_slot, p.pl_agent, p.pl_ok, p.pl_key, p.pl_n, p.pl_T, p.pre_hint,
                     p.raw_lt, p.raw_slot, p.raw_list, p.raw_agent, p.raw_hdr,
-                    (void*)p.spec, p.spec_hop, p.bel_nu, p.bel_kid, p.bel_kid_slot, (void*)p.bel_ref, (void*)p.bel_ref_off, (void*)p.bel_depth,
+                    (void*)p.spec, (void*)p.spec_hop, p.bel_nu, p.bel_kid, p.bel_kid_slot, (void*)p.bel_ref, (void*)p.bel_ref_off, (void*)p.bel_depth,
                     (void*)p.bel_kid_of, p.bel_hi, p.bel_lo, p.bel_cand, p.bel_ctl};
     for (void* q : ptrs)
         if (q) cudaFree(q);

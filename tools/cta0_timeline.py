@@ -41,11 +41,10 @@ for it in range(40):
     dsub.append(((per[0, 10:16] - ent) / 1e3))
     if os.environ.get("CS_DEBUG_WARPS"):
         full = np.array(buf[:16 * g + 256], dtype=np.int64)
-        fnd.append([(full[16 * g + 100 + 4 * w + k] - ent) / 1e3 for w in range(3) for k in range(3)] +
-                   [full[16 * g + 100 + 4 * w + 3] >> 32 for w in range(3)] + [full[16 * g + 100 + 4 * w + 3] & 1 for w in range(3)])
+        fnd.append([(full[16 * g + 100 + 4 * w + k] - ent) / 1e3 for w in range(3) for k in range(4)])
         wr.append(np.concatenate([(full[16 * g + 48:16 * g + 65] - ent) / 1e3, (full[16 * g + 72:16 * g + 89] - ent) / 1e3]))
     svc.append([(per[1, 6] - ent) / 1e3, (per[1, 7] - ent) / 1e3, (per[2, 6] - ent) / 1e3, (per[2, 7] - ent) / 1e3,
-                (per[2, 8] - ent) / 1e3])
+                (per[2, 8] - ent) / 1e3] + [(per[3, c] - ent) / 1e3 for c in (6, 7, 8, 9)])
     # streaming CTAs 4..: start, stream end, writeout end (= verdict wait start), verdict seen
     ends.append([((per[4:, c] - ent) / 1e3).max() for c in (0, 1, 4, 5)])
 # the admission server's trace ring over runs of 8 consecutive admissions (one server launch)
@@ -72,11 +71,10 @@ if wr:
     print("phase 0 round 1, per warp end (us):", " ".join("%.1f" % x for x in w[:17]))
     print("phase 0 round 2, per warp end (us):", " ".join("%.1f" % x for x in w[17:]))
     f = np.array(fnd)
-    print("finds (lane 0 of warps 0-2): start / key loaded / found (us), probe distance, miss:")
+    print("finds (lane 0 of warps 0-2): start / key loaded / found / found again (us):")
     for k in range(3):
-        print("  warp %d: %.2f %.2f %.2f  dist median %.0f max %.0f  miss frac %.2f" % (
-            k, np.median(f[:, 3 * k]), np.median(f[:, 3 * k + 1]), np.median(f[:, 3 * k + 2]),
-            np.median(f[:, 9 + k]), f[:, 9 + k].max(), f[:, 12 + k].mean()))
+        print("  warp %d: %.2f %.2f %.2f %.2f" % (k, np.median(f[:, 4 * k]), np.median(f[:, 4 * k + 1]),
+                                                np.median(f[:, 4 * k + 2]), np.median(f[:, 4 * k + 3])))
 print("replay_apply sub-phases (us from CTA 0 entry): start %.2f lists %.2f bulk decided %.2f prep %.2f victim keys %.2f end %.2f"
       % tuple(ds))
 for k in [0, 1, 2, 3, 13, 14, 4, 5, 6, 7, 9, 10, 11, 12]:
@@ -85,7 +83,8 @@ e = np.median(np.array(ends), axis=0)
 print("streaming CTAs (max over CTAs): start %.2f stream end %.2f writeout %.2f verdict seen %.2f us" % tuple(e))
 sv = np.median(np.array(svc), axis=0)
 print("service CTA 1 (table queue): start %.2f done %.2f us; CTA 2 (lists): start %.2f gathered %.2f published %.2f us"
-      % tuple(sv))
+      % tuple(sv[:5]))
+print("learner service CTA 3: start %.2f window loaded %.2f BFS done %.2f published %.2f us" % tuple(sv[5:]))
 if srv:
     v = np.median(np.array(srv), axis=0)
     print("admission server, us after the pickup (median over %d consecutive pairs):" % len(srv))
