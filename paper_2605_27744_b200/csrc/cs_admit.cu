@@ -303,7 +303,7 @@ __device__ void observe_dispatch(const DevPool& P, int prev, int next, unsigned 
     // K3: TransitionLearner::record (transition_learner.cpp:22-51): one pair per dispatch
     if (prev >= 0 && tid == 0) {
         const long long head = C->win_head, size = C->win_size;
-        C->recorded += 1ull;
+        atomicAdd(&C->recorded, 1ull);
         if (prefetched) {  // the new pair's count and row total (the BFS below needs them)
             BfsSmem& Bq = *reinterpret_cast<BfsSmem*>(dsm);
             Bq.rec_c = atomicAdd(&P.counts[(long long)prev * Acap + next], 1u);
@@ -340,7 +340,7 @@ __device__ void observe_dispatch(const DevPool& P, int prev, int next, unsigned 
             if (cls_smem) cls_smem[x] = B.hop[x];
         }
         if (tid == 0) {
-            C->rebuilds += 1ull;
+            atomicAdd(&C->rebuilds, 1ull);
             C->reach_built = 1;
         }
         __syncthreads();
@@ -393,7 +393,7 @@ __device__ void observe_dispatch(const DevPool& P, int prev, int next, unsigned 
             if (cls_smem) cls_smem[x] = B.hop[x];  // the admission kernel's class table on chip
         }
         if (tid == 0) {
-            C->rebuilds += 1ull;
+            atomicAdd(&C->rebuilds, 1ull);
             C->reach_built = 1;
         }
         __syncthreads();
@@ -645,7 +645,7 @@ __device__ void commit_observe(const DevPool& P, const AdmitArgs& a, unsigned lo
     if (tid == 0) {
         if (prev >= 0) {  // record: fire-and-forget count updates, the window ring
             const long long head = A.pf_head, size = A.pf_size;
-            C->recorded += 1ull;
+            atomicAdd(&C->recorded, 1ull);
             atomicAdd(&P.counts[(long long)prev * Acap + next], 1u);
             atomicAdd(&P.totals[prev], 1u);
             if (size == W) {
@@ -663,7 +663,7 @@ __device__ void commit_observe(const DevPool& P, const AdmitArgs& a, unsigned lo
         }
         C->cur_agent = next;
         if (sp.changed) {
-            C->rebuilds += 1ull;
+            atomicAdd(&C->rebuilds, 1ull);
             C->reach_built = 1;
         }
         // maybe_prefetch on argmax_row(next) of the recorded learner
@@ -3043,8 +3043,8 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
             }
             dec = block_sum(dec, Red);  // (its barriers also publish the overlay and the U list)
             if (tid == 0) {
-                C->pinned -= dec;
                 A.pin_c -= dec;
+                C->pinned = A.pin_c;  // (a store, not a read-modify-write round trip)
             }
             pstamp(P, 1);
             pf_issue2();
@@ -3117,8 +3117,8 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
                 }
                 dec = block_sum(dec, Red);
                 if (tid == 0) {
-                C->pinned -= dec;
                 A.pin_c -= dec;
+                C->pinned = A.pin_c;  // (a store, not a read-modify-write round trip)
             }
                 __syncthreads();
             }
@@ -3258,8 +3258,8 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
         } else {
             if (tid == 0) {  // this launch's scoring pass is the prescan
                 A.scans += 1;
-                C->scans += 1;
-                C->scanned_slots += P.cap;
+                atomicAdd(reinterpret_cast<unsigned long long*>(&C->scans), 1ull);
+                atomicAdd(reinterpret_cast<unsigned long long*>(&C->scanned_slots), (unsigned long long)P.cap);
                 A.need_full = 0;
             }
             __syncthreads();
@@ -3278,9 +3278,9 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
                 if (tid == 0) {
                     if (ok && !A.need_full) {
                         A.chunk = 1;
-                        C->pre_used += 1;
+                        atomicAdd(reinterpret_cast<unsigned long long*>(&C->pre_used), 1ull);
                     } else {
-                        C->pre_fallbacks += 1;
+                        atomicAdd(reinterpret_cast<unsigned long long*>(&C->pre_fallbacks), 1ull);
                     }
                 }
                 __syncthreads();
@@ -3316,8 +3316,8 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
             need_scan0 = C->resident + absent > P.cap ? 1 : 0;
             if (tid == 0) {
                 A.scans += 1;
-                C->scans += 1;
-                C->scanned_slots += P.cap;
+                atomicAdd(reinterpret_cast<unsigned long long*>(&C->scans), 1ull);
+                atomicAdd(reinterpret_cast<unsigned long long*>(&C->scanned_slots), (unsigned long long)P.cap);
                 C->keep = keep0;  // a rescan of this chunk keeps the same candidate count
             }
         }
@@ -3439,8 +3439,8 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
                     C->keep = hi - lo;
                     if (need_scan) {
                         A.scans += 1;
-                        C->scans += 1;
-                        C->scanned_slots += P.cap;
+                        atomicAdd(reinterpret_cast<unsigned long long*>(&C->scans), 1ull);
+                        atomicAdd(reinterpret_cast<unsigned long long*>(&C->scanned_slots), (unsigned long long)P.cap);
                     }
                 }
             }
@@ -3506,8 +3506,8 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
     }
     if (pre_run && !pre_avail && blockIdx.x == 0 && tid == 0) {
         A.scans += 1;
-        C->scans += 1;
-        C->scanned_slots += P.cap;
+        atomicAdd(reinterpret_cast<unsigned long long*>(&C->scans), 1ull);
+        atomicAdd(reinterpret_cast<unsigned long long*>(&C->scanned_slots), (unsigned long long)P.cap);
     }
 
     // ---- epilogue (CTA 0): EngineSim::admit unpins at once; pins out; status
@@ -3526,8 +3526,8 @@ __device__ __forceinline__ void admit_body(const DevPool& P, const AdmitArgs& a,
             }
             dec = block_sum(dec, Red);
             if (tid == 0) {
-                C->pinned -= dec;
                 A.pin_c -= dec;
+                C->pinned = A.pin_c;  // (a store, not a read-modify-write round trip)
             }
         }
         __syncthreads();
