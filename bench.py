@@ -187,13 +187,18 @@ def lib_sha16():
 def load_traffic(pool):
     """DRAM bytes (read + write) per admission of the dominant kernel from the committed ncu
     capture (profiles/ncu_admit_summary.json), only if that capture was taken on THIS build of
-    the library (its so_sha16) and this pool size; else None."""
+    the library (the sources' src_sha16, or the .so's so_sha16) and this pool size; else None."""
+    from paper_2605_27744_b200.build import src_sha16
+
     p = os.path.join(ROOT, "profiles", "ncu_admit_summary.json")
     try:
         with open(p) as f:
             d = json.load(f)
-        if d.get("pool_blocks") == pool and d.get("so_sha16") == lib_sha16():
-            return d.get("dram_bytes_per_launch"), d.get("so_sha16")
+        if d.get("pool_blocks") == pool:
+            if d.get("src_sha16") and d["src_sha16"] == src_sha16():
+                return d.get("dram_bytes_per_launch"), "src:" + d["src_sha16"]
+            if d.get("so_sha16") == lib_sha16():
+                return d.get("dram_bytes_per_launch"), "so:" + d["so_sha16"]
     except Exception:
         pass
     return None, None

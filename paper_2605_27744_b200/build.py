@@ -44,6 +44,23 @@ def _stale(target, sources):
     return any(os.path.getmtime(s) > t for s in sources)
 
 
+def src_sha16() -> str:
+    """sha256 prefix over every source and header compiled into the library plus this file (the
+    flags): identifies a build by its inputs, so a committed ncu capture stays bound to it when
+    nvcc's output bytes differ between containers."""
+    import hashlib
+
+    h = hashlib.sha256()
+    files = sorted(f for f in os.listdir(CSRC) if f.endswith((".cu", ".cuh", ".cpp", ".hpp", ".h", ".map")))
+    paths = [os.path.join(CSRC, f) for f in files] + [os.path.join(ROOT, "include", "cachesage_b200.h"),
+                                                      os.path.abspath(__file__)]
+    for p in paths:
+        h.update(os.path.basename(p).encode() + b"\0")
+        with open(p, "rb") as f:
+            h.update(f.read())
+    return h.hexdigest()[:16]
+
+
 def build(verbose: bool = False, force: bool = False) -> str:
     os.makedirs(OUT_DIR, exist_ok=True)
     inc = ["-I", os.path.join(ROOT, "include"), "-I", CSRC]

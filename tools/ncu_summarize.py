@@ -26,6 +26,13 @@ def lib_sha16():
         return hashlib.sha256(f.read()).hexdigest()[:16]
 
 
+def src_sha16():
+    sys.path.insert(0, ROOT)
+    from paper_2605_27744_b200.build import src_sha16 as f
+
+    return f()
+
+
 def raw_metrics(rep):
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
@@ -67,6 +74,7 @@ def main():
     out = {
         "kernel": "csb::admit_kernel(DevPool, AdmitArgs)",
         "so_sha16": lib_sha16(),
+        "src_sha16": src_sha16(),
         "round": 2,
         "command": "CS_SERVER=0 ncu --set full --import-source on --clock-control none -k regex:admit_kernel -s 1600 -c 1 "
                    "python tools/ncu_admit.py --skip 1600 --n 2",
