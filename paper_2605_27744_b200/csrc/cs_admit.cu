@@ -1266,13 +1266,35 @@ __device__ void scan_pass(const DevPool& P, int NL, int keep, const ScanBufs& B,
                 const long long i0 = lo + (long long)t * TV + (long long)tid * kV;
                 const unsigned char* st = ring + (size_t)s * kRingStage;
                 mbar_wait(&S.mbar[s], (unsigned int)((t / kRing) & 1));
-                unsigned long long x4[kV];
-                unsigned int a4[kV], r4[kV];
-                read4(st, tid, i0 + kV <= hi, x4, a4, r4);
+                // classify the packed words as they sit in the stage (no decode; thresholds
+                // clamped below the free tick, so a free slot never passes a compare)
+                const ulonglong2 w01 = *reinterpret_cast<const ulonglong2*>(st + (size_t)tid * 32);
+                const ulonglong2 w23 = *reinterpret_cast<const ulonglong2*>(st + (size_t)tid * 32 + 16);
                 __syncwarp();
                 if (lane_id() == 0) mbar_arrive(&S.mbar_empty[s]);  // stage s consumed by this warp
+                const unsigned long long w[kV] = {w01.x, w01.y, w23.x, w23.y};
+                const unsigned long long cR = min(thr[R], kPkFree - 1ull), cE = min(thr[E], kPkFree - 1ull);
+                unsigned long long x4[kV];
                 int cl[kV];
-                unsigned int acc = classify4(x4, a4, r4, thr[R], thr[E], thr, cls, E, cl);
+                unsigned int acc = 0u;
+#pragma unroll
+                for (int k = 0; k < kV; ++k) {
+                    const unsigned long long x = w[k] & kPkLtMask;
+                    const unsigned int ag = (unsigned int)((w[k] >> 40) & kPkNoAgent);
+                    x4[k] = x;
+                    cl[k] = E;
+                    acc |= (unsigned int)(x <= cR) << k;
+                    if ((long long)w[k] >= 0) {  // unpinned
+                        if (ag == (unsigned int)kPkNoAgent) {
+                            acc |= (unsigned int)(x <= cE) << (kV + k);
+                        } else {  // agent-carrying (rare in real pools)
+                            const int c = cls[ag];
+                            cl[k] = c;
+                            acc |= (unsigned int)(x <= min(thr[c], kPkFree - 1ull)) << (kV + k);
+                        }
+                    }
+                }
+                if (i0 + kV > hi) acc = 0u;
                 append4(acc, x4, cl, i0, R, B, S, true);
             }
         }

@@ -124,9 +124,10 @@ struct CallbackComm : cs_comm {
 };
 
 // ------------------------------------------------------------------ peer memory (fused exchange)
-// Each rank owns a window (2 parity slots x world x cap bytes) and world flag words on its own
-// device; every rank maps every peer's window and flags (same process: plain pointers with peer
-// access enabled between distinct devices; other processes: CUDA IPC handles). An exchange is one
+// Each rank owns a window (2 parity slots x world x cap bytes) and one flag word per source rank
+// and message part on its own device; every rank maps every peer's window and flags (same
+// process: plain pointers with peer access enabled between distinct devices; other processes:
+// CUDA IPC handles). An exchange is one
 // stream-ordered kernel (csb::launch_peer_allgather): no host round trip, no NCCL.
 struct PeerComm : cs_comm {
     int device = 0;
@@ -172,7 +173,9 @@ struct PeerComm : cs_comm {
         if (!connected) return;
         const unsigned long long poison = ~0ull;
         for (int p = 0; p < world; ++p)
-            if (t.flags[p]) cudaMemcpy(t.flags[p] + rank, &poison, 8, cudaMemcpyHostToDevice);
+            if (t.flags[p])
+                for (int q = 0; q < csb::kPeerParts; ++q)
+                    cudaMemcpy(t.flags[p] + rank * csb::kPeerParts + q, &poison, 8, cudaMemcpyHostToDevice);
     }
     ~PeerComm() override {
         for (void* q : ipc_opened) cudaIpcCloseMemHandle(q);
@@ -190,8 +193,9 @@ PeerComm* peer_new(int rank, int world, int device, size_t cap) {
     c->cap = (cap + 15) & ~size_t(15);
     try {
         ck(cudaMalloc(reinterpret_cast<void**>(&c->my_win), 2 * (size_t)world * c->cap), "cudaMalloc(peer window)");
-        ck(cudaMalloc(reinterpret_cast<void**>(&c->my_flags), 8 * (size_t)csb::kMaxShards), "cudaMalloc(peer flags)");
-        ck(cudaMemset(c->my_flags, 0, 8 * (size_t)csb::kMaxShards), "memset");
+        const size_t fbytes = 8 * (size_t)csb::kMaxShards * csb::kPeerParts;
+        ck(cudaMalloc(reinterpret_cast<void**>(&c->my_flags), fbytes), "cudaMalloc(peer flags)");
+        ck(cudaMemset(c->my_flags, 0, fbytes), "memset");
         ck(cudaDeviceSynchronize(), "peer window");
     } catch (...) {
         delete c;

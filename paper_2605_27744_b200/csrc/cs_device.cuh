@@ -2,6 +2,7 @@
 // shares. See DESIGN.md §3 for the byte layout and the roofline each kernel is held to.
 #pragma once
 
+#include <cstddef>
 #include <cstdint>
 
 namespace csb {
@@ -157,6 +158,11 @@ struct ShardLists {
     int n[kMaxLists];
     ShardCand c[kMaxLists][kChunk + 1];
 };
+// bytes of one shard's list message with NL lists in use: the counts and the first NL lists
+// (the exchange moves only those; receivers index shard r at r * this stride)
+__host__ __device__ __forceinline__ size_t shard_lists_bytes(int NL) {
+    return (offsetof(ShardLists, c) + (size_t)NL * (kChunk + 1) * sizeof(ShardCand) + 15) & ~(size_t)15;
+}
 // replicated admission state (identical on every shard), carried between the admission's kernels
 struct ShardState {
     unsigned long long tick, first_touch;

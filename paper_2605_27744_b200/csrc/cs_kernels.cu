@@ -457,36 +457,43 @@ cudaError_t launch_check_pool(const DevPool& P, unsigned long long* out, cudaStr
     return cudaGetLastError();
 }
 
-// ---- the peer-memory allgather (PeerTable). One CTA per rank p of the group: push this rank's
-// bytes into p's window slot [seq & 1][rank], release p's flag for this rank (system scope:
-// the window is on another GPU), then wait for p's contribution in this rank's own window and
-// copy it to drecv + p * bytes. Windows are double-buffered by exchange parity: a rank can start
+// ---- the peer-memory allgather (PeerTable). kPeerParts CTAs per rank p of the group, each
+// owning one contiguous part of the message: push this rank's part into p's window slot
+// [seq & 1][rank], release p's flag for (this rank, part) (system scope: the window is on
+// another GPU), then wait for p's flag for (p, part) in this rank's own flags and copy p's part
+// to drecv + p * bytes. Windows are double-buffered by exchange parity: a rank can start
 // exchange k + 2 only after every peer finished exchange k + 1, so after every peer read slot
-// k & 1 (all ranks run the same sequence of exchanges).
+// k & 1 (all ranks run the same sequence of exchanges). Parts split the copy over SMs (one CTA
+// moved a 31 KB list exchange at ~1 GB/s: latency-bound) and need no cross-CTA counting.
 // (128 threads, few registers: a CTA of it fits beside a cooperative scan CTA on one SM, so
 // shards that share a GPU in the tests never starve each other's cooperative launches)
 __global__ void __launch_bounds__(128) peer_allgather_kernel(const unsigned char* __restrict__ src, unsigned char* __restrict__ dst,
                                       size_t bytes, PeerTable t, int rank, unsigned long long seq, size_t cap) {
-    const int p = blockIdx.x;
+    const int p = blockIdx.x / kPeerParts, part = blockIdx.x % kPeerParts;
     const int tid = threadIdx.x, T = blockDim.x;
-    const int world = gridDim.x;
+    const int world = gridDim.x / kPeerParts;
     const size_t slot = (size_t)(seq & 1ull) * (size_t)world * cap;
     const bool vec = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst) | bytes | cap) & 15u) == 0;
+    // this CTA's part: 16-byte granules when aligned, else bytes
+    const size_t units = vec ? bytes / 16 : bytes;
+    const size_t per = (units + kPeerParts - 1) / kPeerParts;
+    const size_t u0 = min(units, (size_t)part * per), u1 = min(units, u0 + per);
     {
         unsigned char* d = t.win[p] + slot + (size_t)rank * cap;
         if (vec) {
             const uint4* s4 = reinterpret_cast<const uint4*>(src);
             uint4* d4 = reinterpret_cast<uint4*>(d);
-            for (size_t i = tid; i < bytes / 16; i += T) d4[i] = s4[i];
+            for (size_t i = u0 + tid; i < u1; i += T) d4[i] = s4[i];
         } else {
-            for (size_t i = tid; i < bytes; i += T) d[i] = src[i];
+            for (size_t i = u0 + tid; i < u1; i += T) d[i] = src[i];
         }
     }
     __syncthreads();
     if (tid == 0) {
         __threadfence_system();
-        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(t.flags[p] + rank), "l"(seq) : "memory");
-        const unsigned long long* mine = t.flags[rank] + p;
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(t.flags[p] + rank * kPeerParts + part), "l"(seq)
+                     : "memory");
+        const unsigned long long* mine = t.flags[rank] + p * kPeerParts + part;
         unsigned long long spins = 0, v;
         for (;;) {
             asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(mine) : "memory");
@@ -503,9 +510,9 @@ __global__ void __launch_bounds__(128) peer_allgather_kernel(const unsigned char
         if (vec) {
             const uint4* w4 = reinterpret_cast<const uint4*>(w);
             uint4* d4 = reinterpret_cast<uint4*>(d);
-            for (size_t i = tid; i < bytes / 16; i += T) d4[i] = __ldcg(w4 + i);
+            for (size_t i = u0 + tid; i < u1; i += T) d4[i] = __ldcg(w4 + i);
         } else {
-            for (size_t i = tid; i < bytes; i += T) d[i] = __ldcg(w + i);
+            for (size_t i = u0 + tid; i < u1; i += T) d[i] = __ldcg(w + i);
         }
     }
 }
@@ -518,8 +525,9 @@ cudaError_t launch_peer_allgather(const void* dsend, void* drecv, size_t bytes, 
                              cudaSharedmemCarveoutMaxShared);
         attr = true;
     }
-    peer_allgather_kernel<<<world, 128, 0, s>>>(static_cast<const unsigned char*>(dsend),
-                                                static_cast<unsigned char*>(drecv), bytes, t, rank, seq, cap);
+    peer_allgather_kernel<<<world * kPeerParts, 128, 0, s>>>(static_cast<const unsigned char*>(dsend),
+                                                             static_cast<unsigned char*>(drecv), bytes, t, rank, seq,
+                                                             cap);
     return cudaGetLastError();
 }
 

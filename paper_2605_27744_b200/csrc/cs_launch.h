@@ -181,9 +181,10 @@ cudaError_t launch_table_rebuild(const DevPool& P, cudaStream_t s);
 // The peer-memory shard exchange (cs_comm.cpp PeerComm): every rank pushes its bytes into every
 // peer's window over NVLink / NVSwitch (or the same device's memory), raises a flag in that
 // peer's memory, then gathers the peers' contributions from its own window into drecv.
+constexpr int kPeerParts = 8;  // CTAs (message parts) per peer in one exchange
 struct PeerTable {
     unsigned char* win[kMaxShards];          // each rank's window, as addressable from this device
-    unsigned long long* flags[kMaxShards];   // each rank's flags (one word per source rank)
+    unsigned long long* flags[kMaxShards];   // each rank's flags (one word per source rank x part)
 };
 cudaError_t launch_peer_allgather(const void* dsend, void* drecv, size_t bytes, const PeerTable& t, int rank,
                                   int world, unsigned long long seq, size_t cap, cudaStream_t s);

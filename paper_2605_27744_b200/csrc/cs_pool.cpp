@@ -359,8 +359,10 @@ const csb::AdmitStatus& cs_pool::admit_sharded_once(const csb::AdmitArgs& in) {
     if (timing) ck(cudaEventRecord(ev0, stream), "cudaEventRecord");
     ck(csb::launch_shard_probe(P, a, stream), "shard probe");
     ++launches;
-    comm->allgather(P.sh_send1, P.sh_recv1, sizeof(csb::ShardHdr) + sizeof(csb::ShardPos) * (size_t)std::max(a.n, 0),
-                    stream);
+    // a pool of one shard exchanges nothing: its kernels read the send buffers (shard_recv1/shard_in)
+    if (P.world > 1)
+        comm->allgather(P.sh_send1, P.sh_recv1,
+                        sizeof(csb::ShardHdr) + sizeof(csb::ShardPos) * (size_t)std::max(a.n, 0), stream);
     ck(csb::launch_shard_decide(P, a, stream), "shard decide");
     ++launches;
     // every possible chunk is enqueued without a host round trip: the kernels read the
@@ -368,7 +370,7 @@ const csb::AdmitStatus& cs_pool::admit_sharded_once(const csb::AdmitArgs& in) {
     const int n_chunks = (std::max(a.n, 1) + csb::kChunk - 1) / csb::kChunk;
     for (int c = 0; c < n_chunks; ++c) {
         ck(csb::launch_shard_scan(P, a, c, lc, stream), "shard scan");
-        comm->allgather(P.sh_send2, P.sh_recv2, sizeof(csb::ShardLists), stream);
+        if (P.world > 1) comm->allgather(P.sh_send2, P.sh_recv2, csb::shard_lists_bytes(P.n_lists), stream);
         ck(csb::launch_shard_replay(P, a, stream), "shard replay");
         launches += 2;
     }

@@ -31,7 +31,24 @@ __device__ __forceinline__ bool own_gslot(const DevPool& P, unsigned int g) {
     return g < kNewRemote && (int)(g >> kShardBits) == P.rank;
 }
 
+// Instrumentation: %globaltimer at sharded-admission phase k (< 18), thread 0 of CTA 0, in the
+// unused words 10..15 of CTAs 8..10's debug rows (tools/shard_timeline.py reads them).
+__device__ __forceinline__ void shstamp(const DevPool& P, int k) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) P.dbg[(8 + k / 6) * 16 + 10 + k % 6] = gtimer();
+}
+
 __device__ __forceinline__ size_t shard_rec1(int n) { return sizeof(ShardHdr) + sizeof(ShardPos) * (size_t)n; }
+
+// The exchanged messages as this shard receives them. A pool of one shard has nothing to
+// exchange: the host skips both exchanges and the receivers read the send buffers.
+__device__ __forceinline__ const unsigned char* shard_recv1(const DevPool& P) {
+    return P.world == 1 ? P.sh_send1 : P.sh_recv1;
+}
+__device__ __forceinline__ const ShardLists* shard_in(const DevPool& P, int r) {
+    const unsigned char* base = P.world == 1 ? reinterpret_cast<const unsigned char*>(P.sh_send2)
+                                             : reinterpret_cast<const unsigned char*>(P.sh_recv2);
+    return reinterpret_cast<const ShardLists*>(base + (size_t)r * shard_lists_bytes(P.n_lists));
+}
 
 // Deferred EngineSim::unpin calls (engine.cpp:170-180) of this shard's slots; kNoSlot entries
 // are positions another shard owns. All threads of one CTA.
@@ -58,8 +75,11 @@ __global__ void __launch_bounds__(512, 1) shard_probe_kernel(DevPool P, AdmitArg
     __shared__ RedSmem Red;
     Ctrl* C = P.ctrl;
     const int tid = threadIdx.x, T = blockDim.x;
+    shstamp(P, 0);
     apply_table_queue(P, Red);
+    shstamp(P, 1);
     shard_unpins(P, a, Red);
+    shstamp(P, 2);
     ShardHdr* hdr = reinterpret_cast<ShardHdr*>(P.sh_send1);
     ShardPos* pos = reinterpret_cast<ShardPos*>(P.sh_send1 + sizeof(ShardHdr));
     for (int i = tid; i < a.n; i += T) {
@@ -78,6 +98,7 @@ __global__ void __launch_bounds__(512, 1) shard_probe_kernel(DevPool P, AdmitArg
         hdr->resident = C->resident;
         hdr->pinned = C->pinned;
     }
+    shstamp(P, 3);
 }
 
 __device__ void shard_write_status(const DevPool& P, const AdmitArgs& a, const ShardState& s) {
@@ -120,6 +141,7 @@ __global__ void __launch_bounds__(512, 1) shard_decide_kernel(DevPool P, AdmitAr
     Ctrl* C = P.ctrl;
     const int tid = threadIdx.x, T = blockDim.x;
     const int G = P.world, n = a.n;
+    shstamp(P, 4);
     if (tid == 0) {
         A.started = 1;
         A.error = 0;
@@ -132,7 +154,7 @@ __global__ void __launch_bounds__(512, 1) shard_decide_kernel(DevPool P, AdmitAr
         A.tick = a.tick_base;
         long long res = 0, pin = 0;
         for (int r = 0; r < G; ++r) {
-            const ShardHdr* h = reinterpret_cast<const ShardHdr*>(P.sh_recv1 + (size_t)r * shard_rec1(n));
+            const ShardHdr* h = reinterpret_cast<const ShardHdr*>(shard_recv1(P) + (size_t)r * shard_rec1(n));
             res += h->resident;
             pin += h->pinned;
         }
@@ -152,7 +174,7 @@ __global__ void __launch_bounds__(512, 1) shard_decide_kernel(DevPool P, AdmitAr
         unsigned int gs = kNoSlot, r0 = 0u;
         for (int r = 0; r < G; ++r) {
             const ShardPos q =
-                reinterpret_cast<const ShardPos*>(P.sh_recv1 + (size_t)r * shard_rec1(n) + sizeof(ShardHdr))[i];
+                reinterpret_cast<const ShardPos*>(shard_recv1(P) + (size_t)r * shard_rec1(n) + sizeof(ShardHdr))[i];
             if (q.gslot != kNoSlot) {
                 gs = q.gslot;
                 r0 = q.refs0;
@@ -226,6 +248,7 @@ __global__ void __launch_bounds__(512, 1) shard_decide_kernel(DevPool P, AdmitAr
         *P.sh_state = s;
         if (!A.started || A.admit_n <= 0) shard_write_status(P, a, s);  // nothing to admit
     }
+    shstamp(P, 5);
 }
 
 // ---- scan: this shard's per-list keep oldest (the single-pool K4 + K5a), packed for exchange 2
@@ -247,6 +270,7 @@ __global__ void __launch_bounds__(kThreads + 32, 1) shard_scan_kernel(DevPool P,
         return;  // uniform across the grid: SS is not written during this kernel
     }
     const int keep = min(kChunk, admit_n - chunk * kChunk);
+    shstamp(P, 6);
     if (tid == 0) {
         S.spec = 0;
         S.cls_ready = 1;
@@ -279,6 +303,7 @@ __global__ void __launch_bounds__(kThreads + 32, 1) shard_scan_kernel(DevPool P,
         __syncthreads();
         scan_pass(P, NL, keep, B, S, Sel, dsm, fast != 0, a);
         grid_barrier(C);
+        shstamp(P, 7);
         int mine = 0;
         for (int l = blockIdx.x; l < NL; l += gridDim.x) {
             finalize_list(P, l, NL, keep, B, Sel);
@@ -302,6 +327,7 @@ __global__ void __launch_bounds__(kThreads + 32, 1) shard_scan_kernel(DevPool P,
             }
         }
         grid_barrier(C);
+        shstamp(P, 8);
         if (*(volatile int*)&C->done) break;
     }
     if (blockIdx.x == 0) {
@@ -329,12 +355,15 @@ __global__ void __launch_bounds__(kThreads + 32, 1) shard_scan_kernel(DevPool P,
             C->rescan = 0;
         }
     }
+    shstamp(P, 9);
 }
 
 struct ShardReplaySmem {
     ReplaySmem R;
     unsigned long long L_key[kMaxLists][kChunk + 2];
     unsigned char vreused[kChunk];  // victim k's slot was reused by a new block of this shard
+    unsigned char own_key[kChunk];  // chunk position i's key lives on this shard
+    int n_in[kMaxShards][kMaxLists];  // received list lengths
     int n_own_erase;
 };
 
@@ -349,6 +378,7 @@ __global__ void __launch_bounds__(512, 1) shard_replay_kernel(DevPool P, AdmitAr
     ShardState* SS = P.sh_state;
     const int tid = threadIdx.x, T = blockDim.x;
     const int NL = P.n_lists, Rl = NL - 1, G = P.world;
+    shstamp(P, 10);
     if (tid == 0) {
         A.tick = SS->tick;
         A.first_touch = SS->first_touch;
@@ -382,6 +412,7 @@ __global__ void __launch_bounds__(512, 1) shard_replay_kernel(DevPool P, AdmitAr
         R.c_refs0[i] = r0;
         R.touched[i] = 0;
         R.pevict[i] = 0;
+        X.own_key[i] = shard_owner(a.keys[lo + i], G) == P.rank ? 1 : 0;
         if (gs == kNoSlot) ++absent;
         else if (r0 == 0u) ++pre_unpinned;
     }
@@ -415,36 +446,43 @@ __global__ void __launch_bounds__(512, 1) shard_replay_kernel(DevPool P, AdmitAr
     // ---- the global lists: per list the keep smallest of the union of the shard lists. Every
     // shard list is sorted and ticks are distinct across shards, so an entry's global rank is
     // its own index plus, per other shard, the number of that shard's entries below it.
-    const ShardLists* in = P.sh_recv2;
+    shstamp(P, 11);
+    // One round over every (list, shard, entry) instead of a round per list.
     for (int l = tid; l < kMaxLists; l += T) R.L_n[l] = 0;
+    for (int q = tid; q < G * kMaxLists; q += T) {
+        const int r = q / kMaxLists, l = q - r * kMaxLists;
+        X.n_in[r][l] = l < NL ? shard_in(P, r)->n[l] : 0;
+    }
     __syncthreads();
     if (scanned) {
-        for (int l = 0; l < NL; ++l) {
-            const int kl = keep_of(l, NL, len);
-            int tot = 0;
-            for (int r = 0; r < G; ++r) tot += in[r].n[l];
-            for (int q = tid; q < G * (kChunk + 1); q += T) {
-                const int r = q / (kChunk + 1), j = q - r * (kChunk + 1);
-                if (j >= in[r].n[l]) continue;
-                const ShardCand c = in[r].c[l][j];
-                int rank = j;
-                for (int o = 0; o < G; ++o) {
-                    if (o == r) continue;
-                    int lo2 = 0, hi2 = in[o].n[l];
-                    while (lo2 < hi2) {
-                        const int mid = (lo2 + hi2) >> 1;
-                        if (in[o].c[l][mid].lt < c.lt) lo2 = mid + 1;
-                        else hi2 = mid;
-                    }
-                    rank += lo2;
+        const int per_list = G * (kChunk + 1);
+        for (int q = tid; q < NL * per_list; q += T) {
+            const int l = q / per_list, q2 = q - l * per_list;
+            const int r = q2 / (kChunk + 1), j = q2 - r * (kChunk + 1);
+            if (j >= X.n_in[r][l]) continue;
+            const ShardCand c = shard_in(P, r)->c[l][j];
+            int rank = j;
+            for (int o = 0; o < G; ++o) {
+                if (o == r) continue;
+                const ShardCand* co = shard_in(P, o)->c[l];
+                int lo2 = 0, hi2 = X.n_in[o][l];
+                while (lo2 < hi2) {
+                    const int mid = (lo2 + hi2) >> 1;
+                    if (co[mid].lt < c.lt) lo2 = mid + 1;
+                    else hi2 = mid;
                 }
-                if (rank < kl) {
-                    R.L_lt[l][rank] = c.lt;
-                    R.L_slot[l][rank] = c.gslot;
-                    X.L_key[l][rank] = c.key;
-                }
+                rank += lo2;
             }
-            if (tid == 0) R.L_n[l] = min(tot, kl);
+            if (rank < keep_of(l, NL, len)) {
+                R.L_lt[l][rank] = c.lt;
+                R.L_slot[l][rank] = c.gslot;
+                X.L_key[l][rank] = c.key;
+            }
+        }
+        for (int l = tid; l < NL; l += T) {
+            int tot = 0;
+            for (int r = 0; r < G; ++r) tot += X.n_in[r][l];
+            R.L_n[l] = min(tot, keep_of(l, NL, len));
         }
     }
     __syncthreads();
@@ -483,6 +521,7 @@ __global__ void __launch_bounds__(512, 1) shard_replay_kernel(DevPool P, AdmitAr
     }
     __syncthreads();
 
+    shstamp(P, 12);
     // ---- the sequential replay of admit_pinned (engine.cpp:141-168), warp 0; lane l owns list l
     if (warp_id() == 0) {
         const int lane = lane_id();
@@ -496,19 +535,26 @@ __global__ void __launch_bounds__(512, 1) shard_replay_kernel(DevPool P, AdmitAr
         int nv = 0, nglob = 0, own_cur = 0;
         int error = 0;
         for (int i = 0; i < len; ++i) {
-            const unsigned int s = R.c_slot[i];
-            if (s != kNoSlot && !R.pevict[i]) {  // resident: touch + pin
-                ++tick;
-                if (lane == 0) {
-                    R.out_slot[i] = s;
-                    R.out_lt[i] = tick;
-                    R.out_new[i] = 0;
-                    R.touched[i] = 1;
+            {  // the run of resident positions from i (touch + pin), up to 32 per round, one lane each:
+               // evictions happen only at absent positions, so the run's flags are settled here
+                const int j = i + lane;
+                const bool res = j < len && R.c_slot[j] != kNoSlot && !R.pevict[j];
+                const unsigned int bal = __ballot_sync(0xffffffffu, res);
+                const int run = bal == 0xffffffffu ? 32 : __ffs(~bal) - 1;
+                if (run > 0) {
+                    if (lane < run) {
+                        R.out_slot[j] = R.c_slot[j];
+                        R.out_lt[j] = tick + 1 + (unsigned long long)lane;
+                        R.out_new[j] = 0;
+                        R.touched[j] = 1;
+                    }
+                    pinned += __popc(__ballot_sync(0xffffffffu, lane < run && R.c_refs0[j] == 0u));
+                    if (first_touch == ~0ull) first_touch = tick + 1;
+                    tick += (unsigned long long)run;
+                    i += run - 1;
+                    __syncwarp();
+                    continue;
                 }
-                if (R.c_refs0[i] == 0u) ++pinned;
-                if (first_touch == ~0ull) first_touch = tick;
-                __syncwarp();
-                continue;
             }
             while (resident >= P.gbudget) {  // evict_one (engine.cpp:102-125)
                 if (lane < NL) {  // skip entries touched (pinned) or evicted via another list
@@ -563,9 +609,8 @@ __global__ void __launch_bounds__(512, 1) shard_replay_kernel(DevPool P, AdmitAr
             if (error) break;
             // the new block lives on its key's shard: that shard reuses its own victims of this
             // chunk first, then its free stack; the other shards only count it
-            const unsigned long long key_i = a.keys[lo + i];
             unsigned int ns = kNewRemote;
-            if (shard_owner(key_i, G) == P.rank) {
+            if (X.own_key[i]) {
                 while (own_cur < nv && !own_gslot(P, R.victims[own_cur])) ++own_cur;
                 if (own_cur < nv) {
                     ns = R.victims[own_cur];
@@ -601,6 +646,7 @@ __global__ void __launch_bounds__(512, 1) shard_replay_kernel(DevPool P, AdmitAr
     }
     __syncthreads();
 
+    shstamp(P, 13);
     // ---- apply: every shard logs every victim; owners erase / free / touch / insert
     const int err = A.error;
     const int nv = R.n_vict;
@@ -694,6 +740,7 @@ __global__ void __launch_bounds__(512, 1) shard_replay_kernel(DevPool P, AdmitAr
         (void)own_reused;
     }
     __syncthreads();
+    shstamp(P, 14);
     // ---- next chunk, or the admission's epilogue (EngineSim::admit unpins at once)
     const int next_lo = hi;
     const bool last = err || next_lo >= A.admit_n;
@@ -732,6 +779,7 @@ __global__ void __launch_bounds__(512, 1) shard_replay_kernel(DevPool P, AdmitAr
         *SS = s;
         if (last) shard_write_status(P, a, s);
     }
+    shstamp(P, 15);
 }
 
 cudaError_t launch_shard_probe(const DevPool& P, const AdmitArgs& a, cudaStream_t s) {
