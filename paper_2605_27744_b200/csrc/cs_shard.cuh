@@ -534,6 +534,8 @@ __global__ void __launch_bounds__(512, 1) shard_replay_kernel(DevPool P, AdmitAr
         long long pinned = A.pinned;
         int nv = 0, nglob = 0, own_cur = 0;
         int error = 0;
+        long long ev_cyc = 0;  // (instrumentation: SM cycles in evict_one loops)
+        const long long loop_t0 = clock64();
         for (int i = 0; i < len; ++i) {
             {  // the run of resident positions from i (touch + pin), up to 32 per round, one lane each:
                // evictions happen only at absent positions, so the run's flags are settled here
@@ -556,6 +558,7 @@ __global__ void __launch_bounds__(512, 1) shard_replay_kernel(DevPool P, AdmitAr
                     continue;
                 }
             }
+            const long long ev_t0 = clock64();
             while (resident >= P.gbudget) {  // evict_one (engine.cpp:102-125)
                 if (lane < NL) {  // skip entries touched (pinned) or evicted via another list
                     while (cursor < my_n) {
@@ -606,6 +609,7 @@ __global__ void __launch_bounds__(512, 1) shard_replay_kernel(DevPool P, AdmitAr
                 --resident;
                 __syncwarp();
             }
+            ev_cyc += clock64() - ev_t0;
             if (error) break;
             // the new block lives on its key's shard: that shard reuses its own victims of this
             // chunk first, then its free stack; the other shards only count it
@@ -633,6 +637,10 @@ __global__ void __launch_bounds__(512, 1) shard_replay_kernel(DevPool P, AdmitAr
             ++pinned;
             if (first_touch == ~0ull) first_touch = tick;
             __syncwarp();
+        }
+        if (lane == 0 && blockIdx.x == 0) {
+            P.dbg[10 * 16 + 14] = (unsigned long long)ev_cyc;
+            P.dbg[10 * 16 + 15] = (unsigned long long)(clock64() - loop_t0) | ((unsigned long long)nv << 48);
         }
         if (lane == 0) {
             A.tick = tick;

@@ -22,6 +22,7 @@ eng = bench.build_engine(W, spec, pool, 0, False, seed, comm=comm)
 eng.run_timed(int(sys.argv[1]) if len(sys.argv) > 1 else 100)
 rows = []
 cta = []
+loop = []
 for it in range(60):
     eng.run_timed(1)
     buf = (C.c_uint64 * (16 * 1024))()
@@ -34,6 +35,7 @@ for it in range(60):
     if st[6] <= st[0] or st[10] <= st[6]:
         continue  # an admission that did not scan
     rows.append((st - st[0]) / 1e3)
+    loop.append([d[10, 14], d[10, 15] & ((1 << 48) - 1), d[10, 15] >> 48, d[0, 14] if False else 0])
     # scanning CTAs: stream start / stream end / flushed / published (us from scan entry), fast pass
     cta.append([((d[:, c] - st[6]) / 1e3).max() for c in (0, 1, 2, 3)] + [d[:, 8].mean(), d[:, 5].mean()])
 r = np.array(rows)
@@ -43,3 +45,6 @@ for k, n in enumerate(NAMES):
 c = np.array(cta)
 print("scan CTAs (max over CTAs, us from scan entry): stream start %.2f, stream end %.2f, flushed %.2f, "
       "published %.2f; fast-pass fraction %.2f; staged candidates per CTA %.1f" % tuple(np.mean(c, axis=0)))
+lp = np.array(loop, dtype=np.float64)
+print("replay loop: %.0f SM cycles, of which %.0f in evict_one loops; %.1f evictions per admission"
+      % (lp[:, 1].mean(), lp[:, 0].mean(), lp[:, 2].mean()))
