@@ -607,7 +607,7 @@ __device__ void service_learner(const DevPool& P, const AdmitArgs& a, unsigned c
 __device__ void commit_observe(const DevPool& P, const AdmitArgs& a, unsigned long long tick, AdmSmem& A,
                                unsigned char* cls_smem) {
     Ctrl* C = P.ctrl;
-    const int tid = threadIdx.x, T = blockDim.x;
+    const int tid = threadIdx.x;
     const long long W = P.window;
     const int Acap = P.a_cap, prev = a.prev, next = a.next, n_agents = a.n_agents;
     __shared__ __align__(16) LearnSpec sp;

@@ -162,6 +162,22 @@ struct PeerComm : cs_comm {
         ck(csb::launch_peer_allgather(dsend, drecv, bytes, t, rank, world, seq, cap, s), "peer allgather");
         if (g) ck(cudaStreamSynchronize(s), "peer exchange");
     }
+    bool fused(csb::PeerTable* out, size_t* c) override {
+        if (!connected || std::getenv("CS_PEER_UNFUSED")) return false;
+        *out = t;
+        *c = cap;
+        return true;
+    }
+    unsigned long long fused_next() override { return ++seq; }
+    void fused_meet(cudaStream_t s) override {
+        if (g) {
+            ck(cudaStreamSynchronize(s), "fused exchange: send ready");
+            g->barrier();
+        }
+    }
+    void fused_end(cudaStream_t s) override {
+        if (g) ck(cudaStreamSynchronize(s), "fused exchange");
+    }
     // a failing shard must not leave its peers spinning: poison its flag in every peer (their
     // exchange kernels then trap with an error instead of waiting forever)
     void abort() override {

@@ -13,6 +13,10 @@
 
 #include <cstddef>
 
+namespace csb {
+struct PeerTable;
+}
+
 struct cs_comm {
     int rank = 0, world = 1;
     virtual ~cs_comm() {}
@@ -22,4 +26,14 @@ struct cs_comm {
     virtual const char* kind() const = 0;
     // this shard failed mid-admission: release (with an error) the peers waiting on it
     virtual void abort() {}
+    // The fused exchange (peer transport only): the admission kernels store into the peers'
+    // windows and wait on their flags themselves (csb::ShardX). fused() fills the table and the
+    // window bytes per rank; fused_next() numbers the next exchange; fused_meet() precedes the
+    // kernel that waits and fused_end() follows it (shards that share a GPU in one process
+    // drain their stream and meet there, so no kernel that waits is queued behind another
+    // shard's cooperative scan).
+    virtual bool fused(csb::PeerTable*, size_t*) { return false; }
+    virtual unsigned long long fused_next() { return 0; }
+    virtual void fused_meet(cudaStream_t) {}
+    virtual void fused_end(cudaStream_t) {}
 };

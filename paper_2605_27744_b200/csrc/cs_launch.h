@@ -142,10 +142,14 @@ long long build_belady_index(const unsigned long long* keys, long long n_flat, c
 
 // Hash-sharded admission (cs_shard.cuh): probe -> exchange 1 -> decide -> per chunk
 // [scan -> exchange 2] -> replay.
+struct ShardX;
 cudaError_t launch_shard_probe(const DevPool& P, const AdmitArgs& a, cudaStream_t s);
 cudaError_t launch_shard_decide(const DevPool& P, const AdmitArgs& a, cudaStream_t s);
-cudaError_t launch_shard_scan(const DevPool& P, const AdmitArgs& a, int chunk, const LaunchCfg& lc, cudaStream_t s);
-cudaError_t launch_shard_replay(const DevPool& P, const AdmitArgs& a, cudaStream_t s);
+// probe + (fused) exchange 1 + decide in one kernel: world 1, or the peer transport
+cudaError_t launch_shard_front(const DevPool& P, const AdmitArgs& a, const ShardX& x, cudaStream_t s);
+cudaError_t launch_shard_scan(const DevPool& P, const AdmitArgs& a, int chunk, const ShardX& x, const LaunchCfg& lc,
+                              cudaStream_t s);
+cudaError_t launch_shard_replay(const DevPool& P, const AdmitArgs& a, const ShardX& x, cudaStream_t s);
 
 cudaError_t launch_init_pool(const DevPool& P, cudaStream_t s);
 cudaError_t launch_hash_prompts(const unsigned int* tokens, const long long* tok_off, int n, int bs, int skip,
@@ -188,6 +192,16 @@ struct PeerTable {
 };
 cudaError_t launch_peer_allgather(const void* dsend, void* drecv, size_t bytes, const PeerTable& t, int rank,
                                   int world, unsigned long long seq, size_t cap, cudaStream_t s);
+// The fused exchange of a sharded admission (peer transport): the admission kernels themselves
+// store their message into the peers' windows and wait on the peers' flags (exchange 1 inside
+// shard_front_kernel, exchange 2 from shard_scan_kernel's CTA 0 to shard_replay_kernel).
+// fused 0: the exchange is an allgather between kernels, or nothing at world 1.
+struct ShardX {
+    PeerTable t;
+    unsigned long long seq;  // this exchange's number (window parity seq & 1, flag value)
+    size_t cap;              // window bytes per source rank
+    int fused;
+};
 cudaError_t launch_check_pool(const DevPool& P, unsigned long long* out, cudaStream_t s);  // out[4], zeroed
 // Applies the block-table updates the last admission queued (before any other table user).
 cudaError_t launch_table_flush(const DevPool& P, cudaStream_t s);

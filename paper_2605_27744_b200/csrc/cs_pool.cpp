@@ -357,21 +357,39 @@ const csb::AdmitStatus& cs_pool::admit_sharded_once(const csb::AdmitArgs& in) {
     a.seq = ++seq;
     st->started = -1;
     if (timing) ck(cudaEventRecord(ev0, stream), "cudaEventRecord");
-    ck(csb::launch_shard_probe(P, a, stream), "shard probe");
-    ++launches;
-    // a pool of one shard exchanges nothing: its kernels read the send buffers (shard_recv1/shard_in)
-    if (P.world > 1)
-        comm->allgather(P.sh_send1, P.sh_recv1,
-                        sizeof(csb::ShardHdr) + sizeof(csb::ShardPos) * (size_t)std::max(a.n, 0), stream);
-    ck(csb::launch_shard_decide(P, a, stream), "shard decide");
-    ++launches;
+    // exchange 1 (probe -> decide) and, per chunk, exchange 2 (scan -> replay). World 1: nothing
+    // to exchange (one front kernel). Peer transport: fused into the admission kernels. Other
+    // transports: an allgather between the kernels.
+    csb::ShardX x{};
+    const bool fz = P.world > 1 && comm->fused(&x.t, &x.cap);
+    const size_t rec1 = sizeof(csb::ShardHdr) + sizeof(csb::ShardPos) * (size_t)std::max(a.n, 0);
+    if (fz && (rec1 > x.cap || csb::shard_lists_bytes(P.n_lists) > x.cap))
+        throw CsError(CS_ERR_CAPACITY, "peer exchange: message exceeds the window capacity");
+    if (P.world == 1 || fz) {
+        if (fz) {
+            x.fused = 1;
+            x.seq = comm->fused_next();
+            comm->fused_meet(stream);
+        }
+        ck(csb::launch_shard_front(P, a, x, stream), "shard front");
+        ++launches;
+        if (fz) comm->fused_end(stream);
+    } else {
+        ck(csb::launch_shard_probe(P, a, stream), "shard probe");
+        comm->allgather(P.sh_send1, P.sh_recv1, rec1, stream);
+        ck(csb::launch_shard_decide(P, a, stream), "shard decide");
+        launches += 2;
+    }
     // every possible chunk is enqueued without a host round trip: the kernels read the
     // replicated state (admit_n, need_scan) and no-op past the admission's end
     const int n_chunks = (std::max(a.n, 1) + csb::kChunk - 1) / csb::kChunk;
     for (int c = 0; c < n_chunks; ++c) {
-        ck(csb::launch_shard_scan(P, a, c, lc, stream), "shard scan");
-        if (P.world > 1) comm->allgather(P.sh_send2, P.sh_recv2, csb::shard_lists_bytes(P.n_lists), stream);
-        ck(csb::launch_shard_replay(P, a, stream), "shard replay");
+        if (fz) x.seq = comm->fused_next();
+        ck(csb::launch_shard_scan(P, a, c, x, lc, stream), "shard scan");
+        if (fz) comm->fused_meet(stream);
+        else if (P.world > 1) comm->allgather(P.sh_send2, P.sh_recv2, csb::shard_lists_bytes(P.n_lists), stream);
+        ck(csb::launch_shard_replay(P, a, x, stream), "shard replay");
+        if (fz) comm->fused_end(stream);
         launches += 2;
     }
     if (timing) ck(cudaEventRecord(ev1, stream), "cudaEventRecord");

@@ -39,15 +39,63 @@ __device__ __forceinline__ void shstamp(const DevPool& P, int k) {
 
 __device__ __forceinline__ size_t shard_rec1(int n) { return sizeof(ShardHdr) + sizeof(ShardPos) * (size_t)n; }
 
-// The exchanged messages as this shard receives them. A pool of one shard has nothing to
-// exchange: the host skips both exchanges and the receivers read the send buffers.
-__device__ __forceinline__ const unsigned char* shard_recv1(const DevPool& P) {
-    return P.world == 1 ? P.sh_send1 : P.sh_recv1;
+// ---- the fused exchange (peer transport, ShardX.fused): one CTA of an admission kernel stores
+// this shard's message into every peer's window slot [seq & 1][rank] over NVLink / NVSwitch and
+// releases the peer's flag word for this rank (system scope); a later kernel of the same
+// admission waits for every peer's flag and reads the peers' messages in place. A window slot
+// is reused two exchanges later, by which time every peer has waited on the exchange between,
+// so it has finished reading (every shard runs the same sequence of exchanges, and waits in each).
+__device__ __forceinline__ const unsigned char* fx_msg(const DevPool& P, const ShardX& X, int r) {
+    return X.t.win[P.rank] + (size_t)(X.seq & 1ull) * (size_t)P.world * X.cap + (size_t)r * X.cap;
 }
-__device__ __forceinline__ const ShardLists* shard_in(const DevPool& P, int r) {
-    const unsigned char* base = P.world == 1 ? reinterpret_cast<const unsigned char*>(P.sh_send2)
-                                             : reinterpret_cast<const unsigned char*>(P.sh_recv2);
-    return reinterpret_cast<const ShardLists*>(base + (size_t)r * shard_lists_bytes(P.n_lists));
+
+// All threads of the CTA; bytes a multiple of 8.
+__device__ void fx_push(const DevPool& P, const ShardX& X, const unsigned char* src, size_t bytes) {
+    const size_t off = (size_t)(X.seq & 1ull) * (size_t)P.world * X.cap + (size_t)P.rank * X.cap;
+    const unsigned long long* s8 = reinterpret_cast<const unsigned long long*>(src);
+    for (int p = 0; p < P.world; ++p) {
+        if (p == P.rank) continue;
+        unsigned long long* d8 = reinterpret_cast<unsigned long long*>(X.t.win[p] + off);
+        for (size_t i = threadIdx.x; i < bytes / 8; i += blockDim.x) d8[i] = s8[i];
+    }
+    __threadfence_system();
+    __syncthreads();
+    const int p = (int)threadIdx.x;
+    if (p < P.world && p != P.rank)
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(X.t.flags[p] + P.rank * kPeerParts), "l"(X.seq)
+                     : "memory");
+}
+
+// All threads of the CTA: returns once every peer's message of exchange X.seq is in this
+// shard's window.
+__device__ void fx_wait(const DevPool& P, const ShardX& X) {
+    const int p = (int)threadIdx.x;
+    if (p < P.world && p != P.rank) {
+        const unsigned long long* f = X.t.flags[P.rank] + p * kPeerParts;
+        unsigned long long spins = 0, v;
+        for (;;) {
+            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(f) : "memory");
+            if (v == ~0ull) trap_at(404);  // the peer aborted its admission (PeerComm::abort)
+            if (v >= X.seq) break;
+            if (++spins > 64) __nanosleep(100);
+            if (spins > (1ull << 27)) trap_at(403);
+        }
+    }
+    __syncthreads();
+}
+
+// The exchanged messages as this shard reads them: its own from its send buffer; a peer's from
+// this shard's window (fused) or the allgathered receive buffer.
+__device__ __forceinline__ const unsigned char* shard_rec1_of(const DevPool& P, const ShardX& X, int r, int n) {
+    if (r == P.rank) return P.sh_send1;
+    if (X.fused) return fx_msg(P, X, r);
+    return P.sh_recv1 + (size_t)r * shard_rec1(n);
+}
+__device__ __forceinline__ const ShardLists* shard_in(const DevPool& P, const ShardX& X, int r) {
+    if (r == P.rank) return P.sh_send2;
+    if (X.fused) return reinterpret_cast<const ShardLists*>(fx_msg(P, X, r));
+    return reinterpret_cast<const ShardLists*>(reinterpret_cast<const unsigned char*>(P.sh_recv2) +
+                                               (size_t)r * shard_lists_bytes(P.n_lists));
 }
 
 // Deferred EngineSim::unpin calls (engine.cpp:170-180) of this shard's slots; kNoSlot entries
@@ -71,8 +119,7 @@ __device__ void shard_unpins(const DevPool& P, const AdmitArgs& a, RedSmem& Red)
 }
 
 // ---- probe: this shard's part of EngineSim::lookup / try_start_head (engine.cpp:127-139, 337-346)
-__global__ void __launch_bounds__(512, 1) shard_probe_kernel(DevPool P, AdmitArgs a) {
-    __shared__ RedSmem Red;
+__device__ void shard_probe_body(const DevPool& P, const AdmitArgs& a, RedSmem& Red) {
     Ctrl* C = P.ctrl;
     const int tid = threadIdx.x, T = blockDim.x;
     shstamp(P, 0);
@@ -99,6 +146,11 @@ __global__ void __launch_bounds__(512, 1) shard_probe_kernel(DevPool P, AdmitArg
         hdr->pinned = C->pinned;
     }
     shstamp(P, 3);
+}
+
+__global__ void __launch_bounds__(512, 1) shard_probe_kernel(DevPool P, AdmitArgs a) {
+    __shared__ RedSmem Red;
+    shard_probe_body(P, a, Red);
 }
 
 __device__ void shard_write_status(const DevPool& P, const AdmitArgs& a, const ShardState& s) {
@@ -134,10 +186,8 @@ __device__ long long shard_absent(const DevPool& P, int lo, int hi, RedSmem& Red
 }
 
 // ---- decide: replicated feasibility, observe and lookup (the single-pool phase 0)
-__global__ void __launch_bounds__(512, 1) shard_decide_kernel(DevPool P, AdmitArgs a) {
-    extern __shared__ __align__(16) unsigned char dsm[];
-    __shared__ RedSmem Red;
-    __shared__ AdmSmem A;
+__device__ void shard_decide_body(const DevPool& P, const AdmitArgs& a, const ShardX& X, unsigned char* dsm,
+                                  RedSmem& Red, AdmSmem& A) {
     Ctrl* C = P.ctrl;
     const int tid = threadIdx.x, T = blockDim.x;
     const int G = P.world, n = a.n;
@@ -154,7 +204,7 @@ __global__ void __launch_bounds__(512, 1) shard_decide_kernel(DevPool P, AdmitAr
         A.tick = a.tick_base;
         long long res = 0, pin = 0;
         for (int r = 0; r < G; ++r) {
-            const ShardHdr* h = reinterpret_cast<const ShardHdr*>(shard_recv1(P) + (size_t)r * shard_rec1(n));
+            const ShardHdr* h = reinterpret_cast<const ShardHdr*>(shard_rec1_of(P, X, r, n));
             res += h->resident;
             pin += h->pinned;
         }
@@ -174,7 +224,7 @@ __global__ void __launch_bounds__(512, 1) shard_decide_kernel(DevPool P, AdmitAr
         unsigned int gs = kNoSlot, r0 = 0u;
         for (int r = 0; r < G; ++r) {
             const ShardPos q =
-                reinterpret_cast<const ShardPos*>(shard_recv1(P) + (size_t)r * shard_rec1(n) + sizeof(ShardHdr))[i];
+                reinterpret_cast<const ShardPos*>(shard_rec1_of(P, X, r, n) + sizeof(ShardHdr))[i];
             if (q.gslot != kNoSlot) {
                 gs = q.gslot;
                 r0 = q.refs0;
@@ -251,10 +301,34 @@ __global__ void __launch_bounds__(512, 1) shard_decide_kernel(DevPool P, AdmitAr
     shstamp(P, 5);
 }
 
+__global__ void __launch_bounds__(512, 1) shard_decide_kernel(DevPool P, AdmitArgs a) {
+    extern __shared__ __align__(16) unsigned char dsm[];
+    __shared__ RedSmem Red;
+    __shared__ AdmSmem A;
+    ShardX X{};
+    shard_decide_body(P, a, X, dsm, Red, A);
+}
+
+// ---- front: probe, exchange 1 and decide in one kernel (one CTA per shard). At world 1 there
+// is nothing to exchange; with the fused exchange the probe's record goes straight into the
+// peers' windows and decide reads theirs in place.
+__global__ void __launch_bounds__(512, 1) shard_front_kernel(DevPool P, AdmitArgs a, ShardX X) {
+    extern __shared__ __align__(16) unsigned char dsm[];
+    __shared__ RedSmem Red;
+    __shared__ AdmSmem A;
+    shard_probe_body(P, a, Red);
+    __syncthreads();
+    if (X.fused) {
+        fx_push(P, X, P.sh_send1, shard_rec1(a.n));
+        fx_wait(P, X);
+    }
+    shard_decide_body(P, a, X, dsm, Red, A);
+}
+
 // ---- scan: this shard's per-list keep oldest (the single-pool K4 + K5a), packed for exchange 2
 // The host enqueues one scan + exchange + replay per possible chunk without waiting; a chunk
 // that does not exist (admission smaller, not started) or cannot evict sends empty lists.
-__global__ void __launch_bounds__(kThreads + 32, 1) shard_scan_kernel(DevPool P, AdmitArgs a, int chunk) {
+__global__ void __launch_bounds__(kThreads + 32, 1) shard_scan_kernel(DevPool P, AdmitArgs a, int chunk, ShardX X) {
     extern __shared__ __align__(16) unsigned char dsm[];
     __shared__ ScanSmem S;
     __shared__ SelectSmem Sel;
@@ -265,8 +339,13 @@ __global__ void __launch_bounds__(kThreads + 32, 1) shard_scan_kernel(DevPool P,
     const ShardState* SS = P.sh_state;
     const int admit_n = SS->admit_n;
     if (SS->error || SS->chunk != chunk || chunk * kChunk >= admit_n || !SS->need_scan) {
-        if (blockIdx.x == 0)
+        if (blockIdx.x == 0) {
             for (int l = tid; l < kMaxLists; l += T) P.sh_send2->n[l] = 0;
+            if (X.fused) {  // every shard's replay waits for this exchange: send the empty counts
+                __syncthreads();
+                fx_push(P, X, reinterpret_cast<const unsigned char*>(P.sh_send2), offsetof(ShardLists, c));
+            }
+        }
         return;  // uniform across the grid: SS is not written during this kernel
     }
     const int keep = min(kChunk, admit_n - chunk * kChunk);
@@ -354,6 +433,10 @@ __global__ void __launch_bounds__(kThreads + 32, 1) shard_scan_kernel(DevPool P,
             C->fin_done = 0u;
             C->rescan = 0;
         }
+        if (X.fused) {  // exchange 2: the lists in use straight into the peers' windows
+            __syncthreads();
+            fx_push(P, X, reinterpret_cast<const unsigned char*>(P.sh_send2), shard_lists_bytes(NL));
+        }
     }
     shstamp(P, 9);
 }
@@ -368,7 +451,7 @@ struct ShardReplaySmem {
 };
 
 // ---- replay: replicated exact evict_one loop over the merged lists; owners apply
-__global__ void __launch_bounds__(512, 1) shard_replay_kernel(DevPool P, AdmitArgs a) {
+__global__ void __launch_bounds__(512, 1) shard_replay_kernel(DevPool P, AdmitArgs a, ShardX Xc) {
     extern __shared__ __align__(16) unsigned char dsm[];
     __shared__ RedSmem Red;
     __shared__ AdmSmem A;
@@ -379,6 +462,7 @@ __global__ void __launch_bounds__(512, 1) shard_replay_kernel(DevPool P, AdmitAr
     const int tid = threadIdx.x, T = blockDim.x;
     const int NL = P.n_lists, Rl = NL - 1, G = P.world;
     shstamp(P, 10);
+    if (Xc.fused) fx_wait(P, Xc);  // always, even for a chunk that does not exist (see fx_push)
     if (tid == 0) {
         A.tick = SS->tick;
         A.first_touch = SS->first_touch;
@@ -451,7 +535,7 @@ __global__ void __launch_bounds__(512, 1) shard_replay_kernel(DevPool P, AdmitAr
     for (int l = tid; l < kMaxLists; l += T) R.L_n[l] = 0;
     for (int q = tid; q < G * kMaxLists; q += T) {
         const int r = q / kMaxLists, l = q - r * kMaxLists;
-        X.n_in[r][l] = l < NL ? shard_in(P, r)->n[l] : 0;
+        X.n_in[r][l] = l < NL ? shard_in(P, Xc, r)->n[l] : 0;
     }
     __syncthreads();
     if (scanned) {
@@ -460,11 +544,11 @@ __global__ void __launch_bounds__(512, 1) shard_replay_kernel(DevPool P, AdmitAr
             const int l = q / per_list, q2 = q - l * per_list;
             const int r = q2 / (kChunk + 1), j = q2 - r * (kChunk + 1);
             if (j >= X.n_in[r][l]) continue;
-            const ShardCand c = shard_in(P, r)->c[l][j];
+            const ShardCand c = shard_in(P, Xc, r)->c[l][j];
             int rank = j;
             for (int o = 0; o < G; ++o) {
                 if (o == r) continue;
-                const ShardCand* co = shard_in(P, o)->c[l];
+                const ShardCand* co = shard_in(P, Xc, o)->c[l];
                 int lo2 = 0, hi2 = X.n_in[o][l];
                 while (lo2 < hi2) {
                     const int mid = (lo2 + hi2) >> 1;
@@ -807,7 +891,20 @@ cudaError_t launch_shard_decide(const DevPool& P, const AdmitArgs& a, cudaStream
     return cudaGetLastError();
 }
 
-cudaError_t launch_shard_scan(const DevPool& P, const AdmitArgs& a, int chunk, const LaunchCfg& lc, cudaStream_t s) {
+cudaError_t launch_shard_front(const DevPool& P, const AdmitArgs& a, const ShardX& x, cudaStream_t s) {
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(shard_front_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)sizeof(BfsSmem));
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    shard_front_kernel<<<1, 512, sizeof(BfsSmem), s>>>(P, a, x);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_shard_scan(const DevPool& P, const AdmitArgs& a, int chunk, const ShardX& x, const LaunchCfg& lc,
+                              cudaStream_t s) {
     static bool attr = false;
     if (!attr) {
         cudaError_t e =
@@ -818,12 +915,13 @@ cudaError_t launch_shard_scan(const DevPool& P, const AdmitArgs& a, int chunk, c
     DevPool p = P;
     AdmitArgs aa = a;
     int k = chunk;
-    void* args[] = {&p, &aa, &k};
+    ShardX xx = x;
+    void* args[] = {&p, &aa, &k, &xx};
     return cudaLaunchCooperativeKernel((const void*)shard_scan_kernel, dim3(lc.grid), dim3(lc.threads), args, lc.smem,
                                        s);
 }
 
-cudaError_t launch_shard_replay(const DevPool& P, const AdmitArgs& a, cudaStream_t s) {
+cudaError_t launch_shard_replay(const DevPool& P, const AdmitArgs& a, const ShardX& x, cudaStream_t s) {
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(shard_replay_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -831,6 +929,6 @@ cudaError_t launch_shard_replay(const DevPool& P, const AdmitArgs& a, cudaStream
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    shard_replay_kernel<<<1, 512, sizeof(ShardReplaySmem), s>>>(P, a);
+    shard_replay_kernel<<<1, 512, sizeof(ShardReplaySmem), s>>>(P, a, x);
     return cudaGetLastError();
 }
