@@ -18,7 +18,8 @@ so no flush is needed between steps.
 Multi-GPU (torchrun, one process per GPU; default --parallel auto = sharded when N > 1): ONE
 pool of N x 16M slots hash-partitioned over the N GPUs; every rank runs the same
 global trace, scans its own shard and the ranks exchange per-shard candidates each admission
-(the fused peer-memory exchange over NVLink, or --comm nccl). --parallel replicas: N independent pools and trace partitions
+(the fused exchange: the admission kernels store into the peers' windows over NVLink and wait
+on their flags; or --comm nccl). --parallel replicas: N independent pools and trace partitions
 (no data-path collective). Either way per-GPU work is fixed as N grows ("scaling": weak).
 Timing: CUDA events on the engine's stream, barrier + max over ranks.
 
@@ -249,9 +250,9 @@ SHARD_SLACK = 8192
 
 
 def make_comm(dist, kind="peer"):
-    """The shard exchange. 'peer' (default): the fused exchange, each shard's bytes stored into
-    its peers' windows over NVLink / NVSwitch by one kernel (CUDA IPC handles exchanged once
-    through torch.distributed); every rank falls back to NCCL together when any of them cannot
+    """The shard exchange. 'peer' (default): the fused exchange, each shard's message stored into
+    its peers' windows over NVLink / NVSwitch by the admission kernels themselves (CUDA IPC
+    handles exchanged once through torch.distributed); every rank falls back to NCCL together when any of them cannot
     map its peers. 'nccl': ncclAllGather (rank 0 makes the id, torch.distributed broadcasts it)."""
     from paper_2605_27744_b200 import shard
 
@@ -386,7 +387,7 @@ def run_ours(args, dist):
                    "policy": "cachesage",
                    "parallelism": (f"hash-sharded{dist.world} (pool of {dist.world} x {pool} slots, owner = "
                                    f"(key >> 40) % N, per-shard candidates exchanged by "
-                                   f"{'peer-memory stores (fused exchange kernel)' if comm_kind == 'peer' else 'NCCL allgather'})")
+                                   f"{'peer-memory stores inside the admission kernels (fused exchange)' if comm_kind == 'peer' else 'NCCL allgather'})")
                    if sharded
                    else f"replicas{dist.world} (sessions partitioned)",
                    "l2": "no flush: each pass streams 134 MB of packed scan words (> 126 MB L2) with an L2 evict-first policy; ncu DRAM reads = 1.003x the streamed bytes per launch"},
