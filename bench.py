@@ -421,26 +421,33 @@ def run_ours(args, dist):
     }
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(pool, args)
-        line["parity"] = parity_leg(spec, pool, snap_seed, gpu_state)
+        line["parity"] = parity_leg(spec, pool, snap_seed, gpu_state, sharded)
     return line
 
 
-def parity_leg(spec, pool, snap_seed, g):
+def parity_leg(spec, pool, snap_seed, g, sharded=False):
     """CPU leg: the `value` run's decisions (every victim in order, per-turn cached tokens and
     completion times, drained warmups) against the fast exact CPU oracle (oracle/cs_oracle.c,
     pinned to the reference in tests/test_oracle_fast.py) replaying the same trace from the same
     16M-slot snapshot for the same scheduler steps. The oracle is the checker here, never the
-    thing measured."""
+    thing measured. sharded (N = 1): the one-shard pool's own configuration (build_engine):
+    budget pool - SHARD_SLACK and the global snapshot of that many blocks."""
     from oracle import pyoracle as orc
+    from paper_2605_27744_b200 import shard
     from paper_2605_27744_b200 import workloads as W
 
     t = time.time()
-    keys, lt, agents, refs = W.pool_snapshot(pool, len(g["agents"]), seed=snap_seed, mode="realistic")
+    budget = None
+    if sharded:
+        budget = pool - SHARD_SLACK
+        keys, lt, agents, refs = shard.snapshot_shard(budget, 1, 0, len(g["agents"]), seed=snap_seed)
+    else:
+        keys, lt, agents, refs = W.pool_snapshot(pool, len(g["agents"]), seed=snap_seed, mode="realistic")
     has = agents != np.uint32(0xFFFFFFFF)
     ids = np.zeros(keys.size, np.uint64)
     ids[has] = g["agents"][agents[has]]
     o = orc.run(spec, snapshot=(keys, lt, has.astype(np.int32), ids, refs.astype(np.int32)), max_steps=g["steps"],
-                policy="cachesage", fast=True)
+                policy="cachesage", fast=True, budget=budget)
     del keys, lt, agents, refs, ids
     checks = {
         "victims": bool(np.array_equal(g["evictions"], o["evictions"])),

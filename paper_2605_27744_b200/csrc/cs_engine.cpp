@@ -385,8 +385,9 @@ void cs_engine::build(const cs_engine_cfg& c, const cs_workload_spec* ws, long l
     }
     pool->timing = c.timing != 0;
     // the scheduler needs only the status of an admission: it enqueues the next one while the
-    // previous launch's prescan CTAs finish (cs_pool::wait_status)
-    pool->early_status = comm == nullptr;
+    // previous launch's prescan CTAs (sharded: the replay's table updates) finish
+    // (cs_pool::wait_status)
+    pool->early_status = true;
     d_keys.ensure(8 * total_blocks);
     d_counts.ensure(4 * total_blocks);
     d_pins.ensure(4 * total_blocks);

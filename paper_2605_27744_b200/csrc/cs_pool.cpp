@@ -356,7 +356,12 @@ const csb::AdmitStatus& cs_pool::admit_sharded_once(const csb::AdmitArgs& in) {
     unpin_q_slots = 0;
     a.seq = ++seq;
     st->started = -1;
-    if (timing) ck(cudaEventRecord(ev0, stream), "cudaEventRecord");
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (timing) {
+        e0 = take_event();
+        e1 = take_event();
+        ck(cudaEventRecord(e0, stream), "cudaEventRecord");
+    }
     // exchange 1 (probe -> decide) and, per chunk, exchange 2 (scan -> replay). World 1: nothing
     // to exchange (one front kernel). Peer transport: fused into the admission kernels. Other
     // transports: an allgather between the kernels.
@@ -392,18 +397,16 @@ const csb::AdmitStatus& cs_pool::admit_sharded_once(const csb::AdmitArgs& in) {
         if (fz) comm->fused_end(stream);
         launches += 2;
     }
-    if (timing) ck(cudaEventRecord(ev1, stream), "cudaEventRecord");
-    sync();
+    if (timing) ck(cudaEventRecord(e1, stream), "cudaEventRecord");
+    // the replay (or decide, for an admission that does not start) publishes the status before
+    // it applies the table updates: inside an engine loop the host schedules the next admission
+    // meanwhile (stream order keeps every later device operation behind this one)
+    wait_status(a.seq, "shard kernels");
+    if (!early_status) ck(cudaStreamSynchronize(stream), "shard kernels");
     poll_reset_pending = false;
     if (timing) {
-        float ms = 0.f;
-        ck(cudaEventElapsedTime(&ms, ev0, ev1), "cudaEventElapsedTime");
-        admit_ms += ms;
-        ++admit_launches;
-        if (st->scans > 0) {
-            scan_launch_ms += ms;
-            ++scan_launches;
-        }
+        t_pending.push_back({e0, e1, st->scans > 0});
+        resolve_timing(false);
     }
     if (st->started < 0) throw CsError(CS_ERR_CUDA, "shard kernels did not report a status");
     resident = st->resident;

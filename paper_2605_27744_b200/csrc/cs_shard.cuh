@@ -176,6 +176,10 @@ __device__ void shard_write_status(const DevPool& P, const AdmitArgs& a, const S
         st->pend_target[k] = C->pend_target[k];
         st->pend_tick[k] = C->pend_tick[k];
     }
+    // early status: the host schedules the next admission while this kernel finishes (the
+    // replay's table updates); every field above and the pins are written by now
+    __threadfence_system();
+    *(volatile unsigned long long*)&st->done_seq = a.seq;
 }
 
 // number of absent positions in [lo, hi) of the replicated position table
@@ -212,10 +216,17 @@ __device__ void shard_decide_body(const DevPool& P, const AdmitArgs& a, const Sh
         A.pinned = pin;
         C->done = 0;
         C->error = 0;
+        C->rescan = 0;  // the scans of this admission start from clean bounds (no grid barrier)
+        C->fin_done = 0u;
         if (a.flags & kPollReset) {
             C->step_warmups = 0;
             C->n_pend = 0;
         }
+    }
+    if (tid < kMaxLists) {
+        P.gbound[tid] = kNoBound;
+        P.gcount[tid] = 0;
+        P.gmaxk[tid] = 0ull;
     }
     __syncthreads();
     // the replicated position table: at most one shard owns (and reports) each position
@@ -355,29 +366,36 @@ __global__ void __launch_bounds__(kThreads + 32, 1) shard_scan_kernel(DevPool P,
         S.cls_ready = 1;
     }
     for (int pass = 0;; ++pass) {
-        if (blockIdx.x == 0) {
-            if (tid < NL) {
-                if (pass > 0) P.ghint[tid] = kNoBound;  // a hint was too tight: safe pass without hints
-                P.gbound[tid] = kNoBound;
-                P.gcount[tid] = 0;
-                P.gmaxk[tid] = 0ull;
+        int fast = 0;
+        if (pass == 0) {
+            // no grid barrier: the bounds and counters were reset before this kernel (decide, or
+            // the previous chunk's scan), and every CTA derives the fast flag from the same hints
+            fast = !__syncthreads_or(tid < NL && !(P.ghint[tid] < kNoBound) && !P.gsmall[tid]);
+            if (blockIdx.x == 0 && tid == 0) {
+                C->pass = 0;
+                C->fast = fast;
+                C->scans += 1;
+                C->scanned_slots += P.cap;
             }
-            const int slow = __syncthreads_or(tid < NL && !(P.ghint[tid] < kNoBound) && !P.gsmall[tid]);
-            if (tid == 0) {
-                C->rescan = 0;
-                C->fin_done = 0u;
-                C->pass = pass;
-                C->fast = (pass == 0 && !slow) ? 1 : 0;
-                if (pass == 0) {
-                    C->scans += 1;
-                    C->scanned_slots += P.cap;
-                } else {
+        } else {
+            if (blockIdx.x == 0) {
+                if (tid < NL) {
+                    P.ghint[tid] = kNoBound;  // a hint was too tight: safe pass without hints
+                    P.gbound[tid] = kNoBound;
+                    P.gcount[tid] = 0;
+                    P.gmaxk[tid] = 0ull;
+                }
+                __syncthreads();
+                if (tid == 0) {
+                    C->rescan = 0;
+                    C->fin_done = 0u;
+                    C->pass = pass;
+                    C->fast = 0;
                     C->rescans += 1;
                 }
             }
+            grid_barrier(C);
         }
-        grid_barrier(C);
-        const int fast = *(volatile int*)&C->fast;
         for (int x = tid; x < a.n_agents; x += T) B.cls[x] = P.cls[x];
         __syncthreads();
         scan_pass(P, NL, keep, B, S, Sel, dsm, fast != 0, a);
@@ -872,6 +890,10 @@ __global__ void __launch_bounds__(512, 1) shard_replay_kernel(DevPool P, AdmitAr
         if (last) shard_write_status(P, a, s);
     }
     shstamp(P, 15);
+    // the admission's queued block-table updates, applied behind its early status (the host's
+    // turnaround hides them; the next probe would otherwise apply them first)
+    __syncthreads();
+    if (last) apply_table_queue(P, Red);
 }
 
 cudaError_t launch_shard_probe(const DevPool& P, const AdmitArgs& a, cudaStream_t s) {
