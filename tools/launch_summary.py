@@ -5,7 +5,7 @@ import sys
 
 rows = [ln for ln in open(sys.argv[1]) if ln.startswith('"')]
 d = collections.defaultdict(list)
-scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}
+scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}
 for r in csv.DictReader(rows):
     if r["Metric Name"] != "gpu__time_duration.sum":
         continue
