@@ -106,10 +106,21 @@ def test_sharded_engine_matches_reference(name, world):
 @pytest.mark.parametrize("name", ["supervisor-a-cachesage", "cfg1@128-cachesage", "pins-defer-lru",
                                   "supervisor-a-emax3-cachesage"])
 def test_sharded_engine_peer_exchange(name, world):
-    """The fused exchange (peer-memory stores + flags, one kernel per exchange, no NCCL, no host
-    round trip): every shard reproduces the reference run bit-exactly."""
+    """The fused exchange (the admission kernels store into the peers' windows and wait on their
+    flags; no exchange kernel, no NCCL, no host round trip): every shard reproduces the reference
+    run bit-exactly."""
     g = RUNS[name]
     for res, t, ev, w, ps in _run_shards(g, world, transport="peer"):
+        _check_golden(g, res, t, ev, w)
+
+
+@pytest.mark.parametrize("name", ["supervisor-a-cachesage", "pins-defer-lru"])
+def test_sharded_engine_peer_unfused(name, monkeypatch):
+    """The peer transport exchanging between kernels (CS_PEER_UNFUSED: the stand-alone
+    8-CTA-per-peer allgather kernel between probe and decide, and between scan and replay)."""
+    monkeypatch.setenv("CS_PEER_UNFUSED", "1")
+    g = RUNS[name]
+    for res, t, ev, w, ps in _run_shards(g, 2, transport="peer"):
         _check_golden(g, res, t, ev, w)
 
 
