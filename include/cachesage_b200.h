@@ -355,10 +355,11 @@ int cs_comm_callback(int rank, int world, cs_allgather_fn fn, void* ctx, cs_comm
  * the caller broadcasts its 128 bytes; libnccl.so.2 is loaded at run time (CS_NCCL_LIB). */
 int cs_nccl_unique_id(uint8_t* id128);
 int cs_comm_nccl(const uint8_t* id128, int rank, int world, int device, cs_comm_t* out);
-/* Peer memory (the fused exchange): each shard's contribution is stored straight into every
- * peer's window over NVLink / NVSwitch by one stream-ordered kernel that then waits on the peers'
- * flags (no NCCL, no host round trip). cap: the largest exchange in bytes per rank (the shard
- * lists are 74,400 B; 262,144 fits prompts of up to 32,766 blocks).
+/* Peer memory (the fused exchange): a sharded engine's admission kernels store each shard's
+ * contribution straight into every peer's window over NVLink / NVSwitch and wait on the peers'
+ * flags themselves (no exchange kernel, no NCCL, no host round trip; CS_PEER_UNFUSED=1 exchanges
+ * between kernels instead). cap: the largest exchange in bytes per rank (the shard lists in use
+ * are <= 74,400 B; 262,144 fits prompts of up to 32,766 blocks).
  *   cs_comm_peer_group   world shards of this process (devices[r], NULL = all on device 0);
  *                        peer access is enabled between distinct devices.
  *   cs_comm_peer_create  one shard per process: returns this rank's 128-byte handle (CUDA IPC
