@@ -6,17 +6,23 @@
 // owner(k) = (k >> 40) % G (shard_owner). Per admission (EngineSim::start_request /
 // execute_warmup, engine.cpp:141-323, paths relative to /root/reference/proj), every shard runs
 //
-//   probe   (1 CTA)   deferred table updates + unpins of this shard, probe of the prompt
-//                     positions this shard owns                      -> exchange 1 (allgather)
-//   decide  (1 CTA)   replicated: global residency of every position, try_start_head
+//   front   (1 CTA)   probe: this shard's unpins (and any table updates still queued), a probe
+//                     of the prompt positions this shard owns        -> exchange 1
+//                     decide, replicated: global residency of every position, try_start_head
 //                     feasibility, observe(AgentDispatch) on the replicated learner, lookup
 //                     (owners touch their prefix blocks)
 //   per chunk of <= 128 prompt blocks that can evict:
 //     scan  (grid)    the shard's keep oldest unpinned per survival class + keep+1 oldest
-//                     resident (the single-pool K4/K5a)              -> exchange 2 (allgather)
+//                     resident (the single-pool K4/K5a)              -> exchange 2
 //     replay (1 CTA)  replicated: per list the global keep oldest = the keep smallest of the
 //                     union of the shard lists; the exact evict_one replay
-//                     (engine.cpp:102-125); owners apply their victims, touches and inserts
+//                     (engine.cpp:102-125); owners apply their victims, touches and inserts;
+//                     the status goes to the host, then the queued table updates are applied
+//
+// Exchanges: with the peer transport they are fused into these kernels (fx_push / fx_wait: the
+// front's probe record and the scan's lists are stored into the peers' windows, the front's
+// decide and the replay read the peers' messages in place); other transports allgather between
+// separate probe / decide kernels and between scan and replay; one shard exchanges nothing.
 //
 // Exactness: the global keep oldest of a list are among the union of every shard's keep oldest
 // of that list (a global member is beaten by at most keep-1 members, so by at most keep-1 of its
